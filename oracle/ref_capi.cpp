@@ -1,0 +1,359 @@
+// ref_capi.cpp — extern "C" entry points into the reference implementation
+// compiled from /root/reference/proj sources (oracle/Makefile -> oracle/_ref).
+//
+// TEST INFRASTRUCTURE ONLY: used by tests/golden/make_golden.py to produce the
+// committed golden vectors, by tests/test_oracle.py to pin the C restatement
+// against the real reference when oracle/_ref exists, and by bench.py
+// --impl reference (the reference's own CPU path on the GPU box's host).
+//
+// Every function converts flat arrays to the reference's Eigen-typed structs,
+// calls the reference function unchanged, and flattens the result. Exceptions
+// become status codes: 1 std::invalid_argument, 2 std::domain_error, 3 other.
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "oea/latency.hpp"
+#include "oea/moe_layer.hpp"
+#include "oea/routing.hpp"
+#include "oracle.hpp"
+
+using namespace oea;
+
+namespace {
+
+thread_local std::string g_err;
+
+int record(int code, const char* what) {
+  g_err = what;
+  return code;
+}
+
+#define REF_GUARD(body)                                          \
+  try {                                                          \
+    body;                                                        \
+    return 0;                                                    \
+  } catch (const std::domain_error& e) {                         \
+    return record(2, e.what());                                  \
+  } catch (const std::invalid_argument& e) {                     \
+    return record(1, e.what());                                  \
+  } catch (const std::exception& e) {                            \
+    return record(3, e.what());                                  \
+  }
+
+RoutingConfig make_cfg(int mode, int k, int k0, double p, int k_max, int max_p, int cap) {
+  RoutingConfig c;
+  c.mode = static_cast<RoutingMode>(mode);
+  c.k = k;
+  c.k0 = k0;
+  c.p = p;
+  c.k_max = k_max;
+  c.max_p = max_p;
+  c.cap = static_cast<CapSemantics>(cap);
+  return c;
+}
+
+ScoreMatrix make_scores(const double* s, const uint8_t* mask, int B, int N) {
+  ScoreMatrix m;
+  m.scores.resize(B, N);
+  std::memcpy(m.scores.data(), s, sizeof(double) * B * N);
+  if (mask) {
+    m.mask.resize(B);
+    for (int i = 0; i < B; ++i) m.mask[i] = mask[i] != 0;
+  }
+  return m;
+}
+
+void flatten_plan(const RoutingPlan& plan, int B, int N, int stride, int32_t* sets,
+                  int32_t* set_len, double* weights, int32_t* loads,
+                  int32_t* active_union, int32_t* active_count, int64_t* total_load) {
+  for (int i = 0; i < B; ++i) {
+    const auto& s = plan.sets[i];
+    set_len[i] = static_cast<int32_t>(s.size());
+    for (int j = 0; j < stride; ++j) {
+      sets[i * stride + j] = j < static_cast<int>(s.size()) ? s[j] : -1;
+      if (weights) {
+        const auto& w = plan.weights[i];
+        weights[i * stride + j] = j < static_cast<int>(w.size()) ? w[j] : 0.0;
+      }
+    }
+  }
+  if (loads)
+    for (int e = 0; e < N; ++e) loads[e] = plan.loads[e];
+  if (active_union) {
+    for (int e = 0; e < N; ++e)
+      active_union[e] = e < static_cast<int>(plan.active_union.size()) ? plan.active_union[e] : -1;
+  }
+  if (active_count) *active_count = plan.active_count;
+  if (total_load) *total_load = plan.total_load;
+}
+
+template <typename Scalar>
+struct RefLayer {
+  MoeLayerParams<Scalar> p;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+int ref_resolve(int mode, int k, int k0, double p, int k_max, int max_p, int cap, int n,
+                int32_t* out7, double* out_p) {
+  REF_GUARD({
+    const auto r = make_cfg(mode, k, k0, p, k_max, max_p, cap).resolved(n);
+    out7[0] = static_cast<int>(r.mode);
+    out7[1] = r.k;
+    out7[2] = r.k0;
+    out7[3] = r.k_max;
+    out7[4] = r.max_p;
+    out7[5] = static_cast<int>(r.cap);
+    out7[6] = 0;
+    *out_p = r.p;
+  })
+}
+
+int ref_sort_experts(const double* scores, int B, int N, int32_t* order) {
+  REF_GUARD({
+    ScoreMatrix m = make_scores(scores, nullptr, B, N);
+    const auto s = sort_experts(m);
+    for (int i = 0; i < B; ++i)
+      for (int j = 0; j < N; ++j) order[i * N + j] = s.order(i, j);
+  })
+}
+
+// route(): the reference production path (routing.cpp:305-326).
+int ref_route(const double* scores, const uint8_t* mask, int B, int N, int mode, int k,
+              int k0, double p, int k_max, int max_p, int cap, int stride, int32_t* sets,
+              int32_t* set_len, double* weights, int32_t* loads, int32_t* active_union,
+              int32_t* active_count, int64_t* total_load) {
+  REF_GUARD({
+    ScoreMatrix m = make_scores(scores, mask, B, N);
+    const auto plan = route(m, make_cfg(mode, k, k0, p, k_max, max_p, cap));
+    flatten_plan(plan, B, N, stride, sets, set_len, weights, loads, active_union,
+                 active_count, total_load);
+  })
+}
+
+// The reference's own naive oracle (tests/oracle/oracle.cpp:212-215).
+int ref_reference_route(const double* scores, const uint8_t* mask, int B, int N, int mode,
+                        int k, int k0, double p, int k_max, int max_p, int cap, int stride,
+                        int32_t* sets, int32_t* set_len, double* weights, int32_t* loads,
+                        int32_t* active_union, int32_t* active_count,
+                        int64_t* total_load) {
+  REF_GUARD({
+    ScoreMatrix m = make_scores(scores, mask, B, N);
+    const auto plan = oracle::reference_route(m, make_cfg(mode, k, k0, p, k_max, max_p, cap));
+    flatten_plan(plan, B, N, stride, sets, set_len, weights, loads, active_union,
+                 active_count, total_load);
+  })
+}
+
+int ref_phase1(const double* scores, const uint8_t* mask, int B, int N, int mode, int k,
+               int k0, double p, int k_max, int max_p, int cap, int32_t* t, int32_t* n,
+               int32_t* base_union, int32_t* base_union_count) {
+  REF_GUARD({
+    ScoreMatrix m = make_scores(scores, mask, B, N);
+    const auto cfg = make_cfg(mode, k, k0, p, k_max, max_p, cap);
+    const auto ph = phase1_baseline(m, sort_experts(m), cfg);
+    for (int i = 0; i < B; ++i) {
+      t[i] = ph.t[i];
+      n[i] = ph.n[i];
+    }
+    for (int e = 0; e < N; ++e)
+      base_union[e] = e < static_cast<int>(ph.base_union.size()) ? ph.base_union[e] : -1;
+    *base_union_count = static_cast<int32_t>(ph.base_union.size());
+  })
+}
+
+int ref_check_invariants(const double* scores, const uint8_t* mask, int B, int N, int mode,
+                         int k, int k0, double p, int k_max, int max_p, int cap, int stride,
+                         const int32_t* sets, const int32_t* set_len, const double* weights,
+                         const int32_t* loads, const int32_t* active_union, int active_count,
+                         int64_t total_load, char* msg, int msglen) {
+  REF_GUARD({
+    ScoreMatrix m = make_scores(scores, mask, B, N);
+    RoutingPlan plan;
+    plan.n_experts = N;
+    plan.sets.resize(B);
+    plan.weights.resize(B);
+    for (int i = 0; i < B; ++i)
+      for (int j = 0; j < set_len[i]; ++j) {
+        plan.sets[i].push_back(sets[i * stride + j]);
+        plan.weights[i].push_back(weights[i * stride + j]);
+      }
+    plan.loads = Eigen::VectorXi::Zero(N);
+    for (int e = 0; e < N; ++e) plan.loads[e] = loads[e];
+    for (int e = 0; e < active_count; ++e) plan.active_union.push_back(active_union[e]);
+    plan.active_count = active_count;
+    plan.total_load = total_load;
+    const std::string r =
+        oracle::check_plan_invariants(m, make_cfg(mode, k, k0, p, k_max, max_p, cap), plan);
+    std::strncpy(msg, r.c_str(), msglen - 1);
+    msg[msglen - 1] = '\0';
+  })
+}
+
+int ref_exhaustive_small_check(int max_n, int max_b, int denom, int64_t* checks,
+                               int64_t* mismatches, int64_t* violations) {
+  REF_GUARD({
+    const auto rep = oracle::exhaustive_small_check(max_n, max_b, denom);
+    *checks = rep.checks;
+    *mismatches = rep.mismatches;
+    *violations = rep.violations;
+  })
+}
+
+double ref_expected_active_experts(int N, int k, int B) {
+  return expected_active_experts(N, k, B);
+}
+
+// make_random_layer / make_random_batch (moe_layer.cpp:76-116) into flat arrays.
+int ref_make_random_layer(int D, int H, int N, uint64_t seed, double* router, double* wg,
+                          double* wu, double* wd) {
+  REF_GUARD({
+    const auto layer = make_random_layer({D, H, N}, seed);
+    std::memcpy(router, layer.router.data(), sizeof(double) * D * N);
+    for (int e = 0; e < N; ++e) {
+      std::memcpy(wg + static_cast<size_t>(e) * D * H, layer.experts[e].w_gate.data(),
+                  sizeof(double) * D * H);
+      std::memcpy(wu + static_cast<size_t>(e) * D * H, layer.experts[e].w_up.data(),
+                  sizeof(double) * D * H);
+      std::memcpy(wd + static_cast<size_t>(e) * H * D, layer.experts[e].w_down.data(),
+                  sizeof(double) * H * D);
+    }
+  })
+}
+
+int ref_make_random_batch(int B, int D, uint64_t seed, int step, int layer, double* x) {
+  REF_GUARD({
+    const auto b = make_random_batch(B, D, seed, step, layer);
+    std::memcpy(x, b.embeddings.data(), sizeof(double) * B * D);
+  })
+}
+
+// A reference MoE layer held across calls (bench reference arm). Values are
+// copied from flat arrays in reference layout.
+void* ref_layer_create(int scalar_is_float, int D, int H, int N, const double* router,
+                       const double* wg, const double* wu, const double* wd) {
+  try {
+    if (scalar_is_float) {
+      auto* L = new RefLayer<float>;
+      L->p.router.resize(D, N);
+      for (int i = 0; i < D * N; ++i) L->p.router.data()[i] = static_cast<float>(router[i]);
+      L->p.experts.resize(N);
+      for (int e = 0; e < N; ++e) {
+        auto& ex = L->p.experts[e];
+        ex.w_gate.resize(D, H);
+        ex.w_up.resize(D, H);
+        ex.w_down.resize(H, D);
+        for (size_t i = 0; i < static_cast<size_t>(D) * H; ++i) {
+          ex.w_gate.data()[i] = static_cast<float>(wg[static_cast<size_t>(e) * D * H + i]);
+          ex.w_up.data()[i] = static_cast<float>(wu[static_cast<size_t>(e) * D * H + i]);
+          ex.w_down.data()[i] = static_cast<float>(wd[static_cast<size_t>(e) * H * D + i]);
+        }
+      }
+      return L;
+    }
+    auto* L = new RefLayer<double>;
+    L->p.router.resize(D, N);
+    std::memcpy(L->p.router.data(), router, sizeof(double) * D * N);
+    L->p.experts.resize(N);
+    for (int e = 0; e < N; ++e) {
+      auto& ex = L->p.experts[e];
+      ex.w_gate.resize(D, H);
+      ex.w_up.resize(D, H);
+      ex.w_down.resize(H, D);
+      std::memcpy(ex.w_gate.data(), wg + static_cast<size_t>(e) * D * H, sizeof(double) * D * H);
+      std::memcpy(ex.w_up.data(), wu + static_cast<size_t>(e) * D * H, sizeof(double) * D * H);
+      std::memcpy(ex.w_down.data(), wd + static_cast<size_t>(e) * H * D, sizeof(double) * H * D);
+    }
+    return L;
+  } catch (const std::exception& e) {
+    record(3, e.what());
+    return nullptr;
+  }
+}
+
+void ref_layer_destroy(void* layer, int scalar_is_float) {
+  if (scalar_is_float)
+    delete static_cast<RefLayer<float>*>(layer);
+  else
+    delete static_cast<RefLayer<double>*>(layer);
+}
+
+int ref_router_scores(void* layer, int scalar_is_float, const double* x, int B, int D,
+                      double* scores) {
+  REF_GUARD({
+    TokenBatch batch;
+    batch.embeddings.resize(B, D);
+    std::memcpy(batch.embeddings.data(), x, sizeof(double) * B * D);
+    const ScoreMatrix s = scalar_is_float
+                              ? router_scores(static_cast<RefLayer<float>*>(layer)->p, batch)
+                              : router_scores(static_cast<RefLayer<double>*>(layer)->p, batch);
+    std::memcpy(scores, s.scores.data(), sizeof(double) * s.scores.size());
+  })
+}
+
+// moe_forward (moe_layer.hpp:114-158) on a flat plan.
+int ref_moe_forward(void* layer, int scalar_is_float, const double* x, int B, int D,
+                    const int32_t* sets, const int32_t* set_len, const double* weights,
+                    int stride, int n_experts, const uint8_t* mask, double* out) {
+  REF_GUARD({
+    TokenBatch batch;
+    batch.embeddings.resize(B, D);
+    std::memcpy(batch.embeddings.data(), x, sizeof(double) * B * D);
+    RoutingPlan plan;
+    plan.n_experts = n_experts;
+    plan.sets.resize(B);
+    plan.weights.resize(B);
+    for (int i = 0; i < B; ++i)
+      for (int j = 0; j < set_len[i]; ++j) {
+        plan.sets[i].push_back(sets[i * stride + j]);
+        plan.weights[i].push_back(weights[i * stride + j]);
+      }
+    MaskArray m;
+    if (mask) {
+      m.resize(B);
+      for (int i = 0; i < B; ++i) m[i] = mask[i] != 0;
+    }
+    const RowMatrixXd r =
+        scalar_is_float
+            ? moe_forward(static_cast<RefLayer<float>*>(layer)->p, batch, plan, mask ? &m : nullptr)
+            : moe_forward(static_cast<RefLayer<double>*>(layer)->p, batch, plan, mask ? &m : nullptr);
+    std::memcpy(out, r.data(), sizeof(double) * B * D);
+  })
+}
+
+// The reference's full CPU decode cell for one batch: router_scores -> route
+// -> moe_forward (the toy-layer cell of simulate.cpp:181-189, minus the
+// shadow vanilla run). Returns T via *active_count.
+int ref_decode(void* layer, int scalar_is_float, const double* x, int B, int D, int mode,
+               int k, int k0, double p, int k_max, int max_p, int cap, double* out,
+               int32_t* active_count, int64_t* total_load) {
+  REF_GUARD({
+    TokenBatch batch;
+    batch.embeddings.resize(B, D);
+    std::memcpy(batch.embeddings.data(), x, sizeof(double) * B * D);
+    const auto cfg = make_cfg(mode, k, k0, p, k_max, max_p, cap);
+    RowMatrixXd r;
+    RoutingPlan plan;
+    if (scalar_is_float) {
+      const auto& L = static_cast<RefLayer<float>*>(layer)->p;
+      plan = route(router_scores(L, batch), cfg);
+      r = moe_forward(L, batch, plan);
+    } else {
+      const auto& L = static_cast<RefLayer<double>*>(layer)->p;
+      plan = route(router_scores(L, batch), cfg);
+      r = moe_forward(L, batch, plan);
+    }
+    std::memcpy(out, r.data(), sizeof(double) * B * D);
+    *active_count = plan.active_count;
+    *total_load = plan.total_load;
+  })
+}
+
+}  // extern "C"
