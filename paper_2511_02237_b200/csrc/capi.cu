@@ -1,0 +1,1128 @@
+// capi.cu — the extern "C" boundary (include/oea_cuda.h): contexts, the
+// workspace arena, argument validation with the reference's error texts, and
+// the orchestration of the kernel families. No arithmetic of the hot path
+// happens on the host: every compute entry point launches CUDA work (and the
+// context refuses to exist without an sm_100 device).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "oea_device.cuh"
+#include "oea_internal.cuh"
+
+using namespace oea_dev;
+
+namespace {
+
+thread_local std::string t_last_error;
+
+struct Workspace {
+  void* base = nullptr;
+  size_t bytes = 0;
+  // capacities
+  int B = 0, N = 0, Np = 0, D = 0, Dp = 0, H = 0, Hp = 0, S = 0, R = 0, G = 0;
+  // carved pointers
+  double* scores = nullptr;
+  double* logits64 = nullptr;
+  double* x64 = nullptr;
+  void* xT = nullptr;
+  float* logits = nullptr;
+  int32_t* order = nullptr;
+  int32_t* t = nullptr;
+  int32_t* n = nullptr;
+  uint32_t* union_bits = nullptr;
+  int32_t* sets = nullptr;
+  int32_t* set_len = nullptr;
+  double* w64 = nullptr;
+  float* w32 = nullptr;
+  int32_t* loads = nullptr;
+  int32_t* active_union = nullptr;
+  int32_t* active_count = nullptr;
+  int64_t* total_load = nullptr;
+  int32_t* base_union = nullptr;
+  int32_t* base_union_count = nullptr;
+  int32_t* err_token = nullptr;
+  uint32_t* tokbits = nullptr;
+  int32_t* row_tok = nullptr;
+  int32_t* row_slot = nullptr;
+  int32_t* group_a = nullptr;
+  int32_t* group_row0 = nullptr;
+  int32_t* group_rows = nullptr;
+  FfnHeader* hdr = nullptr;
+  int32_t* counters = nullptr;
+  __nv_bfloat16* xpad = nullptr;
+  void* hbuf = nullptr;
+  void* ybuf = nullptr;
+  uint8_t* mask = nullptr;
+  void* xin = nullptr;   // device copy of caller input (host entry points)
+  void* out = nullptr;   // device output (host entry points)
+  float* out32 = nullptr;
+};
+
+struct Need {
+  int B, N, D, H, S;
+};
+
+size_t carve(Workspace& w, bool assign) {
+  size_t off = 0;
+  auto take = [&](auto*& ptr, size_t bytes) {
+    off = (off + 255) & ~static_cast<size_t>(255);
+    if (assign) ptr = reinterpret_cast<std::remove_reference_t<decltype(ptr)>>(
+                    static_cast<char*>(w.base) + off);
+    off += bytes;
+  };
+  const size_t B = w.B, N = w.N, Np = w.Np, D = w.D, Dp = w.Dp, H = w.H, Hp = w.Hp, S = w.S,
+               R = w.R, G = w.G;
+  const size_t Nmax = std::max(N, Np);
+  take(w.scores, B * N * 8);
+  take(w.logits64, B * N * 8);
+  take(w.x64, B * D * 8);
+  take(w.xT, B * D * 8);
+  take(w.logits, B * Np * 4);
+  take(w.order, B * Nmax * 4);
+  take(w.t, B * 4);
+  take(w.n, B * 4);
+  take(w.union_bits, ((Nmax + 31) / 32 + 1) * 4);
+  take(w.sets, B * S * 4);
+  take(w.set_len, B * 4);
+  take(w.w64, B * S * 8);
+  take(w.w32, B * S * 4);
+  take(w.loads, Nmax * 4);
+  take(w.active_union, Nmax * 4);
+  take(w.active_count, 4);
+  take(w.total_load, 8);
+  take(w.base_union, Nmax * 4);
+  take(w.base_union_count, 4);
+  take(w.err_token, 4);
+  take(w.tokbits, Nmax * ((B + 31) / 32) * 4);
+  take(w.row_tok, R * 4);
+  take(w.row_slot, R * 4);
+  take(w.group_a, G * 4);
+  take(w.group_row0, G * 4);
+  take(w.group_rows, G * 4);
+  take(w.hdr, sizeof(FfnHeader));
+  take(w.counters, (G + Dp / 16 + 1) * 4);
+  take(w.xpad, B * Dp * 2);
+  take(w.hbuf, R * std::max(Hp, H) * 8);
+  take(w.ybuf, B * S * std::max(Dp, D) * 8);
+  take(w.mask, B);
+  take(w.xin, B * D * 8);
+  take(w.out, B * D * 8);
+  take(w.out32, B * D * 4);
+  return off + 256;
+}
+
+void set_caps(Workspace& w, const Need& nd) {
+  w.B = nd.B;
+  w.N = nd.N;
+  w.Np = round_up(nd.N, 16);
+  w.D = nd.D;
+  w.Dp = round_up(nd.D, kPadD);
+  w.H = nd.H;
+  w.Hp = round_up(nd.H, kPadH);
+  w.S = std::max(nd.S, 1);
+  w.G = nd.N + (nd.B * w.S) / kTokGroup + 2;
+  w.R = nd.B * w.S + 8 * w.G;
+}
+
+bool covers(const Workspace& w, const Need& nd) {
+  return w.base && nd.B <= w.B && nd.N <= w.N && nd.D <= w.D && nd.H <= w.H && nd.S <= w.S;
+}
+
+int ensure(oea_ctx* ctx, Workspace& w, Need nd) {
+  if (covers(w, nd)) return OEA_OK;
+  if (w.base) {
+    // grow monotonically in every dimension
+    nd.B = std::max(nd.B, w.B);
+    nd.N = std::max(nd.N, w.N);
+    nd.D = std::max(nd.D, w.D);
+    nd.H = std::max(nd.H, w.H);
+    nd.S = std::max(nd.S, w.S);
+    OEA_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    cudaFree(w.base);
+    w.base = nullptr;
+  }
+  set_caps(w, nd);
+  const size_t bytes = carve(w, false);
+  OEA_CUDA_TRY(ctx, cudaMalloc(&w.base, bytes));
+  w.bytes = bytes;
+  carve(w, true);
+  return OEA_OK;
+}
+
+struct CtxExtra {
+  Workspace ws;
+};
+
+CtxExtra* extra(oea_ctx* ctx) { return reinterpret_cast<CtxExtra*>(ctx->ws); }
+
+int fail(oea_ctx* ctx, int code, const std::string& msg) { return oea_set_error(ctx, code, msg); }
+
+#define CHECK_CTX(ctx)                                                              \
+  do {                                                                             \
+    if ((ctx) == nullptr) return fail(nullptr, OEA_ERR_INVALID_ARGUMENT, "null context"); \
+  } while (0)
+
+// RoutingConfig::resolved (routing.cpp:153-182), same messages.
+int resolve(oea_ctx* ctx, const oea_routing_cfg* in, int n, oea_routing_cfg* out) {
+  if (in == nullptr) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "null routing config");
+  if (n < 1) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "RoutingConfig: expert count must be >= 1");
+  oea_routing_cfg c = *in;
+  if (c.mode < OEA_MODE_VANILLA || c.mode > OEA_MODE_SIMPLIFIED)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "unknown routing mode");
+  if (c.cap != OEA_CAP_EXACT && c.cap != OEA_CAP_PSEUDOCODE)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "unknown cap semantics");
+  if (c.mode == OEA_MODE_SIMPLIFIED) {
+    c.p = 1.0;
+    c.k_max = c.k;
+    c.max_p = n;
+  }
+  if (c.max_p == 0) c.max_p = n;
+  if (c.k < 1 || c.k > n) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "RoutingConfig: k must be in [1, N]");
+  if (c.mode != OEA_MODE_VANILLA) {
+    if (c.k0 < 1 || c.k0 > n)
+      return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "RoutingConfig: k0 must be in [1, N]");
+    if (!(c.p > 0.0) || c.p > 1.0)
+      return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "RoutingConfig: p must be in (0, 1]");
+    if (c.k_max < c.k0 || c.k_max > n)
+      return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "RoutingConfig: need k0 <= k_max <= N");
+    if (c.max_p < 1 || c.max_p > n)
+      return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "RoutingConfig: max_p must be in [1, N]");
+  }
+  *out = c;
+  return OEA_OK;
+}
+
+int32_t stride_of(const oea_routing_cfg& c) {
+  switch (c.mode) {
+    case OEA_MODE_VANILLA: return c.k;
+    case OEA_MODE_PRUNED: return c.k0;
+    default: return c.k_max + (c.cap == OEA_CAP_PSEUDOCODE ? 1 : 0);
+  }
+}
+
+Cfg dev_cfg(const oea_routing_cfg& c, int stride) {
+  Cfg d;
+  d.mode = c.mode;
+  d.k = c.k;
+  d.k0 = c.k0;
+  d.p = c.p;
+  d.k_max = c.k_max;
+  d.max_p = c.max_p;
+  d.cap = c.cap;
+  d.limit = c.k_max + (c.cap == OEA_CAP_PSEUDOCODE ? 1 : 0);
+  d.stride = stride;
+  return d;
+}
+
+oea_host::RouteBuffers route_buffers(Workspace& w, const double* scores, const uint8_t* mask) {
+  oea_host::RouteBuffers rb;
+  rb.scores = scores;
+  rb.mask = mask;
+  rb.order = w.order;
+  rb.t = w.t;
+  rb.n = w.n;
+  rb.union_bits = w.union_bits;
+  rb.sets = w.sets;
+  rb.set_len = w.set_len;
+  rb.weights = w.w64;
+  rb.weights_f32 = w.w32;
+  rb.loads = w.loads;
+  rb.active_union = w.active_union;
+  rb.active_count = w.active_count;
+  rb.total_load = w.total_load;
+  rb.base_union = w.base_union;
+  rb.base_union_count = w.base_union_count;
+  rb.err_token = w.err_token;
+  return rb;
+}
+
+template <typename T>
+int d2h(oea_ctx* ctx, T* host, const T* dev, size_t n) {
+  if (host == nullptr || n == 0) return OEA_OK;
+  OEA_CUDA_TRY(ctx, cudaMemcpyAsync(host, dev, n * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+  return OEA_OK;
+}
+
+// Copy a [B][dev_stride] int/double matrix into a host [B][host_stride] one.
+template <typename T>
+int d2h_rows(oea_ctx* ctx, T* host, int host_stride, const T* dev, int dev_stride, int B, int cols) {
+  if (host == nullptr) return OEA_OK;
+  OEA_CUDA_TRY(ctx, cudaMemcpy2DAsync(host, host_stride * sizeof(T), dev, dev_stride * sizeof(T),
+                                      cols * sizeof(T), B, cudaMemcpyDeviceToHost, ctx->stream));
+  return OEA_OK;
+}
+
+int check_domain(oea_ctx* ctx, Workspace& w, int B) {
+  int32_t tok = INT_MAX;
+  OEA_CUDA_TRY(ctx, cudaMemcpyAsync(&tok, w.err_token, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  OEA_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (tok >= 0 && tok < B)
+    return fail(ctx, OEA_ERR_DOMAIN, "route: degenerate selected-set mass for token " +
+                                         std::to_string(tok) + " (sum <= 1e-12)");
+  return OEA_OK;
+}
+
+// Export a device plan held in the workspace to caller host buffers.
+int export_plan(oea_ctx* ctx, Workspace& w, const oea_plan_view* plan, int B, int N, int stride,
+                int order_stride) {
+  if (plan == nullptr) return OEA_OK;
+  const int ps = plan->set_stride;
+  const int cols = std::min(ps, stride);
+  int rc = OEA_OK;
+  if (plan->sets) {
+    if (ps > stride) std::fill(plan->sets, plan->sets + static_cast<size_t>(B) * ps, -1);
+    rc = d2h_rows(ctx, plan->sets, ps, w.sets, stride, B, cols);
+  }
+  if (!rc && plan->weights) {
+    if (ps > stride) std::fill(plan->weights, plan->weights + static_cast<size_t>(B) * ps, 0.0);
+    rc = d2h_rows(ctx, plan->weights, ps, w.w64, stride, B, cols);
+  }
+  if (!rc && plan->weights_f32) {
+    if (ps > stride) std::fill(plan->weights_f32, plan->weights_f32 + static_cast<size_t>(B) * ps, 0.0f);
+    rc = d2h_rows(ctx, plan->weights_f32, ps, w.w32, stride, B, cols);
+  }
+  if (!rc) rc = d2h(ctx, plan->set_len, w.set_len, B);
+  if (!rc) rc = d2h(ctx, plan->loads, w.loads, N);
+  if (!rc) rc = d2h(ctx, plan->active_union, w.active_union, N);
+  if (!rc) rc = d2h(ctx, plan->active_count, w.active_count, 1);
+  if (!rc) rc = d2h(ctx, plan->total_load, w.total_load, 1);
+  if (!rc && plan->order) rc = d2h_rows(ctx, plan->order, N, w.order, order_stride, B, N);
+  if (!rc) rc = d2h(ctx, plan->phase1_t, w.t, B);
+  if (!rc) rc = d2h(ctx, plan->phase1_n, w.n, B);
+  if (!rc) rc = d2h(ctx, plan->base_union, w.base_union, N);
+  if (!rc) rc = d2h(ctx, plan->base_union_count, w.base_union_count, 1);
+  if (rc) return rc;
+  OEA_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return OEA_OK;
+}
+
+__global__ void k_pad_x_bf16_from_f64(const double* __restrict__ x, int B, int D, int Dp,
+                                      __nv_bfloat16* __restrict__ xpad) {
+  const size_t total = static_cast<size_t>(B) * Dp;
+  for (size_t f = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; f < total;
+       f += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int t = static_cast<int>(f / Dp), d = static_cast<int>(f % Dp);
+    xpad[f] = d < D ? __double2bfloat16(x[static_cast<size_t>(t) * D + d]) : __float2bfloat16_rn(0.f);
+  }
+}
+
+__global__ void k_f32_to_f64(const float* __restrict__ a, size_t n, double* __restrict__ b) {
+  for (size_t f = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; f < n;
+       f += static_cast<size_t>(gridDim.x) * blockDim.x)
+    b[f] = static_cast<double>(a[f]);
+}
+
+int blocks_for(size_t n) {
+  return static_cast<int>(std::max<size_t>(1, std::min<size_t>(4096, (n + 255) / 256)));
+}
+
+// ---------------------------------------------------------------------------
+// Decode orchestration (shared by the direct call and graph capture).
+// ---------------------------------------------------------------------------
+int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const uint8_t* mask,
+                int B, const oea_routing_cfg& rc, void* out, cudaStream_t s) {
+  const int stride = stride_of(rc);
+  const Cfg cfg = dev_cfg(rc, stride);
+  oea_host::FusedRouterBuffers rb;
+  rb.x = static_cast<const __nv_bfloat16*>(x);
+  rb.mask = mask;
+  rb.xpad = w.xpad;
+  rb.logits = w.logits;
+  rb.order = w.order;
+  rb.sets = w.sets;
+  rb.set_len = w.set_len;
+  rb.weights_f32 = w.w32;
+  rb.weights_f64 = w.w64;
+  rb.loads = w.loads;
+  rb.active_union = w.active_union;
+  rb.active_count = w.active_count;
+  rb.total_load = w.total_load;
+  rb.row_tok = w.row_tok;
+  rb.row_slot = w.row_slot;
+  rb.group_a = w.group_a;
+  rb.group_row0 = w.group_row0;
+  rb.group_rows = w.group_rows;
+  rb.hdr = w.hdr;
+  rb.counters = w.counters;
+  rb.n_counters = w.G + L->Dp / 16;
+  rb.out = static_cast<float*>(out);
+  rb.phase1_n = w.n;
+  rb.base_union = w.base_union;
+  rb.base_union_count = w.base_union_count;
+  int r = oea_host::router_fused_launch(ctx, L, cfg, B, rb, s);
+  if (r) return r;
+  oea_host::FfnBuffers fb;
+  fb.x = w.xpad;
+  fb.row_tok = w.row_tok;
+  fb.row_slot = w.row_slot;
+  fb.group_a = w.group_a;
+  fb.group_row0 = w.group_row0;
+  fb.group_rows = w.group_rows;
+  fb.hdr = w.hdr;
+  fb.counters = w.counters;
+  fb.max_groups = w.G;
+  fb.hbuf = w.hbuf;
+  fb.ybuf = w.ybuf;
+  fb.set_len = w.set_len;
+  fb.weights_f32 = w.w32;
+  fb.weights_f64 = w.w64;
+  fb.out = out;
+  return oea_host::ffn_bf16_launch(ctx, L, B, stride, fb, true, s);
+}
+
+// f32/f64 layers: router_scores (fp64) -> route_f64 -> compaction -> SIMT FFN.
+int decode_simt(oea_ctx* ctx, Workspace& w, oea_layer* L, const double* x, const uint8_t* mask,
+                int B, const oea_routing_cfg& rc, double* out, cudaStream_t s) {
+  const int stride = stride_of(rc);
+  const Cfg cfg = dev_cfg(rc, stride);
+  int r = oea_host::router_scores_launch(ctx, L, x, B, w.logits64, w.scores, s);
+  if (r) return r;
+  const int set_mode = rc.mode == OEA_MODE_VANILLA ? 0 : rc.mode == OEA_MODE_PRUNED ? 1 : 2;
+  r = oea_host::route_f64_launch(ctx, cfg, B, L->N, route_buffers(w, w.scores, mask), false,
+                                 rc.mode != OEA_MODE_VANILLA, set_mode, false, s);
+  if (r) return r;
+  oea_host::CompactBuffers cb{w.sets, w.set_len, w.row_tok, w.row_slot, w.group_a,
+                              w.group_row0, w.group_rows, w.hdr, w.counters, w.G + 1};
+  r = oea_host::compact_launch(ctx, B, L->N, stride, cb, w.tokbits, w.active_union,
+                               w.active_count, s);
+  if (r) return r;
+  r = oea_host::cast_f64_launch(ctx, x, static_cast<size_t>(B) * L->D, L->dtype, w.xT, s);
+  if (r) return r;
+  oea_host::FfnBuffers fb{};
+  fb.x = w.xT;
+  fb.row_tok = w.row_tok;
+  fb.row_slot = w.row_slot;
+  fb.group_a = w.group_a;
+  fb.group_row0 = w.group_row0;
+  fb.group_rows = w.group_rows;
+  fb.hdr = w.hdr;
+  fb.hbuf = w.hbuf;
+  fb.ybuf = w.ybuf;
+  fb.set_len = w.set_len;
+  fb.weights_f64 = w.w64;
+  fb.out = out;
+  return oea_host::ffn_simt_launch(ctx, L, B, stride, fb, w.G, s);
+}
+
+int validate_decode(oea_ctx* ctx, oea_layer* L, int B, const oea_routing_cfg* cfg,
+                    oea_routing_cfg* rc) {
+  if (L == nullptr) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "null layer");
+  if (B < 1) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "moe_decode: batch must be >= 1");
+  int r = resolve(ctx, cfg, L->N, rc);
+  if (r) return r;
+  if (L->dtype == OEA_DTYPE_BF16) {
+    if (B > kMaxFusedB)
+      return fail(ctx, OEA_ERR_INVALID_ARGUMENT,
+                  "moe_decode: bf16 fused decode supports B <= " + std::to_string(kMaxFusedB));
+    if (L->N > kMaxFusedN)
+      return fail(ctx, OEA_ERR_INVALID_ARGUMENT,
+                  "moe_decode: bf16 fused router supports N <= " + std::to_string(kMaxFusedN));
+  }
+  return OEA_OK;
+}
+
+Need need_for(const oea_layer* L, int B, int S) { return Need{B, L->N, L->D, L->H, S}; }
+
+}  // namespace
+
+// ===========================================================================
+// Status helpers.
+// ===========================================================================
+int oea_set_error(oea_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->last_error = msg;
+  t_last_error = msg;
+  return code;
+}
+
+int oea_check_cuda(oea_ctx* ctx, cudaError_t e, const char* what) {
+  return oea_set_error(ctx, OEA_ERR_CUDA,
+                       std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+extern "C" {
+
+int oea_abi_version(void) { return OEA_ABI_VERSION; }
+
+int oea_ctx_create(int32_t device, oea_ctx_t* out) {
+  if (out == nullptr) return fail(nullptr, OEA_ERR_INVALID_ARGUMENT, "null output pointer");
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return fail(nullptr, OEA_ERR_CUDA,
+                std::string("no CUDA device available (oea has no CPU path): ") +
+                    (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices"));
+  if (device < 0 || device >= count) return fail(nullptr, OEA_ERR_INVALID_ARGUMENT, "bad device index");
+  cudaDeviceProp prop;
+  e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) return oea_check_cuda(nullptr, e, "cudaGetDeviceProperties");
+  if (prop.major != 10)
+    return fail(nullptr, OEA_ERR_CUDA,
+                "oea kernels are built for sm_100a; device is sm_" + std::to_string(prop.major) +
+                    std::to_string(prop.minor));
+  e = cudaSetDevice(device);
+  if (e != cudaSuccess) return oea_check_cuda(nullptr, e, "cudaSetDevice");
+  auto* ctx = new oea_ctx;
+  ctx->device = device;
+  ctx->num_sms = prop.multiProcessorCount;
+  e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return oea_check_cuda(nullptr, e, "cudaStreamCreate");
+  }
+  ctx->ws = new CtxExtra;
+  *out = ctx;
+  return OEA_OK;
+}
+
+int oea_ctx_destroy(oea_ctx_t ctx) {
+  if (ctx == nullptr) return OEA_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  CtxExtra* x = extra(ctx);
+  if (x) {
+    if (x->ws.base) cudaFree(x->ws.base);
+    delete x;
+  }
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return OEA_OK;
+}
+
+const char* oea_last_error(oea_ctx_t ctx) {
+  return ctx ? ctx->last_error.c_str() : t_last_error.c_str();
+}
+
+int oea_ctx_stream(oea_ctx_t ctx, void** stream_out) {
+  CHECK_CTX(ctx);
+  *stream_out = ctx->stream;
+  return OEA_OK;
+}
+
+int oea_ctx_synchronize(oea_ctx_t ctx) {
+  CHECK_CTX(ctx);
+  OEA_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return OEA_OK;
+}
+
+int64_t oea_ctx_kernel_launches(oea_ctx_t ctx) { return ctx ? ctx->launches : 0; }
+
+int oea_config_resolve(const oea_routing_cfg* in, int32_t n_experts, oea_routing_cfg* out) {
+  if (out == nullptr) return fail(nullptr, OEA_ERR_INVALID_ARGUMENT, "null output pointer");
+  return resolve(nullptr, in, n_experts, out);
+}
+
+int32_t oea_plan_set_stride(const oea_routing_cfg* resolved) {
+  return resolved ? stride_of(*resolved) : 0;
+}
+
+// ---------------------------------------------------------------------------
+// K1 routing entry points.
+// ---------------------------------------------------------------------------
+int oea_route_f64(oea_ctx_t ctx, const double* scores_dev, const uint8_t* mask_dev, int32_t B,
+                  int32_t N, const oea_routing_cfg* cfg, const oea_plan_view* plan, void* stream) {
+  CHECK_CTX(ctx);
+  oea_routing_cfg rc;
+  int r = resolve(ctx, cfg, N, &rc);
+  if (r) return r;
+  if (B < 1 || N < 1) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "sort_experts: dimensions must be >= 1");
+  if (N > kMaxRouteN)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "route: N > " + std::to_string(kMaxRouteN));
+  if (plan == nullptr || plan->sets == nullptr || plan->set_len == nullptr)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "route: plan sets/set_len are required");
+  const int stride = stride_of(rc);
+  if (plan->set_stride < stride)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "route: plan set_stride too small");
+  Workspace& w = extra(ctx)->ws;
+  r = ensure(ctx, w, Need{B, N, 1, 1, plan->set_stride});
+  if (r) return r;
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  oea_host::RouteBuffers rb = route_buffers(w, scores_dev, mask_dev);
+  rb.sets = plan->sets;
+  rb.set_len = plan->set_len;
+  rb.weights = plan->weights;
+  rb.weights_f32 = plan->weights_f32;
+  if (plan->loads) rb.loads = plan->loads;
+  if (plan->active_union) rb.active_union = plan->active_union;
+  if (plan->active_count) rb.active_count = plan->active_count;
+  if (plan->total_load) rb.total_load = plan->total_load;
+  if (plan->order) rb.order = plan->order;
+  if (plan->phase1_t) rb.t = plan->phase1_t;
+  if (plan->phase1_n) rb.n = plan->phase1_n;
+  rb.base_union = plan->base_union;
+  rb.base_union_count = plan->base_union_count;
+  if (rb.weights == nullptr && rb.weights_f32 == nullptr) rb.weights = w.w64;  // domain check
+  const Cfg dc = dev_cfg(rc, plan->set_stride);
+  const int set_mode = rc.mode == OEA_MODE_VANILLA ? 0 : rc.mode == OEA_MODE_PRUNED ? 1 : 2;
+  return oea_host::route_f64_launch(ctx, dc, B, N, rb, false, rc.mode != OEA_MODE_VANILLA,
+                                    set_mode, false, s);
+}
+
+int oea_route_f64_host(oea_ctx_t ctx, const double* scores, const uint8_t* mask, int32_t B,
+                       int32_t N, const oea_routing_cfg* cfg, const oea_plan_view* plan) {
+  CHECK_CTX(ctx);
+  oea_routing_cfg rc;
+  int r = resolve(ctx, cfg, N, &rc);
+  if (r) return r;
+  if (B < 1 || N < 1) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "sort_experts: dimensions must be >= 1");
+  if (N > kMaxRouteN)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "route: N > " + std::to_string(kMaxRouteN));
+  if (plan == nullptr || plan->sets == nullptr || plan->set_len == nullptr)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "route: plan sets/set_len are required");
+  const int stride = stride_of(rc);
+  if (plan->set_stride < stride)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "route: plan set_stride too small");
+  Workspace& w = extra(ctx)->ws;
+  r = ensure(ctx, w, Need{B, N, 1, 1, stride});
+  if (r) return r;
+  cudaStream_t s = ctx->stream;
+  OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.scores, scores, sizeof(double) * B * N,
+                                    cudaMemcpyHostToDevice, s));
+  if (mask) OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.mask, mask, B, cudaMemcpyHostToDevice, s));
+  const Cfg dc = dev_cfg(rc, stride);
+  const int set_mode = rc.mode == OEA_MODE_VANILLA ? 0 : rc.mode == OEA_MODE_PRUNED ? 1 : 2;
+  r = oea_host::route_f64_launch(ctx, dc, B, N, route_buffers(w, w.scores, mask ? w.mask : nullptr),
+                                 false, rc.mode != OEA_MODE_VANILLA, set_mode, false, s);
+  if (r) return r;
+  r = check_domain(ctx, w, B);
+  if (r) return r;
+  ctx->last_B = B;
+  ctx->last_N = N;
+  ctx->last_stride = stride;
+  ctx->last_kind = 2;
+  return export_plan(ctx, w, plan, B, N, stride, N);
+}
+
+int oea_sort_experts_f64_host(oea_ctx_t ctx, const double* scores, int32_t B, int32_t N,
+                              int32_t* order) {
+  CHECK_CTX(ctx);
+  if (B < 1 || N < 1) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "sort_experts: dimensions must be >= 1");
+  if (N > kMaxRouteN)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "sort_experts: N > " + std::to_string(kMaxRouteN));
+  Workspace& w = extra(ctx)->ws;
+  int r = ensure(ctx, w, Need{B, N, 1, 1, 1});
+  if (r) return r;
+  cudaStream_t s = ctx->stream;
+  OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.scores, scores, sizeof(double) * B * N,
+                                    cudaMemcpyHostToDevice, s));
+  oea_routing_cfg rc{OEA_MODE_VANILLA, 1, 1, 1.0, 1, N, OEA_CAP_EXACT};
+  Cfg dc = dev_cfg(rc, 1);
+  oea_host::RouteBuffers rb = route_buffers(w, w.scores, nullptr);
+  rb.weights = nullptr;
+  rb.weights_f32 = nullptr;
+  r = oea_host::route_f64_launch(ctx, dc, B, N, rb, false, false, 0, false, s);
+  if (r) return r;
+  r = d2h(ctx, order, w.order, static_cast<size_t>(B) * N);
+  if (r) return r;
+  OEA_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  return OEA_OK;
+}
+
+int oea_phase1_f64_host(oea_ctx_t ctx, const double* scores, const uint8_t* mask, int32_t B,
+                        int32_t N, const int32_t* order, const oea_routing_cfg* cfg, int32_t* t,
+                        int32_t* n, int32_t* base_sets, int32_t base_stride, int32_t* base_union,
+                        int32_t* base_union_count) {
+  CHECK_CTX(ctx);
+  oea_routing_cfg rc;
+  int r = resolve(ctx, cfg, N, &rc);
+  if (r) return r;
+  if (B < 1 || N < 1) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "sort_experts: dimensions must be >= 1");
+  if (order == nullptr) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "phase1: order is required");
+  const int k0 = std::max(rc.k0, 1);
+  if (base_sets && base_stride < k0)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "phase1: base_stride must be >= k0");
+  Workspace& w = extra(ctx)->ws;
+  r = ensure(ctx, w, Need{B, N, 1, 1, k0});
+  if (r) return r;
+  cudaStream_t s = ctx->stream;
+  OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.scores, scores, sizeof(double) * B * N,
+                                    cudaMemcpyHostToDevice, s));
+  OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.order, order, sizeof(int32_t) * B * N,
+                                    cudaMemcpyHostToDevice, s));
+  if (mask) OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.mask, mask, B, cudaMemcpyHostToDevice, s));
+  Cfg dc = dev_cfg(rc, k0);
+  oea_host::RouteBuffers rb = route_buffers(w, w.scores, mask ? w.mask : nullptr);
+  rb.weights = nullptr;
+  rb.weights_f32 = nullptr;
+  r = oea_host::route_f64_launch(ctx, dc, B, N, rb, true, true, 1, false, s);
+  if (r) return r;
+  r = d2h(ctx, t, w.t, B);
+  if (!r) r = d2h(ctx, n, w.n, B);
+  if (!r && base_sets) r = d2h_rows(ctx, base_sets, base_stride, w.sets, k0, B, k0);
+  if (!r) r = d2h(ctx, base_union, w.base_union, N);
+  if (!r) r = d2h(ctx, base_union_count, w.base_union_count, 1);
+  if (r) return r;
+  OEA_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  if (base_sets && base_stride > k0)
+    for (int i = 0; i < B; ++i)
+      for (int j = k0; j < base_stride; ++j) base_sets[static_cast<size_t>(i) * base_stride + j] = -1;
+  return OEA_OK;
+}
+
+int oea_phase2_f64_host(oea_ctx_t ctx, const uint8_t* mask, int32_t B, int32_t N,
+                        const int32_t* order, const int32_t* n, const int32_t* base_union,
+                        int32_t base_union_count, const oea_routing_cfg* cfg,
+                        const oea_plan_view* plan) {
+  CHECK_CTX(ctx);
+  oea_routing_cfg rc;
+  int r = resolve(ctx, cfg, N, &rc);
+  if (r) return r;
+  if (B < 1 || N < 1) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "sort_experts: dimensions must be >= 1");
+  if (order == nullptr || n == nullptr || plan == nullptr || plan->sets == nullptr ||
+      plan->set_len == nullptr)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "phase2: order, n and plan sets are required");
+  int max_n = 0;
+  for (int i = 0; i < B; ++i) {
+    if (n[i] < 0 || n[i] > N) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "phase2: n out of range");
+    max_n = std::max(max_n, n[i]);
+  }
+  const int limit = rc.k_max + (rc.cap == OEA_CAP_PSEUDOCODE ? 1 : 0);
+  const int stride = std::max(std::max(limit, max_n), 1);
+  if (plan->set_stride < stride)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "phase2: plan set_stride too small");
+  Workspace& w = extra(ctx)->ws;
+  r = ensure(ctx, w, Need{B, N, 1, 1, stride});
+  if (r) return r;
+  cudaStream_t s = ctx->stream;
+  OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.order, order, sizeof(int32_t) * B * N, cudaMemcpyHostToDevice, s));
+  OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.n, n, sizeof(int32_t) * B, cudaMemcpyHostToDevice, s));
+  if (base_union_count > 0)
+    OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.base_union, base_union, sizeof(int32_t) * base_union_count,
+                                      cudaMemcpyHostToDevice, s));
+  if (mask) OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.mask, mask, B, cudaMemcpyHostToDevice, s));
+  r = oea_host::union_from_list_launch(ctx, w.base_union, base_union_count, N, w.union_bits, s);
+  if (r) return r;
+  Cfg dc = dev_cfg(rc, stride);
+  oea_host::RouteBuffers rb = route_buffers(w, w.scores, mask ? w.mask : nullptr);
+  rb.weights = nullptr;
+  rb.weights_f32 = nullptr;
+  rb.base_union = nullptr;
+  rb.base_union_count = nullptr;
+  r = oea_host::route_f64_launch(ctx, dc, B, N, rb, true, false, 2, true, s);
+  if (r) return r;
+  oea_plan_view pv = *plan;
+  pv.weights = nullptr;
+  pv.weights_f32 = nullptr;
+  pv.order = nullptr;
+  pv.phase1_t = nullptr;
+  pv.phase1_n = nullptr;
+  pv.base_union = nullptr;
+  pv.base_union_count = nullptr;
+  return export_plan(ctx, w, &pv, B, N, stride, N);
+}
+
+// ---------------------------------------------------------------------------
+// Layers.
+// ---------------------------------------------------------------------------
+int oea_layer_create(oea_ctx_t ctx, int32_t D, int32_t H, int32_t N, int32_t dtype,
+                     oea_layer_t* out) {
+  CHECK_CTX(ctx);
+  if (out == nullptr) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "null output pointer");
+  *out = nullptr;
+  if (D < 1 || H < 1 || N < 1)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "make_random_layer: dims must be positive");
+  if (dtype != OEA_DTYPE_BF16 && dtype != OEA_DTYPE_F32 && dtype != OEA_DTYPE_F64)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "layer: unknown dtype");
+  auto* L = new oea_layer;
+  L->ctx = ctx;
+  L->D = D;
+  L->H = H;
+  L->N = N;
+  L->dtype = dtype;
+  L->Dp = round_up(D, kPadD);
+  L->Hp = round_up(H, kPadH);
+  L->Np = round_up(N, 16);
+  cudaError_t e = cudaSuccess;
+  if (dtype == OEA_DTYPE_BF16) {
+    L->router_bytes = static_cast<size_t>(L->Np) * L->Dp * 2;
+    L->w1_bytes = static_cast<size_t>(N) * 2 * L->Dp * L->Hp * 2;
+    L->w2_bytes = static_cast<size_t>(N) * L->Dp * L->Hp * 2;
+  } else {
+    const size_t es = dtype == OEA_DTYPE_F64 ? 8 : 4;
+    L->router_bytes = static_cast<size_t>(D) * N * es;
+    L->w1_bytes = static_cast<size_t>(N) * D * H * es;
+    L->up_bytes = L->w1_bytes;
+    L->w2_bytes = static_cast<size_t>(N) * H * D * es;
+  }
+  e = cudaMalloc(&L->router, L->router_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&L->w1, L->w1_bytes);
+  if (e == cudaSuccess && L->up_bytes) e = cudaMalloc(&L->w_up, L->up_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&L->w2, L->w2_bytes);
+  if (e == cudaSuccess) e = cudaMemsetAsync(L->router, 0, L->router_bytes, ctx->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(L->w1, 0, L->w1_bytes, ctx->stream);
+  if (e == cudaSuccess && L->up_bytes) e = cudaMemsetAsync(L->w_up, 0, L->up_bytes, ctx->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(L->w2, 0, L->w2_bytes, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) {
+    oea_layer_destroy(L);
+    return oea_check_cuda(ctx, e, "layer allocation");
+  }
+  *out = L;
+  return OEA_OK;
+}
+
+int oea_layer_destroy(oea_layer_t L) {
+  if (L == nullptr) return OEA_OK;
+  if (L->ctx) cudaStreamSynchronize(L->ctx->stream);
+  cudaFree(L->router);
+  cudaFree(L->w1);
+  cudaFree(L->w_up);
+  cudaFree(L->w2);
+  delete L;
+  return OEA_OK;
+}
+
+static int check_dtype(oea_ctx* ctx, int dt) {
+  if (dt != OEA_DTYPE_F64 && dt != OEA_DTYPE_F32 && dt != OEA_DTYPE_BF16)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "unknown dtype");
+  return OEA_OK;
+}
+
+int oea_layer_upload_router(oea_layer_t L, const void* router, int32_t src_dtype,
+                            int32_t src_on_device) {
+  if (L == nullptr || router == nullptr) return fail(nullptr, OEA_ERR_INVALID_ARGUMENT, "null argument");
+  int r = check_dtype(L->ctx, src_dtype);
+  if (r) return r;
+  return oea_host::layer_upload_router(L, router, src_dtype, src_on_device);
+}
+
+int oea_layer_upload_expert(oea_layer_t L, int32_t e, const void* w_gate, const void* w_up,
+                            const void* w_down, int32_t src_dtype, int32_t src_on_device) {
+  if (L == nullptr || !w_gate || !w_up || !w_down)
+    return fail(nullptr, OEA_ERR_INVALID_ARGUMENT, "null argument");
+  if (e < 0 || e >= L->N) return fail(L->ctx, OEA_ERR_INVALID_ARGUMENT, "expert index out of range");
+  int r = check_dtype(L->ctx, src_dtype);
+  if (r) return r;
+  return oea_host::layer_upload_expert(L, e, w_gate, w_up, w_down, src_dtype, src_on_device);
+}
+
+int oea_layer_init_random(oea_layer_t L, uint64_t seed) {
+  if (L == nullptr) return fail(nullptr, OEA_ERR_INVALID_ARGUMENT, "null layer");
+  return oea_host::layer_init_random(L, seed);
+}
+
+int oea_layer_download_router(oea_layer_t L, void* router, int32_t dst_dtype) {
+  if (L == nullptr || router == nullptr) return fail(nullptr, OEA_ERR_INVALID_ARGUMENT, "null argument");
+  int r = check_dtype(L->ctx, dst_dtype);
+  if (r) return r;
+  return oea_host::layer_download_router(L, router, dst_dtype);
+}
+
+int oea_layer_download_expert(oea_layer_t L, int32_t e, void* w_gate, void* w_up, void* w_down,
+                              int32_t dst_dtype) {
+  if (L == nullptr || !w_gate || !w_up || !w_down)
+    return fail(nullptr, OEA_ERR_INVALID_ARGUMENT, "null argument");
+  if (e < 0 || e >= L->N) return fail(L->ctx, OEA_ERR_INVALID_ARGUMENT, "expert index out of range");
+  int r = check_dtype(L->ctx, dst_dtype);
+  if (r) return r;
+  return oea_host::layer_download_expert(L, e, w_gate, w_up, w_down, dst_dtype);
+}
+
+int oea_layer_info(oea_layer_t L, int32_t* D, int32_t* H, int32_t* N, int32_t* dtype,
+                   int64_t* bytes_per_expert, int64_t* device_bytes) {
+  if (L == nullptr) return fail(nullptr, OEA_ERR_INVALID_ARGUMENT, "null layer");
+  if (D) *D = L->D;
+  if (H) *H = L->H;
+  if (N) *N = L->N;
+  if (dtype) *dtype = L->dtype;
+  if (bytes_per_expert)
+    *bytes_per_expert = static_cast<int64_t>((L->w1_bytes + L->up_bytes + L->w2_bytes) / L->N);
+  if (device_bytes)
+    *device_bytes = static_cast<int64_t>(L->router_bytes + L->w1_bytes + L->up_bytes + L->w2_bytes);
+  return OEA_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Decode.
+// ---------------------------------------------------------------------------
+int oea_moe_decode(oea_ctx_t ctx, oea_layer_t L, const void* x_dev, const uint8_t* mask_dev,
+                   int32_t B, const oea_routing_cfg* cfg, void* out_dev, void* stream) {
+  CHECK_CTX(ctx);
+  oea_routing_cfg rc;
+  int r = validate_decode(ctx, L, B, cfg, &rc);
+  if (r) return r;
+  if (x_dev == nullptr || out_dev == nullptr)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "moe_decode: null x/out");
+  Workspace& w = extra(ctx)->ws;
+  r = ensure(ctx, w, need_for(L, B, stride_of(rc)));
+  if (r) return r;
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  ctx->last_B = B;
+  ctx->last_N = L->N;
+  ctx->last_stride = stride_of(rc);
+  if (L->dtype == OEA_DTYPE_BF16) {
+    ctx->last_kind = 1;
+    return decode_bf16(ctx, w, L, x_dev, mask_dev, B, rc, out_dev, s);
+  }
+  ctx->last_kind = 2;
+  return decode_simt(ctx, w, L, static_cast<const double*>(x_dev), mask_dev, B, rc,
+                     static_cast<double*>(out_dev), s);
+}
+
+int oea_moe_decode_host(oea_ctx_t ctx, oea_layer_t L, const void* x_host,
+                        const uint8_t* mask_host, int32_t B, const oea_routing_cfg* cfg,
+                        void* out_host) {
+  CHECK_CTX(ctx);
+  oea_routing_cfg rc;
+  int r = validate_decode(ctx, L, B, cfg, &rc);
+  if (r) return r;
+  if (x_host == nullptr || out_host == nullptr)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "moe_decode: null x/out");
+  Workspace& w = extra(ctx)->ws;
+  r = ensure(ctx, w, need_for(L, B, stride_of(rc)));
+  if (r) return r;
+  cudaStream_t s = ctx->stream;
+  const bool bf = L->dtype == OEA_DTYPE_BF16;
+  const size_t xbytes = static_cast<size_t>(B) * L->D * (bf ? 2 : 8);
+  const size_t obytes = static_cast<size_t>(B) * L->D * (bf ? 4 : 8);
+  OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.xin, x_host, xbytes, cudaMemcpyHostToDevice, s));
+  if (mask_host) OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.mask, mask_host, B, cudaMemcpyHostToDevice, s));
+  ctx->last_B = B;
+  ctx->last_N = L->N;
+  ctx->last_stride = stride_of(rc);
+  if (bf) {
+    ctx->last_kind = 1;
+    r = decode_bf16(ctx, w, L, w.xin, mask_host ? w.mask : nullptr, B, rc, w.out, s);
+  } else {
+    ctx->last_kind = 2;
+    r = decode_simt(ctx, w, L, static_cast<const double*>(w.xin), mask_host ? w.mask : nullptr, B,
+                    rc, static_cast<double*>(w.out), s);
+  }
+  if (r) return r;
+  OEA_CUDA_TRY(ctx, cudaMemcpyAsync(out_host, w.out, obytes, cudaMemcpyDeviceToHost, s));
+  OEA_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  if (!bf) return check_domain(ctx, w, B);
+  return OEA_OK;
+}
+
+int oea_last_plan_host(oea_ctx_t ctx, const oea_plan_view* plan, float* logits, double* scores) {
+  CHECK_CTX(ctx);
+  if (ctx->last_kind == 0) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "no decode/route has run");
+  Workspace& w = extra(ctx)->ws;
+  OEA_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  const int B = ctx->last_B, N = ctx->last_N;
+  const int order_stride = ctx->last_kind == 1 ? round_up(N, 16) : N;
+  int r = export_plan(ctx, w, plan, B, N, ctx->last_stride, order_stride);
+  if (r) return r;
+  if (logits && ctx->last_kind == 1) {
+    r = d2h_rows(ctx, logits, N, w.logits, round_up(N, 16), B, N);
+    if (r) return r;
+  }
+  if (scores && ctx->last_kind == 2) {
+    r = d2h(ctx, scores, w.scores, static_cast<size_t>(B) * N);
+    if (r) return r;
+  }
+  OEA_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return OEA_OK;
+}
+
+int oea_decode_graph_create(oea_ctx_t ctx, oea_layer_t L, const void* x_dev,
+                            const uint8_t* mask_dev, int32_t B, const oea_routing_cfg* cfg,
+                            void* out_dev, oea_graph_t* out) {
+  CHECK_CTX(ctx);
+  if (out == nullptr) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "null output pointer");
+  *out = nullptr;
+  oea_routing_cfg rc;
+  int r = validate_decode(ctx, L, B, cfg, &rc);
+  if (r) return r;
+  Workspace& w = extra(ctx)->ws;
+  r = ensure(ctx, w, need_for(L, B, stride_of(rc)));
+  if (r) return r;
+  // The graph binds the context workspace as sized now; later calls that need
+  // a larger workspace re-allocate it, so create graphs after sizing (or
+  // destroy/re-create them).
+  OEA_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  auto* g = new oea_graph;
+  g->ctx = ctx;
+  cudaStream_t s = ctx->stream;
+  cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) {
+    delete g;
+    return oea_check_cuda(ctx, e, "cudaStreamBeginCapture");
+  }
+  if (L->dtype == OEA_DTYPE_BF16)
+    r = decode_bf16(ctx, w, L, x_dev, mask_dev, B, rc, out_dev, s);
+  else
+    r = decode_simt(ctx, w, L, static_cast<const double*>(x_dev), mask_dev, B, rc,
+                    static_cast<double*>(out_dev), s);
+  cudaGraph_t graph = nullptr;
+  e = cudaStreamEndCapture(s, &graph);
+  if (r || e != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    delete g;
+    return r ? r : oea_check_cuda(ctx, e, "cudaStreamEndCapture");
+  }
+  g->graph = graph;
+  e = cudaGraphInstantiate(&g->exec, graph, 0);
+  if (e != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    delete g;
+    return oea_check_cuda(ctx, e, "cudaGraphInstantiate");
+  }
+  ctx->last_B = B;
+  ctx->last_N = L->N;
+  ctx->last_stride = stride_of(rc);
+  ctx->last_kind = L->dtype == OEA_DTYPE_BF16 ? 1 : 2;
+  *out = g;
+  return OEA_OK;
+}
+
+int oea_graph_launch(oea_graph_t g, void* stream) {
+  if (g == nullptr) return fail(nullptr, OEA_ERR_INVALID_ARGUMENT, "null graph");
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->ctx->stream;
+  OEA_CUDA_TRY(g->ctx, cudaGraphLaunch(g->exec, s));
+  g->ctx->launches += 2;
+  return OEA_OK;
+}
+
+int oea_graph_destroy(oea_graph_t g) {
+  if (g == nullptr) return OEA_OK;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  delete g;
+  return OEA_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Drop-in layer math on a given plan.
+// ---------------------------------------------------------------------------
+int oea_moe_forward_plan_host(oea_ctx_t ctx, oea_layer_t L, const double* x, int32_t B,
+                              const int32_t* sets, const int32_t* set_len, const double* weights,
+                              int32_t set_stride, const uint8_t* mask, double* out) {
+  CHECK_CTX(ctx);
+  if (L == nullptr || x == nullptr || out == nullptr || sets == nullptr || set_len == nullptr ||
+      weights == nullptr)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "moe_forward: null argument");
+  if (B < 1) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "moe_forward: plan batch size mismatch");
+  if (set_stride < 1) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "moe_forward: bad set stride");
+  // Plan validation (moe_layer.hpp:134-152), host-side argument checks.
+  for (int i = 0; i < B; ++i) {
+    if (set_len[i] < 0 || set_len[i] > set_stride)
+      return fail(ctx, OEA_ERR_INVALID_ARGUMENT,
+                  "moe_forward: weights/set size mismatch for token " + std::to_string(i));
+    const bool real = mask == nullptr || mask[i] != 0;
+    if (set_len[i] == 0) {
+      if (real && mask != nullptr)
+        return fail(ctx, OEA_ERR_INVALID_ARGUMENT,
+                    "moe_forward: empty selected set for unmasked token " + std::to_string(i));
+      continue;
+    }
+    for (int j = 0; j < set_len[i]; ++j) {
+      const int e = sets[static_cast<size_t>(i) * set_stride + j];
+      if (e < 0 || e >= L->N)
+        return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "moe_forward: expert index out of range");
+      for (int jj = 0; jj < j; ++jj)
+        if (sets[static_cast<size_t>(i) * set_stride + jj] == e)
+          return fail(ctx, OEA_ERR_INVALID_ARGUMENT,
+                      "moe_forward: duplicate expert in the set of token " + std::to_string(i));
+    }
+  }
+  Workspace& w = extra(ctx)->ws;
+  int r = ensure(ctx, w, need_for(L, B, set_stride));
+  if (r) return r;
+  cudaStream_t s = ctx->stream;
+  OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.x64, x, sizeof(double) * B * L->D, cudaMemcpyHostToDevice, s));
+  OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.sets, sets, sizeof(int32_t) * B * set_stride,
+                                    cudaMemcpyHostToDevice, s));
+  // zero lengths of masked rows are already 0 in the caller's plan
+  OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.set_len, set_len, sizeof(int32_t) * B, cudaMemcpyHostToDevice, s));
+  OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.w64, weights, sizeof(double) * B * set_stride,
+                                    cudaMemcpyHostToDevice, s));
+  oea_host::CompactBuffers cb{w.sets, w.set_len, w.row_tok, w.row_slot, w.group_a,
+                              w.group_row0, w.group_rows, w.hdr, w.counters,
+                              w.G + L->Dp / 16 + 1};
+  r = oea_host::compact_launch(ctx, B, L->N, set_stride, cb, w.tokbits, w.active_union,
+                               w.active_count, s);
+  if (r) return r;
+  if (L->dtype == OEA_DTYPE_BF16) {
+    // weights to fp32 for the tensor-core combine; x to padded bf16
+    r = oea_host::cast_f64_launch(ctx, w.w64, static_cast<size_t>(B) * set_stride, OEA_DTYPE_F32,
+                                  w.w32, s);
+    if (r) return r;
+    k_pad_x_bf16_from_f64<<<blocks_for(static_cast<size_t>(B) * L->Dp), 256, 0, s>>>(
+        w.x64, B, L->D, L->Dp, w.xpad);
+    OEA_LAUNCHED(ctx);
+    OEA_CUDA_TRY(ctx, cudaMemsetAsync(w.out32, 0, sizeof(float) * B * L->D, s));
+    oea_host::FfnBuffers fb{};
+    fb.x = w.xpad;
+    fb.row_tok = w.row_tok;
+    fb.row_slot = w.row_slot;
+    fb.group_a = w.group_a;
+    fb.group_row0 = w.group_row0;
+    fb.group_rows = w.group_rows;
+    fb.hdr = w.hdr;
+    fb.counters = w.counters;
+    fb.max_groups = w.G;
+    fb.hbuf = w.hbuf;
+    fb.ybuf = w.ybuf;
+    fb.set_len = w.set_len;
+    fb.weights_f32 = w.w32;
+    fb.out = w.out32;
+    r = oea_host::ffn_bf16_launch(ctx, L, B, set_stride, fb, false, s);
+    if (r) return r;
+    k_f32_to_f64<<<blocks_for(static_cast<size_t>(B) * L->D), 256, 0, s>>>(
+        w.out32, static_cast<size_t>(B) * L->D, static_cast<double*>(w.out));
+    OEA_LAUNCHED(ctx);
+  } else {
+    r = oea_host::cast_f64_launch(ctx, w.x64, static_cast<size_t>(B) * L->D, L->dtype, w.xT, s);
+    if (r) return r;
+    oea_host::FfnBuffers fb{};
+    fb.x = w.xT;
+    fb.row_tok = w.row_tok;
+    fb.row_slot = w.row_slot;
+    fb.group_a = w.group_a;
+    fb.group_row0 = w.group_row0;
+    fb.group_rows = w.group_rows;
+    fb.hdr = w.hdr;
+    fb.hbuf = w.hbuf;
+    fb.ybuf = w.ybuf;
+    fb.set_len = w.set_len;
+    fb.weights_f64 = w.w64;
+    fb.out = w.out;
+    r = oea_host::ffn_simt_launch(ctx, L, B, set_stride, fb, w.G, s);
+    if (r) return r;
+  }
+  OEA_CUDA_TRY(ctx, cudaMemcpyAsync(out, w.out, sizeof(double) * B * L->D, cudaMemcpyDeviceToHost, s));
+  OEA_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  return OEA_OK;
+}
+
+int oea_router_scores_host(oea_ctx_t ctx, oea_layer_t L, const double* x, int32_t B,
+                           double* scores) {
+  CHECK_CTX(ctx);
+  if (L == nullptr || x == nullptr || scores == nullptr)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "router_scores: null argument");
+  if (L->dtype == OEA_DTYPE_BF16)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT,
+                "router_scores: bf16 layers route on fused fp32 logits; use oea_last_plan_host");
+  if (B < 1) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "router_scores: batch must be >= 1");
+  Workspace& w = extra(ctx)->ws;
+  int r = ensure(ctx, w, need_for(L, B, 1));
+  if (r) return r;
+  cudaStream_t s = ctx->stream;
+  OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.x64, x, sizeof(double) * B * L->D, cudaMemcpyHostToDevice, s));
+  r = oea_host::router_scores_launch(ctx, L, w.x64, B, w.logits64, w.scores, s);
+  if (r) return r;
+  OEA_CUDA_TRY(ctx, cudaMemcpyAsync(scores, w.scores, sizeof(double) * B * L->N,
+                                    cudaMemcpyDeviceToHost, s));
+  OEA_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  return OEA_OK;
+}
+
+int oea_ep_owner(int32_t N, int32_t world, int32_t expert) {
+  if (N < 1 || world < 1 || expert < 0 || expert >= N) return -1;
+  // rank r owns experts [floor(N r / P), floor(N (r+1) / P))
+  for (int r = 0; r < world; ++r) {
+    const int64_t hi = static_cast<int64_t>(N) * (r + 1) / world;
+    if (expert < hi) return r;
+  }
+  return world - 1;
+}
+
+}  // extern "C"

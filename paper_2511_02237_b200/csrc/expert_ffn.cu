@@ -1,0 +1,535 @@
+// expert_ffn.cu — K4/K5: the grouped SwiGLU expert FFN over the batch's
+// active experts, fused with the weighted combine.
+//
+// Reference semantics: expert_forward (moe_layer.hpp:92-107)
+//   h = silu(x Wg) * (x Wu);  y = h Wd
+// and the Eq.-1 mixture of moe_forward (moe_layer.hpp:148-155)
+//   out[t] = sum_j w[t][j] * y_{S_t[j]}(x_t)   (set order)
+// The reference re-reads an expert's weights for every (token, expert) pair;
+// here every active expert's weights are streamed from HBM exactly once per
+// token group (<= 64 tokens), which is the point of OEA.
+//
+// k_ffn_bf16 (persistent, one CTA per SM, 8 consumer warps + 1 producer warp)
+//   work unit  = one 16-row A block of one expert and one token group:
+//                W1 unit: 8 gate + 8 up rows (h = 8rb..8rb+7) x K=Dp
+//                W2 unit: 16 down rows (d = 16rb..16rb+15) x K=Hp
+//   global order: all W1 units (expert-major) then all W2 units; each CTA
+//   owns a contiguous, byte-balanced range and processes it in rounds of up to
+//   8 units, one per consumer warp, so no cross-warp reduction is needed.
+//   producer  : one lane issues cp.async.bulk (TMA bulk copies, L2
+//               evict_first) of 4 KiB slots into a 6-stage x 32 KiB smem ring
+//               with mbarrier complete_tx; it runs ahead across unit and
+//               W1/W2 boundaries (W2 weights do not depend on h).
+//   consumers : per k-tile one LDS.128 A fragment + per 8-token n-block two
+//               32-bit B fragment loads + one mma.sync.m16n8k16 (bf16 in,
+//               fp32 accumulate). Tokens are the mma N dimension (swap-AB),
+//               so a 1-3 token expert pads to 8, not 16.
+//   W1 epilogue: h = silu(g) * u -> bf16 hbuf, then a release counter per
+//               token group. W2 units acquire-wait on that counter (units of
+//               the same group were issued earlier in global order, so the
+//               wait cannot deadlock), write y per (token, slot) to ybuf, and
+//               the last W2 unit of each 16-column block (arrival counter)
+//               performs the deterministic slot-ordered combine for it.
+// k_ffn_simt<T> (f32 / f64 layers, drop-in moe_forward<float/double>)
+//   plain FMA kernels over the same compaction (rows/groups) metadata.
+#include <climits>
+
+#include "oea_device.cuh"
+#include "oea_internal.cuh"
+
+namespace oea_dev {
+
+struct FfnParams {
+  const uint4* w1;
+  const uint4* w2;
+  const __nv_bfloat16* xpad;  // [B][Dp]
+  int D, Dp, Hp, B, stride;
+  const int32_t* row_tok;
+  const int32_t* row_slot;
+  const int32_t* group_a;
+  const int32_t* group_row0;
+  const int32_t* group_rows;
+  const FfnHeader* hdr;
+  int* w1_done;  // [max_groups]
+  int* cnt2;     // [Dp/16]
+  __nv_bfloat16* hbuf;  // [rows][Hp]
+  float* ybuf;          // [B][stride][Dp]
+  const int32_t* set_len;
+  const float* wts;     // [B][stride]
+  float* out;           // [B][D]
+};
+
+struct Unit {
+  int g;       // token group
+  int rb;      // row block
+  int row0;    // first padded row of the group
+  int rows;    // real rows (tokens) in the group
+};
+
+template <int NB, bool W1>
+__device__ __forceinline__ void consume_unit(const FfnParams& P, const uint8_t* ring,
+                                             uint64_t* full, uint64_t* empty, int& stage,
+                                             uint32_t& phase, int nst, const Unit& U, int G) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int RB1 = P.Hp >> 3;
+
+  // B-operand row pointers (u32 view) for this lane's token in each n-block.
+  const uint32_t* bp[NB];
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb) {
+    const int r = nb * 8 + g;
+    bp[nb] = nullptr;
+    if (r < U.rows) {
+      if (W1) {
+        const int t = P.row_tok[U.row0 + r];
+        bp[nb] = reinterpret_cast<const uint32_t*>(P.xpad + static_cast<size_t>(t) * P.Dp);
+      } else {
+        bp[nb] = reinterpret_cast<const uint32_t*>(P.hbuf + static_cast<size_t>(U.row0 + r) * P.Hp);
+      }
+    }
+  }
+  if (!W1) {
+    // h of this token group must be complete (all RB1 W1 units released).
+    while (ld_acquire_gpu(&P.w1_done[U.g]) < RB1) __nanosleep(64);
+  }
+
+  float acc[NB][4];
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb) acc[nb][0] = acc[nb][1] = acc[nb][2] = acc[nb][3] = 0.0f;
+
+  for (int s = 0; s < nst; ++s) {
+    mbar_wait(&full[stage], phase);
+    const uint4* tiles =
+        reinterpret_cast<const uint4*>(ring + stage * kStageBytes + warp * kSlotBytes);
+#pragma unroll
+    for (int j = 0; j < kKtPerSlot; ++j) {
+      const uint4 a = tiles[j * 32 + lane];
+      const int kt = s * kKtPerSlot + j;
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) {
+        uint32_t b0 = 0, b1 = 0;
+        if (bp[nb] != nullptr) {
+          if (W1) {
+            b0 = __ldg(bp[nb] + kt * 8 + q);
+            b1 = __ldg(bp[nb] + kt * 8 + 4 + q);
+          } else {
+            b0 = __ldcg(bp[nb] + kt * 8 + q);
+            b1 = __ldcg(bp[nb] + kt * 8 + 4 + q);
+          }
+        }
+        mma_bf16_16816(acc[nb], a, b0, b1);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == kStages) {
+      stage = 0;
+      phase ^= 1u;
+    }
+  }
+
+  if (W1) {
+    // Thread (g, q) holds gate[h][tok 2q, 2q+1] (c0, c1) and up[h][...] (c2, c3)
+    // for h = 8 rb + g.
+    const int h = U.rb * 8 + g;
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int r = nb * 8 + 2 * q + i;
+        if (r < U.rows) {
+          const float hv = silu_f(acc[nb][i]) * acc[nb][2 + i];
+          P.hbuf[static_cast<size_t>(U.row0 + r) * P.Hp + h] = __float2bfloat16_rn(hv);
+        }
+      }
+    }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) atomicAdd(&P.w1_done[U.g], 1);
+  } else {
+    const int d0 = U.rb * 16;
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int r = nb * 8 + 2 * q + i;
+        if (r < U.rows) {
+          const int row = U.row0 + r;
+          const int t = P.row_tok[row], sl = P.row_slot[row];
+          float* y = P.ybuf + (static_cast<size_t>(t) * P.stride + sl) * P.Dp + d0;
+          y[g] = acc[nb][i];
+          y[g + 8] = acc[nb][2 + i];
+        }
+      }
+    }
+    __threadfence();
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) last = atomicAdd(&P.cnt2[U.rb], 1) == G - 1;
+    last = __shfl_sync(kFull, last, 0);
+    if (last) {
+      // Deterministic combine of this 16-column block, in set order
+      // (moe_layer.hpp:148-155): out[t][d] = sum_s w[t][s] * y[t][s][d].
+      __threadfence();
+      for (int idx = lane; idx < P.B * 16; idx += 32) {
+        const int t = idx >> 4, d = d0 + (idx & 15);
+        if (d >= P.D) continue;
+        const int len = P.set_len[t];
+        float sum = 0.0f;
+        for (int sl = 0; sl < len; ++sl)
+          sum = fmaf(P.wts[t * P.stride + sl],
+                     __ldcg(P.ybuf + (static_cast<size_t>(t) * P.stride + sl) * P.Dp + d), sum);
+        P.out[static_cast<size_t>(t) * P.D + d] = sum;
+      }
+    }
+  }
+}
+
+// Idle warp in a short round: keeps the stage barrier protocol in step.
+__device__ __forceinline__ void skip_unit(uint64_t* full, uint64_t* empty, int& stage,
+                                          uint32_t& phase, int nst) {
+  const int lane = threadIdx.x & 31;
+  for (int s = 0; s < nst; ++s) {
+    mbar_wait(&full[stage], phase);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == kStages) {
+      stage = 0;
+      phase ^= 1u;
+    }
+  }
+}
+
+template <bool W1>
+__device__ __forceinline__ void dispatch_unit(int nbk, const FfnParams& P, const uint8_t* ring,
+                                              uint64_t* full, uint64_t* empty, int& stage,
+                                              uint32_t& phase, int nst, const Unit& U, int G) {
+  switch (nbk) {
+    case 1: consume_unit<1, W1>(P, ring, full, empty, stage, phase, nst, U, G); break;
+    case 2: consume_unit<2, W1>(P, ring, full, empty, stage, phase, nst, U, G); break;
+    case 3: consume_unit<3, W1>(P, ring, full, empty, stage, phase, nst, U, G); break;
+    case 4: consume_unit<4, W1>(P, ring, full, empty, stage, phase, nst, U, G); break;
+    case 5:
+    case 6: consume_unit<6, W1>(P, ring, full, empty, stage, phase, nst, U, G); break;
+    default: consume_unit<8, W1>(P, ring, full, empty, stage, phase, nst, U, G); break;
+  }
+}
+
+__global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnParams P) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* ring = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kFfnWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // Everything below reads the router kernel's outputs.
+  pdl_wait();
+
+  const int G = P.hdr->n_groups;
+  if (G == 0) return;
+  const int KT1 = P.Dp >> 4, KT2 = P.Hp >> 4;
+  const int RB1 = P.Hp >> 3, RB2 = P.Dp >> 4;
+  const int64_t U1 = static_cast<int64_t>(G) * RB1, U2 = static_cast<int64_t>(G) * RB2;
+  // Two phases, each balanced over all CTAs: every CTA first streams its
+  // share of the W1 (gate/up) units, then its share of the W2 (down) units.
+  // W2 units acquire-wait on their token group's W1 counter, and their weights
+  // are prefetched by the producer while the wait is pending.
+  const int64_t c = blockIdx.x, nC = gridDim.x;
+  const int64_t r1b = c * U1 / nC, r1e = (c + 1) * U1 / nC;
+  const int64_t r2b = U1 + c * U2 / nC, r2e = U1 + (c + 1) * U2 / nC;
+
+  int stage = 0;
+  uint32_t phase = 0;
+
+  if (warp == kFfnWarps) {
+    // ---------------- producer: TMA bulk weight stream ----------------
+    if (lane == 0) {
+      const uint64_t pol = l2_policy_evict_first();
+      for (int64_t u = r1b; u < r2e;) {
+        if (u == r1e) u = r2b;
+        if (u >= r2e) break;
+        const bool is1 = u < U1;
+        const int64_t rend = is1 ? r1e : r2e;
+        const int n = static_cast<int>(rend - u < kFfnWarps ? rend - u : kFfnWarps);
+        const int nst = (is1 ? KT1 : KT2) / kKtPerSlot;
+        const uint4* src[kFfnWarps];
+        for (int w = 0; w < n; ++w) {
+          const int64_t uu = u + w;
+          if (is1) {
+            const int g = static_cast<int>(uu / RB1), rb = static_cast<int>(uu % RB1);
+            const int e = P.group_a[g];
+            src[w] = P.w1 + (static_cast<size_t>(e) * RB1 + rb) * KT1 * 32;
+          } else {
+            const int64_t v = uu - U1;
+            const int g = static_cast<int>(v / RB2), rb = static_cast<int>(v % RB2);
+            const int e = P.group_a[g];
+            src[w] = P.w2 + (static_cast<size_t>(e) * RB2 + rb) * KT2 * 32;
+          }
+        }
+        for (int s = 0; s < nst; ++s) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          mbar_arrive_expect_tx(&full[stage], n * kSlotBytes);
+          uint8_t* dst = ring + stage * kStageBytes;
+          for (int w = 0; w < n; ++w)
+            bulk_g2s(dst + w * kSlotBytes, src[w] + s * kKtPerSlot * 32, kSlotBytes, &full[stage],
+                     pol);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        u += n;
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  for (int64_t u = r1b; u < r2e;) {
+    if (u == r1e) u = r2b;
+    if (u >= r2e) break;
+    const bool is1 = u < U1;
+    const int64_t rend = is1 ? r1e : r2e;
+    const int n = static_cast<int>(rend - u < kFfnWarps ? rend - u : kFfnWarps);
+    const int nst = (is1 ? KT1 : KT2) / kKtPerSlot;
+    if (warp < n) {
+      const int64_t uu = u + warp;
+      Unit U;
+      if (is1) {
+        U.g = static_cast<int>(uu / RB1);
+        U.rb = static_cast<int>(uu % RB1);
+      } else {
+        const int64_t v = uu - U1;
+        U.g = static_cast<int>(v / RB2);
+        U.rb = static_cast<int>(v % RB2);
+      }
+      U.row0 = P.group_row0[U.g];
+      U.rows = P.group_rows[U.g];
+      const int nbk = (U.rows + 7) >> 3;
+      if (is1)
+        dispatch_unit<true>(nbk, P, ring, full, empty, stage, phase, nst, U, G);
+      else
+        dispatch_unit<false>(nbk, P, ring, full, empty, stage, phase, nst, U, G);
+    } else {
+      skip_unit(full, empty, stage, phase, nst);
+    }
+    u += n;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// SIMT FFN for f32 / f64 layers (reference layout weights).
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T silu_t(T z) {
+  return z / (T(1) + exp(-z));
+}
+
+// h[row][h] = silu(x Wg) * (x Wu) for the group's rows; thread per h column,
+// 8 rows per pass, sequential sum over d (the reference's dot order).
+template <typename T>
+__global__ void __launch_bounds__(128)
+    k_simt_gateup(const T* __restrict__ x, int D, int H, const T* __restrict__ wg,
+                  const T* __restrict__ wu, const int32_t* __restrict__ row_tok,
+                  const int32_t* __restrict__ group_a, const int32_t* __restrict__ group_row0,
+                  const int32_t* __restrict__ group_rows, const FfnHeader* __restrict__ hdr,
+                  T* __restrict__ hbuf) {
+  const int g = blockIdx.y;
+  if (g >= hdr->n_groups) return;
+  const int h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h >= H) return;
+  const int e = group_a[g], row0 = group_row0[g], rows = group_rows[g];
+  const T* Wg = wg + static_cast<size_t>(e) * D * H;
+  const T* Wu = wu + static_cast<size_t>(e) * D * H;
+  for (int r0 = 0; r0 < rows; r0 += 8) {
+    T ag[8], au[8];
+    const T* xr[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      ag[r] = au[r] = T(0);
+      xr[r] = r0 + r < rows ? x + static_cast<size_t>(row_tok[row0 + r0 + r]) * D : nullptr;
+    }
+    for (int d = 0; d < D; ++d) {
+      const T vg = Wg[static_cast<size_t>(d) * H + h];
+      const T vu = Wu[static_cast<size_t>(d) * H + h];
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (xr[r]) {
+          const T xv = xr[r][d];
+          ag[r] += xv * vg;
+          au[r] += xv * vu;
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+      if (xr[r]) hbuf[static_cast<size_t>(row0 + r0 + r) * H + h] = silu_t(ag[r]) * au[r];
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128)
+    k_simt_down(int D, int H, const T* __restrict__ wd, const int32_t* __restrict__ row_tok,
+                const int32_t* __restrict__ row_slot, const int32_t* __restrict__ group_a,
+                const int32_t* __restrict__ group_row0, const int32_t* __restrict__ group_rows,
+                const FfnHeader* __restrict__ hdr, const T* __restrict__ hbuf, int stride,
+                T* __restrict__ ybuf) {
+  const int g = blockIdx.y;
+  if (g >= hdr->n_groups) return;
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= D) return;
+  const int e = group_a[g], row0 = group_row0[g], rows = group_rows[g];
+  const T* Wd = wd + static_cast<size_t>(e) * H * D;
+  for (int r0 = 0; r0 < rows; r0 += 8) {
+    T acc[8];
+    const T* hr[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      acc[r] = T(0);
+      hr[r] = r0 + r < rows ? hbuf + static_cast<size_t>(row0 + r0 + r) * H : nullptr;
+    }
+    for (int h = 0; h < H; ++h) {
+      const T w = Wd[static_cast<size_t>(h) * D + d];
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (hr[r]) acc[r] += hr[r][h] * w;
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+      if (hr[r]) {
+        const int row = row0 + r0 + r;
+        ybuf[(static_cast<size_t>(row_tok[row]) * stride + row_slot[row]) * D + d] = acc[r];
+      }
+  }
+}
+
+// out[t][d] = sum_j w[t][j] * double(y[t][j][d]) in set order, fp64
+// (moe_layer.hpp:153: out.row(i) += w[j] * expert_forward(...)).
+template <typename T>
+__global__ void k_simt_combine(int B, int D, int stride, const int32_t* __restrict__ set_len,
+                               const double* __restrict__ w, const T* __restrict__ ybuf,
+                               double* __restrict__ out) {
+  const size_t total = static_cast<size_t>(B) * D;
+  for (size_t f = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; f < total;
+       f += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int t = static_cast<int>(f / D), d = static_cast<int>(f % D);
+    double acc = 0.0;
+    for (int j = 0; j < set_len[t]; ++j)
+      acc = __dadd_rn(acc, __dmul_rn(w[static_cast<size_t>(t) * stride + j],
+                                     static_cast<double>(ybuf[(static_cast<size_t>(t) * stride + j) * D + d])));
+    out[f] = acc;
+  }
+}
+
+template <typename S, typename T>
+__global__ void k_cast(const S* __restrict__ src, size_t n, T* __restrict__ dst) {
+  for (size_t f = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; f < n;
+       f += static_cast<size_t>(gridDim.x) * blockDim.x)
+    dst[f] = static_cast<T>(src[f]);
+}
+
+}  // namespace oea_dev
+
+namespace oea_host {
+
+using namespace oea_dev;
+
+size_t ffn_bf16_smem_bytes() { return kStages * kStageBytes + 2 * kStages * sizeof(uint64_t); }
+
+int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const FfnBuffers& fb,
+                    bool pdl, cudaStream_t s) {
+  FfnParams P;
+  P.w1 = static_cast<const uint4*>(L->w1);
+  P.w2 = static_cast<const uint4*>(L->w2);
+  P.xpad = static_cast<const __nv_bfloat16*>(fb.x);
+  P.D = L->D;
+  P.Dp = L->Dp;
+  P.Hp = L->Hp;
+  P.B = B;
+  P.stride = stride;
+  P.row_tok = fb.row_tok;
+  P.row_slot = fb.row_slot;
+  P.group_a = fb.group_a;
+  P.group_row0 = fb.group_row0;
+  P.group_rows = fb.group_rows;
+  P.hdr = fb.hdr;
+  P.w1_done = fb.counters;
+  P.cnt2 = fb.counters + fb.max_groups;
+  P.hbuf = static_cast<__nv_bfloat16*>(fb.hbuf);
+  P.ybuf = static_cast<float*>(fb.ybuf);
+  P.set_len = fb.set_len;
+  P.wts = fb.weights_f32;
+  P.out = static_cast<float*>(fb.out);
+
+  static bool attr_set = false;
+  const size_t smem = ffn_bf16_smem_bytes();
+  if (!attr_set) {
+    OEA_CUDA_TRY(ctx, cudaFuncSetAttribute(k_ffn_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem)));
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctx->num_sms);
+  cfg.blockDim = dim3((kFfnWarps + 1) * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  OEA_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, k_ffn_bf16, P));
+  OEA_LAUNCHED(ctx);
+  return OEA_OK;
+}
+
+template <typename T>
+static int simt_impl(oea_ctx* ctx, const oea_layer* L, int B, int stride, const FfnBuffers& fb,
+                     int max_groups, cudaStream_t s) {
+  const int D = L->D, H = L->H;
+  dim3 g1((H + 127) / 128, max_groups), g2((D + 127) / 128, max_groups);
+  k_simt_gateup<T><<<g1, 128, 0, s>>>(static_cast<const T*>(fb.x), D, H,
+                                      static_cast<const T*>(L->w1), static_cast<const T*>(L->w_up),
+                                      fb.row_tok, fb.group_a, fb.group_row0, fb.group_rows, fb.hdr,
+                                      static_cast<T*>(fb.hbuf));
+  OEA_LAUNCHED(ctx);
+  k_simt_down<T><<<g2, 128, 0, s>>>(D, H, static_cast<const T*>(L->w2), fb.row_tok, fb.row_slot,
+                                    fb.group_a, fb.group_row0, fb.group_rows, fb.hdr,
+                                    static_cast<const T*>(fb.hbuf), stride,
+                                    static_cast<T*>(fb.ybuf));
+  OEA_LAUNCHED(ctx);
+  const size_t total = static_cast<size_t>(B) * D;
+  const int blocks = static_cast<int>((total + 255) / 256 > 4096 ? 4096 : (total + 255) / 256);
+  k_simt_combine<T><<<blocks, 256, 0, s>>>(B, D, stride, fb.set_len, fb.weights_f64,
+                                           static_cast<const T*>(fb.ybuf),
+                                           static_cast<double*>(fb.out));
+  OEA_LAUNCHED(ctx);
+  return OEA_OK;
+}
+
+int ffn_simt_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const FfnBuffers& fb,
+                    int max_groups, cudaStream_t s) {
+  if (L->dtype == OEA_DTYPE_F64) return simt_impl<double>(ctx, L, B, stride, fb, max_groups, s);
+  return simt_impl<float>(ctx, L, B, stride, fb, max_groups, s);
+}
+
+int cast_f64_launch(oea_ctx* ctx, const double* src, size_t n, int dst_dtype, void* dst,
+                    cudaStream_t s) {
+  const int blocks = static_cast<int>((n + 255) / 256 > 4096 ? 4096 : (n + 255) / 256 + 0);
+  if (dst_dtype == OEA_DTYPE_F64)
+    k_cast<double, double><<<blocks > 0 ? blocks : 1, 256, 0, s>>>(src, n, static_cast<double*>(dst));
+  else
+    k_cast<double, float><<<blocks > 0 ? blocks : 1, 256, 0, s>>>(src, n, static_cast<float*>(dst));
+  OEA_LAUNCHED(ctx);
+  return OEA_OK;
+}
+
+}  // namespace oea_host

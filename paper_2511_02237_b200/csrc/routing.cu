@@ -1,0 +1,286 @@
+// routing.cu — K1 `route_f64`: batch-aware OEA routing on fp64 router
+// probabilities, bit-exact with the reference's route() (routing.cpp:305-326).
+//
+// Three launches on one stream (the batch union is a global barrier):
+//   A  k_rank_phase1   warp per token: bitonic rank sort of the row
+//                      (sort_experts, routing.cpp:184-203), Phase-1 baseline
+//                      size t/n (phase1_baseline :226-268) and the base union
+//                      as an atomicOr bitmap.
+//   B  k_build_sets    warp per token: top-k / baseline / Phase-2 piggyback
+//                      scan with both cap semantics (phase2_piggyback
+//                      :270-303) as a ballot scan, sequential fp64
+//                      renormalisation (renormalize_weights :33-49), per-expert
+//                      loads by integer atomics (fill_aggregates :17-31).
+//   C  k_aggregate     one CTA: active_union (ascending, load > 0), T, and the
+//                      exported base union.
+// Bit-exactness: ranking uses an order-preserving integer image of each double
+// (-0.0 canonicalised), so comparisons equal the reference's `!=`/`>`; the
+// cumulative mass and the renormalisation are sequential __dadd_rn/__ddiv_rn in
+// the reference's order (no FMA contraction is possible: adds and divides only).
+#include <climits>
+
+#include "oea_device.cuh"
+#include "oea_internal.cuh"
+
+namespace oea_dev {
+
+constexpr int kRouteWarps = 8;
+
+template <int E>
+__global__ void __launch_bounds__(kRouteWarps * 32)
+    k_rank_phase1(const Cfg cfg, const int B, const int N, const double* __restrict__ scores,
+                  const uint8_t* __restrict__ mask, int32_t* __restrict__ order,
+                  int32_t* __restrict__ t_out, int32_t* __restrict__ n_out,
+                  uint32_t* __restrict__ union_bits, const int order_given,
+                  const int run_phase1) {
+  __shared__ int32_t s_ord[kRouteWarps][32 * E];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kRouteWarps + warp;
+  if (i >= B) return;
+  const double* row = scores + static_cast<size_t>(i) * N;
+  int32_t* ord_row = order + static_cast<size_t>(i) * N;
+  int32_t* so = s_ord[warp];
+
+  if (!order_given) {
+    uint64_t k[E];
+    uint32_t id[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const int p = j * 32 + lane;
+      k[j] = p < N ? order_key_f64(__ldg(row + p)) : 0ull;
+      id[j] = static_cast<uint32_t>(p);
+    }
+    warp_rank_sort<E>(k, id);
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const int p = j * 32 + lane;
+      so[p] = static_cast<int32_t>(id[j]);
+      if (p < N) ord_row[p] = static_cast<int32_t>(id[j]);
+    }
+  } else {
+    for (int p = lane; p < N; p += 32) so[p] = ord_row[p];
+  }
+  __syncwarp();
+  if (!run_phase1) return;
+
+  const bool real = mask == nullptr || mask[i] != 0;
+  int t_i = 0, n_i = 0;
+  if (real) {
+    if (cfg.p == 1.0) {
+      t_i = N;  // exact-compare short-circuit, routing.cpp:243-245
+    } else {
+      if (lane == 0) {
+        t_i = N;
+        double cum = 0.0;
+        for (int j = 0; j < N; ++j) {  // routing.cpp:247-255, sequential
+          cum = __dadd_rn(cum, row[so[j]]);
+          if (cum >= cfg.p) {
+            t_i = j + 1;
+            break;
+          }
+        }
+      }
+      t_i = __shfl_sync(kFull, t_i, 0);
+    }
+    n_i = min(cfg.k0, t_i);
+    for (int j = lane; j < n_i; j += 32) {
+      const int e = so[j];
+      atomicOr(&union_bits[e >> 5], 1u << (e & 31));
+    }
+  }
+  if (lane == 0) {
+    if (t_out) t_out[i] = t_i;
+    n_out[i] = n_i;
+  }
+}
+
+// set_mode: 0 = first k ranks (route_topk), 1 = baseline only (pruned),
+//           2 = baseline + piggyback scan (oea / simplified / phase2).
+__global__ void __launch_bounds__(kRouteWarps * 32)
+    k_build_sets(const Cfg cfg, const int B, const int N, const int set_mode,
+                 const int do_weights, const double* __restrict__ scores,
+                 const uint8_t* __restrict__ mask, const int32_t* __restrict__ order,
+                 const int32_t* __restrict__ n_in, const uint32_t* __restrict__ union_bits,
+                 int32_t* __restrict__ sets, int32_t* __restrict__ set_len,
+                 double* __restrict__ weights, float* __restrict__ weights_f32,
+                 int32_t* __restrict__ loads, unsigned long long* __restrict__ total_load,
+                 int32_t* __restrict__ err_token) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kRouteWarps + warp;
+  if (i >= B) return;
+  const int stride = cfg.stride;
+  const int32_t* ord = order + static_cast<size_t>(i) * N;
+  int32_t* srow = sets + static_cast<size_t>(i) * stride;
+  const bool real = mask == nullptr || mask[i] != 0;
+
+  int len = 0;
+  if (real) {
+    if (set_mode == 0) {
+      len = cfg.k;
+      for (int j = lane; j < len; j += 32) srow[j] = ord[j];
+    } else {
+      const int n_i = n_in[i];
+      for (int j = lane; j < n_i; j += 32) srow[j] = ord[j];
+      len = n_i;
+      if (set_mode == 2) {
+        // Phase 2 (routing.cpp:291-299): candidates are ranks n_i..max_p-1 in
+        // order; the cap is checked before each candidate, so members are
+        // appended until |S| reaches `limit` (k_max, or k_max+1 for the
+        // pseudocode cap); non-members are skipped without stopping.
+        for (int base = n_i; base < cfg.max_p && len < cfg.limit; base += 32) {
+          const int j = base + lane;
+          const int e = j < cfg.max_p ? ord[j] : -1;
+          const bool member = e >= 0 && ((union_bits[e >> 5] >> (e & 31)) & 1u);
+          const unsigned m = __ballot_sync(kFull, member);
+          const int pos = __popc(m & lanemask_lt());
+          const int take = cfg.limit - len;
+          if (member && pos < take) srow[len + pos] = e;
+          len += min(__popc(m), take);
+        }
+      }
+    }
+  }
+  for (int j = len + lane; j < stride; j += 32) {
+    srow[j] = -1;
+    if (weights) weights[static_cast<size_t>(i) * stride + j] = 0.0;
+    if (weights_f32) weights_f32[static_cast<size_t>(i) * stride + j] = 0.0f;
+  }
+  __syncwarp();
+  for (int j = lane; j < len; j += 32) atomicAdd(&loads[srow[j]], 1);
+  if (lane == 0) {
+    set_len[i] = len;
+    atomicAdd(total_load, static_cast<unsigned long long>(len));
+  }
+  if (!do_weights || len == 0) return;
+
+  // renormalize_weights (routing.cpp:33-49): sequential mass in set order.
+  const double* row = scores + static_cast<size_t>(i) * N;
+  double mass = 0.0;
+  if (lane == 0) {
+    for (int j = 0; j < len; ++j) mass = __dadd_rn(mass, row[srow[j]]);
+    if (!(mass > 1e-12)) atomicMin(err_token, i);
+  }
+  mass = __shfl_sync(kFull, mass, 0);
+  for (int j = lane; j < len; j += 32) {
+    const double w = __ddiv_rn(row[srow[j]], mass);
+    if (weights) weights[static_cast<size_t>(i) * stride + j] = w;
+    if (weights_f32) weights_f32[static_cast<size_t>(i) * stride + j] = static_cast<float>(w);
+  }
+}
+
+// Ascending compaction of {e : pred(e)} with a block-wide ballot scan.
+template <typename Pred>
+__device__ void block_compact(int N, Pred pred, int32_t* out, int32_t* count) {
+  __shared__ int s_warp[32];
+  __shared__ int s_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  for (int base = 0; base < N; base += blockDim.x) {
+    const int e = base + threadIdx.x;
+    const bool f = e < N && pred(e);
+    const unsigned m = __ballot_sync(kFull, f);
+    if (lane == 0) s_warp[warp] = __popc(m);
+    __syncthreads();
+    int off = s_base;
+    for (int w = 0; w < warp; ++w) off += s_warp[w];
+    if (f && out) out[off + __popc(m & lanemask_lt())] = e;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int w = 0; w < nwarps; ++w) tot += s_warp[w];
+      s_base += tot;
+    }
+    __syncthreads();
+  }
+  const int total = s_base;
+  if (out)
+    for (int e = total + threadIdx.x; e < N; e += blockDim.x) out[e] = -1;
+  if (threadIdx.x == 0 && count) *count = total;
+}
+
+__global__ void __launch_bounds__(1024)
+    k_aggregate(const int N, const int32_t* __restrict__ loads, int32_t* __restrict__ active_union,
+                int32_t* __restrict__ active_count, const uint32_t* __restrict__ union_bits,
+                int32_t* __restrict__ base_union, int32_t* __restrict__ base_count) {
+  block_compact(N, [&](int e) { return loads[e] > 0; }, active_union, active_count);
+  if (base_union || base_count)
+    block_compact(N, [&](int e) { return (union_bits[e >> 5] >> (e & 31)) & 1u; },
+                  base_union, base_count);
+}
+
+__global__ void k_union_from_list(const int32_t* __restrict__ list, const int count, const int N,
+                                  uint32_t* __restrict__ bits) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < count; j += gridDim.x * blockDim.x) {
+    const int e = list[j];
+    if (e >= 0 && e < N) atomicOr(&bits[e >> 5], 1u << (e & 31));
+  }
+}
+
+}  // namespace oea_dev
+
+namespace oea_host {
+
+using namespace oea_dev;
+
+template <int E>
+static void launch_rank(const Cfg& cfg, int B, int N, const RouteBuffers& rb, int order_given,
+                        int run_phase1, cudaStream_t s) {
+  const int grid = (B + kRouteWarps - 1) / kRouteWarps;
+  k_rank_phase1<E><<<grid, kRouteWarps * 32, 0, s>>>(cfg, B, N, rb.scores, rb.mask, rb.order,
+                                                     rb.t, rb.n, rb.union_bits, order_given,
+                                                     run_phase1);
+}
+
+int route_f64_launch(oea_ctx* ctx, const Cfg& cfg, int B, int N, const RouteBuffers& rb,
+                     bool order_given, bool run_phase1, int set_mode, bool n_given,
+                     cudaStream_t s) {
+  const int words = (N + 31) / 32;
+  if (!n_given) OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.union_bits, 0, words * 4, s));
+  OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.loads, 0, sizeof(int32_t) * N, s));
+  OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.total_load, 0, sizeof(int64_t), s));
+  OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.err_token, 0x7f, sizeof(int32_t), s));
+
+  if (!n_given) {
+    const int Np = round_up(N, 32);
+    const int need_phase1 = run_phase1 ? 1 : 0;
+    if (Np <= 32)
+      launch_rank<1>(cfg, B, N, rb, order_given, need_phase1, s);
+    else if (Np <= 64)
+      launch_rank<2>(cfg, B, N, rb, order_given, need_phase1, s);
+    else if (Np <= 128)
+      launch_rank<4>(cfg, B, N, rb, order_given, need_phase1, s);
+    else if (Np <= 256)
+      launch_rank<8>(cfg, B, N, rb, order_given, need_phase1, s);
+    else if (Np <= 512)
+      launch_rank<16>(cfg, B, N, rb, order_given, need_phase1, s);
+    else
+      launch_rank<32>(cfg, B, N, rb, order_given, need_phase1, s);
+    OEA_LAUNCHED(ctx);
+  }
+  // Set construction: 0 vanilla (route_topk), 1 pruned (baseline), 2 piggyback.
+  const int do_weights = (rb.weights != nullptr || rb.weights_f32 != nullptr) ? 1 : 0;
+  const int grid = (B + kRouteWarps - 1) / kRouteWarps;
+  k_build_sets<<<grid, kRouteWarps * 32, 0, s>>>(
+      cfg, B, N, set_mode, do_weights, rb.scores, rb.mask, rb.order, rb.n, rb.union_bits,
+      rb.sets, rb.set_len, rb.weights, rb.weights_f32, rb.loads,
+      reinterpret_cast<unsigned long long*>(rb.total_load), rb.err_token);
+  OEA_LAUNCHED(ctx);
+  k_aggregate<<<1, 1024, 0, s>>>(N, rb.loads, rb.active_union, rb.active_count, rb.union_bits,
+                                 rb.base_union, rb.base_union_count);
+  OEA_LAUNCHED(ctx);
+  return OEA_OK;
+}
+
+int union_from_list_launch(oea_ctx* ctx, const int32_t* list, int count, int N, uint32_t* bits,
+                           cudaStream_t s) {
+  OEA_CUDA_TRY(ctx, cudaMemsetAsync(bits, 0, ((N + 31) / 32) * 4, s));
+  if (count > 0) {
+    k_union_from_list<<<1, 256, 0, s>>>(list, count, N, bits);
+    OEA_LAUNCHED(ctx);
+  }
+  return OEA_OK;
+}
+
+}  // namespace oea_host

@@ -1,0 +1,132 @@
+"""The fused bf16 decode layer (K2 router + K3 compaction + K4/K5 FFN) vs the
+CPU oracle.
+
+Parity bar (BASELINE.json north_star):
+  * expert sets bit-exact vs the reference routing fed the same router logits
+    (the exported fp32 logits, softmax in fp64 by the oracle);
+  * gate weights within 1e-5;
+  * layer output within 2e-2 relative (output_divergence, moe_layer.cpp:57-74)
+    of moe_forward<double> on the same bf16-rounded weights and inputs.
+"""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+W_TOL = 1e-5
+OUT_TOL = 2e-2
+
+
+def to_bf16_bits(x):
+    xb = oracle.bf16_round(x)
+    return xb, (xb.astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+
+
+def oracle_output(layer, x, want):
+    """moe_forward<double> on the layer's stored bf16 weights, restricted to
+    the active experts (remapped), so large layers stay cheap to check."""
+    act = [int(e) for e in want.active_union]
+    if not act:
+        return np.zeros((x.shape[0], layer.D))
+    remap = {e: i for i, e in enumerate(act)}
+    ws = [layer.download_expert(e, "f64") for e in act]
+    wg = np.stack([w[0] for w in ws])
+    wu = np.stack([w[1] for w in ws])
+    wd = np.stack([w[2] for w in ws])
+    sets = np.where(want.sets >= 0, np.vectorize(lambda e: remap.get(int(e), -1))(want.sets), -1)
+    return oracle.moe_forward(wg, wu, wd, x, sets.astype(np.int32), want.set_len, want.weights)
+
+
+def run_case(oea, D, H, N, B, cfg, seed=1, mask=None, check_logits=True):
+    layer = oea.DeviceMoeLayer(D, H, N, dtype="bf16")
+    layer.init_random(seed)
+    x, xbits = to_bf16_bits(oracle.make_random_batch(B, D, 1000 + seed))
+    out = layer.decode_host(xbits, cfg, mask=mask)
+    plan = layer.last_plan(B, cfg)
+    m8 = None if mask is None else np.asarray(mask, np.uint8)
+    if check_logits:
+        R = layer.download_router("f64")
+        ref_logits = x @ R
+        err = np.abs(plan["logits"] - ref_logits).max() / max(np.abs(ref_logits).max(), 1e-30)
+        assert err < 1e-4, f"router logits rel err {err}"
+    want = oracle.route(oracle.softmax_rows(plan["logits"].astype(np.float64)), cfg, m8)
+    for i in range(B):
+        got = [int(v) for v in plan["sets"][i, : plan["set_len"][i]]]
+        assert got == want.set_list(i), f"token {i}: {got} != {want.set_list(i)}"
+    assert plan["active_count"] == want.active_count
+    assert list(plan["active_union"]) == list(want.active_union)
+    assert plan["total_load"] == want.total_load
+    assert np.array_equal(plan["loads"], want.loads)
+    assert np.abs(plan["weights"] - want.weights).max() <= W_TOL
+    ref = oracle_output(layer, x, want)
+    if want.active_count == 0:
+        assert np.all(out == 0)
+        return plan, 0.0
+    real = np.ones(B, bool) if mask is None else np.asarray(mask, bool)
+    _, max_rel = oracle.output_divergence(ref[real], out[real].astype(np.float64))
+    assert max_rel <= OUT_TOL, f"output max relative error {max_rel}"
+    if mask is not None:
+        assert np.all(out[~real] == 0)
+    return plan, max_rel
+
+
+def test_decode_qwen30b_shape_oea(oea):
+    """BASELINE C1 shape: N=128, k=8, D=2048, H=768, B=16, simplified(4, 8)."""
+    plan, err = run_case(oea, 2048, 768, 128, 16, oea.RoutingConfig.simplified(4, 8))
+    assert 20 <= plan["active_count"] <= 90
+    assert plan["total_load"] == 16 * 8
+
+
+def test_decode_qwen30b_shape_vanilla(oea):
+    run_case(oea, 2048, 768, 128, 16, oea.RoutingConfig.vanilla(8), seed=2)
+
+
+@pytest.mark.parametrize("mode", ["vanilla", "pruned", "oea", "simplified", "strict"])
+def test_decode_modes_small(oea, mode):
+    R = oea.RoutingConfig
+    cfg = {"vanilla": R.vanilla(4), "pruned": R.pruned(2, 1.0, 4),
+           "oea": R.oea(2, 1.0, 4, 10, 4), "simplified": R.simplified(2, 4),
+           "strict": R.simplified(2, 4, oea.CapSemantics.PseudocodeStrict)}[mode]
+    run_case(oea, 256, 128, 16, 8, cfg, seed=3)
+
+
+def test_decode_odd_dims_and_mask(oea):
+    mask = np.array([1, 0, 1, 1, 0, 1, 1], bool)
+    run_case(oea, 100, 72, 10, 7, oea.RoutingConfig.simplified(2, 3), seed=4, mask=mask)
+
+
+def test_decode_all_masked_is_zero(oea):
+    mask = np.zeros(5, bool)
+    run_case(oea, 128, 128, 8, 5, oea.RoutingConfig.simplified(2, 4), seed=5, mask=mask)
+
+
+def test_decode_large_token_groups(oea):
+    """More than 64 tokens on one expert -> several token groups per expert."""
+    run_case(oea, 256, 256, 4, 150, oea.RoutingConfig.vanilla(4), seed=6)
+
+
+@pytest.mark.parametrize("B", [1, 4, 32, 64, 128, 256])
+def test_decode_batch_sweep(oea, B):
+    """BASELINE C2 batch sizes (smaller D/H keeps the CPU check fast)."""
+    run_case(oea, 512, 256, 128, B, oea.RoutingConfig.simplified(3, 8), seed=7 + B)
+
+
+def test_decode_deterministic_and_graph(oea):
+    import torch
+    D, H, N, B = 1024, 512, 64, 16
+    layer = oea.DeviceMoeLayer(D, H, N, dtype="bf16")
+    layer.init_random(8)
+    x = torch.randn(B, D, device="cuda").to(torch.bfloat16)
+    out1 = torch.empty(B, D, device="cuda", dtype=torch.float32)
+    out2 = torch.empty_like(out1)
+    cfg = oea.RoutingConfig.simplified(4, 8)
+    torch.cuda.synchronize()
+    layer.decode(x, cfg, out1)
+    layer.ctx.synchronize()
+    g = layer.graph(x, cfg, out2)
+    for _ in range(3):
+        g.launch()
+    layer.ctx.synchronize()
+    assert torch.equal(out1, out2)
