@@ -222,6 +222,11 @@ int oea_moe_forward_plan_host(oea_ctx_t ctx, oea_layer_t layer, const double* x,
 int oea_router_scores_host(oea_ctx_t ctx, oea_layer_t layer, const double* x,
                            int32_t B, double* scores);
 
+/* Debug: per-CTA globaltimer stamps of the last FFN launch when the process
+ * ran with OEA_FFN_TRACE=1 ([grid][8]: start, end of W1 phase, first W2 unit
+ * ready, end, producer done). */
+int oea_debug_ffn_trace(oea_ctx_t ctx, uint64_t* host, int32_t n);
+
 /* ---- expert parallelism (Qwen3-235B stack, NCCL all-to-all) ------------ */
 /* Expert-block ownership: rank r owns experts [N*r/P, N*(r+1)/P). */
 int oea_ep_owner(int32_t N, int32_t world, int32_t expert);

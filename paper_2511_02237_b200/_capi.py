@@ -95,6 +95,7 @@ def lib():
                 "oea_moe_forward_plan_host": [vp, vp, vp, i32, vp, vp, vp, i32, vp, vp],
                 "oea_router_scores_host": [vp, vp, vp, i32, vp],
                 "oea_ep_owner": [i32, i32, i32],
+                "oea_debug_ffn_trace": [vp, vp, i32],
             }
             for name, args in sigs.items():
                 fn = getattr(L, name)
@@ -115,7 +116,7 @@ EXPORTED = (
     "oea_layer_download_router", "oea_layer_download_expert", "oea_layer_info",
     "oea_moe_decode", "oea_moe_decode_host", "oea_last_plan_host", "oea_decode_graph_create",
     "oea_graph_launch", "oea_graph_destroy", "oea_moe_forward_plan_host",
-    "oea_router_scores_host", "oea_ep_owner")
+    "oea_router_scores_host", "oea_ep_owner", "oea_debug_ffn_trace")
 
 
 def check(rc: int, ctx=None):

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -106,7 +107,7 @@ size_t carve(Workspace& w, bool assign) {
   take(w.group_row0, G * 4);
   take(w.group_rows, G * 4);
   take(w.hdr, sizeof(FfnHeader));
-  take(w.counters, (G + Dp / 16 + 1) * 4);
+  take(w.counters, (G + Dp / 16 + 4) * 4);
   take(w.xpad, B * Dp * 2);
   take(w.hbuf, R * std::max(Hp, H) * 8);
   take(w.ybuf, B * S * std::max(Dp, D) * 8);
@@ -332,7 +333,8 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   oea_host::FusedRouterBuffers rb;
   rb.x = static_cast<const __nv_bfloat16*>(x);
   rb.mask = mask;
-  rb.xpad = w.xpad;
+  const bool padded = L->D != L->Dp;
+  rb.xpad = padded ? w.xpad : nullptr;
   rb.logits = w.logits;
   rb.order = w.order;
   rb.sets = w.sets;
@@ -350,15 +352,17 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   rb.group_rows = w.group_rows;
   rb.hdr = w.hdr;
   rb.counters = w.counters;
-  rb.n_counters = w.G + L->Dp / 16;
+  rb.n_counters = w.G + L->Dp / 16 + 2;
   rb.out = static_cast<float*>(out);
   rb.phase1_n = w.n;
   rb.base_union = w.base_union;
   rb.base_union_count = w.base_union_count;
+  rb.trace = ctx->ffn_trace;
+  if (rb.trace) OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.trace, 0, 8 * 8 * 1024, s));
   int r = oea_host::router_fused_launch(ctx, L, cfg, B, rb, s);
   if (r) return r;
   oea_host::FfnBuffers fb;
-  fb.x = w.xpad;
+  fb.x = padded ? static_cast<const void*>(w.xpad) : x;
   fb.row_tok = w.row_tok;
   fb.row_slot = w.row_slot;
   fb.group_a = w.group_a;
@@ -373,6 +377,8 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   fb.weights_f32 = w.w32;
   fb.weights_f64 = w.w64;
   fb.out = out;
+  fb.trace = ctx->ffn_trace;
+  fb.mode = ctx->ffn_mode;
   return oea_host::ffn_bf16_launch(ctx, L, B, stride, fb, true, s);
 }
 
@@ -477,7 +483,20 @@ int oea_ctx_create(int32_t device, oea_ctx_t* out) {
     return oea_check_cuda(nullptr, e, "cudaStreamCreate");
   }
   ctx->ws = new CtxExtra;
+  if (const char* tr = getenv("OEA_FFN_TRACE")) {
+    if (tr[0] == '1' && cudaMalloc(&ctx->ffn_trace, 8 * 8 * 1024) != cudaSuccess) ctx->ffn_trace = nullptr;
+  }
+  if (const char* md = getenv("OEA_FFN_MODE")) ctx->ffn_mode = atoi(md);
   *out = ctx;
+  return OEA_OK;
+}
+
+int oea_debug_ffn_trace(oea_ctx_t ctx, uint64_t* host, int32_t n) {
+  CHECK_CTX(ctx);
+  if (ctx->ffn_trace == nullptr) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "OEA_FFN_TRACE not enabled");
+  OEA_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  OEA_CUDA_TRY(ctx, cudaMemcpy(host, ctx->ffn_trace, sizeof(uint64_t) * std::min(n, 8 * 1024),
+                               cudaMemcpyDeviceToHost));
   return OEA_OK;
 }
 
@@ -490,6 +509,7 @@ int oea_ctx_destroy(oea_ctx_t ctx) {
     if (x->ws.base) cudaFree(x->ws.base);
     delete x;
   }
+  if (ctx->ffn_trace) cudaFree(ctx->ffn_trace);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
   return OEA_OK;
@@ -1036,7 +1056,7 @@ int oea_moe_forward_plan_host(oea_ctx_t ctx, oea_layer_t L, const double* x, int
                                     cudaMemcpyHostToDevice, s));
   oea_host::CompactBuffers cb{w.sets, w.set_len, w.row_tok, w.row_slot, w.group_a,
                               w.group_row0, w.group_rows, w.hdr, w.counters,
-                              w.G + L->Dp / 16 + 1};
+                              w.G + L->Dp / 16 + 2};
   r = oea_host::compact_launch(ctx, B, L->N, set_stride, cb, w.tokbits, w.active_union,
                                w.active_count, s);
   if (r) return r;

@@ -51,13 +51,24 @@ struct FfnParams {
   const int32_t* group_rows;
   const FfnHeader* hdr;
   int* w1_done;  // [max_groups]
-  int* cnt2;     // [Dp/16]
+  int* cnt2;     // [Dp/16] combine arrivals, then [2] round claim counters
   __nv_bfloat16* hbuf;  // [rows][Hp]
   float* ybuf;          // [B][stride][Dp]
   const int32_t* set_len;
   const float* wts;     // [B][stride]
   float* out;           // [B][D]
+  unsigned long long* trace;  // debug: [gridDim][8] globaltimer stamps, or null
+  int mode;                   // debug: 1 = stream weights only (no math)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void stamp(const FfnParams& P, int slot) {
+  if (P.trace) P.trace[blockIdx.x * 8 + slot] = gtimer();
+}
 
 struct Unit {
   int g;       // token group
@@ -90,18 +101,27 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const uint8_t* 
     }
   }
   if (!W1) {
-    // h of this token group must be complete (all RB1 W1 units released).
-    while (ld_acquire_gpu(&P.w1_done[U.g]) < RB1) __nanosleep(64);
+    // h of this token group must be complete (all RB1 W1 units released):
+    // lane 0 acquires, the warp barrier orders the other lanes after it.
+    if (lane == 0)
+      while (ld_acquire_gpu(&P.w1_done[U.g]) < RB1) __nanosleep(64);
+    __syncwarp();
+    if (warp == 0 && lane == 0 && P.trace && P.trace[blockIdx.x * 8 + 2] == 0) stamp(P, 2);
   }
 
-  float acc[NB][4];
+  // two accumulator sets (even / odd k-tiles) halve the dependent HMMA chain
+  float acc2[2][NB][4];
 #pragma unroll
-  for (int nb = 0; nb < NB; ++nb) acc[nb][0] = acc[nb][1] = acc[nb][2] = acc[nb][3] = 0.0f;
+  for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+      acc2[h2][nb][0] = acc2[h2][nb][1] = acc2[h2][nb][2] = acc2[h2][nb][3] = 0.0f;
 
   for (int s = 0; s < nst; ++s) {
     mbar_wait(&full[stage], phase);
     const uint4* tiles =
         reinterpret_cast<const uint4*>(ring + stage * kStageBytes + warp * kSlotBytes);
+    if (P.mode != 1)
 #pragma unroll
     for (int j = 0; j < kKtPerSlot; ++j) {
       const uint4 a = tiles[j * 32 + lane];
@@ -118,7 +138,7 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const uint8_t* 
             b1 = __ldcg(bp[nb] + kt * 8 + 4 + q);
           }
         }
-        mma_bf16_16816(acc[nb], a, b0, b1);
+        mma_bf16_16816(acc2[j & 1][nb], a, b0, b1);
       }
     }
     __syncwarp();
@@ -128,6 +148,12 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const uint8_t* 
       phase ^= 1u;
     }
   }
+
+  float acc[NB][4];
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[nb][i] = acc2[0][nb][i] + acc2[1][nb][i];
 
   if (W1) {
     // Thread (g, q) holds gate[h][tok 2q, 2q+1] (c0, c1) and up[h][...] (c2, c3)
@@ -144,9 +170,12 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const uint8_t* 
         }
       }
     }
-    __threadfence();
+    // release: warp barrier (orders the lanes' stores) + one gpu-scope fence
     __syncwarp();
-    if (lane == 0) atomicAdd(&P.w1_done[U.g], 1);
+    if (lane == 0) {
+      __threadfence();
+      atomicAdd(&P.w1_done[U.g], 1);
+    }
   } else {
     const int d0 = U.rb * 16;
 #pragma unroll
@@ -163,10 +192,12 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const uint8_t* 
         }
       }
     }
-    __threadfence();
     __syncwarp();
     int last = 0;
-    if (lane == 0) last = atomicAdd(&P.cnt2[U.rb], 1) == G - 1;
+    if (lane == 0) {
+      __threadfence();
+      last = atomicAdd(&P.cnt2[U.rb], 1) == G - 1;
+    }
     last = __shfl_sync(kFull, last, 0);
     if (last) {
       // Deterministic combine of this 16-column block, in set order
@@ -216,11 +247,21 @@ __device__ __forceinline__ void dispatch_unit(int nbk, const FfnParams& P, const
   }
 }
 
+// Round descriptor published by the producer through the stage barrier.
+struct RoundDesc {
+  int u0;    // first unit
+  int n;     // units (one per consumer warp); 0 = end of work
+  int kind;  // 1 = W1, 2 = W2
+  int pad;
+};
+constexpr int kRoundRing = 8;  // > kStages: a round spans >= 1 stage
+
 __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
+  RoundDesc* rdesc = reinterpret_cast<RoundDesc*>(empty + kStages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -233,53 +274,73 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
   __syncthreads();
   // Everything below reads the router kernel's outputs.
   pdl_wait();
+  if (threadIdx.x == 0) stamp(P, 0);
 
   const int G = P.hdr->n_groups;
   if (G == 0) return;
   const int KT1 = P.Dp >> 4, KT2 = P.Hp >> 4;
   const int RB1 = P.Hp >> 3, RB2 = P.Dp >> 4;
-  const int64_t U1 = static_cast<int64_t>(G) * RB1, U2 = static_cast<int64_t>(G) * RB2;
-  // Two phases, each balanced over all CTAs: every CTA first streams its
-  // share of the W1 (gate/up) units, then its share of the W2 (down) units.
-  // W2 units acquire-wait on their token group's W1 counter, and their weights
-  // are prefetched by the producer while the wait is pending.
-  const int64_t c = blockIdx.x, nC = gridDim.x;
-  const int64_t r1b = c * U1 / nC, r1e = (c + 1) * U1 / nC;
-  const int64_t r2b = U1 + c * U2 / nC, r2e = U1 + (c + 1) * U2 / nC;
+  const int U1 = G * RB1, U2 = G * RB2;
+  // Dynamic scheduling: rounds of up to 8 consecutive units are claimed from
+  // two global counters, all W1 (gate/up) rounds before any W2 (down) round.
+  // A CTA therefore finishes its own W1 rounds before it starts W2 rounds,
+  // and W2 units only wait for W1 units claimed earlier (by any CTA), so the
+  // acquire-waits cannot deadlock; faster SMs simply claim more rounds.
+  int* claims = P.cnt2 + RB2;
 
   int stage = 0;
   uint32_t phase = 0;
 
   if (warp == kFfnWarps) {
-    // ---------------- producer: TMA bulk weight stream ----------------
+    // ---------------- producer: claims rounds, TMA bulk weight stream ----------
     if (lane == 0) {
       const uint64_t pol = l2_policy_evict_first();
-      for (int64_t u = r1b; u < r2e;) {
-        if (u == r1e) u = r2b;
-        if (u >= r2e) break;
-        const bool is1 = u < U1;
-        const int64_t rend = is1 ? r1e : r2e;
-        const int n = static_cast<int>(rend - u < kFfnWarps ? rend - u : kFfnWarps);
+      bool w1_left = true;
+      for (int seq = 0;; ++seq) {
+        RoundDesc d{0, 0, 0, 0};
+        if (w1_left) {
+          const int r = atomicAdd(&claims[0], 1);
+          if (r * kFfnWarps < U1) {
+            d.u0 = r * kFfnWarps;
+            d.n = min(kFfnWarps, U1 - d.u0);
+            d.kind = 1;
+          } else {
+            w1_left = false;
+          }
+        }
+        if (!w1_left) {
+          const int r = atomicAdd(&claims[1], 1);
+          if (r * kFfnWarps < U2) {
+            d.u0 = U1 + r * kFfnWarps;
+            d.n = min(kFfnWarps, U2 - r * kFfnWarps);
+            d.kind = 2;
+          }
+        }
+        mbar_wait(&empty[stage], phase ^ 1u);
+        rdesc[seq & (kRoundRing - 1)] = d;
+        if (d.n == 0) {
+          mbar_arrive(&full[stage]);  // end-of-work message, no payload
+          break;
+        }
+        const bool is1 = d.kind == 1;
         const int nst = (is1 ? KT1 : KT2) / kKtPerSlot;
         const uint4* src[kFfnWarps];
-        for (int w = 0; w < n; ++w) {
-          const int64_t uu = u + w;
+        for (int w = 0; w < d.n; ++w) {
+          const int uu = d.u0 + w;
           if (is1) {
-            const int g = static_cast<int>(uu / RB1), rb = static_cast<int>(uu % RB1);
-            const int e = P.group_a[g];
-            src[w] = P.w1 + (static_cast<size_t>(e) * RB1 + rb) * KT1 * 32;
+            const int g = uu / RB1, rb = uu % RB1;
+            src[w] = P.w1 + (static_cast<size_t>(P.group_a[g]) * RB1 + rb) * KT1 * 32;
           } else {
-            const int64_t v = uu - U1;
-            const int g = static_cast<int>(v / RB2), rb = static_cast<int>(v % RB2);
-            const int e = P.group_a[g];
-            src[w] = P.w2 + (static_cast<size_t>(e) * RB2 + rb) * KT2 * 32;
+            const int v = uu - U1;
+            const int g = v / RB2, rb = v % RB2;
+            src[w] = P.w2 + (static_cast<size_t>(P.group_a[g]) * RB2 + rb) * KT2 * 32;
           }
         }
         for (int s = 0; s < nst; ++s) {
-          mbar_wait(&empty[stage], phase ^ 1u);
-          mbar_arrive_expect_tx(&full[stage], n * kSlotBytes);
+          if (s > 0) mbar_wait(&empty[stage], phase ^ 1u);
+          mbar_arrive_expect_tx(&full[stage], d.n * kSlotBytes);
           uint8_t* dst = ring + stage * kStageBytes;
-          for (int w = 0; w < n; ++w)
+          for (int w = 0; w < d.n; ++w)
             bulk_g2s(dst + w * kSlotBytes, src[w] + s * kKtPerSlot * 32, kSlotBytes, &full[stage],
                      pol);
           if (++stage == kStages) {
@@ -287,30 +348,34 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
             phase ^= 1u;
           }
         }
-        u += n;
       }
+      stamp(P, 4);
     }
     return;
   }
 
   // ---------------- consumers ----------------
-  for (int64_t u = r1b; u < r2e;) {
-    if (u == r1e) u = r2b;
-    if (u >= r2e) break;
-    const bool is1 = u < U1;
-    const int64_t rend = is1 ? r1e : r2e;
-    const int n = static_cast<int>(rend - u < kFfnWarps ? rend - u : kFfnWarps);
+  bool in_w2 = false;
+  for (int seq = 0;; ++seq) {
+    mbar_wait(&full[stage], phase);  // the round's first stage carries its descriptor
+    const RoundDesc d = rdesc[seq & (kRoundRing - 1)];
+    if (d.n == 0) break;
+    const bool is1 = d.kind == 1;
+    if (!is1 && !in_w2) {
+      in_w2 = true;
+      if (threadIdx.x == 0) stamp(P, 1);
+    }
     const int nst = (is1 ? KT1 : KT2) / kKtPerSlot;
-    if (warp < n) {
-      const int64_t uu = u + warp;
+    if (warp < d.n) {
+      const int uu = d.u0 + warp;
       Unit U;
       if (is1) {
-        U.g = static_cast<int>(uu / RB1);
-        U.rb = static_cast<int>(uu % RB1);
+        U.g = uu / RB1;
+        U.rb = uu % RB1;
       } else {
-        const int64_t v = uu - U1;
-        U.g = static_cast<int>(v / RB2);
-        U.rb = static_cast<int>(v % RB2);
+        const int v = uu - U1;
+        U.g = v / RB2;
+        U.rb = v % RB2;
       }
       U.row0 = P.group_row0[U.g];
       U.rows = P.group_rows[U.g];
@@ -322,8 +387,8 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
     } else {
       skip_unit(full, empty, stage, phase, nst);
     }
-    u += n;
   }
+  if (threadIdx.x == 0) stamp(P, 3);
 }
 
 // ---------------------------------------------------------------------------
@@ -442,7 +507,9 @@ namespace oea_host {
 
 using namespace oea_dev;
 
-size_t ffn_bf16_smem_bytes() { return kStages * kStageBytes + 2 * kStages * sizeof(uint64_t); }
+size_t ffn_bf16_smem_bytes() {
+  return kStages * kStageBytes + 2 * kStages * sizeof(uint64_t) + kRoundRing * sizeof(RoundDesc);
+}
 
 int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const FfnBuffers& fb,
                     bool pdl, cudaStream_t s) {
@@ -468,6 +535,8 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   P.set_len = fb.set_len;
   P.wts = fb.weights_f32;
   P.out = static_cast<float*>(fb.out);
+  P.trace = fb.trace;
+  P.mode = fb.mode;
 
   static bool attr_set = false;
   const size_t smem = ffn_bf16_smem_bytes();

@@ -73,6 +73,9 @@ struct oea_ctx {
   size_t pinned_bytes = 0;
   // Last decode, for oea_last_plan_host.
   int last_B = 0, last_N = 0, last_stride = 0, last_kind = 0;  // kind 1 = fused bf16, 2 = f64 route
+  // Debug instrumentation of the FFN (env OEA_FFN_TRACE=1 / OEA_FFN_MODE=n).
+  unsigned long long* ffn_trace = nullptr;
+  int ffn_mode = 0;
 };
 
 struct oea_layer {
@@ -182,6 +185,8 @@ struct FfnBuffers {
   const float* weights_f32;
   const double* weights_f64;
   void* out;               // [B][D] f32 (bf16 path) / f64 (simt)
+  unsigned long long* trace = nullptr;  // debug timeline (OEA_FFN_TRACE)
+  int mode = 0;                         // debug mode (OEA_FFN_MODE)
 };
 size_t ffn_bf16_smem_bytes();
 int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride,
@@ -216,8 +221,9 @@ struct FusedRouterBuffers {
   int32_t* phase1_n;        // [B] may be null
   int32_t* base_union;      // [N] may be null
   int32_t* base_union_count;
+  unsigned long long* trace = nullptr;
 };
-size_t router_fused_smem_bytes(int B, int Np);
+size_t router_fused_smem_bytes(int B, int Np, int Dp, int stride);
 int router_fused_launch(oea_ctx* ctx, const oea_layer* L, const oea_dev::Cfg& cfg, int B,
                         const FusedRouterBuffers& rb, cudaStream_t s);
 

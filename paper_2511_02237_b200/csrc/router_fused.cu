@@ -239,11 +239,11 @@ struct RouterParams {
   const uint4* rfrag;  // [Np/16][Dp/16][32] uint4
   const __nv_bfloat16* x;
   const uint8_t* mask;
-  __nv_bfloat16* xpad;
+  __nv_bfloat16* xpad;  // null when D == Dp (the FFN then reads x directly)
   int B, D, Dp, N, Np;
   Cfg cfg;
   float* logits;  // [B][Np]
-  int32_t* order;  // [B][Np]
+  int32_t* order;  // [B][Np] (export only)
   int32_t* sets;
   int32_t* set_len;
   float* wts32;
@@ -264,38 +264,226 @@ struct RouterParams {
   int32_t* phase1_n;
   int32_t* base_union;
   int32_t* base_union_count;
+  unsigned long long* trace;  // debug: rows 1000+rank of the FFN trace buffer
 };
 
-constexpr int kRW = kRouterThreads / 32;  // 16 warps
-
-__device__ __forceinline__ uint32_t load_x_pair(const __nv_bfloat16* xrow, int k, int D) {
-  // elements k, k+1 of a bf16 row (zero beyond D)
-  if ((D & 1) == 0 && k + 1 < D) return __ldg(reinterpret_cast<const uint32_t*>(xrow + k));
-  const unsigned short lo = k < D ? __bfloat16_as_ushort(xrow[k]) : 0;
-  const unsigned short hi = k + 1 < D ? __bfloat16_as_ushort(xrow[k + 1]) : 0;
-  return static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+__device__ __forceinline__ void rstamp(const RouterParams& P, int rank, int slot) {
+  if (P.trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    P.trace[(1000 + rank) * 8 + slot] = t;
+  }
 }
 
+constexpr int kRW = kRouterThreads / 32;  // 16 warps
+constexpr int kMaxKtPerWarp = 16;          // k-tiles loaded per HBM round trip
+constexpr int kXsPad = 8;                  // bf16 elements of row padding (bank spread)
+
+__device__ __forceinline__ float key_to_logit(uint64_t k) {
+  const uint32_t u = static_cast<uint32_t>(k >> 32);
+  return __uint_as_float((u >> 31) ? (u & 0x7fffffffu) : ~u);
+}
+
+// Per-token routing state kept in registers between the two union phases.
 template <int E>
-__device__ void route_token_sort(const RouterParams& P, int t, float* s_rowmax) {
-  const int lane = threadIdx.x & 31;
-  const float* l = P.logits + static_cast<size_t>(t) * P.Np;
+struct TokState {
   uint64_t k[E];
   uint32_t id[E];
+  int n_i;
+};
+
+template <int E>
+__device__ __forceinline__ void tok_load_sort(const RouterParams& P, int t, TokState<E>& S) {
+  const int lane = threadIdx.x & 31;
+  const float* l = P.logits + static_cast<size_t>(t) * P.Np;
+  float v[E];
 #pragma unroll
   for (int j = 0; j < E; ++j) {
     const int p = j * 32 + lane;
-    k[j] = p < P.N ? order_key_f32(__ldcg(l + p)) : 0ull;
-    id[j] = static_cast<uint32_t>(p);
+    v[j] = p < P.N ? __ldcg(l + p) : 0.0f;
   }
-  warp_rank_sort<E>(k, id);
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const int p = j * 32 + lane;
+    S.k[j] = p < P.N ? order_key_f32(v[j]) : 0ull;
+    S.id[j] = static_cast<uint32_t>(p);
+  }
+  warp_rank_sort<E>(S.k, S.id);
+}
+
+// Phase 1 (routing.cpp:226-268): baseline size n_i and the union bitmap.
+template <int E>
+__device__ __forceinline__ void tok_phase1(const RouterParams& P, int t, TokState<E>& S,
+                                           uint32_t* s_union) {
+  const int lane = threadIdx.x & 31;
+  const Cfg& cfg = P.cfg;
+  const bool real = P.mask == nullptr || P.mask[t] != 0;
+  S.n_i = 0;
+  if (!real || cfg.mode == OEA_MODE_VANILLA) return;
+  int t_i = P.N;
+  if (cfg.p != 1.0) {
+    // Best-effort parity (documented): fp64 softmax of the fp32 logits, then
+    // the reference's sequential cumulative mass in rank order.
+    const double m = static_cast<double>(key_to_logit(__shfl_sync(kFull, S.k[0], 0)));
+    double e[E], z = 0.0;
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      e[j] = (j * 32 + lane) < P.N ? exp(static_cast<double>(key_to_logit(S.k[j])) - m) : 0.0;
+      z += e[j];
+    }
+    for (int off = 16; off > 0; off >>= 1) z += __shfl_xor_sync(kFull, z, off);
+    double cum = 0.0;
+    bool done = false;
+    for (int j = 0; j < E && !done; ++j)
+      for (int src = 0; src < 32; ++src) {
+        const int p = j * 32 + src;
+        if (p >= P.N) {
+          done = true;
+          break;
+        }
+        cum = __dadd_rn(cum, __shfl_sync(kFull, e[j], src) / z);
+        if (cum >= cfg.p) {
+          t_i = p + 1;
+          done = true;
+          break;
+        }
+      }
+  }
+  S.n_i = min(cfg.k0, t_i);
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const int p = j * 32 + lane;
+    if (p < S.n_i) atomicOr(&s_union[S.id[j] >> 5], 1u << (S.id[j] & 31));
+  }
+}
+
+// Phase 2 (routing.cpp:270-303) + weights (routing.cpp:33-49) + outputs.
+// The selected set is always in ascending rank order (baseline ranks, then
+// piggybacked ranks in scan order), so each lane knows which of its sorted
+// positions are selected and the fp64 renormalisation runs over registers.
+template <int E>
+__device__ __forceinline__ void tok_phase2(const RouterParams& P, int t, const TokState<E>& S,
+                                           const uint32_t* s_union, int* s_sets, int* s_len) {
+  const int lane = threadIdx.x & 31;
+  const Cfg& cfg = P.cfg;
+  const bool real = P.mask == nullptr || P.mask[t] != 0;
+  bool sel[E];
+  int len = 0;
+#pragma unroll
+  for (int j = 0; j < E; ++j) sel[j] = false;
+  if (real) {
+    if (cfg.mode == OEA_MODE_VANILLA) {
+#pragma unroll
+      for (int j = 0; j < E; ++j) sel[j] = (j * 32 + lane) < cfg.k;
+      len = cfg.k;
+    } else {
+#pragma unroll
+      for (int j = 0; j < E; ++j) sel[j] = (j * 32 + lane) < S.n_i;
+      len = S.n_i;
+      if (cfg.mode != OEA_MODE_PRUNED) {
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+          const int p = j * 32 + lane;
+          const bool cand = p >= S.n_i && p < cfg.max_p && p < P.N &&
+                            ((s_union[S.id[j] >> 5] >> (S.id[j] & 31)) & 1u);
+          const unsigned m = __ballot_sync(kFull, cand);
+          const int take = max(cfg.limit - len, 0);
+          if (cand && __popc(m & lanemask_lt()) < take) sel[j] = true;
+          len += min(__popc(m), take);
+        }
+      }
+    }
+  }
+  // fp64 weights: w = e / sum_set e, e = exp(l - max) (the softmax
+  // denominator cancels); sequential sum in set order by lane 0.
+  const double m = static_cast<double>(key_to_logit(__shfl_sync(kFull, S.k[0], 0)));
+  double e[E];
+#pragma unroll
+  for (int j = 0; j < E; ++j)
+    e[j] = sel[j] ? exp(static_cast<double>(key_to_logit(S.k[j])) - m) : 0.0;
+  double mass = 0.0;
+  int pos = 0;
+  int32_t* gset = P.sets + static_cast<size_t>(t) * cfg.stride;
+  int* sset = s_sets + t * cfg.stride;
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    unsigned m2 = __ballot_sync(kFull, sel[j]);
+    // set slots of the selected positions of this j-row, in lane order
+    const int my = pos + __popc(m2 & lanemask_lt());
+    if (sel[j]) {
+      gset[my] = static_cast<int32_t>(S.id[j]);
+      sset[my] = static_cast<int>(S.id[j]);
+    }
+    while (m2) {
+      const int src = __ffs(m2) - 1;
+      m2 &= m2 - 1;
+      mass = __dadd_rn(mass, __shfl_sync(kFull, e[j], src));
+    }
+    pos += __popc(__ballot_sync(kFull, sel[j]));
+  }
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const unsigned m2 = __ballot_sync(kFull, sel[j]);
+    int before = 0;
+#pragma unroll
+    for (int jj = 0; jj < j; ++jj) before += __popc(__ballot_sync(kFull, sel[jj]));
+    if (sel[j]) {
+      const int slot = before + __popc(m2 & lanemask_lt());
+      const double w = e[j] / mass;
+      P.wts32[static_cast<size_t>(t) * cfg.stride + slot] = static_cast<float>(w);
+      if (P.wts64) P.wts64[static_cast<size_t>(t) * cfg.stride + slot] = w;
+    }
+  }
+  for (int j = len + lane; j < cfg.stride; j += 32) {
+    gset[j] = -1;
+    P.wts32[static_cast<size_t>(t) * cfg.stride + j] = 0.0f;
+    if (P.wts64) P.wts64[static_cast<size_t>(t) * cfg.stride + j] = 0.0;
+  }
+  // export of the full order (sort_experts) for the parity harness
   int32_t* ord = P.order + static_cast<size_t>(t) * P.Np;
 #pragma unroll
   for (int j = 0; j < E; ++j) {
     const int p = j * 32 + lane;
-    if (p < P.N) ord[p] = static_cast<int32_t>(id[j]);
+    if (p < P.N) ord[p] = static_cast<int32_t>(S.id[j]);
   }
-  if (lane == 0) s_rowmax[t] = __ldcg(l + id[0]);
+  if (lane == 0) {
+    P.set_len[t] = len;
+    s_len[t] = len;
+    if (P.phase1_n) P.phase1_n[t] = S.n_i;
+  }
+}
+
+template <int E>
+__device__ void route_all(const RouterParams& P, uint32_t* s_union, int* s_sets, int* s_len,
+                          int* s_n) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (P.B <= kRW) {
+    // one token per warp: the sorted row stays in registers across the
+    // union barrier
+    TokState<E> S;
+    const int t = warp;
+    if (t < P.B) {
+      tok_load_sort<E>(P, t, S);
+      tok_phase1<E>(P, t, S, s_union);
+    }
+    __syncthreads();
+    if (t < P.B) tok_phase2<E>(P, t, S, s_union, s_sets, s_len);
+  } else {
+    for (int t = warp; t < P.B; t += kRW) {
+      TokState<E> S;
+      tok_load_sort<E>(P, t, S);
+      tok_phase1<E>(P, t, S, s_union);
+      if (lane == 0) s_n[t] = S.n_i;
+    }
+    __syncthreads();
+    for (int t = warp; t < P.B; t += kRW) {
+      TokState<E> S;
+      tok_load_sort<E>(P, t, S);  // re-rank (cheaper than keeping B rows)
+      S.n_i = s_n[t];
+      tok_phase2<E>(P, t, S, s_union, s_sets, s_len);
+    }
+  }
+  __syncthreads();
 }
 
 __global__ void __cluster_dims__(kRouterCluster, 1, 1) __launch_bounds__(kRouterThreads, 1)
@@ -309,30 +497,50 @@ __global__ void __cluster_dims__(kRouterCluster, 1, 1) __launch_bounds__(kRouter
   // Let the FFN grid get resident early; it waits (griddepcontrol.wait) for
   // this grid's completion before touching any of its outputs.
   pdl_launch_dependents();
+  rstamp(P, crank, 0);
 
   const int Np = P.Np, B = P.B;
-  float* part = reinterpret_cast<float*>(smem);  // [kRouterTokChunk][Np]
-
-  // ---- x -> zero-padded bf16 copy for the FFN (all CTAs share the work) ----
-  {
-    const size_t total = static_cast<size_t>(B) * P.Dp;
-    for (size_t f = crank * kRouterThreads + threadIdx.x; f < total;
-         f += kRouterCluster * kRouterThreads) {
-      const int t = static_cast<int>(f / P.Dp), d = static_cast<int>(f % P.Dp);
-      P.xpad[f] = d < P.D ? P.x[static_cast<size_t>(t) * P.D + d] : __float2bfloat16_rn(0.0f);
-    }
-  }
-
-  // ---- 1. split-K gate GEMV over the cluster ----
   const int KT = P.Dp >> 4, nrb = Np >> 4;
   const int kt0 = static_cast<int>(crank) * KT / kRouterCluster;
   const int kt1 = (static_cast<int>(crank) + 1) * KT / kRouterCluster;
+  const int kslice = (kt1 - kt0) * 16;
+  const int xs_stride = kslice + kXsPad;  // bf16 elements
+  float* part = reinterpret_cast<float*>(smem);  // [kRouterTokChunk][Np]
+  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(part + kRouterTokChunk * Np);
+
+  // ---- x -> zero-padded bf16 copy for the FFN when D is not a tile multiple ----
+  if (P.xpad) {
+    for (int t = crank; t < B; t += kRouterCluster)
+      for (int d = threadIdx.x; d < P.Dp; d += kRouterThreads)
+        P.xpad[static_cast<size_t>(t) * P.Dp + d] =
+            d < P.D ? P.x[static_cast<size_t>(t) * P.D + d] : __float2bfloat16_rn(0.0f);
+  }
+
+  // ---- 1. split-K gate GEMV over the cluster ----
   const int ks_split = nrb <= kRW / 2 ? 2 : 1;
   for (int tc = 0; tc < B; tc += kRouterTokChunk) {
     const int ntok = min(kRouterTokChunk, B - tc);
     const int nbc = (ntok + 7) >> 3;
+    // stage this CTA's K-slice of x (zero beyond D / the chunk)
     for (int i = threadIdx.x; i < kRouterTokChunk * Np; i += kRouterThreads) part[i] = 0.0f;
+    for (int i = threadIdx.x; i < nbc * 8 * (kslice >> 1); i += kRouterThreads) {
+      const int tt = i / (kslice >> 1), kk = (i % (kslice >> 1)) * 2;
+      const int k = kt0 * 16 + kk;
+      uint32_t v = 0;
+      if (tt < ntok) {
+        const __nv_bfloat16* xr = P.x + static_cast<size_t>(tc + tt) * P.D;
+        if ((P.D & 1) == 0 && k + 1 < P.D) {
+          v = __ldg(reinterpret_cast<const uint32_t*>(xr + k));
+        } else {
+          const unsigned short lo = k < P.D ? __bfloat16_as_ushort(xr[k]) : 0;
+          const unsigned short hi = k + 1 < P.D ? __bfloat16_as_ushort(xr[k + 1]) : 0;
+          v = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+        }
+      }
+      *reinterpret_cast<uint32_t*>(xs + tt * xs_stride + kk) = v;
+    }
     __syncthreads();
+    rstamp(P, crank, 1);
     for (int job = warp; job < nrb * ks_split; job += kRW) {
       const int rb = job % nrb, ks = job / nrb;
       const int ka = kt0 + (kt1 - kt0) * ks / ks_split;
@@ -340,23 +548,27 @@ __global__ void __cluster_dims__(kRouterCluster, 1, 1) __launch_bounds__(kRouter
       float acc[8][4];
 #pragma unroll
       for (int nb = 0; nb < 8; ++nb) acc[nb][0] = acc[nb][1] = acc[nb][2] = acc[nb][3] = 0.0f;
-      const __nv_bfloat16* xr[8];
+      // A-tile loads of up to 16 k-tiles in flight at once (one HBM round
+      // trip per 16 k-tiles; a single trip at D <= 4096, N <= 128).
+      for (int kc = ka; kc < kb; kc += kMaxKtPerWarp) {
+        uint4 a[kMaxKtPerWarp];
 #pragma unroll
-      for (int nb = 0; nb < 8; ++nb) {
-        const int tt = tc + nb * 8 + gq;
-        xr[nb] = (nb < nbc && tt < B) ? P.x + static_cast<size_t>(tt) * P.D : nullptr;
-      }
-      for (int kt = ka; kt < kb; ++kt) {
-        const uint4 a = __ldg(P.rfrag + (static_cast<size_t>(rb) * KT + kt) * 32 + lane);
+        for (int i = 0; i < kMaxKtPerWarp; ++i)
+          if (kc + i < kb)
+            a[i] = __ldg(P.rfrag + (static_cast<size_t>(rb) * KT + kc + i) * 32 + lane);
 #pragma unroll
-        for (int nb = 0; nb < 8; ++nb) {
-          if (nb < nbc) {
-            uint32_t b0 = 0, b1 = 0;
-            if (xr[nb]) {
-              b0 = load_x_pair(xr[nb], kt * 16 + 2 * q, P.D);
-              b1 = load_x_pair(xr[nb], kt * 16 + 8 + 2 * q, P.D);
+        for (int i = 0; i < kMaxKtPerWarp; ++i) {
+          if (kc + i < kb) {
+            const int kk = (kc + i - kt0) * 16 + 2 * q;
+#pragma unroll
+            for (int nb = 0; nb < 8; ++nb) {
+              if (nb < nbc) {
+                const __nv_bfloat16* xr = xs + (nb * 8 + gq) * xs_stride + kk;
+                const uint32_t b0 = *reinterpret_cast<const uint32_t*>(xr);
+                const uint32_t b1 = *reinterpret_cast<const uint32_t*>(xr + 8);
+                mma_bf16_16816(acc[nb], a[i], b0, b1);
+              }
             }
-            mma_bf16_16816(acc[nb], a, b0, b1);
           }
         }
       }
@@ -374,7 +586,10 @@ __global__ void __cluster_dims__(kRouterCluster, 1, 1) __launch_bounds__(kRouter
         }
       }
     }
+    __syncthreads();
+    rstamp(P, crank, 2);
     cluster.sync();
+    rstamp(P, crank, 3);
     // Distributed fixed-order reduction over DSMEM: CTA c sums slice c of
     // every CTA's partial (ranks 0..7 in order) into the global logits.
     {
@@ -382,154 +597,66 @@ __global__ void __cluster_dims__(kRouterCluster, 1, 1) __launch_bounds__(kRouter
       const int e0 = static_cast<int>(crank) * elems / kRouterCluster;
       const int e1 = (static_cast<int>(crank) + 1) * elems / kRouterCluster;
       for (int i = e0 + threadIdx.x; i < e1; i += kRouterThreads) {
+        float v[kRouterCluster];
+#pragma unroll
+        for (int r = 0; r < kRouterCluster; ++r) v[r] = cluster.map_shared_rank(part, r)[i];
         float s = 0.0f;
 #pragma unroll
-        for (int r = 0; r < kRouterCluster; ++r) s += cluster.map_shared_rank(part, r)[i];
-        const int tt = i / Np, n = i % Np;
-        P.logits[static_cast<size_t>(tc + tt) * Np + n] = s;
+        for (int r = 0; r < kRouterCluster; ++r) s += v[r];
+        P.logits[static_cast<size_t>(tc) * Np + i] = s;
       }
     }
     cluster.sync();
   }
+  rstamp(P, crank, 4);
   if (crank != 0) return;
 
-  // ---- 2. routing (CTA 0) ----
-  int* s_n = reinterpret_cast<int*>(smem);                   // [B]
-  float* s_rowmax = reinterpret_cast<float*>(s_n + B);        // [B]
-  int* s_len = reinterpret_cast<int*>(s_rowmax + B);          // [B]
-  uint32_t* s_union = reinterpret_cast<uint32_t*>(s_len + B); // [Np/32]
+  // ---- 2. routing (CTA 0), register-resident per token ----
+  uint32_t* s_union = reinterpret_cast<uint32_t*>(smem);      // [ceil(Np/32)]
   const int uw = (Np + 31) >> 5;
-  int* s_loads = reinterpret_cast<int*>(s_union + uw);        // [Np]
+  int* s_len = reinterpret_cast<int*>(s_union + uw);           // [B]
+  int* s_sets = s_len + B;                                     // [B][stride]
+  int* s_loads = s_sets + B * P.cfg.stride;                    // [Np]
   int* s_eslot = s_loads + Np;
   int* s_rowb = s_eslot + Np;
   int* s_grpb = s_rowb + Np;
-  int* s_tmp = s_grpb + Np;                                   // [40]
-  uint32_t* s_tokbits = reinterpret_cast<uint32_t*>(s_tmp + 40);  // [Np][Bw]
+  int* s_tmp = s_grpb + Np;                                    // [40]
+  int* s_n = s_tmp + 40;                                       // [B]
+  uint32_t* s_tokbits = reinterpret_cast<uint32_t*>(s_n + B);  // [Np][Bw]
   const int Bw = (B + 31) >> 5;
   for (int i = threadIdx.x; i < uw; i += kRouterThreads) s_union[i] = 0u;
   for (int i = threadIdx.x; i < Np * Bw; i += kRouterThreads) s_tokbits[i] = 0u;
   __syncthreads();
 
-  const Cfg& cfg = P.cfg;
-  for (int t = warp; t < B; t += kRW) {
-    const int E = (Np <= 32) ? 1 : (Np <= 64) ? 2 : (Np <= 128) ? 4 : 8;
-    if (E == 1)
-      route_token_sort<1>(P, t, s_rowmax);
-    else if (E == 2)
-      route_token_sort<2>(P, t, s_rowmax);
-    else if (E == 4)
-      route_token_sort<4>(P, t, s_rowmax);
-    else
-      route_token_sort<8>(P, t, s_rowmax);
-    __syncwarp();
-    const bool real = P.mask == nullptr || P.mask[t] != 0;
-    int n_i = 0;
-    if (real && cfg.mode != OEA_MODE_VANILLA) {
-      const int32_t* ord = P.order + static_cast<size_t>(t) * Np;
-      int t_i = P.N;
-      if (cfg.p != 1.0) {
-        // Best-effort parity (documented): fp64 softmax of the fp32 logits,
-        // then the reference's sequential cumulative mass in rank order.
-        const float* l = P.logits + static_cast<size_t>(t) * Np;
-        const double m = static_cast<double>(s_rowmax[t]);
-        double z = 0.0;
-        for (int j = lane; j < P.N; j += 32) z += exp(static_cast<double>(__ldcg(l + j)) - m);
-        for (int off = 16; off > 0; off >>= 1) z += __shfl_xor_sync(kFull, z, off);
-        if (lane == 0) {
-          double cum = 0.0;
-          for (int j = 0; j < P.N; ++j) {
-            cum = __dadd_rn(cum, exp(static_cast<double>(__ldcg(l + ord[j])) - m) / z);
-            if (cum >= cfg.p) {
-              t_i = j + 1;
-              break;
-            }
-          }
-        }
-        t_i = __shfl_sync(kFull, t_i, 0);
-      }
-      n_i = min(cfg.k0, t_i);
-      for (int j = lane; j < n_i; j += 32) {
-        const int e = ord[j];
-        atomicOr(&s_union[e >> 5], 1u << (e & 31));
-      }
-    }
-    if (lane == 0) s_n[t] = n_i;
-  }
-  __syncthreads();
+  if (Np <= 32)
+    route_all<1>(P, s_union, s_sets, s_len, s_n);
+  else if (Np <= 64)
+    route_all<2>(P, s_union, s_sets, s_len, s_n);
+  else if (Np <= 128)
+    route_all<4>(P, s_union, s_sets, s_len, s_n);
+  else
+    route_all<8>(P, s_union, s_sets, s_len, s_n);
 
-  for (int i = threadIdx.x; i < Np; i += kRouterThreads) s_loads[i] = 0;
-  __syncthreads();
-  for (int t = warp; t < B; t += kRW) {
-    const bool real = P.mask == nullptr || P.mask[t] != 0;
-    const int32_t* ord = P.order + static_cast<size_t>(t) * Np;
-    int32_t* srow = P.sets + static_cast<size_t>(t) * cfg.stride;
-    int len = 0;
-    if (real) {
-      if (cfg.mode == OEA_MODE_VANILLA) {
-        len = cfg.k;
-        for (int j = lane; j < len; j += 32) srow[j] = ord[j];
-      } else {
-        const int n_i = s_n[t];
-        for (int j = lane; j < n_i; j += 32) srow[j] = ord[j];
-        len = n_i;
-        if (cfg.mode != OEA_MODE_PRUNED) {
-          for (int base = n_i; base < cfg.max_p && len < cfg.limit; base += 32) {
-            const int j = base + lane;
-            const int e = j < cfg.max_p ? ord[j] : -1;
-            const bool member = e >= 0 && ((s_union[e >> 5] >> (e & 31)) & 1u);
-            const unsigned mm = __ballot_sync(kFull, member);
-            const int pos = __popc(mm & lanemask_lt());
-            const int take = cfg.limit - len;
-            if (member && pos < take) srow[len + pos] = e;
-            len += min(__popc(mm), take);
-          }
-        }
-      }
+  rstamp(P, 0, 5);
+  if ((P.base_union || P.base_union_count) && warp == 0) {
+    int c = 0;
+    for (int base = 0; base < P.N; base += 32) {
+      const int e = base + lane;
+      const bool f = e < P.N && ((s_union[e >> 5] >> (e & 31)) & 1u);
+      const unsigned m = __ballot_sync(kFull, f);
+      if (f && P.base_union) P.base_union[c + __popc(m & lanemask_lt())] = e;
+      c += __popc(m);
     }
-    for (int j = len + lane; j < cfg.stride; j += 32) {
-      srow[j] = -1;
-      P.wts32[static_cast<size_t>(t) * cfg.stride + j] = 0.0f;
-      if (P.wts64) P.wts64[static_cast<size_t>(t) * cfg.stride + j] = 0.0;
-    }
-    __syncwarp();
-    // Weights: w_j = e_j / sum_set e with e = exp(l - max) in fp64.
-    const float* l = P.logits + static_cast<size_t>(t) * Np;
-    const double m = static_cast<double>(s_rowmax[t]);
-    double mass = 0.0;
-    if (lane == 0)
-      for (int j = 0; j < len; ++j)
-        mass = __dadd_rn(mass, exp(static_cast<double>(__ldcg(l + srow[j])) - m));
-    mass = __shfl_sync(kFull, mass, 0);
-    for (int j = lane; j < len; j += 32) {
-      const double w = exp(static_cast<double>(__ldcg(l + srow[j])) - m) / mass;
-      P.wts32[static_cast<size_t>(t) * cfg.stride + j] = static_cast<float>(w);
-      if (P.wts64) P.wts64[static_cast<size_t>(t) * cfg.stride + j] = w;
-    }
-    if (lane == 0) {
-      P.set_len[t] = len;
-      s_len[t] = len;
-      if (P.phase1_n) P.phase1_n[t] = s_n[t];
-    }
-  }
-  __syncthreads();
-  if (P.base_union || P.base_union_count) {
-    if (threadIdx.x == 0) {
-      int c = 0;
-      for (int e = 0; e < P.N; ++e)
-        if ((s_union[e >> 5] >> (e & 31)) & 1u) {
-          if (P.base_union) P.base_union[c] = e;
-          ++c;
-        }
-      if (P.base_union_count) *P.base_union_count = c;
-    }
+    if (lane == 0 && P.base_union_count) *P.base_union_count = c;
   }
 
-  // ---- 3. compaction for the FFN ----
+  // ---- 3. compaction for the FFN (from shared memory) ----
   CompactOut o{P.active_union, P.active_count, P.total_load, P.loads, P.row_tok, P.row_slot,
                P.group_a, P.group_row0, P.group_rows, P.hdr, P.counters, P.n_counters};
-  compact_plan(B, P.N, cfg.stride, P.sets, P.set_len, s_loads, s_eslot, s_rowb, s_grpb, s_tokbits,
+  compact_plan(B, P.N, P.cfg.stride, s_sets, s_len, s_loads, s_eslot, s_rowb, s_grpb, s_tokbits,
                s_tmp, o);
-  if (P.hdr->n_groups == 0) {
+  rstamp(P, 0, 6);
+  if (o.hdr->n_groups == 0) {
     for (size_t f = threadIdx.x; f < static_cast<size_t>(B) * P.D; f += kRouterThreads)
       P.out[f] = 0.0f;
   }
@@ -541,10 +668,13 @@ namespace oea_host {
 
 using namespace oea_dev;
 
-size_t router_fused_smem_bytes(int B, int Np) {
-  const size_t gemv = static_cast<size_t>(kRouterTokChunk) * Np * sizeof(float);
-  const size_t route = (3 * static_cast<size_t>(B) + ((Np + 31) >> 5) + 4 * Np + 40) * 4 +
-                       static_cast<size_t>(Np) * ((B + 31) / 32) * 4;
+size_t router_fused_smem_bytes(int B, int Np, int Dp, int stride) {
+  const int KT = Dp >> 4;
+  const int kslice_max = ((KT + kRouterCluster - 1) / kRouterCluster) * 16;
+  const size_t gemv = static_cast<size_t>(kRouterTokChunk) * Np * sizeof(float) +
+                      static_cast<size_t>(kRouterTokChunk) * (kslice_max + kXsPad) * 2;
+  const size_t route = (static_cast<size_t>((Np + 31) >> 5) + 2 * B + static_cast<size_t>(B) * stride +
+                        4 * Np + 40) * 4 + static_cast<size_t>(Np) * ((B + 31) / 32) * 4;
   return gemv > route ? gemv : route;
 }
 
@@ -583,7 +713,8 @@ int router_fused_launch(oea_ctx* ctx, const oea_layer* L, const Cfg& cfg, int B,
   P.phase1_n = rb.phase1_n;
   P.base_union = rb.base_union;
   P.base_union_count = rb.base_union_count;
-  const size_t smem = router_fused_smem_bytes(B, L->Np);
+  P.trace = rb.trace;
+  const size_t smem = router_fused_smem_bytes(B, L->Np, L->Dp, cfg.stride);
   OEA_CUDA_TRY(ctx, cudaFuncSetAttribute(k_router_fused,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
