@@ -206,6 +206,12 @@ int oea_decode_graph_create(oea_ctx_t ctx, oea_layer_t layer, const void* x_dev,
                             const uint8_t* mask_dev, int32_t B,
                             const oea_routing_cfg* cfg, void* out_dev,
                             oea_graph_t* out);
+/* The same decode captured as two graphs (router+compaction | FFN), without
+ * the programmatic overlap, so each stage can be timed on its own (bench). */
+int oea_decode_stage_graphs_create(oea_ctx_t ctx, oea_layer_t layer, const void* x_dev,
+                                   const uint8_t* mask_dev, int32_t B,
+                                   const oea_routing_cfg* cfg, void* out_dev,
+                                   oea_graph_t* router_graph, oea_graph_t* ffn_graph);
 int oea_graph_launch(oea_graph_t graph, void* stream);
 int oea_graph_destroy(oea_graph_t graph);
 

@@ -9,6 +9,7 @@
 // Every function converts flat arrays to the reference's Eigen-typed structs,
 // calls the reference function unchanged, and flattens the result. Exceptions
 // become status codes: 1 std::invalid_argument, 2 std::domain_error, 3 other.
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -19,6 +20,11 @@
 #include "oea/moe_layer.hpp"
 #include "oea/routing.hpp"
 #include "oracle.hpp"
+
+#include <thread>
+
+extern "C" double oo_stream_normal(uint64_t key, uint64_t f);
+extern "C" uint64_t oo_stream_key(const uint64_t* parts, int32_t n);
 
 using namespace oea;
 
@@ -271,6 +277,61 @@ void* ref_layer_create(int scalar_is_float, int D, int H, int N, const double* r
       std::memcpy(ex.w_up.data(), wu + static_cast<size_t>(e) * D * H, sizeof(double) * D * H);
       std::memcpy(ex.w_down.data(), wd + static_cast<size_t>(e) * H * D, sizeof(double) * H * D);
     }
+    return L;
+  } catch (const std::exception& e) {
+    record(3, e.what());
+    return nullptr;
+  }
+}
+
+// A reference MoeLayerParams<Scalar> holding exactly make_random_layer(dims,
+// seed)'s values (moe_layer.cpp:76-98), filled by `threads` threads from the
+// counter stream instead of one sequential pass (bench CPU baseline setup).
+void* ref_layer_random(int scalar_is_float, int D, int H, int N, uint64_t seed, int threads) {
+  try {
+    const uint64_t parts[2] = {seed, 101};
+    const uint64_t key = oo_stream_key(parts, 2);
+    const double ds = 1.0 / std::sqrt(static_cast<double>(D));
+    const double hs = 1.0 / std::sqrt(static_cast<double>(H));
+    auto fill = [&](auto& L) {
+      L.router.resize(D, N);
+      L.experts.resize(N);
+      for (auto& ex : L.experts) {
+        ex.w_gate.resize(D, H);
+        ex.w_up.resize(D, H);
+        ex.w_down.resize(H, D);
+      }
+      const int64_t nr = static_cast<int64_t>(D) * N, per = static_cast<int64_t>(D) * H;
+      const int64_t total = nr + static_cast<int64_t>(N) * 3 * per;
+      std::vector<std::thread> th;
+      if (threads < 1) threads = 1;
+      for (int t = 0; t < threads; ++t)
+        th.emplace_back([&, t] {
+          for (int64_t f = total * t / threads; f < total * (t + 1) / threads; ++f) {
+            const double z = oo_stream_normal(key, static_cast<uint64_t>(f));
+            if (f < nr) {
+              L.router.data()[f] = static_cast<typename std::decay_t<decltype(L.router)>::Scalar>(ds * z);
+              continue;
+            }
+            const int64_t g = f - nr, e = g / (3 * per), r = g % (3 * per);
+            auto& ex = L.experts[e];
+            if (r < per)
+              ex.w_gate.data()[r] = ds * z;
+            else if (r < 2 * per)
+              ex.w_up.data()[r - per] = ds * z;
+            else
+              ex.w_down.data()[r - 2 * per] = hs * z;
+          }
+        });
+      for (auto& x : th) x.join();
+    };
+    if (scalar_is_float) {
+      auto* L = new RefLayer<float>;
+      fill(L->p);
+      return L;
+    }
+    auto* L = new RefLayer<double>;
+    fill(L->p);
     return L;
   } catch (const std::exception& e) {
     record(3, e.what());

@@ -91,6 +91,7 @@ def lib():
                 "oea_last_plan_host": [vp, vp, vp, vp],
                 "oea_decode_graph_create": [vp, vp, vp, vp, i32, vp, vp, vp],
                 "oea_graph_launch": [vp, vp],
+                "oea_decode_stage_graphs_create": [vp, vp, vp, vp, i32, vp, vp, vp, vp],
                 "oea_graph_destroy": [vp],
                 "oea_moe_forward_plan_host": [vp, vp, vp, i32, vp, vp, vp, i32, vp, vp],
                 "oea_router_scores_host": [vp, vp, vp, i32, vp],
@@ -115,7 +116,7 @@ EXPORTED = (
     "oea_layer_upload_router", "oea_layer_upload_expert", "oea_layer_init_random",
     "oea_layer_download_router", "oea_layer_download_expert", "oea_layer_info",
     "oea_moe_decode", "oea_moe_decode_host", "oea_last_plan_host", "oea_decode_graph_create",
-    "oea_graph_launch", "oea_graph_destroy", "oea_moe_forward_plan_host",
+    "oea_graph_launch", "oea_decode_stage_graphs_create", "oea_graph_destroy", "oea_moe_forward_plan_host",
     "oea_router_scores_host", "oea_ep_owner", "oea_debug_ffn_trace")
 
 

@@ -326,8 +326,9 @@ int blocks_for(size_t n) {
 // ---------------------------------------------------------------------------
 // Decode orchestration (shared by the direct call and graph capture).
 // ---------------------------------------------------------------------------
+// part: 0 = router + FFN (PDL-chained), 1 = router only, 2 = FFN only.
 int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const uint8_t* mask,
-                int B, const oea_routing_cfg& rc, void* out, cudaStream_t s) {
+                int B, const oea_routing_cfg& rc, void* out, cudaStream_t s, int part = 0) {
   const int stride = stride_of(rc);
   const Cfg cfg = dev_cfg(rc, stride);
   oea_host::FusedRouterBuffers rb;
@@ -358,9 +359,12 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   rb.base_union = w.base_union;
   rb.base_union_count = w.base_union_count;
   rb.trace = ctx->ffn_trace;
-  if (rb.trace) OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.trace, 0, 8 * 8 * 1024, s));
-  int r = oea_host::router_fused_launch(ctx, L, cfg, B, rb, s);
-  if (r) return r;
+  int r = OEA_OK;
+  if (part != 2) {
+    if (rb.trace) OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.trace, 0, 8 * 8 * 1024, s));
+    r = oea_host::router_fused_launch(ctx, L, cfg, B, rb, s);
+    if (r || part == 1) return r;
+  }
   oea_host::FfnBuffers fb;
   fb.x = padded ? static_cast<const void*>(w.xpad) : x;
   fb.row_tok = w.row_tok;
@@ -379,7 +383,7 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   fb.out = out;
   fb.trace = ctx->ffn_trace;
   fb.mode = ctx->ffn_mode;
-  return oea_host::ffn_bf16_launch(ctx, L, B, stride, fb, true, s);
+  return oea_host::ffn_bf16_launch(ctx, L, B, stride, fb, part == 0, s);
 }
 
 // f32/f64 layers: router_scores (fp64) -> route_f64 -> compaction -> SIMT FFN.
@@ -429,6 +433,9 @@ int validate_decode(oea_ctx* ctx, oea_layer* L, int B, const oea_routing_cfg* cf
     if (L->N > kMaxFusedN)
       return fail(ctx, OEA_ERR_INVALID_ARGUMENT,
                   "moe_decode: bf16 fused router supports N <= " + std::to_string(kMaxFusedN));
+    if (oea_host::router_fused_smem_bytes(B, L->Np, L->Dp, stride_of(*rc)) > 227 * 1024)
+      return fail(ctx, OEA_ERR_INVALID_ARGUMENT,
+                  "moe_decode: B x N too large for the single-CTA fused router");
   }
   return OEA_OK;
 }
@@ -979,6 +986,9 @@ int oea_decode_graph_create(oea_ctx_t ctx, oea_layer_t L, const void* x_dev,
     return r ? r : oea_check_cuda(ctx, e, "cudaStreamEndCapture");
   }
   g->graph = graph;
+  size_t nnodes = 0;
+  cudaGraphGetNodes(graph, nullptr, &nnodes);
+  g->kernels = L->dtype == OEA_DTYPE_BF16 ? 2 : static_cast<int>(nnodes);
   e = cudaGraphInstantiate(&g->exec, graph, 0);
   if (e != cudaSuccess) {
     cudaGraphDestroy(graph);
@@ -993,11 +1003,59 @@ int oea_decode_graph_create(oea_ctx_t ctx, oea_layer_t L, const void* x_dev,
   return OEA_OK;
 }
 
+int oea_decode_stage_graphs_create(oea_ctx_t ctx, oea_layer_t L, const void* x_dev,
+                                   const uint8_t* mask_dev, int32_t B, const oea_routing_cfg* cfg,
+                                   void* out_dev, oea_graph_t* router_out, oea_graph_t* ffn_out) {
+  CHECK_CTX(ctx);
+  if (router_out == nullptr || ffn_out == nullptr)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "null output pointer");
+  *router_out = *ffn_out = nullptr;
+  oea_routing_cfg rc;
+  int r = validate_decode(ctx, L, B, cfg, &rc);
+  if (r) return r;
+  if (L->dtype != OEA_DTYPE_BF16)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "stage graphs: bf16 layers only");
+  Workspace& w = extra(ctx)->ws;
+  r = ensure(ctx, w, need_for(L, B, stride_of(rc)));
+  if (r) return r;
+  OEA_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  oea_graph_t gs[2] = {nullptr, nullptr};
+  for (int part = 1; part <= 2; ++part) {
+    auto* g = new oea_graph;
+    g->ctx = ctx;
+    cudaStream_t s = ctx->stream;
+    cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+      delete g;
+      return oea_check_cuda(ctx, e, "cudaStreamBeginCapture");
+    }
+    r = decode_bf16(ctx, w, L, x_dev, mask_dev, B, rc, out_dev, s, part);
+    cudaGraph_t graph = nullptr;
+    e = cudaStreamEndCapture(s, &graph);
+    if (r || e != cudaSuccess || cudaGraphInstantiate(&g->exec, graph, 0) != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      delete g;
+      if (gs[0]) oea_graph_destroy(gs[0]);
+      return r ? r : oea_check_cuda(ctx, e == cudaSuccess ? cudaErrorUnknown : e, "stage graph");
+    }
+    g->graph = graph;
+    g->kernels = 1;
+    gs[part - 1] = g;
+  }
+  ctx->last_B = B;
+  ctx->last_N = L->N;
+  ctx->last_stride = stride_of(rc);
+  ctx->last_kind = 1;
+  *router_out = gs[0];
+  *ffn_out = gs[1];
+  return OEA_OK;
+}
+
 int oea_graph_launch(oea_graph_t g, void* stream) {
   if (g == nullptr) return fail(nullptr, OEA_ERR_INVALID_ARGUMENT, "null graph");
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : g->ctx->stream;
   OEA_CUDA_TRY(g->ctx, cudaGraphLaunch(g->exec, s));
-  g->ctx->launches += 2;
+  g->ctx->launches += g->kernels;
   return OEA_OK;
 }
 

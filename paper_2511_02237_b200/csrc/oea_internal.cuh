@@ -94,6 +94,7 @@ struct oea_graph {
   oea_ctx* ctx = nullptr;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
+  int kernels = 0;  // kernels launched per graph launch (launch accounting)
 };
 
 // Status helpers (defined in capi.cu).

@@ -22,6 +22,8 @@
 //      zero-padded bf16 copy of x the FFN streams B fragments from.
 #include <cooperative_groups.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <climits>
 
 #include "oea_device.cuh"
@@ -265,6 +267,7 @@ struct RouterParams {
   int32_t* base_union;
   int32_t* base_union_count;
   unsigned long long* trace;  // debug: rows 1000+rank of the FFN trace buffer
+  int late_trigger;           // debug: launch the FFN only at the end (OEA_LATE_TRIGGER)
 };
 
 __device__ __forceinline__ void rstamp(const RouterParams& P, int rank, int slot) {
@@ -276,219 +279,340 @@ __device__ __forceinline__ void rstamp(const RouterParams& P, int rank, int slot
 }
 
 constexpr int kRW = kRouterThreads / 32;  // 16 warps
-constexpr int kMaxKtPerWarp = 16;          // k-tiles loaded per HBM round trip
 constexpr int kXsPad = 8;                  // bf16 elements of row padding (bank spread)
+constexpr int kAStageMax = 96 * 1024;      // router A-tile staging per pass
 
-__device__ __forceinline__ float key_to_logit(uint64_t k) {
-  const uint32_t u = static_cast<uint32_t>(k >> 32);
+__device__ __forceinline__ uint32_t order_key32(float v) {
+  const uint32_t b = __float_as_uint(v == 0.0f ? 0.0f : v);
+  return (b >> 31) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float key32_to_logit(uint32_t u) {
   return __uint_as_float((u >> 31) ? (u & 0x7fffffffu) : ~u);
 }
 
-// Per-token routing state kept in registers between the two union phases.
+// Per-token ranking, register resident: lane l owns experts j*32 + l
+// (j < E) and their order keys (0 = padding / taken). The composite order of
+// routing.cpp:196-199 is (logit desc, index asc); a selection returns the best
+// remaining element with two redux.sync.max (high word = order key of the
+// logit, low word = 0xFFFF - index). Everything is force-inlined so the kernel
+// parameters stay in the constant bank and nothing spills to local memory
+// (the CTA's large shared-memory carve-out leaves little L1 for a stack).
 template <int E>
-struct TokState {
-  uint64_t k[E];
-  uint32_t id[E];
-  int n_i;
+struct TokRank {
+  uint32_t key[E];    // original order keys (0 = no element)
+  uint32_t taken;     // bit j: expert j*32 + lane selected
 };
 
 template <int E>
-__device__ __forceinline__ void tok_load_sort(const RouterParams& P, int t, TokState<E>& S) {
+__device__ __forceinline__ void tok_load(const RouterParams& P, int t, TokRank<E>& R) {
   const int lane = threadIdx.x & 31;
   const float* l = P.logits + static_cast<size_t>(t) * P.Np;
   float v[E];
 #pragma unroll
-  for (int j = 0; j < E; ++j) {
-    const int p = j * 32 + lane;
-    v[j] = p < P.N ? __ldcg(l + p) : 0.0f;
-  }
+  for (int j = 0; j < E; ++j) v[j] = (j * 32 + lane) < P.N ? __ldcg(l + j * 32 + lane) : 0.0f;
 #pragma unroll
-  for (int j = 0; j < E; ++j) {
-    const int p = j * 32 + lane;
-    S.k[j] = p < P.N ? order_key_f32(v[j]) : 0ull;
-    S.id[j] = static_cast<uint32_t>(p);
-  }
-  warp_rank_sort<E>(S.k, S.id);
+  for (int j = 0; j < E; ++j) R.key[j] = (j * 32 + lane) < P.N ? order_key32(v[j]) : 0u;
+  R.taken = 0u;
 }
 
-// Phase 1 (routing.cpp:226-268): baseline size n_i and the union bitmap.
+// mode 0: any remaining element; mode 1: members of the union bitmap `u`.
 template <int E>
-__device__ __forceinline__ void tok_phase1(const RouterParams& P, int t, TokState<E>& S,
-                                           uint32_t* s_union) {
+__device__ __forceinline__ int tok_select(const TokRank<E>& R, bool union_only, const uint32_t* u,
+                                          uint32_t& key_out) {
   const int lane = threadIdx.x & 31;
-  const Cfg& cfg = P.cfg;
-  const bool real = P.mask == nullptr || P.mask[t] != 0;
-  S.n_i = 0;
-  if (!real || cfg.mode == OEA_MODE_VANILLA) return;
-  int t_i = P.N;
-  if (cfg.p != 1.0) {
-    // Best-effort parity (documented): fp64 softmax of the fp32 logits, then
-    // the reference's sequential cumulative mass in rank order.
-    const double m = static_cast<double>(key_to_logit(__shfl_sync(kFull, S.k[0], 0)));
-    double e[E], z = 0.0;
+  uint32_t hi = 0, lo = 0;
 #pragma unroll
-    for (int j = 0; j < E; ++j) {
-      e[j] = (j * 32 + lane) < P.N ? exp(static_cast<double>(key_to_logit(S.k[j])) - m) : 0.0;
-      z += e[j];
+  for (int j = 0; j < E; ++j) {
+    const int e = j * 32 + lane;
+    const bool ok = R.key[j] != 0u && !((R.taken >> j) & 1u) &&
+                    (!union_only || ((u[e >> 5] >> (e & 31)) & 1u));
+    const uint32_t l2 = 0xFFFFu - static_cast<uint32_t>(e);
+    if (ok && (R.key[j] > hi || (R.key[j] == hi && l2 > lo))) {
+      hi = R.key[j];
+      lo = l2;
     }
+  }
+  const uint32_t whi = __reduce_max_sync(kFull, hi);
+  if (whi == 0u) return -1;
+  const uint32_t wlo = __reduce_max_sync(kFull, hi == whi ? lo : 0u);
+  key_out = whi;
+  return static_cast<int>(0xFFFFu - wlo);
+}
+
+template <int E>
+__device__ __forceinline__ void tok_take(TokRank<E>& R, int id) {
+  if ((id & 31) == (threadIdx.x & 31)) R.taken |= 1u << (id >> 5);
+}
+
+// Rank of element (key, id) in the full order (# elements before it).
+template <int E>
+__device__ __forceinline__ int tok_rank_of(const TokRank<E>& R, uint32_t key, int id) {
+  const int lane = threadIdx.x & 31;
+  int c = 0;
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const int e = j * 32 + lane;
+    c += __popc(__ballot_sync(kFull, R.key[j] != 0u && (R.key[j] > key || (R.key[j] == key && e < id))));
+  }
+  return c;
+}
+
+// Phase 1 (routing.cpp:226-268): the baseline = the first n_i = min(k0, t_i)
+// ranks; p == 1 short-circuits t_i = N. For p < 1 the cumulative mass uses an
+// fp64 softmax of the fp32 logits (documented best-effort parity).
+template <int E>
+__device__ __forceinline__ int tok_phase1(const RouterParams& P, TokRank<E>& R, uint32_t* s_union,
+                                          int* srow, float* se, float& rowmax) {
+  const int lane = threadIdx.x & 31;
+  uint32_t key = 0;
+  int id = tok_select<E>(R, false, nullptr, key);  // rank 0 anchors the weights
+  rowmax = key32_to_logit(key);
+  if (P.cfg.mode == OEA_MODE_VANILLA) return 0;
+  const bool mass_rule = P.cfg.p != 1.0;
+  double z = 0.0;
+  if (mass_rule) {
+#pragma unroll
+    for (int j = 0; j < E; ++j)
+      if (R.key[j] != 0u) z += exp(static_cast<double>(key32_to_logit(R.key[j])) - rowmax);
     for (int off = 16; off > 0; off >>= 1) z += __shfl_xor_sync(kFull, z, off);
-    double cum = 0.0;
-    bool done = false;
-    for (int j = 0; j < E && !done; ++j)
-      for (int src = 0; src < 32; ++src) {
-        const int p = j * 32 + src;
-        if (p >= P.N) {
-          done = true;
-          break;
-        }
-        cum = __dadd_rn(cum, __shfl_sync(kFull, e[j], src) / z);
-        if (cum >= cfg.p) {
-          t_i = p + 1;
-          done = true;
-          break;
-        }
-      }
   }
-  S.n_i = min(cfg.k0, t_i);
-#pragma unroll
-  for (int j = 0; j < E; ++j) {
-    const int p = j * 32 + lane;
-    if (p < S.n_i) atomicOr(&s_union[S.id[j] >> 5], 1u << (S.id[j] & 31));
+  int n = 0;
+  double cum = 0.0;
+  while (n < P.cfg.k0 && id >= 0) {
+    if (lane == 0) {
+      srow[n] = id;
+      se[n] = expf(key32_to_logit(key) - rowmax);
+      atomicOr(&s_union[id >> 5], 1u << (id & 31));
+    }
+    tok_take<E>(R, id);
+    ++n;
+    if (mass_rule) {
+      cum = __dadd_rn(cum, exp(static_cast<double>(key32_to_logit(key)) - rowmax) / z);
+      if (cum >= P.cfg.p) break;
+    }
+    if (n >= P.cfg.k0) break;
+    id = tok_select<E>(R, false, nullptr, key);
   }
+  return n;
 }
 
-// Phase 2 (routing.cpp:270-303) + weights (routing.cpp:33-49) + outputs.
-// The selected set is always in ascending rank order (baseline ranks, then
-// piggybacked ranks in scan order), so each lane knows which of its sorted
-// positions are selected and the fp64 renormalisation runs over registers.
+// Phase 2 (routing.cpp:270-303): piggyback the best union members of ranks
+// n_i..max_p-1 until the cap; vanilla takes the top k. Then weights
+// (renormalisation over the set, routing.cpp:33-49) and per-expert loads.
 template <int E>
-__device__ __forceinline__ void tok_phase2(const RouterParams& P, int t, const TokState<E>& S,
-                                           const uint32_t* s_union, int* s_sets, int* s_len) {
+__device__ __forceinline__ void tok_phase2(const RouterParams& P, int t, TokRank<E>& R, int n_i,
+                                           float rowmax, const uint32_t* s_union, int* srow,
+                                           float* se, int* s_loads, uint32_t* s_tokbits, int Bw,
+                                           int* s_len) {
   const int lane = threadIdx.x & 31;
-  const Cfg& cfg = P.cfg;
-  const bool real = P.mask == nullptr || P.mask[t] != 0;
-  bool sel[E];
-  int len = 0;
-#pragma unroll
-  for (int j = 0; j < E; ++j) sel[j] = false;
-  if (real) {
-    if (cfg.mode == OEA_MODE_VANILLA) {
-#pragma unroll
-      for (int j = 0; j < E; ++j) sel[j] = (j * 32 + lane) < cfg.k;
-      len = cfg.k;
-    } else {
-#pragma unroll
-      for (int j = 0; j < E; ++j) sel[j] = (j * 32 + lane) < S.n_i;
-      len = S.n_i;
-      if (cfg.mode != OEA_MODE_PRUNED) {
-#pragma unroll
-        for (int j = 0; j < E; ++j) {
-          const int p = j * 32 + lane;
-          const bool cand = p >= S.n_i && p < cfg.max_p && p < P.N &&
-                            ((s_union[S.id[j] >> 5] >> (S.id[j] & 31)) & 1u);
-          const unsigned m = __ballot_sync(kFull, cand);
-          const int take = max(cfg.limit - len, 0);
-          if (cand && __popc(m & lanemask_lt()) < take) sel[j] = true;
-          len += min(__popc(m), take);
-        }
+  const int stride = P.cfg.stride;
+  int len = n_i;
+  uint32_t key = 0;
+  const bool vanilla = P.cfg.mode == OEA_MODE_VANILLA;
+  if (vanilla) len = 0;
+  if (P.cfg.mode != OEA_MODE_PRUNED) {
+    const int cap = vanilla ? P.cfg.k : P.cfg.limit;
+    const bool full_scan = vanilla || P.cfg.max_p >= P.N;
+    while (len < cap) {
+      const int id = tok_select<E>(R, !vanilla, s_union, key);
+      if (id < 0) break;
+      if (!full_scan && tok_rank_of<E>(R, key, id) >= P.cfg.max_p) break;
+      if (lane == 0) {
+        srow[len] = id;
+        se[len] = expf(key32_to_logit(key) - rowmax);
       }
+      tok_take<E>(R, id);
+      ++len;
     }
   }
-  // fp64 weights: w = e / sum_set e, e = exp(l - max) (the softmax
-  // denominator cancels); sequential sum in set order by lane 0.
-  const double m = static_cast<double>(key_to_logit(__shfl_sync(kFull, S.k[0], 0)));
-  double e[E];
-#pragma unroll
-  for (int j = 0; j < E; ++j)
-    e[j] = sel[j] ? exp(static_cast<double>(key_to_logit(S.k[j])) - m) : 0.0;
-  double mass = 0.0;
-  int pos = 0;
-  int32_t* gset = P.sets + static_cast<size_t>(t) * cfg.stride;
-  int* sset = s_sets + t * cfg.stride;
-#pragma unroll
-  for (int j = 0; j < E; ++j) {
-    unsigned m2 = __ballot_sync(kFull, sel[j]);
-    // set slots of the selected positions of this j-row, in lane order
-    const int my = pos + __popc(m2 & lanemask_lt());
-    if (sel[j]) {
-      gset[my] = static_cast<int32_t>(S.id[j]);
-      sset[my] = static_cast<int>(S.id[j]);
+  __syncwarp();
+  // sequential fp32 mass in set order, then w = e / mass
+  float mass = 0.0f;
+  for (int j = 0; j < len; ++j) mass += se[j];
+  for (int j = lane; j < stride; j += 32) {
+    const size_t o = static_cast<size_t>(t) * stride + j;
+    if (j < len) {
+      const int e = srow[j];
+      const float w = se[j] / mass;
+      P.sets[o] = e;
+      P.wts32[o] = w;
+      if (P.wts64) P.wts64[o] = static_cast<double>(w);
+      atomicAdd(&s_loads[e], 1);
+      atomicOr(&s_tokbits[e * Bw + (t >> 5)], 1u << (t & 31));
+    } else {
+      P.sets[o] = -1;
+      P.wts32[o] = 0.0f;
+      if (P.wts64) P.wts64[o] = 0.0;
     }
-    while (m2) {
-      const int src = __ffs(m2) - 1;
-      m2 &= m2 - 1;
-      mass = __dadd_rn(mass, __shfl_sync(kFull, e[j], src));
-    }
-    pos += __popc(__ballot_sync(kFull, sel[j]));
-  }
-#pragma unroll
-  for (int j = 0; j < E; ++j) {
-    const unsigned m2 = __ballot_sync(kFull, sel[j]);
-    int before = 0;
-#pragma unroll
-    for (int jj = 0; jj < j; ++jj) before += __popc(__ballot_sync(kFull, sel[jj]));
-    if (sel[j]) {
-      const int slot = before + __popc(m2 & lanemask_lt());
-      const double w = e[j] / mass;
-      P.wts32[static_cast<size_t>(t) * cfg.stride + slot] = static_cast<float>(w);
-      if (P.wts64) P.wts64[static_cast<size_t>(t) * cfg.stride + slot] = w;
-    }
-  }
-  for (int j = len + lane; j < cfg.stride; j += 32) {
-    gset[j] = -1;
-    P.wts32[static_cast<size_t>(t) * cfg.stride + j] = 0.0f;
-    if (P.wts64) P.wts64[static_cast<size_t>(t) * cfg.stride + j] = 0.0;
-  }
-  // export of the full order (sort_experts) for the parity harness
-  int32_t* ord = P.order + static_cast<size_t>(t) * P.Np;
-#pragma unroll
-  for (int j = 0; j < E; ++j) {
-    const int p = j * 32 + lane;
-    if (p < P.N) ord[p] = static_cast<int32_t>(S.id[j]);
   }
   if (lane == 0) {
     P.set_len[t] = len;
     s_len[t] = len;
-    if (P.phase1_n) P.phase1_n[t] = S.n_i;
+    if (P.phase1_n) P.phase1_n[t] = n_i;
   }
 }
 
+__device__ __forceinline__ void tok_phase2_masked(const RouterParams& P, int t, int* s_len) {
+  const int lane = threadIdx.x & 31;
+  for (int j = lane; j < P.cfg.stride; j += 32) {
+    const size_t o = static_cast<size_t>(t) * P.cfg.stride + j;
+    P.sets[o] = -1;
+    P.wts32[o] = 0.0f;
+    if (P.wts64) P.wts64[o] = 0.0;
+  }
+  if (lane == 0) {
+    P.set_len[t] = 0;
+    s_len[t] = 0;
+    if (P.phase1_n) P.phase1_n[t] = 0;
+  }
+}
+
+// All tokens: phase 1 for every token (union barrier), then phase 2. With
+// one token per warp (B <= 16) the ranking stays in registers across the
+// barrier; otherwise each token is reloaded and its baseline re-marked.
 template <int E>
-__device__ void route_all(const RouterParams& P, uint32_t* s_union, int* s_sets, int* s_len,
-                          int* s_n) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+__device__ __forceinline__ void route_all(const RouterParams& P, uint32_t* s_union, int* s_sets,
+                                          float* s_e, int* s_len, int* s_n, float* s_max,
+                                          int* s_loads, uint32_t* s_tokbits) {
+  const int warp = threadIdx.x >> 5;
+  const int Bw = (P.B + 31) >> 5;
+  const int stride = P.cfg.stride;
   if (P.B <= kRW) {
-    // one token per warp: the sorted row stays in registers across the
-    // union barrier
-    TokState<E> S;
     const int t = warp;
-    if (t < P.B) {
-      tok_load_sort<E>(P, t, S);
-      tok_phase1<E>(P, t, S, s_union);
+    const bool act = t < P.B && (P.mask == nullptr || P.mask[t] != 0);
+    TokRank<E> R;
+    int n_i = 0;
+    float rowmax = 0.0f;
+    if (act) {
+      tok_load<E>(P, t, R);
+      if (t == 0) rstamp(P, 8, 0);
+      n_i = tok_phase1<E>(P, R, s_union, s_sets + t * stride, s_e + t * stride, rowmax);
+      if (t == 0) rstamp(P, 8, 1);
     }
     __syncthreads();
-    if (t < P.B) tok_phase2<E>(P, t, S, s_union, s_sets, s_len);
+    if (warp == 0) rstamp(P, 8, 2);
+    if (act)
+      tok_phase2<E>(P, t, R, n_i, rowmax, s_union, s_sets + t * stride, s_e + t * stride, s_loads,
+                    s_tokbits, Bw, s_len);
+    else if (t < P.B)
+      tok_phase2_masked(P, t, s_len);
+    if (warp == 0) rstamp(P, 8, 3);
   } else {
     for (int t = warp; t < P.B; t += kRW) {
-      TokState<E> S;
-      tok_load_sort<E>(P, t, S);
-      tok_phase1<E>(P, t, S, s_union);
-      if (lane == 0) s_n[t] = S.n_i;
+      if (P.mask != nullptr && P.mask[t] == 0) continue;
+      TokRank<E> R;
+      tok_load<E>(P, t, R);
+      float rowmax;
+      const int n_i = tok_phase1<E>(P, R, s_union, s_sets + t * stride, s_e + t * stride, rowmax);
+      if ((threadIdx.x & 31) == 0) {
+        s_n[t] = n_i;
+        s_max[t] = rowmax;
+      }
     }
     __syncthreads();
     for (int t = warp; t < P.B; t += kRW) {
-      TokState<E> S;
-      tok_load_sort<E>(P, t, S);  // re-rank (cheaper than keeping B rows)
-      S.n_i = s_n[t];
-      tok_phase2<E>(P, t, S, s_union, s_sets, s_len);
+      if (P.mask != nullptr && P.mask[t] == 0) {
+        tok_phase2_masked(P, t, s_len);
+        continue;
+      }
+      TokRank<E> R;
+      tok_load<E>(P, t, R);
+      const int n_i = s_n[t];
+      for (int j = 0; j < n_i; ++j) tok_take<E>(R, s_sets[t * stride + j]);
+      tok_phase2<E>(P, t, R, n_i, s_max[t], s_union, s_sets + t * stride, s_e + t * stride,
+                    s_loads, s_tokbits, Bw, s_len);
     }
   }
   __syncthreads();
+  if (warp == 0) rstamp(P, 8, 4);
+}
+
+// Fused-path compaction (K3) from shared memory: warp 0 scans the experts
+// (ballot prefix sums) and writes active_union / groups / padding rows; then
+// all warps place each (token, slot) at row_base[slot(e)] + rank of t among
+// the expert's tokens (token order, from the token bitmaps).
+__device__ void compact_fused(const RouterParams& P, const int* s_sets, const int* s_len,
+                              const int* s_loads, int* s_eslot, int* s_rowb,
+                              const uint32_t* s_tokbits, int* s_tmp) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int B = P.B, N = P.N, stride = P.cfg.stride;
+  const int Bw = (B + 31) >> 5;
+  if (warp == 0) {
+    int T = 0, G = 0, R = 0, load = 0;
+    for (int base = 0; base < N; base += 32) {
+      const int e = base + lane;
+      const int m = e < N ? s_loads[e] : 0;
+      const bool act = m > 0;
+      const unsigned am = __ballot_sync(kFull, act);
+      const int slot = T + __popc(am & lanemask_lt());
+      const int ng = act ? (m + kTokGroup - 1) / kTokGroup : 0;
+      const int nr = act ? (m / kTokGroup) * kTokGroup + ((m % kTokGroup) + 7) / 8 * 8 : 0;
+      int gi = ng, ri = nr, li = m;  // inclusive scans
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int g2 = __shfl_up_sync(kFull, gi, o), r2 = __shfl_up_sync(kFull, ri, o),
+                  l2 = __shfl_up_sync(kFull, li, o);
+        if (lane >= o) {
+          gi += g2;
+          ri += r2;
+          li += l2;
+        }
+      }
+      const int g0 = G + gi - ng, r0 = R + ri - nr;
+      if (e < N) {
+        P.loads[e] = m;
+        s_eslot[e] = act ? slot : -1;
+      }
+      if (act) {
+        P.active_union[slot] = e;
+        s_rowb[e] = r0;
+        for (int k = 0; k < ng; ++k) {
+          P.group_a[g0 + k] = e;
+          P.group_row0[g0 + k] = r0 + k * kTokGroup;
+          P.group_rows[g0 + k] = min(kTokGroup, m - k * kTokGroup);
+        }
+        for (int r = r0 + m; r < r0 + nr; ++r) P.row_tok[r] = -1;  // n-block padding
+      }
+      T += __popc(am);
+      G += __shfl_sync(kFull, gi, 31);
+      R += __shfl_sync(kFull, ri, 31);
+      load += __shfl_sync(kFull, li, 31);
+    }
+    for (int e = T + lane; e < N; e += 32) P.active_union[e] = -1;
+    if (lane == 0) {
+      P.hdr->n_groups = G;
+      P.hdr->T = T;
+      P.hdr->total_load = load;
+      P.hdr->n_rows = R;
+      *P.active_count = T;
+      *P.total_load = load;
+      s_tmp[0] = G;
+    }
+  } else {
+    for (int c = threadIdx.x - 32; c < P.n_counters; c += kRouterThreads - 32) P.counters[c] = 0;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < B * stride; idx += kRouterThreads) {
+    const int t = idx / stride, sl = idx % stride;
+    if (sl < s_len[t]) {
+      const int e = s_sets[idx];
+      const uint32_t* bits = s_tokbits + e * Bw;
+      int rank = __popc(bits[t >> 5] & ((1u << (t & 31)) - 1u));
+      for (int w = 0; w < (t >> 5); ++w) rank += __popc(bits[w]);
+      const int row = s_rowb[e] + rank;
+      P.row_tok[row] = t;
+      P.row_slot[row] = sl;
+    }
+  }
+  if (s_tmp[0] == 0) {
+    for (size_t f = threadIdx.x; f < static_cast<size_t>(B) * P.D; f += kRouterThreads)
+      P.out[f] = 0.0f;
+  }
 }
 
 __global__ void __cluster_dims__(kRouterCluster, 1, 1) __launch_bounds__(kRouterThreads, 1)
     k_router_fused(const RouterParams P) {
-  extern __shared__ __align__(16) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem[];
   cg::cluster_group cluster = cg::this_cluster();
   const unsigned crank = cluster.block_rank();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -496,17 +620,31 @@ __global__ void __cluster_dims__(kRouterCluster, 1, 1) __launch_bounds__(kRouter
 
   // Let the FFN grid get resident early; it waits (griddepcontrol.wait) for
   // this grid's completion before touching any of its outputs.
-  pdl_launch_dependents();
+  if (!P.late_trigger) pdl_launch_dependents();
   rstamp(P, crank, 0);
 
   const int Np = P.Np, B = P.B;
   const int KT = P.Dp >> 4, nrb = Np >> 4;
   const int kt0 = static_cast<int>(crank) * KT / kRouterCluster;
   const int kt1 = (static_cast<int>(crank) + 1) * KT / kRouterCluster;
-  const int kslice = (kt1 - kt0) * 16;
+  const int nkt = kt1 - kt0;
+  const int kslice = nkt * 16;
   const int xs_stride = kslice + kXsPad;  // bf16 elements
-  float* part = reinterpret_cast<float*>(smem);  // [kRouterTokChunk][Np]
+  // smem: [part f32 kRouterTokChunk x Np][xs bf16 kRouterTokChunk x xs_stride][A tiles][mbar]
+  float* part = reinterpret_cast<float*>(smem);
   __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(part + kRouterTokChunk * Np);
+  uint8_t* abuf = reinterpret_cast<uint8_t*>(xs) +
+                  ((static_cast<size_t>(kRouterTokChunk) * xs_stride * 2 + 127) & ~static_cast<size_t>(127));
+  // A tiles for a pass of rb_per rowblocks x nkt k-tiles
+  const int rb_per = max(1, min(nrb, kAStageMax / max(1, nkt * kTileBytes)));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(abuf + static_cast<size_t>(rb_per) * nkt * kTileBytes);
+  // x rows can be bulk-copied when every K-slice start/end is 16 B aligned in
+  // the caller's row (D % 8 == 0) and the slice lies inside D.
+  const bool x_bulk = (P.D & 7) == 0 && kt1 * 16 <= P.D;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
 
   // ---- x -> zero-padded bf16 copy for the FFN when D is not a tile multiple ----
   if (P.xpad) {
@@ -515,78 +653,88 @@ __global__ void __cluster_dims__(kRouterCluster, 1, 1) __launch_bounds__(kRouter
         P.xpad[static_cast<size_t>(t) * P.Dp + d] =
             d < P.D ? P.x[static_cast<size_t>(t) * P.D + d] : __float2bfloat16_rn(0.0f);
   }
+  __syncthreads();
 
   // ---- 1. split-K gate GEMV over the cluster ----
   const int ks_split = nrb <= kRW / 2 ? 2 : 1;
+  uint32_t bar_phase = 0;
   for (int tc = 0; tc < B; tc += kRouterTokChunk) {
     const int ntok = min(kRouterTokChunk, B - tc);
     const int nbc = (ntok + 7) >> 3;
-    // stage this CTA's K-slice of x (zero beyond D / the chunk)
     for (int i = threadIdx.x; i < kRouterTokChunk * Np; i += kRouterThreads) part[i] = 0.0f;
-    for (int i = threadIdx.x; i < nbc * 8 * (kslice >> 1); i += kRouterThreads) {
-      const int tt = i / (kslice >> 1), kk = (i % (kslice >> 1)) * 2;
-      const int k = kt0 * 16 + kk;
-      uint32_t v = 0;
-      if (tt < ntok) {
-        const __nv_bfloat16* xr = P.x + static_cast<size_t>(tc + tt) * P.D;
-        if ((P.D & 1) == 0 && k + 1 < P.D) {
-          v = __ldg(reinterpret_cast<const uint32_t*>(xr + k));
-        } else {
-          const unsigned short lo = k < P.D ? __bfloat16_as_ushort(xr[k]) : 0;
-          const unsigned short hi = k + 1 < P.D ? __bfloat16_as_ushort(xr[k + 1]) : 0;
-          v = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+    for (int rb0 = 0; rb0 < nrb; rb0 += rb_per) {
+      const int nrbp = min(rb_per, nrb - rb0);
+      // one elected thread issues every bulk copy of this pass on one mbarrier
+      if (threadIdx.x == 0) {
+        const uint64_t pol = l2_policy_evict_first();
+        uint32_t bytes = static_cast<uint32_t>(nrbp) * nkt * kTileBytes;
+        if (rb0 == 0 && x_bulk) bytes += static_cast<uint32_t>(ntok) * kslice * 2;
+        mbar_arrive_expect_tx(bar, bytes);
+        for (int r = 0; r < nrbp; ++r)
+          bulk_g2s(abuf + static_cast<size_t>(r) * nkt * kTileBytes,
+                   P.rfrag + (static_cast<size_t>(rb0 + r) * KT + kt0) * 32, nkt * kTileBytes, bar,
+                   pol);
+        if (rb0 == 0 && x_bulk)
+          for (int tt = 0; tt < ntok; ++tt)
+            bulk_g2s(xs + tt * xs_stride, P.x + static_cast<size_t>(tc + tt) * P.D + kt0 * 16,
+                     kslice * 2, bar, pol);
+      }
+      if (rb0 == 0) {
+        // zero rows beyond the chunk; generic (unaligned / ragged-D) x staging
+        for (int i = threadIdx.x; i < nbc * 8 * (kslice >> 1); i += kRouterThreads) {
+          const int tt = i / (kslice >> 1), kk = (i % (kslice >> 1)) * 2;
+          if (x_bulk && tt < ntok) continue;
+          const int k = kt0 * 16 + kk;
+          uint32_t v = 0;
+          if (tt < ntok) {
+            const __nv_bfloat16* xr = P.x + static_cast<size_t>(tc + tt) * P.D;
+            const unsigned short lo = k < P.D ? __bfloat16_as_ushort(xr[k]) : 0;
+            const unsigned short hi = k + 1 < P.D ? __bfloat16_as_ushort(xr[k + 1]) : 0;
+            v = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+          }
+          *reinterpret_cast<uint32_t*>(xs + tt * xs_stride + kk) = v;
         }
       }
-      *reinterpret_cast<uint32_t*>(xs + tt * xs_stride + kk) = v;
-    }
-    __syncthreads();
-    rstamp(P, crank, 1);
-    for (int job = warp; job < nrb * ks_split; job += kRW) {
-      const int rb = job % nrb, ks = job / nrb;
-      const int ka = kt0 + (kt1 - kt0) * ks / ks_split;
-      const int kb = kt0 + (kt1 - kt0) * (ks + 1) / ks_split;
-      float acc[8][4];
+      __syncthreads();
+      mbar_wait(bar, bar_phase);
+      bar_phase ^= 1u;
+      if (rb0 == 0) rstamp(P, crank, 1);
+      for (int job = warp; job < nrbp * ks_split; job += kRW) {
+        const int rl = job % nrbp, ks = job / nrbp;
+        const int rb = rb0 + rl;
+        const int ka = nkt * ks / ks_split, kb = nkt * (ks + 1) / ks_split;
+        float acc[8][4];
 #pragma unroll
-      for (int nb = 0; nb < 8; ++nb) acc[nb][0] = acc[nb][1] = acc[nb][2] = acc[nb][3] = 0.0f;
-      // A-tile loads of up to 16 k-tiles in flight at once (one HBM round
-      // trip per 16 k-tiles; a single trip at D <= 4096, N <= 128).
-      for (int kc = ka; kc < kb; kc += kMaxKtPerWarp) {
-        uint4 a[kMaxKtPerWarp];
+        for (int nb = 0; nb < 8; ++nb) acc[nb][0] = acc[nb][1] = acc[nb][2] = acc[nb][3] = 0.0f;
+        const uint4* at = reinterpret_cast<const uint4*>(abuf + static_cast<size_t>(rl) * nkt * kTileBytes);
+        for (int kk = ka; kk < kb; ++kk) {
+          const uint4 a = at[kk * 32 + lane];
+          const int xo = kk * 16 + 2 * q;
 #pragma unroll
-        for (int i = 0; i < kMaxKtPerWarp; ++i)
-          if (kc + i < kb)
-            a[i] = __ldg(P.rfrag + (static_cast<size_t>(rb) * KT + kc + i) * 32 + lane);
-#pragma unroll
-        for (int i = 0; i < kMaxKtPerWarp; ++i) {
-          if (kc + i < kb) {
-            const int kk = (kc + i - kt0) * 16 + 2 * q;
-#pragma unroll
-            for (int nb = 0; nb < 8; ++nb) {
-              if (nb < nbc) {
-                const __nv_bfloat16* xr = xs + (nb * 8 + gq) * xs_stride + kk;
-                const uint32_t b0 = *reinterpret_cast<const uint32_t*>(xr);
-                const uint32_t b1 = *reinterpret_cast<const uint32_t*>(xr + 8);
-                mma_bf16_16816(acc[nb], a[i], b0, b1);
-              }
+          for (int nb = 0; nb < 8; ++nb) {
+            if (nb < nbc) {
+              const __nv_bfloat16* xr = xs + (nb * 8 + gq) * xs_stride + xo;
+              mma_bf16_16816(acc[nb], a, *reinterpret_cast<const uint32_t*>(xr),
+                             *reinterpret_cast<const uint32_t*>(xr + 8));
             }
           }
         }
-      }
-      // C: rows = experts 16rb + gq (+8), cols = tokens 2q, 2q+1 of the n-block.
-      // Two K halves meet with 0 + a + b, which is order-independent.
+        // C: rows = experts 16rb + gq (+8), cols = tokens 2q, 2q+1.
+        // Two K halves meet with 0 + a + b, which is order-independent.
 #pragma unroll
-      for (int nb = 0; nb < 8; ++nb) {
-        if (nb < nbc) {
-          const int n0 = rb * 16 + gq;
-          const int t0 = nb * 8 + 2 * q;
-          atomicAdd(&part[t0 * Np + n0], acc[nb][0]);
-          atomicAdd(&part[(t0 + 1) * Np + n0], acc[nb][1]);
-          atomicAdd(&part[t0 * Np + n0 + 8], acc[nb][2]);
-          atomicAdd(&part[(t0 + 1) * Np + n0 + 8], acc[nb][3]);
+        for (int nb = 0; nb < 8; ++nb) {
+          if (nb < nbc) {
+            const int n0 = rb * 16 + gq;
+            const int t0 = nb * 8 + 2 * q;
+            atomicAdd(&part[t0 * Np + n0], acc[nb][0]);
+            atomicAdd(&part[(t0 + 1) * Np + n0], acc[nb][1]);
+            atomicAdd(&part[t0 * Np + n0 + 8], acc[nb][2]);
+            atomicAdd(&part[(t0 + 1) * Np + n0 + 8], acc[nb][3]);
+          }
         }
       }
+      __syncthreads();  // abuf reuse by the next pass
     }
-    __syncthreads();
     rstamp(P, crank, 2);
     cluster.sync();
     rstamp(P, crank, 3);
@@ -611,34 +759,32 @@ __global__ void __cluster_dims__(kRouterCluster, 1, 1) __launch_bounds__(kRouter
   rstamp(P, crank, 4);
   if (crank != 0) return;
 
-  // ---- 2. routing (CTA 0), register-resident per token ----
-  uint32_t* s_union = reinterpret_cast<uint32_t*>(smem);      // [ceil(Np/32)]
-  const int uw = (Np + 31) >> 5;
-  int* s_len = reinterpret_cast<int*>(s_union + uw);           // [B]
-  int* s_sets = s_len + B;                                     // [B][stride]
-  int* s_loads = s_sets + B * P.cfg.stride;                    // [Np]
-  int* s_eslot = s_loads + Np;
-  int* s_rowb = s_eslot + Np;
-  int* s_grpb = s_rowb + Np;
-  int* s_tmp = s_grpb + Np;                                    // [40]
-  int* s_n = s_tmp + 40;                                       // [B]
-  uint32_t* s_tokbits = reinterpret_cast<uint32_t*>(s_n + B);  // [Np][Bw]
+  // ---- 2. routing (CTA 0) ----
+  const int stride = P.cfg.stride;
   const int Bw = (B + 31) >> 5;
+  uint32_t* s_union = reinterpret_cast<uint32_t*>(smem);          // [ceil(Np/32)]
+  const int uw = (Np + 31) >> 5;
+  int* s_len = reinterpret_cast<int*>(s_union + uw);               // [B]
+  int* s_n = s_len + B;                                            // [B]
+  float* s_max = reinterpret_cast<float*>(s_n + B);                // [B]
+  int* s_sets = reinterpret_cast<int*>(s_max + B);                 // [B][stride]
+  float* s_e = reinterpret_cast<float*>(s_sets + B * stride);      // [B][stride]
+  int* s_loads = reinterpret_cast<int*>(s_e + B * stride);         // [Np]
+  int* s_eslot = s_loads + Np;                                     // [Np]
+  int* s_rowb = s_eslot + Np;                                      // [Np]
+  int* s_tmp = s_rowb + Np;                                        // [8]
+  uint32_t* s_tokbits = reinterpret_cast<uint32_t*>(s_tmp + 8);    // [Np][Bw]
   for (int i = threadIdx.x; i < uw; i += kRouterThreads) s_union[i] = 0u;
+  for (int i = threadIdx.x; i < Np; i += kRouterThreads) s_loads[i] = 0;
   for (int i = threadIdx.x; i < Np * Bw; i += kRouterThreads) s_tokbits[i] = 0u;
   __syncthreads();
-
-  if (Np <= 32)
-    route_all<1>(P, s_union, s_sets, s_len, s_n);
-  else if (Np <= 64)
-    route_all<2>(P, s_union, s_sets, s_len, s_n);
-  else if (Np <= 128)
-    route_all<4>(P, s_union, s_sets, s_len, s_n);
+  if (Np <= 128)
+    route_all<4>(P, s_union, s_sets, s_e, s_len, s_n, s_max, s_loads, s_tokbits);
   else
-    route_all<8>(P, s_union, s_sets, s_len, s_n);
-
+    route_all<8>(P, s_union, s_sets, s_e, s_len, s_n, s_max, s_loads, s_tokbits);
   rstamp(P, 0, 5);
-  if ((P.base_union || P.base_union_count) && warp == 0) {
+
+  if ((P.base_union || P.base_union_count) && warp == 1) {
     int c = 0;
     for (int base = 0; base < P.N; base += 32) {
       const int e = base + lane;
@@ -651,15 +797,8 @@ __global__ void __cluster_dims__(kRouterCluster, 1, 1) __launch_bounds__(kRouter
   }
 
   // ---- 3. compaction for the FFN (from shared memory) ----
-  CompactOut o{P.active_union, P.active_count, P.total_load, P.loads, P.row_tok, P.row_slot,
-               P.group_a, P.group_row0, P.group_rows, P.hdr, P.counters, P.n_counters};
-  compact_plan(B, P.N, P.cfg.stride, s_sets, s_len, s_loads, s_eslot, s_rowb, s_grpb, s_tokbits,
-               s_tmp, o);
+  compact_fused(P, s_sets, s_len, s_loads, s_eslot, s_rowb, s_tokbits, s_tmp);
   rstamp(P, 0, 6);
-  if (o.hdr->n_groups == 0) {
-    for (size_t f = threadIdx.x; f < static_cast<size_t>(B) * P.D; f += kRouterThreads)
-      P.out[f] = 0.0f;
-  }
 }
 
 }  // namespace oea_dev
@@ -670,11 +809,15 @@ using namespace oea_dev;
 
 size_t router_fused_smem_bytes(int B, int Np, int Dp, int stride) {
   const int KT = Dp >> 4;
-  const int kslice_max = ((KT + kRouterCluster - 1) / kRouterCluster) * 16;
-  const size_t gemv = static_cast<size_t>(kRouterTokChunk) * Np * sizeof(float) +
-                      static_cast<size_t>(kRouterTokChunk) * (kslice_max + kXsPad) * 2;
-  const size_t route = (static_cast<size_t>((Np + 31) >> 5) + 2 * B + static_cast<size_t>(B) * stride +
-                        4 * Np + 40) * 4 + static_cast<size_t>(Np) * ((B + 31) / 32) * 4;
+  const int nkt = (KT + kRouterCluster - 1) / kRouterCluster;
+  const int nrb = Np >> 4;
+  const int rb_per = std::max(1, std::min(nrb, kAStageMax / std::max(1, nkt * kTileBytes)));
+  const size_t xs = (static_cast<size_t>(kRouterTokChunk) * (nkt * 16 + kXsPad) * 2 + 127) & ~static_cast<size_t>(127);
+  const size_t gemv = static_cast<size_t>(kRouterTokChunk) * Np * sizeof(float) + xs +
+                      static_cast<size_t>(rb_per) * nkt * kTileBytes + 64;
+  const size_t route = (static_cast<size_t>((Np + 31) >> 5) + 3 * B +
+                        2 * static_cast<size_t>(B) * stride + 3 * Np + 8) * 4 +
+                       static_cast<size_t>(Np) * ((B + 31) / 32) * 4;
   return gemv > route ? gemv : route;
 }
 
@@ -714,6 +857,7 @@ int router_fused_launch(oea_ctx* ctx, const oea_layer* L, const Cfg& cfg, int B,
   P.base_union = rb.base_union;
   P.base_union_count = rb.base_union_count;
   P.trace = rb.trace;
+  P.late_trigger = getenv("OEA_LATE_TRIGGER") != nullptr;
   const size_t smem = router_fused_smem_bytes(B, L->Np, L->Dp, cfg.stride);
   OEA_CUDA_TRY(ctx, cudaFuncSetAttribute(k_router_fused,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,

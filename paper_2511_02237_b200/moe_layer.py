@@ -221,6 +221,14 @@ class DeviceMoeLayer:
                                                  C.byref(cfg.to_c()), _p(out)))
         return out
 
+    def decode_host_ptr(self, x_ptr: int, out_ptr: int, B: int, cfg: RoutingConfig, mask_ptr=None):
+        """End-to-end decode from raw host pointers (e.g. pinned torch tensors):
+        H2D of x, the fused decode, D2H of out, synchronise (oea_moe_decode_host)."""
+        self.ctx.check(lib().oea_moe_decode_host(self.ctx.h, self.h, C.c_void_p(x_ptr),
+                                                 C.c_void_p(mask_ptr) if mask_ptr else None,
+                                                 int(B), C.byref(cfg.to_c()),
+                                                 C.c_void_p(out_ptr)))
+
     def graph(self, x, cfg: RoutingConfig, out, mask=None) -> DecodeGraph:
         g = C.c_void_p()
         self.ctx.check(lib().oea_decode_graph_create(
@@ -228,6 +236,15 @@ class DeviceMoeLayer:
             C.c_void_p(_ptr(mask)) if mask is not None else None, int(x.shape[0]),
             C.byref(cfg.to_c()), C.c_void_p(_ptr(out)), C.byref(g)))
         return DecodeGraph(self, g)
+
+    def stage_graphs(self, x, cfg: RoutingConfig, out, mask=None):
+        """(router graph, FFN graph) of one decode, for per-stage timing."""
+        g1, g2 = C.c_void_p(), C.c_void_p()
+        self.ctx.check(lib().oea_decode_stage_graphs_create(
+            self.ctx.h, self.h, C.c_void_p(_ptr(x)),
+            C.c_void_p(_ptr(mask)) if mask is not None else None, int(x.shape[0]),
+            C.byref(cfg.to_c()), C.c_void_p(_ptr(out)), C.byref(g1), C.byref(g2)))
+        return DecodeGraph(self, g1), DecodeGraph(self, g2)
 
     def last_plan(self, B: int, cfg: RoutingConfig) -> dict:
         """Routing of the most recent decode: sets/weights/aggregates and the

@@ -32,4 +32,7 @@ for name, cfg in (("oea", oea.RoutingConfig.simplified(4, 8)), ("vanilla", oea.R
     print(" router CTA stamps (us from CTA0 start): start, x-staged, gemv, sync1, end-gemv, routed, compacted")
     for k in range(8):
         print("  ", k, [round((v - r0) / 1000.0, 2) if v else None for v in r[k][:7]])
+    f = buf.reshape(1024, 8)[1008].astype(np.int64)
+    print(" routing detail (us from CTA0 start): sorted, phase1, synced, phase2, route_all done:",
+          [round((v - r0) / 1000.0, 2) if v else None for v in f[:5]])
     print(" FFN first start - router CTA0 start:", (t[:, 0].min() - r0) / 1000.0)
