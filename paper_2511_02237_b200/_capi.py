@@ -10,7 +10,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "liboea_cuda.so")
+LIB_PATH = os.environ.get("OEA_LIB") or os.path.join(_HERE, "lib", "liboea_cuda.so")
 
 OEA_OK = 0
 OEA_ERR_INVALID_ARGUMENT = 1

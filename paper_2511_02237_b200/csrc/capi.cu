@@ -353,7 +353,7 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   rb.group_rows = w.group_rows;
   rb.hdr = w.hdr;
   rb.counters = w.counters;
-  rb.n_counters = w.G + L->Dp / 16 + 2;
+  rb.n_counters = w.G + L->Dp / 16 + 3;
   rb.out = static_cast<float*>(out);
   rb.phase1_n = w.n;
   rb.base_union = w.base_union;
@@ -1114,7 +1114,7 @@ int oea_moe_forward_plan_host(oea_ctx_t ctx, oea_layer_t L, const double* x, int
                                     cudaMemcpyHostToDevice, s));
   oea_host::CompactBuffers cb{w.sets, w.set_len, w.row_tok, w.row_slot, w.group_a,
                               w.group_row0, w.group_rows, w.hdr, w.counters,
-                              w.G + L->Dp / 16 + 2};
+                              w.G + L->Dp / 16 + 3};
   r = oea_host::compact_launch(ctx, B, L->N, set_stride, cb, w.tokbits, w.active_union,
                                w.active_count, s);
   if (r) return r;

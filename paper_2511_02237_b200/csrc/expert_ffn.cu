@@ -117,14 +117,16 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const uint8_t* 
     for (int nb = 0; nb < NB; ++nb)
       acc2[h2][nb][0] = acc2[h2][nb][1] = acc2[h2][nb][2] = acc2[h2][nb][3] = 0.0f;
 
-  for (int s = 0; s < nst; ++s) {
-    mbar_wait(&full[stage], phase);
-    const uint4* tiles =
-        reinterpret_cast<const uint4*>(ring + stage * kStageBytes + warp * kSlotBytes);
-    if (P.mode != 1)
+  // B fragments (x for W1, h for W2) do not depend on the streamed A tiles:
+  // for small n-block counts the next stage's fragments are loaded right after
+  // the current stage is consumed, so their latency hides behind the stage
+  // barrier wait (single register buffer, software pipelined).
+  constexpr bool kPref = NB <= 1;  // NB=2 would spill at the 168-register cap (9 warps)
+  constexpr int KB = kPref ? kKtPerSlot : 1;
+  uint32_t bf[KB][NB][2];
+  auto load_b = [&](int s) {
 #pragma unroll
-    for (int j = 0; j < kKtPerSlot; ++j) {
-      const uint4 a = tiles[j * 32 + lane];
+    for (int j = 0; j < KB; ++j) {
       const int kt = s * kKtPerSlot + j;
 #pragma unroll
       for (int nb = 0; nb < NB; ++nb) {
@@ -138,8 +140,42 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const uint8_t* 
             b1 = __ldcg(bp[nb] + kt * 8 + 4 + q);
           }
         }
-        mma_bf16_16816(acc2[j & 1][nb], a, b0, b1);
+        bf[j][nb][0] = b0;
+        bf[j][nb][1] = b1;
       }
+    }
+  };
+  const bool math = P.mode != 1;
+  if (kPref && math) load_b(0);
+
+  for (int s = 0; s < nst; ++s) {
+    mbar_wait(&full[stage], phase);
+    const uint4* tiles =
+        reinterpret_cast<const uint4*>(ring + stage * kStageBytes + warp * kSlotBytes);
+    if (math) {
+#pragma unroll
+      for (int j = 0; j < kKtPerSlot; ++j) {
+        const uint4 a = tiles[j * 32 + lane];
+        const int kt = s * kKtPerSlot + j;
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) {
+          uint32_t b0 = 0, b1 = 0;
+          if (kPref) {
+            b0 = bf[kPref ? j : 0][nb][0];
+            b1 = bf[kPref ? j : 0][nb][1];
+          } else if (bp[nb] != nullptr) {
+            if (W1) {
+              b0 = __ldg(bp[nb] + kt * 8 + q);
+              b1 = __ldg(bp[nb] + kt * 8 + 4 + q);
+            } else {
+              b0 = __ldcg(bp[nb] + kt * 8 + q);
+              b1 = __ldcg(bp[nb] + kt * 8 + 4 + q);
+            }
+          }
+          mma_bf16_16816(acc2[j & 1][nb], a, b0, b1);
+        }
+      }
+      if (kPref && s + 1 < nst) load_b(s + 1);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);
@@ -192,28 +228,7 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const uint8_t* 
         }
       }
     }
-    __syncwarp();
-    int last = 0;
-    if (lane == 0) {
-      __threadfence();
-      last = atomicAdd(&P.cnt2[U.rb], 1) == G - 1;
-    }
-    last = __shfl_sync(kFull, last, 0);
-    if (last) {
-      // Deterministic combine of this 16-column block, in set order
-      // (moe_layer.hpp:148-155): out[t][d] = sum_s w[t][s] * y[t][s][d].
-      __threadfence();
-      for (int idx = lane; idx < P.B * 16; idx += 32) {
-        const int t = idx >> 4, d = d0 + (idx & 15);
-        if (d >= P.D) continue;
-        const int len = P.set_len[t];
-        float sum = 0.0f;
-        for (int sl = 0; sl < len; ++sl)
-          sum = fmaf(P.wts[t * P.stride + sl],
-                     __ldcg(P.ybuf + (static_cast<size_t>(t) * P.stride + sl) * P.Dp + d), sum);
-        P.out[static_cast<size_t>(t) * P.D + d] = sum;
-      }
-    }
+    // y is combined by the grid-wide pass at the end of the kernel.
   }
 }
 
@@ -296,7 +311,7 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
     if (lane == 0) {
       const uint64_t pol = l2_policy_evict_first();
       bool w1_left = true;
-      for (int seq = 0;; ++seq) {
+      auto claim = [&]() {
         RoundDesc d{0, 0, 0, 0};
         if (w1_left) {
           const int r = atomicAdd(&claims[0], 1);
@@ -304,18 +319,21 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
             d.u0 = r * kFfnWarps;
             d.n = min(kFfnWarps, U1 - d.u0);
             d.kind = 1;
-          } else {
-            w1_left = false;
+            return d;
           }
+          w1_left = false;
         }
-        if (!w1_left) {
-          const int r = atomicAdd(&claims[1], 1);
-          if (r * kFfnWarps < U2) {
-            d.u0 = U1 + r * kFfnWarps;
-            d.n = min(kFfnWarps, U2 - r * kFfnWarps);
-            d.kind = 2;
-          }
+        const int r = atomicAdd(&claims[1], 1);
+        if (r * kFfnWarps < U2) {
+          d.u0 = U1 + r * kFfnWarps;
+          d.n = min(kFfnWarps, U2 - r * kFfnWarps);
+          d.kind = 2;
         }
+        return d;
+      };
+      RoundDesc next = claim();
+      for (int seq = 0;; ++seq) {
+        const RoundDesc d = next;
         mbar_wait(&empty[stage], phase ^ 1u);
         rdesc[seq & (kRoundRing - 1)] = d;
         if (d.n == 0) {
@@ -323,26 +341,22 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
           break;
         }
         const bool is1 = d.kind == 1;
-        const int nst = (is1 ? KT1 : KT2) / kKtPerSlot;
-        const uint4* src[kFfnWarps];
-        for (int w = 0; w < d.n; ++w) {
-          const int uu = d.u0 + w;
-          if (is1) {
-            const int g = uu / RB1, rb = uu % RB1;
-            src[w] = P.w1 + (static_cast<size_t>(P.group_a[g]) * RB1 + rb) * KT1 * 32;
-          } else {
-            const int v = uu - U1;
-            const int g = v / RB2, rb = v % RB2;
-            src[w] = P.w2 + (static_cast<size_t>(P.group_a[g]) * RB2 + rb) * KT2 * 32;
-          }
-        }
+        const int KT = is1 ? KT1 : KT2;
+        const int nst = KT / kKtPerSlot;
+        // The round's 8 units are 8 consecutive row blocks of one expert (RB1
+        // and RB2 are multiples of 8, rounds start at multiples of 8), stored
+        // round-interleaved: stage s is one contiguous block.
+        const int v = is1 ? d.u0 : d.u0 - U1;
+        const int RB = is1 ? RB1 : RB2;
+        const int g = v / RB, rr = (v % RB) / kFfnWarps;
+        const uint4* base = (is1 ? P.w1 : P.w2) +
+                            (static_cast<size_t>(P.group_a[g]) * RB + rr * kFfnWarps) * KT * 32;
         for (int s = 0; s < nst; ++s) {
           if (s > 0) mbar_wait(&empty[stage], phase ^ 1u);
           mbar_arrive_expect_tx(&full[stage], d.n * kSlotBytes);
-          uint8_t* dst = ring + stage * kStageBytes;
-          for (int w = 0; w < d.n; ++w)
-            bulk_g2s(dst + w * kSlotBytes, src[w] + s * kKtPerSlot * 32, kSlotBytes, &full[stage],
-                     pol);
+          bulk_g2s(ring + stage * kStageBytes, base + static_cast<size_t>(s) * kFfnWarps * kKtPerSlot * 32,
+                   d.n * kSlotBytes, &full[stage], pol);
+          if (s == 0) next = claim();  // overlap the next claim with this round
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1u;
@@ -389,6 +403,40 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
     }
   }
   if (threadIdx.x == 0) stamp(P, 3);
+
+  // ---- grid-wide deterministic combine (moe_layer.hpp:148-155) ----
+  // out[t][d] = sum_s w[t][s] * y[t][s][d] in set order. Every CTA publishes
+  // its y writes (consumer barrier + one gpu-scope release), waits until all
+  // CTAs have, then combines a contiguous slice of the B x D outputs with all
+  // slot loads of an output issued together.
+  int* done = claims + 2;
+  asm volatile("bar.sync 1, %0;" ::"r"(kFfnWarps * 32) : "memory");
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(done, 1);
+    while (ld_acquire_gpu(done) < static_cast<int>(gridDim.x)) __nanosleep(128);
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(kFfnWarps * 32) : "memory");
+  const int64_t BD = static_cast<int64_t>(P.B) * P.D;
+  const int64_t f0 = BD * blockIdx.x / gridDim.x, f1 = BD * (blockIdx.x + 1) / gridDim.x;
+  constexpr int kSlotBatch = 16;
+  for (int64_t f = f0 + threadIdx.x; f < f1; f += kFfnWarps * 32) {
+    const int t = static_cast<int>(f / P.D), d = static_cast<int>(f % P.D);
+    const int len = P.set_len[t];
+    float sum = 0.0f;
+    for (int s0 = 0; s0 < len; s0 += kSlotBatch) {
+      float y[kSlotBatch];
+#pragma unroll
+      for (int j = 0; j < kSlotBatch; ++j)
+        y[j] = s0 + j < len
+                   ? __ldcg(P.ybuf + (static_cast<size_t>(t) * P.stride + s0 + j) * P.Dp + d)
+                   : 0.0f;
+#pragma unroll
+      for (int j = 0; j < kSlotBatch; ++j)
+        if (s0 + j < len) sum = fmaf(P.wts[t * P.stride + s0 + j], y[j], sum);
+    }
+    P.out[f] = sum;
+  }
 }
 
 // ---------------------------------------------------------------------------

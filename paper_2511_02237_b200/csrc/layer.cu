@@ -7,12 +7,13 @@
 // order (lane-major, 16 B per lane), so a warp loads one tile with one
 // coalesced 16 B/lane access and no ldmatrix/shuffle:
 //   router  [Np/16][Dp/16] tiles, A(r,c) = R[d=16kt+c][n=16rb+r]
-//   W1 (e)  [Hp/8 ][Dp/16] tiles, rows 0-7 gate, 8-15 up of h = 8rb + (r&7):
+//   W1 (e)  row blocks rb < Hp/8, rows 0-7 gate, 8-15 up of h = 8rb + (r&7):
 //           A(r,c) = (r<8 ? Wg : Wu)[d=16kt+c][h]
-//   W2 (e)  [Dp/16][Hp/16] tiles, A(r,c) = Wd[h=16kt+c][d=16rb+r]
-// Each W1 row-block is one FFN "unit" (64 KiB at D=2048) and consecutive
-// row-blocks of an expert are contiguous, so a CTA's share of an expert is one
-// contiguous byte range for the TMA bulk-copy producer.
+//   W2 (e)  row blocks rb < Dp/16, A(r,c) = Wd[h=16kt+c][d=16rb+r]
+// Expert tiles are round-interleaved (round_tile): 8 row blocks (= 8 FFN
+// units, one per consumer warp) form a round, and each pipeline stage of a
+// round (8 warps x 8 k-tiles = 32 KiB) is contiguous, so the FFN producer
+// streams a stage with one TMA bulk copy.
 #include <cmath>
 #include <vector>
 
@@ -56,13 +57,23 @@ __device__ __forceinline__ size_t router_frag_idx(int d, int n, int Dp) {
   const int rb = n >> 4, r = n & 15, kt = d >> 4, c = d & 15;
   return (static_cast<size_t>(rb) * (Dp >> 4) + kt) * 256 + frag_offset(r, c);
 }
+// Expert tiles are stored round-interleaved: a round = 8 consecutive row
+// blocks (one per FFN consumer warp); inside a round the k-tiles are ordered
+// [stage][warp][k-tile within the stage's slot], so every pipeline stage of a
+// round is one contiguous kStageBytes block (a single TMA bulk copy).
+__device__ __forceinline__ size_t round_tile(int rb, int kt, int KT) {
+  const int rr = rb / kFfnWarps, w = rb % kFfnWarps;
+  const int s = kt / kKtPerSlot, j = kt % kKtPerSlot;
+  const int S = KT / kKtPerSlot;
+  return ((static_cast<size_t>(rr) * S + s) * kFfnWarps + w) * kKtPerSlot + j;
+}
 __device__ __forceinline__ size_t w1_frag_idx(int d, int h, int up, int Dp) {
   const int rb = h >> 3, r = (h & 7) + (up ? 8 : 0), kt = d >> 4, c = d & 15;
-  return (static_cast<size_t>(rb) * (Dp >> 4) + kt) * 256 + frag_offset(r, c);
+  return round_tile(rb, kt, Dp >> 4) * 256 + frag_offset(r, c);
 }
 __device__ __forceinline__ size_t w2_frag_idx(int h, int d, int Hp) {
   const int rb = d >> 4, r = d & 15, kt = h >> 4, c = h & 15;
-  return (static_cast<size_t>(rb) * (Hp >> 4) + kt) * 256 + frag_offset(r, c);
+  return round_tile(rb, kt, Hp >> 4) * 256 + frag_offset(r, c);
 }
 
 // kind: 0 router (rows=D, cols=N), 1 gate (D,H), 2 up (D,H), 3 down (H,D).

@@ -23,7 +23,10 @@ constexpr int kFfnWarps = 8;           // consumer warps per FFN CTA
 constexpr int kKtPerSlot = 8;          // k-tiles per warp per pipeline stage
 constexpr int kSlotBytes = kKtPerSlot * kTileBytes;   // 4 KiB
 constexpr int kStageBytes = kFfnWarps * kSlotBytes;   // 32 KiB
-constexpr int kStages = 6;                            // 192 KiB ring
+#ifndef OEA_FFN_STAGES
+#define OEA_FFN_STAGES 4
+#endif
+constexpr int kStages = OEA_FFN_STAGES;               // 4 x 32 KiB ring (tools/stream_bench.cu)
 constexpr int kPadD = 128;             // D padded so D/16 % 8 == 0
 constexpr int kPadH = 128;             // H padded so H/16 % 8 == 0
 constexpr int kRouterCluster = 8;      // CTAs in the fused-router cluster
