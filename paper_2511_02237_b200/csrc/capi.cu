@@ -359,6 +359,13 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   rb.base_union = w.base_union;
   rb.base_union_count = w.base_union_count;
   rb.trace = ctx->ffn_trace;
+  // Optional (OEA_FFN_ROUTES=1, B <= 64): every FFN CTA ranks the batch from
+  // the logits in its prologue (expert_ffn.cu route_prologue) and the router
+  // kernel only computes the logits. Default: the router cluster routes.
+  const bool rik = B <= kRouterTokChunk && getenv("OEA_FFN_ROUTES") != nullptr &&
+                   oea_host::ffn_bf16_smem_bytes() +
+                           oea_host::ffn_route_smem_bytes(B, L->Np, stride) <= 227 * 1024;
+  rb.logits_only = rik ? 1 : 0;
   int r = OEA_OK;
   if (part != 2) {
     if (rb.trace) OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.trace, 0, 8 * 8 * 1024, s));
@@ -383,6 +390,24 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   fb.out = out;
   fb.trace = ctx->ffn_trace;
   fb.mode = ctx->ffn_mode;
+  if (rik) {
+    fb.route_in_kernel = 1;
+    fb.logits = w.logits;
+    fb.mask = mask;
+    fb.cfg = cfg;
+    fb.x_sets = w.sets;
+    fb.x_set_len = w.set_len;
+    fb.x_w32 = w.w32;
+    fb.x_w64 = w.w64;
+    fb.x_loads = w.loads;
+    fb.x_active = w.active_union;
+    fb.x_active_count = w.active_count;
+    fb.x_total_load = w.total_load;
+    fb.x_phase1_n = w.n;
+    fb.x_base_union = w.base_union;
+    fb.x_base_union_count = w.base_union_count;
+    fb.x_hdr = w.hdr;
+  }
   return oea_host::ffn_bf16_launch(ctx, L, B, stride, fb, part == 0, s);
 }
 

@@ -36,6 +36,7 @@
 
 #include "oea_device.cuh"
 #include "oea_internal.cuh"
+#include "route_dev.cuh"
 
 namespace oea_dev {
 
@@ -59,6 +60,39 @@ struct FfnParams {
   float* out;           // [B][D]
   unsigned long long* trace;  // debug: [gridDim][8] globaltimer stamps, or null
   int mode;                   // debug: 1 = stream weights only (no math)
+  // In-kernel routing (see route_prologue).
+  int route_in_kernel;
+  const float* logits;  // [B][Np]
+  const uint8_t* mask;
+  int N, Np;
+  Cfg cfg;
+  int32_t* x_sets;
+  int32_t* x_set_len;
+  float* x_w32;
+  double* x_w64;
+  int32_t* x_loads;
+  int32_t* x_active;
+  int32_t* x_active_count;
+  int64_t* x_total_load;
+  int32_t* x_phase1_n;
+  int32_t* x_base_union;
+  int32_t* x_base_union_count;
+  FfnHeader* x_hdr;
+};
+
+// The compacted plan's tables (global from the router kernel, or this CTA's
+// shared-memory copy when the FFN routes in its prologue). Kept in shared
+// memory and read where needed so they do not occupy registers in the
+// consumer loop (the kernel runs at its 168-register cap).
+struct PlanRef {
+  const int32_t* row_tok;
+  const int32_t* row_slot;
+  const int32_t* group_a;
+  const int32_t* group_row0;
+  const int32_t* group_rows;
+  const int32_t* set_len;
+  const float* wts;
+  int G;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -78,9 +112,9 @@ struct Unit {
 };
 
 template <int NB, bool W1>
-__device__ __forceinline__ void consume_unit(const FfnParams& P, const uint8_t* ring,
-                                             uint64_t* full, uint64_t* empty, int& stage,
-                                             uint32_t& phase, int nst, const Unit& U, int G) {
+__device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* PR,
+                                             const uint8_t* ring, uint64_t* full, uint64_t* empty,
+                                             int& stage, uint32_t& phase, int nst, const Unit& U) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
   const int RB1 = P.Hp >> 3;
@@ -93,7 +127,7 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const uint8_t* 
     bp[nb] = nullptr;
     if (r < U.rows) {
       if (W1) {
-        const int t = P.row_tok[U.row0 + r];
+        const int t = PR->row_tok[U.row0 + r];
         bp[nb] = reinterpret_cast<const uint32_t*>(P.xpad + static_cast<size_t>(t) * P.Dp);
       } else {
         bp[nb] = reinterpret_cast<const uint32_t*>(P.hbuf + static_cast<size_t>(U.row0 + r) * P.Hp);
@@ -221,7 +255,7 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const uint8_t* 
         const int r = nb * 8 + 2 * q + i;
         if (r < U.rows) {
           const int row = U.row0 + r;
-          const int t = P.row_tok[row], sl = P.row_slot[row];
+          const int t = PR->row_tok[row], sl = PR->row_slot[row];
           float* y = P.ybuf + (static_cast<size_t>(t) * P.stride + sl) * P.Dp + d0;
           y[g] = acc[nb][i];
           y[g + 8] = acc[nb][2 + i];
@@ -248,18 +282,318 @@ __device__ __forceinline__ void skip_unit(uint64_t* full, uint64_t* empty, int& 
 }
 
 template <bool W1>
-__device__ __forceinline__ void dispatch_unit(int nbk, const FfnParams& P, const uint8_t* ring,
-                                              uint64_t* full, uint64_t* empty, int& stage,
-                                              uint32_t& phase, int nst, const Unit& U, int G) {
+__device__ __forceinline__ void dispatch_unit(int nbk, const FfnParams& P, const PlanRef* PR,
+                                              const uint8_t* ring, uint64_t* full, uint64_t* empty,
+                                              int& stage, uint32_t& phase, int nst, const Unit& U) {
   switch (nbk) {
-    case 1: consume_unit<1, W1>(P, ring, full, empty, stage, phase, nst, U, G); break;
-    case 2: consume_unit<2, W1>(P, ring, full, empty, stage, phase, nst, U, G); break;
-    case 3: consume_unit<3, W1>(P, ring, full, empty, stage, phase, nst, U, G); break;
-    case 4: consume_unit<4, W1>(P, ring, full, empty, stage, phase, nst, U, G); break;
+    case 1: consume_unit<1, W1>(P, PR, ring, full, empty, stage, phase, nst, U); break;
+    case 2: consume_unit<2, W1>(P, PR, ring, full, empty, stage, phase, nst, U); break;
+    case 3: consume_unit<3, W1>(P, PR, ring, full, empty, stage, phase, nst, U); break;
+    case 4: consume_unit<4, W1>(P, PR, ring, full, empty, stage, phase, nst, U); break;
     case 5:
-    case 6: consume_unit<6, W1>(P, ring, full, empty, stage, phase, nst, U, G); break;
-    default: consume_unit<8, W1>(P, ring, full, empty, stage, phase, nst, U, G); break;
+    case 6: consume_unit<6, W1>(P, PR, ring, full, empty, stage, phase, nst, U); break;
+    default: consume_unit<8, W1>(P, PR, ring, full, empty, stage, phase, nst, U); break;
   }
+}
+
+// ---------------------------------------------------------------------------
+// In-kernel routing (B <= 64): every CTA ranks the whole batch from the router
+// logits in shared memory — phase 1 (routing.cpp:226-268) for all tokens, the
+// union, then phase 2 (routing.cpp:270-303), fp32 renormalisation
+// (routing.cpp:33-49) and the compaction (one token group per active expert).
+// All CTAs compute the identical plan (deterministic code on identical
+// inputs), so no cross-CTA exchange or plan round trip through HBM is needed,
+// and each CTA's producer starts streaming as soon as its union is known.
+// ---------------------------------------------------------------------------
+struct RouteSmem {
+  size_t lg, uni, sets, e, len, n, mx, loads, tokbits, active, eslot, rowb, rows, rtok, rslot, misc,
+      total;
+};
+
+__host__ __device__ inline RouteSmem route_smem_layout(int B, int Np, int stride) {
+  RouteSmem L;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o = (o + bytes + 15) & ~static_cast<size_t>(15);
+    return at;
+  };
+  const int Bw = (B + 31) >> 5, uw = (Np + 31) >> 5;
+  const int rmax = B * stride + 8 * Np;
+  L.lg = take(static_cast<size_t>(B) * Np * 4);
+  L.uni = take(uw * 4);
+  L.sets = take(static_cast<size_t>(B) * stride * 4);
+  L.e = take(static_cast<size_t>(B) * stride * 4);
+  L.len = take(B * 4);
+  L.n = take(B * 4);
+  L.mx = take(B * 4);
+  L.loads = take(Np * 4);
+  L.tokbits = take(static_cast<size_t>(Np) * Bw * 4);
+  L.active = take(Np * 4);
+  L.eslot = take(Np * 4);
+  L.rowb = take(Np * 4);
+  L.rows = take(Np * 4);
+  L.rtok = take(rmax * 4);
+  L.rslot = take(rmax * 4);
+  L.misc = take(8 * 4);
+  L.total = o;
+  return L;
+}
+
+template <int E>
+__device__ __forceinline__ void route_phase1_tok(const FfnParams& P, int t, uint8_t* rs,
+                                                 const RouteSmem& L) {
+  const int lane = threadIdx.x & 31;
+  const int stride = P.cfg.stride;
+  float* lg = reinterpret_cast<float*>(rs + L.lg) + t * P.Np;
+  int* srow = reinterpret_cast<int*>(rs + L.sets) + t * stride;
+  float* se = reinterpret_cast<float*>(rs + L.e) + t * stride;
+  uint32_t* uni = reinterpret_cast<uint32_t*>(rs + L.uni);
+  TokRank<E> R;
+  tok_load<E>(P.N, lg, R);
+  uint32_t key = 0;
+  int id = tok_select<E>(R, false, nullptr, key);
+  const float rowmax = key32_to_logit(key);
+  int n = 0;
+  if (P.cfg.mode != OEA_MODE_VANILLA) {
+    const bool mass_rule = P.cfg.p != 1.0;
+    double z = 0.0, cum = 0.0;
+    if (mass_rule) {
+      // documented best-effort parity: fp64 softmax of the fp32 logits
+#pragma unroll
+      for (int j = 0; j < E; ++j)
+        if (R.key[j] != 0u) z += exp(static_cast<double>(key32_to_logit(R.key[j])) - rowmax);
+      for (int off = 16; off > 0; off >>= 1) z += __shfl_xor_sync(kFull, z, off);
+    }
+    while (n < P.cfg.k0 && id >= 0) {
+      if (lane == 0) {
+        srow[n] = id;
+        se[n] = expf(key32_to_logit(key) - rowmax);
+        atomicOr(&uni[id >> 5], 1u << (id & 31));
+      }
+      tok_take<E>(R, id);
+      ++n;
+      if (mass_rule) {
+        cum = __dadd_rn(cum, exp(static_cast<double>(key32_to_logit(key)) - rowmax) / z);
+        if (cum >= P.cfg.p) break;
+      }
+      if (n >= P.cfg.k0) break;
+      id = tok_select<E>(R, false, nullptr, key);
+    }
+  }
+  if (lane == 0) {
+    reinterpret_cast<int*>(rs + L.n)[t] = n;
+    reinterpret_cast<float*>(rs + L.mx)[t] = rowmax;
+  }
+}
+
+template <int E>
+__device__ __forceinline__ void route_phase2_tok(const FfnParams& P, int t, uint8_t* rs,
+                                                 const RouteSmem& L, bool exporter) {
+  const int lane = threadIdx.x & 31;
+  const int stride = P.cfg.stride;
+  const int Bw = (P.B + 31) >> 5;
+  float* lg = reinterpret_cast<float*>(rs + L.lg) + t * P.Np;
+  int* srow = reinterpret_cast<int*>(rs + L.sets) + t * stride;
+  float* se = reinterpret_cast<float*>(rs + L.e) + t * stride;
+  const uint32_t* uni = reinterpret_cast<const uint32_t*>(rs + L.uni);
+  int* loads = reinterpret_cast<int*>(rs + L.loads);
+  uint32_t* tokbits = reinterpret_cast<uint32_t*>(rs + L.tokbits);
+  const int n_i = reinterpret_cast<const int*>(rs + L.n)[t];
+  const float rowmax = reinterpret_cast<const float*>(rs + L.mx)[t];
+  TokRank<E> R;
+  tok_load<E>(P.N, lg, R);
+  for (int j = 0; j < n_i; ++j) tok_take<E>(R, srow[j]);
+  int len = n_i;
+  uint32_t key = 0;
+  const bool vanilla = P.cfg.mode == OEA_MODE_VANILLA;
+  if (vanilla) len = 0;
+  if (P.cfg.mode != OEA_MODE_PRUNED) {
+    const int cap = vanilla ? P.cfg.k : P.cfg.limit;
+    const bool full_scan = vanilla || P.cfg.max_p >= P.N;
+    while (len < cap) {
+      const int id = tok_select<E>(R, !vanilla, uni, key);
+      if (id < 0) break;
+      if (!full_scan && tok_rank_of<E>(R, key, id) >= P.cfg.max_p) break;
+      if (lane == 0) {
+        srow[len] = id;
+        se[len] = expf(key32_to_logit(key) - rowmax);
+      }
+      tok_take<E>(R, id);
+      ++len;
+    }
+  }
+  __syncwarp();
+  float mass = 0.0f;  // sequential fp32 mass in set order
+  for (int j = 0; j < len; ++j) mass += se[j];
+  __syncwarp();
+  for (int j = lane; j < stride; j += 32) {
+    float w = 0.0f;
+    if (j < len) {
+      const int e = srow[j];
+      w = se[j] / mass;
+      se[j] = w;
+      atomicAdd(&loads[e], 1);
+      atomicOr(&tokbits[e * Bw + (t >> 5)], 1u << (t & 31));
+    } else {
+      se[j] = 0.0f;
+    }
+    if (exporter) {
+      const size_t o = static_cast<size_t>(t) * stride + j;
+      P.x_sets[o] = j < len ? srow[j] : -1;
+      P.x_w32[o] = w;
+      if (P.x_w64) P.x_w64[o] = static_cast<double>(w);
+    }
+  }
+  if (lane == 0) {
+    reinterpret_cast<int*>(rs + L.len)[t] = len;
+    if (exporter) {
+      P.x_set_len[t] = len;
+      if (P.x_phase1_n) P.x_phase1_n[t] = n_i;
+    }
+  }
+}
+
+// Returns the number of token groups (= active experts).
+__device__ __forceinline__ int route_prologue(const FfnParams& P, uint8_t* rs, const RouteSmem& L) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int B = P.B, Np = P.Np, N = P.N, stride = P.cfg.stride;
+  const int nthreads = (kFfnWarps + 1) * 32;
+  const int Bw = (B + 31) >> 5;
+  float* lg = reinterpret_cast<float*>(rs + L.lg);
+  uint32_t* uni = reinterpret_cast<uint32_t*>(rs + L.uni);
+  int* loads = reinterpret_cast<int*>(rs + L.loads);
+  uint32_t* tokbits = reinterpret_cast<uint32_t*>(rs + L.tokbits);
+  int* len = reinterpret_cast<int*>(rs + L.len);
+  int* active = reinterpret_cast<int*>(rs + L.active);
+  int* misc = reinterpret_cast<int*>(rs + L.misc);
+  const bool exporter = blockIdx.x == 0;
+  for (int i = threadIdx.x; i < B * Np; i += nthreads) lg[i] = __ldcg(P.logits + i);
+  for (int i = threadIdx.x; i < ((Np + 31) >> 5); i += nthreads) uni[i] = 0u;
+  for (int i = threadIdx.x; i < Np; i += nthreads) loads[i] = 0;
+  for (int i = threadIdx.x; i < Np * Bw; i += nthreads) tokbits[i] = 0u;
+  __syncthreads();
+  // phase 1 for every real token (all 9 warps)
+  for (int t = warp; t < B; t += kFfnWarps + 1) {
+    if (P.mask != nullptr && P.mask[t] == 0) {
+      if (lane == 0) reinterpret_cast<int*>(rs + L.n)[t] = 0;
+      continue;
+    }
+    if (Np <= 128)
+      route_phase1_tok<4>(P, t, rs, L);
+    else
+      route_phase1_tok<8>(P, t, rs, L);
+  }
+  __syncthreads();
+  // active experts = the union (OEA conservation; vanilla: phase 2 decides,
+  // so vanilla plans are compacted after phase 2 below)
+  const bool union_is_active = P.cfg.mode != OEA_MODE_VANILLA;
+  // phase 2 (all warps) — cheap; keeps the code path single
+  for (int t = warp; t < B; t += kFfnWarps + 1) {
+    if (P.mask != nullptr && P.mask[t] == 0) {
+      if (lane == 0) len[t] = 0;
+      if (exporter)
+        for (int j = lane; j < stride; j += 32) {
+          const size_t o = static_cast<size_t>(t) * stride + j;
+          P.x_sets[o] = -1;
+          P.x_w32[o] = 0.0f;
+          if (P.x_w64) P.x_w64[o] = 0.0;
+          if (j == 0) {
+            P.x_set_len[t] = 0;
+            if (P.x_phase1_n) P.x_phase1_n[t] = 0;
+          }
+        }
+      continue;
+    }
+    if (Np <= 128)
+      route_phase2_tok<4>(P, t, rs, L, exporter);
+    else
+      route_phase2_tok<8>(P, t, rs, L, exporter);
+  }
+  (void)union_is_active;
+  __syncthreads();
+  // compaction: warp 0 scans the experts (ascending), groups = active experts
+  if (warp == 0) {
+    int* eslot = reinterpret_cast<int*>(rs + L.eslot);
+    int* rowb = reinterpret_cast<int*>(rs + L.rowb);
+    int* rows = reinterpret_cast<int*>(rs + L.rows);
+    int* rtok = reinterpret_cast<int*>(rs + L.rtok);
+    int T = 0, R = 0, load = 0;
+    for (int base = 0; base < N; base += 32) {
+      const int e = base + lane;
+      const int m = e < N ? loads[e] : 0;
+      const bool act = m > 0;
+      const unsigned am = __ballot_sync(kFull, act);
+      const int slot = T + __popc(am & lanemask_lt());
+      const int nr = act ? (m + 7) / 8 * 8 : 0;
+      int ri = nr, li = m;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int r2 = __shfl_up_sync(kFull, ri, o), l2 = __shfl_up_sync(kFull, li, o);
+        if (lane >= o) {
+          ri += r2;
+          li += l2;
+        }
+      }
+      const int r0 = R + ri - nr;
+      if (e < N) eslot[e] = act ? slot : -1;
+      if (act) {
+        active[slot] = e;
+        rowb[slot] = r0;
+        rows[slot] = m;
+        for (int r = r0 + m; r < r0 + nr; ++r) rtok[r] = -1;
+      }
+      if (exporter && e < N) P.x_loads[e] = m;
+      if (exporter && act) P.x_active[slot] = e;
+      T += __popc(am);
+      R += __shfl_sync(kFull, ri, 31);
+      load += __shfl_sync(kFull, li, 31);
+    }
+    if (lane == 0) misc[0] = T;
+    if (exporter) {
+      for (int e = T + lane; e < N; e += 32) P.x_active[e] = -1;
+      if (lane == 0) {
+        *P.x_active_count = T;
+        *P.x_total_load = load;
+        P.x_hdr->n_groups = T;
+        P.x_hdr->T = T;
+        P.x_hdr->total_load = load;
+        P.x_hdr->n_rows = R;
+      }
+    }
+  } else if (warp == 1 && exporter && (P.x_base_union || P.x_base_union_count)) {
+    int c = 0;
+    for (int base = 0; base < N; base += 32) {
+      const int e = base + lane;
+      const bool f = e < N && ((uni[e >> 5] >> (e & 31)) & 1u);
+      const unsigned m = __ballot_sync(kFull, f);
+      if (f && P.x_base_union) P.x_base_union[c + __popc(m & lanemask_lt())] = e;
+      c += __popc(m);
+    }
+    if (lane == 0 && P.x_base_union_count) *P.x_base_union_count = c;
+  }
+  __syncthreads();
+  {
+    const int* sets = reinterpret_cast<const int*>(rs + L.sets);
+    const int* eslot = reinterpret_cast<const int*>(rs + L.eslot);
+    const int* rowb = reinterpret_cast<const int*>(rs + L.rowb);
+    int* rtok = reinterpret_cast<int*>(rs + L.rtok);
+    int* rslot = reinterpret_cast<int*>(rs + L.rslot);
+    for (int idx = threadIdx.x; idx < B * stride; idx += nthreads) {
+      const int t = idx / stride, sl = idx % stride;
+      if (sl < len[t]) {
+        const int e = sets[idx];
+        const uint32_t* bits = tokbits + e * Bw;
+        int rank = __popc(bits[t >> 5] & ((1u << (t & 31)) - 1u));
+        for (int w = 0; w < (t >> 5); ++w) rank += __popc(bits[w]);
+        const int row = rowb[eslot[e]] + rank;
+        rtok[row] = t;
+        rslot[row] = sl;
+      }
+    }
+  }
+  __syncthreads();
+  return misc[0];
 }
 
 // Round descriptor published by the producer through the stage barrier.
@@ -291,8 +625,38 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
   pdl_wait();
   if (threadIdx.x == 0) stamp(P, 0);
 
-  const int G = P.hdr->n_groups;
-  if (G == 0) return;
+  PlanRef* PR = reinterpret_cast<PlanRef*>(rdesc + kRoundRing);
+  uint8_t* rs = reinterpret_cast<uint8_t*>(PR + 1);
+  const RouteSmem RL = route_smem_layout(P.B, P.Np, P.stride);
+  if (P.route_in_kernel) {
+    const int g = route_prologue(P, rs, RL);
+    if (threadIdx.x == 0) {
+      PR->row_tok = reinterpret_cast<const int32_t*>(rs + RL.rtok);
+      PR->row_slot = reinterpret_cast<const int32_t*>(rs + RL.rslot);
+      PR->group_a = reinterpret_cast<const int32_t*>(rs + RL.active);
+      PR->group_row0 = reinterpret_cast<const int32_t*>(rs + RL.rowb);
+      PR->group_rows = reinterpret_cast<const int32_t*>(rs + RL.rows);
+      PR->set_len = reinterpret_cast<const int32_t*>(rs + RL.len);
+      PR->wts = reinterpret_cast<const float*>(rs + RL.e);
+      PR->G = g;
+    }
+  } else if (threadIdx.x == 0) {
+    PR->row_tok = P.row_tok;
+    PR->row_slot = P.row_slot;
+    PR->group_a = P.group_a;
+    PR->group_row0 = P.group_row0;
+    PR->group_rows = P.group_rows;
+    PR->set_len = P.set_len;
+    PR->wts = P.wts;
+    PR->G = P.hdr->n_groups;
+  }
+  __syncthreads();
+  const int G = PR->G;
+  if (G == 0) {
+    if (P.route_in_kernel && blockIdx.x == 0)
+      for (int f = threadIdx.x; f < P.B * P.D; f += (kFfnWarps + 1) * 32) P.out[f] = 0.0f;
+    return;
+  }
   const int KT1 = P.Dp >> 4, KT2 = P.Hp >> 4;
   const int RB1 = P.Hp >> 3, RB2 = P.Dp >> 4;
   const int U1 = G * RB1, U2 = G * RB2;
@@ -350,7 +714,7 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
         const int RB = is1 ? RB1 : RB2;
         const int g = v / RB, rr = (v % RB) / kFfnWarps;
         const uint4* base = (is1 ? P.w1 : P.w2) +
-                            (static_cast<size_t>(P.group_a[g]) * RB + rr * kFfnWarps) * KT * 32;
+                            (static_cast<size_t>(PR->group_a[g]) * RB + rr * kFfnWarps) * KT * 32;
         for (int s = 0; s < nst; ++s) {
           if (s > 0) mbar_wait(&empty[stage], phase ^ 1u);
           mbar_arrive_expect_tx(&full[stage], d.n * kSlotBytes);
@@ -391,13 +755,13 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
         U.g = v / RB2;
         U.rb = v % RB2;
       }
-      U.row0 = P.group_row0[U.g];
-      U.rows = P.group_rows[U.g];
+      U.row0 = PR->group_row0[U.g];
+      U.rows = PR->group_rows[U.g];
       const int nbk = (U.rows + 7) >> 3;
       if (is1)
-        dispatch_unit<true>(nbk, P, ring, full, empty, stage, phase, nst, U, G);
+        dispatch_unit<true>(nbk, P, PR, ring, full, empty, stage, phase, nst, U);
       else
-        dispatch_unit<false>(nbk, P, ring, full, empty, stage, phase, nst, U, G);
+        dispatch_unit<false>(nbk, P, PR, ring, full, empty, stage, phase, nst, U);
     } else {
       skip_unit(full, empty, stage, phase, nst);
     }
@@ -422,7 +786,7 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
   constexpr int kSlotBatch = 16;
   for (int64_t f = f0 + threadIdx.x; f < f1; f += kFfnWarps * 32) {
     const int t = static_cast<int>(f / P.D), d = static_cast<int>(f % P.D);
-    const int len = P.set_len[t];
+    const int len = PR->set_len[t];
     float sum = 0.0f;
     for (int s0 = 0; s0 < len; s0 += kSlotBatch) {
       float y[kSlotBatch];
@@ -433,7 +797,7 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
                    : 0.0f;
 #pragma unroll
       for (int j = 0; j < kSlotBatch; ++j)
-        if (s0 + j < len) sum = fmaf(P.wts[t * P.stride + s0 + j], y[j], sum);
+        if (s0 + j < len) sum = fmaf(PR->wts[t * P.stride + s0 + j], y[j], sum);
     }
     P.out[f] = sum;
   }
@@ -556,7 +920,12 @@ namespace oea_host {
 using namespace oea_dev;
 
 size_t ffn_bf16_smem_bytes() {
-  return kStages * kStageBytes + 2 * kStages * sizeof(uint64_t) + kRoundRing * sizeof(RoundDesc);
+  return kStages * kStageBytes + 2 * kStages * sizeof(uint64_t) + kRoundRing * sizeof(RoundDesc) +
+         sizeof(PlanRef);
+}
+
+size_t ffn_route_smem_bytes(int B, int Np, int stride) {
+  return route_smem_layout(B, Np, stride).total;
 }
 
 int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const FfnBuffers& fb,
@@ -585,14 +954,29 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   P.out = static_cast<float*>(fb.out);
   P.trace = fb.trace;
   P.mode = fb.mode;
+  P.route_in_kernel = fb.route_in_kernel;
+  P.logits = fb.logits;
+  P.mask = fb.mask;
+  P.N = L->N;
+  P.Np = L->Np;
+  P.cfg = fb.cfg;
+  P.x_sets = fb.x_sets;
+  P.x_set_len = fb.x_set_len;
+  P.x_w32 = fb.x_w32;
+  P.x_w64 = fb.x_w64;
+  P.x_loads = fb.x_loads;
+  P.x_active = fb.x_active;
+  P.x_active_count = fb.x_active_count;
+  P.x_total_load = fb.x_total_load;
+  P.x_phase1_n = fb.x_phase1_n;
+  P.x_base_union = fb.x_base_union;
+  P.x_base_union_count = fb.x_base_union_count;
+  P.x_hdr = fb.x_hdr;
 
-  static bool attr_set = false;
-  const size_t smem = ffn_bf16_smem_bytes();
-  if (!attr_set) {
-    OEA_CUDA_TRY(ctx, cudaFuncSetAttribute(k_ffn_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(smem)));
-    attr_set = true;
-  }
+  const size_t smem = ffn_bf16_smem_bytes() +
+                      (fb.route_in_kernel ? ffn_route_smem_bytes(B, L->Np, stride) : 0);
+  OEA_CUDA_TRY(ctx, cudaFuncSetAttribute(k_ffn_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ctx->num_sms);
   cfg.blockDim = dim3((kFfnWarps + 1) * 32);

@@ -191,7 +191,26 @@ struct FfnBuffers {
   void* out;               // [B][D] f32 (bf16 path) / f64 (simt)
   unsigned long long* trace = nullptr;  // debug timeline (OEA_FFN_TRACE)
   int mode = 0;                         // debug mode (OEA_FFN_MODE)
+  // In-kernel routing (B small): the FFN routes the batch from the logits in
+  // its prologue; the plan is exported by CTA 0.
+  int route_in_kernel = 0;
+  const float* logits = nullptr;        // [B][Np]
+  const uint8_t* mask = nullptr;
+  oea_dev::Cfg cfg{};
+  int32_t* x_sets = nullptr;
+  int32_t* x_set_len = nullptr;
+  float* x_w32 = nullptr;
+  double* x_w64 = nullptr;
+  int32_t* x_loads = nullptr;
+  int32_t* x_active = nullptr;
+  int32_t* x_active_count = nullptr;
+  int64_t* x_total_load = nullptr;
+  int32_t* x_phase1_n = nullptr;
+  int32_t* x_base_union = nullptr;
+  int32_t* x_base_union_count = nullptr;
+  oea_dev::FfnHeader* x_hdr = nullptr;
 };
+size_t ffn_route_smem_bytes(int B, int Np, int stride);
 size_t ffn_bf16_smem_bytes();
 int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride,
                     const FfnBuffers& fb, bool pdl, cudaStream_t s);
@@ -226,6 +245,7 @@ struct FusedRouterBuffers {
   int32_t* base_union;      // [N] may be null
   int32_t* base_union_count;
   unsigned long long* trace = nullptr;
+  int logits_only = 0;
 };
 size_t router_fused_smem_bytes(int B, int Np, int Dp, int stride);
 int router_fused_launch(oea_ctx* ctx, const oea_layer* L, const oea_dev::Cfg& cfg, int B,

@@ -28,6 +28,7 @@
 
 #include "oea_device.cuh"
 #include "oea_internal.cuh"
+#include "route_dev.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -268,6 +269,7 @@ struct RouterParams {
   int32_t* base_union_count;
   unsigned long long* trace;  // debug: rows 1000+rank of the FFN trace buffer
   int late_trigger;           // debug: launch the FFN only at the end (OEA_LATE_TRIGGER)
+  int logits_only;            // 1: only the GEMV (the FFN routes in its prologue)
 };
 
 __device__ __forceinline__ void rstamp(const RouterParams& P, int rank, int slot) {
@@ -280,88 +282,15 @@ __device__ __forceinline__ void rstamp(const RouterParams& P, int rank, int slot
 
 constexpr int kRW = kRouterThreads / 32;  // 16 warps
 constexpr int kXsPad = 8;                  // bf16 elements of row padding (bank spread)
-constexpr int kAStageMax = 96 * 1024;      // router A-tile staging per pass
-
-__device__ __forceinline__ uint32_t order_key32(float v) {
-  const uint32_t b = __float_as_uint(v == 0.0f ? 0.0f : v);
-  return (b >> 31) ? ~b : (b | 0x80000000u);
-}
-__device__ __forceinline__ float key32_to_logit(uint32_t u) {
-  return __uint_as_float((u >> 31) ? (u & 0x7fffffffu) : ~u);
-}
-
-// Per-token ranking, register resident: lane l owns experts j*32 + l
-// (j < E) and their order keys (0 = padding / taken). The composite order of
-// routing.cpp:196-199 is (logit desc, index asc); a selection returns the best
-// remaining element with two redux.sync.max (high word = order key of the
-// logit, low word = 0xFFFF - index). Everything is force-inlined so the kernel
-// parameters stay in the constant bank and nothing spills to local memory
-// (the CTA's large shared-memory carve-out leaves little L1 for a stack).
-template <int E>
-struct TokRank {
-  uint32_t key[E];    // original order keys (0 = no element)
-  uint32_t taken;     // bit j: expert j*32 + lane selected
-};
-
-template <int E>
-__device__ __forceinline__ void tok_load(const RouterParams& P, int t, TokRank<E>& R) {
-  const int lane = threadIdx.x & 31;
-  const float* l = P.logits + static_cast<size_t>(t) * P.Np;
-  float v[E];
-#pragma unroll
-  for (int j = 0; j < E; ++j) v[j] = (j * 32 + lane) < P.N ? __ldcg(l + j * 32 + lane) : 0.0f;
-#pragma unroll
-  for (int j = 0; j < E; ++j) R.key[j] = (j * 32 + lane) < P.N ? order_key32(v[j]) : 0u;
-  R.taken = 0u;
-}
-
-// mode 0: any remaining element; mode 1: members of the union bitmap `u`.
-template <int E>
-__device__ __forceinline__ int tok_select(const TokRank<E>& R, bool union_only, const uint32_t* u,
-                                          uint32_t& key_out) {
-  const int lane = threadIdx.x & 31;
-  uint32_t hi = 0, lo = 0;
-#pragma unroll
-  for (int j = 0; j < E; ++j) {
-    const int e = j * 32 + lane;
-    const bool ok = R.key[j] != 0u && !((R.taken >> j) & 1u) &&
-                    (!union_only || ((u[e >> 5] >> (e & 31)) & 1u));
-    const uint32_t l2 = 0xFFFFu - static_cast<uint32_t>(e);
-    if (ok && (R.key[j] > hi || (R.key[j] == hi && l2 > lo))) {
-      hi = R.key[j];
-      lo = l2;
-    }
-  }
-  const uint32_t whi = __reduce_max_sync(kFull, hi);
-  if (whi == 0u) return -1;
-  const uint32_t wlo = __reduce_max_sync(kFull, hi == whi ? lo : 0u);
-  key_out = whi;
-  return static_cast<int>(0xFFFFu - wlo);
-}
-
-template <int E>
-__device__ __forceinline__ void tok_take(TokRank<E>& R, int id) {
-  if ((id & 31) == (threadIdx.x & 31)) R.taken |= 1u << (id >> 5);
-}
-
-// Rank of element (key, id) in the full order (# elements before it).
-template <int E>
-__device__ __forceinline__ int tok_rank_of(const TokRank<E>& R, uint32_t key, int id) {
-  const int lane = threadIdx.x & 31;
-  int c = 0;
-#pragma unroll
-  for (int j = 0; j < E; ++j) {
-    const int e = j * 32 + lane;
-    c += __popc(__ballot_sync(kFull, R.key[j] != 0u && (R.key[j] > key || (R.key[j] == key && e < id))));
-  }
-  return c;
-}
+constexpr int kAStageMax = 64 * 1024;      // router A-tile staging per pass
 
 // Phase 1 (routing.cpp:226-268): the baseline = the first n_i = min(k0, t_i)
 // ranks; p == 1 short-circuits t_i = N. For p < 1 the cumulative mass uses an
-// fp64 softmax of the fp32 logits (documented best-effort parity).
+// fp64 softmax of the fp32 logits (documented best-effort parity). The
+// baseline experts are OR-ed into the cluster's union bitmap (DSMEM atomics on
+// CTA 0's copy).
 template <int E>
-__device__ __forceinline__ int tok_phase1(const RouterParams& P, TokRank<E>& R, uint32_t* s_union,
+__device__ __forceinline__ int tok_phase1(const RouterParams& P, TokRank<E>& R, uint32_t* g_union,
                                           int* srow, float* se, float& rowmax) {
   const int lane = threadIdx.x & 31;
   uint32_t key = 0;
@@ -382,7 +311,7 @@ __device__ __forceinline__ int tok_phase1(const RouterParams& P, TokRank<E>& R, 
     if (lane == 0) {
       srow[n] = id;
       se[n] = expf(key32_to_logit(key) - rowmax);
-      atomicOr(&s_union[id >> 5], 1u << (id & 31));
+      atomicOr(&g_union[id >> 5], 1u << (id & 31));
     }
     tok_take<E>(R, id);
     ++n;
@@ -398,12 +327,21 @@ __device__ __forceinline__ int tok_phase1(const RouterParams& P, TokRank<E>& R, 
 
 // Phase 2 (routing.cpp:270-303): piggyback the best union members of ranks
 // n_i..max_p-1 until the cap; vanilla takes the top k. Then weights
-// (renormalisation over the set, routing.cpp:33-49) and per-expert loads.
+// (renormalisation over the set, routing.cpp:33-49); the set, its length and
+// the per-expert load / token-bitmap updates go to CTA 0 (DSMEM) for the
+// compaction.
+struct Gather {
+  int* sets;           // CTA 0: [B][stride]
+  int* len;            // CTA 0: [B]
+  int* loads;          // CTA 0: [Np]
+  uint32_t* tokbits;   // CTA 0: [Np][Bw]
+  int Bw;
+};
+
 template <int E>
 __device__ __forceinline__ void tok_phase2(const RouterParams& P, int t, TokRank<E>& R, int n_i,
-                                           float rowmax, const uint32_t* s_union, int* srow,
-                                           float* se, int* s_loads, uint32_t* s_tokbits, int Bw,
-                                           int* s_len) {
+                                           float rowmax, const uint32_t* l_union, int* srow,
+                                           float* se, const Gather& G0) {
   const int lane = threadIdx.x & 31;
   const int stride = P.cfg.stride;
   int len = n_i;
@@ -414,7 +352,7 @@ __device__ __forceinline__ void tok_phase2(const RouterParams& P, int t, TokRank
     const int cap = vanilla ? P.cfg.k : P.cfg.limit;
     const bool full_scan = vanilla || P.cfg.max_p >= P.N;
     while (len < cap) {
-      const int id = tok_select<E>(R, !vanilla, s_union, key);
+      const int id = tok_select<E>(R, !vanilla, l_union, key);
       if (id < 0) break;
       if (!full_scan && tok_rank_of<E>(R, key, id) >= P.cfg.max_p) break;
       if (lane == 0) {
@@ -437,8 +375,9 @@ __device__ __forceinline__ void tok_phase2(const RouterParams& P, int t, TokRank
       P.sets[o] = e;
       P.wts32[o] = w;
       if (P.wts64) P.wts64[o] = static_cast<double>(w);
-      atomicAdd(&s_loads[e], 1);
-      atomicOr(&s_tokbits[e * Bw + (t >> 5)], 1u << (t & 31));
+      G0.sets[t * stride + j] = e;
+      atomicAdd(&G0.loads[e], 1);
+      atomicOr(&G0.tokbits[e * G0.Bw + (t >> 5)], 1u << (t & 31));
     } else {
       P.sets[o] = -1;
       P.wts32[o] = 0.0f;
@@ -447,12 +386,12 @@ __device__ __forceinline__ void tok_phase2(const RouterParams& P, int t, TokRank
   }
   if (lane == 0) {
     P.set_len[t] = len;
-    s_len[t] = len;
+    G0.len[t] = len;
     if (P.phase1_n) P.phase1_n[t] = n_i;
   }
 }
 
-__device__ __forceinline__ void tok_phase2_masked(const RouterParams& P, int t, int* s_len) {
+__device__ __forceinline__ void tok_phase2_masked(const RouterParams& P, int t, const Gather& G0) {
   const int lane = threadIdx.x & 31;
   for (int j = lane; j < P.cfg.stride; j += 32) {
     const size_t o = static_cast<size_t>(t) * P.cfg.stride + j;
@@ -462,75 +401,64 @@ __device__ __forceinline__ void tok_phase2_masked(const RouterParams& P, int t, 
   }
   if (lane == 0) {
     P.set_len[t] = 0;
-    s_len[t] = 0;
+    G0.len[t] = 0;
     if (P.phase1_n) P.phase1_n[t] = 0;
   }
 }
 
-// All tokens: phase 1 for every token (union barrier), then phase 2. With
-// one token per warp (B <= 16) the ranking stays in registers across the
-// barrier; otherwise each token is reloaded and its baseline re-marked.
-template <int E>
-__device__ __forceinline__ void route_all(const RouterParams& P, uint32_t* s_union, int* s_sets,
-                                          float* s_e, int* s_len, int* s_n, float* s_max,
-                                          int* s_loads, uint32_t* s_tokbits) {
-  const int warp = threadIdx.x >> 5;
-  const int Bw = (P.B + 31) >> 5;
-  const int stride = P.cfg.stride;
-  if (P.B <= kRW) {
-    const int t = warp;
-    const bool act = t < P.B && (P.mask == nullptr || P.mask[t] != 0);
-    TokRank<E> R;
-    int n_i = 0;
-    float rowmax = 0.0f;
-    if (act) {
-      tok_load<E>(P, t, R);
-      if (t == 0) rstamp(P, 8, 0);
-      n_i = tok_phase1<E>(P, R, s_union, s_sets + t * stride, s_e + t * stride, rowmax);
-      if (t == 0) rstamp(P, 8, 1);
-    }
-    __syncthreads();
-    if (warp == 0) rstamp(P, 8, 2);
-    if (act)
-      tok_phase2<E>(P, t, R, n_i, rowmax, s_union, s_sets + t * stride, s_e + t * stride, s_loads,
-                    s_tokbits, Bw, s_len);
-    else if (t < P.B)
-      tok_phase2_masked(P, t, s_len);
-    if (warp == 0) rstamp(P, 8, 3);
-  } else {
-    for (int t = warp; t < P.B; t += kRW) {
-      if (P.mask != nullptr && P.mask[t] == 0) continue;
-      TokRank<E> R;
-      tok_load<E>(P, t, R);
-      float rowmax;
-      const int n_i = tok_phase1<E>(P, R, s_union, s_sets + t * stride, s_e + t * stride, rowmax);
-      if ((threadIdx.x & 31) == 0) {
-        s_n[t] = n_i;
-        s_max[t] = rowmax;
-      }
-    }
-    __syncthreads();
-    for (int t = warp; t < P.B; t += kRW) {
-      if (P.mask != nullptr && P.mask[t] == 0) {
-        tok_phase2_masked(P, t, s_len);
-        continue;
-      }
-      TokRank<E> R;
-      tok_load<E>(P, t, R);
-      const int n_i = s_n[t];
-      for (int j = 0; j < n_i; ++j) tok_take<E>(R, s_sets[t * stride + j]);
-      tok_phase2<E>(P, t, R, n_i, s_max[t], s_union, s_sets + t * stride, s_e + t * stride,
-                    s_loads, s_tokbits, Bw, s_len);
-    }
-  }
-  __syncthreads();
-  if (warp == 0) rstamp(P, 8, 4);
+// Token ownership: within each 64-token chunk, CTA c owns tokens 8c..8c+7;
+// local token li = chunk * 8 + i (<= 32 per CTA, <= 2 per warp).
+__device__ __forceinline__ int owned_token(int crank, int li) {
+  return (li >> 3) * kRouterTokChunk + crank * 8 + (li & 7);
 }
 
-// Fused-path compaction (K3) from shared memory: warp 0 scans the experts
-// (ballot prefix sums) and writes active_union / groups / padding rows; then
-// all warps place each (token, slot) at row_base[slot(e)] + rank of t among
-// the expert's tokens (token order, from the token bitmaps).
+template <int E>
+__device__ __forceinline__ void route_cluster(const RouterParams& P, cg::cluster_group& cluster,
+                                              unsigned crank, const float* s_lg, uint32_t* s_union,
+                                              uint32_t* s_lunion, int* srow_all, float* se_all,
+                                              const Gather& G0) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int stride = P.cfg.stride;
+  const int nloc = ((P.B + kRouterTokChunk - 1) / kRouterTokChunk) * 8;
+  uint32_t* g_union = cluster.map_shared_rank(s_union, 0);
+  TokRank<E> R[2];
+  int n_i[2] = {0, 0};
+  float rmax[2] = {0.0f, 0.0f};
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int li = warp + k * kRW;
+    const int t = owned_token(crank, li);
+    if (li < nloc && t < P.B && (P.mask == nullptr || P.mask[t] != 0)) {
+      tok_load<E>(P.N, s_lg + li * P.Np, R[k]);
+      n_i[k] = tok_phase1<E>(P, R[k], g_union, srow_all + li * stride, se_all + li * stride, rmax[k]);
+    }
+  }
+  if (crank == 0 && warp == 0) rstamp(P, 8, 1);
+  cluster.sync();  // union complete (CTA 0's bitmap)
+  if (crank == 0 && warp == 0) rstamp(P, 8, 2);
+  for (int i = threadIdx.x; i < ((P.Np + 31) >> 5); i += kRouterThreads) s_lunion[i] = g_union[i];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int li = warp + k * kRW;
+    const int t = owned_token(crank, li);
+    if (li < nloc && t < P.B) {
+      if (P.mask == nullptr || P.mask[t] != 0)
+        tok_phase2<E>(P, t, R[k], n_i[k], rmax[k], s_lunion, srow_all + li * stride,
+                      se_all + li * stride, G0);
+      else
+        tok_phase2_masked(P, t, G0);
+    }
+  }
+  if (crank == 0 && warp == 0) rstamp(P, 8, 3);
+  cluster.sync();  // CTA 0 holds every token's set, length, loads, token bits
+}
+
+// Fused-path compaction (K3) from CTA 0's gathered shared memory: warp 0
+// scans the experts (ballot prefix sums) and writes active_union / groups /
+// padding rows; then all warps place each (token, slot) at
+// row_base[slot(e)] + rank of t among the expert's tokens (token order, from
+// the token bitmaps).
 __device__ void compact_fused(const RouterParams& P, const int* s_sets, const int* s_len,
                               const int* s_loads, int* s_eslot, int* s_rowb,
                               const uint32_t* s_tokbits, int* s_tmp) {
@@ -610,6 +538,50 @@ __device__ void compact_fused(const RouterParams& P, const int* s_sets, const in
   }
 }
 
+// Shared-memory carve-up of the router kernel (identical in every CTA).
+struct RouterSmem {
+  size_t part, xs, abuf, bar, lg, uni, luni, len, sets, srow, se, loads, eslot, rowb, tmp, tokbits,
+      total;
+  int ks_split, nkt, kslice, xs_stride, rb_per;
+};
+
+__host__ __device__ inline RouterSmem router_smem_layout(int B, int Np, int Dp, int stride) {
+  RouterSmem L;
+  const int KT = Dp >> 4, nrb = Np >> 4;
+  L.ks_split = nrb <= kRW / 2 ? 2 : 1;
+  L.nkt = (KT + kRouterCluster - 1) / kRouterCluster;
+  L.kslice = L.nkt * 16;
+  L.xs_stride = L.kslice + kXsPad;
+  const int per_rb = L.nkt * kTileBytes;
+  L.rb_per = nrb < kAStageMax / per_rb ? nrb : (kAStageMax / per_rb > 0 ? kAStageMax / per_rb : 1);
+  const int uw = (Np + 31) >> 5, Bw = (B + 31) >> 5;
+  const int nloc = ((B + kRouterTokChunk - 1) / kRouterTokChunk) * 8;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o = (o + bytes + 127) & ~static_cast<size_t>(127);
+    return at;
+  };
+  L.part = take(static_cast<size_t>(L.ks_split) * kRouterTokChunk * Np * 4);
+  L.xs = take(static_cast<size_t>(kRouterTokChunk) * L.xs_stride * 2);
+  L.abuf = take(static_cast<size_t>(L.rb_per) * per_rb);
+  L.bar = take(8);
+  L.lg = take(static_cast<size_t>(nloc) * Np * 4);
+  L.uni = take(uw * 4);
+  L.luni = take(uw * 4);
+  L.len = take(B * 4);
+  L.sets = take(static_cast<size_t>(B) * stride * 4);
+  L.srow = take(static_cast<size_t>(nloc) * stride * 4);
+  L.se = take(static_cast<size_t>(nloc) * stride * 4);
+  L.loads = take(Np * 4);
+  L.eslot = take(Np * 4);
+  L.rowb = take(Np * 4);
+  L.tmp = take(8 * 4);
+  L.tokbits = take(static_cast<size_t>(Np) * Bw * 4);
+  L.total = o;
+  return L;
+}
+
 __global__ void __cluster_dims__(kRouterCluster, 1, 1) __launch_bounds__(kRouterThreads, 1)
     k_router_fused(const RouterParams P) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -625,19 +597,30 @@ __global__ void __cluster_dims__(kRouterCluster, 1, 1) __launch_bounds__(kRouter
 
   const int Np = P.Np, B = P.B;
   const int KT = P.Dp >> 4, nrb = Np >> 4;
+  const RouterSmem SL = router_smem_layout(B, Np, P.Dp, P.cfg.stride);
   const int kt0 = static_cast<int>(crank) * KT / kRouterCluster;
   const int kt1 = (static_cast<int>(crank) + 1) * KT / kRouterCluster;
   const int nkt = kt1 - kt0;
   const int kslice = nkt * 16;
-  const int xs_stride = kslice + kXsPad;  // bf16 elements
-  // smem: [part f32 kRouterTokChunk x Np][xs bf16 kRouterTokChunk x xs_stride][A tiles][mbar]
-  float* part = reinterpret_cast<float*>(smem);
-  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(part + kRouterTokChunk * Np);
-  uint8_t* abuf = reinterpret_cast<uint8_t*>(xs) +
-                  ((static_cast<size_t>(kRouterTokChunk) * xs_stride * 2 + 127) & ~static_cast<size_t>(127));
-  // A tiles for a pass of rb_per rowblocks x nkt k-tiles
-  const int rb_per = max(1, min(nrb, kAStageMax / max(1, nkt * kTileBytes)));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(abuf + static_cast<size_t>(rb_per) * nkt * kTileBytes);
+  const int xs_stride = SL.xs_stride;
+  float* part = reinterpret_cast<float*>(smem + SL.part);  // [ks][kRouterTokChunk][Np]
+  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(smem + SL.xs);
+  uint8_t* abuf = smem + SL.abuf;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SL.bar);
+  float* s_lg = reinterpret_cast<float*>(smem + SL.lg);
+  uint32_t* s_union = reinterpret_cast<uint32_t*>(smem + SL.uni);
+  uint32_t* s_lunion = reinterpret_cast<uint32_t*>(smem + SL.luni);
+  int* s_len = reinterpret_cast<int*>(smem + SL.len);
+  int* s_sets = reinterpret_cast<int*>(smem + SL.sets);
+  int* s_srow = reinterpret_cast<int*>(smem + SL.srow);
+  float* s_se = reinterpret_cast<float*>(smem + SL.se);
+  int* s_loads = reinterpret_cast<int*>(smem + SL.loads);
+  int* s_eslot = reinterpret_cast<int*>(smem + SL.eslot);
+  int* s_rowb = reinterpret_cast<int*>(smem + SL.rowb);
+  int* s_tmp = reinterpret_cast<int*>(smem + SL.tmp);
+  uint32_t* s_tokbits = reinterpret_cast<uint32_t*>(smem + SL.tokbits);
+  const int Bw = (B + 31) >> 5;
+  const int rb_per = SL.rb_per;
   // x rows can be bulk-copied when every K-slice start/end is 16 B aligned in
   // the caller's row (D % 8 == 0) and the slice lies inside D.
   const bool x_bulk = (P.D & 7) == 0 && kt1 * 16 <= P.D;
@@ -645,6 +628,10 @@ __global__ void __cluster_dims__(kRouterCluster, 1, 1) __launch_bounds__(kRouter
     mbar_init(bar, 1);
     fence_mbar_init();
   }
+  // gather targets live in CTA 0; zero them before the first cluster barrier
+  for (int i = threadIdx.x; i < ((Np + 31) >> 5); i += kRouterThreads) s_union[i] = 0u;
+  for (int i = threadIdx.x; i < Np; i += kRouterThreads) s_loads[i] = 0;
+  for (int i = threadIdx.x; i < Np * Bw; i += kRouterThreads) s_tokbits[i] = 0u;
 
   // ---- x -> zero-padded bf16 copy for the FFN when D is not a tile multiple ----
   if (P.xpad) {
@@ -656,12 +643,11 @@ __global__ void __cluster_dims__(kRouterCluster, 1, 1) __launch_bounds__(kRouter
   __syncthreads();
 
   // ---- 1. split-K gate GEMV over the cluster ----
-  const int ks_split = nrb <= kRW / 2 ? 2 : 1;
+  const int ks_split = SL.ks_split;
   uint32_t bar_phase = 0;
-  for (int tc = 0; tc < B; tc += kRouterTokChunk) {
+  for (int tc = 0, chunk = 0; tc < B; tc += kRouterTokChunk, ++chunk) {
     const int ntok = min(kRouterTokChunk, B - tc);
     const int nbc = (ntok + 7) >> 3;
-    for (int i = threadIdx.x; i < kRouterTokChunk * Np; i += kRouterThreads) part[i] = 0.0f;
     for (int rb0 = 0; rb0 < nrb; rb0 += rb_per) {
       const int nrbp = min(rb_per, nrb - rb0);
       // one elected thread issues every bulk copy of this pass on one mbarrier
@@ -719,17 +705,18 @@ __global__ void __cluster_dims__(kRouterCluster, 1, 1) __launch_bounds__(kRouter
             }
           }
         }
-        // C: rows = experts 16rb + gq (+8), cols = tokens 2q, 2q+1.
-        // Two K halves meet with 0 + a + b, which is order-independent.
+        // C: rows = experts 16rb + gq (+8), cols = tokens 2q, 2q+1; each K half
+        // owns its own partial buffer (no atomics, fixed reduction order).
+        float* pk = part + static_cast<size_t>(ks) * kRouterTokChunk * Np;
 #pragma unroll
         for (int nb = 0; nb < 8; ++nb) {
           if (nb < nbc) {
             const int n0 = rb * 16 + gq;
             const int t0 = nb * 8 + 2 * q;
-            atomicAdd(&part[t0 * Np + n0], acc[nb][0]);
-            atomicAdd(&part[(t0 + 1) * Np + n0], acc[nb][1]);
-            atomicAdd(&part[t0 * Np + n0 + 8], acc[nb][2]);
-            atomicAdd(&part[(t0 + 1) * Np + n0 + 8], acc[nb][3]);
+            pk[t0 * Np + n0] = acc[nb][0];
+            pk[(t0 + 1) * Np + n0] = acc[nb][1];
+            pk[t0 * Np + n0 + 8] = acc[nb][2];
+            pk[(t0 + 1) * Np + n0 + 8] = acc[nb][3];
           }
         }
       }
@@ -738,51 +725,50 @@ __global__ void __cluster_dims__(kRouterCluster, 1, 1) __launch_bounds__(kRouter
     rstamp(P, crank, 2);
     cluster.sync();
     rstamp(P, crank, 3);
-    // Distributed fixed-order reduction over DSMEM: CTA c sums slice c of
-    // every CTA's partial (ranks 0..7 in order) into the global logits.
-    {
-      const int elems = ntok * Np;
-      const int e0 = static_cast<int>(crank) * elems / kRouterCluster;
-      const int e1 = (static_cast<int>(crank) + 1) * elems / kRouterCluster;
-      for (int i = e0 + threadIdx.x; i < e1; i += kRouterThreads) {
-        float v[kRouterCluster];
+    // Token-sliced fixed-order reduction over DSMEM: CTA c sums, for its 8
+    // tokens of this chunk, every CTA's partials (ranks 0..7, K halves in
+    // order) into its local logits rows (and the exported global logits).
+    for (int i = threadIdx.x; i < 8 * Np; i += kRouterThreads) {
+      const int tl = i / Np, n = i % Np;
+      const int row = static_cast<int>(crank) * 8 + tl;  // row within the chunk
+      if (row >= ntok) continue;
+      float v[kRouterCluster * 2];
 #pragma unroll
-        for (int r = 0; r < kRouterCluster; ++r) v[r] = cluster.map_shared_rank(part, r)[i];
-        float s = 0.0f;
-#pragma unroll
-        for (int r = 0; r < kRouterCluster; ++r) s += v[r];
-        P.logits[static_cast<size_t>(tc) * Np + i] = s;
+      for (int r = 0; r < kRouterCluster; ++r) {
+        const float* pr = cluster.map_shared_rank(part, r);
+        v[2 * r] = pr[row * Np + n];
+        v[2 * r + 1] = ks_split == 2 ? pr[kRouterTokChunk * Np + row * Np + n] : 0.0f;
       }
+      float s = 0.0f;
+#pragma unroll
+      for (int r = 0; r < 2 * kRouterCluster; ++r) s += v[r];
+      s_lg[(chunk * 8 + tl) * Np + n] = s;
+      P.logits[static_cast<size_t>(tc + row) * Np + n] = s;
     }
-    cluster.sync();
+    cluster.sync();  // partials may be overwritten by the next chunk
   }
   rstamp(P, crank, 4);
-  if (crank != 0) return;
-
-  // ---- 2. routing (CTA 0) ----
-  const int stride = P.cfg.stride;
-  const int Bw = (B + 31) >> 5;
-  uint32_t* s_union = reinterpret_cast<uint32_t*>(smem);          // [ceil(Np/32)]
-  const int uw = (Np + 31) >> 5;
-  int* s_len = reinterpret_cast<int*>(s_union + uw);               // [B]
-  int* s_n = s_len + B;                                            // [B]
-  float* s_max = reinterpret_cast<float*>(s_n + B);                // [B]
-  int* s_sets = reinterpret_cast<int*>(s_max + B);                 // [B][stride]
-  float* s_e = reinterpret_cast<float*>(s_sets + B * stride);      // [B][stride]
-  int* s_loads = reinterpret_cast<int*>(s_e + B * stride);         // [Np]
-  int* s_eslot = s_loads + Np;                                     // [Np]
-  int* s_rowb = s_eslot + Np;                                      // [Np]
-  int* s_tmp = s_rowb + Np;                                        // [8]
-  uint32_t* s_tokbits = reinterpret_cast<uint32_t*>(s_tmp + 8);    // [Np][Bw]
-  for (int i = threadIdx.x; i < uw; i += kRouterThreads) s_union[i] = 0u;
-  for (int i = threadIdx.x; i < Np; i += kRouterThreads) s_loads[i] = 0;
-  for (int i = threadIdx.x; i < Np * Bw; i += kRouterThreads) s_tokbits[i] = 0u;
+  if (P.logits_only) {
+    // the FFN kernel routes in its prologue; reset its counters here
+    if (crank == 0)
+      for (int c = threadIdx.x; c < P.n_counters; c += kRouterThreads) P.counters[c] = 0;
+    return;
+  }
   __syncthreads();
+
+  // ---- 2. routing, distributed: each CTA ranks its own tokens ----
+  Gather G0;
+  G0.sets = cluster.map_shared_rank(s_sets, 0);
+  G0.len = cluster.map_shared_rank(s_len, 0);
+  G0.loads = cluster.map_shared_rank(s_loads, 0);
+  G0.tokbits = cluster.map_shared_rank(s_tokbits, 0);
+  G0.Bw = Bw;
   if (Np <= 128)
-    route_all<4>(P, s_union, s_sets, s_e, s_len, s_n, s_max, s_loads, s_tokbits);
+    route_cluster<4>(P, cluster, crank, s_lg, s_union, s_lunion, s_srow, s_se, G0);
   else
-    route_all<8>(P, s_union, s_sets, s_e, s_len, s_n, s_max, s_loads, s_tokbits);
-  rstamp(P, 0, 5);
+    route_cluster<8>(P, cluster, crank, s_lg, s_union, s_lunion, s_srow, s_se, G0);
+  rstamp(P, crank, 5);
+  if (crank != 0) return;
 
   if ((P.base_union || P.base_union_count) && warp == 1) {
     int c = 0;
@@ -796,7 +782,7 @@ __global__ void __cluster_dims__(kRouterCluster, 1, 1) __launch_bounds__(kRouter
     if (lane == 0 && P.base_union_count) *P.base_union_count = c;
   }
 
-  // ---- 3. compaction for the FFN (from shared memory) ----
+  // ---- 3. compaction for the FFN (CTA 0, from the gathered shared memory) ----
   compact_fused(P, s_sets, s_len, s_loads, s_eslot, s_rowb, s_tokbits, s_tmp);
   rstamp(P, 0, 6);
 }
@@ -808,17 +794,7 @@ namespace oea_host {
 using namespace oea_dev;
 
 size_t router_fused_smem_bytes(int B, int Np, int Dp, int stride) {
-  const int KT = Dp >> 4;
-  const int nkt = (KT + kRouterCluster - 1) / kRouterCluster;
-  const int nrb = Np >> 4;
-  const int rb_per = std::max(1, std::min(nrb, kAStageMax / std::max(1, nkt * kTileBytes)));
-  const size_t xs = (static_cast<size_t>(kRouterTokChunk) * (nkt * 16 + kXsPad) * 2 + 127) & ~static_cast<size_t>(127);
-  const size_t gemv = static_cast<size_t>(kRouterTokChunk) * Np * sizeof(float) + xs +
-                      static_cast<size_t>(rb_per) * nkt * kTileBytes + 64;
-  const size_t route = (static_cast<size_t>((Np + 31) >> 5) + 3 * B +
-                        2 * static_cast<size_t>(B) * stride + 3 * Np + 8) * 4 +
-                       static_cast<size_t>(Np) * ((B + 31) / 32) * 4;
-  return gemv > route ? gemv : route;
+  return router_smem_layout(B, Np, Dp, stride).total;
 }
 
 int router_fused_launch(oea_ctx* ctx, const oea_layer* L, const Cfg& cfg, int B,
@@ -858,6 +834,7 @@ int router_fused_launch(oea_ctx* ctx, const oea_layer* L, const Cfg& cfg, int B,
   P.base_union_count = rb.base_union_count;
   P.trace = rb.trace;
   P.late_trigger = getenv("OEA_LATE_TRIGGER") != nullptr;
+  P.logits_only = rb.logits_only;
   const size_t smem = router_fused_smem_bytes(B, L->Np, L->Dp, cfg.stride);
   OEA_CUDA_TRY(ctx, cudaFuncSetAttribute(k_router_fused,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
