@@ -9,7 +9,8 @@
  *                                           route, batch_stats)
  *   proj/include/oea/moe_layer.hpp:70-178  (router_scores, expert_forward,
  *                                           moe_forward, make_random_layer, ...)
- * This repo keeps that C++ API verbatim in include/oea/*.hpp; its adapter
+ * This repo keeps that C++ API verbatim in include/oea/ (routing.hpp,
+ * moe_layer.hpp, rng.hpp); its adapter
  * (paper_2511_02237_b200/csrc/adapter.cpp) and the Python mirror
  * (paper_2511_02237_b200/__init__.py) both call the entry points below, which
  * run hand-written sm_100a kernels. There is no CPU fallback: every compute

@@ -417,7 +417,7 @@ __device__ __forceinline__ void route_cluster(const RouterParams& P, cg::cluster
                                               unsigned crank, const float* s_lg, uint32_t* s_union,
                                               uint32_t* s_lunion, int* srow_all, float* se_all,
                                               const Gather& G0) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
   const int stride = P.cfg.stride;
   const int nloc = ((P.B + kRouterTokChunk - 1) / kRouterTokChunk) * 8;
   uint32_t* g_union = cluster.map_shared_rank(s_union, 0);
