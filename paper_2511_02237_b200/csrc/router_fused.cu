@@ -289,7 +289,7 @@ constexpr int kAStageMax = 64 * 1024;      // router A-tile staging per pass
 // fp64 softmax of the fp32 logits (documented best-effort parity). The
 // baseline experts are OR-ed into the cluster's union bitmap (DSMEM atomics on
 // CTA 0's copy).
-template <int E>
+template <int E, bool kMass>
 __device__ __forceinline__ int tok_phase1(const RouterParams& P, TokRank<E>& R, uint32_t* g_union,
                                           int* srow, float* se, float& rowmax) {
   const int lane = threadIdx.x & 31;
@@ -297,16 +297,18 @@ __device__ __forceinline__ int tok_phase1(const RouterParams& P, TokRank<E>& R, 
   int id = tok_select<E>(R, false, nullptr, key);  // rank 0 anchors the weights
   rowmax = key32_to_logit(key);
   if (P.cfg.mode == OEA_MODE_VANILLA) return 0;
-  const bool mass_rule = P.cfg.p != 1.0;
+  constexpr bool mass_rule = kMass;  // p < 1: compiled into its own kernel variant
   double z = 0.0;
   if (mass_rule) {
 #pragma unroll
     for (int j = 0; j < E; ++j)
       if (R.key[j] != 0u) z += exp(static_cast<double>(key32_to_logit(R.key[j])) - rowmax);
+    #pragma unroll 1
     for (int off = 16; off > 0; off >>= 1) z += __shfl_xor_sync(kFull, z, off);
   }
   int n = 0;
   double cum = 0.0;
+#pragma unroll 1
   while (n < P.cfg.k0 && id >= 0) {
     if (lane == 0) {
       srow[n] = id;
@@ -351,6 +353,7 @@ __device__ __forceinline__ void tok_phase2(const RouterParams& P, int t, TokRank
   if (P.cfg.mode != OEA_MODE_PRUNED) {
     const int cap = vanilla ? P.cfg.k : P.cfg.limit;
     const bool full_scan = vanilla || P.cfg.max_p >= P.N;
+#pragma unroll 1
     while (len < cap) {
       const int id = tok_select<E>(R, !vanilla, l_union, key);
       if (id < 0) break;
@@ -366,7 +369,9 @@ __device__ __forceinline__ void tok_phase2(const RouterParams& P, int t, TokRank
   __syncwarp();
   // sequential fp32 mass in set order, then w = e / mass
   float mass = 0.0f;
+  #pragma unroll 1
   for (int j = 0; j < len; ++j) mass += se[j];
+  #pragma unroll 1
   for (int j = lane; j < stride; j += 32) {
     const size_t o = static_cast<size_t>(t) * stride + j;
     if (j < len) {
@@ -393,6 +398,7 @@ __device__ __forceinline__ void tok_phase2(const RouterParams& P, int t, TokRank
 
 __device__ __forceinline__ void tok_phase2_masked(const RouterParams& P, int t, const Gather& G0) {
   const int lane = threadIdx.x & 31;
+  #pragma unroll 1
   for (int j = lane; j < P.cfg.stride; j += 32) {
     const size_t o = static_cast<size_t>(t) * P.cfg.stride + j;
     P.sets[o] = -1;
@@ -412,43 +418,54 @@ __device__ __forceinline__ int owned_token(int crank, int li) {
   return (li >> 3) * kRouterTokChunk + crank * 8 + (li & 7);
 }
 
-template <int E>
+template <int E, bool kMass>
 __device__ __forceinline__ void route_cluster(const RouterParams& P, cg::cluster_group& cluster,
                                               unsigned crank, const float* s_lg, uint32_t* s_union,
                                               uint32_t* s_lunion, int* srow_all, float* se_all,
-                                              const Gather& G0) {
-  const int warp = threadIdx.x >> 5;
+                                              int* s_nloc, float* s_mloc, const Gather& G0) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int stride = P.cfg.stride;
   const int nloc = ((P.B + kRouterTokChunk - 1) / kRouterTokChunk) * 8;
   uint32_t* g_union = cluster.map_shared_rank(s_union, 0);
-  TokRank<E> R[2];
-  int n_i[2] = {0, 0};
-  float rmax[2] = {0.0f, 0.0f};
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const int li = warp + k * kRW;
+  // Phase 1 for this CTA's tokens; per-token state goes to shared memory so
+  // the token loop stays rolled (small code: this runs cold once per launch).
+#pragma unroll 1
+  for (int li = warp; li < nloc; li += kRW) {
     const int t = owned_token(crank, li);
-    if (li < nloc && t < P.B && (P.mask == nullptr || P.mask[t] != 0)) {
-      tok_load<E>(P.N, s_lg + li * P.Np, R[k]);
-      n_i[k] = tok_phase1<E>(P, R[k], g_union, srow_all + li * stride, se_all + li * stride, rmax[k]);
+    int n_i = 0;
+    float rmax = 0.0f;
+    if (t < P.B && (P.mask == nullptr || P.mask[t] != 0)) {
+      TokRank<E> R;
+      tok_load<E>(P.N, s_lg + li * P.Np, R);
+      n_i = tok_phase1<E, kMass>(P, R, g_union, srow_all + li * stride, se_all + li * stride, rmax);
+    }
+    if (lane == 0) {
+      s_nloc[li] = n_i;
+      s_mloc[li] = rmax;
     }
   }
   if (crank == 0 && warp == 0) rstamp(P, 8, 1);
   cluster.sync();  // union complete (CTA 0's bitmap)
   if (crank == 0 && warp == 0) rstamp(P, 8, 2);
+  #pragma unroll 1
   for (int i = threadIdx.x; i < ((P.Np + 31) >> 5); i += kRouterThreads) s_lunion[i] = g_union[i];
   __syncthreads();
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const int li = warp + k * kRW;
+#pragma unroll 1
+  for (int li = warp; li < nloc; li += kRW) {
     const int t = owned_token(crank, li);
-    if (li < nloc && t < P.B) {
-      if (P.mask == nullptr || P.mask[t] != 0)
-        tok_phase2<E>(P, t, R[k], n_i[k], rmax[k], s_lunion, srow_all + li * stride,
-                      se_all + li * stride, G0);
-      else
-        tok_phase2_masked(P, t, G0);
+    if (t >= P.B) continue;
+    if (P.mask != nullptr && P.mask[t] == 0) {
+      tok_phase2_masked(P, t, G0);
+      continue;
     }
+    TokRank<E> R;
+    tok_load<E>(P.N, s_lg + li * P.Np, R);
+    const int n_i = s_nloc[li];
+    const int* srow = srow_all + li * stride;
+#pragma unroll 1
+    for (int j = 0; j < n_i; ++j) tok_take<E>(R, srow[j]);
+    tok_phase2<E>(P, t, R, n_i, s_mloc[li], s_lunion, srow_all + li * stride, se_all + li * stride,
+                  G0);
   }
   if (crank == 0 && warp == 0) rstamp(P, 8, 3);
   cluster.sync();  // CTA 0 holds every token's set, length, loads, token bits
@@ -467,6 +484,7 @@ __device__ void compact_fused(const RouterParams& P, const int* s_sets, const in
   const int Bw = (B + 31) >> 5;
   if (warp == 0) {
     int T = 0, G = 0, R = 0, load = 0;
+    #pragma unroll 1
     for (int base = 0; base < N; base += 32) {
       const int e = base + lane;
       const int m = e < N ? s_loads[e] : 0;
@@ -494,11 +512,13 @@ __device__ void compact_fused(const RouterParams& P, const int* s_sets, const in
       if (act) {
         P.active_union[slot] = e;
         s_rowb[e] = r0;
+        #pragma unroll 1
         for (int k = 0; k < ng; ++k) {
           P.group_a[g0 + k] = e;
           P.group_row0[g0 + k] = r0 + k * kTokGroup;
           P.group_rows[g0 + k] = min(kTokGroup, m - k * kTokGroup);
         }
+        #pragma unroll 1
         for (int r = r0 + m; r < r0 + nr; ++r) P.row_tok[r] = -1;  // n-block padding
       }
       T += __popc(am);
@@ -506,6 +526,7 @@ __device__ void compact_fused(const RouterParams& P, const int* s_sets, const in
       R += __shfl_sync(kFull, ri, 31);
       load += __shfl_sync(kFull, li, 31);
     }
+    #pragma unroll 1
     for (int e = T + lane; e < N; e += 32) P.active_union[e] = -1;
     if (lane == 0) {
       P.hdr->n_groups = G;
@@ -517,15 +538,18 @@ __device__ void compact_fused(const RouterParams& P, const int* s_sets, const in
       s_tmp[0] = G;
     }
   } else {
+    #pragma unroll 1
     for (int c = threadIdx.x - 32; c < P.n_counters; c += kRouterThreads - 32) P.counters[c] = 0;
   }
   __syncthreads();
+  #pragma unroll 1
   for (int idx = threadIdx.x; idx < B * stride; idx += kRouterThreads) {
     const int t = idx / stride, sl = idx % stride;
     if (sl < s_len[t]) {
       const int e = s_sets[idx];
       const uint32_t* bits = s_tokbits + e * Bw;
       int rank = __popc(bits[t >> 5] & ((1u << (t & 31)) - 1u));
+      #pragma unroll 1
       for (int w = 0; w < (t >> 5); ++w) rank += __popc(bits[w]);
       const int row = s_rowb[e] + rank;
       P.row_tok[row] = t;
@@ -533,6 +557,7 @@ __device__ void compact_fused(const RouterParams& P, const int* s_sets, const in
     }
   }
   if (s_tmp[0] == 0) {
+    #pragma unroll 1
     for (size_t f = threadIdx.x; f < static_cast<size_t>(B) * P.D; f += kRouterThreads)
       P.out[f] = 0.0f;
   }
@@ -541,7 +566,7 @@ __device__ void compact_fused(const RouterParams& P, const int* s_sets, const in
 // Shared-memory carve-up of the router kernel (identical in every CTA).
 struct RouterSmem {
   size_t part, xs, abuf, bar, lg, uni, luni, len, sets, srow, se, loads, eslot, rowb, tmp, tokbits,
-      total;
+      nloc, mloc, total;
   int ks_split, nkt, kslice, xs_stride, rb_per;
 };
 
@@ -578,10 +603,13 @@ __host__ __device__ inline RouterSmem router_smem_layout(int B, int Np, int Dp, 
   L.rowb = take(Np * 4);
   L.tmp = take(8 * 4);
   L.tokbits = take(static_cast<size_t>(Np) * Bw * 4);
+  L.nloc = take(static_cast<size_t>(nloc) * 4);
+  L.mloc = take(static_cast<size_t>(nloc) * 4);
   L.total = o;
   return L;
 }
 
+template <bool kMass>
 __global__ void __cluster_dims__(kRouterCluster, 1, 1) __launch_bounds__(kRouterThreads, 1)
     k_router_fused(const RouterParams P) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -629,8 +657,11 @@ __global__ void __cluster_dims__(kRouterCluster, 1, 1) __launch_bounds__(kRouter
     fence_mbar_init();
   }
   // gather targets live in CTA 0; zero them before the first cluster barrier
+#pragma unroll 1
   for (int i = threadIdx.x; i < ((Np + 31) >> 5); i += kRouterThreads) s_union[i] = 0u;
+#pragma unroll 1
   for (int i = threadIdx.x; i < Np; i += kRouterThreads) s_loads[i] = 0;
+#pragma unroll 1
   for (int i = threadIdx.x; i < Np * Bw; i += kRouterThreads) s_tokbits[i] = 0u;
 
   // ---- x -> zero-padded bf16 copy for the FFN when D is not a tile multiple ----
@@ -763,10 +794,12 @@ __global__ void __cluster_dims__(kRouterCluster, 1, 1) __launch_bounds__(kRouter
   G0.loads = cluster.map_shared_rank(s_loads, 0);
   G0.tokbits = cluster.map_shared_rank(s_tokbits, 0);
   G0.Bw = Bw;
+  int* s_nloc = reinterpret_cast<int*>(smem + SL.nloc);      // per local token: n_i
+  float* s_mloc = reinterpret_cast<float*>(smem + SL.mloc);  // per local token: max logit
   if (Np <= 128)
-    route_cluster<4>(P, cluster, crank, s_lg, s_union, s_lunion, s_srow, s_se, G0);
+    route_cluster<4, kMass>(P, cluster, crank, s_lg, s_union, s_lunion, s_srow, s_se, s_nloc, s_mloc, G0);
   else
-    route_cluster<8>(P, cluster, crank, s_lg, s_union, s_lunion, s_srow, s_se, G0);
+    route_cluster<8, kMass>(P, cluster, crank, s_lg, s_union, s_lunion, s_srow, s_se, s_nloc, s_mloc, G0);
   rstamp(P, crank, 5);
   if (crank != 0) return;
 
@@ -836,10 +869,17 @@ int router_fused_launch(oea_ctx* ctx, const oea_layer* L, const Cfg& cfg, int B,
   P.late_trigger = getenv("OEA_LATE_TRIGGER") != nullptr;
   P.logits_only = rb.logits_only;
   const size_t smem = router_fused_smem_bytes(B, L->Np, L->Dp, cfg.stride);
-  OEA_CUDA_TRY(ctx, cudaFuncSetAttribute(k_router_fused,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
-  k_router_fused<<<kRouterCluster, kRouterThreads, smem, s>>>(P);
+  if (cfg.p != 1.0 && cfg.mode != OEA_MODE_VANILLA) {
+    OEA_CUDA_TRY(ctx, cudaFuncSetAttribute(k_router_fused<true>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem)));
+    k_router_fused<true><<<kRouterCluster, kRouterThreads, smem, s>>>(P);
+  } else {
+    OEA_CUDA_TRY(ctx, cudaFuncSetAttribute(k_router_fused<false>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem)));
+    k_router_fused<false><<<kRouterCluster, kRouterThreads, smem, s>>>(P);
+  }
   OEA_LAUNCHED(ctx);
   return OEA_OK;
 }
