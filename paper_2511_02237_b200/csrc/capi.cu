@@ -107,7 +107,7 @@ size_t carve(Workspace& w, bool assign) {
   take(w.group_row0, G * 4);
   take(w.group_rows, G * 4);
   take(w.hdr, sizeof(FfnHeader));
-  take(w.counters, (G + Dp / 16 + 4) * 4);
+  take(w.counters, (G + Dp / 16 + 8) * 4);
   take(w.xpad, B * Dp * 2);
   take(w.hbuf, R * std::max(Hp, H) * 8);
   take(w.ybuf, B * S * std::max(Dp, D) * 8);
@@ -151,6 +151,9 @@ int ensure(oea_ctx* ctx, Workspace& w, Need nd) {
   set_caps(w, nd);
   const size_t bytes = carve(w, false);
   OEA_CUDA_TRY(ctx, cudaMalloc(&w.base, bytes));
+  // the fused decode's grid counters must start at zero (they self-reset)
+  OEA_CUDA_TRY(ctx, cudaMemsetAsync(w.base, 0, bytes, ctx->stream));
+  OEA_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   w.bytes = bytes;
   carve(w, true);
   return OEA_OK;
@@ -353,22 +356,23 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   rb.group_rows = w.group_rows;
   rb.hdr = w.hdr;
   rb.counters = w.counters;
-  rb.n_counters = w.G + L->Dp / 16 + 3;
+  rb.n_counters = w.G + L->Dp / 16 + 5;
   rb.out = static_cast<float*>(out);
   rb.phase1_n = w.n;
   rb.base_union = w.base_union;
   rb.base_union_count = w.base_union_count;
   rb.trace = ctx->ffn_trace;
-  // Optional (OEA_FFN_ROUTES=1, B <= 64): every FFN CTA ranks the batch from
-  // the logits in its prologue (expert_ffn.cu route_prologue) and the router
-  // kernel only computes the logits. Default: the router cluster routes.
-  const bool rik = B <= kRouterTokChunk && getenv("OEA_FFN_ROUTES") != nullptr &&
-                   oea_host::ffn_bf16_smem_bytes() +
-                           oea_host::ffn_route_smem_bytes(B, L->Np, stride) <= 227 * 1024;
-  rb.logits_only = rik ? 1 : 0;
+  // Fused single launch (B <= 64): the FFN grid computes the logits, routes
+  // the batch in every CTA and streams the union's weights as soon as it is
+  // known (expert_ffn.cu fused_*). OEA_TWO_KERNEL=1 forces the router-cluster
+  // + FFN pair (always used for B > 64 and for the router-only stage graph).
+  const bool fused = part == 0 && B <= kRouterTokChunk && L->router_t != nullptr &&
+                     getenv("OEA_TWO_KERNEL") == nullptr &&
+                     oea_host::ffn_bf16_smem_bytes() +
+                             oea_host::ffn_route_smem_bytes(B, L->Np, stride) <= 227 * 1024;
   int r = OEA_OK;
-  if (part != 2) {
-    if (rb.trace) OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.trace, 0, 8 * 8 * 1024, s));
+  if (rb.trace) OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.trace, 0, 8 * 8 * 1024, s));
+  if (part != 2 && !fused) {
     r = oea_host::router_fused_launch(ctx, L, cfg, B, rb, s);
     if (r || part == 1) return r;
   }
@@ -390,8 +394,11 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   fb.out = out;
   fb.trace = ctx->ffn_trace;
   fb.mode = ctx->ffn_mode;
-  if (rik) {
-    fb.route_in_kernel = 1;
+  if (fused) {
+    fb.fused = 1;
+    fb.xnc = padded ? 0 : 1;
+    fb.x_in = static_cast<const __nv_bfloat16*>(x);
+    fb.xpad_out = padded ? w.xpad : nullptr;
     fb.logits = w.logits;
     fb.mask = mask;
     fb.cfg = cfg;
@@ -408,7 +415,7 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
     fb.x_base_union_count = w.base_union_count;
     fb.x_hdr = w.hdr;
   }
-  return oea_host::ffn_bf16_launch(ctx, L, B, stride, fb, part == 0, s);
+  return oea_host::ffn_bf16_launch(ctx, L, B, stride, fb, part == 0 && !fused, s);
 }
 
 // f32/f64 layers: router_scores (fp64) -> route_f64 -> compaction -> SIMT FFN.
@@ -803,6 +810,10 @@ int oea_layer_create(oea_ctx_t ctx, int32_t D, int32_t H, int32_t N, int32_t dty
     L->w2_bytes = static_cast<size_t>(N) * H * D * es;
   }
   e = cudaMalloc(&L->router, L->router_bytes);
+  if (e == cudaSuccess && dtype == OEA_DTYPE_BF16) {
+    e = cudaMalloc(&L->router_t, L->router_bytes);
+    if (e == cudaSuccess) e = cudaMemsetAsync(L->router_t, 0, L->router_bytes, ctx->stream);
+  }
   if (e == cudaSuccess) e = cudaMalloc(&L->w1, L->w1_bytes);
   if (e == cudaSuccess && L->up_bytes) e = cudaMalloc(&L->w_up, L->up_bytes);
   if (e == cudaSuccess) e = cudaMalloc(&L->w2, L->w2_bytes);
@@ -823,6 +834,7 @@ int oea_layer_destroy(oea_layer_t L) {
   if (L == nullptr) return OEA_OK;
   if (L->ctx) cudaStreamSynchronize(L->ctx->stream);
   cudaFree(L->router);
+  cudaFree(L->router_t);
   cudaFree(L->w1);
   cudaFree(L->w_up);
   cudaFree(L->w2);

@@ -60,9 +60,13 @@ struct FfnParams {
   float* out;           // [B][D]
   unsigned long long* trace;  // debug: [gridDim][8] globaltimer stamps, or null
   int mode;                   // debug: 1 = stream weights only (no math)
-  // In-kernel routing (see route_prologue).
-  int route_in_kernel;
-  const float* logits;  // [B][Np]
+  // Fused single-launch decode (see fused_gemv / fused_route_phase1/2).
+  int fused;
+  int xnc;                      // x is read-only for the kernel (non-coherent loads ok)
+  const uint4* router_t;        // [Np][Dp/8] expert-major bf16 router
+  const __nv_bfloat16* x_in;    // [B][D] caller tokens
+  __nv_bfloat16* xpad_out;      // [B][Dp], written in-kernel when D != Dp, else null
+  float* logits;        // [B][Np]
   const uint8_t* mask;
   int N, Np;
   Cfg cfg;
@@ -101,7 +105,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 __device__ __forceinline__ void stamp(const FfnParams& P, int slot) {
-  if (P.trace) P.trace[blockIdx.x * 8 + slot] = gtimer();
+  if (P.trace) P.trace[blockIdx.x * 16 + slot] = gtimer();
 }
 
 struct Unit {
@@ -140,7 +144,7 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
     if (lane == 0)
       while (ld_acquire_gpu(&P.w1_done[U.g]) < RB1) __nanosleep(64);
     __syncwarp();
-    if (warp == 0 && lane == 0 && P.trace && P.trace[blockIdx.x * 8 + 2] == 0) stamp(P, 2);
+    if (warp == 0 && lane == 0 && P.trace && P.trace[blockIdx.x * 16 + 2] == 0) stamp(P, 2);
   }
 
   // two accumulator sets (even / odd k-tiles) halve the dependent HMMA chain
@@ -166,7 +170,7 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
       for (int nb = 0; nb < NB; ++nb) {
         uint32_t b0 = 0, b1 = 0;
         if (bp[nb] != nullptr) {
-          if (W1) {
+          if (W1 && P.xnc) {
             b0 = __ldg(bp[nb] + kt * 8 + q);
             b1 = __ldg(bp[nb] + kt * 8 + 4 + q);
           } else {
@@ -198,7 +202,7 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
             b0 = bf[kPref ? j : 0][nb][0];
             b1 = bf[kPref ? j : 0][nb][1];
           } else if (bp[nb] != nullptr) {
-            if (W1) {
+            if (W1 && P.xnc) {
               b0 = __ldg(bp[nb] + kt * 8 + q);
               b1 = __ldg(bp[nb] + kt * 8 + 4 + q);
             } else {
@@ -297,17 +301,28 @@ __device__ __forceinline__ void dispatch_unit(int nbk, const FfnParams& P, const
 }
 
 // ---------------------------------------------------------------------------
-// In-kernel routing (B <= 64): every CTA ranks the whole batch from the router
-// logits in shared memory — phase 1 (routing.cpp:226-268) for all tokens, the
-// union, then phase 2 (routing.cpp:270-303), fp32 renormalisation
-// (routing.cpp:33-49) and the compaction (one token group per active expert).
-// All CTAs compute the identical plan (deterministic code on identical
-// inputs), so no cross-CTA exchange or plan round trip through HBM is needed,
-// and each CTA's producer starts streaming as soon as its union is known.
+// Fused single-launch decode (B <= 64): the FFN grid computes the router
+// logits itself, exchanges them through one grid barrier, and every CTA then
+// ranks the whole batch redundantly from shared memory (deterministic code on
+// identical inputs -> identical plans, no plan round trip through HBM).
+//
+//   G  gate GEMV (router_scores, moe_layer.hpp:71-90, on bf16 weights):
+//      CTA c computes the logits of experts c, c + grid, ... for every token
+//      from the expert-major router copy (4 KiB per expert at D=2048) and the
+//      bf16 tokens; fixed-order warp transpose-reduction + fixed warp order,
+//      so logits are deterministic. Then one grid barrier.
+//   R1 Phase 1 (routing.cpp:226-268) for every token (all 9 warps): the
+//      baseline top-k0 (vanilla: top-k, route_topk routing.cpp:205-224) and
+//      the batch union bitmap. active_union == base_union for the OEA modes
+//      (conservation, acceptance.cpp:158-184), so the union IS the list of
+//      expert groups: the producer warp starts streaming weights here.
+//   R2 Phase 2 (routing.cpp:270-303) + fp32 renormalisation (routing.cpp:
+//      33-49) + compaction (token lists in token order, inverse permutation)
+//      on the 8 consumer warps, overlapped with the producer's first stages.
 // ---------------------------------------------------------------------------
 struct RouteSmem {
-  size_t lg, uni, sets, e, len, n, mx, loads, tokbits, active, eslot, rowb, rows, rtok, rslot, misc,
-      total;
+  size_t lg, uni, sets, e, len, n, mx, loads, tokbits, active, eslot, rowb, rows, rtok, rslot, red,
+      misc, total;
 };
 
 __host__ __device__ inline RouteSmem route_smem_layout(int B, int Np, int stride) {
@@ -335,51 +350,183 @@ __host__ __device__ inline RouteSmem route_smem_layout(int B, int Np, int stride
   L.rows = take(Np * 4);
   L.rtok = take(rmax * 4);
   L.rslot = take(rmax * 4);
+  L.red = take((kFfnWarps + 1) * 16 * 4);
   L.misc = take(8 * 4);
   L.total = o;
   return L;
 }
 
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+
+// 8 bf16 of token row `xr` starting at element d0 (zero beyond D).
+__device__ __forceinline__ void load_x8(const __nv_bfloat16* xr, int d0, int D, bool vec,
+                                        float (&f)[8]) {
+  if (vec) {
+    if (d0 < D) {
+      bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(xr + d0)), f);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) f[i] = 0.0f;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = d0 + i < D ? __bfloat162float(xr[d0 + i]) : 0.0f;
+  }
+}
+
+// G: logits[t][e] for this CTA's experts; also the zero-padded x copy the
+// FFN's B fragments read when D is not a tile multiple. Ends with the grid
+// barrier after which every CTA may read all logits (and xpad).
+__device__ __forceinline__ void fused_gemv(const FfnParams& P, float* red, int* sync_cnt) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NT = (kFfnWarps + 1) * 32;
+  const int nch = P.Dp >> 3;
+  const bool vec = (P.D & 7) == 0;
+  if (P.xpad_out != nullptr) {
+#pragma unroll 1
+    for (int t = blockIdx.x; t < P.B; t += gridDim.x)
+#pragma unroll 1
+      for (int d = tid; d < P.Dp; d += NT)
+        P.xpad_out[static_cast<size_t>(t) * P.Dp + d] =
+            d < P.D ? P.x_in[static_cast<size_t>(t) * P.D + d] : __float2bfloat16_rn(0.0f);
+  }
+  if (tid == 0) stamp(P, 8);
+#pragma unroll 1
+  for (int e = blockIdx.x; e < P.N; e += gridDim.x) {
+    const uint4* rrow = P.router_t + static_cast<size_t>(e) * nch;
+#pragma unroll 1
+    for (int tc = 0; tc < P.B; tc += 16) {
+      float a[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) a[t] = 0.0f;
+      if (vec) {
+        // all 16 token chunks + the router chunk in flight before any FMA
+#pragma unroll 1
+        for (int c = tid; c < nch; c += NT) {
+          const uint4 rv = __ldg(rrow + c);
+          uint4 xv[16];
+#pragma unroll
+          for (int t = 0; t < 16; ++t)
+            xv[t] = (tc + t < P.B && c * 8 < P.D)
+                        ? __ldg(reinterpret_cast<const uint4*>(
+                              P.x_in + static_cast<size_t>(tc + t) * P.D + c * 8))
+                        : make_uint4(0u, 0u, 0u, 0u);
+          float rf[8];
+          bf16x8_to_f32(rv, rf);
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            float xf[8];
+            bf16x8_to_f32(xv[t], xf);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[t] = fmaf(rf[i], xf[i], a[t]);
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int c = tid; c < nch; c += NT) {
+          float rf[8];
+          bf16x8_to_f32(__ldg(rrow + c), rf);
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            if (tc + t < P.B) {
+              float xf[8];
+              load_x8(P.x_in + static_cast<size_t>(tc + t) * P.D, c * 8, P.D, false, xf);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) a[t] = fmaf(rf[i], xf[i], a[t]);
+            }
+          }
+        }
+      }
+      // warp transpose-reduction: 16 values -> lane pair (2i, 2i+1) holds the
+      // warp sum of value idx(lane), fixed order
+#pragma unroll
+      for (int off = 16, n = 16; off >= 2; off >>= 1, n >>= 1) {
+        const bool up = (lane & off) != 0;
+#pragma unroll
+        for (int j = 0; j < n / 2; ++j) {
+          const float send = up ? a[j] : a[j + n / 2];
+          const float keep = up ? a[j + n / 2] : a[j];
+          a[j] = keep + __shfl_xor_sync(kFull, send, off);
+        }
+      }
+      a[0] += __shfl_xor_sync(kFull, a[0], 1);
+      const int idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
+                      ((lane >> 1) & 1);
+      if ((lane & 1) == 0) red[warp * 16 + idx] = a[0];
+      __syncthreads();
+      if (tid < 16 && tc + tid < P.B) {
+        float s = 0.0f;
+#pragma unroll
+        for (int w = 0; w <= kFfnWarps; ++w) s += red[w * 16 + tid];
+        P.logits[static_cast<size_t>(tc + tid) * P.Np + e] = s;
+      }
+      __syncthreads();
+    }
+  }
+  // grid barrier: every CTA's logits / xpad rows are visible after it
+  __syncthreads();
+  if (tid == 0) {
+    stamp(P, 9);
+    __threadfence();
+    atomicAdd(sync_cnt, 1);
+    stamp(P, 10);
+    while (ld_acquire_gpu(sync_cnt) < static_cast<int>(gridDim.x)) __nanosleep(32);
+  }
+  __syncthreads();
+}
+
+// R1 for token t (one warp): the first n_i = min(k0, t_i) ranks (vanilla:
+// the first k) into the token's set row, their e_j = exp(l_j - l_max) and the
+// union bitmap. p == 1 short-circuits t_i = N (routing.cpp:243-245); p < 1
+// uses an fp64 softmax of the fp32 logits (documented best-effort parity).
 template <int E>
-__device__ __forceinline__ void route_phase1_tok(const FfnParams& P, int t, uint8_t* rs,
-                                                 const RouteSmem& L) {
+__device__ __forceinline__ void fz_phase1_tok(const FfnParams& P, int t, uint8_t* rs,
+                                              const RouteSmem& L) {
   const int lane = threadIdx.x & 31;
   const int stride = P.cfg.stride;
-  float* lg = reinterpret_cast<float*>(rs + L.lg) + t * P.Np;
+  const float* lg = reinterpret_cast<const float*>(rs + L.lg) + t * P.Np;
   int* srow = reinterpret_cast<int*>(rs + L.sets) + t * stride;
   float* se = reinterpret_cast<float*>(rs + L.e) + t * stride;
   uint32_t* uni = reinterpret_cast<uint32_t*>(rs + L.uni);
+  const bool vanilla = P.cfg.mode == OEA_MODE_VANILLA;
+  const int want = vanilla ? P.cfg.k : P.cfg.k0;
+  const bool mass_rule = !vanilla && P.cfg.p != 1.0;
   TokRank<E> R;
   tok_load<E>(P.N, lg, R);
   uint32_t key = 0;
   int id = tok_select<E>(R, false, nullptr, key);
   const float rowmax = key32_to_logit(key);
-  int n = 0;
-  if (P.cfg.mode != OEA_MODE_VANILLA) {
-    const bool mass_rule = P.cfg.p != 1.0;
-    double z = 0.0, cum = 0.0;
-    if (mass_rule) {
-      // documented best-effort parity: fp64 softmax of the fp32 logits
+  double z = 0.0, cum = 0.0;
+  if (mass_rule) {
 #pragma unroll
-      for (int j = 0; j < E; ++j)
-        if (R.key[j] != 0u) z += exp(static_cast<double>(key32_to_logit(R.key[j])) - rowmax);
-      for (int off = 16; off > 0; off >>= 1) z += __shfl_xor_sync(kFull, z, off);
+    for (int j = 0; j < E; ++j)
+      if (R.key[j] != 0u) z += exp(static_cast<double>(key32_to_logit(R.key[j])) - rowmax);
+#pragma unroll 1
+    for (int off = 16; off > 0; off >>= 1) z += __shfl_xor_sync(kFull, z, off);
+  }
+  int n = 0;
+#pragma unroll 1
+  while (n < want && id >= 0) {
+    if (lane == 0) {
+      srow[n] = id;
+      se[n] = expf(key32_to_logit(key) - rowmax);
+      atomicOr(&uni[id >> 5], 1u << (id & 31));
     }
-    while (n < P.cfg.k0 && id >= 0) {
-      if (lane == 0) {
-        srow[n] = id;
-        se[n] = expf(key32_to_logit(key) - rowmax);
-        atomicOr(&uni[id >> 5], 1u << (id & 31));
-      }
-      tok_take<E>(R, id);
-      ++n;
-      if (mass_rule) {
-        cum = __dadd_rn(cum, exp(static_cast<double>(key32_to_logit(key)) - rowmax) / z);
-        if (cum >= P.cfg.p) break;
-      }
-      if (n >= P.cfg.k0) break;
-      id = tok_select<E>(R, false, nullptr, key);
+    tok_take<E>(R, id);
+    ++n;
+    if (mass_rule) {
+      cum = __dadd_rn(cum, exp(static_cast<double>(key32_to_logit(key)) - rowmax) / z);
+      if (cum >= P.cfg.p) break;
     }
+    if (n >= want) break;
+    id = tok_select<E>(R, false, nullptr, key);
   }
   if (lane == 0) {
     reinterpret_cast<int*>(rs + L.n)[t] = n;
@@ -387,13 +534,16 @@ __device__ __forceinline__ void route_phase1_tok(const FfnParams& P, int t, uint
   }
 }
 
+// R2 for token t (one warp): piggyback union members of ranks n_i..max_p-1
+// until the cap (Oea / Simplified), then w_j = e_j / sum_set e in set order
+// (fp32), per-expert loads and token bitmaps; CTA 0 exports the plan.
 template <int E>
-__device__ __forceinline__ void route_phase2_tok(const FfnParams& P, int t, uint8_t* rs,
-                                                 const RouteSmem& L, bool exporter) {
+__device__ __forceinline__ void fz_phase2_tok(const FfnParams& P, int t, uint8_t* rs,
+                                              const RouteSmem& L, bool exporter) {
   const int lane = threadIdx.x & 31;
   const int stride = P.cfg.stride;
   const int Bw = (P.B + 31) >> 5;
-  float* lg = reinterpret_cast<float*>(rs + L.lg) + t * P.Np;
+  const float* lg = reinterpret_cast<const float*>(rs + L.lg) + t * P.Np;
   int* srow = reinterpret_cast<int*>(rs + L.sets) + t * stride;
   float* se = reinterpret_cast<float*>(rs + L.e) + t * stride;
   const uint32_t* uni = reinterpret_cast<const uint32_t*>(rs + L.uni);
@@ -401,18 +551,17 @@ __device__ __forceinline__ void route_phase2_tok(const FfnParams& P, int t, uint
   uint32_t* tokbits = reinterpret_cast<uint32_t*>(rs + L.tokbits);
   const int n_i = reinterpret_cast<const int*>(rs + L.n)[t];
   const float rowmax = reinterpret_cast<const float*>(rs + L.mx)[t];
-  TokRank<E> R;
-  tok_load<E>(P.N, lg, R);
-  for (int j = 0; j < n_i; ++j) tok_take<E>(R, srow[j]);
   int len = n_i;
-  uint32_t key = 0;
-  const bool vanilla = P.cfg.mode == OEA_MODE_VANILLA;
-  if (vanilla) len = 0;
-  if (P.cfg.mode != OEA_MODE_PRUNED) {
-    const int cap = vanilla ? P.cfg.k : P.cfg.limit;
-    const bool full_scan = vanilla || P.cfg.max_p >= P.N;
-    while (len < cap) {
-      const int id = tok_select<E>(R, !vanilla, uni, key);
+  if (P.cfg.mode == OEA_MODE_OEA || P.cfg.mode == OEA_MODE_SIMPLIFIED) {
+    TokRank<E> R;
+    tok_load<E>(P.N, lg, R);
+#pragma unroll 1
+    for (int j = 0; j < n_i; ++j) tok_take<E>(R, srow[j]);
+    const bool full_scan = P.cfg.max_p >= P.N;
+    uint32_t key = 0;
+#pragma unroll 1
+    while (len < P.cfg.limit) {
+      const int id = tok_select<E>(R, true, uni, key);
       if (id < 0) break;
       if (!full_scan && tok_rank_of<E>(R, key, id) >= P.cfg.max_p) break;
       if (lane == 0) {
@@ -425,8 +574,10 @@ __device__ __forceinline__ void route_phase2_tok(const FfnParams& P, int t, uint
   }
   __syncwarp();
   float mass = 0.0f;  // sequential fp32 mass in set order
+#pragma unroll 1
   for (int j = 0; j < len; ++j) mass += se[j];
   __syncwarp();
+#pragma unroll 1
   for (int j = lane; j < stride; j += 32) {
     float w = 0.0f;
     if (j < len) {
@@ -449,83 +600,125 @@ __device__ __forceinline__ void route_phase2_tok(const FfnParams& P, int t, uint
     reinterpret_cast<int*>(rs + L.len)[t] = len;
     if (exporter) {
       P.x_set_len[t] = len;
-      if (P.x_phase1_n) P.x_phase1_n[t] = n_i;
+      if (P.x_phase1_n) P.x_phase1_n[t] = P.cfg.mode == OEA_MODE_VANILLA ? 0 : n_i;
     }
   }
 }
 
-// Returns the number of token groups (= active experts).
-__device__ __forceinline__ int route_prologue(const FfnParams& P, uint8_t* rs, const RouteSmem& L) {
+// R1 on all 9 warps; returns T (= the number of expert groups, one per active
+// expert since B <= 64). On return active[]/eslot[] are valid CTA-wide.
+__device__ __forceinline__ int fused_route_phase1(const FfnParams& P, uint8_t* rs, const RouteSmem& L) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int B = P.B, Np = P.Np, N = P.N, stride = P.cfg.stride;
-  const int nthreads = (kFfnWarps + 1) * 32;
+  constexpr int NT = (kFfnWarps + 1) * 32;
+  const int B = P.B, Np = P.Np, N = P.N;
   const int Bw = (B + 31) >> 5;
   float* lg = reinterpret_cast<float*>(rs + L.lg);
   uint32_t* uni = reinterpret_cast<uint32_t*>(rs + L.uni);
   int* loads = reinterpret_cast<int*>(rs + L.loads);
   uint32_t* tokbits = reinterpret_cast<uint32_t*>(rs + L.tokbits);
-  int* len = reinterpret_cast<int*>(rs + L.len);
   int* active = reinterpret_cast<int*>(rs + L.active);
+  int* eslot = reinterpret_cast<int*>(rs + L.eslot);
   int* misc = reinterpret_cast<int*>(rs + L.misc);
   const bool exporter = blockIdx.x == 0;
-  for (int i = threadIdx.x; i < B * Np; i += nthreads) lg[i] = __ldcg(P.logits + i);
-  for (int i = threadIdx.x; i < ((Np + 31) >> 5); i += nthreads) uni[i] = 0u;
-  for (int i = threadIdx.x; i < Np; i += nthreads) loads[i] = 0;
-  for (int i = threadIdx.x; i < Np * Bw; i += nthreads) tokbits[i] = 0u;
+  // B * Np is a multiple of 16: float4 copies, several in flight per thread
+#pragma unroll 4
+  for (int i = threadIdx.x; i < (B * Np) >> 2; i += NT)
+    reinterpret_cast<float4*>(lg)[i] = __ldcg(reinterpret_cast<const float4*>(P.logits) + i);
+#pragma unroll 1
+  for (int i = threadIdx.x; i < ((Np + 31) >> 5); i += NT) uni[i] = 0u;
+#pragma unroll 1
+  for (int i = threadIdx.x; i < Np; i += NT) loads[i] = 0;
+#pragma unroll 1
+  for (int i = threadIdx.x; i < Np * Bw; i += NT) tokbits[i] = 0u;
   __syncthreads();
-  // phase 1 for every real token (all 9 warps)
+  if (threadIdx.x == 0) stamp(P, 11);
+#pragma unroll 1
   for (int t = warp; t < B; t += kFfnWarps + 1) {
     if (P.mask != nullptr && P.mask[t] == 0) {
       if (lane == 0) reinterpret_cast<int*>(rs + L.n)[t] = 0;
       continue;
     }
     if (Np <= 128)
-      route_phase1_tok<4>(P, t, rs, L);
+      fz_phase1_tok<4>(P, t, rs, L);
     else
-      route_phase1_tok<8>(P, t, rs, L);
+      fz_phase1_tok<8>(P, t, rs, L);
   }
   __syncthreads();
-  // active experts = the union (OEA conservation; vanilla: phase 2 decides,
-  // so vanilla plans are compacted after phase 2 below)
-  const bool union_is_active = P.cfg.mode != OEA_MODE_VANILLA;
-  // phase 2 (all warps) — cheap; keeps the code path single
-  for (int t = warp; t < B; t += kFfnWarps + 1) {
+  if (warp == 0) {
+    int T = 0;
+#pragma unroll 1
+    for (int base = 0; base < N; base += 32) {
+      const int e = base + lane;
+      const bool f = e < N && ((uni[e >> 5] >> (e & 31)) & 1u);
+      const unsigned m = __ballot_sync(kFull, f);
+      const int slot = T + __popc(m & lanemask_lt());
+      if (e < N) eslot[e] = f ? slot : -1;
+      if (f) active[slot] = e;
+      if (exporter && f && P.x_base_union && P.cfg.mode != OEA_MODE_VANILLA)
+        P.x_base_union[slot] = e;
+      T += __popc(m);
+    }
+    if (lane == 0) {
+      misc[0] = T;
+      if (exporter && P.x_base_union_count)
+        *P.x_base_union_count = P.cfg.mode == OEA_MODE_VANILLA ? 0 : T;
+    }
+  }
+  __syncthreads();
+  return misc[0];
+}
+
+// R2 on the 8 consumer warps (named barrier 1): sets, weights, loads, then
+// the compaction tables (row base per active expert, token lists in token
+// order, inverse permutation) in shared memory.
+__device__ __forceinline__ void fused_route_phase2(const FfnParams& P, uint8_t* rs, const RouteSmem& L,
+                                                int T) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NC = kFfnWarps * 32;
+  const int B = P.B, N = P.N, stride = P.cfg.stride;
+  const int Bw = (B + 31) >> 5;
+  const bool exporter = blockIdx.x == 0;
+  int* len = reinterpret_cast<int*>(rs + L.len);
+  const int* loads = reinterpret_cast<const int*>(rs + L.loads);
+  const int* active = reinterpret_cast<const int*>(rs + L.active);
+  const int* eslot = reinterpret_cast<const int*>(rs + L.eslot);
+  int* rowb = reinterpret_cast<int*>(rs + L.rowb);
+  int* rows = reinterpret_cast<int*>(rs + L.rows);
+  int* rtok = reinterpret_cast<int*>(rs + L.rtok);
+  int* rslot = reinterpret_cast<int*>(rs + L.rslot);
+  const uint32_t* tokbits = reinterpret_cast<const uint32_t*>(rs + L.tokbits);
+#pragma unroll 1
+  for (int t = warp; t < B; t += kFfnWarps) {
     if (P.mask != nullptr && P.mask[t] == 0) {
       if (lane == 0) len[t] = 0;
-      if (exporter)
+      if (exporter) {
+#pragma unroll 1
         for (int j = lane; j < stride; j += 32) {
           const size_t o = static_cast<size_t>(t) * stride + j;
           P.x_sets[o] = -1;
           P.x_w32[o] = 0.0f;
           if (P.x_w64) P.x_w64[o] = 0.0;
-          if (j == 0) {
-            P.x_set_len[t] = 0;
-            if (P.x_phase1_n) P.x_phase1_n[t] = 0;
-          }
         }
+        if (lane == 0) {
+          P.x_set_len[t] = 0;
+          if (P.x_phase1_n) P.x_phase1_n[t] = 0;
+        }
+      }
       continue;
     }
-    if (Np <= 128)
-      route_phase2_tok<4>(P, t, rs, L, exporter);
+    if (P.Np <= 128)
+      fz_phase2_tok<4>(P, t, rs, L, exporter);
     else
-      route_phase2_tok<8>(P, t, rs, L, exporter);
+      fz_phase2_tok<8>(P, t, rs, L, exporter);
   }
-  (void)union_is_active;
-  __syncthreads();
-  // compaction: warp 0 scans the experts (ascending), groups = active experts
+  asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
   if (warp == 0) {
-    int* eslot = reinterpret_cast<int*>(rs + L.eslot);
-    int* rowb = reinterpret_cast<int*>(rs + L.rowb);
-    int* rows = reinterpret_cast<int*>(rs + L.rows);
-    int* rtok = reinterpret_cast<int*>(rs + L.rtok);
-    int T = 0, R = 0, load = 0;
-    for (int base = 0; base < N; base += 32) {
-      const int e = base + lane;
-      const int m = e < N ? loads[e] : 0;
-      const bool act = m > 0;
-      const unsigned am = __ballot_sync(kFull, act);
-      const int slot = T + __popc(am & lanemask_lt());
-      const int nr = act ? (m + 7) / 8 * 8 : 0;
+    int R = 0, load = 0;
+#pragma unroll 1
+    for (int base = 0; base < T; base += 32) {
+      const int a = base + lane;
+      const int m = a < T ? loads[active[a]] : 0;
+      const int nr = (m + 7) / 8 * 8;
       int ri = nr, li = m;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -536,22 +729,21 @@ __device__ __forceinline__ int route_prologue(const FfnParams& P, uint8_t* rs, c
         }
       }
       const int r0 = R + ri - nr;
-      if (e < N) eslot[e] = act ? slot : -1;
-      if (act) {
-        active[slot] = e;
-        rowb[slot] = r0;
-        rows[slot] = m;
+      if (a < T) {
+        rowb[a] = r0;
+        rows[a] = m;
+#pragma unroll 1
         for (int r = r0 + m; r < r0 + nr; ++r) rtok[r] = -1;
       }
-      if (exporter && e < N) P.x_loads[e] = m;
-      if (exporter && act) P.x_active[slot] = e;
-      T += __popc(am);
       R += __shfl_sync(kFull, ri, 31);
       load += __shfl_sync(kFull, li, 31);
     }
-    if (lane == 0) misc[0] = T;
     if (exporter) {
-      for (int e = T + lane; e < N; e += 32) P.x_active[e] = -1;
+#pragma unroll 1
+      for (int e = lane; e < N; e += 32) {
+        P.x_loads[e] = loads[e];
+        P.x_active[e] = e < T ? active[e] : -1;
+      }
       if (lane == 0) {
         *P.x_active_count = T;
         *P.x_total_load = load;
@@ -561,39 +753,38 @@ __device__ __forceinline__ int route_prologue(const FfnParams& P, uint8_t* rs, c
         P.x_hdr->n_rows = R;
       }
     }
-  } else if (warp == 1 && exporter && (P.x_base_union || P.x_base_union_count)) {
-    int c = 0;
-    for (int base = 0; base < N; base += 32) {
-      const int e = base + lane;
-      const bool f = e < N && ((uni[e >> 5] >> (e & 31)) & 1u);
-      const unsigned m = __ballot_sync(kFull, f);
-      if (f && P.x_base_union) P.x_base_union[c + __popc(m & lanemask_lt())] = e;
-      c += __popc(m);
-    }
-    if (lane == 0 && P.x_base_union_count) *P.x_base_union_count = c;
   }
-  __syncthreads();
-  {
-    const int* sets = reinterpret_cast<const int*>(rs + L.sets);
-    const int* eslot = reinterpret_cast<const int*>(rs + L.eslot);
-    const int* rowb = reinterpret_cast<const int*>(rs + L.rowb);
-    int* rtok = reinterpret_cast<int*>(rs + L.rtok);
-    int* rslot = reinterpret_cast<int*>(rs + L.rslot);
-    for (int idx = threadIdx.x; idx < B * stride; idx += nthreads) {
-      const int t = idx / stride, sl = idx % stride;
-      if (sl < len[t]) {
-        const int e = sets[idx];
-        const uint32_t* bits = tokbits + e * Bw;
-        int rank = __popc(bits[t >> 5] & ((1u << (t & 31)) - 1u));
-        for (int w = 0; w < (t >> 5); ++w) rank += __popc(bits[w]);
-        const int row = rowb[eslot[e]] + rank;
-        rtok[row] = t;
-        rslot[row] = sl;
-      }
+  asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
+  const int* sets = reinterpret_cast<const int*>(rs + L.sets);
+#pragma unroll 1
+  for (int idx = threadIdx.x; idx < B * stride; idx += NC) {
+    const int t = idx / stride, sl = idx % stride;
+    if (sl < len[t]) {
+      const int e = sets[idx];
+      const uint32_t* bits = tokbits + e * Bw;
+      int rank = __popc(bits[t >> 5] & ((1u << (t & 31)) - 1u));
+#pragma unroll 1
+      for (int w = 0; w < (t >> 5); ++w) rank += __popc(bits[w]);
+      const int row = rowb[eslot[e]] + rank;
+      rtok[row] = t;
+      rslot[row] = sl;
     }
   }
-  __syncthreads();
-  return misc[0];
+  asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
+}
+
+// The last CTA to leave resets the grid's counters (round claims, combine /
+// logits barriers, per-group W1 release counters), so the next launch (fused
+// or two-kernel, graph-captured or not) starts from zero. Called by thread 0
+// once its CTA no longer touches any counter.
+__device__ __forceinline__ void grid_exit(const FfnParams& P, int* claims, int G) {
+  __threadfence();
+  if (atomicAdd(&claims[4], 1) == static_cast<int>(gridDim.x) - 1) {
+    for (int g = 0; g < G; ++g) P.w1_done[g] = 0;
+    claims[0] = claims[1] = claims[2] = claims[3] = 0;
+    __threadfence();
+    claims[4] = 0;
+  }
 }
 
 // Round descriptor published by the producer through the stage barrier.
@@ -621,15 +812,15 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
     fence_mbar_init();
   }
   __syncthreads();
-  // Everything below reads the router kernel's outputs.
+  // Everything below reads the router kernel's outputs (two-kernel path).
   pdl_wait();
   if (threadIdx.x == 0) stamp(P, 0);
 
   PlanRef* PR = reinterpret_cast<PlanRef*>(rdesc + kRoundRing);
   uint8_t* rs = reinterpret_cast<uint8_t*>(PR + 1);
   const RouteSmem RL = route_smem_layout(P.B, P.Np, P.stride);
-  if (P.route_in_kernel) {
-    const int g = route_prologue(P, rs, RL);
+  int* claims = P.cnt2 + (P.Dp >> 4);  // [0..1] round claims, [2] combine, [3] logits barrier, [4] exit
+  if (P.fused) {
     if (threadIdx.x == 0) {
       PR->row_tok = reinterpret_cast<const int32_t*>(rs + RL.rtok);
       PR->row_slot = reinterpret_cast<const int32_t*>(rs + RL.rslot);
@@ -638,7 +829,13 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
       PR->group_rows = reinterpret_cast<const int32_t*>(rs + RL.rows);
       PR->set_len = reinterpret_cast<const int32_t*>(rs + RL.len);
       PR->wts = reinterpret_cast<const float*>(rs + RL.e);
-      PR->G = g;
+    }
+    fused_gemv(P, reinterpret_cast<float*>(rs + RL.red), claims + 3);
+    if (threadIdx.x == 0) stamp(P, 5);
+    const int T = fused_route_phase1(P, rs, RL);  // ends with __syncthreads
+    if (threadIdx.x == 0) {
+      PR->G = T;
+      stamp(P, 6);
     }
   } else if (threadIdx.x == 0) {
     PR->row_tok = P.row_tok;
@@ -653,8 +850,14 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
   __syncthreads();
   const int G = PR->G;
   if (G == 0) {
-    if (P.route_in_kernel && blockIdx.x == 0)
-      for (int f = threadIdx.x; f < P.B * P.D; f += (kFfnWarps + 1) * 32) P.out[f] = 0.0f;
+    if (P.fused) {
+      if (blockIdx.x == 0)
+        for (int f = threadIdx.x; f < P.B * P.D; f += (kFfnWarps + 1) * 32) P.out[f] = 0.0f;
+      if (warp < kFfnWarps) {
+        fused_route_phase2(P, rs, RL, 0);  // exports the (empty) plan
+        if (threadIdx.x == 0) grid_exit(P, claims, 0);
+      }
+    }
     return;
   }
   const int KT1 = P.Dp >> 4, KT2 = P.Hp >> 4;
@@ -665,7 +868,6 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
   // A CTA therefore finishes its own W1 rounds before it starts W2 rounds,
   // and W2 units only wait for W1 units claimed earlier (by any CTA), so the
   // acquire-waits cannot deadlock; faster SMs simply claim more rounds.
-  int* claims = P.cnt2 + RB2;
 
   int stage = 0;
   uint32_t phase = 0;
@@ -733,6 +935,10 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
   }
 
   // ---------------- consumers ----------------
+  if (P.fused) {
+    fused_route_phase2(P, rs, RL, G);  // overlaps the producer's first stages
+    if (threadIdx.x == 0) stamp(P, 7);
+  }
   bool in_w2 = false;
   for (int seq = 0;; ++seq) {
     mbar_wait(&full[stage], phase);  // the round's first stage carries its descriptor
@@ -779,6 +985,7 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
     __threadfence();
     atomicAdd(done, 1);
     while (ld_acquire_gpu(done) < static_cast<int>(gridDim.x)) __nanosleep(128);
+    grid_exit(P, claims, G);
   }
   asm volatile("bar.sync 1, %0;" ::"r"(kFfnWarps * 32) : "memory");
   const int64_t BD = static_cast<int64_t>(P.B) * P.D;
@@ -954,7 +1161,11 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   P.out = static_cast<float*>(fb.out);
   P.trace = fb.trace;
   P.mode = fb.mode;
-  P.route_in_kernel = fb.route_in_kernel;
+  P.fused = fb.fused;
+  P.xnc = fb.xnc;
+  P.router_t = static_cast<const uint4*>(L->router_t);
+  P.x_in = fb.x_in;
+  P.xpad_out = fb.xpad_out;
   P.logits = fb.logits;
   P.mask = fb.mask;
   P.N = L->N;
@@ -974,7 +1185,7 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   P.x_hdr = fb.x_hdr;
 
   const size_t smem = ffn_bf16_smem_bytes() +
-                      (fb.route_in_kernel ? ffn_route_smem_bytes(B, L->Np, stride) : 0);
+                      (fb.fused ? ffn_route_smem_bytes(B, L->Np, stride) : 0);
   OEA_CUDA_TRY(ctx, cudaFuncSetAttribute(k_ffn_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
   cudaLaunchConfig_t cfg = {};

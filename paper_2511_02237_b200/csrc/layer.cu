@@ -168,6 +168,18 @@ __global__ void k_init_matrix(uint64_t key, uint64_t base, int rows, int cols, d
   }
 }
 
+// Expert-major router copy for the fused gate GEMV: router_t[n][d] = R[d][n]
+// (zero padding included), unpacked from the fragment-ordered tiles.
+__global__ void k_router_unpack(const __nv_bfloat16* __restrict__ frag, int Np, int Dp,
+                                __nv_bfloat16* __restrict__ out) {
+  const size_t total = static_cast<size_t>(Np) * Dp;
+  for (size_t f = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; f < total;
+       f += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int n = static_cast<int>(f / Dp), d = static_cast<int>(f % Dp);
+    out[f] = frag[router_frag_idx(d, n, Dp)];
+  }
+}
+
 }  // namespace oea_dev
 
 namespace oea_host {
@@ -242,12 +254,24 @@ static int pack_or_convert(oea_layer* L, const void* src, int rows, int cols, in
   return OEA_OK;
 }
 
+int layer_router_refresh(oea_layer* L) {
+  if (L->router_t == nullptr) return OEA_OK;
+  oea_ctx* ctx = L->ctx;
+  const size_t n = static_cast<size_t>(L->Np) * L->Dp;
+  k_router_unpack<<<grid_for(n), 256, 0, ctx->stream>>>(
+      static_cast<const __nv_bfloat16*>(L->router), L->Np, L->Dp,
+      static_cast<__nv_bfloat16*>(L->router_t));
+  OEA_LAUNCHED(ctx);
+  return OEA_OK;
+}
+
 int layer_upload_router(oea_layer* L, const void* src, int src_dtype, int on_device) {
   oea_ctx* ctx = L->ctx;
   Staged st;
   int rc = stage(ctx, src, static_cast<size_t>(L->D) * L->N * dtype_size(src_dtype), on_device, st);
   if (rc) return rc;
   rc = pack_or_convert(L, st.p, L->D, L->N, 0, src_dtype, L->router);
+  if (!rc) rc = layer_router_refresh(L);
   if (rc) return rc;
   OEA_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   return OEA_OK;
@@ -332,7 +356,12 @@ int layer_init_random(oea_layer* L, uint64_t seed) {
   uint64_t h = 0x853C49E6748FEA9Bull;
   h = host_splitmix64(h + 0x9E3779B97F4A7C15ull + seed);
   h = host_splitmix64(h + 0x9E3779B97F4A7C15ull + 101);
-  if (L->dtype == OEA_DTYPE_BF16) return init_all<__nv_bfloat16>(L, h);
+  if (L->dtype == OEA_DTYPE_BF16) {
+    int rc = init_all<__nv_bfloat16>(L, h);
+    if (!rc) rc = layer_router_refresh(L);
+    if (!rc) OEA_CUDA_TRY(L->ctx, cudaStreamSynchronize(L->ctx->stream));
+    return rc;
+  }
   if (L->dtype == OEA_DTYPE_F32) return init_all<float>(L, h);
   return init_all<double>(L, h);
 }

@@ -87,6 +87,7 @@ struct oea_layer {
   int Dp = 0, Hp = 0, Np = 0;  // padded (bf16 fragment layout)
   // bf16: fragment-ordered weights. f32/f64: reference layout.
   void* router = nullptr;      // bf16: [Np/16][Dp/16][32][8]; else [D][N]
+  void* router_t = nullptr;    // bf16 only: [Np][Dp] expert-major copy (fused gate GEMV)
   void* w1 = nullptr;          // bf16: [N][Hp/8][Dp/16][32][8] (gate|up); else gate [N][D][H]
   void* w_up = nullptr;        // f32/f64 only: [N][D][H]
   void* w2 = nullptr;          // bf16: [N][Dp/16][Hp/16][32][8]; else down [N][H][D]
@@ -191,10 +192,13 @@ struct FfnBuffers {
   void* out;               // [B][D] f32 (bf16 path) / f64 (simt)
   unsigned long long* trace = nullptr;  // debug timeline (OEA_FFN_TRACE)
   int mode = 0;                         // debug mode (OEA_FFN_MODE)
-  // In-kernel routing (B small): the FFN routes the batch from the logits in
-  // its prologue; the plan is exported by CTA 0.
-  int route_in_kernel = 0;
-  const float* logits = nullptr;        // [B][Np]
+  // Fused single-launch decode (B <= 64): the FFN grid computes the logits
+  // (gate GEMV), routes the batch in every CTA and exports the plan (CTA 0).
+  int fused = 0;
+  int xnc = 1;                          // x read-only for the kernel (ld.global.nc ok)
+  const __nv_bfloat16* x_in = nullptr;  // [B][D] caller tokens
+  __nv_bfloat16* xpad_out = nullptr;    // [B][Dp] when D != Dp
+  float* logits = nullptr;              // [B][Np]
   const uint8_t* mask = nullptr;
   oea_dev::Cfg cfg{};
   int32_t* x_sets = nullptr;
@@ -245,7 +249,6 @@ struct FusedRouterBuffers {
   int32_t* base_union;      // [N] may be null
   int32_t* base_union_count;
   unsigned long long* trace = nullptr;
-  int logits_only = 0;
 };
 size_t router_fused_smem_bytes(int B, int Np, int Dp, int stride);
 int router_fused_launch(oea_ctx* ctx, const oea_layer* L, const oea_dev::Cfg& cfg, int B,
@@ -256,6 +259,7 @@ int layer_upload_router(oea_layer* L, const void* src, int src_dtype, int on_dev
 int layer_upload_expert(oea_layer* L, int e, const void* wg, const void* wu, const void* wd,
                         int src_dtype, int on_device);
 int layer_init_random(oea_layer* L, uint64_t seed);
+int layer_router_refresh(oea_layer* L);  // router_t from the fragment-ordered router
 int layer_download_router(oea_layer* L, void* dst, int dst_dtype);
 int layer_download_expert(oea_layer* L, int e, void* wg, void* wu, void* wd, int dst_dtype);
 

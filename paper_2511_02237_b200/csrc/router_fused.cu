@@ -269,7 +269,6 @@ struct RouterParams {
   int32_t* base_union_count;
   unsigned long long* trace;  // debug: rows 1000+rank of the FFN trace buffer
   int late_trigger;           // debug: launch the FFN only at the end (OEA_LATE_TRIGGER)
-  int logits_only;            // 1: only the GEMV (the FFN routes in its prologue)
 };
 
 __device__ __forceinline__ void rstamp(const RouterParams& P, int rank, int slot) {
@@ -779,12 +778,6 @@ __global__ void __cluster_dims__(kRouterCluster, 1, 1) __launch_bounds__(kRouter
     cluster.sync();  // partials may be overwritten by the next chunk
   }
   rstamp(P, crank, 4);
-  if (P.logits_only) {
-    // the FFN kernel routes in its prologue; reset its counters here
-    if (crank == 0)
-      for (int c = threadIdx.x; c < P.n_counters; c += kRouterThreads) P.counters[c] = 0;
-    return;
-  }
   __syncthreads();
 
   // ---- 2. routing, distributed: each CTA ranks its own tokens ----
@@ -867,7 +860,6 @@ int router_fused_launch(oea_ctx* ctx, const oea_layer* L, const Cfg& cfg, int B,
   P.base_union_count = rb.base_union_count;
   P.trace = rb.trace;
   P.late_trigger = getenv("OEA_LATE_TRIGGER") != nullptr;
-  P.logits_only = rb.logits_only;
   const size_t smem = router_fused_smem_bytes(B, L->Np, L->Dp, cfg.stride);
   if (cfg.p != 1.0 && cfg.mode != OEA_MODE_VANILLA) {
     OEA_CUDA_TRY(ctx, cudaFuncSetAttribute(k_router_fused<true>,

@@ -17,7 +17,7 @@ for name, cfg in (("oea", oea.RoutingConfig.simplified(4, 8)), ("vanilla", oea.R
         L.ctx.synchronize()
     buf = np.zeros(8 * 1024, np.uint64)
     L.ctx.check(lib().oea_debug_ffn_trace(L.ctx.h, buf.ctypes.data_as(C.c_void_p), buf.size))
-    t = buf.reshape(1024, 8)[:148].astype(np.int64)
+    t = buf[:148 * 16].reshape(148, 16).astype(np.int64)
     base = t[:, 0].min()
     rel = (t - base) / 1000.0
     def st(a): return f"min {a.min():7.1f} med {np.median(a):7.1f} max {a.max():7.1f}"
@@ -27,6 +27,14 @@ for name, cfg in (("oea", oea.RoutingConfig.simplified(4, 8)), ("vanilla", oea.R
     print(" W2 1st rdy ", st(rel[:, 2]))
     print(" end        ", st(rel[:, 3]))
     print(" prod done  ", st(rel[:, 4]))
+    if t[:, 5].any():
+        print(" fused: gemv start (xpad)  ", st(rel[:, 8]))
+        print(" fused: gemv done          ", st(rel[:, 9]))
+        print(" fused: barrier arrived    ", st(rel[:, 10]))
+        print(" fused: logits barrier passed", st(rel[:, 5]))
+        print(" fused: logits in smem     ", st(rel[:, 11]))
+        print(" fused: union known (phase 1)", st(rel[:, 6]))
+        print(" fused: plan ready (phase 2) ", st(rel[:, 7]))
     r = buf.reshape(1024, 8)[1000:1008].astype(np.int64)
     r0 = r[0, 0]
     print(" router CTA stamps (us from CTA0 start): start, x-staged, gemv, sync1, end-gemv, routed, compacted")
