@@ -396,7 +396,6 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   fb.mode = ctx->ffn_mode;
   if (fused) {
     fb.fused = 1;
-    fb.xnc = padded ? 0 : 1;
     fb.x_in = static_cast<const __nv_bfloat16*>(x);
     fb.xpad_out = padded ? w.xpad : nullptr;
     fb.logits = w.logits;

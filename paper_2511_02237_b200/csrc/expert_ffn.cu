@@ -62,7 +62,6 @@ struct FfnParams {
   int mode;                   // debug: 1 = stream weights only (no math)
   // Fused single-launch decode (see fused_gemv / fused_route_phase1/2).
   int fused;
-  int xnc;                      // x is read-only for the kernel (non-coherent loads ok)
   const uint4* router_t;        // [Np][Dp/8] expert-major bf16 router
   const __nv_bfloat16* x_in;    // [B][D] caller tokens
   __nv_bfloat16* xpad_out;      // [B][Dp], written in-kernel when D != Dp, else null
@@ -124,6 +123,9 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
   const int RB1 = P.Hp >> 3;
 
   // B-operand row pointers (u32 view) for this lane's token in each n-block.
+  // x rows are read through the non-coherent path: on the fused path the
+  // zero-padded copy (D != Dp) is written before the logits grid barrier and
+  // first read after it, so no stale line can exist in this SM's L1.
   const uint32_t* bp[NB];
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb) {
@@ -170,7 +172,7 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
       for (int nb = 0; nb < NB; ++nb) {
         uint32_t b0 = 0, b1 = 0;
         if (bp[nb] != nullptr) {
-          if (W1 && P.xnc) {
+          if (W1) {
             b0 = __ldg(bp[nb] + kt * 8 + q);
             b1 = __ldg(bp[nb] + kt * 8 + 4 + q);
           } else {
@@ -202,7 +204,7 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
             b0 = bf[kPref ? j : 0][nb][0];
             b1 = bf[kPref ? j : 0][nb][1];
           } else if (bp[nb] != nullptr) {
-            if (W1 && P.xnc) {
+            if (W1) {
               b0 = __ldg(bp[nb] + kt * 8 + q);
               b1 = __ldg(bp[nb] + kt * 8 + 4 + q);
             } else {
@@ -1162,7 +1164,6 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   P.trace = fb.trace;
   P.mode = fb.mode;
   P.fused = fb.fused;
-  P.xnc = fb.xnc;
   P.router_t = static_cast<const uint4*>(L->router_t);
   P.x_in = fb.x_in;
   P.xpad_out = fb.xpad_out;

@@ -195,7 +195,6 @@ struct FfnBuffers {
   // Fused single-launch decode (B <= 64): the FFN grid computes the logits
   // (gate GEMV), routes the batch in every CTA and exports the plan (CTA 0).
   int fused = 0;
-  int xnc = 1;                          // x read-only for the kernel (ld.global.nc ok)
   const __nv_bfloat16* x_in = nullptr;  // [B][D] caller tokens
   __nv_bfloat16* xpad_out = nullptr;    // [B][Dp] when D != Dp
   float* logits = nullptr;              // [B][Np]
