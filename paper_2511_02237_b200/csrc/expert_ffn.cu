@@ -112,6 +112,7 @@ struct Unit {
   int rb;      // row block
   int row0;    // first padded row of the group
   int rows;    // real rows (tokens) in the group
+  int ready;   // W2: the group's h is known complete (acquired by the producer)
 };
 
 template <int NB, bool W1>
@@ -122,11 +123,15 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
   const int g = lane >> 2, q = lane & 3;
   const int RB1 = P.Hp >> 3;
 
-  // B-operand row pointers (u32 view) for this lane's token in each n-block.
+  // B-operand rows (uint4 view) for this lane's token in each n-block. The
+  // weights are packed with the k-permutation of layer.cu (kperm): in every
+  // 128-wide K slice (one pipeline stage) lane quad q of k-tile j covers
+  // k = 32q + 4j .. 32q + 4j + 3, so the lane's B operand for a whole stage is
+  // ONE contiguous 64-byte run of its token row: 4 x 16-byte loads.
   // x rows are read through the non-coherent path: on the fused path the
   // zero-padded copy (D != Dp) is written before the logits grid barrier and
   // first read after it, so no stale line can exist in this SM's L1.
-  const uint32_t* bp[NB];
+  const uint4* bp[NB];
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb) {
     const int r = nb * 8 + g;
@@ -134,20 +139,22 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
     if (r < U.rows) {
       if (W1) {
         const int t = PR->row_tok[U.row0 + r];
-        bp[nb] = reinterpret_cast<const uint32_t*>(P.xpad + static_cast<size_t>(t) * P.Dp);
+        bp[nb] = reinterpret_cast<const uint4*>(P.xpad + static_cast<size_t>(t) * P.Dp) + 4 * q;
       } else {
-        bp[nb] = reinterpret_cast<const uint32_t*>(P.hbuf + static_cast<size_t>(U.row0 + r) * P.Hp);
+        bp[nb] = reinterpret_cast<const uint4*>(P.hbuf + static_cast<size_t>(U.row0 + r) * P.Hp) +
+                 4 * q;
       }
     }
   }
-  if (!W1) {
+  if (!W1 && !U.ready) {
     // h of this token group must be complete (all RB1 W1 units released):
     // lane 0 acquires, the warp barrier orders the other lanes after it.
+    // (U.ready: the producer already acquired it when it issued the round.)
     if (lane == 0)
       while (ld_acquire_gpu(&P.w1_done[U.g]) < RB1) __nanosleep(64);
     __syncwarp();
-    if (warp == 0 && lane == 0 && P.trace && P.trace[blockIdx.x * 16 + 2] == 0) stamp(P, 2);
   }
+  if (!W1 && warp == 0 && lane == 0 && P.trace && P.trace[blockIdx.x * 16 + 2] == 0) stamp(P, 2);
 
   // two accumulator sets (even / odd k-tiles) halve the dependent HMMA chain
   float acc2[2][NB][4];
@@ -157,65 +164,52 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
     for (int nb = 0; nb < NB; ++nb)
       acc2[h2][nb][0] = acc2[h2][nb][1] = acc2[h2][nb][2] = acc2[h2][nb][3] = 0.0f;
 
-  // B fragments (x for W1, h for W2) do not depend on the streamed A tiles:
-  // for small n-block counts the next stage's fragments are loaded right after
-  // the current stage is consumed, so their latency hides behind the stage
-  // barrier wait (single register buffer, software pipelined).
-  constexpr bool kPref = NB <= 1;  // NB=2 would spill at the 168-register cap (9 warps)
-  constexpr int KB = kPref ? kKtPerSlot : 1;
-  uint32_t bf[KB][NB][2];
-  auto load_b = [&](int s) {
-#pragma unroll
-    for (int j = 0; j < KB; ++j) {
-      const int kt = s * kKtPerSlot + j;
-#pragma unroll
-      for (int nb = 0; nb < NB; ++nb) {
-        uint32_t b0 = 0, b1 = 0;
-        if (bp[nb] != nullptr) {
-          if (W1) {
-            b0 = __ldg(bp[nb] + kt * 8 + q);
-            b1 = __ldg(bp[nb] + kt * 8 + 4 + q);
-          } else {
-            b0 = __ldcg(bp[nb] + kt * 8 + q);
-            b1 = __ldcg(bp[nb] + kt * 8 + 4 + q);
-          }
-        }
-        bf[j][nb][0] = b0;
-        bf[j][nb][1] = b1;
-      }
-    }
+  auto ldb = [&](const uint4* p) -> uint4 {
+    if (p == nullptr) return make_uint4(0u, 0u, 0u, 0u);
+    return W1 ? __ldg(p) : __ldcg(p);
   };
+  // One n-block: the next stage's 4 loads are issued right after the current
+  // stage is consumed, so their latency hides behind the stage barrier wait.
+  // More n-blocks: per quarter stage (2 k-tiles) one 16-byte load per n-block.
+  constexpr bool kPref = NB <= 1;
+  uint4 bpre[4];
   const bool math = P.mode != 1;
-  if (kPref && math) load_b(0);
+  if (kPref && math)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) bpre[i] = ldb(bp[0] == nullptr ? nullptr : bp[0] + i);
 
   for (int s = 0; s < nst; ++s) {
     mbar_wait(&full[stage], phase);
     const uint4* tiles =
         reinterpret_cast<const uint4*>(ring + stage * kStageBytes + warp * kSlotBytes);
     if (math) {
+      if (kPref) {
 #pragma unroll
-      for (int j = 0; j < kKtPerSlot; ++j) {
-        const uint4 a = tiles[j * 32 + lane];
-        const int kt = s * kKtPerSlot + j;
+        for (int j = 0; j < kKtPerSlot; ++j) {
+          const uint4 a = tiles[j * 32 + lane];
+          const uint4& v = bpre[j >> 1];
+          mma_bf16_16816(acc2[j & 1][0], a, (j & 1) ? v.z : v.x, (j & 1) ? v.w : v.y);
+        }
+        if (s + 1 < nst)
 #pragma unroll
-        for (int nb = 0; nb < NB; ++nb) {
-          uint32_t b0 = 0, b1 = 0;
-          if (kPref) {
-            b0 = bf[kPref ? j : 0][nb][0];
-            b1 = bf[kPref ? j : 0][nb][1];
-          } else if (bp[nb] != nullptr) {
-            if (W1) {
-              b0 = __ldg(bp[nb] + kt * 8 + q);
-              b1 = __ldg(bp[nb] + kt * 8 + 4 + q);
-            } else {
-              b0 = __ldcg(bp[nb] + kt * 8 + q);
-              b1 = __ldcg(bp[nb] + kt * 8 + 4 + q);
-            }
+          for (int i = 0; i < 4; ++i)
+            bpre[i] = ldb(bp[0] == nullptr ? nullptr : bp[0] + (s + 1) * 16 + i);
+      } else {
+#pragma unroll
+        for (int jj = 0; jj < kKtPerSlot / 2; ++jj) {
+          uint4 v[NB];
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb)
+            v[nb] = ldb(bp[nb] == nullptr ? nullptr : bp[nb] + s * 16 + jj);
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const uint4 a = tiles[(2 * jj + h2) * 32 + lane];
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb)
+              mma_bf16_16816(acc2[h2][nb], a, h2 ? v[nb].z : v[nb].x, h2 ? v[nb].w : v[nb].y);
           }
-          mma_bf16_16816(acc2[j & 1][nb], a, b0, b1);
         }
       }
-      if (kPref && s + 1 < nst) load_b(s + 1);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);
@@ -246,12 +240,10 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
         }
       }
     }
-    // release: warp barrier (orders the lanes' stores) + one gpu-scope fence
+    // release: the warp barrier orders the lanes' h stores before lane 0's
+    // gpu-scope release increment (cumulative; no full fence, no L1 flush)
     __syncwarp();
-    if (lane == 0) {
-      __threadfence();
-      atomicAdd(&P.w1_done[U.g], 1);
-    }
+    if (lane == 0) red_release_gpu_add(&P.w1_done[U.g], 1);
   } else {
     const int d0 = U.rb * 16;
 #pragma unroll
@@ -794,7 +786,7 @@ struct RoundDesc {
   int u0;    // first unit
   int n;     // units (one per consumer warp); 0 = end of work
   int kind;  // 1 = W1, 2 = W2
-  int pad;
+  int ready; // W2: the group's h was acquired complete by the producer
 };
 constexpr int kRoundRing = 8;  // > kStages: a round spans >= 1 stage
 
@@ -921,9 +913,20 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
                             (static_cast<size_t>(PR->group_a[g]) * RB + rr * kFfnWarps) * KT * 32;
         for (int s = 0; s < nst; ++s) {
           if (s > 0) mbar_wait(&empty[stage], phase ^ 1u);
-          mbar_arrive_expect_tx(&full[stage], d.n * kSlotBytes);
-          bulk_g2s(ring + stage * kStageBytes, base + static_cast<size_t>(s) * kFfnWarps * kKtPerSlot * 32,
-                   d.n * kSlotBytes, &full[stage], pol);
+          if (s == 0 && !is1) {
+            // W2: while the first stage is in flight, check (non-blocking) that
+            // the group's h is complete; the descriptor is published by the
+            // arrive below, and consumers skip their own acquire-wait
+            mbar_expect_tx(&full[stage], d.n * kSlotBytes);
+            bulk_g2s(ring + stage * kStageBytes, base, d.n * kSlotBytes, &full[stage], pol);
+            rdesc[seq & (kRoundRing - 1)].ready = ld_acquire_gpu(&P.w1_done[g]) >= RB1;
+            mbar_arrive(&full[stage]);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], d.n * kSlotBytes);
+            bulk_g2s(ring + stage * kStageBytes,
+                     base + static_cast<size_t>(s) * kFfnWarps * kKtPerSlot * 32, d.n * kSlotBytes,
+                     &full[stage], pol);
+          }
           if (s == 0) next = claim();  // overlap the next claim with this round
           if (++stage == kStages) {
             stage = 0;
@@ -965,6 +968,7 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
       }
       U.row0 = PR->group_row0[U.g];
       U.rows = PR->group_rows[U.g];
+      U.ready = d.ready;
       const int nbk = (U.rows + 7) >> 3;
       if (is1)
         dispatch_unit<true>(nbk, P, PR, ring, full, empty, stage, phase, nst, U);

@@ -67,12 +67,27 @@ __device__ __forceinline__ size_t round_tile(int rb, int kt, int KT) {
   const int S = KT / kKtPerSlot;
   return ((static_cast<size_t>(rr) * S + s) * kFfnWarps + w) * kKtPerSlot + j;
 }
+// Expert K permutation: inside every 128-wide K slice (one FFN pipeline
+// stage) k-tile j's fragment columns {2q, 2q+1, 2q+8, 2q+9} (the ones mma
+// lane quad q holds) carry k = 32q + 4j + {0, 1, 2, 3}. The contraction is
+// unchanged (A and B see the same order) and a lane's B operand for a whole
+// stage becomes one contiguous 64-byte run of the token row.
+__device__ __forceinline__ void kperm(int k, int& kt, int& c) {
+  const int s = k >> 7, w = k & 127;
+  const int q = w >> 5, j = (w >> 2) & 7, e = w & 3;
+  kt = s * 8 + j;
+  c = 2 * q + (e & 1) + ((e >> 1) << 3);
+}
 __device__ __forceinline__ size_t w1_frag_idx(int d, int h, int up, int Dp) {
-  const int rb = h >> 3, r = (h & 7) + (up ? 8 : 0), kt = d >> 4, c = d & 15;
+  const int rb = h >> 3, r = (h & 7) + (up ? 8 : 0);
+  int kt, c;
+  kperm(d, kt, c);
   return round_tile(rb, kt, Dp >> 4) * 256 + frag_offset(r, c);
 }
 __device__ __forceinline__ size_t w2_frag_idx(int h, int d, int Hp) {
-  const int rb = d >> 4, r = d & 15, kt = h >> 4, c = h & 15;
+  const int rb = d >> 4, r = d & 15;
+  int kt, c;
+  kperm(h, kt, c);
   return round_tile(rb, kt, Hp >> 4) * 256 + frag_offset(r, c);
 }
 
