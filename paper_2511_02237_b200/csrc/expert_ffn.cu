@@ -157,9 +157,12 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
   if (!W1 && warp == 0 && lane == 0 && P.trace && P.trace[blockIdx.x * 16 + 2] == 0) stamp(P, 2);
 
   // two accumulator sets (even / odd k-tiles) halve the dependent HMMA chain
-  float acc2[2][NB][4];
+  // (one n-block: two sets halve the dependent HMMA chain; more n-blocks
+  // already interleave independent chains, so they use one set)
+  constexpr int NA = NB == 1 ? 2 : 1;
+  float acc2[NA][NB][4];
 #pragma unroll
-  for (int h2 = 0; h2 < 2; ++h2)
+  for (int h2 = 0; h2 < NA; ++h2)
 #pragma unroll
     for (int nb = 0; nb < NB; ++nb)
       acc2[h2][nb][0] = acc2[h2][nb][1] = acc2[h2][nb][2] = acc2[h2][nb][3] = 0.0f;
@@ -188,7 +191,7 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
         for (int j = 0; j < kKtPerSlot; ++j) {
           const uint4 a = tiles[j * 32 + lane];
           const uint4& v = bpre[j >> 1];
-          mma_bf16_16816(acc2[j & 1][0], a, (j & 1) ? v.z : v.x, (j & 1) ? v.w : v.y);
+          mma_bf16_16816(acc2[(j & 1) % NA][0], a, (j & 1) ? v.z : v.x, (j & 1) ? v.w : v.y);
         }
         if (s + 1 < nst)
 #pragma unroll
@@ -206,7 +209,7 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
             const uint4 a = tiles[(2 * jj + h2) * 32 + lane];
 #pragma unroll
             for (int nb = 0; nb < NB; ++nb)
-              mma_bf16_16816(acc2[h2][nb], a, h2 ? v[nb].z : v[nb].x, h2 ? v[nb].w : v[nb].y);
+              mma_bf16_16816(acc2[h2 % NA][nb], a, h2 ? v[nb].z : v[nb].x, h2 ? v[nb].w : v[nb].y);
           }
         }
       }
@@ -223,7 +226,7 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) acc[nb][i] = acc2[0][nb][i] + acc2[1][nb][i];
+    for (int i = 0; i < 4; ++i) acc[nb][i] = NA == 2 ? acc2[0][nb][i] + acc2[1][nb][i] : acc2[0][nb][i];
 
   if (W1) {
     // Thread (g, q) holds gate[h][tok 2q, 2q+1] (c0, c1) and up[h][...] (c2, c3)

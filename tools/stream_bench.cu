@@ -5,6 +5,7 @@
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o stream_bench tools/stream_bench.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -35,7 +36,7 @@ __device__ __forceinline__ void bulk_nohint(void* dst, const void* src, uint32_t
 // Each CTA streams its contiguous share; a stage = `copies` bulk copies of
 // `chunk` bytes; `stages` deep ring; consumers = 8 warps that just release.
 __global__ void k_tma(const uint8_t* src, size_t total, int chunk, int copies, int stages, int hint,
-                      int stride_mode) {
+                      int stride_mode, int hold) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int stage_bytes = chunk * copies;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
@@ -73,6 +74,10 @@ __global__ void k_tma(const uint8_t* src, size_t total, int chunk, int copies, i
   int st = 0; uint32_t ph = 0;
   for (size_t i = 0; i < nstage; ++i) {
     mbar_wait(&full[st], ph);
+    if (hold) {  // emulate the consumer's per-stage math: hold the slot `hold` cycles
+      const long long t0 = clock64();
+      while (clock64() - t0 < hold) {}
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
     if (++st == stages) { st = 0; ph ^= 1u; }
@@ -100,34 +105,29 @@ int main() {
   unsigned long long* sink; cudaMalloc(&sink, 8);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  auto run_tma = [&](int chunk, int copies, int stages, int ctas_per_sm, int hint, int stride_mode) {
+  auto run_tma = [&](int chunk, int copies, int stages, int ctas_per_sm, int hint, int stride_mode, int hold = 0) {
     const int smem = chunk * copies * stages + 2 * stages * 8;
     cudaFuncSetAttribute(k_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int grid = sms * ctas_per_sm;
-    for (int w = 0; w < 2; ++w) k_tma<<<grid, 288, smem>>>(buf[w], total, chunk, copies, stages, hint, stride_mode);
+    for (int w = 0; w < 2; ++w) k_tma<<<grid, 288, smem>>>(buf[w], total, chunk, copies, stages, hint, stride_mode, hold);
     cudaEventRecord(e0);
     const int reps = 8;
-    for (int r = 0; r < reps; ++r) k_tma<<<grid, 288, smem>>>(buf[r % 4], total, chunk, copies, stages, hint, stride_mode);
+    for (int r = 0; r < reps; ++r) k_tma<<<grid, 288, smem>>>(buf[r % 4], total, chunk, copies, stages, hint, stride_mode, hold);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     cudaError_t err = cudaGetLastError();
-    printf("tma chunk=%6d copies=%d stages=%d (ring %3d KiB) ctas/sm=%d hint=%d mode=%d : %7.1f GB/s %s\n", chunk, copies,
-           stages, smem >> 10, ctas_per_sm, hint, stride_mode, reps * (double)((total / grid) & ~((size_t(1) << 20) - 1)) * grid / (ms * 1e6), err ? cudaGetErrorString(err) : "");
+    printf("tma chunk=%6d copies=%d stages=%d (ring %3d KiB) ctas/sm=%d hint=%d mode=%d hold=%5d : %7.1f GB/s %s\n", chunk, copies,
+           stages, smem >> 10, ctas_per_sm, hint, stride_mode, hold, reps * (double)((total / grid) & ~((size_t(1) << 20) - 1)) * grid / (ms * 1e6), err ? cudaGetErrorString(err) : "");
   };
-  run_tma(4096, 8, 6, 1, 1, 1);   // current FFN pattern
-  run_tma(4096, 8, 6, 1, 1, 0);
-  run_tma(4096, 8, 6, 1, 0, 1);
-  run_tma(32768, 1, 6, 1, 1, 0);
-  run_tma(16384, 2, 6, 1, 1, 0);
-  run_tma(8192, 4, 6, 1, 1, 0);
-  run_tma(4096, 8, 3, 1, 1, 0);
-  run_tma(4096, 4, 12, 1, 1, 0);
-  run_tma(8192, 8, 3, 1, 1, 0);
-  run_tma(16384, 8, 1, 1, 1, 0);
-  run_tma(65536, 1, 3, 1, 1, 0);
-  run_tma(4096, 8, 3, 2, 1, 0);
-  run_tma(8192, 4, 3, 2, 1, 0);
-  run_tma(2048, 8, 6, 2, 1, 0);
+  // the FFN's pattern: one 32 KiB copy per stage; ring depth x consumer hold
+  for (int stages : {3, 4, 5, 6})
+    for (int hold : {0, 500, 1000, 2000})
+      run_tma(32768, 1, stages, 1, 1, 0, hold);
+  run_tma(65536, 1, 3, 1, 1, 0, 0);
+  run_tma(65536, 1, 3, 1, 1, 0, 1000);
+  run_tma(16384, 1, 8, 1, 1, 0, 0);
+  run_tma(16384, 1, 8, 1, 1, 0, 1000);
+  if (getenv("LDG_TOO") == nullptr) return 0;
   for (int threads : {256, 512, 1024}) {
     for (int cps : {1, 2, 4}) {
       k_ldg<<<sms * cps, threads>>>(reinterpret_cast<uint4*>(buf[0]), total / 16, sink);
