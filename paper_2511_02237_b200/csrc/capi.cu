@@ -366,7 +366,11 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   // the batch in every CTA and streams the union's weights as soon as it is
   // known (expert_ffn.cu fused_*). OEA_TWO_KERNEL=1 forces the router-cluster
   // + FFN pair (always used for B > 64 and for the router-only stage graph).
+  // (The fused prologue is kept small — it runs cold once per launch — so it
+  // covers N <= 128, p == 1 and D % 8 == 0; other shapes/configs use the pair.)
   const bool fused = part == 0 && B <= kRouterTokChunk && L->router_t != nullptr &&
+                     L->Np <= 128 && (L->D & 7) == 0 &&
+                     (rc.mode == OEA_MODE_VANILLA || rc.p == 1.0) &&
                      getenv("OEA_TWO_KERNEL") == nullptr &&
                      oea_host::ffn_bf16_smem_bytes() +
                              oea_host::ffn_route_smem_bytes(B, L->Np, stride) <= 227 * 1024;

@@ -362,22 +362,6 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
   }
 }
 
-// 8 bf16 of token row `xr` starting at element d0 (zero beyond D).
-__device__ __forceinline__ void load_x8(const __nv_bfloat16* xr, int d0, int D, bool vec,
-                                        float (&f)[8]) {
-  if (vec) {
-    if (d0 < D) {
-      bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(xr + d0)), f);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) f[i] = 0.0f;
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) f[i] = d0 + i < D ? __bfloat162float(xr[d0 + i]) : 0.0f;
-  }
-}
-
 // G: logits[t][e] for this CTA's experts; also the zero-padded x copy the
 // FFN's B fragments read when D is not a tile multiple. Ends with the grid
 // barrier after which every CTA may read all logits (and xpad).
@@ -385,7 +369,6 @@ __device__ __forceinline__ void fused_gemv(const FfnParams& P, float* red, int* 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NT = (kFfnWarps + 1) * 32;
   const int nch = P.Dp >> 3;
-  const bool vec = (P.D & 7) == 0;
   if (P.xpad_out != nullptr) {
 #pragma unroll 1
     for (int t = blockIdx.x; t < P.B; t += gridDim.x)
@@ -403,42 +386,25 @@ __device__ __forceinline__ void fused_gemv(const FfnParams& P, float* red, int* 
       float a[16];
 #pragma unroll
       for (int t = 0; t < 16; ++t) a[t] = 0.0f;
-      if (vec) {
-        // all 16 token chunks + the router chunk in flight before any FMA
+      // all 16 token chunks + the router chunk in flight before any FMA
 #pragma unroll 1
-        for (int c = tid; c < nch; c += NT) {
-          const uint4 rv = __ldg(rrow + c);
-          uint4 xv[16];
+      for (int c = tid; c < nch; c += NT) {
+        const uint4 rv = __ldg(rrow + c);
+        uint4 xv[16];
 #pragma unroll
-          for (int t = 0; t < 16; ++t)
-            xv[t] = (tc + t < P.B && c * 8 < P.D)
-                        ? __ldg(reinterpret_cast<const uint4*>(
-                              P.x_in + static_cast<size_t>(tc + t) * P.D + c * 8))
-                        : make_uint4(0u, 0u, 0u, 0u);
-          float rf[8];
-          bf16x8_to_f32(rv, rf);
+        for (int t = 0; t < 16; ++t)
+          xv[t] = (tc + t < P.B && c * 8 < P.D)
+                      ? __ldg(reinterpret_cast<const uint4*>(
+                            P.x_in + static_cast<size_t>(tc + t) * P.D + c * 8))
+                      : make_uint4(0u, 0u, 0u, 0u);
+        float rf[8];
+        bf16x8_to_f32(rv, rf);
 #pragma unroll
-          for (int t = 0; t < 16; ++t) {
-            float xf[8];
-            bf16x8_to_f32(xv[t], xf);
+        for (int t = 0; t < 16; ++t) {
+          float xf[8];
+          bf16x8_to_f32(xv[t], xf);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) a[t] = fmaf(rf[i], xf[i], a[t]);
-          }
-        }
-      } else {
-#pragma unroll 1
-        for (int c = tid; c < nch; c += NT) {
-          float rf[8];
-          bf16x8_to_f32(__ldg(rrow + c), rf);
-#pragma unroll
-          for (int t = 0; t < 16; ++t) {
-            if (tc + t < P.B) {
-              float xf[8];
-              load_x8(P.x_in + static_cast<size_t>(tc + t) * P.D, c * 8, P.D, false, xf);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) a[t] = fmaf(rf[i], xf[i], a[t]);
-            }
-          }
+          for (int i = 0; i < 8; ++i) a[t] = fmaf(rf[i], xf[i], a[t]);
         }
       }
       // warp transpose-reduction: 16 values -> lane pair (2i, 2i+1) holds the
@@ -481,9 +447,8 @@ __device__ __forceinline__ void fused_gemv(const FfnParams& P, float* red, int* 
 
 // R1 for token t (one warp): the first n_i = min(k0, t_i) ranks (vanilla:
 // the first k) into the token's set row, their e_j = exp(l_j - l_max) and the
-// union bitmap. p == 1 short-circuits t_i = N (routing.cpp:243-245); p < 1
-// uses an fp64 softmax of the fp32 logits (documented best-effort parity).
-template <int E>
+// union bitmap. The fused path runs with p == 1, so t_i = N (routing.cpp:
+// 243-245); p < 1 configurations take the two-kernel path.
 __device__ __forceinline__ void fz_phase1_tok(const FfnParams& P, int t, uint8_t* rs,
                                               const RouteSmem& L) {
   const int lane = threadIdx.x & 31;
@@ -492,38 +457,23 @@ __device__ __forceinline__ void fz_phase1_tok(const FfnParams& P, int t, uint8_t
   int* srow = reinterpret_cast<int*>(rs + L.sets) + t * stride;
   float* se = reinterpret_cast<float*>(rs + L.e) + t * stride;
   uint32_t* uni = reinterpret_cast<uint32_t*>(rs + L.uni);
-  const bool vanilla = P.cfg.mode == OEA_MODE_VANILLA;
-  const int want = vanilla ? P.cfg.k : P.cfg.k0;
-  const bool mass_rule = !vanilla && P.cfg.p != 1.0;
-  TokRank<E> R;
-  tok_load<E>(P.N, lg, R);
-  uint32_t key = 0;
-  int id = tok_select<E>(R, false, nullptr, key);
-  const float rowmax = key32_to_logit(key);
-  double z = 0.0, cum = 0.0;
-  if (mass_rule) {
-#pragma unroll
-    for (int j = 0; j < E; ++j)
-      if (R.key[j] != 0u) z += exp(static_cast<double>(key32_to_logit(R.key[j])) - rowmax);
-#pragma unroll 1
-    for (int off = 16; off > 0; off >>= 1) z += __shfl_xor_sync(kFull, z, off);
-  }
+  const int want = P.cfg.mode == OEA_MODE_VANILLA ? P.cfg.k : P.cfg.k0;
+  TokRank<4> R;
+  tok_load<4>(P.N, lg, R);
+  float rowmax = 0.0f;
   int n = 0;
 #pragma unroll 1
-  while (n < want && id >= 0) {
+  for (; n < want; ++n) {
+    uint32_t key = 0;
+    const int id = tok_select<4>(R, false, nullptr, key);
+    if (id < 0) break;
+    if (n == 0) rowmax = key32_to_logit(key);
     if (lane == 0) {
       srow[n] = id;
       se[n] = expf(key32_to_logit(key) - rowmax);
       atomicOr(&uni[id >> 5], 1u << (id & 31));
     }
-    tok_take<E>(R, id);
-    ++n;
-    if (mass_rule) {
-      cum = __dadd_rn(cum, exp(static_cast<double>(key32_to_logit(key)) - rowmax) / z);
-      if (cum >= P.cfg.p) break;
-    }
-    if (n >= want) break;
-    id = tok_select<E>(R, false, nullptr, key);
+    tok_take<4>(R, id);
   }
   if (lane == 0) {
     reinterpret_cast<int*>(rs + L.n)[t] = n;
@@ -534,7 +484,6 @@ __device__ __forceinline__ void fz_phase1_tok(const FfnParams& P, int t, uint8_t
 // R2 for token t (one warp): piggyback union members of ranks n_i..max_p-1
 // until the cap (Oea / Simplified), then w_j = e_j / sum_set e in set order
 // (fp32), per-expert loads and token bitmaps; CTA 0 exports the plan.
-template <int E>
 __device__ __forceinline__ void fz_phase2_tok(const FfnParams& P, int t, uint8_t* rs,
                                               const RouteSmem& L, bool exporter) {
   const int lane = threadIdx.x & 31;
@@ -550,22 +499,22 @@ __device__ __forceinline__ void fz_phase2_tok(const FfnParams& P, int t, uint8_t
   const float rowmax = reinterpret_cast<const float*>(rs + L.mx)[t];
   int len = n_i;
   if (P.cfg.mode == OEA_MODE_OEA || P.cfg.mode == OEA_MODE_SIMPLIFIED) {
-    TokRank<E> R;
-    tok_load<E>(P.N, lg, R);
+    TokRank<4> R;
+    tok_load<4>(P.N, lg, R);
 #pragma unroll 1
-    for (int j = 0; j < n_i; ++j) tok_take<E>(R, srow[j]);
+    for (int j = 0; j < n_i; ++j) tok_take<4>(R, srow[j]);
     const bool full_scan = P.cfg.max_p >= P.N;
     uint32_t key = 0;
 #pragma unroll 1
     while (len < P.cfg.limit) {
-      const int id = tok_select<E>(R, true, uni, key);
+      const int id = tok_select<4>(R, true, uni, key);
       if (id < 0) break;
-      if (!full_scan && tok_rank_of<E>(R, key, id) >= P.cfg.max_p) break;
+      if (!full_scan && tok_rank_of<4>(R, key, id) >= P.cfg.max_p) break;
       if (lane == 0) {
         srow[len] = id;
         se[len] = expf(key32_to_logit(key) - rowmax);
       }
-      tok_take<E>(R, id);
+      tok_take<4>(R, id);
       ++len;
     }
   }
@@ -635,10 +584,7 @@ __device__ __forceinline__ int fused_route_phase1(const FfnParams& P, uint8_t* r
       if (lane == 0) reinterpret_cast<int*>(rs + L.n)[t] = 0;
       continue;
     }
-    if (Np <= 128)
-      fz_phase1_tok<4>(P, t, rs, L);
-    else
-      fz_phase1_tok<8>(P, t, rs, L);
+    fz_phase1_tok(P, t, rs, L);
   }
   __syncthreads();
   if (warp == 0) {
@@ -703,10 +649,7 @@ __device__ __forceinline__ void fused_route_phase2(const FfnParams& P, uint8_t* 
       }
       continue;
     }
-    if (P.Np <= 128)
-      fz_phase2_tok<4>(P, t, rs, L, exporter);
-    else
-      fz_phase2_tok<8>(P, t, rs, L, exporter);
+    fz_phase2_tok(P, t, rs, L, exporter);
   }
   asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
   if (warp == 0) {
@@ -829,7 +772,12 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
     }
     fused_gemv(P, reinterpret_cast<float*>(rs + RL.red), claims + 3);
     if (threadIdx.x == 0) stamp(P, 5);
-    const int T = fused_route_phase1(P, rs, RL);  // ends with __syncthreads
+    int T = fused_route_phase1(P, rs, RL);  // ends with __syncthreads
+    if (P.mode == 2) {  // debug: phase 1 again, warm (icache) — stamps 12/13
+      if (threadIdx.x == 0) stamp(P, 12);
+      T = fused_route_phase1(P, rs, RL);
+      if (threadIdx.x == 0) stamp(P, 13);
+    }
     if (threadIdx.x == 0) {
       PR->G = T;
       stamp(P, 6);
@@ -845,18 +793,9 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
     PR->G = P.hdr->n_groups;
   }
   __syncthreads();
+  // G == 0 (every token masked) needs no special case: the producer's first
+  // claim ends the work, and the combine writes zeros (empty sets).
   const int G = PR->G;
-  if (G == 0) {
-    if (P.fused) {
-      if (blockIdx.x == 0)
-        for (int f = threadIdx.x; f < P.B * P.D; f += (kFfnWarps + 1) * 32) P.out[f] = 0.0f;
-      if (warp < kFfnWarps) {
-        fused_route_phase2(P, rs, RL, 0);  // exports the (empty) plan
-        if (threadIdx.x == 0) grid_exit(P, claims, 0);
-      }
-    }
-    return;
-  }
   const int KT1 = P.Dp >> 4, KT2 = P.Hp >> 4;
   const int RB1 = P.Hp >> 3, RB2 = P.Dp >> 4;
   const int U1 = G * RB1, U2 = G * RB2;

@@ -12,9 +12,11 @@ x = torch.randn(B, D, device="cuda").to(torch.bfloat16)
 out = torch.empty(B, D, device="cuda", dtype=torch.float32)
 torch.cuda.synchronize()
 for name, cfg in (("oea", oea.RoutingConfig.simplified(4, 8)), ("vanilla", oea.RoutingConfig.vanilla(8))):
-    for rep in range(3):
+    # back-to-back calls (no host sync in between, clocks stay up); the trace
+    # buffer holds the last call
+    for rep in range(int(os.environ.get("REPS", "20"))):
         (L if rep % 2 == 0 else L2).decode(x, cfg, out)
-        L.ctx.synchronize()
+    L.ctx.synchronize()
     buf = np.zeros(8 * 1024, np.uint64)
     L.ctx.check(lib().oea_debug_ffn_trace(L.ctx.h, buf.ctypes.data_as(C.c_void_p), buf.size))
     t = buf[:148 * 16].reshape(148, 16).astype(np.int64)
@@ -35,6 +37,9 @@ for name, cfg in (("oea", oea.RoutingConfig.simplified(4, 8)), ("vanilla", oea.R
         print(" fused: logits in smem     ", st(rel[:, 11]))
         print(" fused: union known (phase 1)", st(rel[:, 6]))
         print(" fused: plan ready (phase 2) ", st(rel[:, 7]))
+        if t[:, 12].any():
+            print(" debug: phase 1 rerun start  ", st(rel[:, 12]))
+            print(" debug: phase 1 rerun end    ", st(rel[:, 13]))
     r = buf.reshape(1024, 8)[1000:1008].astype(np.int64)
     r0 = r[0, 0]
     print(" router CTA stamps (us from CTA0 start): start, x-staged, gemv, sync1, end-gemv, routed, compacted")
