@@ -109,8 +109,9 @@ size_t carve(Workspace& w, bool assign) {
   take(w.hdr, sizeof(FfnHeader));
   take(w.counters, (G + Dp / 16 + 8) * 4);
   take(w.xpad, B * Dp * 2);
-  take(w.hbuf, R * std::max(Hp, H) * 8);
-  take(w.ybuf, B * S * std::max(Dp, D) * 8);
+  // (dense decode: h [G][16][Hp] bf16, y [G][16][Dp] f32 with G <= N)
+  take(w.hbuf, std::max(R * std::max(Hp, H) * 8, Nmax * 16 * Hp * 2));
+  take(w.ybuf, std::max(B * S * std::max(Dp, D) * 8, Nmax * 16 * Dp * 4));
   take(w.mask, B);
   take(w.xin, B * D * 8);
   take(w.out, B * D * 8);
@@ -356,7 +357,7 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   rb.group_rows = w.group_rows;
   rb.hdr = w.hdr;
   rb.counters = w.counters;
-  rb.n_counters = w.G + L->Dp / 16 + 5;
+  rb.n_counters = w.G + L->Dp / 16 + 6;
   rb.out = static_cast<float*>(out);
   rb.phase1_n = w.n;
   rb.base_union = w.base_union;
@@ -400,6 +401,11 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   fb.mode = ctx->ffn_mode;
   if (fused) {
     fb.fused = 1;
+    // dense-over-batch FFN when the batch is one or two n-blocks and the
+    // swizzled x tile fits next to the ring (OEA_SPARSE=1 forces token lists)
+    fb.dense = B <= 16 && getenv("OEA_SPARSE") == nullptr &&
+               oea_host::ffn_bf16_smem_bytes() + oea_host::ffn_route_smem_bytes(B, L->Np, stride) +
+                       oea_host::ffn_dense_xs_bytes(L->Dp) <= 227 * 1024;
     fb.x_in = static_cast<const __nv_bfloat16*>(x);
     fb.xpad_out = padded ? w.xpad : nullptr;
     fb.logits = w.logits;

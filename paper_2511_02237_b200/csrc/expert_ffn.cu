@@ -40,6 +40,12 @@
 
 namespace oea_dev {
 
+// 8 consumer warps, 1 producer warp (lane 0 streams weights), 1 router warp
+// (fused dense path: this CTA's token's phase 2 while the weights stream).
+constexpr int kProducerWarp = kFfnWarps;
+constexpr int kRouterWarp = kFfnWarps + 1;
+constexpr int kFfnThreads = (kFfnWarps + 2) * 32;
+
 struct FfnParams {
   const uint4* w1;
   const uint4* w2;
@@ -60,8 +66,11 @@ struct FfnParams {
   float* out;           // [B][D]
   unsigned long long* trace;  // debug: [gridDim][8] globaltimer stamps, or null
   int mode;                   // debug: 1 = stream weights only (no math)
-  // Fused single-launch decode (see fused_gemv / fused_route_phase1/2).
-  int fused;
+  // Fused single-launch decode (k_ffn_bf16<1|2>, see fused_gemv /
+  // fused_route_phase1/2). Dense path (<2>, B <= 16): W1 computes h for ALL
+  // tokens of the batch, so it needs only the union (phase 1); the token lists
+  // (phase 2) are needed only from the first W2 round on.
+  int xs_row;                   // bytes per token row of the shared-memory x tile
   const uint4* router_t;        // [Np][Dp/8] expert-major bf16 router
   const __nv_bfloat16* x_in;    // [B][D] caller tokens
   __nv_bfloat16* xpad_out;      // [B][Dp], written in-kernel when D != Dp, else null
@@ -115,13 +124,23 @@ struct Unit {
   int ready;   // W2: the group's h is known complete (acquired by the producer)
 };
 
-template <int NB, bool W1>
+// Shared-memory x tile of the dense path: 16 token rows of Dp bf16, row
+// stride Dp*2 + 32 bytes; inside every 256-byte K slice (one stage) the 16
+// chunks of 16 bytes are placed at xs_chunk(cc) so that the 8 lanes of one
+// LDS.128 phase (two token rows x four lane quads) hit 8 distinct bank groups.
+__device__ __forceinline__ int xs_chunk(int cc) { return (cc & 8) | ((cc + (cc >> 3)) & 7); }
+
+template <int NB, bool W1, bool DENSE>
 __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* PR,
                                              const uint8_t* ring, uint64_t* full, uint64_t* empty,
-                                             int& stage, uint32_t& phase, int nst, const Unit& U) {
+                                             int& stage, uint32_t& phase, int nst, const Unit& U,
+                                             const uint8_t* xs) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
   const int RB1 = P.Hp >> 3;
+  // dense W1: B operand = all B tokens from the swizzled shared-memory x tile;
+  // dense W2: token lists as usual, h rows at [group][token] (written by W1)
+  constexpr bool XSM = DENSE && W1;
 
   // B-operand rows (uint4 view) for this lane's token in each n-block. The
   // weights are packed with the k-permutation of layer.cu (kperm): in every
@@ -136,13 +155,16 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
   for (int nb = 0; nb < NB; ++nb) {
     const int r = nb * 8 + g;
     bp[nb] = nullptr;
-    if (r < U.rows) {
+    if (XSM) {
+      // token r; the per-quarter chunk offsets are added at the load
+      bp[nb] = reinterpret_cast<const uint4*>(xs + r * P.xs_row);
+    } else if (r < U.rows) {
       if (W1) {
         const int t = PR->row_tok[U.row0 + r];
         bp[nb] = reinterpret_cast<const uint4*>(P.xpad + static_cast<size_t>(t) * P.Dp) + 4 * q;
       } else {
-        bp[nb] = reinterpret_cast<const uint4*>(P.hbuf + static_cast<size_t>(U.row0 + r) * P.Hp) +
-                 4 * q;
+        const int hrow = DENSE ? U.g * 16 + PR->row_tok[U.row0 + r] : U.row0 + r;
+        bp[nb] = reinterpret_cast<const uint4*>(P.hbuf + static_cast<size_t>(hrow) * P.Hp) + 4 * q;
       }
     }
   }
@@ -171,10 +193,14 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
     if (p == nullptr) return make_uint4(0u, 0u, 0u, 0u);
     return W1 ? __ldg(p) : __ldcg(p);
   };
+  // dense W1: byte offsets of this lane's quarter-stage chunks inside a slice
+  int xoff[4];
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) xoff[jj] = xs_chunk(4 * q + jj) * 16;
   // One n-block: the next stage's 4 loads are issued right after the current
   // stage is consumed, so their latency hides behind the stage barrier wait.
   // More n-blocks: per quarter stage (2 k-tiles) one 16-byte load per n-block.
-  constexpr bool kPref = NB <= 1;
+  constexpr bool kPref = !XSM && NB <= 1;
   uint4 bpre[4];
   const bool math = P.mode != 1;
   if (kPref && math)
@@ -202,8 +228,12 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
         for (int jj = 0; jj < kKtPerSlot / 2; ++jj) {
           uint4 v[NB];
 #pragma unroll
-          for (int nb = 0; nb < NB; ++nb)
-            v[nb] = ldb(bp[nb] == nullptr ? nullptr : bp[nb] + s * 16 + jj);
+          for (int nb = 0; nb < NB; ++nb) {
+            if (XSM)
+              v[nb] = lds128(reinterpret_cast<const uint8_t*>(bp[nb]) + s * 256 + xoff[jj]);
+            else
+              v[nb] = ldb(bp[nb] == nullptr ? nullptr : bp[nb] + s * 16 + jj);
+          }
 #pragma unroll
           for (int h2 = 0; h2 < 2; ++h2) {
             const uint4 a = tiles[(2 * jj + h2) * 32 + lane];
@@ -282,19 +312,39 @@ __device__ __forceinline__ void skip_unit(uint64_t* full, uint64_t* empty, int& 
   }
 }
 
-template <bool W1>
+template <bool W1, bool DENSE>
 __device__ __forceinline__ void dispatch_unit(int nbk, const FfnParams& P, const PlanRef* PR,
                                               const uint8_t* ring, uint64_t* full, uint64_t* empty,
-                                              int& stage, uint32_t& phase, int nst, const Unit& U) {
-  switch (nbk) {
-    case 1: consume_unit<1, W1>(P, PR, ring, full, empty, stage, phase, nst, U); break;
-    case 2: consume_unit<2, W1>(P, PR, ring, full, empty, stage, phase, nst, U); break;
-    case 3: consume_unit<3, W1>(P, PR, ring, full, empty, stage, phase, nst, U); break;
-    case 4: consume_unit<4, W1>(P, PR, ring, full, empty, stage, phase, nst, U); break;
-    case 5:
-    case 6: consume_unit<6, W1>(P, PR, ring, full, empty, stage, phase, nst, U); break;
-    default: consume_unit<8, W1>(P, PR, ring, full, empty, stage, phase, nst, U); break;
+                                              int& stage, uint32_t& phase, int nst, const Unit& U,
+                                              const uint8_t* xs) {
+  if (DENSE) {  // B <= 16: at most two n-blocks
+    if (nbk == 1)
+      consume_unit<1, W1, true>(P, PR, ring, full, empty, stage, phase, nst, U, xs);
+    else
+      consume_unit<2, W1, true>(P, PR, ring, full, empty, stage, phase, nst, U, xs);
+    return;
   }
+  switch (nbk) {
+    case 1: consume_unit<1, W1, false>(P, PR, ring, full, empty, stage, phase, nst, U, xs); break;
+    case 2: consume_unit<2, W1, false>(P, PR, ring, full, empty, stage, phase, nst, U, xs); break;
+    case 3: consume_unit<3, W1, false>(P, PR, ring, full, empty, stage, phase, nst, U, xs); break;
+    case 4: consume_unit<4, W1, false>(P, PR, ring, full, empty, stage, phase, nst, U, xs); break;
+    case 5:
+    case 6: consume_unit<6, W1, false>(P, PR, ring, full, empty, stage, phase, nst, U, xs); break;
+    default: consume_unit<8, W1, false>(P, PR, ring, full, empty, stage, phase, nst, U, xs); break;
+  }
+}
+
+// Dense path W2: token lists of the group (router warp), h rows at
+// [group][token]; consume_unit<NB, false, true> (W2 ignores the x tile).
+__device__ __forceinline__ void dispatch_w2_dense(int nbk, const FfnParams& P, const PlanRef* PR,
+                                                  const uint8_t* ring, uint64_t* full,
+                                                  uint64_t* empty, int& stage, uint32_t& phase,
+                                                  int nst, const Unit& U, const uint8_t* xs) {
+  if (nbk == 1)
+    consume_unit<1, false, true>(P, PR, ring, full, empty, stage, phase, nst, U, xs);
+  else
+    consume_unit<2, false, true>(P, PR, ring, full, empty, stage, phase, nst, U, xs);
 }
 
 // ---------------------------------------------------------------------------
@@ -347,7 +397,7 @@ __host__ __device__ inline RouteSmem route_smem_layout(int B, int Np, int stride
   L.rows = take(Np * 4);
   L.rtok = take(rmax * 4);
   L.rslot = take(rmax * 4);
-  L.red = take((kFfnWarps + 1) * 16 * 4);
+  L.red = take((kFfnThreads / 32) * 16 * 4);
   L.misc = take(8 * 4);
   L.total = o;
   return L;
@@ -367,7 +417,7 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
 // barrier after which every CTA may read all logits (and xpad).
 __device__ __forceinline__ void fused_gemv(const FfnParams& P, float* red, int* sync_cnt) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NT = (kFfnWarps + 1) * 32;
+  constexpr int NT = kFfnThreads;
   const int nch = P.Dp >> 3;
   if (P.xpad_out != nullptr) {
 #pragma unroll 1
@@ -427,7 +477,7 @@ __device__ __forceinline__ void fused_gemv(const FfnParams& P, float* red, int* 
       if (tid < 16 && tc + tid < P.B) {
         float s = 0.0f;
 #pragma unroll
-        for (int w = 0; w <= kFfnWarps; ++w) s += red[w * 16 + tid];
+        for (int w = 0; w < kFfnThreads / 32; ++w) s += red[w * 16 + tid];
         P.logits[static_cast<size_t>(tc + tid) * P.Np + e] = s;
       }
       __syncthreads();
@@ -485,7 +535,7 @@ __device__ __forceinline__ void fz_phase1_tok(const FfnParams& P, int t, uint8_t
 // until the cap (Oea / Simplified), then w_j = e_j / sum_set e in set order
 // (fp32), per-expert loads and token bitmaps; CTA 0 exports the plan.
 __device__ __forceinline__ void fz_phase2_tok(const FfnParams& P, int t, uint8_t* rs,
-                                              const RouteSmem& L, bool exporter) {
+                                              const RouteSmem& L, bool exporter, bool count) {
   const int lane = threadIdx.x & 31;
   const int stride = P.cfg.stride;
   const int Bw = (P.B + 31) >> 5;
@@ -530,8 +580,10 @@ __device__ __forceinline__ void fz_phase2_tok(const FfnParams& P, int t, uint8_t
       const int e = srow[j];
       w = se[j] / mass;
       se[j] = w;
-      atomicAdd(&loads[e], 1);
-      atomicOr(&tokbits[e * Bw + (t >> 5)], 1u << (t & 31));
+      if (count) {
+        atomicAdd(&loads[e], 1);
+        atomicOr(&tokbits[e * Bw + (t >> 5)], 1u << (t & 31));
+      }
     } else {
       se[j] = 0.0f;
     }
@@ -551,11 +603,28 @@ __device__ __forceinline__ void fz_phase2_tok(const FfnParams& P, int t, uint8_t
   }
 }
 
+// Masked token (padding row): empty set and weights in the exported plan.
+__device__ __forceinline__ void fz_phase2_masked(const FfnParams& P, int t) {
+  const int lane = threadIdx.x & 31;
+  const int stride = P.cfg.stride;
+#pragma unroll 1
+  for (int j = lane; j < stride; j += 32) {
+    const size_t o = static_cast<size_t>(t) * stride + j;
+    P.x_sets[o] = -1;
+    P.x_w32[o] = 0.0f;
+    if (P.x_w64) P.x_w64[o] = 0.0;
+  }
+  if (lane == 0) {
+    P.x_set_len[t] = 0;
+    if (P.x_phase1_n) P.x_phase1_n[t] = 0;
+  }
+}
+
 // R1 on all 9 warps; returns T (= the number of expert groups, one per active
 // expert since B <= 64). On return active[]/eslot[] are valid CTA-wide.
 __device__ __forceinline__ int fused_route_phase1(const FfnParams& P, uint8_t* rs, const RouteSmem& L) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int NT = (kFfnWarps + 1) * 32;
+  constexpr int NT = kFfnThreads;
   const int B = P.B, Np = P.Np, N = P.N;
   const int Bw = (B + 31) >> 5;
   float* lg = reinterpret_cast<float*>(rs + L.lg);
@@ -579,7 +648,7 @@ __device__ __forceinline__ int fused_route_phase1(const FfnParams& P, uint8_t* r
   __syncthreads();
   if (threadIdx.x == 0) stamp(P, 11);
 #pragma unroll 1
-  for (int t = warp; t < B; t += kFfnWarps + 1) {
+  for (int t = warp; t < B; t += kFfnThreads / 32) {
     if (P.mask != nullptr && P.mask[t] == 0) {
       if (lane == 0) reinterpret_cast<int*>(rs + L.n)[t] = 0;
       continue;
@@ -599,6 +668,7 @@ __device__ __forceinline__ int fused_route_phase1(const FfnParams& P, uint8_t* r
       if (f) active[slot] = e;
       if (exporter && f && P.x_base_union && P.cfg.mode != OEA_MODE_VANILLA)
         P.x_base_union[slot] = e;
+
       T += __popc(m);
     }
     if (lane == 0) {
@@ -614,14 +684,43 @@ __device__ __forceinline__ int fused_route_phase1(const FfnParams& P, uint8_t* r
 // R2 on the 8 consumer warps (named barrier 1): sets, weights, loads, then
 // the compaction tables (row base per active expert, token lists in token
 // order, inverse permutation) in shared memory.
-__device__ __forceinline__ void fused_route_phase2(const FfnParams& P, uint8_t* rs, const RouteSmem& L,
-                                                int T) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int NC = kFfnWarps * 32;
+// R2, per-token part on NW warps (tokens t0, t0 + step, ...): sets,
+// weights; `count` also accumulates the per-expert loads / token bitmaps.
+template <int NW>
+__device__ __forceinline__ void route_phase2_tokens(const FfnParams& P, uint8_t* rs,
+                                                    const RouteSmem& L, int t0, int step,
+                                                    bool exporter, bool count) {
+  const int lane = threadIdx.x & 31;
+  int* len = reinterpret_cast<int*>(rs + L.len);
+#pragma unroll 1
+  for (int t = t0; t < P.B; t += step) {
+    if (P.mask != nullptr && P.mask[t] == 0) {
+      if (lane == 0) len[t] = 0;
+      if (exporter) fz_phase2_masked(P, t);
+      continue;
+    }
+    fz_phase2_tok(P, t, rs, L, exporter, count);
+  }
+}
+
+// Compaction from the CTA's plan in shared memory (sets / len / loads / token
+// bitmaps): row base per active expert (slot order), token lists in token
+// order, inverse permutation; CTA 0 exports the aggregates.
+template <int NW>
+__device__ __forceinline__ void compact_smem(const FfnParams& P, uint8_t* rs, const RouteSmem& L,
+                                             int T, bool exporter) {
+  const int warp = NW == 1 ? 0 : threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ltid = warp * 32 + lane;
+  constexpr int NC = NW * 32;
+  auto sync = [&]() {
+    if (NW == 1)
+      __syncwarp();
+    else
+      asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
+  };
   const int B = P.B, N = P.N, stride = P.cfg.stride;
   const int Bw = (B + 31) >> 5;
-  const bool exporter = blockIdx.x == 0;
-  int* len = reinterpret_cast<int*>(rs + L.len);
+  const int* len = reinterpret_cast<const int*>(rs + L.len);
   const int* loads = reinterpret_cast<const int*>(rs + L.loads);
   const int* active = reinterpret_cast<const int*>(rs + L.active);
   const int* eslot = reinterpret_cast<const int*>(rs + L.eslot);
@@ -630,28 +729,6 @@ __device__ __forceinline__ void fused_route_phase2(const FfnParams& P, uint8_t* 
   int* rtok = reinterpret_cast<int*>(rs + L.rtok);
   int* rslot = reinterpret_cast<int*>(rs + L.rslot);
   const uint32_t* tokbits = reinterpret_cast<const uint32_t*>(rs + L.tokbits);
-#pragma unroll 1
-  for (int t = warp; t < B; t += kFfnWarps) {
-    if (P.mask != nullptr && P.mask[t] == 0) {
-      if (lane == 0) len[t] = 0;
-      if (exporter) {
-#pragma unroll 1
-        for (int j = lane; j < stride; j += 32) {
-          const size_t o = static_cast<size_t>(t) * stride + j;
-          P.x_sets[o] = -1;
-          P.x_w32[o] = 0.0f;
-          if (P.x_w64) P.x_w64[o] = 0.0;
-        }
-        if (lane == 0) {
-          P.x_set_len[t] = 0;
-          if (P.x_phase1_n) P.x_phase1_n[t] = 0;
-        }
-      }
-      continue;
-    }
-    fz_phase2_tok(P, t, rs, L, exporter);
-  }
-  asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
   if (warp == 0) {
     int R = 0, load = 0;
 #pragma unroll 1
@@ -694,10 +771,10 @@ __device__ __forceinline__ void fused_route_phase2(const FfnParams& P, uint8_t* 
       }
     }
   }
-  asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
+  sync();
   const int* sets = reinterpret_cast<const int*>(rs + L.sets);
 #pragma unroll 1
-  for (int idx = threadIdx.x; idx < B * stride; idx += NC) {
+  for (int idx = ltid; idx < B * stride; idx += NC) {
     const int t = idx / stride, sl = idx % stride;
     if (sl < len[t]) {
       const int e = sets[idx];
@@ -710,7 +787,61 @@ __device__ __forceinline__ void fused_route_phase2(const FfnParams& P, uint8_t* 
       rslot[row] = sl;
     }
   }
-  asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
+  sync();
+}
+
+// R2 on the 8 consumer warps (sparse fused path): every token's phase 2,
+// then the compaction, all in shared memory.
+__device__ __forceinline__ void fused_route_phase2(const FfnParams& P, uint8_t* rs,
+                                                   const RouteSmem& L, int T) {
+  const int warp = threadIdx.x >> 5;
+  const bool exporter = blockIdx.x == 0;
+  route_phase2_tokens<kFfnWarps>(P, rs, L, warp, kFfnWarps, exporter, true);
+  asm volatile("bar.sync 1, %0;" ::"r"(kFfnWarps * 32) : "memory");
+  compact_smem<kFfnWarps>(P, rs, L, T, exporter);
+}
+
+// R2 on the router warp (dense path): CTA t routes token t and publishes it
+// (exported plan rows + a release count); then every CTA gathers the whole
+// batch's plan, counts per-expert loads and compacts the W2 token lists.
+__device__ __forceinline__ void dense_route_phase2(const FfnParams& P, uint8_t* rs,
+                                                   const RouteSmem& L, int T, int* plan_cnt) {
+  const int lane = threadIdx.x & 31;
+  const int B = P.B, stride = P.cfg.stride, Np = P.Np;
+  const int Bw = (B + 31) >> 5;
+  if (static_cast<int>(blockIdx.x) < B) {
+    route_phase2_tokens<1>(P, rs, L, blockIdx.x, B, true, false);
+    __syncwarp();
+    if (lane == 0) red_release_gpu_add(plan_cnt, 1);
+  }
+  if (lane == 0)
+    while (ld_acquire_gpu(plan_cnt) < B) __nanosleep(64);
+  __syncwarp();
+  int* len = reinterpret_cast<int*>(rs + L.len);
+  int* sets = reinterpret_cast<int*>(rs + L.sets);
+  float* wts = reinterpret_cast<float*>(rs + L.e);
+  int* loads = reinterpret_cast<int*>(rs + L.loads);
+  uint32_t* tokbits = reinterpret_cast<uint32_t*>(rs + L.tokbits);
+#pragma unroll 1
+  for (int i = lane; i < Np; i += 32) loads[i] = 0;
+#pragma unroll 1
+  for (int i = lane; i < Np * Bw; i += 32) tokbits[i] = 0u;
+#pragma unroll 1
+  for (int t = lane; t < B; t += 32) len[t] = __ldcg(P.x_set_len + t);
+  __syncwarp();
+#pragma unroll 4
+  for (int idx = lane; idx < B * stride; idx += 32) {
+    const int t = idx / stride, sl = idx % stride;
+    const int e = __ldcg(P.x_sets + idx);
+    sets[idx] = e;
+    wts[idx] = __ldcg(P.x_w32 + idx);
+    if (sl < len[t]) {
+      atomicAdd(&loads[e], 1);
+      atomicOr(&tokbits[e * Bw + (t >> 5)], 1u << (t & 31));
+    }
+  }
+  __syncwarp();
+  compact_smem<1>(P, rs, L, T, blockIdx.x == 0);
 }
 
 // The last CTA to leave resets the grid's counters (round claims, combine /
@@ -721,7 +852,7 @@ __device__ __forceinline__ void grid_exit(const FfnParams& P, int* claims, int G
   __threadfence();
   if (atomicAdd(&claims[4], 1) == static_cast<int>(gridDim.x) - 1) {
     for (int g = 0; g < G; ++g) P.w1_done[g] = 0;
-    claims[0] = claims[1] = claims[2] = claims[3] = 0;
+    claims[0] = claims[1] = claims[2] = claims[3] = claims[5] = 0;
     __threadfence();
     claims[4] = 0;
   }
@@ -736,12 +867,20 @@ struct RoundDesc {
 };
 constexpr int kRoundRing = 8;  // > kStages: a round spans >= 1 stage
 
-__global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnParams P) {
+// MODE 0: two-kernel path (plan from the router kernel); 1: fused, token
+// lists (B <= 64); 2: fused, dense-over-batch W1 (B <= 16). Separate
+// instantiations keep each variant's register allocation and code small.
+template <int MODE>
+__global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) {
+  constexpr bool kFused = MODE != 0;
+  constexpr bool kDense = MODE == 2;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
   RoundDesc* rdesc = reinterpret_cast<RoundDesc*>(empty + kStages);
+  uint64_t* plan_bar = reinterpret_cast<uint64_t*>(
+      reinterpret_cast<PlanRef*>(rdesc + kRoundRing) + 1);  // dense: router warp -> W2
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -749,6 +888,7 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kFfnWarps);
     }
+    mbar_init(plan_bar, 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -757,10 +897,12 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
   if (threadIdx.x == 0) stamp(P, 0);
 
   PlanRef* PR = reinterpret_cast<PlanRef*>(rdesc + kRoundRing);
-  uint8_t* rs = reinterpret_cast<uint8_t*>(PR + 1);
+  uint8_t* rs = reinterpret_cast<uint8_t*>(PR + 1) + 16;
   const RouteSmem RL = route_smem_layout(P.B, P.Np, P.stride);
-  int* claims = P.cnt2 + (P.Dp >> 4);  // [0..1] round claims, [2] combine, [3] logits barrier, [4] exit
-  if (P.fused) {
+  uint8_t* xs = rs + RL.total;  // dense path: x tile (16 B aligned)
+  // [0..1] round claims, [2] combine, [3] logits barrier, [4] exit, [5] dense plan rows
+  int* claims = P.cnt2 + (P.Dp >> 4);
+  if (kFused) {
     if (threadIdx.x == 0) {
       PR->row_tok = reinterpret_cast<const int32_t*>(rs + RL.rtok);
       PR->row_slot = reinterpret_cast<const int32_t*>(rs + RL.rslot);
@@ -808,7 +950,19 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
   int stage = 0;
   uint32_t phase = 0;
 
-  if (warp == kFfnWarps) {
+  if (warp == kRouterWarp) {
+    // ---------------- router warp ----------------
+    // Dense path: phase 2, weights and the token lists of the W2 units for
+    // the whole batch (redundantly per CTA, like phase 1) while the W1
+    // weights stream; consumers wait for it only before their first W2 round.
+    if (kDense) {
+      dense_route_phase2(P, rs, RL, G, claims + 5);
+      if (lane == 0) {
+        stamp(P, 7);
+        mbar_arrive(plan_bar);  // W2 rounds may start
+      }
+    }
+  } else if (warp == kProducerWarp) {
     // ---------------- producer: claims rounds, TMA bulk weight stream ----------
     if (lane == 0) {
       const uint64_t pol = l2_policy_evict_first();
@@ -879,10 +1033,23 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
       stamp(P, 4);
     }
     return;
-  }
-
+  } else {
   // ---------------- consumers ----------------
-  if (P.fused) {
+  if (kDense) {
+    // x (final since the logits barrier) -> swizzled shared tile, 16 rows
+    // (rows >= B zero-filled), while the producer's first stages land
+    const int nch = P.Dp >> 3;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < 16 * nch; i += kFfnWarps * 32) {
+      const int t = i / nch, c = i % nch;
+      const uint32_t dst = smem_u32(xs + t * P.xs_row + (c >> 4) * 256 + xs_chunk(c & 15) * 16);
+      const __nv_bfloat16* src = P.xpad + static_cast<size_t>(t < P.B ? t : 0) * P.Dp + c * 8;
+      cp_async16(dst, src, t < P.B ? 16 : 0);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    asm volatile("bar.sync 1, %0;" ::"r"(kFfnWarps * 32) : "memory");
+  } else if (kFused) {
     fused_route_phase2(P, rs, RL, G);  // overlaps the producer's first stages
     if (threadIdx.x == 0) stamp(P, 7);
   }
@@ -894,6 +1061,7 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
     const bool is1 = d.kind == 1;
     if (!is1 && !in_w2) {
       in_w2 = true;
+      if (kDense) mbar_wait(plan_bar, 0);  // token lists of the W2 units
       if (threadIdx.x == 0) stamp(P, 1);
     }
     const int nst = (is1 ? KT1 : KT2) / kKtPerSlot;
@@ -908,51 +1076,67 @@ __global__ void __launch_bounds__((kFfnWarps + 1) * 32, 1) k_ffn_bf16(const FfnP
         U.g = v / RB2;
         U.rb = v % RB2;
       }
-      U.row0 = PR->group_row0[U.g];
-      U.rows = PR->group_rows[U.g];
+      if (kDense && is1) {
+        U.row0 = U.g * 16;
+        U.rows = P.B;
+      } else {
+        U.row0 = PR->group_row0[U.g];
+        U.rows = PR->group_rows[U.g];
+      }
       U.ready = d.ready;
       const int nbk = (U.rows + 7) >> 3;
       if (is1)
-        dispatch_unit<true>(nbk, P, PR, ring, full, empty, stage, phase, nst, U);
+        dispatch_unit<true, kDense>(nbk, P, PR, ring, full, empty, stage, phase, nst, U, xs);
+      else if (kDense)
+        dispatch_w2_dense(nbk, P, PR, ring, full, empty, stage, phase, nst, U, xs);
       else
-        dispatch_unit<false>(nbk, P, PR, ring, full, empty, stage, phase, nst, U);
+        dispatch_unit<false, false>(nbk, P, PR, ring, full, empty, stage, phase, nst, U, xs);
     } else {
       skip_unit(full, empty, stage, phase, nst);
     }
   }
   if (threadIdx.x == 0) stamp(P, 3);
+  }
 
   // ---- grid-wide deterministic combine (moe_layer.hpp:148-155) ----
-  // out[t][d] = sum_s w[t][s] * y[t][s][d] in set order. Every CTA publishes
-  // its y writes (consumer barrier + one gpu-scope release), waits until all
+  // out[t][d] = sum_s w[t][s] * y_s[t][d] in set order. Every CTA publishes
+  // its y writes (and, dense path, its token's plan) with one gpu-scope
+  // release after a barrier of the consumer + router warps, waits until all
   // CTAs have, then combines a contiguous slice of the B x D outputs with all
   // slot loads of an output issued together.
+  constexpr int kComb = (kFfnWarps + 1) * 32;  // consumers + router warp
   int* done = claims + 2;
-  asm volatile("bar.sync 1, %0;" ::"r"(kFfnWarps * 32) : "memory");
+  asm volatile("bar.sync 2, %0;" ::"r"(kComb) : "memory");
   if (threadIdx.x == 0) {
     __threadfence();
     atomicAdd(done, 1);
     while (ld_acquire_gpu(done) < static_cast<int>(gridDim.x)) __nanosleep(128);
     grid_exit(P, claims, G);
   }
-  asm volatile("bar.sync 1, %0;" ::"r"(kFfnWarps * 32) : "memory");
+  asm volatile("bar.sync 2, %0;" ::"r"(kComb) : "memory");
+  const int ctid = warp == kRouterWarp ? kFfnWarps * 32 + lane : threadIdx.x;
   const int64_t BD = static_cast<int64_t>(P.B) * P.D;
   const int64_t f0 = BD * blockIdx.x / gridDim.x, f1 = BD * (blockIdx.x + 1) / gridDim.x;
   constexpr int kSlotBatch = 16;
-  for (int64_t f = f0 + threadIdx.x; f < f1; f += kFfnWarps * 32) {
+  for (int64_t f = f0 + ctid; f < f1; f += kComb) {
     const int t = static_cast<int>(f / P.D), d = static_cast<int>(f % P.D);
     const int len = PR->set_len[t];
     float sum = 0.0f;
     for (int s0 = 0; s0 < len; s0 += kSlotBatch) {
-      float y[kSlotBatch];
+      float y[kSlotBatch], w[kSlotBatch];
+#pragma unroll
+      for (int j = 0; j < kSlotBatch; ++j) {
+        y[j] = 0.0f;
+        w[j] = 0.0f;
+        if (s0 + j < len) {
+          const size_t o = static_cast<size_t>(t) * P.stride + s0 + j;
+          y[j] = __ldcg(P.ybuf + o * P.Dp + d);
+          w[j] = PR->wts[o];
+        }
+      }
 #pragma unroll
       for (int j = 0; j < kSlotBatch; ++j)
-        y[j] = s0 + j < len
-                   ? __ldcg(P.ybuf + (static_cast<size_t>(t) * P.stride + s0 + j) * P.Dp + d)
-                   : 0.0f;
-#pragma unroll
-      for (int j = 0; j < kSlotBatch; ++j)
-        if (s0 + j < len) sum = fmaf(PR->wts[t * P.stride + s0 + j], y[j], sum);
+        if (s0 + j < len) sum = fmaf(w[j], y[j], sum);
     }
     P.out[f] = sum;
   }
@@ -1076,12 +1260,14 @@ using namespace oea_dev;
 
 size_t ffn_bf16_smem_bytes() {
   return kStages * kStageBytes + 2 * kStages * sizeof(uint64_t) + kRoundRing * sizeof(RoundDesc) +
-         sizeof(PlanRef);
+         sizeof(PlanRef) + 16;
 }
 
 size_t ffn_route_smem_bytes(int B, int Np, int stride) {
   return route_smem_layout(B, Np, stride).total;
 }
+
+size_t ffn_dense_xs_bytes(int Dp) { return static_cast<size_t>(16) * (Dp * 2 + 32); }
 
 int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const FfnBuffers& fb,
                     bool pdl, cudaStream_t s) {
@@ -1109,7 +1295,7 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   P.out = static_cast<float*>(fb.out);
   P.trace = fb.trace;
   P.mode = fb.mode;
-  P.fused = fb.fused;
+  P.xs_row = L->Dp * 2 + 32;
   P.router_t = static_cast<const uint4*>(L->router_t);
   P.x_in = fb.x_in;
   P.xpad_out = fb.xpad_out;
@@ -1132,12 +1318,14 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   P.x_hdr = fb.x_hdr;
 
   const size_t smem = ffn_bf16_smem_bytes() +
-                      (fb.fused ? ffn_route_smem_bytes(B, L->Np, stride) : 0);
-  OEA_CUDA_TRY(ctx, cudaFuncSetAttribute(k_ffn_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                      (fb.fused ? ffn_route_smem_bytes(B, L->Np, stride) : 0) +
+                      (fb.dense ? ffn_dense_xs_bytes(L->Dp) : 0);
+  auto kern = fb.dense ? k_ffn_bf16<2> : fb.fused ? k_ffn_bf16<1> : k_ffn_bf16<0>;
+  OEA_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ctx->num_sms);
-  cfg.blockDim = dim3((kFfnWarps + 1) * 32);
+  cfg.blockDim = dim3(kFfnThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -1145,7 +1333,7 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  OEA_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, k_ffn_bf16, P));
+  OEA_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, P));
   OEA_LAUNCHED(ctx);
   return OEA_OK;
 }

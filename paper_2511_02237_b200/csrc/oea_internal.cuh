@@ -195,6 +195,7 @@ struct FfnBuffers {
   // Fused single-launch decode (B <= 64): the FFN grid computes the logits
   // (gate GEMV), routes the batch in every CTA and exports the plan (CTA 0).
   int fused = 0;
+  int dense = 0;                        // dense-over-batch FFN (fused, B <= 16)
   const __nv_bfloat16* x_in = nullptr;  // [B][D] caller tokens
   __nv_bfloat16* xpad_out = nullptr;    // [B][Dp] when D != Dp
   float* logits = nullptr;              // [B][Np]
@@ -215,6 +216,7 @@ struct FfnBuffers {
 };
 size_t ffn_route_smem_bytes(int B, int Np, int stride);
 size_t ffn_bf16_smem_bytes();
+size_t ffn_dense_xs_bytes(int Dp);
 int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride,
                     const FfnBuffers& fb, bool pdl, cudaStream_t s);
 int ffn_simt_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride,
