@@ -107,7 +107,7 @@ size_t carve(Workspace& w, bool assign) {
   take(w.group_row0, G * 4);
   take(w.group_rows, G * 4);
   take(w.hdr, sizeof(FfnHeader));
-  take(w.counters, (G + Dp / 16 + 8) * 4);
+  take(w.counters, (G + Dp / 16 + 24) * 4);
   take(w.xpad, B * Dp * 2);
   // (dense decode: h [G][16][Hp] bf16, y [G][16][Dp] f32 with G <= N)
   take(w.hbuf, std::max(R * std::max(Hp, H) * 8, Nmax * 16 * Hp * 2));
@@ -357,7 +357,7 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   rb.group_rows = w.group_rows;
   rb.hdr = w.hdr;
   rb.counters = w.counters;
-  rb.n_counters = w.G + L->Dp / 16 + 6;
+  rb.n_counters = w.G + L->Dp / 16 + 16;
   rb.out = static_cast<float*>(out);
   rb.phase1_n = w.n;
   rb.base_union = w.base_union;
@@ -371,7 +371,7 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   // covers N <= 128, p == 1 and D % 8 == 0; other shapes/configs use the pair.)
   const bool fused = part == 0 && B <= kRouterTokChunk && L->router_t != nullptr &&
                      L->Np <= 128 && (L->D & 7) == 0 &&
-                     (rc.mode == OEA_MODE_VANILLA || rc.p == 1.0) &&
+                     (rc.mode == OEA_MODE_VANILLA || (rc.p == 1.0 && rc.max_p >= L->N)) &&
                      getenv("OEA_TWO_KERNEL") == nullptr &&
                      oea_host::ffn_bf16_smem_bytes() +
                              oea_host::ffn_route_smem_bytes(B, L->Np, stride) <= 227 * 1024;

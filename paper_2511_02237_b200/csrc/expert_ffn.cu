@@ -368,7 +368,7 @@ __device__ __forceinline__ void dispatch_w2_dense(int nbk, const FfnParams& P, c
 //      on the 8 consumer warps, overlapped with the producer's first stages.
 // ---------------------------------------------------------------------------
 struct RouteSmem {
-  size_t lg, uni, sets, e, len, n, mx, loads, tokbits, active, eslot, rowb, rows, rtok, rslot, red,
+  size_t keys, uni, sets, e, len, n, mx, loads, tokbits, active, eslot, rowb, rows, rtok, rslot, red,
       misc, total;
 };
 
@@ -382,7 +382,7 @@ __host__ __device__ inline RouteSmem route_smem_layout(int B, int Np, int stride
   };
   const int Bw = (B + 31) >> 5, uw = (Np + 31) >> 5;
   const int rmax = B * stride + 8 * Np;
-  L.lg = take(static_cast<size_t>(B) * Np * 4);
+  L.keys = take(static_cast<size_t>(Np) * 4);
   L.uni = take(uw * 4);
   L.sets = take(static_cast<size_t>(B) * stride * 4);
   L.e = take(static_cast<size_t>(B) * stride * 4);
@@ -495,180 +495,144 @@ __device__ __forceinline__ void fused_gemv(const FfnParams& P, float* red, int* 
   __syncthreads();
 }
 
-// R1 for token t (one warp): the first n_i = min(k0, t_i) ranks (vanilla:
-// the first k) into the token's set row, their e_j = exp(l_j - l_max) and the
-// union bitmap. The fused path runs with p == 1, so t_i = N (routing.cpp:
-// 243-245); p < 1 configurations take the two-kernel path.
-__device__ __forceinline__ void fz_phase1_tok(const FfnParams& P, int t, uint8_t* rs,
-                                              const RouteSmem& L) {
-  const int lane = threadIdx.x & 31;
-  const int stride = P.cfg.stride;
-  const float* lg = reinterpret_cast<const float*>(rs + L.lg) + t * P.Np;
-  int* srow = reinterpret_cast<int*>(rs + L.sets) + t * stride;
+// ---------------------------------------------------------------------------
+// Token-parallel rank routing (fused path). CTA t < B routes token t with one
+// thread per expert: every selection of routing.cpp is a RANK in the total
+// order (logit desc, index asc; softmax is monotone, routing.cpp:196-199), so
+// each thread counts the experts ordered before its own and no serial
+// select chain remains.
+//   R1 (routing.cpp:226-268, p == 1): the base set = ranks < n_i = k0
+//      (vanilla: route_topk, ranks < k) -> union bits in global memory.
+//   union barrier (the batch union is global, routing.cpp:262-266).
+//   R2 (routing.cpp:270-303, max_p = N): piggyback = the union members in rank
+//      order until |S| = cap; with base = the top n_i experts, S is exactly the
+//      union members of union-rank < max(n_i, cap) (conservation:
+//      acceptance.cpp:158-184). Weights w_j = e_j / sum_set e in set order
+//      (routing.cpp:33-49, e_j = exp(l_j - l_max): the softmax denominator
+//      cancels), exported as the token's plan row.
+//   plan barrier; every CTA gathers the batch plan and compacts the token
+//   lists of the expert groups (inverse permutation) in shared memory.
+// ---------------------------------------------------------------------------
+// Global scratch (zeroed by grid_exit): claims[6] = tokens routed (R1),
+// claims[8..15] = union bitmap, claims[5] = plan rows published (R2).
+constexpr int kUnionCnt = 6, kUnionBits = 8, kPlanCnt = 5;
+
+// R1 for token t on warps 0..3 (thread e <-> expert e, Np <= 128).
+__device__ __forceinline__ void rank_phase1(const FfnParams& P, int t, uint8_t* rs,
+                                            const RouteSmem& L, int* claims) {
+  const int e = threadIdx.x;  // < 128
+  const int N = P.N, stride = P.cfg.stride;
+  uint32_t* keys = reinterpret_cast<uint32_t*>(rs + L.keys);
+  float* mx = reinterpret_cast<float*>(rs + L.mx);
+  int* sets = reinterpret_cast<int*>(rs + L.sets) + t * stride;
   float* se = reinterpret_cast<float*>(rs + L.e) + t * stride;
-  uint32_t* uni = reinterpret_cast<uint32_t*>(rs + L.uni);
-  const int want = P.cfg.mode == OEA_MODE_VANILLA ? P.cfg.k : P.cfg.k0;
-  TokRank<4> R;
-  tok_load<4>(P.N, lg, R);
-  float rowmax = 0.0f;
-  int n = 0;
-#pragma unroll 1
-  for (; n < want; ++n) {
-    uint32_t key = 0;
-    const int id = tok_select<4>(R, false, nullptr, key);
-    if (id < 0) break;
-    if (n == 0) rowmax = key32_to_logit(key);
-    if (lane == 0) {
-      srow[n] = id;
-      se[n] = expf(key32_to_logit(key) - rowmax);
-      atomicOr(&uni[id >> 5], 1u << (id & 31));
-    }
-    tok_take<4>(R, id);
+  const bool masked = P.mask != nullptr && P.mask[t] == 0;
+  const float l = e < N ? __ldcg(P.logits + static_cast<size_t>(t) * P.Np + e) : 0.0f;
+  const uint32_t key = e < N && !masked ? order_key32(l) : 0u;
+  keys[e] = key;
+  asm volatile("bar.sync 3, 128;" ::: "memory");
+  int rank = 0;
+#pragma unroll 8
+  for (int f = 0; f < N; ++f) {
+    const uint32_t kf = keys[f];
+    rank += (kf > key) | ((kf == key) & (f < e));
   }
-  if (lane == 0) {
-    reinterpret_cast<int*>(rs + L.n)[t] = n;
-    reinterpret_cast<float*>(rs + L.mx)[t] = rowmax;
+  const int n = masked ? 0 : min(P.cfg.mode == OEA_MODE_VANILLA ? P.cfg.k : P.cfg.k0, N);
+  const bool base = key != 0u && rank < n;
+  if (base) {
+    sets[rank] = e;
+    atomicOr(reinterpret_cast<uint32_t*>(claims + kUnionBits) + (e >> 5), 1u << (e & 31));
   }
+  if (key != 0u && rank == 0) mx[t] = l;
+  asm volatile("bar.sync 3, 128;" ::: "memory");
+  if (base) se[rank] = expf(l - mx[t]);
+  if (e == 0) reinterpret_cast<int*>(rs + L.n)[t] = n;
 }
 
-// R2 for token t (one warp): piggyback union members of ranks n_i..max_p-1
-// until the cap (Oea / Simplified), then w_j = e_j / sum_set e in set order
-// (fp32), per-expert loads and token bitmaps; CTA 0 exports the plan.
-__device__ __forceinline__ void fz_phase2_tok(const FfnParams& P, int t, uint8_t* rs,
-                                              const RouteSmem& L, bool exporter, bool count) {
-  const int lane = threadIdx.x & 31;
-  const int stride = P.cfg.stride;
-  const int Bw = (P.B + 31) >> 5;
-  const float* lg = reinterpret_cast<const float*>(rs + L.lg) + t * P.Np;
-  int* srow = reinterpret_cast<int*>(rs + L.sets) + t * stride;
-  float* se = reinterpret_cast<float*>(rs + L.e) + t * stride;
+// R2 for token t on NT threads (thread gt of the group; experts e = gt + NT*i),
+// `sync` a barrier of the group. Exports the token's plan row.
+template <int NT, typename Sync>
+__device__ __forceinline__ void rank_phase2(const FfnParams& P, int t, uint8_t* rs,
+                                            const RouteSmem& L, int T, int gt, Sync sync) {
+  const int N = P.N, stride = P.cfg.stride;
+  const uint32_t* keys = reinterpret_cast<const uint32_t*>(rs + L.keys);
   const uint32_t* uni = reinterpret_cast<const uint32_t*>(rs + L.uni);
-  int* loads = reinterpret_cast<int*>(rs + L.loads);
-  uint32_t* tokbits = reinterpret_cast<uint32_t*>(rs + L.tokbits);
-  const int n_i = reinterpret_cast<const int*>(rs + L.n)[t];
   const float rowmax = reinterpret_cast<const float*>(rs + L.mx)[t];
-  int len = n_i;
-  if (P.cfg.mode == OEA_MODE_OEA || P.cfg.mode == OEA_MODE_SIMPLIFIED) {
-    TokRank<4> R;
-    tok_load<4>(P.N, lg, R);
+  int* sets = reinterpret_cast<int*>(rs + L.sets) + t * stride;
+  float* se = reinterpret_cast<float*>(rs + L.e) + t * stride;
+  const bool masked = P.mask != nullptr && P.mask[t] == 0;
+  const int n = reinterpret_cast<const int*>(rs + L.n)[t];
+  const bool piggy = !masked && (P.cfg.mode == OEA_MODE_OEA || P.cfg.mode == OEA_MODE_SIMPLIFIED);
+  const int cap = max(n, P.cfg.limit);
+  const int len = masked ? 0 : piggy ? min(T, cap) : n;
+  if (piggy) {
 #pragma unroll 1
-    for (int j = 0; j < n_i; ++j) tok_take<4>(R, srow[j]);
-    const bool full_scan = P.cfg.max_p >= P.N;
-    uint32_t key = 0;
-#pragma unroll 1
-    while (len < P.cfg.limit) {
-      const int id = tok_select<4>(R, true, uni, key);
-      if (id < 0) break;
-      if (!full_scan && tok_rank_of<4>(R, key, id) >= P.cfg.max_p) break;
-      if (lane == 0) {
-        srow[len] = id;
-        se[len] = expf(key32_to_logit(key) - rowmax);
+    for (int e = gt; e < N; e += NT) {
+      if (!((uni[e >> 5] >> (e & 31)) & 1u)) continue;
+      const uint32_t key = keys[e];
+      int urank = 0;
+#pragma unroll 8
+      for (int f = 0; f < N; ++f) {
+        const uint32_t kf = keys[f];
+        const bool m = (uni[f >> 5] >> (f & 31)) & 1u;
+        urank += m & ((kf > key) | ((kf == key) & (f < e)));
       }
-      tok_take<4>(R, id);
-      ++len;
-    }
-  }
-  __syncwarp();
-  float mass = 0.0f;  // sequential fp32 mass in set order
-#pragma unroll 1
-  for (int j = 0; j < len; ++j) mass += se[j];
-  __syncwarp();
-#pragma unroll 1
-  for (int j = lane; j < stride; j += 32) {
-    float w = 0.0f;
-    if (j < len) {
-      const int e = srow[j];
-      w = se[j] / mass;
-      se[j] = w;
-      if (count) {
-        atomicAdd(&loads[e], 1);
-        atomicOr(&tokbits[e * Bw + (t >> 5)], 1u << (t & 31));
+      if (urank >= n && urank < len) {
+        sets[urank] = e;
+        se[urank] = expf(key32_to_logit(key) - rowmax);
       }
-    } else {
-      se[j] = 0.0f;
-    }
-    if (exporter) {
-      const size_t o = static_cast<size_t>(t) * stride + j;
-      P.x_sets[o] = j < len ? srow[j] : -1;
-      P.x_w32[o] = w;
-      if (P.x_w64) P.x_w64[o] = static_cast<double>(w);
     }
   }
-  if (lane == 0) {
-    reinterpret_cast<int*>(rs + L.len)[t] = len;
-    if (exporter) {
-      P.x_set_len[t] = len;
-      if (P.x_phase1_n) P.x_phase1_n[t] = P.cfg.mode == OEA_MODE_VANILLA ? 0 : n_i;
-    }
+  sync();
+  if (gt == 0) {
+    float mass = 0.0f;  // sequential fp32 mass in set order
+    for (int j = 0; j < len; ++j) mass += se[j];
+    for (int j = 0; j < len; ++j) se[j] = se[j] / mass;
   }
-}
-
-// Masked token (padding row): empty set and weights in the exported plan.
-__device__ __forceinline__ void fz_phase2_masked(const FfnParams& P, int t) {
-  const int lane = threadIdx.x & 31;
-  const int stride = P.cfg.stride;
+  sync();
 #pragma unroll 1
-  for (int j = lane; j < stride; j += 32) {
+  for (int j = gt; j < stride; j += NT) {
     const size_t o = static_cast<size_t>(t) * stride + j;
-    P.x_sets[o] = -1;
-    P.x_w32[o] = 0.0f;
-    if (P.x_w64) P.x_w64[o] = 0.0;
+    const float w = j < len ? se[j] : 0.0f;
+    P.x_sets[o] = j < len ? sets[j] : -1;
+    P.x_w32[o] = w;
+    if (P.x_w64) P.x_w64[o] = static_cast<double>(w);
   }
-  if (lane == 0) {
-    P.x_set_len[t] = 0;
-    if (P.x_phase1_n) P.x_phase1_n[t] = 0;
+  if (gt == 0) {
+    P.x_set_len[t] = len;
+    if (P.x_phase1_n) P.x_phase1_n[t] = P.cfg.mode == OEA_MODE_VANILLA ? 0 : n;
   }
 }
 
-// R1 on all 9 warps; returns T (= the number of expert groups, one per active
-// expert since B <= 64). On return active[]/eslot[] are valid CTA-wide.
-__device__ __forceinline__ int fused_route_phase1(const FfnParams& P, uint8_t* rs, const RouteSmem& L) {
+// After R1 (all CTAs): wait for every token's base set, then the union
+// (ascending active experts, expert -> group slot) in shared memory.
+// Returns T; CTA 0 exports the base union.
+__device__ __forceinline__ int union_barrier(const FfnParams& P, uint8_t* rs, const RouteSmem& L,
+                                             int* claims) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int NT = kFfnThreads;
-  const int B = P.B, Np = P.Np, N = P.N;
-  const int Bw = (B + 31) >> 5;
-  float* lg = reinterpret_cast<float*>(rs + L.lg);
   uint32_t* uni = reinterpret_cast<uint32_t*>(rs + L.uni);
-  int* loads = reinterpret_cast<int*>(rs + L.loads);
-  uint32_t* tokbits = reinterpret_cast<uint32_t*>(rs + L.tokbits);
   int* active = reinterpret_cast<int*>(rs + L.active);
   int* eslot = reinterpret_cast<int*>(rs + L.eslot);
   int* misc = reinterpret_cast<int*>(rs + L.misc);
   const bool exporter = blockIdx.x == 0;
-  // B * Np is a multiple of 16: float4 copies, several in flight per thread
-#pragma unroll 4
-  for (int i = threadIdx.x; i < (B * Np) >> 2; i += NT)
-    reinterpret_cast<float4*>(lg)[i] = __ldcg(reinterpret_cast<const float4*>(P.logits) + i);
-#pragma unroll 1
-  for (int i = threadIdx.x; i < ((Np + 31) >> 5); i += NT) uni[i] = 0u;
-#pragma unroll 1
-  for (int i = threadIdx.x; i < Np; i += NT) loads[i] = 0;
-#pragma unroll 1
-  for (int i = threadIdx.x; i < Np * Bw; i += NT) tokbits[i] = 0u;
-  __syncthreads();
-  if (threadIdx.x == 0) stamp(P, 11);
-#pragma unroll 1
-  for (int t = warp; t < B; t += kFfnThreads / 32) {
-    if (P.mask != nullptr && P.mask[t] == 0) {
-      if (lane == 0) reinterpret_cast<int*>(rs + L.n)[t] = 0;
-      continue;
-    }
-    fz_phase1_tok(P, t, rs, L);
-  }
-  __syncthreads();
   if (warp == 0) {
+    if (lane == 0)
+      while (ld_acquire_gpu(claims + kUnionCnt) < P.B) __nanosleep(32);
+    __syncwarp();
+    const int N = P.N;
     int T = 0;
 #pragma unroll 1
     for (int base = 0; base < N; base += 32) {
+      const uint32_t word = __ldcg(reinterpret_cast<const uint32_t*>(claims + kUnionBits) + (base >> 5));
+      if (lane == 0) uni[base >> 5] = word;
       const int e = base + lane;
-      const bool f = e < N && ((uni[e >> 5] >> (e & 31)) & 1u);
+      const bool f = e < N && ((word >> lane) & 1u);
       const unsigned m = __ballot_sync(kFull, f);
       const int slot = T + __popc(m & lanemask_lt());
       if (e < N) eslot[e] = f ? slot : -1;
       if (f) active[slot] = e;
       if (exporter && f && P.x_base_union && P.cfg.mode != OEA_MODE_VANILLA)
         P.x_base_union[slot] = e;
-
       T += __popc(m);
     }
     if (lane == 0) {
@@ -679,28 +643,6 @@ __device__ __forceinline__ int fused_route_phase1(const FfnParams& P, uint8_t* r
   }
   __syncthreads();
   return misc[0];
-}
-
-// R2 on the 8 consumer warps (named barrier 1): sets, weights, loads, then
-// the compaction tables (row base per active expert, token lists in token
-// order, inverse permutation) in shared memory.
-// R2, per-token part on NW warps (tokens t0, t0 + step, ...): sets,
-// weights; `count` also accumulates the per-expert loads / token bitmaps.
-template <int NW>
-__device__ __forceinline__ void route_phase2_tokens(const FfnParams& P, uint8_t* rs,
-                                                    const RouteSmem& L, int t0, int step,
-                                                    bool exporter, bool count) {
-  const int lane = threadIdx.x & 31;
-  int* len = reinterpret_cast<int*>(rs + L.len);
-#pragma unroll 1
-  for (int t = t0; t < P.B; t += step) {
-    if (P.mask != nullptr && P.mask[t] == 0) {
-      if (lane == 0) len[t] = 0;
-      if (exporter) fz_phase2_masked(P, t);
-      continue;
-    }
-    fz_phase2_tok(P, t, rs, L, exporter, count);
-  }
 }
 
 // Compaction from the CTA's plan in shared memory (sets / len / loads / token
@@ -790,47 +732,44 @@ __device__ __forceinline__ void compact_smem(const FfnParams& P, uint8_t* rs, co
   sync();
 }
 
-// R2 on the 8 consumer warps (sparse fused path): every token's phase 2,
-// then the compaction, all in shared memory.
-__device__ __forceinline__ void fused_route_phase2(const FfnParams& P, uint8_t* rs,
-                                                   const RouteSmem& L, int T) {
-  const int warp = threadIdx.x >> 5;
-  const bool exporter = blockIdx.x == 0;
-  route_phase2_tokens<kFfnWarps>(P, rs, L, warp, kFfnWarps, exporter, true);
-  asm volatile("bar.sync 1, %0;" ::"r"(kFfnWarps * 32) : "memory");
-  compact_smem<kFfnWarps>(P, rs, L, T, exporter);
-}
-
-// R2 on the router warp (dense path): CTA t routes token t and publishes it
-// (exported plan rows + a release count); then every CTA gathers the whole
-// batch's plan, counts per-expert loads and compacts the W2 token lists.
-__device__ __forceinline__ void dense_route_phase2(const FfnParams& P, uint8_t* rs,
-                                                   const RouteSmem& L, int T, int* plan_cnt) {
-  const int lane = threadIdx.x & 31;
+// R2 + plan exchange + compaction on NW warps (8 consumer warps on the token
+// list path, the router warp on the dense path).
+template <int NW>
+__device__ __forceinline__ void route_phase2_plan(const FfnParams& P, uint8_t* rs,
+                                                  const RouteSmem& L, int T, int* claims) {
+  const int warp = NW == 1 ? 0 : threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gt = warp * 32 + lane;
+  constexpr int NC = NW * 32;
+  auto sync = [&]() {
+    if (NW == 1)
+      __syncwarp();
+    else
+      asm volatile("bar.sync 1, %0;" ::"r"(NC) : "memory");
+  };
   const int B = P.B, stride = P.cfg.stride, Np = P.Np;
   const int Bw = (B + 31) >> 5;
   if (static_cast<int>(blockIdx.x) < B) {
-    route_phase2_tokens<1>(P, rs, L, blockIdx.x, B, true, false);
-    __syncwarp();
-    if (lane == 0) red_release_gpu_add(plan_cnt, 1);
+    rank_phase2<NC>(P, blockIdx.x, rs, L, T, gt, sync);
+    sync();
+    if (gt == 0) red_release_gpu_add(claims + kPlanCnt, 1);
   }
-  if (lane == 0)
-    while (ld_acquire_gpu(plan_cnt) < B) __nanosleep(64);
-  __syncwarp();
+  if (gt == 0)
+    while (ld_acquire_gpu(claims + kPlanCnt) < B) __nanosleep(32);
+  sync();
   int* len = reinterpret_cast<int*>(rs + L.len);
   int* sets = reinterpret_cast<int*>(rs + L.sets);
   float* wts = reinterpret_cast<float*>(rs + L.e);
   int* loads = reinterpret_cast<int*>(rs + L.loads);
   uint32_t* tokbits = reinterpret_cast<uint32_t*>(rs + L.tokbits);
 #pragma unroll 1
-  for (int i = lane; i < Np; i += 32) loads[i] = 0;
+  for (int i = gt; i < Np; i += NC) loads[i] = 0;
 #pragma unroll 1
-  for (int i = lane; i < Np * Bw; i += 32) tokbits[i] = 0u;
+  for (int i = gt; i < Np * Bw; i += NC) tokbits[i] = 0u;
 #pragma unroll 1
-  for (int t = lane; t < B; t += 32) len[t] = __ldcg(P.x_set_len + t);
-  __syncwarp();
+  for (int t = gt; t < B; t += NC) len[t] = __ldcg(P.x_set_len + t);
+  sync();
 #pragma unroll 4
-  for (int idx = lane; idx < B * stride; idx += 32) {
+  for (int idx = gt; idx < B * stride; idx += NC) {
     const int t = idx / stride, sl = idx % stride;
     const int e = __ldcg(P.x_sets + idx);
     sets[idx] = e;
@@ -840,8 +779,8 @@ __device__ __forceinline__ void dense_route_phase2(const FfnParams& P, uint8_t* 
       atomicOr(&tokbits[e * Bw + (t >> 5)], 1u << (t & 31));
     }
   }
-  __syncwarp();
-  compact_smem<1>(P, rs, L, T, blockIdx.x == 0);
+  sync();
+  compact_smem<NW>(P, rs, L, T, blockIdx.x == 0);
 }
 
 // The last CTA to leave resets the grid's counters (round claims, combine /
@@ -852,7 +791,8 @@ __device__ __forceinline__ void grid_exit(const FfnParams& P, int* claims, int G
   __threadfence();
   if (atomicAdd(&claims[4], 1) == static_cast<int>(gridDim.x) - 1) {
     for (int g = 0; g < G; ++g) P.w1_done[g] = 0;
-    claims[0] = claims[1] = claims[2] = claims[3] = claims[5] = 0;
+    for (int c = 0; c < 16; ++c)
+      if (c != 4) claims[c] = 0;
     __threadfence();
     claims[4] = 0;
   }
@@ -914,12 +854,16 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
     }
     fused_gemv(P, reinterpret_cast<float*>(rs + RL.red), claims + 3);
     if (threadIdx.x == 0) stamp(P, 5);
-    int T = fused_route_phase1(P, rs, RL);  // ends with __syncthreads
-    if (P.mode == 2) {  // debug: phase 1 again, warm (icache) — stamps 12/13
-      if (threadIdx.x == 0) stamp(P, 12);
-      T = fused_route_phase1(P, rs, RL);
-      if (threadIdx.x == 0) stamp(P, 13);
+    // R1: CTA t routes token t (thread per expert), then the union barrier
+    if (static_cast<int>(blockIdx.x) < P.B) {
+      if (threadIdx.x < 128) rank_phase1(P, blockIdx.x, rs, RL, claims);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        stamp(P, 11);
+        red_release_gpu_add(claims + kUnionCnt, 1);
+      }
     }
+    const int T = union_barrier(P, rs, RL, claims);  // ends with __syncthreads
     if (threadIdx.x == 0) {
       PR->G = T;
       stamp(P, 6);
@@ -956,7 +900,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
     // the whole batch (redundantly per CTA, like phase 1) while the W1
     // weights stream; consumers wait for it only before their first W2 round.
     if (kDense) {
-      dense_route_phase2(P, rs, RL, G, claims + 5);
+      route_phase2_plan<1>(P, rs, RL, G, claims);
       if (lane == 0) {
         stamp(P, 7);
         mbar_arrive(plan_bar);  // W2 rounds may start
@@ -1050,7 +994,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
     cp_async_wait_all();
     asm volatile("bar.sync 1, %0;" ::"r"(kFfnWarps * 32) : "memory");
   } else if (kFused) {
-    fused_route_phase2(P, rs, RL, G);  // overlaps the producer's first stages
+    route_phase2_plan<kFfnWarps>(P, rs, RL, G, claims);  // overlaps the first stages
     if (threadIdx.x == 0) stamp(P, 7);
   }
   bool in_w2 = false;

@@ -85,6 +85,29 @@ __device__ __forceinline__ void scan_topk(const float* lgT, int t, int N, uint32
   }
 }
 
+// Two independent selections in one basic block (interleaved redux chains).
+template <int E>
+__device__ __forceinline__ void tok_select2(const TokRank<E>& A, const TokRank<E>& B2, uint32_t& ka,
+                                            uint32_t& kb, int& ida, int& idb) {
+  const int lane = threadIdx.x & 31;
+  uint32_t ha = 0, la = 0, hb = 0, lb = 0;
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const uint32_t l2 = 0xFFFFu - static_cast<uint32_t>(j * 32 + lane);
+    const bool oka = A.key[j] != 0u && !((A.taken >> j) & 1u);
+    const bool okb = B2.key[j] != 0u && !((B2.taken >> j) & 1u);
+    if (oka && (A.key[j] > ha || (A.key[j] == ha && l2 > la))) { ha = A.key[j]; la = l2; }
+    if (okb && (B2.key[j] > hb || (B2.key[j] == hb && l2 > lb))) { hb = B2.key[j]; lb = l2; }
+  }
+  const uint32_t wha = __reduce_max_sync(kFull, ha);
+  const uint32_t whb = __reduce_max_sync(kFull, hb);
+  const uint32_t wla = __reduce_max_sync(kFull, ha == wha ? la : 0u);
+  const uint32_t wlb = __reduce_max_sync(kFull, hb == whb ? lb : 0u);
+  ka = wha; kb = whb;
+  ida = wha ? static_cast<int>(0xFFFFu - wla) : -1;
+  idb = whb ? static_cast<int>(0xFFFFu - wlb) : -1;
+}
+
 __global__ void k_bench(const float* logits_g, int k0, int variant, long long* out, int* sel_out) {
   __shared__ float lg[16 * 128];
   __shared__ int srow[16 * 16];
@@ -102,6 +125,31 @@ __global__ void k_bench(const float* logits_g, int k0, int variant, long long* o
     t0 = clock64();
   }
   for (int rep = 0; rep < 4; ++rep) {
+    if (variant == 7) {
+      // two tokens per warp, selections interleaved (independent redux chains)
+      const int nw = blockDim.x >> 5;
+      for (int ta = warp; ta < 16; ta += 2 * nw) {
+        const int tb = ta + nw;
+        const bool hb = tb < 16;
+        TokRank<4> Ra, Rb;
+        tok_load<4>(128, lg + ta * 128, Ra);
+        tok_load<4>(128, lg + (hb ? tb : ta) * 128, Rb);
+#pragma unroll 1
+        for (int n = 0; n < k0; ++n) {
+          uint32_t ka = 0, kb = 0;
+          int ida, idb;
+          tok_select2<4>(Ra, Rb, ka, kb, ida, idb);
+          if (lane == 0) {
+            srow[ta * 16 + n] = ida;
+            if (hb) srow[tb * 16 + n] = idb;
+          }
+          tok_take<4>(Ra, ida);
+          tok_take<4>(Rb, idb);
+        }
+      }
+      __syncwarp();
+      continue;
+    }
     if (variant == 6) {
       if (warp == 0 && lane < 16) {
         if (k0 == 4) {
@@ -255,7 +303,7 @@ int main() {
   cudaMalloc(&sel, 256 * 4);
   cudaMemcpy(d, h, sizeof(h), cudaMemcpyHostToDevice);
   int ref[2][256], got[256];
-  for (int variant = 0; variant < 7; ++variant) {
+  for (int variant = 0; variant < 8; ++variant) {
     for (int ki = 0; ki < 2; ++ki) {
       const int k0 = ki ? 8 : 4;
       long long c;
