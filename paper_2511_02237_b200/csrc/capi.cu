@@ -107,7 +107,7 @@ size_t carve(Workspace& w, bool assign) {
   take(w.group_row0, G * 4);
   take(w.group_rows, G * 4);
   take(w.hdr, sizeof(FfnHeader));
-  take(w.counters, (G + Dp / 16 + 24) * 4);
+  take(w.counters, (G + Dp / 16 + 16 + 4 * std::max<size_t>(B, 64) + 24) * 4);
   take(w.xpad, B * Dp * 2);
   // (dense decode: h [G][16][Hp] bf16, y [G][16][Dp] f32 with G <= N)
   take(w.hbuf, std::max(R * std::max(Hp, H) * 8, Nmax * 16 * Hp * 2));

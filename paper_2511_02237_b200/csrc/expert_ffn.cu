@@ -513,9 +513,14 @@ __device__ __forceinline__ void fused_gemv(const FfnParams& P, float* red, int* 
 //   plan barrier; every CTA gathers the batch plan and compacts the token
 //   lists of the expert groups (inverse permutation) in shared memory.
 // ---------------------------------------------------------------------------
-// Global scratch (zeroed by grid_exit): claims[6] = tokens routed (R1),
-// claims[8..15] = union bitmap, claims[5] = plan rows published (R2).
-constexpr int kUnionCnt = 6, kUnionBits = 8, kPlanCnt = 5;
+// Global scratch: claims[6] = tokens routed (R1), claims[5] = plan rows
+// published (R2) (both zeroed by grid_exit); claims[16 + 4t .. +4) = token t's
+// base-set bitmap (128 experts), rewritten by CTA t every launch (no atomics).
+constexpr int kUnionCnt = 6, kPlanCnt = 5, kTokBits = 16;
+__device__ __forceinline__ uint32_t* tok_bits(int* claims) {  // 16-byte aligned
+  return reinterpret_cast<uint32_t*>(
+      (reinterpret_cast<uintptr_t>(claims + kTokBits) + 15) & ~static_cast<uintptr_t>(15));
+}
 
 // R1 for token t on warps 0..3 (thread e <-> expert e, Np <= 128).
 __device__ __forceinline__ void rank_phase1(const FfnParams& P, int t, uint8_t* rs,
@@ -539,10 +544,9 @@ __device__ __forceinline__ void rank_phase1(const FfnParams& P, int t, uint8_t* 
   }
   const int n = masked ? 0 : min(P.cfg.mode == OEA_MODE_VANILLA ? P.cfg.k : P.cfg.k0, N);
   const bool base = key != 0u && rank < n;
-  if (base) {
-    sets[rank] = e;
-    atomicOr(reinterpret_cast<uint32_t*>(claims + kUnionBits) + (e >> 5), 1u << (e & 31));
-  }
+  if (base) sets[rank] = e;
+  const unsigned bw = __ballot_sync(kFull, base);  // warp w holds experts 32w..32w+31
+  if ((e & 31) == 0) tok_bits(claims)[4 * t + (e >> 5)] = bw;
   if (key != 0u && rank == 0) mx[t] = l;
   asm volatile("bar.sync 3, 128;" ::: "memory");
   if (base) se[rank] = expf(l - mx[t]);
@@ -619,11 +623,24 @@ __device__ __forceinline__ int union_barrier(const FfnParams& P, uint8_t* rs, co
     if (lane == 0)
       while (ld_acquire_gpu(claims + kUnionCnt) < P.B) __nanosleep(32);
     __syncwarp();
+    // union = OR of the tokens' base bitmaps (lane t < B reads token t's)
+    uint4 tb = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll 1
+    for (int t = lane; t < P.B; t += 32) {
+      const uint4 v = __ldcg(reinterpret_cast<const uint4*>(tok_bits(claims)) + t);
+      tb.x |= v.x;
+      tb.y |= v.y;
+      tb.z |= v.z;
+      tb.w |= v.w;
+    }
+    const uint32_t uw[4] = {__reduce_or_sync(kFull, tb.x), __reduce_or_sync(kFull, tb.y),
+                            __reduce_or_sync(kFull, tb.z), __reduce_or_sync(kFull, tb.w)};
     const int N = P.N;
     int T = 0;
-#pragma unroll 1
-    for (int base = 0; base < N; base += 32) {
-      const uint32_t word = __ldcg(reinterpret_cast<const uint32_t*>(claims + kUnionBits) + (base >> 5));
+#pragma unroll
+    for (int base = 0; base < 128; base += 32) {
+      if (base >= N) break;
+      const uint32_t word = uw[base >> 5];
       if (lane == 0) uni[base >> 5] = word;
       const int e = base + lane;
       const bool f = e < N && ((word >> lane) & 1u);
