@@ -59,7 +59,7 @@ def load_traffic():
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get("k_ffn_bf16", {}).get("dram_bytes_per_launch")
+        return d.get("k_ffn_bf16<2>", {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -196,18 +196,66 @@ def run_reference_arm(args):
 # ---------------------------------------------------------------------------
 # Our arm.
 # ---------------------------------------------------------------------------
+def layer_bytes(T, D, H, N, B):
+    """Algorithmic HBM bytes of one decode layer call: the T
+    active experts' bf16 gate/up/down weights, the bf16 router, bf16 tokens in,
+    fp32 outputs out."""
+    return T * 3 * D * H * 2 + D * N * 2 + B * D * 2 + B * D * 4
+
+
+def time_graphs(torch, stream, graphs, W, per_step=False, ctx=None):
+    """Replays graphs[0:W] untimed, then graphs[W:] back to back between two
+    events on the launching stream; per_step adds an event pair per launch.
+    Returns (mean µs per launch, per-step µs or None, kernels launched in the
+    timed region by this library)."""
+    for i in range(W):
+        graphs[i].launch()
+    torch.cuda.synchronize()
+    l0 = ctx.kernel_launches if ctx is not None else 0
+    n = len(graphs) - W
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(n + 1 if per_step else 2)]
+    with torch.cuda.stream(stream):
+        ev[0].record(stream)
+        for i in range(W, len(graphs)):
+            graphs[i].launch()
+            if per_step:
+                ev[i - W + 1].record(stream)
+        if not per_step:
+            ev[1].record(stream)
+    ev[-1].synchronize()
+    total = ev[0].elapsed_time(ev[-1]) * 1000.0 / n
+    steps = [ev[j].elapsed_time(ev[j + 1]) * 1000.0 for j in range(n)] if per_step else None
+    launched = (ctx.kernel_launches - l0) if ctx is not None else None
+    return total, steps, launched
+
+
+def plan_stats(layers, xs, cfg, out, B, idx, ctx):
+    Ts, loads = [], []
+    for i in idx:
+        L = layers[i % len(layers)]
+        L.decode(xs[i], cfg, out)
+        ctx.synchronize()
+        p = L.last_plan(B, cfg)
+        Ts.append(int(p["active_count"]))
+        loads.append(int(p["total_load"]))
+    return Ts, loads
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c1", choices=["c1", "c2", "c3", "c5"],
+                    help="c1 = the headline line (default); c2 = B x k0 sweep + latency fit; "
+                         "c3 = Qwen3-235B-shaped layer; c5 = router-only B=4096")
+    ap.add_argument("--out-dir", default=os.path.join(ROOT, "gpurun_out", "bench"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
 
-    import numpy as np
     import torch
 
     rank = int(os.environ.get("RANK", "0"))
@@ -219,7 +267,33 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    env = {"torch": torch, "dist": dist, "rank": rank, "world": world, "local": local}
+    fn = {"c1": bench_c1, "c2": bench_c2, "c3": bench_c3, "c5": bench_c5}[args.config]
+    rc = fn(args, env)
+    if dist is not None:
+        dist.destroy_process_group()
+    return rc
 
+
+def _barrier(env):
+    if env["dist"] is not None:
+        env["dist"].barrier()
+
+
+def _max_over_ranks(env, v):
+    if env["dist"] is None:
+        return v
+    torch = env["torch"]
+    t = torch.tensor([v], device="cuda", dtype=torch.float64)
+    env["dist"].all_reduce(t, op=env["dist"].ReduceOp.MAX)
+    return float(t.item())
+
+
+def bench_c1(args, env):
+    """The headline: C1 Qwen3-30B-A3B-shaped layer, B=16, OEA simplified(4, 8)
+    vs vanilla top-8 (BASELINE.json configs[0])."""
+    import numpy as np
+    torch, rank, world, local = env["torch"], env["rank"], env["world"], env["local"]
     import paper_2511_02237_b200 as oea
 
     W, K = max(3, args.warmup), max(1, args.steps)
@@ -236,72 +310,35 @@ def main():
     stream = torch.cuda.ExternalStream(ctx.stream)
     cfgs = {"oea": oea.RoutingConfig.simplified(K0, K_TOP), "vanilla": oea.RoutingConfig.vanilla(K_TOP)}
 
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-
-    def max_over_ranks(v):
-        if dist is None:
-            return v
-        t = torch.tensor([v], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
     results = {}
     clocks = None
     launches = 0
     for name, cfg in cfgs.items():
         graphs = [layers[i % ROTATE].graph(xs[i], cfg, out) for i in range(W + K)]
-        for i in range(W):
-            graphs[i].launch()
-        ctx.synchronize()
-        barrier()
-        torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        l0 = ctx.kernel_launches
+        _barrier(env)
         sampler = ClockSampler(local) if name == "oea" else None
         if sampler:
             sampler.__enter__()
-        with torch.cuda.stream(stream):
-            e0.record(stream)
-            for i in range(W, W + K):
-                graphs[i].launch()
-            e1.record(stream)
-        e1.synchronize()
+        us, _, launched = time_graphs(torch, stream, graphs, W, ctx=ctx)
         if sampler:
             sampler.__exit__()
             clocks = sampler.summary()
-        us = e0.elapsed_time(e1) * 1000.0 / K
         if name == "oea":
-            launches = ctx.kernel_launches - l0
-        barrier()
-        us = max_over_ranks(us)
-        # unique experts T per step (deterministic given layer and tokens)
-        Ts, loads = [], []
-        for i in range(W, W + K):
-            layers[i % ROTATE].decode(xs[i], cfg, out)
-            ctx.synchronize()
-            p = layers[i % ROTATE].last_plan(B, cfg)
-            Ts.append(p["active_count"])
-            loads.append(p["total_load"])
+            launches = launched
+        _barrier(env)
+        us = _max_over_ranks(env, us)
+        Ts, loads = plan_stats(layers, xs, cfg, out, B, range(W, W + K), ctx)
         T = float(np.mean(Ts))
-        expert_bytes = 3 * D * H * 2
-        layer_bytes = T * expert_bytes + D * N * 2 + B * D * 2 + B * D * 4
+        lb = layer_bytes(T, D, H, N, B)
         results[name] = {"us": us, "T_mean": T, "T_min": int(min(Ts)), "T_max": int(max(Ts)),
-                         "total_load_mean": float(np.mean(loads)),
-                         "active_bytes": layer_bytes, "GBps": layer_bytes / us / 1e3}
+                         "total_load_mean": float(np.mean(loads)), "active_bytes": lb,
+                         "GBps": lb / us / 1e3, "kernels_per_call": launched / K}
         for g in graphs:
             g.close()
 
-    # ---- per-stage timing (router | FFN as separate graphs) for the roofline ----
+    # The two-kernel path (router cluster | FFN), for reference: per-stage times.
     cfg = cfgs["oea"]
     stage = [layers[r].stage_graphs(xs[r], cfg, out) for r in range(ROTATE)]
-    Ts_stage = []
-    for r in range(ROTATE):
-        layers[r].decode(xs[r], cfg, out)
-        ctx.synchronize()
-        Ts_stage.append(layers[r].last_plan(B, cfg)["active_count"])
     for i in range(W):
         stage[i % ROTATE][0].launch()
         stage[i % ROTATE][1].launch()
@@ -316,22 +353,25 @@ def main():
             g_f.launch()
             ev[i][2].record(stream)
     torch.cuda.synchronize()
-    router_us = statistics.mean(ev[i][0].elapsed_time(ev[i][1]) * 1000 for i in range(K))
-    ffn_times = [ev[i][1].elapsed_time(ev[i][2]) * 1000 for i in range(K)]
-    ffn_us = statistics.mean(ffn_times)
-    ffn_bytes = statistics.mean(Ts_stage[i % ROTATE] * 3 * D * H * 2 + B * D * 2 + B * D * 4
-                                for i in range(K))
+    two_kernel = {"router_us": statistics.mean(ev[i][0].elapsed_time(ev[i][1]) * 1000 for i in range(K)),
+                  "ffn_us": statistics.mean(ev[i][1].elapsed_time(ev[i][2]) * 1000 for i in range(K))}
     for gr, gf in stage:
         gr.close()
         gf.close()
+
+    # Roofline of the dominant (and only) kernel of the layer call: the fused
+    # single-launch decode k_ffn_bf16<2> (gate GEMV + routing + grouped SwiGLU
+    # + combine). One graph = one launch, so the event-timed step IS the
+    # kernel's average launch duration.
+    o, v = results["oea"], results["vanilla"]
     peak, peak_src = load_peak()
-    achieved = ffn_bytes / ffn_us / 1e3
     traffic = load_traffic()
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "kernel": "k_ffn_bf16",
-                "algorithmic_bytes_per_launch": ffn_bytes, "kernel_us": ffn_us,
-                "peak_source": peak_src,
-                "frac_of_8TBps_nominal": achieved / 8000.0}
+    roofline = {"bound": "hbm", "achieved": o["GBps"], "peak": peak, "unit": "GB/s",
+                "frac": o["GBps"] / peak, "traffic": traffic, "kernel": "k_ffn_bf16<2> (fused layer)",
+                "algorithmic_bytes_per_launch": o["active_bytes"], "kernel_us": o["us"],
+                "bytes_formula": "T*3*D*H*2 + D*N*2 + B*D*2 + B*D*4",
+                "peak_source": peak_src, "frac_of_8TBps_nominal": o["GBps"] / 8000.0,
+                "vanilla_frac": v["GBps"] / peak}
 
     # ---- e2e through the C ABI from pinned host buffers ----
     x_host = torch.empty(W + K, B, D, dtype=torch.bfloat16).pin_memory()
@@ -339,12 +379,12 @@ def main():
     out_host = torch.empty(B, D, dtype=torch.float32).pin_memory()
     for i in range(W):
         layers[i % ROTATE].decode_host_ptr(x_host[i].data_ptr(), out_host.data_ptr(), B, cfg)
-    barrier()
+    _barrier(env)
     t0 = time.perf_counter()
     for i in range(W, W + K):
         layers[i % ROTATE].decode_host_ptr(x_host[i].data_ptr(), out_host.data_ptr(), B, cfg)
     e2e_us = (time.perf_counter() - t0) * 1e6 / K
-    e2e_us = max_over_ranks(e2e_us)
+    e2e_us = _max_over_ranks(env, e2e_us)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -356,7 +396,6 @@ def main():
             cpu = {"value": None, "unit": "us/layer-call", "cores": 1, "kind": "port",
                    "sample": f"failed: {e}"}
 
-    o, v = results["oea"], results["vanilla"]
     line = {
         "metric": METRIC, "value": o["us"], "unit": "us/layer-call", "n_gpus": world,
         "steps": K, "warmup": W, "ms_per_step": o["us"] / 1000.0, "higher_is_better": False,
@@ -373,7 +412,7 @@ def main():
         "oea": o, "vanilla": v,
         "latency_ratio_oea_vs_vanilla": o["us"] / v["us"],
         "unique_expert_ratio_oea_vs_vanilla": o["T_mean"] / v["T_mean"],
-        "stages_us": {"router_and_compaction": router_us, "ffn": ffn_us},
+        "two_kernel_path_us": two_kernel,
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_us, "unit": "us/layer-call", "h2d_bytes_per_step": B * D * 2,
@@ -383,8 +422,160 @@ def main():
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.destroy_process_group()
+    return 0
+
+
+def bench_c2(args, env):
+    """C2: the C1 layer over B in {1..256} x k0 in {1..8} (k0 = 8 is top-8):
+    per-step (T, µs) observations -> latency CSV (io.cpp schema), the OLS fit
+    of µs on T (latency.cpp fit_linear) and an SVG of the curve."""
+    import numpy as np
+    from paper_2511_02237_b200 import latency as lat
+    torch, rank = env["torch"], env["rank"]
+    import paper_2511_02237_b200 as oea
+
+    W, K = max(3, args.warmup), max(2, min(args.steps, 20))
+    layers = []
+    for r in range(ROTATE):
+        L = oea.DeviceMoeLayer(D, H, N, "bf16")
+        L.init_random(1 + r)
+        layers.append(L)
+    ctx = layers[0].ctx
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    gen = torch.Generator(device="cuda").manual_seed(4321)
+    obs, points = [], []
+    for Bs in (1, 4, 8, 16, 32, 64, 128, 256):
+        xs = torch.randn(W + K, Bs, D, device="cuda", generator=gen).to(torch.bfloat16)
+        out = torch.empty(Bs, D, device="cuda", dtype=torch.float32)
+        for k0 in range(1, K_TOP + 1):
+            cfg = oea.RoutingConfig.simplified(k0, K_TOP)
+            graphs = [layers[i % ROTATE].graph(xs[i], cfg, out) for i in range(W + K)]
+            _, steps, _ = time_graphs(torch, stream, graphs, W, per_step=True)
+            for g in graphs:
+                g.close()
+            Ts, _ = plan_stats(layers, xs, cfg, out, Bs, range(W, W + K), ctx)
+            for t, us in zip(Ts, steps):
+                obs.append(lat.LatencyObservation(t, us))
+            points.append({"B": Bs, "k0": k0, "T_mean": float(np.mean(Ts)),
+                           "us_median": float(np.median(steps)),
+                           "E_T_topk0": lat.expected_active_experts(N, k0, Bs)})
+    fit = lat.fit_linear(obs)
+    os.makedirs(args.out_dir, exist_ok=True)
+    csv_path = os.path.join(args.out_dir, "c2_latency.csv")
+    lat.write_latency_csv(csv_path, obs)
+    with open(os.path.join(args.out_dir, "c2_latency.svg"), "w") as f:
+        f.write(lat.latency_svg(obs, fit, "C1 layer (D=2048, H=768, N=128, k=8) on 1 B200: "
+                                          "latency vs unique experts"))
+    with open(os.path.join(args.out_dir, "c2_points.json"), "w") as f:
+        json.dump(points, f, indent=1)
+    per_expert_bytes = 3 * D * H * 2
+    peak, _ = load_peak()
+    line = {"metric": "C2 sweep: layer µs vs unique experts T (B x k0)", "config": {
+                "workload": "C2 Qwen3-30B-A3B-shaped layer, B in {1..256} x k0 in {1..8}, k=8",
+                "steps_per_point": K, "points": len(points)},
+            "fit": {"slope_us_per_expert": fit.b_us, "intercept_us": fit.intercept_us,
+                    "r_squared": fit.r_squared, "slope_stderr": fit.slope_stderr,
+                    "observations": len(obs),
+                    "slope_at_measured_hbm_us": per_expert_bytes / peak / 1e3},
+            "csv": os.path.relpath(csv_path, ROOT), "points": points}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def bench_c3(args, env):
+    """C3: Qwen3-235B-A22B-shaped layer (N=128, k=8, D=4096, H=1536), B=16,
+    OEA simplified(4, 8) vs top-8 on one B200."""
+    import numpy as np
+    torch, rank = env["torch"], env["rank"]
+    import paper_2511_02237_b200 as oea
+    D3, H3 = 4096, 1536
+    W, K = max(3, args.warmup), max(1, min(args.steps, 20))
+    layers = []
+    for r in range(2):  # 2 x 4.83 GB; each call streams ~2-3 GB (>> 126 MB L2)
+        L = oea.DeviceMoeLayer(D3, H3, N, "bf16")
+        L.init_random(1 + r)
+        layers.append(L)
+    ctx = layers[0].ctx
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    gen = torch.Generator(device="cuda").manual_seed(99)
+    xs = torch.randn(W + K, B, D3, device="cuda", generator=gen).to(torch.bfloat16)
+    out = torch.empty(B, D3, device="cuda", dtype=torch.float32)
+    res = {}
+    peak, _ = load_peak()
+    for name, cfg in (("oea", oea.RoutingConfig.simplified(K0, K_TOP)),
+                      ("vanilla", oea.RoutingConfig.vanilla(K_TOP))):
+        graphs = [layers[i % 2].graph(xs[i], cfg, out) for i in range(W + K)]
+        us, _, _ = time_graphs(torch, stream, graphs, W)
+        for g in graphs:
+            g.close()
+        Ts, _ = plan_stats(layers, xs, cfg, out, B, range(W, W + K), ctx)
+        T = float(np.mean(Ts))
+        lb = layer_bytes(T, D3, H3, N, B)
+        res[name] = {"us": us, "T_mean": T, "GBps": lb / us / 1e3, "frac": lb / us / 1e3 / peak}
+    line = {"metric": "C3 MoE-layer decode µs at B=16 (Qwen3-235B-A22B shape)", "value": res["oea"]["us"],
+            "unit": "us/layer-call", "higher_is_better": False, "config": {
+                "workload": "C3 Qwen3-235B-A22B-shaped single MoE layer", "D": D3, "H": H3, "N": N,
+                "k": K_TOP, "B": B, "routing": "simplified(4, 8) vs vanilla top-8"},
+            "oea": res["oea"], "vanilla": res["vanilla"],
+            "latency_ratio_oea_vs_vanilla": res["oea"]["us"] / res["vanilla"]["us"]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def bench_c5(args, env):
+    """C5: router-only stress, B=4096 tokens x N=128, k=8, k0 in 1..8: the
+    fp64 route_f64 path (K1) on device-resident scores (softmax of N(0,1)
+    logits), per call µs and tokens/s."""
+    import ctypes as C
+    torch, rank = env["torch"], env["rank"]
+    import paper_2511_02237_b200 as oea
+    from paper_2511_02237_b200._capi import PlanViewC, lib, default_context
+    ctx = default_context()
+    Bc, Nc = 4096, 128
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    scores = torch.softmax(torch.randn(Bc, Nc, device="cuda", dtype=torch.float64, generator=gen), dim=1)
+    W, K = max(3, args.warmup), max(5, min(args.steps, 50))
+    res = []
+    for k0 in range(1, K_TOP + 1):
+        cfg = oea.RoutingConfig.simplified(k0, K_TOP)
+        stride = oea.plan_set_stride(cfg.resolved(Nc))
+        sets = torch.empty(Bc, stride, dtype=torch.int32, device="cuda")
+        set_len = torch.empty(Bc, dtype=torch.int32, device="cuda")
+        w = torch.empty(Bc, stride, dtype=torch.float64, device="cuda")
+        loads = torch.empty(Nc, dtype=torch.int32, device="cuda")
+        au = torch.empty(Nc, dtype=torch.int32, device="cuda")
+        cnt = torch.empty(1, dtype=torch.int32, device="cuda")
+        tot = torch.empty(1, dtype=torch.int64, device="cuda")
+        pv = PlanViewC(stride, sets.data_ptr(), set_len.data_ptr(), w.data_ptr(), None,
+                       loads.data_ptr(), au.data_ptr(), cnt.data_ptr(), tot.data_ptr(),
+                       None, None, None, None, None)
+        c = cfg.to_c()
+
+        def call():
+            ctx.check(lib().oea_route_f64(ctx.h, C.c_void_p(scores.data_ptr()), None, Bc, Nc,
+                                          C.byref(c), C.byref(pv), None))
+        for _ in range(W):
+            call()
+        ctx.synchronize()
+        stream = torch.cuda.ExternalStream(ctx.stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(K):
+                call()
+            e1.record(stream)
+        e1.synchronize()
+        us = e0.elapsed_time(e1) * 1000.0 / K
+        res.append({"k0": k0, "us": us, "tokens_per_s": Bc / us * 1e6, "T": int(cnt.item())})
+    line = {"metric": "C5 router-only µs per B=4096 route (fp64 route_f64, bit-exact path)",
+            "value": res[3]["us"], "unit": "us/route-call", "higher_is_better": False,
+            "config": {"workload": "C5 router stress", "B": Bc, "N": Nc, "k": K_TOP,
+                       "scores": "softmax of N(0,1) fp64 logits, device-resident"},
+            "sweep": res}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     return 0
 
 

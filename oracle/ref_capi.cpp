@@ -217,6 +217,25 @@ double ref_expected_active_experts(int N, int k, int B) {
   return expected_active_experts(N, k, B);
 }
 
+// fit_linear (latency.cpp:39-85) on n (T, us) observations; out = b, intercept,
+// r2, residual_std, slope_stderr, intercept_stderr.
+int ref_fit_linear(const int32_t* T, const double* us, int n, double* out) {
+  REF_GUARD({
+    std::vector<LatencyObservation> obs(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) {
+      obs[i].active_experts = T[i];
+      obs[i].latency_us = us[i];
+    }
+    const FitResult f = fit_linear(obs);
+    out[0] = f.params.b_us;
+    out[1] = f.intercept_us;
+    out[2] = f.r_squared;
+    out[3] = f.residual_std;
+    out[4] = f.slope_stderr;
+    out[5] = f.intercept_stderr;
+  })
+}
+
 // make_random_layer / make_random_batch (moe_layer.cpp:76-116) into flat arrays.
 int ref_make_random_layer(int D, int H, int N, uint64_t seed, double* router, double* wg,
                           double* wu, double* wd) {

@@ -323,6 +323,20 @@ __global__ void k_f32_to_f64(const float* __restrict__ a, size_t n, double* __re
     b[f] = static_cast<double>(a[f]);
 }
 
+// Kernel nodes of a captured decode graph (launch accounting per replay).
+int count_kernel_nodes(cudaGraph_t graph) {
+  size_t n = 0;
+  if (cudaGraphGetNodes(graph, nullptr, &n) != cudaSuccess || n == 0) return 0;
+  std::vector<cudaGraphNode_t> nodes(n);
+  if (cudaGraphGetNodes(graph, nodes.data(), &n) != cudaSuccess) return 0;
+  int k = 0;
+  for (size_t i = 0; i < n; ++i) {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(nodes[i], &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++k;
+  }
+  return k;
+}
+
 int blocks_for(size_t n) {
   return static_cast<int>(std::max<size_t>(1, std::min<size_t>(4096, (n + 255) / 256)));
 }
@@ -1032,9 +1046,7 @@ int oea_decode_graph_create(oea_ctx_t ctx, oea_layer_t L, const void* x_dev,
     return r ? r : oea_check_cuda(ctx, e, "cudaStreamEndCapture");
   }
   g->graph = graph;
-  size_t nnodes = 0;
-  cudaGraphGetNodes(graph, nullptr, &nnodes);
-  g->kernels = L->dtype == OEA_DTYPE_BF16 ? 2 : static_cast<int>(nnodes);
+  g->kernels = count_kernel_nodes(graph);
   e = cudaGraphInstantiate(&g->exec, graph, 0);
   if (e != cudaSuccess) {
     cudaGraphDestroy(graph);

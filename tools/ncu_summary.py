@@ -16,7 +16,8 @@ units = rows[1]
 res = {}
 for r in rows[2:]:
     name = r[hdr.index("Kernel Name")]
-    key = "k_ffn_bf16" if "k_ffn_bf16" in name else ("k_router_fused" if "k_router_fused" in name else name[:40])
+    # "void oea_dev::k_ffn_bf16<2>(oea_dev::FfnParams)" -> "k_ffn_bf16<2>"
+    key = name.split("(")[0].replace("void ", "").replace("oea_dev::", "").strip()
     d = {}
     for w in want:
         if w in hdr:
@@ -40,7 +41,7 @@ for k, lst in res.items():
         avg["dram_bytes_per_launch"] = avg["dram__bytes_read.sum"] + avg.get("dram__bytes_write.sum", 0)
     avg["launches_captured"] = len(lst)
     summary[k] = avg
-summary["_source"] = "ncu --set full --clock-control none (tools/profile_decode.py, C1 shape, cold-cache replay)"
+summary["_source"] = "ncu --set full --clock-control none (tools/profile_decode.py, C1 shape, OEA simplified(4,8), cold-cache replay)"
 json.dump(summary, open(out, "w"), indent=1)
 for k, v in summary.items():
     if isinstance(v, dict):
