@@ -161,6 +161,14 @@ int oea_phase2_f64_host(oea_ctx_t ctx, const uint8_t* mask, int32_t B, int32_t N
  * drop-in moe_forward<float/double> tolerances (1e-5 / fp64). */
 int oea_layer_create(oea_ctx_t ctx, int32_t D, int32_t H, int32_t N, int32_t dtype,
                      oea_layer_t* out);
+/* Expert-parallel shard (bf16): holds experts [e_begin, e_end) of the N its
+ * full router routes over (ownership: oea_ep_owner). Routing is global, so the
+ * expert sets equal the unsharded layer's bit for bit; oea_moe_decode returns
+ * this shard's partial sum out[t] = sum over held j in S_t of w_j y_j (set
+ * order), to be summed across the EP group (bench/EP: NCCL reduce-scatter).
+ * Expert indices of upload/download stay global. */
+int oea_layer_create_shard(oea_ctx_t ctx, int32_t D, int32_t H, int32_t N, int32_t dtype,
+                           int32_t e_begin, int32_t e_end, oea_layer_t* out);
 int oea_layer_destroy(oea_layer_t layer);
 /* router: D x N row-major (moe_layer.hpp:46). src_dtype: oea_dtype of src.
  * src_on_device: 0 host, 1 device. Values are rounded to the layer dtype
@@ -188,7 +196,11 @@ int oea_layer_info(oea_layer_t layer, int32_t* D, int32_t* H, int32_t* N,
  * out: B x D fp32 (bf16 layers) or fp64 (f32/f64 layers).
  * BF16 layers run the fused router (K2, fp32 logits, ranking on logits) and
  * the tensor-core FFN (K4/K5); F32/F64 layers run router_scores in fp64 +
- * route_f64 + the SIMT FFN. */
+ * route_f64 + the SIMT FFN.
+ * stream: NULL = the context's own (non-blocking) stream; pass
+ * cudaStreamLegacy ((void*)0x1) to order with the legacy default stream.
+ * Launches of one context are serialised on its workspace: do not run two
+ * decodes of the same context concurrently on different streams. */
 int oea_moe_decode(oea_ctx_t ctx, oea_layer_t layer, const void* x_dev,
                    const uint8_t* mask_dev, int32_t B, const oea_routing_cfg* cfg,
                    void* out_dev, void* stream);

@@ -79,6 +79,7 @@ def lib():
                 "oea_phase1_f64_host": [vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, i32, vp, vp],
                 "oea_phase2_f64_host": [vp, vp, i32, i32, vp, vp, vp, i32, vp, vp],
                 "oea_layer_create": [vp, i32, i32, i32, i32, vp],
+                "oea_layer_create_shard": [vp, i32, i32, i32, i32, i32, i32, vp],
                 "oea_layer_destroy": [vp],
                 "oea_layer_upload_router": [vp, vp, i32, i32],
                 "oea_layer_upload_expert": [vp, i32, vp, vp, vp, i32, i32],
@@ -117,7 +118,7 @@ EXPORTED = (
     "oea_layer_download_router", "oea_layer_download_expert", "oea_layer_info",
     "oea_moe_decode", "oea_moe_decode_host", "oea_last_plan_host", "oea_decode_graph_create",
     "oea_graph_launch", "oea_decode_stage_graphs_create", "oea_graph_destroy", "oea_moe_forward_plan_host",
-    "oea_router_scores_host", "oea_ep_owner", "oea_debug_ffn_trace")
+    "oea_router_scores_host", "oea_ep_owner", "oea_debug_ffn_trace", "oea_layer_create_shard")
 
 
 def check(rc: int, ctx=None):

@@ -107,7 +107,8 @@ size_t carve(Workspace& w, bool assign) {
   take(w.group_row0, G * 4);
   take(w.group_rows, G * 4);
   take(w.hdr, sizeof(FfnHeader));
-  take(w.counters, (G + Dp / 16 + 16 + 4 * std::max<size_t>(B, 64) + 24) * 4);
+  // [G] per-group W1 release counters | [16] grid counters | per-token base bitmaps
+  take(w.counters, (G + 16 + 4 * std::max<size_t>(B, 64) + 8) * 4);
   take(w.xpad, B * Dp * 2);
   // (dense decode: h [G][16][Hp] bf16, y [G][16][Dp] f32 with G <= N)
   take(w.hbuf, std::max(R * std::max(Hp, H) * 8, Nmax * 16 * Hp * 2));
@@ -344,6 +345,14 @@ int blocks_for(size_t n) {
 // ---------------------------------------------------------------------------
 // Decode orchestration (shared by the direct call and graph capture).
 // ---------------------------------------------------------------------------
+// The fused single-launch decode covers B <= 64, N <= 128, D % 8 == 0 and
+// p == 1 with a full piggyback window (max_p = N); expert-parallel shards run
+// only on it.
+bool fused_ok(const oea_layer* L, int B, const oea_routing_cfg& rc) {
+  return B <= kRouterTokChunk && L->router_t != nullptr && L->Np <= 128 && (L->D & 7) == 0 &&
+         (rc.mode == OEA_MODE_VANILLA || (rc.p == 1.0 && rc.max_p >= L->N));
+}
+
 // part: 0 = router + FFN (PDL-chained), 1 = router only, 2 = FFN only.
 int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const uint8_t* mask,
                 int B, const oea_routing_cfg& rc, void* out, cudaStream_t s, int part = 0) {
@@ -371,7 +380,7 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   rb.group_rows = w.group_rows;
   rb.hdr = w.hdr;
   rb.counters = w.counters;
-  rb.n_counters = w.G + L->Dp / 16 + 16;
+  rb.n_counters = w.G + 16;
   rb.out = static_cast<float*>(out);
   rb.phase1_n = w.n;
   rb.base_union = w.base_union;
@@ -383,10 +392,9 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   // + FFN pair (always used for B > 64 and for the router-only stage graph).
   // (The fused prologue is kept small — it runs cold once per launch — so it
   // covers N <= 128, p == 1 and D % 8 == 0; other shapes/configs use the pair.)
-  const bool fused = part == 0 && B <= kRouterTokChunk && L->router_t != nullptr &&
-                     L->Np <= 128 && (L->D & 7) == 0 &&
-                     (rc.mode == OEA_MODE_VANILLA || (rc.p == 1.0 && rc.max_p >= L->N)) &&
-                     getenv("OEA_TWO_KERNEL") == nullptr &&
+  const bool shard = L->n_local < L->N;
+  const bool fused = part == 0 && fused_ok(L, B, rc) &&
+                     (shard || getenv("OEA_TWO_KERNEL") == nullptr) &&
                      oea_host::ffn_bf16_smem_bytes() +
                              oea_host::ffn_route_smem_bytes(B, L->Np, stride) <= 227 * 1024;
   int r = OEA_OK;
@@ -491,6 +499,10 @@ int validate_decode(oea_ctx* ctx, oea_layer* L, int B, const oea_routing_cfg* cf
     if (oea_host::router_fused_smem_bytes(B, L->Np, L->Dp, stride_of(*rc)) > 227 * 1024)
       return fail(ctx, OEA_ERR_INVALID_ARGUMENT,
                   "moe_decode: B x N too large for the single-CTA fused router");
+    if (L->n_local < L->N && !fused_ok(L, B, *rc))
+      return fail(ctx, OEA_ERR_INVALID_ARGUMENT,
+                  "moe_decode: expert-parallel shards need the fused path (B <= 64, N <= 128, "
+                  "D % 8 == 0, p == 1, max_p = N)");
   }
   return OEA_OK;
 }
@@ -802,8 +814,8 @@ int oea_phase2_f64_host(oea_ctx_t ctx, const uint8_t* mask, int32_t B, int32_t N
 // ---------------------------------------------------------------------------
 // Layers.
 // ---------------------------------------------------------------------------
-int oea_layer_create(oea_ctx_t ctx, int32_t D, int32_t H, int32_t N, int32_t dtype,
-                     oea_layer_t* out) {
+int oea_layer_create_shard(oea_ctx_t ctx, int32_t D, int32_t H, int32_t N, int32_t dtype,
+                           int32_t e_begin, int32_t e_end, oea_layer_t* out) {
   CHECK_CTX(ctx);
   if (out == nullptr) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "null output pointer");
   *out = nullptr;
@@ -811,7 +823,14 @@ int oea_layer_create(oea_ctx_t ctx, int32_t D, int32_t H, int32_t N, int32_t dty
     return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "make_random_layer: dims must be positive");
   if (dtype != OEA_DTYPE_BF16 && dtype != OEA_DTYPE_F32 && dtype != OEA_DTYPE_F64)
     return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "layer: unknown dtype");
+  if (e_begin < 0 || e_end > N || e_begin >= e_end)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "layer shard: need 0 <= e_begin < e_end <= N");
+  if ((e_begin > 0 || e_end < N) && dtype != OEA_DTYPE_BF16)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "layer shard: expert-parallel shards are bf16");
   auto* L = new oea_layer;
+  L->e_begin = e_begin;
+  L->n_local = e_end - e_begin;
+  const int NL = L->n_local;
   L->ctx = ctx;
   L->D = D;
   L->H = H;
@@ -823,14 +842,14 @@ int oea_layer_create(oea_ctx_t ctx, int32_t D, int32_t H, int32_t N, int32_t dty
   cudaError_t e = cudaSuccess;
   if (dtype == OEA_DTYPE_BF16) {
     L->router_bytes = static_cast<size_t>(L->Np) * L->Dp * 2;
-    L->w1_bytes = static_cast<size_t>(N) * 2 * L->Dp * L->Hp * 2;
-    L->w2_bytes = static_cast<size_t>(N) * L->Dp * L->Hp * 2;
+    L->w1_bytes = static_cast<size_t>(NL) * 2 * L->Dp * L->Hp * 2;
+    L->w2_bytes = static_cast<size_t>(NL) * L->Dp * L->Hp * 2;
   } else {
     const size_t es = dtype == OEA_DTYPE_F64 ? 8 : 4;
     L->router_bytes = static_cast<size_t>(D) * N * es;
-    L->w1_bytes = static_cast<size_t>(N) * D * H * es;
+    L->w1_bytes = static_cast<size_t>(NL) * D * H * es;
     L->up_bytes = L->w1_bytes;
-    L->w2_bytes = static_cast<size_t>(N) * H * D * es;
+    L->w2_bytes = static_cast<size_t>(NL) * H * D * es;
   }
   e = cudaMalloc(&L->router, L->router_bytes);
   if (e == cudaSuccess && dtype == OEA_DTYPE_BF16) {
@@ -851,6 +870,11 @@ int oea_layer_create(oea_ctx_t ctx, int32_t D, int32_t H, int32_t N, int32_t dty
   }
   *out = L;
   return OEA_OK;
+}
+
+int oea_layer_create(oea_ctx_t ctx, int32_t D, int32_t H, int32_t N, int32_t dtype,
+                     oea_layer_t* out) {
+  return oea_layer_create_shard(ctx, D, H, N, dtype, 0, N > 0 ? N : 1, out);
 }
 
 int oea_layer_destroy(oea_layer_t L) {
@@ -883,7 +907,8 @@ int oea_layer_upload_expert(oea_layer_t L, int32_t e, const void* w_gate, const 
                             const void* w_down, int32_t src_dtype, int32_t src_on_device) {
   if (L == nullptr || !w_gate || !w_up || !w_down)
     return fail(nullptr, OEA_ERR_INVALID_ARGUMENT, "null argument");
-  if (e < 0 || e >= L->N) return fail(L->ctx, OEA_ERR_INVALID_ARGUMENT, "expert index out of range");
+  if (e < L->e_begin || e >= L->e_begin + L->n_local)
+    return fail(L->ctx, OEA_ERR_INVALID_ARGUMENT, "expert index out of range");
   int r = check_dtype(L->ctx, src_dtype);
   if (r) return r;
   return oea_host::layer_upload_expert(L, e, w_gate, w_up, w_down, src_dtype, src_on_device);
@@ -905,7 +930,8 @@ int oea_layer_download_expert(oea_layer_t L, int32_t e, void* w_gate, void* w_up
                               int32_t dst_dtype) {
   if (L == nullptr || !w_gate || !w_up || !w_down)
     return fail(nullptr, OEA_ERR_INVALID_ARGUMENT, "null argument");
-  if (e < 0 || e >= L->N) return fail(L->ctx, OEA_ERR_INVALID_ARGUMENT, "expert index out of range");
+  if (e < L->e_begin || e >= L->e_begin + L->n_local)
+    return fail(L->ctx, OEA_ERR_INVALID_ARGUMENT, "expert index out of range");
   int r = check_dtype(L->ctx, dst_dtype);
   if (r) return r;
   return oea_host::layer_download_expert(L, e, w_gate, w_up, w_down, dst_dtype);
@@ -919,7 +945,7 @@ int oea_layer_info(oea_layer_t L, int32_t* D, int32_t* H, int32_t* N, int32_t* d
   if (N) *N = L->N;
   if (dtype) *dtype = L->dtype;
   if (bytes_per_expert)
-    *bytes_per_expert = static_cast<int64_t>((L->w1_bytes + L->up_bytes + L->w2_bytes) / L->N);
+    *bytes_per_expert = static_cast<int64_t>((L->w1_bytes + L->up_bytes + L->w2_bytes) / L->n_local);
   if (device_bytes)
     *device_bytes = static_cast<int64_t>(L->router_bytes + L->w1_bytes + L->up_bytes + L->w2_bytes);
   return OEA_OK;
@@ -1171,8 +1197,7 @@ int oea_moe_forward_plan_host(oea_ctx_t ctx, oea_layer_t L, const double* x, int
   OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.w64, weights, sizeof(double) * B * set_stride,
                                     cudaMemcpyHostToDevice, s));
   oea_host::CompactBuffers cb{w.sets, w.set_len, w.row_tok, w.row_slot, w.group_a,
-                              w.group_row0, w.group_rows, w.hdr, w.counters,
-                              w.G + L->Dp / 16 + 3};
+                              w.group_row0, w.group_rows, w.hdr, w.counters, w.G + 16};
   r = oea_host::compact_launch(ctx, B, L->N, set_stride, cb, w.tokbits, w.active_union,
                                w.active_count, s);
   if (r) return r;

@@ -58,7 +58,7 @@ struct FfnParams {
   const int32_t* group_rows;
   const FfnHeader* hdr;
   int* w1_done;  // [max_groups]
-  int* cnt2;     // [Dp/16] combine arrivals, then [2] round claim counters
+  int* claims;   // grid counters after w1_done (fixed offset, see the kernel)
   __nv_bfloat16* hbuf;  // [rows][Hp]
   float* ybuf;          // [B][stride][Dp]
   const int32_t* set_len;
@@ -70,7 +70,8 @@ struct FfnParams {
   // fused_route_phase1/2). Dense path (<2>, B <= 16): W1 computes h for ALL
   // tokens of the batch, so it needs only the union (phase 1); the token lists
   // (phase 2) are needed only from the first W2 round on.
-  int xs_row;                   // bytes per token row of the shared-memory x tile
+  int xs_row;
+  int e_begin, e_count;         // experts this (possibly EP-shard) layer holds                   // bytes per token row of the shared-memory x tile
   const uint4* router_t;        // [Np][Dp/8] expert-major bf16 router
   const __nv_bfloat16* x_in;    // [B][D] caller tokens
   __nv_bfloat16* xpad_out;      // [B][Dp], written in-kernel when D != Dp, else null
@@ -147,9 +148,9 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
   // 128-wide K slice (one pipeline stage) lane quad q of k-tile j covers
   // k = 32q + 4j .. 32q + 4j + 3, so the lane's B operand for a whole stage is
   // ONE contiguous 64-byte run of its token row: 4 x 16-byte loads.
-  // x rows are read through the non-coherent path: on the fused path the
-  // zero-padded copy (D != Dp) is written before the logits grid barrier and
-  // first read after it, so no stale line can exist in this SM's L1.
+  // Token rows are read through L2 only (ld.global.cg): the caller's x
+  // buffers are rewritten between launches and a non-coherent (L1/texture)
+  // line of a previous launch could otherwise be returned.
   const uint4* bp[NB];
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb) {
@@ -191,7 +192,7 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
 
   auto ldb = [&](const uint4* p) -> uint4 {
     if (p == nullptr) return make_uint4(0u, 0u, 0u, 0u);
-    return W1 ? __ldg(p) : __ldcg(p);
+    return __ldcg(p);  // x / h rows may change between launches: L2 (coherent) only
   };
   // dense W1: byte offsets of this lane's quarter-stage chunks inside a slice
   int xoff[4];
@@ -439,12 +440,12 @@ __device__ __forceinline__ void fused_gemv(const FfnParams& P, float* red, int* 
       // all 16 token chunks + the router chunk in flight before any FMA
 #pragma unroll 1
       for (int c = tid; c < nch; c += NT) {
-        const uint4 rv = __ldg(rrow + c);
+        const uint4 rv = __ldcg(rrow + c);
         uint4 xv[16];
 #pragma unroll
         for (int t = 0; t < 16; ++t)
           xv[t] = (tc + t < P.B && c * 8 < P.D)
-                      ? __ldg(reinterpret_cast<const uint4*>(
+                      ? __ldcg(reinterpret_cast<const uint4*>(
                             P.x_in + static_cast<size_t>(tc + t) * P.D + c * 8))
                       : make_uint4(0u, 0u, 0u, 0u);
         float rf[8];
@@ -610,7 +611,9 @@ __device__ __forceinline__ void rank_phase2(const FfnParams& P, int t, uint8_t* 
 
 // After R1 (all CTAs): wait for every token's base set, then the union
 // (ascending active experts, expert -> group slot) in shared memory.
-// Returns T; CTA 0 exports the base union.
+// Expert-parallel shard: the groups are the active experts this layer holds
+// (slot -1 for the others). Returns the number of groups; CTA 0 exports the
+// full base / active union.
 __device__ __forceinline__ int union_barrier(const FfnParams& P, uint8_t* rs, const RouteSmem& L,
                                              int* claims) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -636,7 +639,7 @@ __device__ __forceinline__ int union_barrier(const FfnParams& P, uint8_t* rs, co
     const uint32_t uw[4] = {__reduce_or_sync(kFull, tb.x), __reduce_or_sync(kFull, tb.y),
                             __reduce_or_sync(kFull, tb.z), __reduce_or_sync(kFull, tb.w)};
     const int N = P.N;
-    int T = 0;
+    int T = 0, G = 0;
 #pragma unroll
     for (int base = 0; base < 128; base += 32) {
       if (base >= N) break;
@@ -644,18 +647,41 @@ __device__ __forceinline__ int union_barrier(const FfnParams& P, uint8_t* rs, co
       if (lane == 0) uni[base >> 5] = word;
       const int e = base + lane;
       const bool f = e < N && ((word >> lane) & 1u);
-      const unsigned m = __ballot_sync(kFull, f);
+      const bool own = f && e >= P.e_begin && e < P.e_begin + P.e_count;
+      const unsigned m = __ballot_sync(kFull, f), mo = __ballot_sync(kFull, own);
       const int slot = T + __popc(m & lanemask_lt());
-      if (e < N) eslot[e] = f ? slot : -1;
-      if (f) active[slot] = e;
-      if (exporter && f && P.x_base_union && P.cfg.mode != OEA_MODE_VANILLA)
-        P.x_base_union[slot] = e;
+      const int gslot = G + __popc(mo & lanemask_lt());
+      if (e < N) eslot[e] = own ? gslot : -1;
+      if (own) active[gslot] = e;
+      if (exporter) {
+        // active_union == base_union for the OEA modes; vanilla: the top-k union
+        if (f && P.x_base_union && P.cfg.mode != OEA_MODE_VANILLA) P.x_base_union[slot] = e;
+        if (e < N) P.x_active[e] = -1;
+      }
       T += __popc(m);
+      G += __popc(mo);
+    }
+    if (exporter) {
+      __syncwarp();
+      int c = 0;
+#pragma unroll
+      for (int base = 0; base < 128; base += 32) {
+        if (base >= N) break;
+        const int e = base + lane;
+        const bool f = e < N && ((uw[base >> 5] >> lane) & 1u);
+        const unsigned m = __ballot_sync(kFull, f);
+        if (f) P.x_active[c + __popc(m & lanemask_lt())] = e;
+        c += __popc(m);
+      }
     }
     if (lane == 0) {
-      misc[0] = T;
-      if (exporter && P.x_base_union_count)
-        *P.x_base_union_count = P.cfg.mode == OEA_MODE_VANILLA ? 0 : T;
+      misc[0] = G;
+      misc[1] = T;  // the full union (R2's |U|)
+      if (exporter) {
+        *P.x_active_count = T;
+        if (P.x_base_union_count)
+          *P.x_base_union_count = P.cfg.mode == OEA_MODE_VANILLA ? 0 : T;
+      }
     }
   }
   __syncthreads();
@@ -716,16 +742,14 @@ __device__ __forceinline__ void compact_smem(const FfnParams& P, uint8_t* rs, co
     }
     if (exporter) {
 #pragma unroll 1
-      for (int e = lane; e < N; e += 32) {
-        P.x_loads[e] = loads[e];
-        P.x_active[e] = e < T ? active[e] : -1;
-      }
+      for (int e = lane; e < N; e += 32) P.x_loads[e] = loads[e];
       if (lane == 0) {
-        *P.x_active_count = T;
-        *P.x_total_load = load;
+        int tl = 0;  // total load over all experts (load above: the held groups)
+        for (int e = 0; e < N; ++e) tl += loads[e];
+        *P.x_total_load = tl;
         P.x_hdr->n_groups = T;
         P.x_hdr->T = T;
-        P.x_hdr->total_load = load;
+        P.x_hdr->total_load = tl;
         P.x_hdr->n_rows = R;
       }
     }
@@ -735,7 +759,7 @@ __device__ __forceinline__ void compact_smem(const FfnParams& P, uint8_t* rs, co
 #pragma unroll 1
   for (int idx = ltid; idx < B * stride; idx += NC) {
     const int t = idx / stride, sl = idx % stride;
-    if (sl < len[t]) {
+    if (sl < len[t] && eslot[sets[idx]] >= 0) {  // (shard: held experts only)
       const int e = sets[idx];
       const uint32_t* bits = tokbits + e * Bw;
       int rank = __popc(bits[t >> 5] & ((1u << (t & 31)) - 1u));
@@ -766,7 +790,7 @@ __device__ __forceinline__ void route_phase2_plan(const FfnParams& P, uint8_t* r
   const int B = P.B, stride = P.cfg.stride, Np = P.Np;
   const int Bw = (B + 31) >> 5;
   if (static_cast<int>(blockIdx.x) < B) {
-    rank_phase2<NC>(P, blockIdx.x, rs, L, T, gt, sync);
+    rank_phase2<NC>(P, blockIdx.x, rs, L, reinterpret_cast<const int*>(rs + L.misc)[1], gt, sync);
     sync();
     if (gt == 0) red_release_gpu_add(claims + kPlanCnt, 1);
   }
@@ -858,7 +882,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
   const RouteSmem RL = route_smem_layout(P.B, P.Np, P.stride);
   uint8_t* xs = rs + RL.total;  // dense path: x tile (16 B aligned)
   // [0..1] round claims, [2] combine, [3] logits barrier, [4] exit, [5] dense plan rows
-  int* claims = P.cnt2 + (P.Dp >> 4);
+  int* claims = P.claims;  // independent of the layer's shape (one workspace, many layers)
   if (kFused) {
     if (threadIdx.x == 0) {
       PR->row_tok = reinterpret_cast<const int32_t*>(rs + RL.rtok);
@@ -967,7 +991,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
         const int RB = is1 ? RB1 : RB2;
         const int g = v / RB, rr = (v % RB) / kFfnWarps;
         const uint4* base = (is1 ? P.w1 : P.w2) +
-                            (static_cast<size_t>(PR->group_a[g]) * RB + rr * kFfnWarps) * KT * 32;
+                            (static_cast<size_t>(PR->group_a[g] - P.e_begin) * RB + rr * kFfnWarps) *
+                                KT * 32;
         for (int s = 0; s < nst; ++s) {
           if (s > 0) mbar_wait(&empty[stage], phase ^ 1u);
           if (s == 0 && !is1) {
@@ -1076,6 +1101,9 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
   }
   asm volatile("bar.sync 2, %0;" ::"r"(kComb) : "memory");
   const int ctid = warp == kRouterWarp ? kFfnWarps * 32 + lane : threadIdx.x;
+  const bool kShard = kFused && P.e_count < P.N;
+  const int* eslot = reinterpret_cast<const int*>(rs + RL.eslot);
+  const int* ssets = reinterpret_cast<const int*>(rs + RL.sets);
   const int64_t BD = static_cast<int64_t>(P.B) * P.D;
   const int64_t f0 = BD * blockIdx.x / gridDim.x, f1 = BD * (blockIdx.x + 1) / gridDim.x;
   constexpr int kSlotBatch = 16;
@@ -1089,8 +1117,9 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
       for (int j = 0; j < kSlotBatch; ++j) {
         y[j] = 0.0f;
         w[j] = 0.0f;
-        if (s0 + j < len) {
-          const size_t o = static_cast<size_t>(t) * P.stride + s0 + j;
+        const size_t o = static_cast<size_t>(t) * P.stride + s0 + j;
+        // expert-parallel shard: this layer's partial sum over its experts
+        if (s0 + j < len && (!kShard || eslot[ssets[o]] >= 0)) {
           y[j] = __ldcg(P.ybuf + o * P.Dp + d);
           w[j] = PR->wts[o];
         }
@@ -1248,7 +1277,7 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   P.group_rows = fb.group_rows;
   P.hdr = fb.hdr;
   P.w1_done = fb.counters;
-  P.cnt2 = fb.counters + fb.max_groups;
+  P.claims = fb.counters + fb.max_groups;
   P.hbuf = static_cast<__nv_bfloat16*>(fb.hbuf);
   P.ybuf = static_cast<float*>(fb.ybuf);
   P.set_len = fb.set_len;
@@ -1257,6 +1286,8 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   P.trace = fb.trace;
   P.mode = fb.mode;
   P.xs_row = L->Dp * 2 + 32;
+  P.e_begin = L->e_begin;
+  P.e_count = L->n_local;
   P.router_t = static_cast<const uint4*>(L->router_t);
   P.x_in = fb.x_in;
   P.xpad_out = fb.xpad_out;
@@ -1289,11 +1320,13 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   cfg.blockDim = dim3(kFfnThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
+  // PDL only as the router kernel's dependent (two-kernel path); the fused
+  // launch carries no programmatic-serialization attribute at all.
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 1 : 0;
   OEA_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, P));
   OEA_LAUNCHED(ctx);
   return OEA_OK;

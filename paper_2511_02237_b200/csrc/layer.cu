@@ -293,7 +293,9 @@ int layer_upload_router(oea_layer* L, const void* src, int src_dtype, int on_dev
 }
 
 static size_t expert_offset(const oea_layer* L, int which, int e) {
-  // which: 1 gate/w1, 2 up, 3 down/w2 ; returns element offset
+  // which: 1 gate/w1, 2 up, 3 down/w2 ; returns element offset of (global)
+  // expert e in this layer's (possibly expert-parallel shard) storage
+  e -= L->e_begin;
   if (L->dtype == OEA_DTYPE_BF16) {
     if (which == 3) return static_cast<size_t>(e) * L->Dp * L->Hp;
     return static_cast<size_t>(e) * 2 * L->Dp * L->Hp;
@@ -339,7 +341,7 @@ static int init_all(oea_layer* L, uint64_t key) {
   k_init_matrix<Dt><<<grid_for(static_cast<size_t>(D) * N), 256, 0, s>>>(
       key, 0, D, N, ds, 0, L->Dp, L->Hp, frag, static_cast<Dt*>(L->router));
   OEA_LAUNCHED(ctx);
-  for (int e = 0; e < N; ++e) {
+  for (int e = L->e_begin; e < L->e_begin + L->n_local; ++e) {
     const uint64_t base = static_cast<uint64_t>(D) * N + static_cast<uint64_t>(e) * 3 * dh;
     Dt* w1 = static_cast<Dt*>(L->w1) + expert_offset(L, 1, e);
     Dt* up = frag ? w1 : static_cast<Dt*>(L->w_up) + expert_offset(L, 2, e);

@@ -84,6 +84,9 @@ struct oea_ctx {
 struct oea_layer {
   oea_ctx* ctx = nullptr;
   int D = 0, H = 0, N = 0, dtype = OEA_DTYPE_BF16;
+  // Expert-parallel shard: this layer holds experts [e_begin, e_begin + n_local)
+  // of the N routed by its (full) router; a full layer has e_begin 0, n_local N.
+  int e_begin = 0, n_local = 0;
   int Dp = 0, Hp = 0, Np = 0;  // padded (bf16 fragment layout)
   // bf16: fragment-ordered weights. f32/f64: reference layout.
   void* router = nullptr;      // bf16: [Np/16][Dp/16][32][8]; else [D][N]

@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(kRouteWarps * 32)
 #pragma unroll
     for (int j = 0; j < E; ++j) {
       const int p = j * 32 + lane;
-      k[j] = p < N ? order_key_f64(__ldg(row + p)) : 0ull;
+      k[j] = p < N ? order_key_f64(__ldcg(row + p)) : 0ull;
       id[j] = static_cast<uint32_t>(p);
     }
     warp_rank_sort<E>(k, id);

@@ -1,0 +1,103 @@
+"""Expert parallelism for the Qwen3-235B-shaped MoE stack (BASELINE C4,
+SURVEY §8(e)): one process per GPU, experts sharded in contiguous blocks
+(rank r holds experts [N r / P, N (r+1) / P), `oea_ep_owner`), tokens in a
+data-parallel layout (B / P per rank).
+
+Per MoE layer (one decode step of the stack):
+  1. all-gather the ranks' token rows (bf16, B x D; 128 KiB at C4) over NCCL;
+  2. every rank runs the fused single-launch decode on its shard
+     (`DeviceMoeLayer(..., experts=(e0, e1))`): the full router routes the
+     whole batch identically on every rank — the batch union, the per-token
+     sets and gate weights are bit-identical to the single-GPU plan — and the
+     grouped SwiGLU streams only the held active experts' weights, writing
+     this rank's partial mixture out_r[t] = sum_{j in S_t held by r} w_j y_j;
+  3. reduce-scatter (sum) of the B x D fp32 partials returns each rank the
+     outputs of its own tokens.
+Per-rank latency is driven by max_r T_r, the most active experts any rank
+holds (PAPER §7).
+
+The collectives are torch.distributed (backend "nccl" on the GPUs, "gloo" for
+the CPU tests of this orchestration); the expert compute is a callable so the
+orchestration is testable without a GPU.
+"""
+from __future__ import annotations
+
+from typing import Callable, List, Optional
+
+__all__ = ["ep_expert_range", "ep_token_range", "ExpertParallelMoE"]
+
+
+def ep_expert_range(n_experts: int, world: int, rank: int):
+    """Experts [floor(N r / P), floor(N (r+1) / P)) of rank r (the block
+    ownership of `oea_ep_owner`)."""
+    if n_experts < 1 or world < 1 or not 0 <= rank < world:
+        raise ValueError("ep_expert_range: need N >= 1, P >= 1, 0 <= rank < P")
+    return (n_experts * rank) // world, (n_experts * (rank + 1)) // world
+
+
+def ep_token_range(batch: int, world: int, rank: int):
+    """Tokens [B r / P, B (r+1) / P) of rank r (data-parallel layout; B % P == 0)."""
+    if batch % world != 0:
+        raise ValueError("ep_token_range: the batch must split evenly over the EP group")
+    per = batch // world
+    return per * rank, per * (rank + 1)
+
+
+class ExpertParallelMoE:
+    """One rank's view of an expert-parallel MoE layer.
+
+    partial_fn(x_all, out_partial) computes this rank's partial mixture for the
+    whole batch x_all [B, D] into out_partial [B, D] (fp32); on the GPU it is
+    the shard layer's decode (`from_shard`)."""
+
+    def __init__(self, partial_fn: Callable, world: int, rank: int, dist=None, group=None):
+        self.partial_fn = partial_fn
+        self.world, self.rank = int(world), int(rank)
+        self.dist, self.group = dist, group
+
+    @classmethod
+    def from_shard(cls, layer, cfg, world, rank, dist=None, group=None):
+        """The GPU path: `layer` is a DeviceMoeLayer shard holding
+        ep_expert_range(N, world, rank)."""
+        want = ep_expert_range(layer.N, world, rank)
+        if tuple(layer.experts) != want:
+            raise ValueError(f"shard holds experts {layer.experts}, rank {rank} of {world} owns {want}")
+
+        def fn(x_all, out_partial):
+            from .moe_layer import torch_stream
+            # on the caller's current stream: ordered with the NCCL collectives
+            layer.decode(x_all, cfg, out_partial, stream=torch_stream())
+        return cls(fn, world, rank, dist, group)
+
+    def forward(self, x_local, out_local, x_all=None, partial=None):
+        """x_local [B/P, D] (this rank's tokens) -> out_local [B/P, D] fp32.
+        x_all / partial: optional preallocated [B, D] buffers."""
+        import torch
+        B = x_local.shape[0] * self.world
+        D = x_local.shape[1]
+        if x_all is None:
+            x_all = torch.empty((B, D), dtype=x_local.dtype, device=x_local.device)
+        if partial is None:
+            partial = torch.empty((B, D), dtype=torch.float32, device=x_local.device)
+        if self.world == 1:
+            x_all.copy_(x_local)
+            self.partial_fn(x_all, out_local)
+            return out_local
+        self.dist.all_gather_into_tensor(x_all, x_local.contiguous(), group=self.group)
+        self.partial_fn(x_all, partial)
+        self.dist.reduce_scatter_tensor(out_local, partial, op=self.dist.ReduceOp.SUM,
+                                        group=self.group)
+        return out_local
+
+
+def stack_forward(layers: List[ExpertParallelMoE], x_local, out_local, cast=None,
+                  bufs: Optional[dict] = None):
+    """A decode step through a stack of EP MoE layers: x_{l+1} = out_l (cast
+    back to the activation dtype). Returns the last layer's fp32 output."""
+    import torch
+    x = x_local
+    for i, L in enumerate(layers):
+        L.forward(x, out_local, **(bufs or {}))
+        if i + 1 < len(layers):
+            x = out_local.to(x_local.dtype) if cast is None else cast(out_local)
+    return out_local

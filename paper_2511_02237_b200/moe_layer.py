@@ -91,6 +91,18 @@ def _ptr(t):
     return t.data_ptr()
 
 
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy: the legacy default stream
+
+
+def torch_stream(stream=None) -> int:
+    """A CUDA stream handle for the C ABI from a torch stream (default: the
+    current one). torch's default stream has handle 0, which the C ABI reads
+    as "the context's own stream", so it is passed as cudaStreamLegacy."""
+    import torch
+    h = (stream or torch.cuda.current_stream()).cuda_stream
+    return h if h else CUDA_STREAM_LEGACY
+
+
 class DecodeGraph:
     """A CUDA graph of one decode call (router -> FFN) with fixed buffers."""
 
@@ -116,12 +128,17 @@ class DecodeGraph:
 class DeviceMoeLayer:
     """A device-resident MoE layer (oea_layer_t)."""
 
-    def __init__(self, D: int, H: int, N: int, dtype: str = "bf16", ctx=None):
+    def __init__(self, D: int, H: int, N: int, dtype: str = "bf16", ctx=None, experts=None):
+        """experts=(e_begin, e_end): an expert-parallel shard holding experts
+        [e_begin, e_end) of the N its full router routes over (bf16); its decode
+        returns this shard's partial sum (experts it does not hold contribute 0)."""
         self.ctx = ctx or default_context()
         self.D, self.H, self.N, self.dtype = int(D), int(H), int(N), dtype
+        self.experts = (0, self.N) if experts is None else (int(experts[0]), int(experts[1]))
         self.h = C.c_void_p()
-        self.ctx.check(lib().oea_layer_create(self.ctx.h, self.D, self.H, self.N, DTYPES[dtype],
-                                              C.byref(self.h)))
+        self.ctx.check(lib().oea_layer_create_shard(
+            self.ctx.h, self.D, self.H, self.N, DTYPES[dtype], self.experts[0], self.experts[1],
+            C.byref(self.h)))
 
     def close(self):
         if getattr(self, "h", None):
@@ -188,7 +205,7 @@ class DeviceMoeLayer:
     def download_params(self, dtype="f64") -> MoeLayerParams:
         return MoeLayerParams(self.download_router(dtype),
                               [ExpertParams(*self.download_expert(e, dtype))
-                               for e in range(self.N)])
+                               for e in range(*self.experts)])
 
     def info(self) -> dict:
         D, H, N, dt = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()

@@ -130,3 +130,61 @@ def test_decode_deterministic_and_graph(oea):
         g.launch()
     layer.ctx.synchronize()
     assert torch.equal(out1, out2)
+
+
+def test_mixed_shapes_share_workspace(oea):
+    """Layers of different shapes and batch sizes decoded back to back on one
+    context (one workspace, one set of self-resetting grid counters) give the
+    same outputs as when each runs alone."""
+    import torch
+    cfg = oea.RoutingConfig.simplified(4, 8)
+    shapes = [(2048, 768, 128, 16), (512, 256, 64, 60), (512, 256, 128, 200), (1024, 512, 64, 8)]
+    layers, xs, solo = [], [], []
+    for i, (D, H, N, B) in enumerate(shapes):
+        L = oea.DeviceMoeLayer(D, H, N, "bf16")
+        L.init_random(40 + i)
+        x = torch.randn(B, D, device="cuda").to(torch.bfloat16)
+        out = torch.empty(B, D, device="cuda", dtype=torch.float32)
+        L.decode(x, cfg, out)
+        L.ctx.synchronize()
+        layers.append(L)
+        xs.append(x)
+        solo.append(out.clone())
+    outs = [torch.empty_like(o) for o in solo]
+    for rep in range(3):
+        for i in (0, 2, 1, 3, 0, 1, 2, 0):
+            layers[i].decode(xs[i], cfg, outs[i])
+        layers[0].ctx.synchronize()
+        for i in range(len(shapes)):
+            assert torch.equal(outs[i], solo[i]), (rep, shapes[i])
+
+
+def test_chained_decodes_on_torch_stream(oea):
+    """x_{l+1} = out_l through torch ops on torch's default stream with no
+    host sync in between (the C ABI gets cudaStreamLegacy for it) equals the
+    per-layer synchronised chain."""
+    import torch
+    from paper_2511_02237_b200.moe_layer import torch_stream
+    cfg = oea.RoutingConfig.simplified(4, 8)
+    layers = []
+    for s in range(4):
+        L = oea.DeviceMoeLayer(2048, 768, 128, "bf16")
+        L.init_random(60 + s)
+        layers.append(L)
+    x = torch.randn(16, 2048, device="cuda").to(torch.bfloat16)
+
+    def run(sync):
+        h, outs = x, []
+        for L in layers:
+            o = torch.empty(16, 2048, device="cuda", dtype=torch.float32)
+            L.decode(h, cfg, o, stream=torch_stream())
+            if sync:
+                torch.cuda.synchronize()
+            outs.append(o)
+            h = o.to(torch.bfloat16)
+        torch.cuda.synchronize()
+        return outs
+    ref = run(True)
+    for _ in range(3):
+        for o, r in zip(run(False), ref):
+            assert torch.equal(o, r)

@@ -1,0 +1,82 @@
+"""Expert-parallel shards on one B200 (BASELINE C4's per-rank kernel): P
+shard layers holding contiguous expert blocks, built with the same seed as
+the unsharded layer, route the batch bit-identically (global routing) and
+their partial mixtures sum to the unsharded layer's output."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _decode(oea, torch, layer, x, cfg):
+    out = torch.empty(x.shape[0], layer.D, device="cuda", dtype=torch.float32)
+    layer.decode(x, cfg, out)
+    layer.ctx.synchronize()
+    return out.double().cpu().numpy(), layer.last_plan(x.shape[0], cfg)
+
+
+@pytest.mark.parametrize("D,H,N,B,P", [
+    (2048, 768, 128, 16, 2),   # C1 shape, dense fused path
+    (2048, 768, 128, 16, 8),
+    (512, 256, 128, 40, 4),    # token-list fused path (16 < B <= 64)
+    (256, 128, 64, 8, 3),      # uneven expert blocks
+])
+def test_shards_sum_to_unsharded(oea, D, H, N, B, P):
+    import torch
+    from paper_2511_02237_b200 import ep
+    cfg = oea.RoutingConfig.simplified(4, 8)
+    full = oea.DeviceMoeLayer(D, H, N, "bf16")
+    full.init_random(11)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(B, D, device="cuda", generator=g).to(torch.bfloat16)
+    want, wplan = _decode(oea, torch, full, x, cfg)
+    total = np.zeros_like(want)
+    for r in range(P):
+        e0, e1 = ep.ep_expert_range(N, P, r)
+        sh = oea.DeviceMoeLayer(D, H, N, "bf16", experts=(e0, e1))
+        sh.init_random(11)
+        assert sh.info()["device_bytes"] < full.info()["device_bytes"]
+        part, plan = _decode(oea, torch, sh, x, cfg)
+        for key in ("sets", "set_len", "active_union", "loads"):
+            assert np.array_equal(plan[key], wplan[key]), key
+        assert plan["active_count"] == wplan["active_count"]
+        assert np.array_equal(plan["weights"], wplan["weights"])
+        total += part
+        sh.close()
+    rel = np.abs(total - want).max() / np.abs(want).max()
+    assert rel < 1e-5, rel
+
+
+def test_shard_needs_fused_path(oea):
+    import torch
+    sh = oea.DeviceMoeLayer(256, 128, 16, "bf16", experts=(0, 8))
+    sh.init_random(1)
+    x = torch.zeros(100, 256, device="cuda", dtype=torch.bfloat16)
+    out = torch.empty(100, 256, device="cuda", dtype=torch.float32)
+    with pytest.raises(oea.InvalidArgument, match="expert-parallel shards need the fused path"):
+        sh.decode(x, oea.RoutingConfig.simplified(2, 4), out)
+
+
+def test_ep_stack_world1_matches_sequential(oea):
+    """The EP orchestration at P = 1 (no collectives) through a 3-layer stack
+    equals plain sequential decodes."""
+    import torch
+    from paper_2511_02237_b200 import ep
+    D, H, N, B = 512, 256, 64, 16
+    cfg = oea.RoutingConfig.simplified(4, 8)
+    layers = []
+    for s in range(3):
+        L = oea.DeviceMoeLayer(D, H, N, "bf16")
+        L.init_random(20 + s)
+        layers.append(L)
+    x = torch.randn(B, D, device="cuda").to(torch.bfloat16)
+    out = torch.empty(B, D, device="cuda", dtype=torch.float32)
+    ep.stack_forward([ep.ExpertParallelMoE.from_shard(L, cfg, 1, 0) for L in layers], x, out)
+    torch.cuda.synchronize()
+    ref = torch.empty_like(out)
+    h = x
+    for L in layers:  # every op on torch's current stream (ref is reused)
+        L.decode(h, cfg, ref, stream=oea.moe_layer.torch_stream())
+        h = ref.to(torch.bfloat16)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
