@@ -90,6 +90,20 @@ class ExpertParallelMoE:
         return out_local
 
 
+def residual_stack_forward(layers: List[ExpertParallelMoE], h_local, out_local,
+                           bufs: Optional[dict] = None, eps: float = 1e-6):
+    """A decode step through a pre-norm residual stack of EP MoE layers (the
+    MoE half of a Qwen3 decoder layer, attention omitted): for each layer
+    x = RMSNorm(h) (bf16), h += moe(x). h_local [B/P, D] fp32 is updated in
+    place; keeps activations at unit scale through any depth."""
+    import torch
+    for L in layers:
+        x = (h_local * torch.rsqrt(h_local.pow(2).mean(dim=1, keepdim=True) + eps)).to(torch.bfloat16)
+        L.forward(x, out_local, **(bufs or {}))
+        h_local.add_(out_local)
+    return h_local
+
+
 def stack_forward(layers: List[ExpertParallelMoE], x_local, out_local, cast=None,
                   bufs: Optional[dict] = None):
     """A decode step through a stack of EP MoE layers: x_{l+1} = out_l (cast
