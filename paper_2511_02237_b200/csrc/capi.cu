@@ -56,6 +56,9 @@ struct Workspace {
   int32_t* group_rows = nullptr;
   FfnHeader* hdr = nullptr;
   int32_t* counters = nullptr;
+  unsigned long long* xlog = nullptr;   // fused decode: tagged logits [B][Np]
+  unsigned long long* xuni = nullptr;   // tagged per-token base bitmaps [B][4]
+  unsigned long long* xplan = nullptr;  // tagged plan-row readiness [B]
   __nv_bfloat16* xpad = nullptr;
   void* hbuf = nullptr;
   void* ybuf = nullptr;
@@ -109,6 +112,9 @@ size_t carve(Workspace& w, bool assign) {
   take(w.hdr, sizeof(FfnHeader));
   // [G] per-group W1 release counters | [16] grid counters | per-token base bitmaps
   take(w.counters, (G + 16 + 4 * std::max<size_t>(B, 64) + 8) * 4);
+  take(w.xlog, B * Nmax * 8);
+  take(w.xuni, B * 8 * 8);
+  take(w.xplan, B * 8);
   take(w.xpad, B * Dp * 2);
   // (dense decode: h [G][16][Hp] bf16, y [G][16][Dp] f32 with G <= N)
   take(w.hbuf, std::max(R * std::max(Hp, H) * 8, Nmax * 16 * Hp * 2));
@@ -431,6 +437,9 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
     fb.x_in = static_cast<const __nv_bfloat16*>(x);
     fb.xpad_out = padded ? w.xpad : nullptr;
     fb.logits = w.logits;
+    fb.xlog = w.xlog;
+    fb.xuni = w.xuni;
+    fb.xplan = w.xplan;
     fb.mask = mask;
     fb.cfg = cfg;
     fb.x_sets = w.sets;

@@ -67,11 +67,16 @@ struct FfnParams {
   unsigned long long* trace;  // debug: [gridDim][8] globaltimer stamps, or null
   int mode;                   // debug: 1 = stream weights only (no math)
   // Fused single-launch decode (k_ffn_bf16<1|2>, see fused_gemv /
-  // fused_route_phase1/2). Dense path (<2>, B <= 16): W1 computes h for ALL
+  // rank_phase1/2). Dense path (<2>, B <= 16): W1 computes h for ALL
   // tokens of the batch, so it needs only the union (phase 1); the token lists
   // (phase 2) are needed only from the first W2 round on.
-  int xs_row;
-  int e_begin, e_count;         // experts this (possibly EP-shard) layer holds                   // bytes per token row of the shared-memory x tile
+  int xs_row;                   // bytes per token row of the shared-memory x tile
+  int e_begin, e_count;         // experts this (possibly EP-shard) layer holds
+  // Epoch-tagged exchange words (fused path): logits [B][Np], per-token base
+  // bitmaps [B][4], plan-row readiness [B]; tag = launch epoch + 1.
+  unsigned long long* xlog;
+  unsigned long long* xuni;
+  unsigned long long* xplan;
   const uint4* router_t;        // [Np][Dp/8] expert-major bf16 router
   const __nv_bfloat16* x_in;    // [B][D] caller tokens
   __nv_bfloat16* xpad_out;      // [B][Dp], written in-kernel when D != Dp, else null
@@ -391,7 +396,7 @@ __host__ __device__ inline RouteSmem route_smem_layout(int B, int Np, int stride
   L.n = take(B * 4);
   L.mx = take(B * 4);
   L.loads = take(Np * 4);
-  L.tokbits = take(static_cast<size_t>(Np) * Bw * 4);
+  L.tokbits = take(static_cast<size_t>(Np * Bw * 4 > 512 ? Np * Bw * 4 : 512));  // (also the union's [32][4] scratch)
   L.active = take(Np * 4);
   L.eslot = take(Np * 4);
   L.rowb = take(Np * 4);
@@ -416,7 +421,8 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
 // G: logits[t][e] for this CTA's experts; also the zero-padded x copy the
 // FFN's B fragments read when D is not a tile multiple. Ends with the grid
 // barrier after which every CTA may read all logits (and xpad).
-__device__ __forceinline__ void fused_gemv(const FfnParams& P, float* red, int* sync_cnt) {
+__device__ __forceinline__ void fused_gemv(const FfnParams& P, float* red, int* sync_cnt,
+                                           uint32_t tag) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NT = kFfnThreads;
   const int nch = P.Dp >> 3;
@@ -479,12 +485,16 @@ __device__ __forceinline__ void fused_gemv(const FfnParams& P, float* red, int* 
         float s = 0.0f;
 #pragma unroll
         for (int w = 0; w < kFfnThreads / 32; ++w) s += red[w * 16 + tid];
-        P.logits[static_cast<size_t>(tc + tid) * P.Np + e] = s;
+        // the token's router CTA polls this word (no grid barrier needed)
+        st_relaxed_u64(P.xlog + static_cast<size_t>(tc + tid) * P.Np + e,
+                       tagged(tag, __float_as_uint(s)));
       }
       __syncthreads();
     }
   }
-  // grid barrier: every CTA's logits / xpad rows are visible after it
+  // grid barrier only for the zero-padded x copy (D != Dp): its readers are
+  // every CTA (x tile, W1); the logits travel as tagged words
+  if (P.xpad_out == nullptr) return;
   __syncthreads();
   if (tid == 0) {
     stamp(P, 9);
@@ -514,18 +524,9 @@ __device__ __forceinline__ void fused_gemv(const FfnParams& P, float* red, int* 
 //   plan barrier; every CTA gathers the batch plan and compacts the token
 //   lists of the expert groups (inverse permutation) in shared memory.
 // ---------------------------------------------------------------------------
-// Global scratch: claims[6] = tokens routed (R1), claims[5] = plan rows
-// published (R2) (both zeroed by grid_exit); claims[16 + 4t .. +4) = token t's
-// base-set bitmap (128 experts), rewritten by CTA t every launch (no atomics).
-constexpr int kUnionCnt = 6, kPlanCnt = 5, kTokBits = 16;
-__device__ __forceinline__ uint32_t* tok_bits(int* claims) {  // 16-byte aligned
-  return reinterpret_cast<uint32_t*>(
-      (reinterpret_cast<uintptr_t>(claims + kTokBits) + 15) & ~static_cast<uintptr_t>(15));
-}
-
 // R1 for token t on warps 0..3 (thread e <-> expert e, Np <= 128).
 __device__ __forceinline__ void rank_phase1(const FfnParams& P, int t, uint8_t* rs,
-                                            const RouteSmem& L, int* claims) {
+                                            const RouteSmem& L, uint32_t tag) {
   const int e = threadIdx.x;  // < 128
   const int N = P.N, stride = P.cfg.stride;
   uint32_t* keys = reinterpret_cast<uint32_t*>(rs + L.keys);
@@ -533,7 +534,17 @@ __device__ __forceinline__ void rank_phase1(const FfnParams& P, int t, uint8_t* 
   int* sets = reinterpret_cast<int*>(rs + L.sets) + t * stride;
   float* se = reinterpret_cast<float*>(rs + L.e) + t * stride;
   const bool masked = P.mask != nullptr && P.mask[t] == 0;
-  const float l = e < N ? __ldcg(P.logits + static_cast<size_t>(t) * P.Np + e) : 0.0f;
+  float l = 0.0f;
+  if (e < N) {  // expert e's CTA publishes logit (t, e) as a tagged word
+    const unsigned long long* w = P.xlog + static_cast<size_t>(t) * P.Np + e;
+    unsigned long long v = ld_relaxed_u64(w);
+    while (static_cast<uint32_t>(v >> 32) != tag) {
+      __nanosleep(20);
+      v = ld_relaxed_u64(w);
+    }
+    l = __uint_as_float(static_cast<uint32_t>(v));
+    P.logits[static_cast<size_t>(t) * P.Np + e] = l;  // exported plan: logits
+  }
   const uint32_t key = e < N && !masked ? order_key32(l) : 0u;
   keys[e] = key;
   asm volatile("bar.sync 3, 128;" ::: "memory");
@@ -547,7 +558,7 @@ __device__ __forceinline__ void rank_phase1(const FfnParams& P, int t, uint8_t* 
   const bool base = key != 0u && rank < n;
   if (base) sets[rank] = e;
   const unsigned bw = __ballot_sync(kFull, base);  // warp w holds experts 32w..32w+31
-  if ((e & 31) == 0) tok_bits(claims)[4 * t + (e >> 5)] = bw;
+  if ((e & 31) == 0) st_relaxed_u64(P.xuni + 4 * t + (e >> 5), tagged(tag, bw));
   if (key != 0u && rank == 0) mx[t] = l;
   asm volatile("bar.sync 3, 128;" ::: "memory");
   if (base) se[rank] = expf(l - mx[t]);
@@ -615,7 +626,7 @@ __device__ __forceinline__ void rank_phase2(const FfnParams& P, int t, uint8_t* 
 // (slot -1 for the others). Returns the number of groups; CTA 0 exports the
 // full base / active union.
 __device__ __forceinline__ int union_barrier(const FfnParams& P, uint8_t* rs, const RouteSmem& L,
-                                             int* claims) {
+                                             uint32_t tag) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t* uni = reinterpret_cast<uint32_t*>(rs + L.uni);
   int* active = reinterpret_cast<int*>(rs + L.active);
@@ -623,58 +634,98 @@ __device__ __forceinline__ int union_barrier(const FfnParams& P, uint8_t* rs, co
   int* misc = reinterpret_cast<int*>(rs + L.misc);
   const bool exporter = blockIdx.x == 0;
   if (warp == 0) {
-    if (lane == 0)
-      while (ld_acquire_gpu(claims + kUnionCnt) < P.B) __nanosleep(32);
-    __syncwarp();
-    // union = OR of the tokens' base bitmaps (lane t < B reads token t's)
+    // parameters the scan below needs, read before the poll (their
+    // constant-cache misses overlap the wait instead of following it)
+    const int N = P.N, e_lo = P.e_begin, e_hi = P.e_begin + P.e_count, nB = P.B;
+    int32_t* const x_active = P.x_active;
+    int32_t* const x_base_union = P.x_base_union;
+    const bool vanilla = P.cfg.mode == OEA_MODE_VANILLA;
+    asm volatile("" ::"r"(N), "r"(e_lo), "r"(e_hi), "r"(nB), "l"(x_active), "l"(x_base_union));
+    // union = OR of the tokens' base bitmaps (lane t < B polls token t's
+    // four tagged words until they carry this launch's tag)
     uint4 tb = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll 1
-    for (int t = lane; t < P.B; t += 32) {
-      const uint4 v = __ldcg(reinterpret_cast<const uint4*>(tok_bits(claims)) + t);
-      tb.x |= v.x;
-      tb.y |= v.y;
-      tb.z |= v.z;
-      tb.w |= v.w;
+    for (int t = lane; t < nB; t += 32) {
+      uint32_t wv[4];
+      bool ready;
+      do {  // the four words in flight together, one round trip per poll
+        unsigned long long v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = ld_relaxed_u64(P.xuni + 4 * t + i);
+        ready = true;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          ready &= static_cast<uint32_t>(v[i] >> 32) == tag;
+          wv[i] = static_cast<uint32_t>(v[i]);
+        }
+        if (!ready) __nanosleep(40);  // 148 CTAs poll the same 512 bytes: back off
+      } while (!ready);
+      tb.x |= wv[0];
+      tb.y |= wv[1];
+      tb.z |= wv[2];
+      tb.w |= wv[3];
     }
-    const uint32_t uw[4] = {__reduce_or_sync(kFull, tb.x), __reduce_or_sync(kFull, tb.y),
-                            __reduce_or_sync(kFull, tb.z), __reduce_or_sync(kFull, tb.w)};
-    const int N = P.N;
+    // OR across the lanes through plain shared-memory rows (no atomics: the
+    // compiler turns warp-uniform atomics into REDUX, and a REDUX costs
+    // several hundred cycles per step on this part, tools/route_bench.cu)
+    uint32_t* rows = reinterpret_cast<uint32_t*>(rs + L.tokbits);  // [32][4] scratch
+    reinterpret_cast<uint4*>(rows)[lane] = tb;  // lanes >= B hold zeros
+    __syncwarp();
+    if (lane < 4) {
+      uint32_t o = 0u;
+#pragma unroll 8
+      for (int j = 0; j < 32; ++j) o |= rows[4 * j + lane];
+      uni[lane] = o;
+    }
+    __syncwarp();
+    const uint32_t uw[4] = {uni[0], uni[1], uni[2], uni[3]};
+    if (lane == 0) stamp(P, 12);
+    // Slots by population counts of the union words held in every lane (no
+    // warp collectives): slot(e) = #union members below e; the held groups
+    // (an EP shard's experts [e_lo, e_hi)) the same over the masked words.
+    uint32_t om[4];
     int T = 0, G = 0;
 #pragma unroll
-    for (int base = 0; base < 128; base += 32) {
-      if (base >= N) break;
-      const uint32_t word = uw[base >> 5];
-      if (lane == 0) uni[base >> 5] = word;
-      const int e = base + lane;
-      const bool f = e < N && ((word >> lane) & 1u);
-      const bool own = f && e >= P.e_begin && e < P.e_begin + P.e_count;
-      const unsigned m = __ballot_sync(kFull, f), mo = __ballot_sync(kFull, own);
-      const int slot = T + __popc(m & lanemask_lt());
-      const int gslot = G + __popc(mo & lanemask_lt());
-      if (e < N) eslot[e] = own ? gslot : -1;
-      if (own) active[gslot] = e;
-      if (exporter) {
-        // active_union == base_union for the OEA modes; vanilla: the top-k union
-        if (f && P.x_base_union && P.cfg.mode != OEA_MODE_VANILLA) P.x_base_union[slot] = e;
-        if (e < N) P.x_active[e] = -1;
+    for (int w = 0; w < 4; ++w) {
+      const int lo = max(e_lo - 32 * w, 0), hi = min(e_hi - 32 * w, 32);
+      const uint32_t range = hi <= lo ? 0u
+                                      : ((hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u)) &
+                                         ~((1u << lo) - 1u));
+      om[w] = uw[w] & range;
+      T += __popc(uw[w]);
+      G += __popc(om[w]);
+    }
+    const uint32_t below = lanemask_lt();
+    int ub = 0, ob = 0;  // members below this lane's word
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const int e = 32 * w + lane;
+      if (e < N) {
+        const bool f = (uw[w] >> lane) & 1u, own = (om[w] >> lane) & 1u;
+        const int slot = ub + __popc(uw[w] & below), gslot = ob + __popc(om[w] & below);
+        eslot[e] = own ? gslot : -1;
+        if (own) active[gslot] = e;
+        if (exporter) {
+          // active_union == base_union for the OEA modes; vanilla: the top-k union
+          if (f && x_base_union && !vanilla) x_base_union[slot] = e;
+          x_active[e] = -1;
+        }
       }
-      T += __popc(m);
-      G += __popc(mo);
+      ub += __popc(uw[w]);
+      ob += __popc(om[w]);
     }
     if (exporter) {
       __syncwarp();
       int c = 0;
 #pragma unroll
-      for (int base = 0; base < 128; base += 32) {
-        if (base >= N) break;
-        const int e = base + lane;
-        const bool f = e < N && ((uw[base >> 5] >> lane) & 1u);
-        const unsigned m = __ballot_sync(kFull, f);
-        if (f) P.x_active[c + __popc(m & lanemask_lt())] = e;
-        c += __popc(m);
+      for (int w = 0; w < 4; ++w) {
+        const int e = 32 * w + lane;
+        if (e < N && ((uw[w] >> lane) & 1u)) x_active[c + __popc(uw[w] & below)] = e;
+        c += __popc(uw[w]);
       }
     }
     if (lane == 0) {
+      stamp(P, 13);
       misc[0] = G;
       misc[1] = T;  // the full union (R2's |U|)
       if (exporter) {
@@ -685,6 +736,7 @@ __device__ __forceinline__ int union_barrier(const FfnParams& P, uint8_t* rs, co
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) stamp(P, 14);
   return misc[0];
 }
 
@@ -777,7 +829,7 @@ __device__ __forceinline__ void compact_smem(const FfnParams& P, uint8_t* rs, co
 // list path, the router warp on the dense path).
 template <int NW>
 __device__ __forceinline__ void route_phase2_plan(const FfnParams& P, uint8_t* rs,
-                                                  const RouteSmem& L, int T, int* claims) {
+                                                  const RouteSmem& L, int T, uint32_t tag) {
   const int warp = NW == 1 ? 0 : threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gt = warp * 32 + lane;
   constexpr int NC = NW * 32;
@@ -791,11 +843,15 @@ __device__ __forceinline__ void route_phase2_plan(const FfnParams& P, uint8_t* r
   const int Bw = (B + 31) >> 5;
   if (static_cast<int>(blockIdx.x) < B) {
     rank_phase2<NC>(P, blockIdx.x, rs, L, reinterpret_cast<const int*>(rs + L.misc)[1], gt, sync);
-    sync();
-    if (gt == 0) red_release_gpu_add(claims + kPlanCnt, 1);
+    sync();  // (orders the group's plan-row stores before the release below)
+    if (gt == 0) st_release_u64(P.xplan + blockIdx.x, tagged(tag, 1u));
   }
-  if (gt == 0)
-    while (ld_acquire_gpu(claims + kPlanCnt) < B) __nanosleep(32);
+  // every token's plan row: acquire its tagged readiness word
+#pragma unroll 1
+  for (int t = gt; t < B; t += NC) {
+    const unsigned long long* w = P.xplan + t;
+    while (static_cast<uint32_t>(ld_acquire_u64(w) >> 32) != tag) __nanosleep(32);
+  }
   sync();
   int* len = reinterpret_cast<int*>(rs + L.len);
   int* sets = reinterpret_cast<int*>(rs + L.sets);
@@ -833,7 +889,8 @@ __device__ __forceinline__ void grid_exit(const FfnParams& P, int* claims, int G
   if (atomicAdd(&claims[4], 1) == static_cast<int>(gridDim.x) - 1) {
     for (int g = 0; g < G; ++g) P.w1_done[g] = 0;
     for (int c = 0; c < 16; ++c)
-      if (c != 4) claims[c] = 0;
+      if (c != 4 && c != 7) claims[c] = 0;
+    claims[7] += 1;  // launch epoch: the tag of the next launch's exchange words
     __threadfence();
     claims[4] = 0;
   }
@@ -881,9 +938,22 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
   uint8_t* rs = reinterpret_cast<uint8_t*>(PR + 1) + 16;
   const RouteSmem RL = route_smem_layout(P.B, P.Np, P.stride);
   uint8_t* xs = rs + RL.total;  // dense path: x tile (16 B aligned)
-  // [0..1] round claims, [2] combine, [3] logits barrier, [4] exit, [5] dense plan rows
+  // [0..1] round claims, [2] combine, [3] padded-x barrier, [4] exit, [7] launch epoch
   int* claims = P.claims;  // independent of the layer's shape (one workspace, many layers)
+  // this launch's exchange tag (the epoch only changes when a launch retires)
+  const uint32_t tag = static_cast<uint32_t>(__ldcg(claims + 7)) + 1u;
   if (kFused) {
+    if (warp == kRouterWarp && lane == 0) {
+      // Touch every line of the parameter block once, early and all at once
+      // (the router warp has no GEMV chunk): the prologue would otherwise
+      // take a constant-cache miss, serially, per newly used line.
+      asm volatile("" ::"l"(P.w1), "l"(P.hbuf), "l"(P.out), "r"(P.xs_row), "r"(P.e_begin),
+                   "l"(P.xuni), "l"(P.xplan), "l"(P.router_t), "l"(P.logits), "l"(P.mask),
+                   "r"(P.N), "r"(P.cfg.mode), "r"(P.cfg.limit));
+      asm volatile("" ::"l"(P.x_sets), "l"(P.x_w64), "l"(P.x_active), "l"(P.x_active_count),
+                   "l"(P.x_phase1_n), "l"(P.x_base_union), "l"(P.x_base_union_count),
+                   "l"(P.x_hdr), "l"(P.x_loads), "l"(P.x_total_load), "l"(P.trace));
+    }
     if (threadIdx.x == 0) {
       PR->row_tok = reinterpret_cast<const int32_t*>(rs + RL.rtok);
       PR->row_slot = reinterpret_cast<const int32_t*>(rs + RL.rslot);
@@ -893,18 +963,14 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
       PR->set_len = reinterpret_cast<const int32_t*>(rs + RL.len);
       PR->wts = reinterpret_cast<const float*>(rs + RL.e);
     }
-    fused_gemv(P, reinterpret_cast<float*>(rs + RL.red), claims + 3);
+    fused_gemv(P, reinterpret_cast<float*>(rs + RL.red), claims + 3, tag);
     if (threadIdx.x == 0) stamp(P, 5);
     // R1: CTA t routes token t (thread per expert), then the union barrier
-    if (static_cast<int>(blockIdx.x) < P.B) {
-      if (threadIdx.x < 128) rank_phase1(P, blockIdx.x, rs, RL, claims);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        stamp(P, 11);
-        red_release_gpu_add(claims + kUnionCnt, 1);
-      }
+    if (static_cast<int>(blockIdx.x) < P.B && threadIdx.x < 128) {
+      rank_phase1(P, blockIdx.x, rs, RL, tag);
+      if (threadIdx.x == 0) stamp(P, 11);
     }
-    const int T = union_barrier(P, rs, RL, claims);  // ends with __syncthreads
+    const int T = union_barrier(P, rs, RL, tag);  // ends with __syncthreads
     if (threadIdx.x == 0) {
       PR->G = T;
       stamp(P, 6);
@@ -941,7 +1007,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
     // the whole batch (redundantly per CTA, like phase 1) while the W1
     // weights stream; consumers wait for it only before their first W2 round.
     if (kDense) {
-      route_phase2_plan<1>(P, rs, RL, G, claims);
+      route_phase2_plan<1>(P, rs, RL, G, tag);
       if (lane == 0) {
         stamp(P, 7);
         mbar_arrive(plan_bar);  // W2 rounds may start
@@ -1036,7 +1102,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
     cp_async_wait_all();
     asm volatile("bar.sync 1, %0;" ::"r"(kFfnWarps * 32) : "memory");
   } else if (kFused) {
-    route_phase2_plan<kFfnWarps>(P, rs, RL, G, claims);  // overlaps the first stages
+    route_phase2_plan<kFfnWarps>(P, rs, RL, G, tag);  // overlaps the first stages
     if (threadIdx.x == 0) stamp(P, 7);
   }
   bool in_w2 = false;
@@ -1292,6 +1358,9 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   P.x_in = fb.x_in;
   P.xpad_out = fb.xpad_out;
   P.logits = fb.logits;
+  P.xlog = fb.xlog;
+  P.xuni = fb.xuni;
+  P.xplan = fb.xplan;
   P.mask = fb.mask;
   P.N = L->N;
   P.Np = L->Np;

@@ -202,6 +202,9 @@ struct FfnBuffers {
   const __nv_bfloat16* x_in = nullptr;  // [B][D] caller tokens
   __nv_bfloat16* xpad_out = nullptr;    // [B][Dp] when D != Dp
   float* logits = nullptr;              // [B][Np]
+  unsigned long long* xlog = nullptr;   // tagged exchange words (fused path)
+  unsigned long long* xuni = nullptr;
+  unsigned long long* xplan = nullptr;
   const uint8_t* mask = nullptr;
   oea_dev::Cfg cfg{};
   int32_t* x_sets = nullptr;

@@ -38,8 +38,9 @@ for name, cfg in (("oea", oea.RoutingConfig.simplified(4, 8)), ("vanilla", oea.R
         print(" fused: union known (phase 1)", st(rel[:, 6]))
         print(" fused: plan ready (phase 2) ", st(rel[:, 7]))
         if t[:, 12].any():
-            print(" debug: phase 1 rerun start  ", st(rel[:, 12]))
-            print(" debug: phase 1 rerun end    ", st(rel[:, 13]))
+            print(" fused: union words polled   ", st(rel[:, 12]))
+            print(" fused: union ballots done   ", st(rel[:, 13]))
+            print(" fused: union syncthreads    ", st(rel[:, 14]))
     r = buf.reshape(1024, 8)[1000:1008].astype(np.int64)
     r0 = r[0, 0]
     print(" router CTA stamps (us from CTA0 start): start, x-staged, gemv, sync1, end-gemv, routed, compacted")
