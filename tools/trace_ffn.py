@@ -11,7 +11,8 @@ L2 = oea.DeviceMoeLayer(D, H, N, "bf16"); L2.init_random(2)
 x = torch.randn(B, D, device="cuda").to(torch.bfloat16)
 out = torch.empty(B, D, device="cuda", dtype=torch.float32)
 torch.cuda.synchronize()
-for name, cfg in (("oea", oea.RoutingConfig.simplified(4, 8)), ("vanilla", oea.RoutingConfig.vanilla(8))):
+K0 = int(os.environ.get("K0", "4"))
+for name, cfg in (("oea", oea.RoutingConfig.simplified(K0, 8)), ("vanilla", oea.RoutingConfig.vanilla(8))):
     # back-to-back calls (no host sync in between, clocks stay up); the trace
     # buffer holds the last call
     for rep in range(int(os.environ.get("REPS", "20"))):
