@@ -554,23 +554,32 @@ def bench_c5(args, env):
                        None, None, None, None, None)
         c = cfg.to_c()
 
+        from paper_2511_02237_b200.moe_layer import torch_stream
+
         def call():
             ctx.check(lib().oea_route_f64(ctx.h, C.c_void_p(scores.data_ptr()), None, Bc, Nc,
-                                          C.byref(c), C.byref(pv), None))
+                                          C.byref(c), C.byref(pv), C.c_void_p(torch_stream())))
         for _ in range(W):
             call()
-        ctx.synchronize()
-        stream = torch.cuda.ExternalStream(ctx.stream)
+        torch.cuda.synchronize()
+        # one route call (memsets + kernels) captured in a CUDA graph: the GPU
+        # time per call, not the host's launch overhead
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            call()
+        for _ in range(W):
+            graph.replay()
+        torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            e0.record(stream)
-            for _ in range(K):
-                call()
-            e1.record(stream)
+        e0.record()
+        for _ in range(K):
+            graph.replay()
+        e1.record()
         e1.synchronize()
         us = e0.elapsed_time(e1) * 1000.0 / K
+        del graph
         res.append({"k0": k0, "us": us, "tokens_per_s": Bc / us * 1e6, "T": int(cnt.item())})
-    line = {"metric": "C5 router-only µs per B=4096 route (fp64 route_f64, bit-exact path)",
+    line = {"metric": "C5 router-only µs per B=4096 route (fp64 route_f64, bit-exact path, CUDA-graph replay)",
             "value": res[3]["us"], "unit": "us/route-call", "higher_is_better": False,
             "config": {"workload": "C5 router stress", "B": Bc, "N": Nc, "k": K_TOP,
                        "scores": "softmax of N(0,1) fp64 logits, device-resident"},

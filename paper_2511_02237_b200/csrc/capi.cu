@@ -663,6 +663,8 @@ int oea_route_f64(oea_ctx_t ctx, const double* scores_dev, const uint8_t* mask_d
   if (rb.weights == nullptr && rb.weights_f32 == nullptr) rb.weights = w.w64;  // domain check
   const Cfg dc = dev_cfg(rc, plan->set_stride);
   const int set_mode = rc.mode == OEA_MODE_VANILLA ? 0 : rc.mode == OEA_MODE_PRUNED ? 1 : 2;
+  if (oea_host::route_fast_ok(dc, N, plan->order != nullptr) && getenv("OEA_ROUTE_SORT") == nullptr)
+    return oea_host::route_f64_fast_launch(ctx, dc, B, N, rb, set_mode, s);
   return oea_host::route_f64_launch(ctx, dc, B, N, rb, false, rc.mode != OEA_MODE_VANILLA,
                                     set_mode, false, s);
 }
@@ -690,8 +692,14 @@ int oea_route_f64_host(oea_ctx_t ctx, const double* scores, const uint8_t* mask,
   if (mask) OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.mask, mask, B, cudaMemcpyHostToDevice, s));
   const Cfg dc = dev_cfg(rc, stride);
   const int set_mode = rc.mode == OEA_MODE_VANILLA ? 0 : rc.mode == OEA_MODE_PRUNED ? 1 : 2;
-  r = oea_host::route_f64_launch(ctx, dc, B, N, route_buffers(w, w.scores, mask ? w.mask : nullptr),
-                                 false, rc.mode != OEA_MODE_VANILLA, set_mode, false, s);
+  if (oea_host::route_fast_ok(dc, N, plan->order != nullptr) && getenv("OEA_ROUTE_SORT") == nullptr)
+    r = oea_host::route_f64_fast_launch(ctx, dc, B, N,
+                                        route_buffers(w, w.scores, mask ? w.mask : nullptr),
+                                        set_mode, s);
+  else
+    r = oea_host::route_f64_launch(ctx, dc, B, N,
+                                   route_buffers(w, w.scores, mask ? w.mask : nullptr), false,
+                                   rc.mode != OEA_MODE_VANILLA, set_mode, false, s);
   if (r) return r;
   r = check_domain(ctx, w, B);
   if (r) return r;

@@ -150,6 +150,11 @@ struct RouteBuffers {
 int route_f64_launch(oea_ctx* ctx, const oea_dev::Cfg& cfg, int B, int N,
                      const RouteBuffers& rb, bool order_given, bool run_phase1,
                      int set_mode, bool n_given, cudaStream_t s);
+// Fast path of route_f64 (p == 1, max_p >= N, N <= 128, no full order
+// requested): top-m picks instead of a full sort; same results bit for bit.
+bool route_fast_ok(const oea_dev::Cfg& cfg, int N, bool need_order);
+int route_f64_fast_launch(oea_ctx* ctx, const oea_dev::Cfg& cfg, int B, int N,
+                          const RouteBuffers& rb, int set_mode, cudaStream_t s);
 int union_from_list_launch(oea_ctx* ctx, const int32_t* list, int count, int N, uint32_t* bits,
                            cudaStream_t s);
 

@@ -203,7 +203,22 @@ __device__ void block_compact(int N, Pred pred, int32_t* out, int32_t* count) {
 __global__ void __launch_bounds__(1024)
     k_aggregate(const int N, const int32_t* __restrict__ loads, int32_t* __restrict__ active_union,
                 int32_t* __restrict__ active_count, const uint32_t* __restrict__ union_bits,
-                int32_t* __restrict__ base_union, int32_t* __restrict__ base_count) {
+                int32_t* __restrict__ base_union, int32_t* __restrict__ base_count,
+                int64_t* __restrict__ total_load) {
+  if (total_load) {  // fast path: total_load = sum of the loads (fill_aggregates)
+    __shared__ long long s_part[32];
+    long long mine = 0;
+    for (int e = threadIdx.x; e < N; e += blockDim.x) mine += loads[e];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(kFull, mine, off);
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = mine;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long t = 0;
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += s_part[w];
+      *total_load = t;
+    }
+  }
   block_compact(N, [&](int e) { return loads[e] > 0; }, active_union, active_count);
   if (base_union || base_count)
     block_compact(N, [&](int e) { return (union_bits[e >> 5] >> (e & 31)) & 1u; },
@@ -216,6 +231,209 @@ __global__ void k_union_from_list(const int32_t* __restrict__ list, const int co
     const int e = list[j];
     if (e >= 0 && e < N) atomicOr(&bits[e >> 5], 1u << (e & 31));
   }
+}
+
+// ---------------------------------------------------------------------------
+// Fast path (p == 1, max_p >= N, N <= 128, no full order requested): the
+// reference's selections are all top-m picks in the composite order (score
+// desc, index asc) with m <= k_max + 1, so no full sort is needed. Each lane
+// keeps its <= 4 experts sorted in registers; a pick is a 5-step shuffle
+// butterfly argmax over the lane heads (no redux: a redux.sync step costs
+// several hundred cycles on this part, tools/route_bench.cu).
+//   F1 k_fast_p1  warp per token: the first n_i = min(k0, N) ranks (p == 1:
+//                 t_i = N, routing.cpp:243-245) or, vanilla, the first k
+//                 (route_topk :205-224); the base union bitmap; for vanilla /
+//                 pruned also the weights and loads (no second pass).
+//   F2 k_fast_p2  warp per token (Oea / Simplified): the next union members
+//                 in rank order until the cap (phase2_piggyback :270-303),
+//                 then the weights and loads.
+// ---------------------------------------------------------------------------
+template <int E>
+__device__ __forceinline__ void lane_sort_desc(uint64_t (&k)[E], int (&id)[E]) {
+#pragma unroll
+  for (int a = 0; a < E; ++a)
+#pragma unroll
+    for (int b = E - 1; b > a; --b)
+      if (ranks_before(k[b], id[b], k[b - 1], id[b - 1])) {
+        const uint64_t tk = k[b];
+        k[b] = k[b - 1];
+        k[b - 1] = tk;
+        const int ti = id[b];
+        id[b] = id[b - 1];
+        id[b - 1] = ti;
+      }
+}
+
+// Best (key desc, id asc) over the warp, in every lane.
+__device__ __forceinline__ void warp_best(uint64_t& k, int& id) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const uint64_t ok = __shfl_xor_sync(kFull, k, off);
+    const int oi = __shfl_xor_sync(kFull, id, off);
+    if (ranks_before(ok, oi, k, id)) {
+      k = ok;
+      id = oi;
+    }
+  }
+}
+
+// Picks up to m more elements in rank order from the lanes' sorted lists
+// (key 0 = no element) into srow[at..]; returns how many were picked.
+template <int E>
+__device__ __forceinline__ int pick_top(const uint64_t (&k)[E], const int (&id)[E], int m,
+                                        int32_t* srow, int at) {
+  const int lane = threadIdx.x & 31;
+  int head = 0, got = 0;
+#pragma unroll 1
+  for (; got < m; ++got) {
+    uint64_t bk = 0;
+    int bid = 0x7fffffff;
+#pragma unroll
+    for (int j = 0; j < E; ++j)
+      if (j == head) {
+        bk = k[j];
+        bid = id[j];
+      }
+    warp_best(bk, bid);
+    if (bk == 0) break;
+    if ((bid & 31) == lane) ++head;  // the owning lane advances its list
+    if (lane == 0) srow[at + got] = bid;
+  }
+  return got;
+}
+
+// Weights (renormalize_weights, routing.cpp:33-49: sequential fp64 mass in
+// set order; the set's scores are loaded in parallel, one per lane, and the
+// sum runs over shuffles) and the per-CTA load histogram.
+__device__ __forceinline__ void fast_finish(const Cfg& cfg, int i, int len, const double* row,
+                                            int32_t* srow, double* weights, float* weights_f32,
+                                            int32_t* set_len, int* s_loads, int32_t* err_token,
+                                            int do_weights) {
+  const int lane = threadIdx.x & 31;
+  const int stride = cfg.stride;
+  __syncwarp();  // lane 0's set stores before the lanes read them
+  const int e = lane < len ? srow[lane] : 0;
+  const double sc = lane < len ? __ldcg(row + e) : 0.0;
+  if (lane < len) atomicAdd(&s_loads[e], 1);
+  for (int j = len + lane; j < stride; j += 32) {
+    srow[j] = -1;
+    if (weights) weights[static_cast<size_t>(i) * stride + j] = 0.0;
+    if (weights_f32) weights_f32[static_cast<size_t>(i) * stride + j] = 0.0f;
+  }
+  if (lane == 0) set_len[i] = len;
+  if (!do_weights || len == 0) return;
+  double mass = 0.0;
+#pragma unroll 1
+  for (int j = 0; j < len; ++j) mass = __dadd_rn(mass, __shfl_sync(kFull, sc, j));
+  if (lane == 0 && !(mass > 1e-12)) atomicMin(err_token, i);
+  if (lane < len) {
+    const double w = __ddiv_rn(sc, mass);
+    if (weights) weights[static_cast<size_t>(i) * stride + lane] = w;
+    if (weights_f32) weights_f32[static_cast<size_t>(i) * stride + lane] = static_cast<float>(w);
+  }
+}
+
+__device__ __forceinline__ void flush_loads(int N, int* s_loads, int32_t* loads) {
+  __syncthreads();
+  for (int e = threadIdx.x; e < N; e += blockDim.x)
+    if (s_loads[e]) atomicAdd(&loads[e], s_loads[e]);
+}
+
+// set_mode: 0 vanilla, 1 pruned (both complete here), 2 piggyback (F2 follows).
+template <int E>
+__global__ void __launch_bounds__(kRouteWarps * 32)
+    k_fast_p1(const Cfg cfg, const int B, const int N, const int set_mode, const int do_weights,
+              const double* __restrict__ scores, const uint8_t* __restrict__ mask,
+              int32_t* __restrict__ sets, int32_t* __restrict__ set_len,
+              int32_t* __restrict__ t_out, int32_t* __restrict__ n_out,
+              uint32_t* __restrict__ union_bits, double* __restrict__ weights,
+              float* __restrict__ weights_f32, int32_t* __restrict__ loads,
+              int32_t* __restrict__ err_token) {
+  __shared__ int s_loads[128];
+  for (int e = threadIdx.x; e < 128; e += blockDim.x) s_loads[e] = 0;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kRouteWarps + warp;
+  if (i < B) {
+    const double* row = scores + static_cast<size_t>(i) * N;
+    int32_t* srow = sets + static_cast<size_t>(i) * cfg.stride;
+    const bool real = mask == nullptr || mask[i] != 0;
+    uint64_t k[E];
+    int id[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const int p = j * 32 + lane;
+      k[j] = p < N && real ? order_key_f64(__ldcg(row + p)) : 0ull;
+      id[j] = p;
+    }
+    lane_sort_desc<E>(k, id);
+    const int want = set_mode == 0 ? cfg.k : cfg.k0;
+    const int n = real ? pick_top<E>(k, id, min(want, N), srow, 0) : 0;
+    __syncwarp();
+    if (set_mode != 0 && lane < n) {
+      const int e = srow[lane];
+      atomicOr(&union_bits[e >> 5], 1u << (e & 31));
+    }
+    if (lane == 0) {
+      if (t_out) t_out[i] = set_mode == 0 ? 0 : (real ? N : 0);
+      if (n_out) n_out[i] = set_mode == 0 ? 0 : n;
+    }
+    if (set_mode != 2)
+      fast_finish(cfg, i, n, row, srow, weights, weights_f32, set_len, s_loads, err_token,
+                  do_weights);
+  }
+  if (set_mode != 2) flush_loads(N, s_loads, loads);
+}
+
+template <int E>
+__global__ void __launch_bounds__(kRouteWarps * 32)
+    k_fast_p2(const Cfg cfg, const int B, const int N, const int do_weights,
+              const double* __restrict__ scores, const uint8_t* __restrict__ mask,
+              const int32_t* __restrict__ n_in, const uint32_t* __restrict__ union_bits,
+              int32_t* __restrict__ sets, int32_t* __restrict__ set_len,
+              double* __restrict__ weights, float* __restrict__ weights_f32,
+              int32_t* __restrict__ loads, int32_t* __restrict__ err_token) {
+  __shared__ int s_loads[128];
+  for (int e = threadIdx.x; e < 128; e += blockDim.x) s_loads[e] = 0;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kRouteWarps + warp;
+  if (i < B) {
+    const double* row = scores + static_cast<size_t>(i) * N;
+    int32_t* srow = sets + static_cast<size_t>(i) * cfg.stride;
+    const bool real = mask == nullptr || mask[i] != 0;
+    const int n = real ? n_in[i] : 0;
+    int len = n;
+    if (real && n < cfg.limit) {
+      // candidates: union members not in the base set (the base set is the
+      // top n overall, so every remaining member ranks after it). Base
+      // bitmap: lane j < n contributes its expert, OR-reduced by shuffles.
+      uint32_t bw[4] = {0u, 0u, 0u, 0u};
+      if (lane < n) {
+        const int e = srow[lane];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) bw[w] = (e >> 5) == w ? 1u << (e & 31) : 0u;
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) bw[w] |= __shfl_xor_sync(kFull, bw[w], off);
+      uint64_t k[E];
+      int id[E];
+#pragma unroll
+      for (int j = 0; j < E; ++j) {
+        const int p = j * 32 + lane;
+        const bool cand = p < N && ((union_bits[j] >> lane) & 1u) && !((bw[j] >> lane) & 1u);
+        k[j] = cand ? order_key_f64(__ldcg(row + p)) : 0ull;
+        id[j] = p;
+      }
+      lane_sort_desc<E>(k, id);
+      len += pick_top<E>(k, id, cfg.limit - n, srow, n);
+    }
+    fast_finish(cfg, i, real ? len : 0, row, srow, weights, weights_f32, set_len, s_loads,
+                err_token, do_weights);
+  }
+  flush_loads(N, s_loads, loads);
 }
 
 }  // namespace oea_dev
@@ -268,7 +486,49 @@ int route_f64_launch(oea_ctx* ctx, const Cfg& cfg, int B, int N, const RouteBuff
       reinterpret_cast<unsigned long long*>(rb.total_load), rb.err_token);
   OEA_LAUNCHED(ctx);
   k_aggregate<<<1, 1024, 0, s>>>(N, rb.loads, rb.active_union, rb.active_count, rb.union_bits,
-                                 rb.base_union, rb.base_union_count);
+                                 rb.base_union, rb.base_union_count, nullptr);
+  OEA_LAUNCHED(ctx);
+  return OEA_OK;
+}
+
+template <int E>
+static void launch_fast(const Cfg& cfg, int B, int N, const RouteBuffers& rb, int set_mode,
+                        int do_weights, cudaStream_t s) {
+  const int grid = (B + kRouteWarps - 1) / kRouteWarps;
+  k_fast_p1<E><<<grid, kRouteWarps * 32, 0, s>>>(cfg, B, N, set_mode, do_weights, rb.scores,
+                                                 rb.mask, rb.sets, rb.set_len, rb.t, rb.n,
+                                                 rb.union_bits, rb.weights, rb.weights_f32,
+                                                 rb.loads, rb.err_token);
+  if (set_mode == 2)
+    k_fast_p2<E><<<grid, kRouteWarps * 32, 0, s>>>(cfg, B, N, do_weights, rb.scores, rb.mask,
+                                                   rb.n, rb.union_bits, rb.sets, rb.set_len,
+                                                   rb.weights, rb.weights_f32, rb.loads,
+                                                   rb.err_token);
+}
+
+bool route_fast_ok(const Cfg& cfg, int N, bool need_order) {
+  // (sets of <= 32 so the set's scores fit one lane each)
+  return !need_order && cfg.p == 1.0 && cfg.max_p >= N && N <= 128 && cfg.k <= 32 &&
+         cfg.limit <= 32;
+}
+
+int route_f64_fast_launch(oea_ctx* ctx, const Cfg& cfg, int B, int N, const RouteBuffers& rb,
+                          int set_mode, cudaStream_t s) {
+  const int words = (N + 31) / 32;
+  OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.union_bits, 0, words * 4, s));
+  OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.loads, 0, sizeof(int32_t) * N, s));
+  OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.err_token, 0x7f, sizeof(int32_t), s));
+  const int do_weights = (rb.weights != nullptr || rb.weights_f32 != nullptr) ? 1 : 0;
+  if (N <= 32)
+    launch_fast<1>(cfg, B, N, rb, set_mode, do_weights, s);
+  else if (N <= 64)
+    launch_fast<2>(cfg, B, N, rb, set_mode, do_weights, s);
+  else
+    launch_fast<4>(cfg, B, N, rb, set_mode, do_weights, s);
+  OEA_LAUNCHED(ctx);
+  if (set_mode == 2) OEA_LAUNCHED(ctx);
+  k_aggregate<<<1, 1024, 0, s>>>(N, rb.loads, rb.active_union, rb.active_count, rb.union_bits,
+                                 rb.base_union, rb.base_union_count, rb.total_load);
   OEA_LAUNCHED(ctx);
   return OEA_OK;
 }
