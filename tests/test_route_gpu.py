@@ -201,3 +201,26 @@ def test_router_stress_b4096(oea):
         got = oea.route(s, cfg)
         want = oracle.route(s, cfg)
         assert not plan_matches(got, want, 4096)
+
+
+@pytest.mark.parametrize("N,B", [(128, 4096), (64, 300), (20, 77), (128, 5)])
+def test_fast_path_equals_sort_path(oea, N, B, monkeypatch):
+    """The p == 1 / max_p = N fast path (top-m picks, no full sort) and the
+    general sort path give bit-identical plans, masks and ties included."""
+    rng = np.random.default_rng(N * 1000 + B)
+    s = rng.exponential(size=(B, N))
+    s[:, ::5] = s[:, 1::5]  # exact ties
+    s /= s.sum(axis=1, keepdims=True)
+    mask = rng.random(B) < 0.9
+    sm = oea.ScoreMatrix(s, mask)
+    cfgs = [oea.RoutingConfig.simplified(4, 8), oea.RoutingConfig.simplified(1, 8),
+            oea.RoutingConfig.vanilla(8), oea.RoutingConfig.pruned(3, 1.0, 3),
+            oea.RoutingConfig.oea(2, 1.0, 6, 0, 6, oea.CapSemantics.PseudocodeStrict)]
+    for cfg in cfgs:
+        monkeypatch.delenv("OEA_ROUTE_SORT", raising=False)
+        fast = oea.route(sm, cfg)
+        monkeypatch.setenv("OEA_ROUTE_SORT", "1")
+        slow = oea.route(sm, cfg)
+        assert fast.sets == slow.sets and fast.weights == slow.weights, cfg
+        assert fast.active_union == slow.active_union and fast.total_load == slow.total_load
+        assert np.array_equal(fast.loads, slow.loads)
