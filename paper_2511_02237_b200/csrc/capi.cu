@@ -386,7 +386,7 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   rb.group_rows = w.group_rows;
   rb.hdr = w.hdr;
   rb.counters = w.counters;
-  rb.n_counters = w.G + 16;
+  rb.n_counters = w.G + 7;  // w1_done + grid counters 0..6 (not the launch epoch, [7])
   rb.out = static_cast<float*>(out);
   rb.phase1_n = w.n;
   rb.base_union = w.base_union;
@@ -403,9 +403,54 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
                      (shard || getenv("OEA_TWO_KERNEL") == nullptr) &&
                      oea_host::ffn_bf16_smem_bytes() +
                              oea_host::ffn_route_smem_bytes(B, L->Np, stride) <= 227 * 1024;
+  // Large batches (64 < B <= 256) with the rank-routing conditions: a
+  // route-only launch of the fused prologue (tensor-core gate GEMV, rank
+  // routing, union, plan rows), the compaction, then the FFN (three launches
+  // instead of the single-cluster router kernel).
+  const bool big = part == 0 && !fused && !shard && B > kRouterTokChunk && B <= kMaxFusedB &&
+                   L->router_t != nullptr && L->Np <= 128 && L->D == L->Dp &&
+                   (rc.mode == OEA_MODE_VANILLA || (rc.p == 1.0 && rc.max_p >= L->N)) &&
+                   getenv("OEA_TWO_KERNEL") == nullptr &&
+                   oea_host::ffn_bf16_smem_bytes() +
+                           oea_host::ffn_route_smem_bytes(B, L->Np, stride) <= 227 * 1024;
   int r = OEA_OK;
   if (rb.trace) OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.trace, 0, 8 * 8 * 1024, s));
-  if (part != 2 && !fused) {
+  if (big) {
+    oea_host::FfnBuffers rf;
+    rf.route_only = 1;
+    rf.fused = 1;
+    rf.x = x;
+    rf.counters = w.counters;
+    rf.max_groups = w.G;
+    rf.hdr = w.hdr;
+    rf.x_in = static_cast<const __nv_bfloat16*>(x);
+    rf.logits = w.logits;
+    rf.xlog = w.xlog;
+    rf.xuni = w.xuni;
+    rf.xplan = w.xplan;
+    rf.mask = mask;
+    rf.cfg = cfg;
+    rf.x_sets = w.sets;
+    rf.x_set_len = w.set_len;
+    rf.x_w32 = w.w32;
+    rf.x_w64 = w.w64;
+    rf.x_loads = w.loads;
+    rf.x_active = w.active_union;
+    rf.x_active_count = w.active_count;
+    rf.x_total_load = w.total_load;
+    rf.x_phase1_n = w.n;
+    rf.x_base_union = w.base_union;
+    rf.x_base_union_count = w.base_union_count;
+    rf.x_hdr = w.hdr;
+    rf.trace = ctx->ffn_trace;
+    r = oea_host::ffn_bf16_launch(ctx, L, B, stride, rf, false, s);
+    if (r) return r;
+    oea_host::CompactBuffers cb{w.sets, w.set_len, w.row_tok, w.row_slot, w.group_a,
+                                w.group_row0, w.group_rows, w.hdr, w.counters, w.G + 7};
+    r = oea_host::compact_launch(ctx, B, L->N, stride, cb, w.tokbits, w.active_union,
+                                 w.active_count, s);
+    if (r) return r;
+  } else if (part != 2 && !fused) {
     r = oea_host::router_fused_launch(ctx, L, cfg, B, rb, s);
     if (r || part == 1) return r;
   }
@@ -455,7 +500,7 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
     fb.x_base_union_count = w.base_union_count;
     fb.x_hdr = w.hdr;
   }
-  return oea_host::ffn_bf16_launch(ctx, L, B, stride, fb, part == 0 && !fused, s);
+  return oea_host::ffn_bf16_launch(ctx, L, B, stride, fb, part == 0 && !fused && !big, s);
 }
 
 // f32/f64 layers: router_scores (fp64) -> route_f64 -> compaction -> SIMT FFN.
@@ -1214,7 +1259,7 @@ int oea_moe_forward_plan_host(oea_ctx_t ctx, oea_layer_t L, const double* x, int
   OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.w64, weights, sizeof(double) * B * set_stride,
                                     cudaMemcpyHostToDevice, s));
   oea_host::CompactBuffers cb{w.sets, w.set_len, w.row_tok, w.row_slot, w.group_a,
-                              w.group_row0, w.group_rows, w.hdr, w.counters, w.G + 16};
+                              w.group_row0, w.group_rows, w.hdr, w.counters, w.G + 7};
   r = oea_host::compact_launch(ctx, B, L->N, set_stride, cb, w.tokbits, w.active_union,
                                w.active_count, s);
   if (r) return r;

@@ -79,6 +79,7 @@ struct FfnParams {
   unsigned long long* xuni;
   unsigned long long* xplan;
   const uint4* router_t;        // [Np][Dp/8] expert-major bf16 router
+  const uint4* router_frag;     // [Np/16][Dp/16] fragment-ordered router tiles
   const __nv_bfloat16* x_in;    // [B][D] caller tokens
   __nv_bfloat16* xpad_out;      // [B][Dp], written in-kernel when D != Dp, else null
   float* logits;        // [B][Np]
@@ -216,17 +217,21 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
   int xoff[4];
 #pragma unroll
   for (int jj = 0; jj < 4; ++jj) xoff[jj] = xs_chunk(4 * q + jj) * 16;
-  // One n-block: the next stage's 4 loads are issued right after the current
-  // stage is consumed, so their latency hides behind the stage barrier wait.
+  // One n-block (global B): the next stage's 4 loads are issued right after
+  // the current stage is consumed, so their latency hides behind the stage
+  // barrier wait (two n-blocks measured slower: spills at the register cap).
   // More n-blocks: per quarter stage (2 k-tiles) one 16-byte load per n-block.
   constexpr bool kPref = !XSM && NB <= 1 && !SPLIT;
+  constexpr int PB = 1;  // prefetched n-blocks
   // slices of this unit (K / 128); SPLIT: this warp's slice of split-stage s
   const int nslices = (W1 ? P.Dp : P.Hp) >> 7;
-  uint4 bpre[4];
+  uint4 bpre[PB][4];
   const bool math = P.mode != 1;
   if (kPref && math)
 #pragma unroll
-    for (int i = 0; i < 4; ++i) bpre[i] = ldb(bp[0] == nullptr ? nullptr : bp[0] + i);
+    for (int nb = 0; nb < PB; ++nb)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) bpre[nb][i] = ldb(bp[nb] == nullptr ? nullptr : bp[nb] + i);
 
   for (int s0 = 0; s0 < nst; ++s0) {
     mbar_wait(&full[stage], phase);
@@ -238,13 +243,18 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
 #pragma unroll
         for (int j = 0; j < kKtPerSlot; ++j) {
           const uint4 a = tiles[j * 32 + lane];
-          const uint4& v = bpre[j >> 1];
-          mma_bf16_16816(acc2[(j & 1) % NA][0], a, (j & 1) ? v.z : v.x, (j & 1) ? v.w : v.y);
+#pragma unroll
+          for (int nb = 0; nb < PB; ++nb) {
+            const uint4& v = bpre[nb][j >> 1];
+            mma_bf16_16816(acc2[(j & 1) % NA][nb], a, (j & 1) ? v.z : v.x, (j & 1) ? v.w : v.y);
+          }
         }
         if (s0 + 1 < nst)
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            bpre[i] = ldb(bp[0] == nullptr ? nullptr : bp[0] + (s + 1) * 16 + i);
+          for (int nb = 0; nb < PB; ++nb)
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              bpre[nb][i] = ldb(bp[nb] == nullptr ? nullptr : bp[nb] + (s + 1) * 16 + i);
       } else {
 #pragma unroll
         for (int jj = 0; jj < kKtPerSlot / 2; ++jj) {
@@ -453,7 +463,8 @@ __host__ __device__ inline RouteSmem route_smem_layout(int B, int Np, int stride
   L.n = take(B * 4);
   L.mx = take(B * 4);
   L.loads = take(Np * 4);
-  L.tokbits = take(static_cast<size_t>(Np * Bw * 4 > 512 ? Np * Bw * 4 : 512));  // (also the union's [32][4] scratch)
+  // (also the union's [B][4] scratch)
+  L.tokbits = take(static_cast<size_t>(Np * Bw * 4 > B * 16 ? Np * Bw * 4 : B * 16));
   L.active = take(Np * 4);
   L.eslot = take(Np * 4);
   L.rowb = take(Np * 4);
@@ -581,6 +592,69 @@ __device__ __forceinline__ void fused_gemv(const FfnParams& P, float* red, int* 
 //   plan barrier; every CTA gathers the batch plan and compacts the token
 //   lists of the expert groups (inverse permutation) in shared memory.
 // ---------------------------------------------------------------------------
+// Gate GEMV for large batches (route-only launch, B > 64): tensor-core tiles
+// of 16 experts x 16 tokens (mma.m16n8k16 on the fragment-ordered router
+// tiles, x rows as B), K split over the 8 consumer warps, partials reduced
+// in fixed warp order; logits go out as tagged words like fused_gemv's.
+__device__ __forceinline__ void tile_gemv(const FfnParams& P, float* red, uint32_t tag) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, q = lane & 3;
+  const int KT = P.Dp >> 4, nEb = P.Np >> 4, nTb = (P.B + 15) >> 4;
+#pragma unroll 1
+  for (int item = blockIdx.x; item < nEb * nTb; item += gridDim.x) {
+    const int eb = item % nEb, tb = item / nEb;
+    if (warp < kFfnWarps) {
+      float acc[2][4];
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) acc[nb][0] = acc[nb][1] = acc[nb][2] = acc[nb][3] = 0.0f;
+      const int kt0 = warp * KT / kFfnWarps, kt1 = (warp + 1) * KT / kFfnWarps;
+      const uint32_t* xr[2];
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) {
+        const int t = tb * 16 + nb * 8 + gq;
+        xr[nb] = t < P.B ? reinterpret_cast<const uint32_t*>(P.x_in + static_cast<size_t>(t) * P.D)
+                         : nullptr;
+      }
+#pragma unroll 4
+      for (int kt = kt0; kt < kt1; ++kt) {
+        const uint4 a = __ldcg(P.router_frag + (static_cast<size_t>(eb) * KT + kt) * 32 + lane);
+        const int k = kt * 16 + 2 * q;
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb) {
+          uint32_t b0 = 0, b1 = 0;
+          if (xr[nb] != nullptr) {
+            if (k < P.D) b0 = __ldcg(xr[nb] + (k >> 1));
+            if (k + 8 < P.D) b1 = __ldcg(xr[nb] + ((k + 8) >> 1));
+          }
+          mma_bf16_16816(acc[nb], a, b0, b1);
+        }
+      }
+      float* mine = red + (warp * 32 + lane) * 8;
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) mine[nb * 4 + i] = acc[nb][i];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      // lane (gq, q): experts 16eb + gq (+8), tokens 16tb + 8nb + 2q (+1)
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float v = 0.0f;
+#pragma unroll
+          for (int w = 0; w < kFfnWarps; ++w) v += red[(w * 32 + lane) * 8 + nb * 4 + i];
+          const int e = eb * 16 + gq + (i >= 2 ? 8 : 0);
+          const int t = tb * 16 + nb * 8 + 2 * q + (i & 1);
+          if (e < P.N && t < P.B)
+            st_relaxed_u64(P.xlog + static_cast<size_t>(t) * P.Np + e, tagged(tag, __float_as_uint(v)));
+        }
+    }
+    __syncthreads();
+  }
+}
+
 // R1 for token t on warps 0..3 (thread e <-> expert e, Np <= 128).
 __device__ __forceinline__ void rank_phase1(const FfnParams& P, int t, uint8_t* rs,
                                             const RouteSmem& L, uint32_t tag) {
@@ -603,7 +677,7 @@ __device__ __forceinline__ void rank_phase1(const FfnParams& P, int t, uint8_t* 
     P.logits[static_cast<size_t>(t) * P.Np + e] = l;  // exported plan: logits
   }
   const uint32_t key = e < N && !masked ? order_key32(l) : 0u;
-  keys[e] = key;
+  if (e < P.Np) keys[e] = key;  // (keys[] holds Np entries)
   asm volatile("bar.sync 3, 128;" ::: "memory");
   int rank = 0;
 #pragma unroll 8
@@ -628,7 +702,6 @@ template <int NT, typename Sync>
 __device__ __forceinline__ void rank_phase2(const FfnParams& P, int t, uint8_t* rs,
                                             const RouteSmem& L, int T, int gt, Sync sync) {
   const int N = P.N, stride = P.cfg.stride;
-  const uint32_t* keys = reinterpret_cast<const uint32_t*>(rs + L.keys);
   const uint32_t* uni = reinterpret_cast<const uint32_t*>(rs + L.uni);
   const float rowmax = reinterpret_cast<const float*>(rs + L.mx)[t];
   int* sets = reinterpret_cast<int*>(rs + L.sets) + t * stride;
@@ -649,7 +722,9 @@ __device__ __forceinline__ void rank_phase2(const FfnParams& P, int t, uint8_t* 
       for (int w = 0; w < 4; ++w) {
         const uint32_t uw = uni[w];
         const int e = 32 * w + gt;
-        if (e < N && ((uw >> gt) & 1u)) ukeys[ub + __popc(uw & below)] = keys[e];
+        if (e < N && ((uw >> gt) & 1u))  // (published by the GEMV; keys[] is per CTA, not per token)
+          ukeys[ub + __popc(uw & below)] = order_key32(__uint_as_float(static_cast<uint32_t>(
+              ld_relaxed_u64(P.xlog + static_cast<size_t>(t) * P.Np + e))));
         ub += __popc(uw);
       }
     }
@@ -716,6 +791,37 @@ __device__ __forceinline__ int union_barrier(const FfnParams& P, uint8_t* rs, co
   int* eslot = reinterpret_cast<int*>(rs + L.eslot);
   int* misc = reinterpret_cast<int*>(rs + L.misc);
   const bool exporter = blockIdx.x == 0;
+  {
+    // union = OR of the tokens' base bitmaps: thread t < B polls token t's
+    // four tagged words (all in flight at once) until they carry this
+    // launch's tag; rows OR-ed by lanes 0..3 of warp 0 below
+    uint32_t* rows = reinterpret_cast<uint32_t*>(rs + L.tokbits);  // [B][4] scratch
+#pragma unroll 1
+    for (int t = threadIdx.x; t < P.B; t += blockDim.x) {
+      uint4 v4;
+      bool ready;
+      do {
+        unsigned long long v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = ld_relaxed_u64(P.xuni + 4 * t + i);
+        ready = true;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ready &= static_cast<uint32_t>(v[i] >> 32) == tag;
+        v4 = make_uint4(static_cast<uint32_t>(v[0]), static_cast<uint32_t>(v[1]),
+                        static_cast<uint32_t>(v[2]), static_cast<uint32_t>(v[3]));
+        if (!ready) __nanosleep(40);  // every CTA polls the same words: back off
+      } while (!ready);
+      reinterpret_cast<uint4*>(rows)[t] = v4;
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+      uint32_t o = 0u;
+#pragma unroll 4
+      for (int t = 0; t < P.B; ++t) o |= rows[4 * t + threadIdx.x];
+      uni[threadIdx.x] = o;
+    }
+    __syncthreads();
+  }
   if (warp == 0) {
     // parameters the scan below needs, read before the poll (their
     // constant-cache misses overlap the wait instead of following it)
@@ -724,43 +830,6 @@ __device__ __forceinline__ int union_barrier(const FfnParams& P, uint8_t* rs, co
     int32_t* const x_base_union = P.x_base_union;
     const bool vanilla = P.cfg.mode == OEA_MODE_VANILLA;
     asm volatile("" ::"r"(N), "r"(e_lo), "r"(e_hi), "r"(nB), "l"(x_active), "l"(x_base_union));
-    // union = OR of the tokens' base bitmaps (lane t < B polls token t's
-    // four tagged words until they carry this launch's tag)
-    uint4 tb = make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll 1
-    for (int t = lane; t < nB; t += 32) {
-      uint32_t wv[4];
-      bool ready;
-      do {  // the four words in flight together, one round trip per poll
-        unsigned long long v[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) v[i] = ld_relaxed_u64(P.xuni + 4 * t + i);
-        ready = true;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          ready &= static_cast<uint32_t>(v[i] >> 32) == tag;
-          wv[i] = static_cast<uint32_t>(v[i]);
-        }
-        if (!ready) __nanosleep(40);  // 148 CTAs poll the same 512 bytes: back off
-      } while (!ready);
-      tb.x |= wv[0];
-      tb.y |= wv[1];
-      tb.z |= wv[2];
-      tb.w |= wv[3];
-    }
-    // OR across the lanes through plain shared-memory rows (no atomics: the
-    // compiler turns warp-uniform atomics into REDUX, and a REDUX costs
-    // several hundred cycles per step on this part, tools/route_bench.cu)
-    uint32_t* rows = reinterpret_cast<uint32_t*>(rs + L.tokbits);  // [32][4] scratch
-    reinterpret_cast<uint4*>(rows)[lane] = tb;  // lanes >= B hold zeros
-    __syncwarp();
-    if (lane < 4) {
-      uint32_t o = 0u;
-#pragma unroll 8
-      for (int j = 0; j < 32; ++j) o |= rows[4 * j + lane];
-      uni[lane] = o;
-    }
-    __syncwarp();
     const uint32_t uw[4] = {uni[0], uni[1], uni[2], uni[3]};
     if (lane == 0) stamp(P, 12);
     // Slots by population counts of the union words held in every lane (no
@@ -1015,7 +1084,8 @@ __device__ __forceinline__ void dense_route_phase2_local(const FfnParams& P, uin
 // list path, the router warp on the dense path).
 template <int NW>
 __device__ __forceinline__ void route_phase2_plan(const FfnParams& P, uint8_t* rs,
-                                                  const RouteSmem& L, int T, uint32_t tag) {
+                                                  const RouteSmem& L, int T, uint32_t tag,
+                                                  bool gather = true) {
   const int warp = NW == 1 ? 0 : threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gt = warp * 32 + lane;
   constexpr int NC = NW * 32;
@@ -1027,11 +1097,13 @@ __device__ __forceinline__ void route_phase2_plan(const FfnParams& P, uint8_t* r
   };
   const int B = P.B, stride = P.cfg.stride, Np = P.Np;
   const int Bw = (B + 31) >> 5;
-  if (static_cast<int>(blockIdx.x) < B) {
-    rank_phase2<NC>(P, blockIdx.x, rs, L, reinterpret_cast<const int*>(rs + L.misc)[1], gt, sync);
+#pragma unroll 1
+  for (int t = blockIdx.x; t < B; t += gridDim.x) {
+    rank_phase2<NC>(P, t, rs, L, reinterpret_cast<const int*>(rs + L.misc)[1], gt, sync);
     sync();  // (orders the group's plan-row stores before the release below)
-    if (gt == 0) st_release_u64(P.xplan + blockIdx.x, tagged(tag, 1u));
+    if (gt == 0) st_release_u64(P.xplan + t, tagged(tag, 1u));
   }
+  if (!gather) return;
   // every token's plan row: acquire its tagged readiness word
 #pragma unroll 1
   for (int t = gt; t < B; t += NC) {
@@ -1098,6 +1170,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) {
   constexpr bool kFused = MODE != 0;
   constexpr bool kDense = MODE == 2;
+  constexpr bool kRouteOnly = MODE == 3;  // plan only (B > 64); the FFN runs as MODE 0
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
@@ -1155,17 +1228,31 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
       PR->set_len = reinterpret_cast<const int32_t*>(rs + RL.len);
       PR->wts = reinterpret_cast<const float*>(rs + RL.e);
     }
-    fused_gemv(P, reinterpret_cast<float*>(rs + RL.red), claims + 3, tag);
+    if (kRouteOnly)
+      tile_gemv(P, SR.buf, tag);
+    else
+      fused_gemv(P, reinterpret_cast<float*>(rs + RL.red), claims + 3, tag);
     if (threadIdx.x == 0) stamp(P, 5);
     // R1: CTA t routes token t (thread per expert), then the union barrier
-    if (static_cast<int>(blockIdx.x) < P.B && threadIdx.x < 128) {
-      rank_phase1(P, blockIdx.x, rs, RL, tag);
+    if (threadIdx.x < 128) {
+#pragma unroll 1
+      for (int t = blockIdx.x; t < P.B; t += gridDim.x) {
+        rank_phase1(P, t, rs, RL, tag);
+        asm volatile("bar.sync 3, 128;" ::: "memory");  // keys[] reused by the next token
+      }
       if (threadIdx.x == 0) stamp(P, 11);
     }
     const int T = union_barrier(P, rs, RL, tag);  // ends with __syncthreads
     if (threadIdx.x == 0) {
       PR->G = T;
       stamp(P, 6);
+    }
+    if (kRouteOnly) {
+      // plan rows (CTA t: token t, t + grid, ...); CTA 0 also gathers the batch
+      // plan and exports the aggregates. The FFN tables follow from k_compact.
+      if (warp < kFfnWarps) route_phase2_plan<kFfnWarps>(P, rs, RL, T, tag, blockIdx.x == 0);
+      if (threadIdx.x == 0) grid_exit(P, claims, 0);
+      return;
     }
   } else if (threadIdx.x == 0) {
     PR->row_tok = P.row_tok;
@@ -1616,6 +1703,7 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   P.e_begin = L->e_begin;
   P.e_count = L->n_local;
   P.router_t = static_cast<const uint4*>(L->router_t);
+  P.router_frag = static_cast<const uint4*>(L->router);
   P.x_in = fb.x_in;
   P.xpad_out = fb.xpad_out;
   P.logits = fb.logits;
@@ -1642,7 +1730,8 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   const size_t smem = ffn_bf16_smem_bytes() +
                       (fb.fused ? ffn_route_smem_bytes(B, L->Np, stride) : 0) +
                       (fb.dense ? ffn_dense_xs_bytes(L->Dp) : 0);
-  auto kern = fb.dense ? k_ffn_bf16<2> : fb.fused ? k_ffn_bf16<1> : k_ffn_bf16<0>;
+  auto kern = fb.route_only ? k_ffn_bf16<3>
+                            : fb.dense ? k_ffn_bf16<2> : fb.fused ? k_ffn_bf16<1> : k_ffn_bf16<0>;
   OEA_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
   cudaLaunchConfig_t cfg = {};

@@ -204,6 +204,7 @@ struct FfnBuffers {
   // (gate GEMV), routes the batch in every CTA and exports the plan (CTA 0).
   int fused = 0;
   int dense = 0;                        // dense-over-batch FFN (fused, B <= 16)
+  int route_only = 0;                   // plan only (B > 64): k_compact + FFN follow
   const __nv_bfloat16* x_in = nullptr;  // [B][D] caller tokens
   __nv_bfloat16* xpad_out = nullptr;    // [B][Dp] when D != Dp
   float* logits = nullptr;              // [B][Np]
