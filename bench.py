@@ -54,14 +54,15 @@ def load_peak():
 
 
 def load_traffic():
-    """dram bytes per FFN launch from the committed ncu --set full summary."""
+    """(dram bytes per launch, dram / algorithmic bytes of that launch) of the
+    fused kernel from the committed ncu --set full summary."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-        return d.get("k_ffn_bf16<2>", {}).get("dram_bytes_per_launch")
+            d = json.load(f).get("k_ffn_bf16<2>", {})
+        return d.get("dram_bytes_per_launch"), d.get("dram_over_algorithmic")
     except Exception:
-        return None
+        return None, None
 
 
 class ClockSampler:
@@ -366,9 +367,11 @@ def bench_c1(args, env):
     # kernel's average launch duration.
     o, v = results["oea"], results["vanilla"]
     peak, peak_src = load_peak()
-    traffic = load_traffic()
+    traffic, traffic_ratio = load_traffic()
     roofline = {"bound": "hbm", "achieved": o["GBps"], "peak": peak, "unit": "GB/s",
-                "frac": o["GBps"] / peak, "traffic": traffic, "kernel": "k_ffn_bf16<2> (fused layer)",
+                "frac": o["GBps"] / peak, "traffic": traffic,
+                "traffic_over_algorithmic_in_capture": traffic_ratio,
+                "kernel": "k_ffn_bf16<2> (fused layer)",
                 "algorithmic_bytes_per_launch": o["active_bytes"], "kernel_us": o["us"],
                 "bytes_formula": "T*3*D*H*2 + D*N*2 + B*D*2 + B*D*4",
                 "peak_source": peak_src, "frac_of_8TBps_nominal": o["GBps"] / 8000.0,

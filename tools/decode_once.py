@@ -12,3 +12,5 @@ torch.cuda.synchronize()
 for _ in range(int(os.environ.get("ITERS", "3"))):
     L.decode(x, oea.RoutingConfig.simplified(k0, 8), out)
 L.ctx.synchronize()
+T = L.last_plan(B, oea.RoutingConfig.simplified(k0, 8))["active_count"]
+print(f"T={T} algorithmic_bytes={T * 3 * D * H * 2 + D * N * 2 + B * D * 2 + B * D * 4}")
