@@ -1203,7 +1203,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
   SR.free = plan_bar + 1;
   SR.idx = nullptr;
   int sidx = 0;  // split rounds consumed by this warp
-  // [0..1] round claims, [2] combine, [3] padded-x barrier, [4] exit, [7] launch epoch
+  // [0..1] round claims, [2]/[5] combine arrivals (epoch parity), [3] padded-x barrier,
+  // [4] exit (route-only launch), [7] launch epoch
   int* claims = P.claims;  // independent of the layer's shape (one workspace, many layers)
   // this launch's exchange tag (the epoch only changes when a launch retires)
   const uint32_t tag = static_cast<uint32_t>(__ldcg(claims + 7)) + 1u;
@@ -1501,46 +1502,79 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
   // release after a barrier of the consumer + router warps, waits until all
   // CTAs have, then combines a contiguous slice of the B x D outputs with all
   // slot loads of an output issued together.
-  constexpr int kComb = (kFfnWarps + 1) * 32;  // consumers + router warp
-  int* done = claims + 2;
-  asm volatile("bar.sync 2, %0;" ::"r"(kComb) : "memory");
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(done, 1);
-    while (ld_acquire_gpu(done) < static_cast<int>(gridDim.x)) __nanosleep(128);
-    grid_exit(P, claims, G);
-  }
-  asm volatile("bar.sync 2, %0;" ::"r"(kComb) : "memory");
-  const int ctid = warp == kRouterWarp ? kFfnWarps * 32 + lane : threadIdx.x;
+  // The router warp (idle by now) arrives for the CTA and polls; meanwhile
+  // the consumer warps fetch the plan side (set length, weights) of their
+  // first output, so only the y loads remain after the barrier.
+  constexpr int kComb = kFfnWarps * 32;  // combining threads (consumer warps)
+  asm volatile("bar.sync 2, %0;" ::"r"(kComb + 32) : "memory");  // + router warp: all y stored
   const bool kShard = kFused && P.e_count < P.N;
   const int* eslot = reinterpret_cast<const int*>(rs + RL.eslot);
   const int* ssets = reinterpret_cast<const int*>(rs + RL.sets);
   const int64_t BD = static_cast<int64_t>(P.B) * P.D;
   const int64_t f0 = BD * blockIdx.x / gridDim.x, f1 = BD * (blockIdx.x + 1) / gridDim.x;
   constexpr int kSlotBatch = 16;
-  for (int64_t f = f0 + ctid; f < f1; f += kComb) {
+  // plan side of output f: y offsets (in floats, -1 = no contribution) and weights
+  auto prep = [&](int64_t f, int& len, int (&yo)[kSlotBatch], float (&w)[kSlotBatch], int s0) {
     const int t = static_cast<int>(f / P.D), d = static_cast<int>(f % P.D);
-    const int len = PR->set_len[t];
-    float sum = 0.0f;
-    for (int s0 = 0; s0 < len; s0 += kSlotBatch) {
-      float y[kSlotBatch], w[kSlotBatch];
+    len = PR->set_len[t];
 #pragma unroll
-      for (int j = 0; j < kSlotBatch; ++j) {
-        y[j] = 0.0f;
-        w[j] = 0.0f;
-        const size_t o = static_cast<size_t>(t) * P.stride + s0 + j;
-        // expert-parallel shard: this layer's partial sum over its experts
-        if (s0 + j < len && (!kShard || eslot[ssets[o]] >= 0)) {
-          y[j] = __ldcg(P.ybuf + o * P.Dp + d);
-          w[j] = PR->wts[o];
+    for (int j = 0; j < kSlotBatch; ++j) {
+      const int o = t * P.stride + s0 + j;
+      // expert-parallel shard: this layer's partial sum over its experts
+      const bool ok = s0 + j < len && (!kShard || eslot[ssets[o]] >= 0);
+      yo[j] = ok ? o * P.Dp + d : -1;
+      w[j] = ok ? PR->wts[o] : 0.0f;
+    }
+  };
+  int len = 0, yo[kSlotBatch];
+  float w[kSlotBatch];
+  if (warp == kRouterWarp) {
+    if (lane == 0) {
+      stamp(P, 9);
+      // Arrival counter of this launch: claims[2] / claims[5] by epoch parity.
+      // The LAST CTA to arrive knows every CTA is past all other counter uses
+      // (round claims, W1 release counts, prologue barrier) and resets them
+      // here, with the other parity's arrival counter (its launch has
+      // retired) and the new epoch: no exit round trip at the end of the
+      // kernel. The arrival is acq_rel: it releases this CTA's y (cumulative
+      // over the CTA barrier) and, for the last CTA, acquires everyone else's.
+      int* done = claims + ((tag & 1u) ? 5 : 2);
+      if (atom_add_acq_rel_gpu(done, 1) == static_cast<int>(gridDim.x) - 1) {
+        for (int g = 0; g < G; ++g) P.w1_done[g] = 0;
+        claims[0] = 0;
+        claims[1] = 0;
+        claims[3] = 0;
+        claims[(tag & 1u) ? 2 : 5] = 0;
+        claims[7] = static_cast<int>(tag);  // launch epoch + 1
+      } else {
+        while (ld_acquire_gpu(done) < static_cast<int>(gridDim.x)) {
         }
       }
+      stamp(P, 10);
+    }
+  } else if (f0 + threadIdx.x < f1) {
+    prep(f0 + threadIdx.x, len, yo, w, 0);
+  }
+  asm volatile("bar.sync 2, %0;" ::"r"(kComb + 32) : "memory");
+  if (warp == kRouterWarp) return;
+  if (threadIdx.x == 0) stamp(P, 2);
+  for (int64_t f = f0 + threadIdx.x; f < f1; f += kComb) {
+    if (f != f0 + threadIdx.x) prep(f, len, yo, w, 0);
+    float sum = 0.0f;
+    for (int s0 = 0;;) {
+      float y[kSlotBatch];
+#pragma unroll
+      for (int j = 0; j < kSlotBatch; ++j) y[j] = yo[j] >= 0 ? __ldcg(P.ybuf + yo[j]) : 0.0f;
 #pragma unroll
       for (int j = 0; j < kSlotBatch; ++j)
         if (s0 + j < len) sum = fmaf(w[j], y[j], sum);
+      s0 += kSlotBatch;
+      if (s0 >= len) break;
+      prep(f, len, yo, w, s0);
     }
     P.out[f] = sum;
   }
+  if (threadIdx.x == 0) stamp(P, 15);
 }
 
 // ---------------------------------------------------------------------------

@@ -167,6 +167,11 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 __device__ __forceinline__ void red_release_gpu_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 
 // Epoch-tagged 64-bit exchange words {tag:32 | payload:32}: a reader polls
 // the word itself until its tag is the current launch's, so no separate
