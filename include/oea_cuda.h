@@ -204,7 +204,13 @@ int oea_layer_info(oea_layer_t layer, int32_t* D, int32_t* H, int32_t* N,
 int oea_moe_decode(oea_ctx_t ctx, oea_layer_t layer, const void* x_dev,
                    const uint8_t* mask_dev, int32_t B, const oea_routing_cfg* cfg,
                    void* out_dev, void* stream);
-/* Same, end to end from host buffers (H2D of x/mask and D2H of out inside). */
+/* Same, end to end from host buffers; synchronises before returning.
+ * When x and out both lie in pinned host memory (cudaHostAlloc /
+ * cudaHostRegister / torch pin_memory), mask is NULL and the call takes the
+ * fused single launch (bf16, B <= 64), the kernel reads x and writes out over
+ * the host link itself (zero copy), replayed from a per-context graph cache
+ * keyed by (layer, B, cfg). Otherwise x/mask are copied in and out copied
+ * back around the device decode. */
 int oea_moe_decode_host(oea_ctx_t ctx, oea_layer_t layer, const void* x_host,
                         const uint8_t* mask_host, int32_t B,
                         const oea_routing_cfg* cfg, void* out_host);

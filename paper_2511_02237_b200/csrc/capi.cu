@@ -167,9 +167,35 @@ int ensure(oea_ctx* ctx, Workspace& w, Need nd) {
   return OEA_OK;
 }
 
+// oea_moe_decode_host's zero-copy launches, captured once per (layer, B,
+// config, workspace) as a one-kernel graph; each call patches the kernel
+// node's x / out pointers and replays it (a graph launch costs ~2 us of host
+// time, a direct launch of the fused kernel ~5 us).
+struct HostGraph {
+  const oea_layer* L = nullptr;
+  int B = 0;
+  oea_routing_cfg rc{};
+  const void* ws_base = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphNode_t node = nullptr;  // the kernel node
+  cudaKernelNodeParams kp{};
+  std::vector<unsigned char> params;  // the node's FfnParams, patched per call
+  void* args[1] = {nullptr};
+  uint64_t used = 0;
+};
+
 struct CtxExtra {
   Workspace ws;
+  std::vector<HostGraph> host_graphs;
+  uint64_t host_graph_clock = 0;
 };
+
+void host_graph_release(HostGraph& h) {
+  if (h.exec) cudaGraphExecDestroy(h.exec);
+  if (h.graph) cudaGraphDestroy(h.graph);
+  h = HostGraph{};
+}
 
 CtxExtra* extra(oea_ctx* ctx) { return reinterpret_cast<CtxExtra*>(ctx->ws); }
 
@@ -360,8 +386,12 @@ bool fused_ok(const oea_layer* L, int B, const oea_routing_cfg& rc) {
 }
 
 // part: 0 = router + FFN (PDL-chained), 1 = router only, 2 = FFN only.
+constexpr int kNotFused = -1000;  // decode_bf16(x_mapped): not on the fused path, nothing launched
+// x_mapped: x and out are device views of mapped (pinned) host memory; only
+// the fused single launch takes them (the caller checks fused_path()).
 int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const uint8_t* mask,
-                int B, const oea_routing_cfg& rc, void* out, cudaStream_t s, int part = 0) {
+                int B, const oea_routing_cfg& rc, void* out, cudaStream_t s, int part = 0,
+                bool x_mapped = false) {
   const int stride = stride_of(rc);
   const Cfg cfg = dev_cfg(rc, stride);
   oea_host::FusedRouterBuffers rb;
@@ -413,6 +443,7 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
                    getenv("OEA_TWO_KERNEL") == nullptr &&
                    oea_host::ffn_bf16_smem_bytes() +
                            oea_host::ffn_route_smem_bytes(B, L->Np, stride) <= 227 * 1024;
+  if (x_mapped && !fused) return kNotFused;  // the caller stages x itself
   int r = OEA_OK;
   if (rb.trace) OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.trace, 0, 8 * 8 * 1024, s));
   if (big) {
@@ -455,7 +486,7 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
     if (r || part == 1) return r;
   }
   oea_host::FfnBuffers fb;
-  fb.x = padded ? static_cast<const void*>(w.xpad) : x;
+  fb.x = padded || x_mapped ? static_cast<const void*>(w.xpad) : x;
   fb.row_tok = w.row_tok;
   fb.row_slot = w.row_slot;
   fb.group_a = w.group_a;
@@ -480,7 +511,8 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
                oea_host::ffn_bf16_smem_bytes() + oea_host::ffn_route_smem_bytes(B, L->Np, stride) +
                        oea_host::ffn_dense_xs_bytes(L->Dp) <= 227 * 1024;
     fb.x_in = static_cast<const __nv_bfloat16*>(x);
-    fb.xpad_out = padded ? w.xpad : nullptr;
+    fb.xpad_out = padded || x_mapped ? w.xpad : nullptr;
+    fb.x_stage = x_mapped ? 1 : 0;
     fb.logits = w.logits;
     fb.xlog = w.xlog;
     fb.xuni = w.xuni;
@@ -634,6 +666,7 @@ int oea_ctx_destroy(oea_ctx_t ctx) {
   cudaStreamSynchronize(ctx->stream);
   CtxExtra* x = extra(ctx);
   if (x) {
+    for (auto& h : x->host_graphs) host_graph_release(h);
     if (x->ws.base) cudaFree(x->ws.base);
     delete x;
   }
@@ -941,7 +974,16 @@ int oea_layer_create(oea_ctx_t ctx, int32_t D, int32_t H, int32_t N, int32_t dty
 
 int oea_layer_destroy(oea_layer_t L) {
   if (L == nullptr) return OEA_OK;
-  if (L->ctx) cudaStreamSynchronize(L->ctx->stream);
+  if (L->ctx) {
+    cudaStreamSynchronize(L->ctx->stream);
+    if (CtxExtra* x = extra(L->ctx)) {
+      auto& v = x->host_graphs;
+      for (auto& h : v)
+        if (h.L == L) host_graph_release(h);
+      v.erase(std::remove_if(v.begin(), v.end(), [](const HostGraph& h) { return h.L == nullptr; }),
+              v.end());
+    }
+  }
   cudaFree(L->router);
   cudaFree(L->router_t);
   cudaFree(L->w1);
@@ -1040,6 +1082,97 @@ int oea_moe_decode(oea_ctx_t ctx, oea_layer_t L, const void* x_dev, const uint8_
                      static_cast<double*>(out_dev), s);
 }
 
+// The zero-copy fused decode through the context's graph cache (see
+// HostGraph). kNotFused when the shape/config is not on the fused path.
+int decode_host_graph(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* xd, int B,
+                      const oea_routing_cfg& rc, void* od) {
+  CtxExtra* ex = extra(ctx);
+  cudaStream_t s = ctx->stream;
+  if (ctx->ffn_trace) return decode_bf16(ctx, w, L, xd, nullptr, B, rc, od, s, 0, true);
+  HostGraph* h = nullptr;
+  for (auto& c : ex->host_graphs)
+    if (c.L == L && c.B == B && c.ws_base == w.base &&
+        std::memcmp(&c.rc, &rc, sizeof rc) == 0) {
+      h = &c;
+      break;
+    }
+  if (h == nullptr) {
+    constexpr size_t kMaxHostGraphs = 16;
+    if (ex->host_graphs.size() >= kMaxHostGraphs) {  // evict the least recently used
+      auto lru = std::min_element(ex->host_graphs.begin(), ex->host_graphs.end(),
+                                  [](const HostGraph& a, const HostGraph& b) { return a.used < b.used; });
+      host_graph_release(*lru);
+      ex->host_graphs.erase(lru);
+    }
+    HostGraph n;
+    n.L = L;
+    n.B = B;
+    n.rc = rc;
+    n.ws_base = w.base;
+    const int64_t launches = ctx->launches;
+    OEA_CUDA_TRY(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    const int r = decode_bf16(ctx, w, L, xd, nullptr, B, rc, od, s, 0, true);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(s, &graph);
+    ctx->launches = launches;  // a capture launches nothing
+    if (r != OEA_OK || e != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      return r != OEA_OK ? r : oea_check_cuda(ctx, e, "cudaStreamEndCapture");
+    }
+    n.graph = graph;
+    size_t nn = 0;
+    cudaGraphGetNodes(graph, nullptr, &nn);
+    std::vector<cudaGraphNode_t> nodes(nn);
+    if (nn) cudaGraphGetNodes(graph, nodes.data(), &nn);
+    cudaGraphNodeType t;
+    if (nn != 1 || cudaGraphNodeGetType(nodes[0], &t) != cudaSuccess ||
+        t != cudaGraphNodeTypeKernel ||
+        cudaGraphKernelNodeGetParams(nodes[0], &n.kp) != cudaSuccess) {
+      host_graph_release(n);
+      return fail(ctx, OEA_ERR_CUDA, "moe_decode_host: unexpected decode graph");
+    }
+    n.node = nodes[0];
+    n.params.assign(static_cast<unsigned char*>(n.kp.kernelParams[0]),
+                    static_cast<unsigned char*>(n.kp.kernelParams[0]) + oea_host::ffn_params_bytes());
+    const cudaError_t ie = cudaGraphInstantiate(&n.exec, graph, 0);
+    if (ie != cudaSuccess) {
+      host_graph_release(n);
+      return oea_check_cuda(ctx, ie, "cudaGraphInstantiate");
+    }
+    ex->host_graphs.push_back(std::move(n));
+    h = &ex->host_graphs.back();
+  }
+  h->used = ++ex->host_graph_clock;
+  oea_host::ffn_params_set_io(h->params.data(), xd, od);
+  h->args[0] = h->params.data();
+  h->kp.kernelParams = h->args;
+  h->kp.extra = nullptr;
+  OEA_CUDA_TRY(ctx, cudaGraphExecKernelNodeSetParams(h->exec, h->node, &h->kp));
+  OEA_CUDA_TRY(ctx, cudaGraphLaunch(h->exec, s));
+  OEA_LAUNCHED(ctx);
+  return OEA_OK;
+}
+
+// Device view of a host buffer when all of [p, p + bytes) lies in pinned,
+// mapped host memory (cudaHostAlloc / cudaHostRegister, e.g. torch's
+// pin_memory); nullptr for pageable memory.
+const void* mapped_view(const void* p, size_t bytes) {
+  cudaPointerAttributes a{}, b{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess || a.type != cudaMemoryTypeHost ||
+      a.devicePointer == nullptr) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  const char* last = static_cast<const char*>(p) + bytes - 1;
+  if (cudaPointerGetAttributes(&b, last) != cudaSuccess || b.type != cudaMemoryTypeHost ||
+      static_cast<const char*>(b.devicePointer) !=
+          static_cast<const char*>(a.devicePointer) + (bytes - 1)) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return a.devicePointer;
+}
+
 int oea_moe_decode_host(oea_ctx_t ctx, oea_layer_t L, const void* x_host,
                         const uint8_t* mask_host, int32_t B, const oea_routing_cfg* cfg,
                         void* out_host) {
@@ -1056,6 +1189,25 @@ int oea_moe_decode_host(oea_ctx_t ctx, oea_layer_t L, const void* x_host,
   const bool bf = L->dtype == OEA_DTYPE_BF16;
   const size_t xbytes = static_cast<size_t>(B) * L->D * (bf ? 2 : 8);
   const size_t obytes = static_cast<size_t>(B) * L->D * (bf ? 4 : 8);
+  ctx->last_B = B;
+  ctx->last_N = L->N;
+  ctx->last_stride = stride_of(rc);
+  if (bf && mask_host == nullptr) {
+    // Zero copy: x and out in pinned (mapped) host memory go straight to the
+    // fused kernel, which stages x into HBM itself and writes out over the
+    // host link; no DMA copies, one launch. Other buffers take the copies.
+    const void* xd = mapped_view(x_host, xbytes);
+    void* od = const_cast<void*>(mapped_view(out_host, obytes));
+    if (xd != nullptr && od != nullptr) {
+      ctx->last_kind = 1;
+      r = decode_host_graph(ctx, w, L, xd, B, rc, od);
+      if (r == OEA_OK) {
+        OEA_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+        return OEA_OK;
+      }
+      if (r != kNotFused) return r;
+    }
+  }
   OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.xin, x_host, xbytes, cudaMemcpyHostToDevice, s));
   if (mask_host) OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.mask, mask_host, B, cudaMemcpyHostToDevice, s));
   ctx->last_B = B;

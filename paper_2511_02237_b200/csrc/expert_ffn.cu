@@ -82,6 +82,7 @@ struct FfnParams {
   const uint4* router_frag;     // [Np/16][Dp/16] fragment-ordered router tiles
   const __nv_bfloat16* x_in;    // [B][D] caller tokens
   __nv_bfloat16* xpad_out;      // [B][Dp], written in-kernel when D != Dp, else null
+  int x_stage;                  // x_in is mapped host memory: staged into xpad_out first
   float* logits;        // [B][Np]
   const uint8_t* mask;
   int N, Np;
@@ -494,7 +495,32 @@ __device__ __forceinline__ void fused_gemv(const FfnParams& P, float* red, int* 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NT = kFfnThreads;
   const int nch = P.Dp >> 3;
-  if (P.xpad_out != nullptr) {
+  // token rows the GEMV reads: the caller's x, or (x in mapped host memory,
+  // oea_moe_decode_host) the device copy staged below
+  const __nv_bfloat16* xsrc = P.x_stage ? P.xpad_out : P.x_in;
+  const int xrow = P.x_stage ? P.Dp : P.D;
+  if (P.x_stage) {
+    // zero-copy input: CTA c copies a 1/grid slice of x (16-byte chunks, one
+    // host round trip, zero-padded to Dp), then a grid barrier. Reading x
+    // from every CTA instead would cross the host link grid-size times.
+    const int n = P.B * nch;
+    const int c0 = static_cast<int>(static_cast<int64_t>(n) * blockIdx.x / gridDim.x);
+    const int c1 = static_cast<int>(static_cast<int64_t>(n) * (blockIdx.x + 1) / gridDim.x);
+    for (int i = c0 + tid; i < c1; i += NT) {
+      const int t = i / nch, c = i % nch;
+      const uint4 v = c * 8 < P.D
+                          ? *reinterpret_cast<const uint4*>(P.x_in + static_cast<size_t>(t) * P.D + c * 8)
+                          : make_uint4(0u, 0u, 0u, 0u);
+      *reinterpret_cast<uint4*>(P.xpad_out + static_cast<size_t>(t) * P.Dp + c * 8) = v;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      red_release_gpu_add(sync_cnt, 1);
+      while (ld_acquire_gpu(sync_cnt) < static_cast<int>(gridDim.x)) {
+      }
+    }
+    __syncthreads();
+  } else if (P.xpad_out != nullptr) {
 #pragma unroll 1
     for (int t = blockIdx.x; t < P.B; t += gridDim.x)
 #pragma unroll 1
@@ -520,7 +546,7 @@ __device__ __forceinline__ void fused_gemv(const FfnParams& P, float* red, int* 
         for (int t = 0; t < 16; ++t)
           xv[t] = (tc + t < P.B && c * 8 < P.D)
                       ? __ldcg(reinterpret_cast<const uint4*>(
-                            P.x_in + static_cast<size_t>(tc + t) * P.D + c * 8))
+                            xsrc + static_cast<size_t>(tc + t) * xrow + c * 8))
                       : make_uint4(0u, 0u, 0u, 0u);
         float rf[8];
         bf16x8_to_f32(rv, rf);
@@ -562,7 +588,7 @@ __device__ __forceinline__ void fused_gemv(const FfnParams& P, float* red, int* 
   }
   // grid barrier only for the zero-padded x copy (D != Dp): its readers are
   // every CTA (x tile, W1); the logits travel as tagged words
-  if (P.xpad_out == nullptr) return;
+  if (P.xpad_out == nullptr || P.x_stage) return;
   __syncthreads();
   if (tid == 0) {
     stamp(P, 9);
@@ -1734,6 +1760,7 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   // split rounds measured slower than 8-unit rounds at small T (per-round
   // reduction overhead, tools/trace_ffn.py): opt-in for experiments
   P.split_ok = getenv("OEA_SPLIT") != nullptr;
+  P.x_stage = fb.x_stage;
   P.e_begin = L->e_begin;
   P.e_count = L->n_local;
   P.router_t = static_cast<const uint4*>(L->router_t);
@@ -1764,10 +1791,14 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   const size_t smem = ffn_bf16_smem_bytes() +
                       (fb.fused ? ffn_route_smem_bytes(B, L->Np, stride) : 0) +
                       (fb.dense ? ffn_dense_xs_bytes(L->Dp) : 0);
-  auto kern = fb.route_only ? k_ffn_bf16<3>
-                            : fb.dense ? k_ffn_bf16<2> : fb.fused ? k_ffn_bf16<1> : k_ffn_bf16<0>;
-  OEA_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
+  const int mode = fb.route_only ? 3 : fb.dense ? 2 : fb.fused ? 1 : 0;
+  auto kern = mode == 3 ? k_ffn_bf16<3>
+                        : mode == 2 ? k_ffn_bf16<2> : mode == 1 ? k_ffn_bf16<1> : k_ffn_bf16<0>;
+  if (static_cast<int>(smem) > ctx->ffn_smem_set[mode]) {  // once per size, not per launch
+    OEA_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem)));
+    ctx->ffn_smem_set[mode] = static_cast<int>(smem);
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ctx->num_sms);
   cfg.blockDim = dim3(kFfnThreads);
@@ -1783,6 +1814,15 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   OEA_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, P));
   OEA_LAUNCHED(ctx);
   return OEA_OK;
+}
+
+// Host-path graph replays (capi.cu decode_host_graph) patch a captured fused
+// launch's parameter block: the caller's x (mapped host rows) and out.
+size_t ffn_params_bytes() { return sizeof(FfnParams); }
+void ffn_params_set_io(void* params, const void* x_in, void* out) {
+  auto* P = static_cast<FfnParams*>(params);
+  P->x_in = static_cast<const __nv_bfloat16*>(x_in);
+  P->out = static_cast<float*>(out);
 }
 
 template <typename T>

@@ -79,6 +79,8 @@ struct oea_ctx {
   // Debug instrumentation of the FFN (env OEA_FFN_TRACE=1 / OEA_FFN_MODE=n).
   unsigned long long* ffn_trace = nullptr;
   int ffn_mode = 0;
+  // dynamic shared memory already allowed per k_ffn_bf16<MODE> on this device
+  int ffn_smem_set[4] = {0, 0, 0, 0};
 };
 
 struct oea_layer {
@@ -206,7 +208,8 @@ struct FfnBuffers {
   int dense = 0;                        // dense-over-batch FFN (fused, B <= 16)
   int route_only = 0;                   // plan only (B > 64): k_compact + FFN follow
   const __nv_bfloat16* x_in = nullptr;  // [B][D] caller tokens
-  __nv_bfloat16* xpad_out = nullptr;    // [B][Dp] when D != Dp
+  __nv_bfloat16* xpad_out = nullptr;    // [B][Dp] when D != Dp (or x_stage)
+  int x_stage = 0;                      // x_in is mapped host memory (staged in-kernel)
   float* logits = nullptr;              // [B][Np]
   unsigned long long* xlog = nullptr;   // tagged exchange words (fused path)
   unsigned long long* xuni = nullptr;
@@ -228,6 +231,8 @@ struct FfnBuffers {
 };
 size_t ffn_route_smem_bytes(int B, int Np, int stride);
 size_t ffn_bf16_smem_bytes();
+size_t ffn_params_bytes();
+void ffn_params_set_io(void* params, const void* x_in, void* out);
 size_t ffn_dense_xs_bytes(int Dp);
 int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride,
                     const FfnBuffers& fb, bool pdl, cudaStream_t s);
