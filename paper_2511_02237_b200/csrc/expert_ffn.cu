@@ -1774,11 +1774,12 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   P.split_ok = getenv("OEA_SPLIT") != nullptr;
   P.x_stage = fb.x_stage;
   {
-    // ~16 MiB in total: what HBM can deliver in the prologue's idle ~2.5 us
-    // (measured C1: 128 KiB per expert saves ~1.3 us; 320 KiB saves nothing)
+    // ~32 MiB in total, about what HBM delivers while the prologue routes
+    // (measured C1, N=128: 128 KiB per expert saves ~1.3 us, 224-288 KiB
+    // ~2.2 us, 320 KiB less again; issuing it before the gate GEMV is slower)
     static const int pf = getenv("OEA_PREFETCH_KB") ? atoi(getenv("OEA_PREFETCH_KB")) : -1;
     P.prefetch_bytes = pf >= 0 ? pf * 1024
-                               : ((16 << 20) / max(L->n_local, 1)) & ~(32 * 1024 - 1);
+                               : ((32 << 20) / max(L->n_local, 1)) & ~(32 * 1024 - 1);
   }
   P.e_begin = L->e_begin;
   P.e_count = L->n_local;
