@@ -137,6 +137,19 @@ int oea_route_f64_host(oea_ctx_t ctx, const double* scores, const uint8_t* mask,
 int oea_route_f64(oea_ctx_t ctx, const double* scores_dev, const uint8_t* mask_dev,
                   int32_t B, int32_t N, const oea_routing_cfg* cfg,
                   const oea_plan_view* plan_dev, void* stream);
+/* Batched route(): R independent records (e.g. the (step, layer) batches of a
+ * score trace, io.cpp:85-172) of rows[r] x N scores each, concatenated row-wise
+ * (mask: sum(rows) bytes or NULL). Each record is routed exactly as
+ * oea_route_f64_host would route it alone (its own union and aggregates);
+ * replaces the per-record loop of the reference's `route` command
+ * (oea_cli.cpp:153-175). Plan layout: sets/weights/set_len/phase1_* per row
+ * as in oea_plan_view over sum(rows) rows; loads/active_union/base_union are
+ * [R][N], active_count/total_load/base_union_count are [R]; order must be
+ * NULL. One launch sequence for p == 1, max_p >= N, N <= 128 (the fast path);
+ * other configurations route record by record. */
+int oea_route_f64_batched_host(oea_ctx_t ctx, const double* scores, const uint8_t* mask,
+                               const int32_t* rows, int32_t R, int32_t N,
+                               const oea_routing_cfg* cfg, const oea_plan_view* plan);
 /* sort_experts (routing.cpp:184-203): order[B*N]; sorts masked rows too. */
 int oea_sort_experts_f64_host(oea_ctx_t ctx, const double* scores, int32_t B,
                               int32_t N, int32_t* order);

@@ -187,6 +187,9 @@ struct HostGraph {
 
 struct CtxExtra {
   Workspace ws;
+  // batched routing (oea_route_f64_batched_host): per-record aggregates
+  void* seg_buf = nullptr;
+  size_t seg_bytes = 0;
   std::vector<HostGraph> host_graphs;
   uint64_t host_graph_clock = 0;
 };
@@ -668,6 +671,7 @@ int oea_ctx_destroy(oea_ctx_t ctx) {
   if (x) {
     for (auto& h : x->host_graphs) host_graph_release(h);
     if (x->ws.base) cudaFree(x->ws.base);
+    if (x->seg_buf) cudaFree(x->seg_buf);
     delete x;
   }
   if (ctx->ffn_trace) cudaFree(ctx->ffn_trace);
@@ -786,6 +790,145 @@ int oea_route_f64_host(oea_ctx_t ctx, const double* scores, const uint8_t* mask,
   ctx->last_stride = stride;
   ctx->last_kind = 2;
   return export_plan(ctx, w, plan, B, N, stride, N);
+}
+
+// Many independent records (a score trace's (step, layer) batches) in one
+// launch sequence: the fast-path kernels with a row -> record map, so each
+// record has its own union and aggregates (io.cpp:85-172 + route() per record
+// in the reference's `route` command, oea_cli.cpp:153-175). Configurations
+// outside the fast path route record by record.
+int oea_route_f64_batched_host(oea_ctx_t ctx, const double* scores, const uint8_t* mask,
+                               const int32_t* rows, int32_t R, int32_t N,
+                               const oea_routing_cfg* cfg, const oea_plan_view* plan) {
+  CHECK_CTX(ctx);
+  if (R < 1 || rows == nullptr)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "route_batched: need R >= 1 records");
+  int64_t total = 0;
+  for (int r = 0; r < R; ++r) {
+    if (rows[r] < 1) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "sort_experts: dimensions must be >= 1");
+    total += rows[r];
+  }
+  if (total > INT_MAX / 2) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "route_batched: too many rows");
+  const int B = static_cast<int>(total);
+  oea_routing_cfg rc;
+  int r = resolve(ctx, cfg, N, &rc);
+  if (r) return r;
+  if (plan == nullptr || plan->sets == nullptr || plan->set_len == nullptr)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "route: plan sets/set_len are required");
+  if (plan->order != nullptr)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "route_batched: order is not exported");
+  const int stride = stride_of(rc);
+  if (plan->set_stride < stride)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "route: plan set_stride too small");
+  const Cfg dc = dev_cfg(rc, stride);
+  if (!oea_host::route_fast_ok(dc, N, false) || getenv("OEA_ROUTE_SORT") != nullptr) {
+    // record by record through the general path
+    int64_t row0 = 0;
+    for (int q = 0; q < R; ++q) {
+      const size_t ps = plan->set_stride;
+      oea_plan_view v = *plan;
+      v.sets = plan->sets + row0 * ps;
+      v.set_len = plan->set_len + row0;
+      if (v.weights) v.weights += row0 * ps;
+      if (v.weights_f32) v.weights_f32 += row0 * ps;
+      if (v.loads) v.loads += static_cast<size_t>(q) * N;
+      if (v.active_union) v.active_union += static_cast<size_t>(q) * N;
+      if (v.active_count) v.active_count += q;
+      if (v.total_load) v.total_load += q;
+      if (v.phase1_t) v.phase1_t += row0;
+      if (v.phase1_n) v.phase1_n += row0;
+      if (v.base_union) v.base_union += static_cast<size_t>(q) * N;
+      if (v.base_union_count) v.base_union_count += q;
+      r = oea_route_f64_host(ctx, scores + row0 * N, mask ? mask + row0 : nullptr, rows[q], N, cfg, &v);
+      if (r) {
+        if (r == OEA_ERR_DOMAIN)  // name the record, like read_score_trace's errors
+          return fail(ctx, r, "record " + std::to_string(q) + ": " + ctx->last_error);
+        return r;
+      }
+      row0 += rows[q];
+    }
+    return OEA_OK;
+  }
+  Workspace& w = extra(ctx)->ws;
+  r = ensure(ctx, w, Need{B, N, 1, 1, stride});
+  if (r) return r;
+  // per-record buffers: seg [B] | union [R][4] | loads, active, base [R][N] | counts [R] x2 | total [R]
+  CtxExtra* ex = extra(ctx);
+  const size_t need = static_cast<size_t>(B) * 4 + static_cast<size_t>(R) * (16 + 12 * N + 8 + 8) + 256;
+  cudaStream_t s = ctx->stream;
+  if (need > ex->seg_bytes) {
+    OEA_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    if (ex->seg_buf) cudaFree(ex->seg_buf);
+    ex->seg_buf = nullptr;
+    ex->seg_bytes = 0;
+    OEA_CUDA_TRY(ctx, cudaMalloc(&ex->seg_buf, need));
+    ex->seg_bytes = need;
+  }
+  char* p = static_cast<char*>(ex->seg_buf);
+  auto take = [&](size_t bytes) {
+    char* q = p;
+    p += (bytes + 15) & ~size_t(15);
+    return q;
+  };
+  int64_t* d_total = reinterpret_cast<int64_t*>(take(8 * static_cast<size_t>(R)));
+  int32_t* d_seg = reinterpret_cast<int32_t*>(take(4 * static_cast<size_t>(B)));
+  uint32_t* d_union = reinterpret_cast<uint32_t*>(take(16 * static_cast<size_t>(R)));
+  int32_t* d_loads = reinterpret_cast<int32_t*>(take(4 * static_cast<size_t>(R) * N));
+  int32_t* d_active = reinterpret_cast<int32_t*>(take(4 * static_cast<size_t>(R) * N));
+  int32_t* d_base = reinterpret_cast<int32_t*>(take(4 * static_cast<size_t>(R) * N));
+  int32_t* d_cnt = reinterpret_cast<int32_t*>(take(4 * static_cast<size_t>(R)));
+  int32_t* d_bcnt = reinterpret_cast<int32_t*>(take(4 * static_cast<size_t>(R)));
+  std::vector<int32_t> seg(B);
+  for (int q = 0, i = 0; q < R; ++q)
+    for (int j = 0; j < rows[q]; ++j) seg[i++] = q;
+  OEA_CUDA_TRY(ctx, cudaMemcpyAsync(d_seg, seg.data(), 4 * static_cast<size_t>(B), cudaMemcpyHostToDevice, s));
+  OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.scores, scores, sizeof(double) * B * N, cudaMemcpyHostToDevice, s));
+  if (mask) OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.mask, mask, B, cudaMemcpyHostToDevice, s));
+  oea_host::RouteBuffers rb = route_buffers(w, w.scores, mask ? w.mask : nullptr);
+  rb.union_bits = d_union;
+  rb.loads = d_loads;
+  rb.active_union = d_active;
+  rb.active_count = d_cnt;
+  rb.total_load = d_total;
+  rb.base_union = d_base;
+  rb.base_union_count = d_bcnt;
+  const int set_mode = rc.mode == OEA_MODE_VANILLA ? 0 : rc.mode == OEA_MODE_PRUNED ? 1 : 2;
+  r = oea_host::route_f64_fast_launch(ctx, dc, B, N, rb, set_mode, s, R, d_seg);
+  if (r) return r;
+  int32_t tok = INT_MAX;
+  OEA_CUDA_TRY(ctx, cudaMemcpyAsync(&tok, w.err_token, 4, cudaMemcpyDeviceToHost, s));
+  OEA_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  if (tok >= 0 && tok < B) {
+    int q = seg[tok], row0 = 0;
+    for (int j = 0; j < q; ++j) row0 += rows[j];
+    return fail(ctx, OEA_ERR_DOMAIN, "record " + std::to_string(q) +
+                                         ": route: degenerate selected-set mass for token " +
+                                         std::to_string(tok - row0) + " (sum <= 1e-12)");
+  }
+  const int ps = plan->set_stride, cols = std::min(ps, stride);
+  if (plan->sets) r = d2h_rows(ctx, plan->sets, ps, w.sets, stride, B, cols);
+  if (!r && plan->weights) r = d2h_rows(ctx, plan->weights, ps, w.w64, stride, B, cols);
+  if (!r && plan->weights_f32) r = d2h_rows(ctx, plan->weights_f32, ps, w.w32, stride, B, cols);
+  if (!r) r = d2h(ctx, plan->set_len, w.set_len, B);
+  if (!r) r = d2h(ctx, plan->loads, d_loads, static_cast<size_t>(R) * N);
+  if (!r) r = d2h(ctx, plan->active_union, d_active, static_cast<size_t>(R) * N);
+  if (!r) r = d2h(ctx, plan->active_count, d_cnt, R);
+  if (!r) r = d2h(ctx, plan->total_load, d_total, R);
+  if (!r) r = d2h(ctx, plan->phase1_t, w.t, B);
+  if (!r) r = d2h(ctx, plan->phase1_n, w.n, B);
+  if (!r) r = d2h(ctx, plan->base_union, d_base, static_cast<size_t>(R) * N);
+  if (!r) r = d2h(ctx, plan->base_union_count, d_bcnt, R);
+  if (r) return r;
+  OEA_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  if (ps > stride) {  // pad the caller's wider rows
+    for (int i = 0; i < B; ++i)
+      for (int j = stride; j < ps; ++j) {
+        plan->sets[static_cast<size_t>(i) * ps + j] = -1;
+        if (plan->weights) plan->weights[static_cast<size_t>(i) * ps + j] = 0.0;
+        if (plan->weights_f32) plan->weights_f32[static_cast<size_t>(i) * ps + j] = 0.0f;
+      }
+  }
+  return OEA_OK;
 }
 
 int oea_sort_experts_f64_host(oea_ctx_t ctx, const double* scores, int32_t B, int32_t N,

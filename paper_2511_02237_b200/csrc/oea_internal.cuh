@@ -156,7 +156,8 @@ int route_f64_launch(oea_ctx* ctx, const oea_dev::Cfg& cfg, int B, int N,
 // requested): top-m picks instead of a full sort; same results bit for bit.
 bool route_fast_ok(const oea_dev::Cfg& cfg, int N, bool need_order);
 int route_f64_fast_launch(oea_ctx* ctx, const oea_dev::Cfg& cfg, int B, int N,
-                          const RouteBuffers& rb, int set_mode, cudaStream_t s);
+                          const RouteBuffers& rb, int set_mode, cudaStream_t s, int R = 1,
+                          const int32_t* seg = nullptr);
 int union_from_list_launch(oea_ctx* ctx, const int32_t* list, int count, int N, uint32_t* bits,
                            cudaStream_t s);
 

@@ -205,6 +205,18 @@ __global__ void __launch_bounds__(1024)
                 int32_t* __restrict__ active_count, const uint32_t* __restrict__ union_bits,
                 int32_t* __restrict__ base_union, int32_t* __restrict__ base_count,
                 int64_t* __restrict__ total_load) {
+  // batched routing (route_f64_batched): CTA b aggregates record b, whose
+  // per-record buffers sit at stride N (bitmaps: 4 words, N <= 128)
+  if (blockIdx.x > 0) {
+    const int b = blockIdx.x;
+    loads += static_cast<size_t>(b) * N;
+    active_union += static_cast<size_t>(b) * N;
+    active_count += b;
+    union_bits += 4 * b;
+    if (base_union) base_union += static_cast<size_t>(b) * N;
+    if (base_count) base_count += b;
+    if (total_load) total_load += b;
+  }
   if (total_load) {  // fast path: total_load = sum of the loads (fill_aggregates)
     __shared__ long long s_part[32];
     long long mine = 0;
@@ -348,7 +360,7 @@ __global__ void __launch_bounds__(kRouteWarps * 32)
               int32_t* __restrict__ t_out, int32_t* __restrict__ n_out,
               uint32_t* __restrict__ union_bits, double* __restrict__ weights,
               float* __restrict__ weights_f32, int32_t* __restrict__ loads,
-              int32_t* __restrict__ err_token) {
+              int32_t* __restrict__ err_token, const int32_t* __restrict__ seg) {
   __shared__ int s_loads[128];
   for (int e = threadIdx.x; e < 128; e += blockDim.x) s_loads[e] = 0;
   __syncthreads();
@@ -358,6 +370,10 @@ __global__ void __launch_bounds__(kRouteWarps * 32)
     const double* row = scores + static_cast<size_t>(i) * N;
     int32_t* srow = sets + static_cast<size_t>(i) * cfg.stride;
     const bool real = mask == nullptr || mask[i] != 0;
+    // batched records: the token's record owns its union bitmap and loads
+    const int sg = seg ? seg[i] : 0;
+    uint32_t* ub = union_bits + 4 * sg;
+    int* cnt = seg ? loads + static_cast<size_t>(sg) * N : s_loads;
     uint64_t k[E];
     int id[E];
 #pragma unroll
@@ -372,17 +388,17 @@ __global__ void __launch_bounds__(kRouteWarps * 32)
     __syncwarp();
     if (set_mode != 0 && lane < n) {
       const int e = srow[lane];
-      atomicOr(&union_bits[e >> 5], 1u << (e & 31));
+      atomicOr(&ub[e >> 5], 1u << (e & 31));
     }
     if (lane == 0) {
       if (t_out) t_out[i] = set_mode == 0 ? 0 : (real ? N : 0);
       if (n_out) n_out[i] = set_mode == 0 ? 0 : n;
     }
     if (set_mode != 2)
-      fast_finish(cfg, i, n, row, srow, weights, weights_f32, set_len, s_loads, err_token,
+      fast_finish(cfg, i, n, row, srow, weights, weights_f32, set_len, cnt, err_token,
                   do_weights);
   }
-  if (set_mode != 2) flush_loads(N, s_loads, loads);
+  if (set_mode != 2 && seg == nullptr) flush_loads(N, s_loads, loads);
 }
 
 template <int E>
@@ -392,7 +408,8 @@ __global__ void __launch_bounds__(kRouteWarps * 32)
               const int32_t* __restrict__ n_in, const uint32_t* __restrict__ union_bits,
               int32_t* __restrict__ sets, int32_t* __restrict__ set_len,
               double* __restrict__ weights, float* __restrict__ weights_f32,
-              int32_t* __restrict__ loads, int32_t* __restrict__ err_token) {
+              int32_t* __restrict__ loads, int32_t* __restrict__ err_token,
+              const int32_t* __restrict__ seg) {
   __shared__ int s_loads[128];
   for (int e = threadIdx.x; e < 128; e += blockDim.x) s_loads[e] = 0;
   __syncthreads();
@@ -402,6 +419,9 @@ __global__ void __launch_bounds__(kRouteWarps * 32)
     const double* row = scores + static_cast<size_t>(i) * N;
     int32_t* srow = sets + static_cast<size_t>(i) * cfg.stride;
     const bool real = mask == nullptr || mask[i] != 0;
+    const int sg = seg ? seg[i] : 0;
+    const uint32_t* ub = union_bits + 4 * sg;
+    int* cnt = seg ? loads + static_cast<size_t>(sg) * N : s_loads;
     const int n = real ? n_in[i] : 0;
     int len = n;
     if (real && n < cfg.limit) {
@@ -423,17 +443,17 @@ __global__ void __launch_bounds__(kRouteWarps * 32)
 #pragma unroll
       for (int j = 0; j < E; ++j) {
         const int p = j * 32 + lane;
-        const bool cand = p < N && ((union_bits[j] >> lane) & 1u) && !((bw[j] >> lane) & 1u);
+        const bool cand = p < N && ((ub[j] >> lane) & 1u) && !((bw[j] >> lane) & 1u);
         k[j] = cand ? order_key_f64(__ldcg(row + p)) : 0ull;
         id[j] = p;
       }
       lane_sort_desc<E>(k, id);
       len += pick_top<E>(k, id, cfg.limit - n, srow, n);
     }
-    fast_finish(cfg, i, real ? len : 0, row, srow, weights, weights_f32, set_len, s_loads,
+    fast_finish(cfg, i, real ? len : 0, row, srow, weights, weights_f32, set_len, cnt,
                 err_token, do_weights);
   }
-  flush_loads(N, s_loads, loads);
+  if (seg == nullptr) flush_loads(N, s_loads, loads);
 }
 
 }  // namespace oea_dev
@@ -493,17 +513,17 @@ int route_f64_launch(oea_ctx* ctx, const Cfg& cfg, int B, int N, const RouteBuff
 
 template <int E>
 static void launch_fast(const Cfg& cfg, int B, int N, const RouteBuffers& rb, int set_mode,
-                        int do_weights, cudaStream_t s) {
+                        int do_weights, const int32_t* seg, cudaStream_t s) {
   const int grid = (B + kRouteWarps - 1) / kRouteWarps;
   k_fast_p1<E><<<grid, kRouteWarps * 32, 0, s>>>(cfg, B, N, set_mode, do_weights, rb.scores,
                                                  rb.mask, rb.sets, rb.set_len, rb.t, rb.n,
                                                  rb.union_bits, rb.weights, rb.weights_f32,
-                                                 rb.loads, rb.err_token);
+                                                 rb.loads, rb.err_token, seg);
   if (set_mode == 2)
     k_fast_p2<E><<<grid, kRouteWarps * 32, 0, s>>>(cfg, B, N, do_weights, rb.scores, rb.mask,
                                                    rb.n, rb.union_bits, rb.sets, rb.set_len,
                                                    rb.weights, rb.weights_f32, rb.loads,
-                                                   rb.err_token);
+                                                   rb.err_token, seg);
 }
 
 bool route_fast_ok(const Cfg& cfg, int N, bool need_order) {
@@ -512,23 +532,28 @@ bool route_fast_ok(const Cfg& cfg, int N, bool need_order) {
          cfg.limit <= 32;
 }
 
+// R > 1: batched independent records (route_f64_batched); seg[i] = record of
+// row i, and union_bits / loads / active_union / active_count / total_load /
+// base_union / base_union_count are per record ([R][4] words, [R][N], [R]).
 int route_f64_fast_launch(oea_ctx* ctx, const Cfg& cfg, int B, int N, const RouteBuffers& rb,
-                          int set_mode, cudaStream_t s) {
-  const int words = (N + 31) / 32;
+                          int set_mode, cudaStream_t s, int R, const int32_t* seg) {
+  const int words = R > 1 ? 4 * R : (N + 31) / 32;
   OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.union_bits, 0, words * 4, s));
-  OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.loads, 0, sizeof(int32_t) * N, s));
+  OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.loads, 0, sizeof(int32_t) * N * R, s));
   OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.err_token, 0x7f, sizeof(int32_t), s));
   const int do_weights = (rb.weights != nullptr || rb.weights_f32 != nullptr) ? 1 : 0;
+  const int32_t* sg = R > 1 ? seg : nullptr;
   if (N <= 32)
-    launch_fast<1>(cfg, B, N, rb, set_mode, do_weights, s);
+    launch_fast<1>(cfg, B, N, rb, set_mode, do_weights, sg, s);
   else if (N <= 64)
-    launch_fast<2>(cfg, B, N, rb, set_mode, do_weights, s);
+    launch_fast<2>(cfg, B, N, rb, set_mode, do_weights, sg, s);
   else
-    launch_fast<4>(cfg, B, N, rb, set_mode, do_weights, s);
+    launch_fast<4>(cfg, B, N, rb, set_mode, do_weights, sg, s);
   OEA_LAUNCHED(ctx);
   if (set_mode == 2) OEA_LAUNCHED(ctx);
-  k_aggregate<<<1, 1024, 0, s>>>(N, rb.loads, rb.active_union, rb.active_count, rb.union_bits,
-                                 rb.base_union, rb.base_union_count, rb.total_load);
+  k_aggregate<<<R, N <= 128 ? 128 : 1024, 0, s>>>(N, rb.loads, rb.active_union, rb.active_count,
+                                                  rb.union_bits, rb.base_union,
+                                                  rb.base_union_count, rb.total_load);
   OEA_LAUNCHED(ctx);
   return OEA_OK;
 }

@@ -13,6 +13,7 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass, field
 from enum import IntEnum
+from typing import List
 
 import numpy as np
 
@@ -22,7 +23,7 @@ __all__ = [
     "RoutingMode", "CapSemantics", "RoutingConfig", "ScoreMatrix", "SortedExperts",
     "Phase1Result", "RoutingPlan", "BatchStats", "to_string", "routing_mode_from_string",
     "cap_semantics_from_string", "sort_experts", "route_topk", "phase1_baseline",
-    "phase2_piggyback", "route", "batch_stats", "plan_set_stride",
+    "phase2_piggyback", "route", "route_batched", "batch_stats", "plan_set_stride",
 ]
 
 
@@ -253,6 +254,49 @@ def _route_call(sm: ScoreMatrix, cfg: RoutingConfig, want_order=False):
     ctx.check(lib().oea_route_f64_host(ctx.h, _p(sm.scores), _p(sm._mask_u8()), B, N,
                                        C.byref(cfg.to_c()), C.byref(pv)))
     return _plan_from_arrays(B, N, sets, set_len, weights, loads, au, cnt[0], tot[0])
+
+
+def route_batched(records, cfg: RoutingConfig) -> List[RoutingPlan]:
+    """route() of every record (score matrices with one expert count) in one
+    GPU launch sequence (oea_route_f64_batched_host): the per-record loop of
+    the reference's `route` command (oea_cli.cpp:153-175). Returns one plan
+    per record, each equal to route(record, cfg)."""
+    sms = [_as_scores(r) for r in records]
+    if not sms:
+        return []
+    N = sms[0].experts()
+    if N < 1:
+        raise InvalidArgument("RoutingConfig: expert count must be >= 1")
+    for sm in sms:
+        if sm.experts() != N:
+            raise InvalidArgument("route_batched: inconsistent expert count")
+    rcfg = cfg.resolved(N)
+    stride = max(plan_set_stride(rcfg), 1)
+    rows = np.array([sm.batch() for sm in sms], np.int32)
+    R, B = len(sms), int(rows.sum())
+    scores = np.ascontiguousarray(np.concatenate([sm.scores for sm in sms], axis=0), np.float64)
+    any_mask = any(sm.mask is not None and len(sm.mask) > 0 for sm in sms)
+    mask = (np.concatenate([sm._mask_u8() if sm._mask_u8() is not None else np.ones(sm.batch(), np.uint8)
+                            for sm in sms]) if any_mask else None)
+    sets = np.full((max(B, 1), stride), -1, np.int32)
+    set_len = np.zeros(max(B, 1), np.int32)
+    weights = np.zeros((max(B, 1), stride), np.float64)
+    loads = np.zeros((R, N), np.int32)
+    au = np.full((R, N), -1, np.int32)
+    cnt = np.zeros(R, np.int32)
+    tot = np.zeros(R, np.int64)
+    pv = PlanViewC(stride, _p(sets), _p(set_len), _p(weights), None, _p(loads), _p(au), _p(cnt),
+                   _p(tot), None, None, None, None, None)
+    ctx = default_context()
+    ctx.check(lib().oea_route_f64_batched_host(ctx.h, _p(scores), _p(mask), _p(rows), R, N,
+                                               C.byref(cfg.to_c()), C.byref(pv)))
+    plans, r0 = [], 0
+    for q in range(R):
+        b = int(rows[q])
+        plans.append(_plan_from_arrays(b, N, sets[r0:r0 + b], set_len[r0:r0 + b],
+                                       weights[r0:r0 + b], loads[q], au[q], cnt[q], tot[q]))
+        r0 += b
+    return plans
 
 
 def route_topk(scores, k: int) -> RoutingPlan:
