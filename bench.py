@@ -582,11 +582,32 @@ def bench_c5(args, env):
         us = e0.elapsed_time(e1) * 1000.0 / K
         del graph
         res.append({"k0": k0, "us": us, "tokens_per_s": Bc / us * 1e6, "T": int(cnt.item())})
+    # Score-trace routing: 256 (step, layer) records of 16
+    # tokens, host buffers, one batched call (oea_route_f64_batched_host) vs
+    # the reference's record-by-record loop through the single-batch API.
+    import numpy as np
+    import time
+    rng = np.random.default_rng(9)
+    recs = [oea.ScoreMatrix(rng.dirichlet(np.full(Nc, 0.3), size=16)) for _ in range(256)]
+    cfg = oea.RoutingConfig.simplified(4, K_TOP)
+    oea.route_batched(recs, cfg)
+    t0 = time.perf_counter()
+    for _ in range(5):
+        oea.route_batched(recs, cfg)
+    batched_ms = (time.perf_counter() - t0) * 1e3 / 5
+    t0 = time.perf_counter()
+    for r in recs:
+        oea.route(r, cfg)
+    loop_ms = (time.perf_counter() - t0) * 1e3
+    trace = {"records": len(recs), "tokens_per_record": 16, "routing": "simplified(4, 8)",
+             "batched_ms": batched_ms, "per_record_loop_ms": loop_ms,
+             "records_per_s_batched": len(recs) / batched_ms * 1e3,
+             "note": "host buffers, wall clock incl. H2D/D2H and plan unpacking"}
     line = {"metric": "C5 router-only µs per B=4096 route (fp64 route_f64, bit-exact path, CUDA-graph replay)",
             "value": res[3]["us"], "unit": "us/route-call", "higher_is_better": False,
             "config": {"workload": "C5 router stress", "B": Bc, "N": Nc, "k": K_TOP,
                        "scores": "softmax of N(0,1) fp64 logits, device-resident"},
-            "sweep": res}
+            "sweep": res, "trace_routing": trace}
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0

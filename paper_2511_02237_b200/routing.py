@@ -215,11 +215,16 @@ def _as_scores(scores) -> ScoreMatrix:
 
 def _plan_from_arrays(B, N, sets, set_len, weights, loads, au, cnt, tot) -> RoutingPlan:
     plan = RoutingPlan(n_experts=N)
-    plan.sets = [[int(v) for v in sets[i, : set_len[i]]] for i in range(B)]
-    plan.weights = ([[float(v) for v in weights[i, : set_len[i]]] for i in range(B)]
-                    if weights is not None else [[] for _ in range(B)])
+    lens = set_len[:B].tolist()
+    srows = sets[:B].tolist()  # (ndarray.tolist: Python ints / floats in one call)
+    plan.sets = [r[:n] for r, n in zip(srows, lens)]
+    if weights is not None:
+        wrows = weights[:B].tolist()
+        plan.weights = [r[:n] for r, n in zip(wrows, lens)]
+    else:
+        plan.weights = [[] for _ in range(B)]
     plan.active_count = int(cnt)
-    plan.active_union = [int(v) for v in au[: int(cnt)]]
+    plan.active_union = au[: int(cnt)].tolist()
     plan.loads = loads.copy()
     plan.total_load = int(tot)
     return plan
