@@ -168,6 +168,28 @@ int oea_phase2_f64_host(oea_ctx_t ctx, const uint8_t* mask, int32_t B, int32_t N
                         const int32_t* base_union, int32_t base_union_count,
                         const oea_routing_cfg* cfg, const oea_plan_view* plan);
 
+/* ---- router-score generators (score_gen.cpp:100-160) ----------------------
+ * ScoreSource batches on the device: Dirichlet(alpha) rows (Marsaglia-Tsang
+ * gammas over the counter RNG) or clustered rows (softmax of group template +
+ * token noise). Steps [step0, step0 + nsteps) x all layers in one launch,
+ * out [nsteps][layers][batch][n_experts] f64, cell (step, layer) = the
+ * reference's gen_scores(cfg, step, layer) within ~1e-15 relative (device
+ * libm). Errors: the reference's ScoreGenConfig::validate texts. */
+enum { OEA_GEN_DIRICHLET = 0, OEA_GEN_CLUSTERED = 1 };
+typedef struct {
+  int32_t kind;
+  int32_t n_experts, batch, steps, layers;
+  uint64_t seed;
+  double alpha;                      /* Dirichlet */
+  int32_t groups;                    /* clustered */
+  double within_group_concentration; /* clustered */
+  double between_group_spread;       /* clustered */
+} oea_score_gen_cfg;
+int oea_gen_scores(oea_ctx_t ctx, const oea_score_gen_cfg* cfg, int32_t step0, int32_t nsteps,
+                   double* out_dev, void* stream);
+int oea_gen_scores_host(oea_ctx_t ctx, const oea_score_gen_cfg* cfg, int32_t step0,
+                        int32_t nsteps, double* out_host);
+
 /* ---- device-resident MoE layer ------------------------------------------
  * dtype BF16: the decode hot path (fragment-ordered bf16 weights streamed by
  * TMA bulk copies, mma.sync tensor tiles). F32 / F64: SIMT FFN kept for the

@@ -496,3 +496,101 @@ double oo_expected_active_experts(int32_t N, int32_t k, int32_t B) {
   const double miss = 1.0 - (double)k / N;
   return N * (1.0 - pow(miss, B));
 }
+
+/* ---- score generators, score_gen.cpp:100-160 + rng.hpp:46-102 ----------- */
+/* Sequential CounterRng (rng.hpp:46-117): counter, cached Box-Muller spare. */
+typedef struct {
+  uint64_t key, counter;
+  double spare;
+  int has_spare;
+} oo_rng;
+
+static double rng_unit(oo_rng* r) { /* rng.hpp:54-62 */
+  r->counter += 1;
+  const uint64_t u = oo_splitmix64(r->key + r->counter * OO_GOLDEN);
+  return (double)((u >> 11) + 1) * 0x1.0p-53;
+}
+
+static double rng_normal(oo_rng* r) { /* rng.hpp:65-77 */
+  if (r->has_spare) {
+    r->has_spare = 0;
+    return r->spare;
+  }
+  const double u1 = rng_unit(r);
+  const double u2 = rng_unit(r);
+  const double rad = sqrt(-2.0 * log(u1));
+  const double theta = 2.0 * OO_PI * u2;
+  r->spare = rad * sin(theta);
+  r->has_spare = 1;
+  return rad * cos(theta);
+}
+
+static double rng_gamma(oo_rng* r, double alpha) { /* rng.hpp:82-98, Marsaglia-Tsang */
+  if (alpha < 1.0) {
+    const double u = rng_unit(r);
+    return rng_gamma(r, alpha + 1.0) * pow(u, 1.0 / alpha);
+  }
+  const double d = alpha - 1.0 / 3.0;
+  const double c = 1.0 / sqrt(9.0 * d);
+  for (;;) {
+    const double x = rng_normal(r);
+    double v = 1.0 + c * x;
+    if (v <= 0.0) continue;
+    v = v * v * v;
+    const double u = rng_unit(r);
+    const double x2 = x * x;
+    if (u < 1.0 - 0.0331 * x2 * x2) return d * v;
+    if (log(u) < 0.5 * x2 + d * (1.0 - v + log(v))) return d * v;
+  }
+}
+
+static oo_rng rng_for(uint64_t seed, int32_t step, int32_t layer, int32_t token, uint64_t tag) {
+  const uint64_t parts[5] = {seed, (uint64_t)step, (uint64_t)layer, (uint64_t)token, tag};
+  oo_rng r = {oo_stream_key(parts, 5), 0, 0.0, 0};
+  return r;
+}
+
+/* Dirichlet(alpha) rows for (step, layer): per token i its own stream
+ * (seed, step, layer, i, 201), N gammas, divided by their sequential sum
+ * (score_gen.cpp:119-133). out [B][N]. */
+void oo_gen_dirichlet(int32_t N, int32_t B, uint64_t seed, double alpha, int32_t step,
+                      int32_t layer, double* out) {
+  for (int32_t i = 0; i < B; ++i) {
+    oo_rng r = rng_for(seed, step, layer, i, 201);
+    double sum = 0.0;
+    double* row = out + (size_t)i * N;
+    for (int32_t e = 0; e < N; ++e) {
+      row[e] = rng_gamma(&r, alpha);
+      sum += row[e];
+    }
+    for (int32_t e = 0; e < N; ++e) row[e] /= sum;
+  }
+}
+
+/* Clustered rows (score_gen.cpp:136-160): group templates from streams
+ * (seed, step, layer, g, 202), token i in group i % groups, logits
+ * spread * (template + noise / concentration) with noise from
+ * (seed, step, layer, i, 203), then softmax (max-subtracted, sequential sum). */
+void oo_gen_clustered(int32_t N, int32_t B, uint64_t seed, int32_t groups, double conc,
+                      double spread, int32_t step, int32_t layer, double* out) {
+  double* tpl = (double*)malloc(sizeof(double) * (size_t)groups * N);
+  for (int32_t g = 0; g < groups; ++g) {
+    oo_rng r = rng_for(seed, step, layer, g, 202);
+    for (int32_t e = 0; e < N; ++e) tpl[(size_t)g * N + e] = rng_normal(&r);
+  }
+  for (int32_t i = 0; i < B; ++i) {
+    oo_rng r = rng_for(seed, step, layer, i, 203);
+    const int32_t g = i % groups;
+    double* row = out + (size_t)i * N;
+    for (int32_t e = 0; e < N; ++e) row[e] = spread * (tpl[(size_t)g * N + e] + rng_normal(&r) / conc);
+    double m = row[0];
+    for (int32_t e = 1; e < N; ++e) m = row[e] > m ? row[e] : m;
+    double sum = 0.0;
+    for (int32_t e = 0; e < N; ++e) {
+      row[e] = exp(row[e] - m);
+      sum += row[e];
+    }
+    for (int32_t e = 0; e < N; ++e) row[e] /= sum;
+  }
+  free(tpl);
+}

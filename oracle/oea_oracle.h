@@ -76,6 +76,12 @@ uint64_t oo_stream_key(const uint64_t* parts, int32_t n);
 /* normal #f (0-based) of the stream `key` (Box-Muller pairs, rng.hpp:65-77) */
 double oo_stream_normal(uint64_t key, uint64_t f);
 
+/* Score generators (score_gen.cpp:100-160): one (step, layer) batch, [B][N]. */
+void oo_gen_dirichlet(int32_t N, int32_t B, uint64_t seed, double alpha, int32_t step,
+                      int32_t layer, double* out);
+void oo_gen_clustered(int32_t N, int32_t B, uint64_t seed, int32_t groups, double conc,
+                      double spread, int32_t step, int32_t layer, double* out);
+
 /* make_random_layer, moe_layer.cpp:76-98 (exact); fills the flat arrays.
  * n_threads > 1 splits the counter stream across pthreads (identical bits). */
 void oo_make_random_layer(int32_t D, int32_t H, int32_t N, uint64_t seed,

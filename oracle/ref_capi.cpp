@@ -19,6 +19,7 @@
 #include "oea/latency.hpp"
 #include "oea/moe_layer.hpp"
 #include "oea/routing.hpp"
+#include "oea/score_gen.hpp"
 #include "oracle.hpp"
 
 #include <thread>
@@ -433,6 +434,28 @@ int ref_decode(void* layer, int scalar_is_float, const double* x, int B, int D, 
     std::memcpy(out, r.data(), sizeof(double) * B * D);
     *active_count = plan.active_count;
     *total_load = plan.total_load;
+  })
+}
+
+// gen_scores (score_gen.cpp:100-160) for one (step, layer): kind 0 =
+// Dirichlet(alpha), 1 = clustered. out [batch][n_experts].
+int ref_gen_scores(int kind, int n_experts, int batch, int steps, int layers, uint64_t seed,
+                   double alpha, int groups, double conc, double spread, int step, int layer,
+                   double* out) {
+  REF_GUARD({
+    ScoreGenConfig cfg;
+    cfg.kind = kind == 0 ? GenKind::Dirichlet : GenKind::Clustered;
+    cfg.n_experts = n_experts;
+    cfg.batch = batch;
+    cfg.steps = steps;
+    cfg.layers = layers;
+    cfg.seed = seed;
+    cfg.alpha = alpha;
+    cfg.groups = groups;
+    cfg.within_group_concentration = conc;
+    cfg.between_group_spread = spread;
+    const ScoreMatrix m = gen_scores(cfg, step, layer);
+    std::memcpy(out, m.scores.data(), sizeof(double) * batch * n_experts);
   })
 }
 

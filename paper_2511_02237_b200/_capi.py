@@ -37,6 +37,13 @@ class RoutingCfgC(C.Structure):
                 ("k_max", C.c_int32), ("max_p", C.c_int32), ("cap", C.c_int32)]
 
 
+class ScoreGenCfgC(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("n_experts", C.c_int32), ("batch", C.c_int32),
+                ("steps", C.c_int32), ("layers", C.c_int32), ("seed", C.c_uint64),
+                ("alpha", C.c_double), ("groups", C.c_int32),
+                ("within_group_concentration", C.c_double), ("between_group_spread", C.c_double)]
+
+
 class PlanViewC(C.Structure):
     _fields_ = [("set_stride", C.c_int32)] + [
         (name, C.c_void_p) for name in (
@@ -76,6 +83,8 @@ def lib():
                 "oea_route_f64_host": [vp, vp, vp, i32, i32, vp, vp],
                 "oea_route_f64": [vp, vp, vp, i32, i32, vp, vp, vp],
                 "oea_route_f64_batched_host": [vp, vp, vp, vp, i32, i32, vp, vp],
+                "oea_gen_scores": [vp, vp, i32, i32, vp, vp],
+                "oea_gen_scores_host": [vp, vp, i32, i32, vp],
                 "oea_sort_experts_f64_host": [vp, vp, i32, i32, vp],
                 "oea_phase1_f64_host": [vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, i32, vp, vp],
                 "oea_phase2_f64_host": [vp, vp, i32, i32, vp, vp, vp, i32, vp, vp],
@@ -114,6 +123,7 @@ EXPORTED = (
     "oea_abi_version", "oea_ctx_create", "oea_ctx_destroy", "oea_last_error", "oea_ctx_stream",
     "oea_ctx_synchronize", "oea_ctx_kernel_launches", "oea_config_resolve",
     "oea_plan_set_stride", "oea_route_f64_host", "oea_route_f64", "oea_route_f64_batched_host",
+    "oea_gen_scores", "oea_gen_scores_host",
     "oea_sort_experts_f64_host",
     "oea_phase1_f64_host", "oea_phase2_f64_host", "oea_layer_create", "oea_layer_destroy",
     "oea_layer_upload_router", "oea_layer_upload_expert", "oea_layer_init_random",

@@ -931,6 +931,57 @@ int oea_route_f64_batched_host(oea_ctx_t ctx, const double* scores, const uint8_
   return OEA_OK;
 }
 
+// ScoreGenConfig::validate (score_gen.cpp:46-76) + the ScoreSource range check.
+static int check_gen(oea_ctx* ctx, const oea_score_gen_cfg* c, int step0, int nsteps) {
+  if (c == nullptr) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "null generator config");
+  if (c->steps < 1 || c->layers < 1)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "score gen: steps and layers must be >= 1");
+  if (c->kind != OEA_GEN_DIRICHLET && c->kind != OEA_GEN_CLUSTERED)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "score gen: replay is read on the host (read_score_trace)");
+  if (c->n_experts < 1 || c->batch < 1)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "score gen: n_experts and batch must be >= 1");
+  if (c->kind == OEA_GEN_DIRICHLET && !(c->alpha > 0.0))
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "score gen: alpha must be > 0");
+  if (c->kind == OEA_GEN_CLUSTERED) {
+    if (c->groups < 1 || c->groups > c->n_experts)
+      return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "score gen: groups must be in [1, n_experts]");
+    if (!(c->within_group_concentration > 0.0))
+      return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "score gen: within_group_concentration must be > 0");
+    if (c->between_group_spread < 0.0)
+      return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "score gen: between_group_spread must be >= 0");
+  }
+  if (nsteps < 1 || step0 < 0 || static_cast<int64_t>(step0) + nsteps > c->steps)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "score source: step/layer out of range");
+  return OEA_OK;
+}
+
+int oea_gen_scores(oea_ctx_t ctx, const oea_score_gen_cfg* cfg, int32_t step0, int32_t nsteps,
+                   double* out_dev, void* stream) {
+  CHECK_CTX(ctx);
+  int r = check_gen(ctx, cfg, step0, nsteps);
+  if (r) return r;
+  if (out_dev == nullptr) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "gen_scores: null output");
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  return oea_host::gen_scores_launch(ctx, *cfg, step0, nsteps, out_dev, s);
+}
+
+int oea_gen_scores_host(oea_ctx_t ctx, const oea_score_gen_cfg* cfg, int32_t step0,
+                        int32_t nsteps, double* out_host) {
+  CHECK_CTX(ctx);
+  int r = check_gen(ctx, cfg, step0, nsteps);
+  if (r) return r;
+  if (out_host == nullptr) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "gen_scores: null output");
+  const size_t n = static_cast<size_t>(nsteps) * cfg->layers * cfg->batch * cfg->n_experts;
+  cudaStream_t s = ctx->stream;
+  double* d = nullptr;
+  OEA_CUDA_TRY(ctx, cudaMallocAsync(reinterpret_cast<void**>(&d), n * sizeof(double), s));
+  r = oea_host::gen_scores_launch(ctx, *cfg, step0, nsteps, d, s);
+  if (r == OEA_OK) r = d2h(ctx, out_host, d, n);
+  cudaFreeAsync(d, s);
+  OEA_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  return r;
+}
+
 int oea_sort_experts_f64_host(oea_ctx_t ctx, const double* scores, int32_t B, int32_t N,
                               int32_t* order) {
   CHECK_CTX(ctx);
