@@ -20,6 +20,7 @@
 #include "oea/moe_layer.hpp"
 #include "oea/routing.hpp"
 #include "oea/score_gen.hpp"
+#include "oea/simulate.hpp"
 #include "oracle.hpp"
 
 #include <thread>
@@ -456,6 +457,72 @@ int ref_gen_scores(int kind, int n_experts, int batch, int steps, int layers, ui
     cfg.between_group_spread = spread;
     const ScoreMatrix m = gen_scores(cfg, step, layer);
     std::memcpy(out, m.scores.data(), sizeof(double) * batch * n_experts);
+  })
+}
+
+static ScoreGenConfig gen_cfg(const int32_t* gi, uint64_t seed, const double* gd) {
+  // gi: kind, n_experts, batch, steps, layers, groups; gd: alpha, conc, spread
+  ScoreGenConfig cfg;
+  cfg.kind = gi[0] == 0 ? GenKind::Dirichlet : GenKind::Clustered;
+  cfg.n_experts = gi[1];
+  cfg.batch = gi[2];
+  cfg.steps = gi[3];
+  cfg.layers = gi[4];
+  cfg.groups = gi[5];
+  cfg.seed = seed;
+  cfg.alpha = gd[0];
+  cfg.within_group_concentration = gd[1];
+  cfg.between_group_spread = gd[2];
+  return cfg;
+}
+
+static void put_records(const std::vector<StepRecord>& v, int32_t* T, int64_t* load, double* lat) {
+  for (size_t i = 0; i < v.size(); ++i) {
+    T[i] = v[i].active_experts;
+    load[i] = v[i].total_load;
+    lat[i] = v[i].modeled_latency_us;
+  }
+}
+
+// simulate_decode (simulate.cpp:128-151): per (step, layer) records of the
+// routed and the vanilla shadow run, plus the 8 aggregates
+// (compute_aggregates :69-103, in TraceAggregates field order).
+int ref_simulate_decode(const int32_t* gi, uint64_t seed, const double* gd, int mode, int k,
+                        int k0, double p, int k_max, int max_p, int cap, double a_us,
+                        double b_us, int32_t* T, int64_t* load, double* lat, int32_t* vT,
+                        int64_t* vload, double* vlat, double* agg) {
+  REF_GUARD({
+    const auto tr = simulate_decode(gen_cfg(gi, seed, gd), make_cfg(mode, k, k0, p, k_max, max_p, cap),
+                                    LatencyParams{a_us, b_us}, 1);
+    put_records(tr.records, T, load, lat);
+    put_records(tr.vanilla_records, vT, vload, vlat);
+    const auto& a = tr.aggregates;
+    agg[0] = a.mean_active_experts;
+    agg[1] = a.mean_total_load;
+    agg[2] = a.mean_latency_us;
+    agg[3] = a.vanilla_mean_active_experts;
+    agg[4] = a.vanilla_mean_total_load;
+    agg[5] = a.vanilla_mean_latency_us;
+    agg[6] = a.normalized_active_experts;
+    agg[7] = a.normalized_latency;
+  })
+}
+
+// padding_experiment (simulate.cpp:185-257): records of the three variants
+// (no / naive / masked padding) and masked_matches_no_padding.
+int ref_padding_experiment(const int32_t* gi, uint64_t seed, const double* gd, int mode, int k,
+                           int k0, double p, int k_max, int max_p, int cap, int pad_to,
+                           double a_us, double b_us, int32_t* T3, int64_t* load3, double* lat3,
+                           int32_t* matches) {
+  REF_GUARD({
+    const auto rep = padding_experiment(gen_cfg(gi, seed, gd),
+                                        make_cfg(mode, k, k0, p, k_max, max_p, cap), pad_to,
+                                        LatencyParams{a_us, b_us}, 1);
+    const size_t n = rep.no_padding.records.size();
+    put_records(rep.no_padding.records, T3, load3, lat3);
+    put_records(rep.naive_padding.records, T3 + n, load3 + n, lat3 + n);
+    put_records(rep.masked_padding.records, T3 + 2 * n, load3 + 2 * n, lat3 + 2 * n);
+    *matches = rep.masked_matches_no_padding ? 1 : 0;
   })
 }
 
