@@ -793,10 +793,10 @@ int oea_route_f64_host(oea_ctx_t ctx, const double* scores, const uint8_t* mask,
 }
 
 // Many independent records (a score trace's (step, layer) batches) in one
-// launch sequence: the fast-path kernels with a row -> record map, so each
-// record has its own union and aggregates (io.cpp:85-172 + route() per record
-// in the reference's `route` command, oea_cli.cpp:153-175). Configurations
-// outside the fast path route record by record.
+// launch sequence: the route kernels (fast path, or the general sort path
+// for p < 1 / max_p < N / N > 128) with a row -> record map, so each record
+// has its own union and aggregates (io.cpp:85-172 + route() per record in the
+// reference's `route` command, oea_cli.cpp:153-175).
 int oea_route_f64_batched_host(oea_ctx_t ctx, const double* scores, const uint8_t* mask,
                                const int32_t* rows, int32_t R, int32_t N,
                                const oea_routing_cfg* cfg, const oea_plan_view* plan) {
@@ -820,41 +820,16 @@ int oea_route_f64_batched_host(oea_ctx_t ctx, const double* scores, const uint8_
   const int stride = stride_of(rc);
   if (plan->set_stride < stride)
     return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "route: plan set_stride too small");
+  if (N > kMaxRouteN)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "route: N > " + std::to_string(kMaxRouteN));
   const Cfg dc = dev_cfg(rc, stride);
-  if (!oea_host::route_fast_ok(dc, N, false) || getenv("OEA_ROUTE_SORT") != nullptr) {
-    // record by record through the general path
-    int64_t row0 = 0;
-    for (int q = 0; q < R; ++q) {
-      const size_t ps = plan->set_stride;
-      oea_plan_view v = *plan;
-      v.sets = plan->sets + row0 * ps;
-      v.set_len = plan->set_len + row0;
-      if (v.weights) v.weights += row0 * ps;
-      if (v.weights_f32) v.weights_f32 += row0 * ps;
-      if (v.loads) v.loads += static_cast<size_t>(q) * N;
-      if (v.active_union) v.active_union += static_cast<size_t>(q) * N;
-      if (v.active_count) v.active_count += q;
-      if (v.total_load) v.total_load += q;
-      if (v.phase1_t) v.phase1_t += row0;
-      if (v.phase1_n) v.phase1_n += row0;
-      if (v.base_union) v.base_union += static_cast<size_t>(q) * N;
-      if (v.base_union_count) v.base_union_count += q;
-      r = oea_route_f64_host(ctx, scores + row0 * N, mask ? mask + row0 : nullptr, rows[q], N, cfg, &v);
-      if (r) {
-        if (r == OEA_ERR_DOMAIN)  // name the record, like read_score_trace's errors
-          return fail(ctx, r, "record " + std::to_string(q) + ": " + ctx->last_error);
-        return r;
-      }
-      row0 += rows[q];
-    }
-    return OEA_OK;
-  }
   Workspace& w = extra(ctx)->ws;
   r = ensure(ctx, w, Need{B, N, 1, 1, stride});
   if (r) return r;
   // per-record buffers: seg [B] | union [R][4] | loads, active, base [R][N] | counts [R] x2 | total [R]
   CtxExtra* ex = extra(ctx);
-  const size_t need = static_cast<size_t>(B) * 4 + static_cast<size_t>(R) * (16 + 12 * N + 8 + 8) + 256;
+  const size_t words = (static_cast<size_t>(N) + 31) / 32;
+  const size_t need = static_cast<size_t>(B) * 4 + static_cast<size_t>(R) * (4 * words + 12 * N + 8 + 8) + 256;
   cudaStream_t s = ctx->stream;
   if (need > ex->seg_bytes) {
     OEA_CUDA_TRY(ctx, cudaStreamSynchronize(s));
@@ -872,7 +847,7 @@ int oea_route_f64_batched_host(oea_ctx_t ctx, const double* scores, const uint8_
   };
   int64_t* d_total = reinterpret_cast<int64_t*>(take(8 * static_cast<size_t>(R)));
   int32_t* d_seg = reinterpret_cast<int32_t*>(take(4 * static_cast<size_t>(B)));
-  uint32_t* d_union = reinterpret_cast<uint32_t*>(take(16 * static_cast<size_t>(R)));
+  uint32_t* d_union = reinterpret_cast<uint32_t*>(take(4 * words * static_cast<size_t>(R)));
   int32_t* d_loads = reinterpret_cast<int32_t*>(take(4 * static_cast<size_t>(R) * N));
   int32_t* d_active = reinterpret_cast<int32_t*>(take(4 * static_cast<size_t>(R) * N));
   int32_t* d_base = reinterpret_cast<int32_t*>(take(4 * static_cast<size_t>(R) * N));
@@ -893,7 +868,11 @@ int oea_route_f64_batched_host(oea_ctx_t ctx, const double* scores, const uint8_
   rb.base_union = d_base;
   rb.base_union_count = d_bcnt;
   const int set_mode = rc.mode == OEA_MODE_VANILLA ? 0 : rc.mode == OEA_MODE_PRUNED ? 1 : 2;
-  r = oea_host::route_f64_fast_launch(ctx, dc, B, N, rb, set_mode, s, R, d_seg);
+  if (oea_host::route_fast_ok(dc, N, false) && getenv("OEA_ROUTE_SORT") == nullptr)
+    r = oea_host::route_f64_fast_launch(ctx, dc, B, N, rb, set_mode, s, R, d_seg);
+  else
+    r = oea_host::route_f64_launch(ctx, dc, B, N, rb, false, rc.mode != OEA_MODE_VANILLA,
+                                   set_mode, false, s, R, d_seg);
   if (r) return r;
   int32_t tok = INT_MAX;
   OEA_CUDA_TRY(ctx, cudaMemcpyAsync(&tok, w.err_token, 4, cudaMemcpyDeviceToHost, s));

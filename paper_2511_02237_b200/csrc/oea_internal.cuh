@@ -151,7 +151,8 @@ struct RouteBuffers {
 };
 int route_f64_launch(oea_ctx* ctx, const oea_dev::Cfg& cfg, int B, int N,
                      const RouteBuffers& rb, bool order_given, bool run_phase1,
-                     int set_mode, bool n_given, cudaStream_t s);
+                     int set_mode, bool n_given, cudaStream_t s, int R = 1,
+                     const int32_t* seg = nullptr);
 // Fast path of route_f64 (p == 1, max_p >= N, N <= 128, no full order
 // requested): top-m picks instead of a full sort; same results bit for bit.
 bool route_fast_ok(const oea_dev::Cfg& cfg, int N, bool need_order);

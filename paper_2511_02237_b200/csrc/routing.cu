@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(kRouteWarps * 32)
                   const uint8_t* __restrict__ mask, int32_t* __restrict__ order,
                   int32_t* __restrict__ t_out, int32_t* __restrict__ n_out,
                   uint32_t* __restrict__ union_bits, const int order_given,
-                  const int run_phase1) {
+                  const int run_phase1, const int32_t* __restrict__ seg) {
   __shared__ int32_t s_ord[kRouteWarps][32 * E];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x * kRouteWarps + warp;
@@ -83,9 +83,11 @@ __global__ void __launch_bounds__(kRouteWarps * 32)
       t_i = __shfl_sync(kFull, t_i, 0);
     }
     n_i = min(cfg.k0, t_i);
+    // batched records: each record's own base union ([R][ceil(N/32)] words)
+    uint32_t* ub = seg ? union_bits + static_cast<size_t>(seg[i]) * ((N + 31) >> 5) : union_bits;
     for (int j = lane; j < n_i; j += 32) {
       const int e = so[j];
-      atomicOr(&union_bits[e >> 5], 1u << (e & 31));
+      atomicOr(&ub[e >> 5], 1u << (e & 31));
     }
   }
   if (lane == 0) {
@@ -104,10 +106,16 @@ __global__ void __launch_bounds__(kRouteWarps * 32)
                  int32_t* __restrict__ sets, int32_t* __restrict__ set_len,
                  double* __restrict__ weights, float* __restrict__ weights_f32,
                  int32_t* __restrict__ loads, unsigned long long* __restrict__ total_load,
-                 int32_t* __restrict__ err_token) {
+                 int32_t* __restrict__ err_token, const int32_t* __restrict__ seg) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x * kRouteWarps + warp;
   if (i >= B) return;
+  if (seg) {  // batched records: the record's union and aggregates
+    const int sg = seg[i];
+    union_bits += static_cast<size_t>(sg) * ((N + 31) >> 5);
+    loads += static_cast<size_t>(sg) * N;
+    total_load += sg;
+  }
   const int stride = cfg.stride;
   const int32_t* ord = order + static_cast<size_t>(i) * N;
   int32_t* srow = sets + static_cast<size_t>(i) * stride;
@@ -206,13 +214,13 @@ __global__ void __launch_bounds__(1024)
                 int32_t* __restrict__ base_union, int32_t* __restrict__ base_count,
                 int64_t* __restrict__ total_load) {
   // batched routing (route_f64_batched): CTA b aggregates record b, whose
-  // per-record buffers sit at stride N (bitmaps: 4 words, N <= 128)
+  // per-record buffers sit at stride N (bitmaps: ceil(N / 32) words)
   if (blockIdx.x > 0) {
     const int b = blockIdx.x;
     loads += static_cast<size_t>(b) * N;
     active_union += static_cast<size_t>(b) * N;
     active_count += b;
-    union_bits += 4 * b;
+    union_bits += static_cast<size_t>(b) * ((N + 31) >> 5);
     if (base_union) base_union += static_cast<size_t>(b) * N;
     if (base_count) base_count += b;
     if (total_load) total_load += b;
@@ -372,7 +380,7 @@ __global__ void __launch_bounds__(kRouteWarps * 32)
     const bool real = mask == nullptr || mask[i] != 0;
     // batched records: the token's record owns its union bitmap and loads
     const int sg = seg ? seg[i] : 0;
-    uint32_t* ub = union_bits + 4 * sg;
+    uint32_t* ub = union_bits + static_cast<size_t>(sg) * ((N + 31) >> 5);
     int* cnt = seg ? loads + static_cast<size_t>(sg) * N : s_loads;
     uint64_t k[E];
     int id[E];
@@ -420,7 +428,7 @@ __global__ void __launch_bounds__(kRouteWarps * 32)
     int32_t* srow = sets + static_cast<size_t>(i) * cfg.stride;
     const bool real = mask == nullptr || mask[i] != 0;
     const int sg = seg ? seg[i] : 0;
-    const uint32_t* ub = union_bits + 4 * sg;
+    const uint32_t* ub = union_bits + static_cast<size_t>(sg) * ((N + 31) >> 5);
     int* cnt = seg ? loads + static_cast<size_t>(sg) * N : s_loads;
     const int n = real ? n_in[i] : 0;
     int len = n;
@@ -464,37 +472,39 @@ using namespace oea_dev;
 
 template <int E>
 static void launch_rank(const Cfg& cfg, int B, int N, const RouteBuffers& rb, int order_given,
-                        int run_phase1, cudaStream_t s) {
+                        int run_phase1, const int32_t* seg, cudaStream_t s) {
   const int grid = (B + kRouteWarps - 1) / kRouteWarps;
   k_rank_phase1<E><<<grid, kRouteWarps * 32, 0, s>>>(cfg, B, N, rb.scores, rb.mask, rb.order,
                                                      rb.t, rb.n, rb.union_bits, order_given,
-                                                     run_phase1);
+                                                     run_phase1, seg);
 }
 
+// R > 1: batched independent records (see route_f64_fast_launch).
 int route_f64_launch(oea_ctx* ctx, const Cfg& cfg, int B, int N, const RouteBuffers& rb,
                      bool order_given, bool run_phase1, int set_mode, bool n_given,
-                     cudaStream_t s) {
+                     cudaStream_t s, int R, const int32_t* seg) {
   const int words = (N + 31) / 32;
-  if (!n_given) OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.union_bits, 0, words * 4, s));
-  OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.loads, 0, sizeof(int32_t) * N, s));
-  OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.total_load, 0, sizeof(int64_t), s));
+  const int32_t* sg = R > 1 ? seg : nullptr;
+  if (!n_given) OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.union_bits, 0, sizeof(uint32_t) * words * R, s));
+  OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.loads, 0, sizeof(int32_t) * N * R, s));
+  OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.total_load, 0, sizeof(int64_t) * R, s));
   OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.err_token, 0x7f, sizeof(int32_t), s));
 
   if (!n_given) {
     const int Np = round_up(N, 32);
     const int need_phase1 = run_phase1 ? 1 : 0;
     if (Np <= 32)
-      launch_rank<1>(cfg, B, N, rb, order_given, need_phase1, s);
+      launch_rank<1>(cfg, B, N, rb, order_given, need_phase1, sg, s);
     else if (Np <= 64)
-      launch_rank<2>(cfg, B, N, rb, order_given, need_phase1, s);
+      launch_rank<2>(cfg, B, N, rb, order_given, need_phase1, sg, s);
     else if (Np <= 128)
-      launch_rank<4>(cfg, B, N, rb, order_given, need_phase1, s);
+      launch_rank<4>(cfg, B, N, rb, order_given, need_phase1, sg, s);
     else if (Np <= 256)
-      launch_rank<8>(cfg, B, N, rb, order_given, need_phase1, s);
+      launch_rank<8>(cfg, B, N, rb, order_given, need_phase1, sg, s);
     else if (Np <= 512)
-      launch_rank<16>(cfg, B, N, rb, order_given, need_phase1, s);
+      launch_rank<16>(cfg, B, N, rb, order_given, need_phase1, sg, s);
     else
-      launch_rank<32>(cfg, B, N, rb, order_given, need_phase1, s);
+      launch_rank<32>(cfg, B, N, rb, order_given, need_phase1, sg, s);
     OEA_LAUNCHED(ctx);
   }
   // Set construction: 0 vanilla (route_topk), 1 pruned (baseline), 2 piggyback.
@@ -503,9 +513,9 @@ int route_f64_launch(oea_ctx* ctx, const Cfg& cfg, int B, int N, const RouteBuff
   k_build_sets<<<grid, kRouteWarps * 32, 0, s>>>(
       cfg, B, N, set_mode, do_weights, rb.scores, rb.mask, rb.order, rb.n, rb.union_bits,
       rb.sets, rb.set_len, rb.weights, rb.weights_f32, rb.loads,
-      reinterpret_cast<unsigned long long*>(rb.total_load), rb.err_token);
+      reinterpret_cast<unsigned long long*>(rb.total_load), rb.err_token, sg);
   OEA_LAUNCHED(ctx);
-  k_aggregate<<<1, 1024, 0, s>>>(N, rb.loads, rb.active_union, rb.active_count, rb.union_bits,
+  k_aggregate<<<R, 1024, 0, s>>>(N, rb.loads, rb.active_union, rb.active_count, rb.union_bits,
                                  rb.base_union, rb.base_union_count, nullptr);
   OEA_LAUNCHED(ctx);
   return OEA_OK;
@@ -537,7 +547,7 @@ bool route_fast_ok(const Cfg& cfg, int N, bool need_order) {
 // base_union / base_union_count are per record ([R][4] words, [R][N], [R]).
 int route_f64_fast_launch(oea_ctx* ctx, const Cfg& cfg, int B, int N, const RouteBuffers& rb,
                           int set_mode, cudaStream_t s, int R, const int32_t* seg) {
-  const int words = R > 1 ? 4 * R : (N + 31) / 32;
+  const int words = ((N + 31) / 32) * R;
   OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.union_bits, 0, words * 4, s));
   OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.loads, 0, sizeof(int32_t) * N * R, s));
   OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.err_token, 0x7f, sizeof(int32_t), s));
