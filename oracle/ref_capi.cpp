@@ -21,6 +21,7 @@
 #include "oea/routing.hpp"
 #include "oea/score_gen.hpp"
 #include "oea/simulate.hpp"
+#include "oea/sweep.hpp"
 #include "oracle.hpp"
 
 #include <thread>
@@ -523,6 +524,35 @@ int ref_padding_experiment(const int32_t* gi, uint64_t seed, const double* gd, i
     put_records(rep.naive_padding.records, T3 + n, load3 + n, lat3 + n);
     put_records(rep.masked_padding.records, T3 + 2 * n, load3 + 2 * n, lat3 + 2 * n);
     *matches = rep.masked_matches_no_padding ? 1 : 0;
+  })
+}
+
+// sweep (sweep.cpp:77-106) over default_sweep_grid(N, k) (:48-75): the mean
+// T of every grid point, in grid order (n_out = grid size; buffer >= 4096).
+int ref_sweep_default(const int32_t* gi, uint64_t seed, const double* gd, int k, double a_us,
+                      double b_us, int rounding, double* mean_t, int32_t* n_out) {
+  REF_GUARD({
+    const ScoreGenConfig gen = gen_cfg(gi, seed, gd);
+    const auto grid = default_sweep_grid(gen.n_experts, k);
+    RoundingRule rr;
+    rr.enabled = rounding != 0;
+    const auto pts = sweep(gen, grid, LatencyParams{a_us, b_us}, nullptr, rr, 1);
+    for (size_t i = 0; i < pts.size(); ++i) mean_t[i] = pts[i].mean_active_experts;
+    *n_out = static_cast<int32_t>(pts.size());
+  })
+}
+
+// pareto_indices (sweep.cpp:108-122) of points (T, quality or NaN = none).
+int ref_pareto_indices(const double* t, const double* q, int n, int32_t* out, int32_t* count) {
+  REF_GUARD({
+    std::vector<SweepPoint> pts(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) {
+      pts[i].mean_active_experts = t[i];
+      if (!std::isnan(q[i])) pts[i].quality_delta = q[i];
+    }
+    const auto idx = pareto_indices(pts);
+    for (size_t i = 0; i < idx.size(); ++i) out[i] = static_cast<int32_t>(idx[i]);
+    *count = static_cast<int32_t>(idx.size());
   })
 }
 

@@ -29,7 +29,9 @@ from .traces import read_score_trace, routing_config_json
 __all__ = ["LatencyParams", "StepRecord", "TraceAggregates", "DecodeTrace", "expert_latency",
            "moe_latency", "simulate_decode", "PaddingVariant", "PaddingReport",
            "padding_experiment", "write_trace_csv", "write_trace_summary_json",
-           "write_padding_json", "gen_config_json", "cell_scores"]
+           "write_padding_json", "gen_config_json", "cell_scores", "RoundingRule", "SweepPoint",
+           "default_sweep_grid", "sweep", "pareto_indices", "pareto_frontier", "write_sweep_csv",
+           "read_sweep_csv"]
 
 
 @dataclass
@@ -317,3 +319,156 @@ def write_padding_json(path: str, rep: PaddingReport, gen: ScoreGenConfig,
                               "mean_total_load": v.mean_total_load,
                               "mean_latency_us": v.mean_latency_us}
                      for v in (rep.no_padding, rep.naive_padding, rep.masked_padding)}})
+
+
+# ---------------------------------------------------------------------------
+# Config sweep and Pareto frontier (sweep.cpp:48-230)
+# ---------------------------------------------------------------------------
+@dataclass
+class RoundingRule:
+    """sweep.hpp:24-28"""
+    enabled: bool = False
+    quality_bin: float = 0.005
+    experts_bin: float = 0.1
+
+
+@dataclass
+class SweepPoint:
+    """sweep.hpp:30-35"""
+    config: RoutingConfig
+    mean_active_experts: float = 0.0
+    quality_delta: Optional[float] = None
+    rounded: bool = False
+
+
+def default_sweep_grid(n_experts: int, k: int) -> List[RoutingConfig]:
+    """sweep.cpp:48-75: vanilla(k) then oea(k0, p, k_max, max_p, k) over
+    k0 in [ceil(k/2), k], k_max in [max(k-1, k0), k + max(1, 3k/8)], p in
+    0.4..1.0, max_p in {k, 2k, 4k, N} (deduplicated, capped at N)."""
+    if n_experts < 1 or k < 1 or k > n_experts:
+        raise InvalidArgument("default_sweep_grid: need 1 <= k <= N")
+    max_ps: List[int] = []
+    for m in (k, 2 * k, 4 * k, n_experts):
+        m = min(m, n_experts)
+        if m not in max_ps:
+            max_ps.append(m)
+    k0_lo = max(1, (k + 1) // 2)
+    kmax_lo = max(1, k - 1)
+    kmax_hi = min(n_experts, k + max(1, (3 * k) // 8))
+    grid = [RoutingConfig.vanilla(k)]
+    for k0 in range(k0_lo, min(k, n_experts) + 1):
+        for kmax in range(max(kmax_lo, k0), kmax_hi + 1):
+            for pi in range(4, 11):
+                for max_p in max_ps:
+                    grid.append(RoutingConfig.oea(k0, pi / 10.0, kmax, max_p, k))
+    return grid
+
+
+def _round_half_away(x: float) -> float:  # std::round
+    import math
+    f = math.floor(abs(x))
+    r = f + 1.0 if abs(x) - f >= 0.5 else f
+    return math.copysign(r, x)
+
+
+def _snap(v: float, b: float) -> float:
+    return _round_half_away(v / b) * b
+
+
+def sweep(gen: ScoreGenConfig, grid: List[RoutingConfig], latency: LatencyParams,
+          rounding: RoundingRule = RoundingRule()) -> List[SweepPoint]:
+    """sweep.cpp:77-106 for a score source: mean T per routing config. The
+    cells are generated once (one launch) and each config routes all of them
+    in one batched call; the reference re-simulates (and shadow-routes
+    vanilla) per config. latency is part of the reference signature; the
+    points carry only T and the quality delta (none for score sources)."""
+    if not grid:
+        raise InvalidArgument("sweep: empty config grid")
+    cfg, cells = cell_scores(gen)
+    n = float(len(cells))
+    pts = []
+    for c in grid:
+        rc = c.resolved(cfg.n_experts)
+        s = 0.0
+        for p in route_batched(cells, rc):
+            s += p.active_count
+        pt = SweepPoint(config=rc, mean_active_experts=s / n)
+        if rounding.enabled:
+            pt.mean_active_experts = _snap(pt.mean_active_experts, rounding.experts_bin)
+            pt.rounded = True
+        pts.append(pt)
+    return pts
+
+
+def _dominates(a: SweepPoint, b: SweepPoint) -> bool:
+    aq, bq = a.quality_delta or 0.0, b.quality_delta or 0.0
+    if a.mean_active_experts > b.mean_active_experts or aq > bq:
+        return False
+    return a.mean_active_experts < b.mean_active_experts or aq < bq
+
+
+def pareto_indices(pts: List[SweepPoint]) -> List[int]:
+    """sweep.cpp:108-122"""
+    return [i for i in range(len(pts))
+            if not any(j != i and _dominates(pts[j], pts[i]) for j in range(len(pts)))]
+
+
+def pareto_frontier(pts: List[SweepPoint]) -> List[SweepPoint]:
+    """sweep.cpp:124-142: non-dominated points by (T, quality, index)."""
+    idx = sorted(pareto_indices(pts),
+                 key=lambda i: (pts[i].mean_active_experts, pts[i].quality_delta or 0.0, i))
+    return [pts[i] for i in idx]
+
+
+_SWEEP_HEADER = ["mode", "k", "k0", "p", "k_max", "max_p", "cap", "mean_active_experts",
+                 "quality_delta", "rounded"]
+
+
+def write_sweep_csv(path: str, pts: List[SweepPoint]) -> None:
+    """sweep.cpp:144-162"""
+    from .routing import to_string as rs
+    try:
+        out = open(path, "w")
+    except OSError:
+        raise InvalidArgument("write_sweep_csv: cannot open " + path)
+    with out:
+        out.write(",".join(_SWEEP_HEADER) + "\n")
+        for p in pts:
+            c = p.config
+            q = _fmt(p.quality_delta) if p.quality_delta is not None else ""
+            out.write(f"{rs(c.mode)},{c.k},{c.k0},{_fmt(c.p)},{c.k_max},{c.max_p},{rs(c.cap)},"
+                      f"{_fmt(p.mean_active_experts)},{q},{1 if p.rounded else 0}\n")
+
+
+def read_sweep_csv(path: str) -> List[SweepPoint]:
+    """sweep.cpp:164-228 (same checks and messages)."""
+    from .routing import cap_semantics_from_string, routing_mode_from_string
+    try:
+        f = open(path)
+    except OSError:
+        raise InvalidArgument("read_sweep_csv: cannot open " + path)
+    with f:
+        lines = f.read().split("\n")
+    if not lines or lines == [""]:
+        raise InvalidArgument(f"read_sweep_csv: {path} is empty")
+    if [h.rstrip("\r ") for h in lines[0].split(",")] != _SWEEP_HEADER:
+        raise InvalidArgument(f"read_sweep_csv: {path} has an unexpected header")
+    pts = []
+    for line_no, line in enumerate(lines[1:], start=2):
+        if line.strip(" \t\r") == "":
+            continue
+        fl = line.rstrip("\r").split(",")
+        where = f"read_sweep_csv: {path} line {line_no}"
+        if len(fl) != len(_SWEEP_HEADER):
+            raise InvalidArgument(where + ": wrong column count")
+        try:
+            cfg = RoutingConfig(routing_mode_from_string(fl[0]), int(fl[1]), int(fl[2]),
+                                float(fl[3]), int(fl[4]), int(fl[5]),
+                                cap_semantics_from_string(fl[6]))
+            pts.append(SweepPoint(cfg, float(fl[7]), float(fl[8]) if fl[8] else None,
+                                  int(fl[9]) != 0))
+        except (ValueError, InvalidArgument) as e:
+            raise InvalidArgument(f"{where}: {e}")
+    if not pts:
+        raise InvalidArgument(f"read_sweep_csv: {path} has no rows")
+    return pts

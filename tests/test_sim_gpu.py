@@ -101,3 +101,36 @@ def test_replay_and_writers(oea, tmp_path):
     missing = G.ScoreGenConfig(G.GenKind.Replay, steps=4, layers=2, trace_path=path)
     with pytest.raises(oea.InvalidArgument, match="no record for step 3 layer 0"):
         S.simulate_decode(missing, oea.RoutingConfig.vanilla(4), LAT)
+
+
+@needs_ref
+@pytest.mark.parametrize("rounding", [False, True])
+def test_sweep_matches_reference(oea, rounding):
+    gen = G.ScoreGenConfig(G.GenKind.Dirichlet, n_experts=64, batch=16, steps=4, layers=2,
+                           seed=17, alpha=0.3)
+    grid = S.default_sweep_grid(64, 8)
+    pts = S.sweep(gen, grid, LAT, S.RoundingRule(enabled=rounding))
+    want = oracle.Reference().sweep_default("dirichlet", 64, 16, 4, 2, 17, 8, LAT.a_us,
+                                            LAT.b_us, rounding, alpha=0.3)
+    assert len(pts) == len(want) == len(grid)
+    assert [p.mean_active_experts for p in pts] == want.tolist()
+    front = S.pareto_frontier(pts)
+    ref_idx = oracle.Reference().pareto_indices([p.mean_active_experts for p in pts],
+                                                [float("nan")] * len(pts))
+    assert sorted(S.pareto_indices(pts)) == sorted(ref_idx)
+    assert front[0].mean_active_experts == min(p.mean_active_experts for p in pts)
+
+
+def test_sweep_csv_round_trip(oea, tmp_path):
+    gen = G.ScoreGenConfig(G.GenKind.Dirichlet, n_experts=32, batch=8, steps=2, layers=1,
+                           seed=2, alpha=0.5)
+    pts = S.sweep(gen, S.default_sweep_grid(32, 4)[:20], LAT)
+    path = str(tmp_path / "sweep.csv")
+    S.write_sweep_csv(path, pts)
+    back = S.read_sweep_csv(path)
+    assert [(b.config, b.mean_active_experts, b.quality_delta) for b in back] == \
+           [(p.config, p.mean_active_experts, p.quality_delta) for p in pts]
+    bad = tmp_path / "bad.csv"
+    bad.write_text("mode,k\n")
+    with pytest.raises(oea.InvalidArgument, match="unexpected header"):
+        S.read_sweep_csv(str(bad))
