@@ -248,10 +248,11 @@ def main():
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c1", choices=["c1", "c2", "c3", "c4", "c5"],
+    ap.add_argument("--config", default="c1", choices=["c1", "c2", "c3", "c4", "c5", "sweep"],
                     help="c1 = the headline line (default); c2 = B x k0 sweep + latency fit; "
                          "c3 = Qwen3-235B-shaped layer; c4 = 94-layer EP stack (torchrun); "
-                         "c5 = router-only B=4096")
+                         "c5 = router-only B=4096; sweep = the 673-config routing sweep "
+                         "on the GPU simulator vs the reference's sweep on the host")
     ap.add_argument("--out-dir", default=os.path.join(ROOT, "gpurun_out", "bench"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -270,7 +271,8 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     env = {"torch": torch, "dist": dist, "rank": rank, "world": world, "local": local}
-    fn = {"c1": bench_c1, "c2": bench_c2, "c3": bench_c3, "c4": bench_c4, "c5": bench_c5}[args.config]
+    fn = {"c1": bench_c1, "c2": bench_c2, "c3": bench_c3, "c4": bench_c4, "c5": bench_c5,
+          "sweep": bench_sweep}[args.config]
     rc = fn(args, env)
     if dist is not None:
         dist.destroy_process_group()
@@ -526,6 +528,46 @@ def bench_c3(args, env):
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
+
+
+def bench_sweep(args, env):
+    """the default 673-config OEA sweep (sweep.cpp:48-106) of
+    Dirichlet(0.3) score batches (N=128, B=16, 8 steps x 4 layers) on the GPU
+    simulator (cells generated once on the device, one batched route per
+    config) vs the reference's sweep compiled in oracle/_ref (1 host thread,
+    cell by cell, + its vanilla shadow routes); the points are compared."""
+    import time
+    import numpy as np
+    torch, rank = env["torch"], env["rank"]
+    from paper_2511_02237_b200 import scoregen as G, sim as S
+    gen = G.ScoreGenConfig(G.GenKind.Dirichlet, n_experts=128, batch=16, steps=8, layers=4,
+                           seed=3, alpha=0.3)
+    lat = S.LatencyParams(0.05, 2.0)
+    grid = S.default_sweep_grid(128, K_TOP)
+    S.sweep(gen, grid[:4], lat)  # warm-up (contexts, workspaces)
+    t0 = time.perf_counter()
+    pts = S.sweep(gen, grid, lat)
+    gpu_s = time.perf_counter() - t0
+    line = {"metric": "default 673-config routing sweep, wall s (GPU simulator)", "value": gpu_s,
+            "unit": "s", "higher_is_better": False,
+            "config": {"workload": "sweep (SURVEY 8f-3)", "grid_points": len(grid), "N": 128,
+                       "B": 16, "steps": 8, "layers": 4, "scores": "dirichlet(0.3), device-generated"},
+            "routes": len(grid) * 32, "pareto_points": len(S.pareto_frontier(pts))}
+    try:
+        import oracle
+        if rank == 0 and oracle.reference_available():
+            t0 = time.perf_counter()
+            want = oracle.Reference().sweep_default("dirichlet", 128, 16, 8, 4, 3, K_TOP, 0.05,
+                                                    2.0, alpha=0.3)
+            line["cpu_baseline"] = {"value": time.perf_counter() - t0, "unit": "s", "cores": 1,
+                                    "kind": "reference",
+                                    "sample": "the same sweep: sweep.cpp over simulate_decode, 1 thread"}
+            line["points_identical"] = bool(np.array_equal(
+                np.array([p.mean_active_experts for p in pts]), want))
+    except Exception as e:  # the CPU baseline is reported, never required
+        line["cpu_baseline"] = {"value": None, "sample": f"failed: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
 
 
 def bench_c5(args, env):

@@ -144,8 +144,8 @@ int oea_route_f64(oea_ctx_t ctx, const double* scores_dev, const uint8_t* mask_d
  * replaces the per-record loop of the reference's `route` command
  * (oea_cli.cpp:153-175). Plan layout: sets/weights/set_len/phase1_* per row
  * as in oea_plan_view over sum(rows) rows; loads/active_union/base_union are
- * [R][N], active_count/total_load/base_union_count are [R]; order must be
- * NULL. One launch sequence for every configuration (the fast path when
+ * [R][N], active_count/total_load/base_union_count are [R]; every member is
+ * optional here (e.g. only active_count for a sweep) and order must be NULL. One launch sequence for every configuration (the fast path when
  * p == 1, max_p >= N, N <= 128; the general rank-sort path otherwise). */
 int oea_route_f64_batched_host(oea_ctx_t ctx, const double* scores, const uint8_t* mask,
                                const int32_t* rows, int32_t R, int32_t N,

@@ -813,12 +813,11 @@ int oea_route_f64_batched_host(oea_ctx_t ctx, const double* scores, const uint8_
   oea_routing_cfg rc;
   int r = resolve(ctx, cfg, N, &rc);
   if (r) return r;
-  if (plan == nullptr || plan->sets == nullptr || plan->set_len == nullptr)
-    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "route: plan sets/set_len are required");
+  if (plan == nullptr) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "route: null plan");
   if (plan->order != nullptr)
     return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "route_batched: order is not exported");
   const int stride = stride_of(rc);
-  if (plan->set_stride < stride)
+  if ((plan->sets || plan->weights || plan->weights_f32) && plan->set_stride < stride)
     return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "route: plan set_stride too small");
   if (N > kMaxRouteN)
     return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "route: N > " + std::to_string(kMaxRouteN));
@@ -902,7 +901,7 @@ int oea_route_f64_batched_host(oea_ctx_t ctx, const double* scores, const uint8_
   if (ps > stride) {  // pad the caller's wider rows
     for (int i = 0; i < B; ++i)
       for (int j = stride; j < ps; ++j) {
-        plan->sets[static_cast<size_t>(i) * ps + j] = -1;
+        if (plan->sets) plan->sets[static_cast<size_t>(i) * ps + j] = -1;
         if (plan->weights) plan->weights[static_cast<size_t>(i) * ps + j] = 0.0;
         if (plan->weights_f32) plan->weights_f32[static_cast<size_t>(i) * ps + j] = 0.0f;
       }

@@ -23,7 +23,7 @@ __all__ = [
     "RoutingMode", "CapSemantics", "RoutingConfig", "ScoreMatrix", "SortedExperts",
     "Phase1Result", "RoutingPlan", "BatchStats", "to_string", "routing_mode_from_string",
     "cap_semantics_from_string", "sort_experts", "route_topk", "phase1_baseline",
-    "phase2_piggyback", "route", "route_batched", "batch_stats", "plan_set_stride",
+    "phase2_piggyback", "route", "route_batched", "BatchedScores", "batch_stats", "plan_set_stride",
 ]
 
 
@@ -302,6 +302,38 @@ def route_batched(records, cfg: RoutingConfig) -> List[RoutingPlan]:
                                        weights[r0:r0 + b], loads[q], au[q], cnt[q], tot[q]))
         r0 += b
     return plans
+
+
+class BatchedScores:
+    """Records concatenated once for repeated batched routing (a config
+    sweep): route_counts(cfg) returns only each record's T and total load."""
+
+    def __init__(self, records):
+        sms = [_as_scores(r) for r in records]
+        if not sms:
+            raise InvalidArgument("route_batched: need R >= 1 records")
+        self.N = sms[0].experts()
+        if any(sm.experts() != self.N for sm in sms):
+            raise InvalidArgument("route_batched: inconsistent expert count")
+        self.rows = np.array([sm.batch() for sm in sms], np.int32)
+        self.scores = np.ascontiguousarray(np.concatenate([sm.scores for sm in sms], axis=0))
+        masked = any(sm.mask is not None for sm in sms)
+        self.mask = (np.concatenate([sm._mask_u8() if sm.mask is not None
+                                     else np.ones(sm.batch(), np.uint8) for sm in sms])
+                     if masked else None)
+
+    def route_counts(self, cfg: RoutingConfig):
+        R = len(self.rows)
+        cnt = np.zeros(R, np.int32)
+        tot = np.zeros(R, np.int64)
+        cfg.resolved(self.N)
+        pv = PlanViewC(0, None, None, None, None, None, None, _p(cnt), _p(tot), None, None, None,
+                       None, None)
+        ctx = default_context()
+        ctx.check(lib().oea_route_f64_batched_host(ctx.h, _p(self.scores), _p(self.mask),
+                                                   _p(self.rows), R, self.N,
+                                                   C.byref(cfg.to_c()), C.byref(pv)))
+        return cnt, tot
 
 
 def route_topk(scores, k: int) -> RoutingPlan:

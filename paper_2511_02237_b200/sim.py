@@ -384,14 +384,16 @@ def sweep(gen: ScoreGenConfig, grid: List[RoutingConfig], latency: LatencyParams
     points carry only T and the quality delta (none for score sources)."""
     if not grid:
         raise InvalidArgument("sweep: empty config grid")
+    from .routing import BatchedScores
     cfg, cells = cell_scores(gen)
+    batched = BatchedScores(cells)  # concatenated once; each config exports only T
     n = float(len(cells))
     pts = []
     for c in grid:
         rc = c.resolved(cfg.n_experts)
         s = 0.0
-        for p in route_batched(cells, rc):
-            s += p.active_count
+        for t in batched.route_counts(rc)[0].tolist():
+            s += t
         pt = SweepPoint(config=rc, mean_active_experts=s / n)
         if rounding.enabled:
             pt.mean_active_experts = _snap(pt.mean_active_experts, rounding.experts_bin)
