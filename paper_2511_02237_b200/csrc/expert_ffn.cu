@@ -601,6 +601,19 @@ __device__ __forceinline__ void fused_gemv(const FfnParams& P, float* red, int* 
   __syncthreads();
 }
 
+// HBM idles until the union is known: warm L2 with the first W1 stages of
+// every held expert (each is active with probability ~T/N; the stream reads
+// them as L2 hits, and its evict_first lines leave before these). Producer
+// warp, one 32 KiB prefetch per lane.
+__device__ __forceinline__ void prefetch_w1_heads(const FfnParams& P, int lane) {
+  const size_t per = static_cast<size_t>(P.Hp >> 3) * (P.Dp >> 4) * 512;  // W1 bytes per expert
+  const uint32_t nb = static_cast<uint32_t>(min(per, static_cast<size_t>(P.prefetch_bytes)));
+  for (int e = blockIdx.x; e < P.e_count; e += gridDim.x)
+    for (uint32_t o = 32u * 1024u * lane; o < nb; o += 32u * 32u * 1024u)
+      bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(P.w1) + e * per + o,
+                       min(32u * 1024u, nb - o));
+}
+
 // ---------------------------------------------------------------------------
 // Token-parallel rank routing (fused path). CTA t < B routes token t with one
 // thread per expert: every selection of routing.cpp is a RANK in the total
@@ -1256,22 +1269,18 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
       PR->set_len = reinterpret_cast<const int32_t*>(rs + RL.len);
       PR->wts = reinterpret_cast<const float*>(rs + RL.e);
     }
+    // (x in host memory: before the GEMV, inside the host round trip of
+    // the x staging, when HBM idles longest)
+    if (!kRouteOnly && P.x_stage && warp == kProducerWarp && P.prefetch_bytes > 0)
+      prefetch_w1_heads(P, lane);
     if (kRouteOnly)
       tile_gemv(P, SR.buf, tag);
     else
       fused_gemv(P, reinterpret_cast<float*>(rs + RL.red), claims + 3, tag);
     if (threadIdx.x == 0) stamp(P, 5);
-    // HBM idles until the union is known: warm L2 with the first W1 stages
-    // of every held expert (each is active with probability ~T/N; the stream
-    // reads them as L2 hits, evict_first lines leave before these)
-    if (!kRouteOnly && warp == kProducerWarp && P.prefetch_bytes > 0) {
-      const size_t per = static_cast<size_t>(P.Hp >> 3) * (P.Dp >> 4) * 512;  // W1 bytes per expert
-      const uint32_t nb = static_cast<uint32_t>(min(per, static_cast<size_t>(P.prefetch_bytes)));
-      for (int e = blockIdx.x; e < P.e_count; e += gridDim.x)
-        for (uint32_t o = 32u * 1024u * lane; o < nb; o += 32u * 32u * 1024u)
-          bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(P.w1) + e * per + o,
-                           min(32u * 1024u, nb - o));
-    }
+    // (x in device memory: after the GEMV, whose loads it would delay)
+    if (!kRouteOnly && !P.x_stage && warp == kProducerWarp && P.prefetch_bytes > 0)
+      prefetch_w1_heads(P, lane);
     // R1: CTA t routes token t (thread per expert), then the union barrier
     if (threadIdx.x < 128) {
 #pragma unroll 1
