@@ -434,7 +434,7 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   const bool shard = L->n_local < L->N;
   const bool fused = part == 0 && fused_ok(L, B, rc) &&
                      (shard || getenv("OEA_TWO_KERNEL") == nullptr) &&
-                     oea_host::ffn_bf16_smem_bytes() +
+                     oea_host::ffn_bf16_smem_bytes() + oea_host::ffn_btile_bytes() +
                              oea_host::ffn_route_smem_bytes(B, L->Np, stride) <= 227 * 1024;
   // Large batches (64 < B <= 256) with the rank-routing conditions: a
   // route-only launch of the fused prologue (tensor-core gate GEMV, rank

@@ -106,7 +106,7 @@ struct FfnParams {
 // shared-memory copy when the FFN routes in its prologue). Kept in shared
 // memory and read where needed so they do not occupy registers in the
 // consumer loop (the kernel runs at its 168-register cap).
-struct PlanRef {
+struct alignas(16) PlanRef {  // (16-byte multiple: the shared-memory tables follow it)
   const int32_t* row_tok;
   const int32_t* row_slot;
   const int32_t* group_a;
@@ -114,6 +114,7 @@ struct PlanRef {
   const int32_t* group_rows;
   const int32_t* set_len;
   const float* wts;
+  uint8_t* btile;  // token-list units with >= 2 n-blocks: shared B-operand stage tiles
   int G;
 };
 
@@ -132,7 +133,23 @@ struct Unit {
   int row0;    // first padded row of the group
   int rows;    // real rows (tokens) in the group
   int ready;   // W2: the group's h is known complete (acquired by the producer)
+  int nw;      // warps with a unit in this round (they share the B tile)
 };
+
+// Shared B-operand tiles (token-list units with >= 2 n-blocks): the 8 units
+// of a round are 8 row blocks of ONE expert, so they multiply the same token
+// rows. Instead of every warp loading those rows from L2 per stage (8x the
+// L2 traffic: ~13 TB/s of L2 reads at B=256, the bound of that path), the
+// round's warps cp.async each stage's [rows][128-wide K slice] tile once into
+// shared memory, 2 stages ahead (3 buffers, one named barrier per stage).
+// Layout: row r at r * 256 B; 16-byte chunk c stored at c ^ (c[3] << 1) ^ r[0]
+// so the 8 lanes of an LDS.128 phase (2 rows x 4 quads) hit 8 bank groups.
+constexpr int kBTileRows = 64;                   // 8 n-blocks
+constexpr int kBTileBuf = kBTileRows * 256;      // one stage slice
+constexpr int kBTileBytes = 3 * kBTileBuf;
+__device__ __forceinline__ int btile_chunk(int c, int r) {
+  return c ^ (((c >> 3) & 1) << 1) ^ (r & 1);
+}
 
 // Shared-memory x tile of the dense path: 16 token rows of Dp bf16, row
 // stride Dp*2 + 32 bytes; inside every 256-byte K slice (one stage) the 16
@@ -163,6 +180,7 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
   // dense W1: B operand = all B tokens from the swizzled shared-memory x tile;
   // dense W2: token lists as usual, h rows at [group][token] (written by W1)
   constexpr bool XSM = DENSE && W1;
+  constexpr bool SHB = !DENSE && !SPLIT && NB >= 2;  // shared B tile
 
   // B-operand rows (uint4 view) for this lane's token in each n-block. The
   // weights are packed with the k-permutation of layer.cu (kperm): in every
@@ -177,7 +195,9 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
   for (int nb = 0; nb < NB; ++nb) {
     const int r = nb * 8 + g;
     bp[nb] = nullptr;
-    if (XSM) {
+    if (SHB) {
+      // (rows come from the shared tile)
+    } else if (XSM) {
       // token r; the per-quarter chunk offsets are added at the load
       bp[nb] = reinterpret_cast<const uint4*>(xs + r * P.xs_row);
     } else if (r < U.rows) {
@@ -219,6 +239,29 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
   int xoff[4];
 #pragma unroll
   for (int jj = 0; jj < 4; ++jj) xoff[jj] = xs_chunk(4 * q + jj) * 16;
+  // shared B tile: this warp's slice of the round's tile loads (chunk k of
+  // stage slice s: row k / 16, 16-byte chunk k % 16), one commit group each
+  const bool math = P.mode != 1;
+  const int nthr = U.nw * 32, ctid = warp * 32 + lane;
+  auto issue_tile = [&](int s, int buf) {
+    uint8_t* dst0 = PR->btile + buf * kBTileBuf;
+    for (int k = ctid; k < U.rows * 16; k += nthr) {
+      const int r = k >> 4, c = k & 15;
+      const __nv_bfloat16* row =
+          W1 ? P.xpad + static_cast<size_t>(PR->row_tok[U.row0 + r]) * P.Dp
+             : P.hbuf + static_cast<size_t>(U.row0 + r) * P.Hp;
+      cp_async16(smem_u32(dst0 + r * 256 + btile_chunk(c, r) * 16),
+                 reinterpret_cast<const uint8_t*>(row) + s * 256 + c * 16, 16);
+    }
+    cp_async_commit();
+  };
+  int boff[4];  // this lane's chunk offsets (row g of an n-block; n-block nb adds nb * 2 KiB)
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) boff[jj] = g * 256 + btile_chunk(4 * q + jj, g) * 16;
+  if (SHB && math) {
+    issue_tile(0, 0);
+    if (nst > 1) issue_tile(1, 1);
+  }
   // One n-block (global B): the next stage's 4 loads are issued right after
   // the current stage is consumed, so their latency hides behind the stage
   // barrier wait (two n-blocks measured slower: spills at the register cap).
@@ -228,7 +271,6 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
   // slices of this unit (K / 128); SPLIT: this warp's slice of split-stage s
   const int nslices = (W1 ? P.Dp : P.Hp) >> 7;
   uint4 bpre[PB][4];
-  const bool math = P.mode != 1;
   if (kPref && math)
 #pragma unroll
     for (int nb = 0; nb < PB; ++nb)
@@ -236,6 +278,16 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
       for (int i = 0; i < 4; ++i) bpre[nb][i] = ldb(bp[nb] == nullptr ? nullptr : bp[nb] + i);
 
   for (int s0 = 0; s0 < nst; ++s0) {
+    if (SHB && math) {
+      // tile s0 landed for every warp of the round (and every warp is past
+      // stage s0 - 1, so buffer (s0 + 2) % 3 is free for the prefetch)
+      if (s0 + 1 < nst)
+        cp_async_wait_group<1>();
+      else
+        cp_async_wait_group<0>();
+      asm volatile("bar.sync 5, %0;" ::"r"(nthr) : "memory");
+      if (s0 + 2 < nst) issue_tile(s0 + 2, (s0 + 2) % 3);
+    }
     mbar_wait(&full[stage], phase);
     const int s = SPLIT ? s0 * kFfnWarps + warp : s0;  // K slice of this stage for this warp
     const uint4* tiles =
@@ -263,7 +315,9 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
           uint4 v[NB];
 #pragma unroll
           for (int nb = 0; nb < NB; ++nb) {
-            if (XSM)
+            if (SHB)
+              v[nb] = lds128(PR->btile + (s0 % 3) * kBTileBuf + nb * 2048 + boff[jj]);
+            else if (XSM)
               v[nb] = lds128(reinterpret_cast<const uint8_t*>(bp[nb]) + s * 256 + xoff[jj]);
             else
               v[nb] = ldb(bp[nb] == nullptr ? nullptr : bp[nb] + s * 16 + jj);
@@ -1237,9 +1291,10 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
   PlanRef* PR = reinterpret_cast<PlanRef*>(rdesc + kRoundRing);
   uint8_t* rs = reinterpret_cast<uint8_t*>(PR + 1) + 16;
   const RouteSmem RL = route_smem_layout(P.B, P.Np, P.stride);
-  uint8_t* xs = rs + RL.total;  // dense path: x tile (16 B aligned)
+  uint8_t* xs = rs + (kFused ? RL.total : 0);  // dense path: x tile (16 B aligned)
   SplitRed SR;
   SR.buf = reinterpret_cast<float*>(xs + (kDense ? 16 * P.xs_row : 0));
+  uint8_t* btile = reinterpret_cast<uint8_t*>(SR.buf) + kSplitRedBytes;  // (token-list modes)
   SR.free = plan_bar + 1;
   SR.idx = nullptr;
   int sidx = 0;  // split rounds consumed by this warp
@@ -1268,6 +1323,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
       PR->group_rows = reinterpret_cast<const int32_t*>(rs + RL.rows);
       PR->set_len = reinterpret_cast<const int32_t*>(rs + RL.len);
       PR->wts = reinterpret_cast<const float*>(rs + RL.e);
+      PR->btile = btile;
     }
     // (x in host memory: before the GEMV, inside the host round trip of
     // the x staging, when HBM idles longest)
@@ -1310,6 +1366,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
     PR->group_rows = P.group_rows;
     PR->set_len = P.set_len;
     PR->wts = P.wts;
+    PR->btile = btile;
     PR->G = P.hdr->n_groups;
   }
   __syncthreads();
@@ -1519,6 +1576,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
         U.rows = PR->group_rows[U.g];
       }
       U.ready = d.ready;
+      U.nw = d.n;
       const int nbk = (U.rows + 7) >> 3;
       if (sp) {
         if (is1)
@@ -1744,6 +1802,7 @@ size_t ffn_bf16_smem_bytes() {
   return kStages * kStageBytes + 2 * kStages * sizeof(uint64_t) + kRoundRing * sizeof(RoundDesc) +
          sizeof(PlanRef) + 16 + kSplitRedBytes;
 }
+size_t ffn_btile_bytes() { return kBTileBytes; }
 
 size_t ffn_route_smem_bytes(int B, int Np, int stride) {
   return route_smem_layout(B, Np, stride).total;
@@ -1819,7 +1878,8 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
 
   const size_t smem = ffn_bf16_smem_bytes() +
                       (fb.fused ? ffn_route_smem_bytes(B, L->Np, stride) : 0) +
-                      (fb.dense ? ffn_dense_xs_bytes(L->Dp) : 0);
+                      (fb.dense ? ffn_dense_xs_bytes(L->Dp) : 0) +
+                      (fb.dense || fb.route_only ? 0 : ffn_btile_bytes());
   const int mode = fb.route_only ? 3 : fb.dense ? 2 : fb.fused ? 1 : 0;
   auto kern = mode == 3 ? k_ffn_bf16<3>
                         : mode == 2 ? k_ffn_bf16<2> : mode == 1 ? k_ffn_bf16<1> : k_ffn_bf16<0>;

@@ -237,6 +237,7 @@ int gen_scores_launch(oea_ctx* ctx, const oea_score_gen_cfg& c, int step0, int n
                       double* out, cudaStream_t s);
 size_t ffn_params_bytes();
 void ffn_params_set_io(void* params, const void* x_in, void* out);
+size_t ffn_btile_bytes();
 size_t ffn_dense_xs_bytes(int Dp);
 int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride,
                     const FfnBuffers& fb, bool pdl, cudaStream_t s);
