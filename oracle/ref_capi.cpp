@@ -556,4 +556,32 @@ int ref_pareto_indices(const double* t, const double* q, int n, int32_t* out, in
   })
 }
 
+// simulate_decode(layer, gen, ...) (simulate.cpp:153-183) on
+// make_random_layer({D, H, N}, layer_seed): T / load / latency and the
+// divergence per record, plus the vanilla records' T.
+int ref_simulate_decode_layer(int D, int H, int N, uint64_t layer_seed, const int32_t* gi,
+                              uint64_t seed, const double* gd, int mode, int k, int k0, double p,
+                              int k_max, int max_p, int cap, double a_us, double b_us,
+                              int32_t* T, int64_t* load, double* lat, double* div, int32_t* vT,
+                              double* mean_div) {
+  REF_GUARD({
+    LayerDims dims;
+    dims.embed = D;
+    dims.hidden = H;
+    dims.experts = N;
+    const auto layer = make_random_layer(dims, layer_seed);
+    const auto tr = simulate_decode(layer, gen_cfg(gi, seed, gd),
+                                    make_cfg(mode, k, k0, p, k_max, max_p, cap),
+                                    LatencyParams{a_us, b_us}, 1);
+    for (size_t i = 0; i < tr.records.size(); ++i) {
+      T[i] = tr.records[i].active_experts;
+      load[i] = tr.records[i].total_load;
+      lat[i] = tr.records[i].modeled_latency_us;
+      div[i] = tr.records[i].divergence.value_or(-1.0);
+      vT[i] = tr.vanilla_records[i].active_experts;
+    }
+    *mean_div = tr.aggregates.mean_divergence.value_or(-1.0);
+  })
+}
+
 }  // extern "C"

@@ -31,7 +31,7 @@ __all__ = ["LatencyParams", "StepRecord", "TraceAggregates", "DecodeTrace", "exp
            "padding_experiment", "write_trace_csv", "write_trace_summary_json",
            "write_padding_json", "gen_config_json", "cell_scores", "RoundingRule", "SweepPoint",
            "default_sweep_grid", "sweep", "pareto_indices", "pareto_frontier", "write_sweep_csv",
-           "read_sweep_csv"]
+           "read_sweep_csv", "simulate_decode_layer"]
 
 
 @dataclass
@@ -376,7 +376,7 @@ def _snap(v: float, b: float) -> float:
 
 
 def sweep(gen: ScoreGenConfig, grid: List[RoutingConfig], latency: LatencyParams,
-          rounding: RoundingRule = RoundingRule()) -> List[SweepPoint]:
+          rounding: RoundingRule = RoundingRule(), layer=None) -> List[SweepPoint]:
     """sweep.cpp:77-106 for a score source: mean T per routing config. The
     cells are generated once (one launch) and each config routes all of them
     in one batched call; the reference re-simulates (and shadow-routes
@@ -384,6 +384,19 @@ def sweep(gen: ScoreGenConfig, grid: List[RoutingConfig], latency: LatencyParams
     points carry only T and the quality delta (none for score sources)."""
     if not grid:
         raise InvalidArgument("sweep: empty config grid")
+    if layer is not None:  # quality = mean output divergence vs vanilla (sweep.cpp:88-99)
+        pts = []
+        for c in grid:
+            tr = simulate_decode_layer(layer, gen, c, latency)
+            pt = SweepPoint(config=tr.routing, mean_active_experts=tr.aggregates.mean_active_experts,
+                            quality_delta=tr.aggregates.mean_divergence)
+            if rounding.enabled:
+                pt.mean_active_experts = _snap(pt.mean_active_experts, rounding.experts_bin)
+                if pt.quality_delta is not None:
+                    pt.quality_delta = _snap(pt.quality_delta, rounding.quality_bin)
+                pt.rounded = True
+            pts.append(pt)
+        return pts
     from .routing import BatchedScores
     cfg, cells = cell_scores(gen)
     batched = BatchedScores(cells)  # concatenated once; each config exports only T
@@ -474,3 +487,42 @@ def read_sweep_csv(path: str) -> List[SweepPoint]:
     if not pts:
         raise InvalidArgument(f"read_sweep_csv: {path} has no rows")
     return pts
+
+
+# ---------------------------------------------------------------------------
+# Toy-layer simulation (simulate.cpp:153-183): the layer's own router scores
+# per-(step, layer, token) embeddings, and every record also carries the mean
+# relative divergence of the routed output from the vanilla top-k mixture.
+# ---------------------------------------------------------------------------
+def simulate_decode_layer(layer, gen: ScoreGenConfig, routing: RoutingConfig,
+                          latency: LatencyParams) -> DecodeTrace:
+    """simulate_decode(layer, gen, routing, latency): `layer` is a
+    DeviceMoeLayer (f64 / f32) or host MoeLayerParams; gen supplies batch,
+    steps, layers and seed (gen.kind is ignored). Router scores, both routes
+    (one batched call each for all cells) and both moe_forward mixtures run on
+    the GPU."""
+    from .moe_layer import DeviceMoeLayer, MoeLayerParams, _flat_plan, make_random_batch, \
+        output_divergence
+    if gen.batch < 1 or gen.steps < 1 or gen.layers < 1:
+        raise InvalidArgument("simulate_decode: batch, steps and layers must be >= 1")
+    dev = DeviceMoeLayer.from_params(layer) if isinstance(layer, MoeLayerParams) else layer
+    if gen.n_experts != dev.N:
+        raise InvalidArgument(f"simulate_decode: gen.n_experts {gen.n_experts} does not match "
+                              f"layer expert count {dev.N}")
+    rcfg = routing.resolved(dev.N)
+    vcfg = RoutingConfig.vanilla(routing.k).resolved(dev.N)
+    cells = [(s, l) for s in range(gen.steps) for l in range(gen.layers)]
+    xs = [make_random_batch(gen.batch, dev.D, gen.seed, s, l).embeddings for s, l in cells]
+    scores = [ScoreMatrix(dev.router_scores(x)) for x in xs]
+    plans = route_batched(scores, rcfg)
+    vplans = route_batched(scores, vcfg)
+    tr = DecodeTrace(routing=rcfg)
+    for (s, l), x, p, vp in zip(cells, xs, plans, vplans):
+        ref = dev.forward_plan(x, *_flat_plan(vp))
+        got = dev.forward_plan(x, *_flat_plan(p))
+        rec = _record(s, l, p, latency)
+        rec.divergence = output_divergence(ref, got).mean_relative_error
+        tr.records.append(rec)
+        tr.vanilla_records.append(_record(s, l, vp, latency))
+    tr.aggregates = _aggregates(tr.records, tr.vanilla_records)
+    return tr

@@ -134,3 +134,35 @@ def test_sweep_csv_round_trip(oea, tmp_path):
     bad.write_text("mode,k\n")
     with pytest.raises(oea.InvalidArgument, match="unexpected header"):
         S.read_sweep_csv(str(bad))
+
+
+@needs_ref
+@pytest.mark.parametrize("cfg_name", ["simplified", "oea"])
+def test_toy_layer_simulation_matches_reference(oea, cfg_name):
+    # simulate.cpp:153-183 on make_random_layer({64, 96, 16}, 7): routed T /
+    # load / latency identical, divergence vs vanilla within fp64 rounding
+    cfg = {"simplified": oea.RoutingConfig.simplified(2, 4),
+           "oea": oea.RoutingConfig.oea(1, 0.6, 4, 16, 4)}[cfg_name]
+    layer = oea.DeviceMoeLayer(64, 96, 16, dtype="f64")
+    layer.init_random(7)
+    gen = G.ScoreGenConfig(G.GenKind.Dirichlet, n_experts=16, batch=6, steps=3, layers=2, seed=5)
+    tr = S.simulate_decode_layer(layer, gen, cfg, LAT)
+    T_, ld, lat, dv, vT, md = oracle.Reference().simulate_decode_layer(
+        64, 96, 16, 7, 6, 3, 2, 5, cfg, LAT.a_us, LAT.b_us)
+    assert [r.active_experts for r in tr.records] == T_.tolist()
+    assert [r.total_load for r in tr.records] == ld.tolist()
+    assert [r.modeled_latency_us for r in tr.records] == lat.tolist()
+    assert [r.active_experts for r in tr.vanilla_records] == vT.tolist()
+    got = np.array([r.divergence for r in tr.records])
+    assert np.allclose(got, dv, rtol=1e-9, atol=1e-12)
+    assert abs(tr.aggregates.mean_divergence - md) <= 1e-9 * max(md, 1e-12)
+
+
+def test_sweep_with_layer_reports_quality(oea):
+    layer = oea.DeviceMoeLayer(64, 96, 16, dtype="f64")
+    layer.init_random(3)
+    gen = G.ScoreGenConfig(G.GenKind.Dirichlet, n_experts=16, batch=4, steps=2, layers=1, seed=1)
+    grid = S.default_sweep_grid(16, 4)[:6]
+    pts = S.sweep(gen, grid, LAT, layer=layer)
+    assert pts[0].config.mode == oea.RoutingMode.Vanilla and pts[0].quality_delta == 0.0
+    assert all(p.quality_delta is not None and p.quality_delta >= 0.0 for p in pts)
