@@ -119,10 +119,12 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU baseline: the reference itself (oracle/_ref) or the C port.
 # ---------------------------------------------------------------------------
-def cpu_reference_decode(calls: int, threads: int, cfg_tuple):
+def cpu_reference_decode(calls: int, threads: int, cfg_tuple, steps: int = 1, warmup: int = 0):
     """Times the reference CPU decode cell (router_scores -> route ->
     moe_forward<double>, moe_layer.hpp:71-158 + routing.cpp:305-326) on a
-    make_random_layer C1 layer. Returns (us_per_call, kind, cores, sample)."""
+    make_random_layer C1 layer (built once): `warmup` untimed steps, then
+    `steps` timed steps of `calls` decode calls each on `threads` host
+    threads. Returns (per-step us per call list, kind, cores, sample)."""
     import numpy as np
 
     import oracle
@@ -139,33 +141,38 @@ def cpu_reference_decode(calls: int, threads: int, cfg_tuple):
             plan = oracle.route(oracle.router_scores(x, router), cfg_tuple)
             return oracle.moe_forward(wg, wu, wd, x, plan.sets, plan.set_len, plan.weights)
     run(xs[0])  # warm caches / page in
-    t0 = time.perf_counter()
-    if threads <= 1:
-        for x in xs:
-            run(x)
-    else:
-        idx = list(range(calls))
-        lock = threading.Lock()
 
-        def worker():
-            while True:
-                with lock:
-                    if not idx:
-                        return
-                    i = idx.pop()
-                run(xs[i])
-        ths = [threading.Thread(target=worker) for _ in range(threads)]
-        for t in ths:
-            t.start()
-        for t in ths:
-            t.join()
-    dt = time.perf_counter() - t0
-    us = dt * 1e6 / calls
-    sample = (f"{calls} C1 decode calls (B=16, D=2048, H=768, N=128, simplified k0=4/k=8): "
-              f"router_scores + route + moe_forward<double> of the "
+    def one_step():
+        t0 = time.perf_counter()
+        if threads <= 1:
+            for x in xs:
+                run(x)
+        else:
+            idx = list(range(calls))
+            lock = threading.Lock()
+
+            def worker():
+                while True:
+                    with lock:
+                        if not idx:
+                            return
+                        i = idx.pop()
+                    run(xs[i])
+            ths = [threading.Thread(target=worker) for _ in range(threads)]
+            for t in ths:
+                t.start()
+            for t in ths:
+                t.join()
+        return (time.perf_counter() - t0) * 1e6 / calls
+
+    for _ in range(warmup):
+        one_step()
+    vals = [one_step() for _ in range(max(1, steps))]
+    sample = (f"{calls} C1 decode calls per step (B=16, D=2048, H=768, N=128, simplified "
+              f"k0=4/k=8): router_scores + route + moe_forward<double> of the "
               f"{'reference sources compiled with the Eigen-subset shim (-O3)' if kind == 'reference' else 'C restatement'}"
               f", {threads} thread(s)")
-    return us, kind, threads, sample
+    return vals, kind, threads, sample
 
 
 def run_reference_arm(args):
@@ -175,13 +182,12 @@ def run_reference_arm(args):
     threads = os.cpu_count() or 1
     calls = max(threads, 4)
     cfg = (3, K_TOP, K0, 1.0, K_TOP, 0, 0)  # simplified(4, 8)
-    vals = []
-    for _ in range(max(1, min(args.steps, 3))):
-        us, kind, cores, sample = cpu_reference_decode(calls, threads, cfg)
-        vals.append(us)
-    us = statistics.median(vals)
+    # each step: one call per host thread (~0.5 s); the layer is built once
+    vals, kind, cores, sample = cpu_reference_decode(calls, threads, cfg, steps=args.steps,
+                                                     warmup=args.warmup)
+    us = statistics.mean(vals)
     line = {"impl": "reference", "metric": METRIC, "value": us, "unit": "us/layer-call",
-            "n_gpus": args.gpus, "steps": len(vals), "warmup": 1, "ms_per_step": us / 1000.0,
+            "n_gpus": args.gpus, "steps": len(vals), "warmup": args.warmup, "ms_per_step": us / 1000.0,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: make_random_layer weights, make_random_batch tokens",
             "config": {"workload": "C1 Qwen3-30B-A3B-shaped MoE decode layer, CPU reference",
@@ -395,7 +401,8 @@ def bench_c1(args, env):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            us_cpu, kind, cores, sample = cpu_reference_decode(3, 1, (3, K_TOP, K0, 1.0, K_TOP, 0, 0))
+            vals, kind, cores, sample = cpu_reference_decode(3, 1, (3, K_TOP, K0, 1.0, K_TOP, 0, 0))
+            us_cpu = vals[0]
             cpu = {"value": us_cpu, "unit": "us/layer-call", "cores": cores, "kind": kind,
                    "sample": sample}
         except Exception as e:  # the CPU baseline is reported, never required
