@@ -182,6 +182,8 @@ struct HostGraph {
   cudaKernelNodeParams kp{};
   std::vector<unsigned char> params;  // the node's FfnParams, patched per call
   void* args[1] = {nullptr};
+  const void* x_set = nullptr;  // x / out the exec node currently points at
+  void* out_set = nullptr;
   uint64_t used = 0;
 };
 
@@ -1315,11 +1317,15 @@ int decode_host_graph(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* xd, 
     h = &ex->host_graphs.back();
   }
   h->used = ++ex->host_graph_clock;
-  oea_host::ffn_params_set_io(h->params.data(), xd, od);
-  h->args[0] = h->params.data();
-  h->kp.kernelParams = h->args;
-  h->kp.extra = nullptr;
-  OEA_CUDA_TRY(ctx, cudaGraphExecKernelNodeSetParams(h->exec, h->node, &h->kp));
+  if (xd != h->x_set || od != h->out_set) {  // serving loops reuse their pinned buffers
+    oea_host::ffn_params_set_io(h->params.data(), xd, od);
+    h->args[0] = h->params.data();
+    h->kp.kernelParams = h->args;
+    h->kp.extra = nullptr;
+    OEA_CUDA_TRY(ctx, cudaGraphExecKernelNodeSetParams(h->exec, h->node, &h->kp));
+    h->x_set = xd;
+    h->out_set = od;
+  }
   OEA_CUDA_TRY(ctx, cudaGraphLaunch(h->exec, s));
   OEA_LAUNCHED(ctx);
   return OEA_OK;

@@ -241,10 +241,10 @@ class DeviceMoeLayer:
     def decode_host_ptr(self, x_ptr: int, out_ptr: int, B: int, cfg: RoutingConfig, mask_ptr=None):
         """End-to-end decode from raw host pointers (e.g. pinned torch tensors):
         H2D of x, the fused decode, D2H of out, synchronise (oea_moe_decode_host)."""
-        self.ctx.check(lib().oea_moe_decode_host(self.ctx.h, self.h, C.c_void_p(x_ptr),
-                                                 C.c_void_p(mask_ptr) if mask_ptr else None,
-                                                 int(B), C.byref(cfg.to_c()),
-                                                 C.c_void_p(out_ptr)))
+        rc = lib().oea_moe_decode_host(self.ctx.h, self.h, x_ptr, mask_ptr or None, B,
+                                       cfg.c_ref(), out_ptr)
+        if rc:
+            self.ctx.check(rc)
 
     def graph(self, x, cfg: RoutingConfig, out, mask=None) -> DecodeGraph:
         g = C.c_void_p()

@@ -69,6 +69,9 @@ def cap_semantics_from_string(s: str) -> CapSemantics:
     raise InvalidArgument("unknown cap semantics: " + s)
 
 
+_C_CFG_CACHE: dict = {}
+
+
 @dataclass
 class RoutingConfig:
     """routing.hpp:56-76 (field for field, same defaults)."""
@@ -100,6 +103,17 @@ class RoutingConfig:
     def to_c(self) -> RoutingCfgC:
         return RoutingCfgC(int(self.mode), int(self.k), int(self.k0), float(self.p),
                            int(self.k_max), int(self.max_p), int(self.cap))
+
+    def c_ref(self):
+        """A byref() of this config's C struct, cached by value (hot host
+        paths call the C ABI once per decode)."""
+        key = (int(self.mode), int(self.k), int(self.k0), float(self.p), int(self.k_max),
+               int(self.max_p), int(self.cap))
+        hit = _C_CFG_CACHE.get(key)
+        if hit is None:
+            c = RoutingCfgC(*key)
+            hit = _C_CFG_CACHE[key] = (c, C.byref(c))
+        return hit[1]
 
     @staticmethod
     def from_c(c: RoutingCfgC) -> "RoutingConfig":
