@@ -168,6 +168,12 @@ int oea_phase2_f64_host(oea_ctx_t ctx, const uint8_t* mask, int32_t B, int32_t N
                         const int32_t* base_union, int32_t base_union_count,
                         const oea_routing_cfg* cfg, const oea_plan_view* plan);
 
+/* Decoder glue between stacked MoE layers (the C4 stack, attention omitted):
+ * h += add (when add != NULL), then x = bf16(h * rsqrt(mean(h^2) + eps)) per
+ * row; h, add: [rows][D] fp32 device, x: [rows][D] bf16 device. One launch. */
+int oea_residual_rmsnorm(oea_ctx_t ctx, float* h, const float* add, void* x_bf16, int32_t rows,
+                         int32_t D, double eps, void* stream);
+
 /* ---- router-score generators (score_gen.cpp:100-160) ----------------------
  * ScoreSource batches on the device: Dirichlet(alpha) rows (Marsaglia-Tsang
  * gammas over the counter RNG) or clustered rows (softmax of group template +

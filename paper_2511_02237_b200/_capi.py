@@ -84,6 +84,7 @@ def lib():
                 "oea_route_f64": [vp, vp, vp, i32, i32, vp, vp, vp],
                 "oea_route_f64_batched_host": [vp, vp, vp, vp, i32, i32, vp, vp],
                 "oea_gen_scores": [vp, vp, i32, i32, vp, vp],
+                "oea_residual_rmsnorm": [vp, vp, vp, vp, i32, i32, C.c_double, vp],
                 "oea_gen_scores_host": [vp, vp, i32, i32, vp],
                 "oea_sort_experts_f64_host": [vp, vp, i32, i32, vp],
                 "oea_phase1_f64_host": [vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, i32, vp, vp],
@@ -123,7 +124,7 @@ EXPORTED = (
     "oea_abi_version", "oea_ctx_create", "oea_ctx_destroy", "oea_last_error", "oea_ctx_stream",
     "oea_ctx_synchronize", "oea_ctx_kernel_launches", "oea_config_resolve",
     "oea_plan_set_stride", "oea_route_f64_host", "oea_route_f64", "oea_route_f64_batched_host",
-    "oea_gen_scores", "oea_gen_scores_host",
+    "oea_gen_scores", "oea_gen_scores_host", "oea_residual_rmsnorm",
     "oea_sort_experts_f64_host",
     "oea_phase1_f64_host", "oea_phase2_f64_host", "oea_layer_create", "oea_layer_destroy",
     "oea_layer_upload_router", "oea_layer_upload_expert", "oea_layer_init_random",

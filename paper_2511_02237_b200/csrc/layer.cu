@@ -433,3 +433,49 @@ int layer_download_expert(oea_layer* L, int e, void* wg, void* wu, void* wd, int
 }
 
 }  // namespace oea_host
+
+// ---------------------------------------------------------------------------
+// Residual + RMSNorm between stacked MoE layers (the decoder glue of the C4
+// stack: h += moe(x); x' = bf16(h * rsqrt(mean(h^2) + eps))), one CTA per
+// token row, fixed-order block reduction (deterministic). add == null: only
+// the normalisation (the stack's first layer).
+// ---------------------------------------------------------------------------
+namespace oea_dev {
+__global__ void __launch_bounds__(256)
+    k_residual_rmsnorm(float* __restrict__ h, const float* __restrict__ add,
+                       __nv_bfloat16* __restrict__ x, int D, float eps) {
+  __shared__ float part[8];
+  const size_t row = static_cast<size_t>(blockIdx.x) * D;
+  float ss = 0.0f;
+  for (int d = threadIdx.x; d < D; d += 256) {
+    float v = h[row + d];
+    if (add) {
+      v += add[row + d];
+      h[row + d] = v;
+    }
+    ss = fmaf(v, v, ss);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.0f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) tot += part[w];
+  const float scale = rsqrtf(tot / static_cast<float>(D) + eps);
+  for (int d = threadIdx.x; d < D; d += 256) x[row + d] = __float2bfloat16_rn(h[row + d] * scale);
+}
+}  // namespace oea_dev
+
+int oea_residual_rmsnorm(oea_ctx_t ctx, float* h, const float* add, void* x_bf16, int32_t rows,
+                         int32_t D, double eps, void* stream) {
+  if (ctx == nullptr) return oea_set_error(nullptr, OEA_ERR_INVALID_ARGUMENT, "null context");
+  if (h == nullptr || x_bf16 == nullptr || rows < 1 || D < 1)
+    return oea_set_error(ctx, OEA_ERR_INVALID_ARGUMENT, "residual_rmsnorm: bad arguments");
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  oea_dev::k_residual_rmsnorm<<<rows, 256, 0, s>>>(h, add, static_cast<__nv_bfloat16*>(x_bf16), D,
+                                                   static_cast<float>(eps));
+  OEA_LAUNCHED(ctx);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? OEA_OK : oea_check_cuda(ctx, e, "k_residual_rmsnorm");
+}

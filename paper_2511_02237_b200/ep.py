@@ -80,8 +80,7 @@ class ExpertParallelMoE:
         if partial is None:
             partial = torch.empty((B, D), dtype=torch.float32, device=x_local.device)
         if self.world == 1:
-            x_all.copy_(x_local)
-            self.partial_fn(x_all, out_local)
+            self.partial_fn(x_local, out_local)  # the whole batch is local
             return out_local
         self.dist.all_gather_into_tensor(x_all, x_local.contiguous(), group=self.group)
         self.partial_fn(x_all, partial)
@@ -95,8 +94,28 @@ def residual_stack_forward(layers: List[ExpertParallelMoE], h_local, out_local,
     """A decode step through a pre-norm residual stack of EP MoE layers (the
     MoE half of a Qwen3 decoder layer, attention omitted): for each layer
     x = RMSNorm(h) (bf16), h += moe(x). h_local [B/P, D] fp32 is updated in
-    place; keeps activations at unit scale through any depth."""
+    place; keeps activations at unit scale through any depth. On the GPU the
+    residual add and the next layer's RMSNorm are one fused launch
+    (oea_residual_rmsnorm); elsewhere (CPU tests) plain torch ops."""
     import torch
+    if h_local.is_cuda:
+        import ctypes as C
+        from ._capi import default_context, lib
+        from .moe_layer import torch_stream
+        ctx = default_context()
+        rows, D = h_local.shape
+        x = torch.empty((rows, D), dtype=torch.bfloat16, device=h_local.device)
+        st = C.c_void_p(torch_stream())
+        ctx.check(lib().oea_residual_rmsnorm(ctx.h, h_local.data_ptr(), None, x.data_ptr(), rows,
+                                             D, eps, st))
+        for i, L in enumerate(layers):
+            L.forward(x, out_local, **(bufs or {}))
+            if i + 1 < len(layers):
+                ctx.check(lib().oea_residual_rmsnorm(ctx.h, h_local.data_ptr(), out_local.data_ptr(),
+                                                     x.data_ptr(), rows, D, eps, st))
+            else:
+                h_local.add_(out_local)
+        return h_local
     for L in layers:
         x = (h_local * torch.rsqrt(h_local.pow(2).mean(dim=1, keepdim=True) + eps)).to(torch.bfloat16)
         L.forward(x, out_local, **(bufs or {}))

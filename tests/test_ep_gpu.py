@@ -83,3 +83,28 @@ def test_ep_stack_world1_matches_sequential(oea):
         h = ref.to(torch.bfloat16)
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
+
+
+def test_residual_rmsnorm_kernel(oea):
+    # the C4 stack glue: h += add; x = bf16(h * rsqrt(mean(h^2) + eps)), vs torch fp32
+    import ctypes as C
+    import torch
+    from paper_2511_02237_b200._capi import default_context, lib
+    ctx = default_context()
+    g = torch.Generator(device="cuda").manual_seed(0)
+    for rows, D in ((1, 64), (16, 2048), (5, 4096), (3, 1000)):
+        h = torch.randn(rows, D, device="cuda", generator=g)
+        add = torch.randn(rows, D, device="cuda", generator=g)
+        want_h = h + add
+        want_x = (want_h * torch.rsqrt(want_h.pow(2).mean(dim=1, keepdim=True) + 1e-6)).to(torch.bfloat16)
+        x = torch.empty(rows, D, dtype=torch.bfloat16, device="cuda")
+        ctx.check(lib().oea_residual_rmsnorm(ctx.h, h.data_ptr(), add.data_ptr(), x.data_ptr(),
+                                             rows, D, 1e-6, None))
+        ctx.synchronize()
+        assert torch.allclose(h, want_h)
+        assert (x.float() - want_x.float()).abs().max().item() <= 2 ** -7 * want_x.float().abs().max().item()
+        x2 = torch.empty_like(x)
+        ctx.check(lib().oea_residual_rmsnorm(ctx.h, h.data_ptr(), None, x2.data_ptr(), rows, D,
+                                             1e-6, None))
+        ctx.synchronize()
+        assert torch.equal(x, x2)  # add == NULL: normalisation only, same bits
