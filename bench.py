@@ -386,15 +386,23 @@ def bench_c1(args, env):
                 "vanilla_frac": v["GBps"] / peak}
 
     # ---- e2e through the C ABI from pinned host buffers ----
-    x_host = torch.empty(W + K, B, D, dtype=torch.bfloat16).pin_memory()
-    x_host.copy_(xs.cpu())
+    # A serving loop's shape: each step's tokens (host memory) are written
+    # into one pinned staging buffer (the CPU copy is inside the timed
+    # region), the decode reads it and writes out to a pinned buffer, and the
+    # call returns when out is on the host.
+    import ctypes
+    x_src = xs.cpu().contiguous()          # the steps' inputs, host memory
+    x_stage = torch.empty(B, D, dtype=torch.bfloat16).pin_memory()
     out_host = torch.empty(B, D, dtype=torch.float32).pin_memory()
+    xb, sp, op = B * D * 2, x_stage.data_ptr(), out_host.data_ptr()
     for i in range(W):
-        layers[i % ROTATE].decode_host_ptr(x_host[i].data_ptr(), out_host.data_ptr(), B, cfg)
+        ctypes.memmove(sp, x_src[i].data_ptr(), xb)
+        layers[i % ROTATE].decode_host_ptr(sp, op, B, cfg)
     _barrier(env)
     t0 = time.perf_counter()
     for i in range(W, W + K):
-        layers[i % ROTATE].decode_host_ptr(x_host[i].data_ptr(), out_host.data_ptr(), B, cfg)
+        ctypes.memmove(sp, x_src[i].data_ptr(), xb)
+        layers[i % ROTATE].decode_host_ptr(sp, op, B, cfg)
     e2e_us = (time.perf_counter() - t0) * 1e6 / K
     e2e_us = _max_over_ranks(env, e2e_us)
 
