@@ -58,7 +58,7 @@ struct Workspace {
   int32_t* counters = nullptr;
   unsigned long long* xlog = nullptr;   // fused decode: tagged logits [B][Np]
   unsigned long long* xuni = nullptr;   // tagged per-token base bitmaps [B][4]
-  unsigned long long* xplan = nullptr;  // tagged plan-row readiness [B]
+  unsigned long long* xplan = nullptr;  // tagged plan rows [B][1 + 2 S]
   __nv_bfloat16* xpad = nullptr;
   void* hbuf = nullptr;
   void* ybuf = nullptr;
@@ -114,7 +114,7 @@ size_t carve(Workspace& w, bool assign) {
   take(w.counters, (G + 16 + 4 * std::max<size_t>(B, 64) + 8) * 4);
   take(w.xlog, B * Nmax * 8);
   take(w.xuni, B * 8 * 8);
-  take(w.xplan, B * 8);
+  take(w.xplan, B * (1 + 2 * S) * 8);  // tagged plan rows: len, then (expert, weight) per slot
   take(w.xpad, B * Dp * 2);
   // (dense decode: h [G][16][Hp] bf16, y [G][16][Dp] f32 with G <= N)
   take(w.hbuf, std::max(R * std::max(Hp, H) * 8, Nmax * 16 * Hp * 2));

@@ -867,6 +867,7 @@ __device__ __forceinline__ void rank_phase2(const FfnParams& P, int t, uint8_t* 
     if (P.x_w64) P.x_w64[o] = static_cast<double>(w);
   }
   if (gt == 0) {
+    reinterpret_cast<int*>(rs + L.len)[t] = len;
     P.x_set_len[t] = len;
     if (P.x_phase1_n) P.x_phase1_n[t] = P.cfg.mode == OEA_MODE_VANILLA ? 0 : n;
   }
@@ -1191,39 +1192,57 @@ __device__ __forceinline__ void route_phase2_plan(const FfnParams& P, uint8_t* r
   };
   const int B = P.B, stride = P.cfg.stride, Np = P.Np;
   const int Bw = (B + 31) >> 5;
+  // plan row of token t as self-validating tagged words {tag | payload}:
+  // [0] = set length, [1 + 2j] = expert of slot j (-1 past the length),
+  // [2 + 2j] = its fp32 weight; readers take all rows in one pass
+  const int W = 1 + 2 * stride;
 #pragma unroll 1
   for (int t = blockIdx.x; t < B; t += gridDim.x) {
     rank_phase2<NC>(P, t, rs, L, reinterpret_cast<const int*>(rs + L.misc)[1], gt, sync);
-    sync();  // (orders the group's plan-row stores before the release below)
-    if (gt == 0) st_release_u64(P.xplan + t, tagged(tag, 1u));
+    sync();  // (the row's sets / weights in shared memory are final)
+    const int* srow = reinterpret_cast<const int*>(rs + L.sets) + t * stride;
+    const float* erow = reinterpret_cast<const float*>(rs + L.e) + t * stride;
+    const int ln = reinterpret_cast<const int*>(rs + L.len)[t];
+    for (int k = gt; k < W; k += NC) {
+      const int j = (k - 1) >> 1;
+      const uint32_t v = k == 0 ? static_cast<uint32_t>(ln)
+                         : ((k - 1) & 1) == 0 ? static_cast<uint32_t>(j < ln ? srow[j] : -1)
+                                              : __float_as_uint(j < ln ? erow[j] : 0.0f);
+      st_relaxed_u64(P.xplan + static_cast<size_t>(t) * W + k, tagged(tag, v));
+    }
   }
   if (!gather) return;
-  // every token's plan row: acquire its tagged readiness word
-#pragma unroll 1
-  for (int t = gt; t < B; t += NC) {
-    const unsigned long long* w = P.xplan + t;
-    while (static_cast<uint32_t>(ld_acquire_u64(w) >> 32) != tag) __nanosleep(32);
-  }
-  sync();
   int* len = reinterpret_cast<int*>(rs + L.len);
   int* sets = reinterpret_cast<int*>(rs + L.sets);
   float* wts = reinterpret_cast<float*>(rs + L.e);
   int* loads = reinterpret_cast<int*>(rs + L.loads);
   uint32_t* tokbits = reinterpret_cast<uint32_t*>(rs + L.tokbits);
+  sync();  // (this CTA's own rows were read above; the arrays are rebuilt below)
+  // every token's plan row in one pass: each word carries its own tag
+#pragma unroll 2
+  for (int idx = gt; idx < B * W; idx += NC) {
+    const unsigned long long* w = P.xplan + idx;
+    unsigned long long v = ld_relaxed_u64(w);
+    while (static_cast<uint32_t>(v >> 32) != tag) v = ld_relaxed_u64(w);
+    const int t = idx / W, k = idx % W;
+    const uint32_t pv = static_cast<uint32_t>(v);
+    if (k == 0)
+      len[t] = static_cast<int>(pv);
+    else if (((k - 1) & 1) == 0)
+      sets[t * stride + ((k - 1) >> 1)] = static_cast<int>(pv);
+    else
+      wts[t * stride + ((k - 1) >> 1)] = __uint_as_float(pv);
+  }
 #pragma unroll 1
   for (int i = gt; i < Np; i += NC) loads[i] = 0;
 #pragma unroll 1
   for (int i = gt; i < Np * Bw; i += NC) tokbits[i] = 0u;
-#pragma unroll 1
-  for (int t = gt; t < B; t += NC) len[t] = __ldcg(P.x_set_len + t);
   sync();
 #pragma unroll 4
   for (int idx = gt; idx < B * stride; idx += NC) {
     const int t = idx / stride, sl = idx % stride;
-    const int e = __ldcg(P.x_sets + idx);
-    sets[idx] = e;
-    wts[idx] = __ldcg(P.x_w32 + idx);
     if (sl < len[t]) {
+      const int e = sets[idx];
       atomicAdd(&loads[e], 1);
       atomicOr(&tokbits[e * Bw + (t >> 5)], 1u << (t & 31));
     }
