@@ -823,15 +823,17 @@ __device__ __forceinline__ void rank_phase2(const FfnParams& P, int t, uint8_t* 
       }
     }
     sync();
-#pragma unroll 1
-    for (int i = gt; i < T; i += NT) {
-      const uint32_t key = ukeys[i];
-      int urank = 0;  // members before member i: larger key, or equal key and lower index
+    // members before member i: larger key, or equal key and lower index
+    auto rank_part = [&](int i, uint32_t key, int j0, int j1) {
+      int c = 0;
 #pragma unroll 4
-      for (int j = 0; j < T; ++j) {
+      for (int j = j0; j < j1; ++j) {
         const uint32_t kj = ukeys[j];
-        urank += (kj > key) | ((kj == key) & (j < i));
+        c += (kj > key) | ((kj == key) & (j < i));
       }
+      return c;
+    };
+    auto place = [&](int i, uint32_t key, int urank) {
       if (urank >= n && urank < len) {
         // expert index of member i: the i-th set bit of the union
         int e = 0, r = i;
@@ -848,6 +850,23 @@ __device__ __forceinline__ void rank_phase2(const FfnParams& P, int t, uint8_t* 
         }
         sets[urank] = e;
         se[urank] = expf(key32_to_logit(key) - rowmax);
+      }
+    };
+    if constexpr (NT >= 256) {
+      // T <= 128: thread (part, i) counts half of member i's compares; the
+      // halves meet in shared memory (R1's per-CTA keys[] is dead by now)
+      int* pc = reinterpret_cast<int*>(rs + L.keys);
+      const int part = gt >> 7, i = gt & 127, half = (T + 1) >> 1;
+      const uint32_t key = i < T ? ukeys[i] : 0u;
+      int urank = i < T ? rank_part(i, key, part * half, min(T, (part + 1) * half)) : 0;
+      if (part == 1 && i < T) pc[i] = urank;
+      sync();
+      if (part == 0 && i < T) place(i, key, urank + pc[i]);
+    } else {
+#pragma unroll 1
+      for (int i = gt; i < T; i += NT) {
+        const uint32_t key = ukeys[i];
+        place(i, key, rank_part(i, key, 0, T));
       }
     }
   }
