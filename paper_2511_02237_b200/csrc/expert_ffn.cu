@@ -74,7 +74,8 @@ struct FfnParams {
   int split_ok;                 // split rounds allowed (OEA_SPLIT=1; off by default)
   int e_begin, e_count;         // experts this (possibly EP-shard) layer holds
   // Epoch-tagged exchange words (fused path): logits [B][Np], per-token base
-  // bitmaps [B][4], plan-row readiness [B]; tag = launch epoch + 1.
+  // bitmaps [B][4], plan rows [B][1 + 2 stride] (length, then expert and weight
+  // per slot); tag = launch epoch + 1.
   unsigned long long* xlog;
   unsigned long long* xuni;
   unsigned long long* xplan;
