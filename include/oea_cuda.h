@@ -168,6 +168,33 @@ int oea_phase2_f64_host(oea_ctx_t ctx, const uint8_t* mask, int32_t B, int32_t N
                         const int32_t* base_union, int32_t base_union_count,
                         const oea_routing_cfg* cfg, const oea_plan_view* plan);
 
+/* Expert parallelism with the combine fused into the decode over peer memory
+ * (NVLink / NVSwitch; no NCCL on the data path). Rank r of `world` (<= 8)
+ * decodes the whole batch x_all (B x D, B % world == 0) on its shard; the
+ * kernel's combine stores token t's partial mixture straight into its owner
+ * o = t / (B / world): recv[o][r][t - o B / world][D] (fp32), then every CTA
+ * adds 1 to every owner's arrival counter cnt[o] (system-scope release).
+ * recv[] / cnt[] are this rank's views of every rank's buffers
+ * (oea_ipc_open_handle); recv[o] holds [world][B / world][D] floats.
+ * oea_ep_combine (owner side, after its own partial launch) waits until its
+ * counter reaches `expected` (launches so far x oea_ep_arrivals_per_launch;
+ * the counter only grows) and sums the world slots in rank order into
+ * out_local [B / world][D]. */
+int oea_moe_decode_ep_partial(oea_ctx_t ctx, oea_layer_t layer, const void* x_all_dev, int32_t B,
+                              const oea_routing_cfg* cfg, int32_t world, int32_t rank,
+                              float* const* recv, int32_t* const* cnt, void* stream);
+int32_t oea_ep_arrivals_per_launch(oea_ctx_t ctx, int32_t world);
+int oea_ep_combine(oea_ctx_t ctx, const float* recv_local, const int32_t* cnt_local,
+                   uint32_t expected, int32_t world, int32_t tokens_per_rank, int32_t D,
+                   float* out_local, void* stream);
+/* CUDA IPC of a device buffer between the ranks' processes (64-byte handle;
+ * use buffers from oea_device_alloc, whose base the handle maps exactly). */
+int oea_device_alloc(oea_ctx_t ctx, uint64_t bytes, void** dev_ptr); /* zero-filled */
+int oea_device_free(oea_ctx_t ctx, void* dev_ptr);
+int oea_ipc_get_handle(oea_ctx_t ctx, const void* dev_ptr, void* handle);
+int oea_ipc_open_handle(oea_ctx_t ctx, const void* handle, void** dev_ptr);
+int oea_ipc_close_handle(oea_ctx_t ctx, void* dev_ptr);
+
 /* Decoder glue between stacked MoE layers (the C4 stack, attention omitted):
  * h += add (when add != NULL), then x = bf16(h * rsqrt(mean(h^2) + eps)) per
  * row; h, add: [rows][D] fp32 device, x: [rows][D] bf16 device. One launch. */

@@ -394,9 +394,15 @@ bool fused_ok(const oea_layer* L, int B, const oea_routing_cfg& rc) {
 constexpr int kNotFused = -1000;  // decode_bf16(x_mapped): not on the fused path, nothing launched
 // x_mapped: x and out are device views of mapped (pinned) host memory; only
 // the fused single launch takes them (the caller checks fused_path()).
+struct EpArgs {  // peer-memory EP combine (oea_moe_decode_ep_partial)
+  int world, rank;
+  float* const* recv;
+  int32_t* const* cnt;
+};
+
 int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const uint8_t* mask,
                 int B, const oea_routing_cfg& rc, void* out, cudaStream_t s, int part = 0,
-                bool x_mapped = false) {
+                bool x_mapped = false, const EpArgs* ep = nullptr) {
   const int stride = stride_of(rc);
   const Cfg cfg = dev_cfg(rc, stride);
   oea_host::FusedRouterBuffers rb;
@@ -491,6 +497,15 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
     if (r || part == 1) return r;
   }
   oea_host::FfnBuffers fb;
+  if (ep != nullptr) {
+    fb.ep_world = ep->world;
+    fb.ep_rank = ep->rank;
+    fb.ep_tpr = B / ep->world;
+    for (int o = 0; o < ep->world; ++o) {
+      fb.ep_recv[o] = ep->recv[o];
+      fb.ep_cnt[o] = ep->cnt[o];
+    }
+  }
   fb.x = padded || x_mapped ? static_cast<const void*>(w.xpad) : x;
   fb.row_tok = w.row_tok;
   fb.row_slot = w.row_slot;
@@ -1254,6 +1269,91 @@ int oea_moe_decode(oea_ctx_t ctx, oea_layer_t L, const void* x_dev, const uint8_
   ctx->last_kind = 2;
   return decode_simt(ctx, w, L, static_cast<const double*>(x_dev), mask_dev, B, rc,
                      static_cast<double*>(out_dev), s);
+}
+
+int oea_moe_decode_ep_partial(oea_ctx_t ctx, oea_layer_t L, const void* x_all_dev, int32_t B,
+                              const oea_routing_cfg* cfg, int32_t world, int32_t rank,
+                              float* const* recv, int32_t* const* cnt, void* stream) {
+  CHECK_CTX(ctx);
+  oea_routing_cfg rc;
+  int r = validate_decode(ctx, L, B, cfg, &rc);
+  if (r) return r;
+  if (L->dtype != OEA_DTYPE_BF16)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "moe_decode_ep: bf16 layers only");
+  if (world < 1 || world > oea_dev::kMaxEpWorld || rank < 0 || rank >= world || B % world != 0)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT,
+                "moe_decode_ep: need 1 <= world <= 8, 0 <= rank < world and B % world == 0");
+  if (x_all_dev == nullptr || recv == nullptr || cnt == nullptr)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "moe_decode_ep: null buffers");
+  for (int o = 0; o < world; ++o)
+    if (recv[o] == nullptr || cnt[o] == nullptr)
+      return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "moe_decode_ep: null peer buffer");
+  Workspace& w = extra(ctx)->ws;
+  r = ensure(ctx, w, need_for(L, B, stride_of(rc)));
+  if (r) return r;
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  ctx->last_B = B;
+  ctx->last_N = L->N;
+  ctx->last_stride = stride_of(rc);
+  ctx->last_kind = 1;
+  const EpArgs ep{world, rank, recv, cnt};
+  // (world == 1 keeps the combine local: out = the receive buffer itself)
+  return decode_bf16(ctx, w, L, x_all_dev, nullptr, B, rc, world > 1 ? nullptr : recv[0], s, 0,
+                     false, world > 1 ? &ep : nullptr);
+}
+
+int32_t oea_ep_arrivals_per_launch(oea_ctx_t ctx, int32_t world) {
+  return ctx == nullptr ? 0 : world * ctx->num_sms;
+}
+
+int oea_ep_combine(oea_ctx_t ctx, const float* recv_local, const int32_t* cnt_local,
+                   uint32_t expected, int32_t world, int32_t tokens_per_rank, int32_t D,
+                   float* out_local, void* stream) {
+  CHECK_CTX(ctx);
+  if (recv_local == nullptr || cnt_local == nullptr || out_local == nullptr || world < 1 ||
+      world > oea_dev::kMaxEpWorld || tokens_per_rank < 1 || D < 1)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "ep_combine: bad arguments");
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  return oea_host::ep_sum_launch(ctx, recv_local, cnt_local, expected, world, tokens_per_rank * D,
+                                 out_local, s);
+}
+
+// Zero-filled device allocation of its own (IPC handles of a cudaMalloc base
+// map exactly, unlike sub-allocations of a caching allocator).
+int oea_device_alloc(oea_ctx_t ctx, uint64_t bytes, void** dev_ptr) {
+  CHECK_CTX(ctx);
+  if (dev_ptr == nullptr || bytes == 0) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "device_alloc: bad arguments");
+  OEA_CUDA_TRY(ctx, cudaMalloc(dev_ptr, bytes));
+  OEA_CUDA_TRY(ctx, cudaMemset(*dev_ptr, 0, bytes));
+  return OEA_OK;
+}
+
+int oea_device_free(oea_ctx_t ctx, void* dev_ptr) {
+  CHECK_CTX(ctx);
+  if (dev_ptr) OEA_CUDA_TRY(ctx, cudaFree(dev_ptr));
+  return OEA_OK;
+}
+
+int oea_ipc_close_handle(oea_ctx_t ctx, void* dev_ptr) {
+  CHECK_CTX(ctx);
+  if (dev_ptr) OEA_CUDA_TRY(ctx, cudaIpcCloseMemHandle(dev_ptr));
+  return OEA_OK;
+}
+
+int oea_ipc_get_handle(oea_ctx_t ctx, const void* dev_ptr, void* handle) {
+  CHECK_CTX(ctx);
+  cudaIpcMemHandle_t h;
+  OEA_CUDA_TRY(ctx, cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  std::memcpy(handle, &h, sizeof h);
+  return OEA_OK;
+}
+
+int oea_ipc_open_handle(oea_ctx_t ctx, const void* handle, void** dev_ptr) {
+  CHECK_CTX(ctx);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  OEA_CUDA_TRY(ctx, cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return OEA_OK;
 }
 
 // The zero-copy fused decode through the context's graph cache (see

@@ -85,6 +85,12 @@ struct FfnParams {
   __nv_bfloat16* xpad_out;      // [B][Dp], written in-kernel when D != Dp, else null
   int x_stage;                  // x_in is mapped host memory: staged into xpad_out first
   int prefetch_bytes;           // speculative L2 prefetch of every held expert's first W1 bytes
+  // Expert-parallel combine over peer memory (oea_moe_decode_ep): the partial
+  // mixture of token t goes straight to its owner's receive buffer, slot
+  // [ep_rank][t - owner * ep_tpr], then every CTA bumps every owner's counter.
+  float* ep_recv[kMaxEpWorld];
+  int* ep_cnt[kMaxEpWorld];
+  int ep_world, ep_rank, ep_tpr;
   float* logits;        // [B][Np]
   const uint8_t* mask;
   int N, Np;
@@ -1716,9 +1722,46 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
       if (s0 >= len) break;
       prep(f, len, yo, w, s0);
     }
-    P.out[f] = sum;
+    if (P.ep_world > 1) {
+      const int t = static_cast<int>(f / P.D), d = static_cast<int>(f % P.D);
+      const int owner = t / P.ep_tpr;
+      P.ep_recv[owner][(static_cast<size_t>(P.ep_rank) * P.ep_tpr + (t - owner * P.ep_tpr)) * P.D +
+                       d] = sum;
+    } else {
+      P.out[f] = sum;
+    }
+  }
+  if (P.ep_world > 1) {
+    // this CTA's remote stores are issued (all combining threads), made
+    // visible system-wide, then counted at every owner (sum in k_ep_sum)
+    asm volatile("bar.sync 2, %0;" ::"r"(kComb) : "memory");
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      for (int o = 0; o < P.ep_world; ++o) atomicAdd_system(P.ep_cnt[o], 1);
+    }
   }
   if (threadIdx.x == 0) stamp(P, 15);
+}
+
+// Owner side of the peer-memory EP combine: wait until every rank's CTAs
+// have delivered this launch's partials (counter >= expected, monotonic
+// across launches), then out[i] = sum over source ranks in rank order
+// (deterministic).
+__global__ void __launch_bounds__(256)
+    k_ep_sum(const float* __restrict__ recv, const int* __restrict__ cnt, uint32_t expected,
+             int world, int n, float* __restrict__ out) {
+  if (threadIdx.x == 0) {
+    uint32_t v;
+    do {  // (wrap-around safe: the counter only ever grows)
+      asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+    } while (static_cast<int32_t>(v - expected) < 0);
+  }
+  __syncthreads();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    float s = 0.0f;
+    for (int r = 0; r < world; ++r) s += __ldcg(recv + static_cast<size_t>(r) * n + i);
+    out[i] = s;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1880,6 +1923,13 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   // reduction overhead, tools/trace_ffn.py): opt-in for experiments
   P.split_ok = getenv("OEA_SPLIT") != nullptr;
   P.x_stage = fb.x_stage;
+  P.ep_world = fb.ep_world;
+  P.ep_rank = fb.ep_rank;
+  P.ep_tpr = fb.ep_tpr;
+  for (int o = 0; o < kMaxEpWorld; ++o) {
+    P.ep_recv[o] = o < fb.ep_world ? fb.ep_recv[o] : nullptr;
+    P.ep_cnt[o] = o < fb.ep_world ? fb.ep_cnt[o] : nullptr;
+  }
   {
     // ~32 MiB in total, about what HBM delivers while the prologue routes
     // (measured C1, N=128: 128 KiB per expert saves ~1.3 us, 224-288 KiB
@@ -1942,6 +1992,15 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   OEA_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, P));
   OEA_LAUNCHED(ctx);
   return OEA_OK;
+}
+
+int ep_sum_launch(oea_ctx* ctx, const float* recv, const int* cnt, uint32_t expected, int world,
+                  int n, float* out, cudaStream_t s) {
+  k_ep_sum<<<std::max(1, std::min(148, (n + 255) / 256)), 256, 0, s>>>(recv, cnt, expected, world,
+                                                                      n, out);
+  OEA_LAUNCHED(ctx);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? OEA_OK : oea_check_cuda(ctx, e, "k_ep_sum");
 }
 
 // Host-path graph replays (capi.cu decode_host_graph) patch a captured fused

@@ -34,6 +34,7 @@ constexpr int kRouterThreads = 512;
 constexpr int kRouterTokChunk = 64;    // tokens per GEMV pass in the router
 constexpr int kMaxFusedB = 256;        // fused decode batch limit
 constexpr int kMaxFusedN = 256;        // fused router expert limit (Np <= 256)
+constexpr int kMaxEpWorld = 8;  // expert-parallel group size of the peer-memory combine
 constexpr int kMaxRouteN = 1024;       // route_f64 expert limit
 
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
@@ -212,6 +213,9 @@ struct FfnBuffers {
   const __nv_bfloat16* x_in = nullptr;  // [B][D] caller tokens
   __nv_bfloat16* xpad_out = nullptr;    // [B][Dp] when D != Dp (or x_stage)
   int x_stage = 0;                      // x_in is mapped host memory (staged in-kernel)
+  int ep_world = 0, ep_rank = 0, ep_tpr = 0;  // peer-memory EP combine (ep_world > 1)
+  float* ep_recv[oea_dev::kMaxEpWorld] = {};
+  int* ep_cnt[oea_dev::kMaxEpWorld] = {};
   float* logits = nullptr;              // [B][Np]
   unsigned long long* xlog = nullptr;   // tagged exchange words (fused path)
   unsigned long long* xuni = nullptr;
@@ -235,6 +239,8 @@ size_t ffn_route_smem_bytes(int B, int Np, int stride);
 size_t ffn_bf16_smem_bytes();
 int gen_scores_launch(oea_ctx* ctx, const oea_score_gen_cfg& c, int step0, int nsteps,
                       double* out, cudaStream_t s);
+int ep_sum_launch(oea_ctx* ctx, const float* recv, const int* cnt, uint32_t expected, int world,
+                  int n, float* out, cudaStream_t s);
 size_t ffn_params_bytes();
 void ffn_params_set_io(void* params, const void* x_in, void* out);
 size_t ffn_btile_bytes();

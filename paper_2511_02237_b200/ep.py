@@ -24,7 +24,7 @@ from __future__ import annotations
 
 from typing import Callable, List, Optional
 
-__all__ = ["ep_expert_range", "ep_token_range", "ExpertParallelMoE"]
+__all__ = ["ep_expert_range", "ep_token_range", "ExpertParallelMoE", "PeerExpertParallelMoE"]
 
 
 def ep_expert_range(n_experts: int, world: int, rank: int):
@@ -134,3 +134,105 @@ def stack_forward(layers: List[ExpertParallelMoE], x_local, out_local, cast=None
         if i + 1 < len(layers):
             x = out_local.to(x_local.dtype) if cast is None else cast(out_local)
     return out_local
+
+
+class PeerExpertParallelMoE:
+    """One rank's EP MoE layer with the combine fused into the decode kernel
+    over peer memory (NVLink / NVSwitch): no NCCL on the data path after the
+    token all-gather. The shard kernel's combine stores each token's partial
+    mixture straight into the token owner's receive buffer and bumps the
+    owner's arrival counter; the owner then sums the `world` slots in rank
+    order (oea_ep_combine). Buffers come from oea_device_alloc and are mapped
+    into the other ranks with CUDA IPC (`connect`), or, for a single-process
+    emulation of the group on one GPU, shared directly (`emulate_group`)."""
+
+    def __init__(self, layer, cfg, world: int, rank: int, B: int):
+        import ctypes as C
+        from ._capi import default_context, lib
+        if B % world != 0:
+            raise ValueError("PeerExpertParallelMoE: B must split evenly over the EP group")
+        self.layer, self.cfg, self.world, self.rank, self.B = layer, cfg, world, rank, B
+        self.tpr, self.D = B // world, layer.D
+        self.ctx = default_context()
+        self._lib = lib()
+        recv, cnt = C.c_void_p(), C.c_void_p()
+        self.ctx.check(self._lib.oea_device_alloc(self.ctx.h, world * self.tpr * self.D * 4,
+                                                  C.byref(recv)))
+        self.ctx.check(self._lib.oea_device_alloc(self.ctx.h, 64, C.byref(cnt)))
+        self.recv_local, self.cnt_local = recv.value, cnt.value
+        self.recv_ptrs = [0] * world
+        self.cnt_ptrs = [0] * world
+        self.recv_ptrs[rank], self.cnt_ptrs[rank] = self.recv_local, self.cnt_local
+        self._opened = []
+        self.launches = 0
+        self.per_launch = self._lib.oea_ep_arrivals_per_launch(self.ctx.h, world)
+
+    def handles(self):
+        """64-byte IPC handles of (receive buffer, counter)."""
+        import ctypes as C
+        out = []
+        for p in (self.recv_local, self.cnt_local):
+            h = (C.c_char * 64)()
+            self.ctx.check(self._lib.oea_ipc_get_handle(self.ctx.h, C.c_void_p(p), h))
+            out.append(bytes(h))
+        return out
+
+    def connect(self, dist, group=None):
+        """Exchange IPC handles over torch.distributed and map every peer's
+        receive buffer and counter (one process per GPU)."""
+        import ctypes as C
+        allh = [None] * self.world
+        dist.all_gather_object(allh, self.handles(), group=group)
+        for r, (hr, hc) in enumerate(allh):
+            if r == self.rank:
+                continue
+            pr, pc = C.c_void_p(), C.c_void_p()
+            self.ctx.check(self._lib.oea_ipc_open_handle(self.ctx.h, C.c_char_p(hr), C.byref(pr)))
+            self.ctx.check(self._lib.oea_ipc_open_handle(self.ctx.h, C.c_char_p(hc), C.byref(pc)))
+            self.recv_ptrs[r], self.cnt_ptrs[r] = pr.value, pc.value
+            self._opened += [pr.value, pc.value]
+
+    @staticmethod
+    def emulate_group(members):
+        """Single-GPU emulation: every member sees the others' buffers."""
+        for m in members:
+            m.recv_ptrs = [o.recv_local for o in members]
+            m.cnt_ptrs = [o.cnt_local for o in members]
+
+    def partial(self, x_all, stream=None):
+        """This rank's shard decode of the whole batch; its combine writes
+        the owners' receive buffers."""
+        import ctypes as C
+        from .moe_layer import torch_stream
+        recv = (C.c_void_p * self.world)(*self.recv_ptrs)
+        cnt = (C.c_void_p * self.world)(*self.cnt_ptrs)
+        st = stream if stream is not None else torch_stream()
+        self.ctx.check(self._lib.oea_moe_decode_ep_partial(
+            self.ctx.h, self.layer.h, C.c_void_p(x_all.data_ptr()), self.B, self.cfg.c_ref(),
+            self.world, self.rank, recv, cnt, C.c_void_p(st)))
+        self.launches += 1
+
+    def combine(self, out_local, stream=None):
+        """Owner side: wait for every rank's partials of this launch, then
+        out_local [B / world][D] = sum over ranks in rank order."""
+        import ctypes as C
+        from .moe_layer import torch_stream
+        expected = (self.launches * self.per_launch) & 0xFFFFFFFF
+        st = stream if stream is not None else torch_stream()
+        self.ctx.check(self._lib.oea_ep_combine(
+            self.ctx.h, C.c_void_p(self.recv_local), C.c_void_p(self.cnt_local), expected,
+            self.world, self.tpr, self.D, C.c_void_p(out_local.data_ptr()), C.c_void_p(st)))
+
+    def forward(self, x_all, out_local, stream=None):
+        """x_all [B, D] bf16 (the all-gathered batch) -> out_local [B/world, D]."""
+        self.partial(x_all, stream)
+        self.combine(out_local, stream)
+        return out_local
+
+    def close(self):
+        import ctypes as C
+        for p in self._opened:
+            self._lib.oea_ipc_close_handle(self.ctx.h, C.c_void_p(p))
+        for p in (self.recv_local, self.cnt_local):
+            self._lib.oea_device_free(self.ctx.h, C.c_void_p(p))
+        self._opened, self.recv_local, self.cnt_local = [], 0, 0

@@ -108,3 +108,59 @@ def test_residual_rmsnorm_kernel(oea):
                                              1e-6, None))
         ctx.synchronize()
         assert torch.equal(x, x2)  # add == NULL: normalisation only, same bits
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_peer_memory_ep_emulated(oea, P):
+    """The peer-memory EP combine on one GPU: P shard members share each
+    other's receive buffers directly (the multi-GPU path maps them with CUDA
+    IPC). Every member's partial decode writes the owners' slots and
+    counters; each owner's combine equals its tokens of the unsharded layer
+    (fp32 partial sums: same tolerance as the NCCL reduce-scatter path), over
+    several launches (monotonic counters)."""
+    import torch
+    from paper_2511_02237_b200 import ep
+    D, H, N, B = 1024, 512, 64, 16
+    cfg = oea.RoutingConfig.simplified(4, 8)
+    full = oea.DeviceMoeLayer(D, H, N, "bf16")
+    full.init_random(11)
+    members = []
+    for r in range(P):
+        sh = oea.DeviceMoeLayer(D, H, N, "bf16", experts=ep.ep_expert_range(N, P, r))
+        sh.init_random(11)
+        members.append(ep.PeerExpertParallelMoE(sh, cfg, P, r, B))
+    ep.PeerExpertParallelMoE.emulate_group(members)
+    tpr = B // P
+    for it in range(3):
+        x = torch.randn(B, D, device="cuda").to(torch.bfloat16)
+        ref = torch.empty(B, D, device="cuda")
+        full.decode(x, cfg, ref, stream=oea.moe_layer.torch_stream())
+        for m in members:  # every rank's partial first (one GPU: no concurrent spin)
+            m.partial(x)
+        outs = [torch.empty(tpr, D, device="cuda") for _ in range(P)]
+        for m, o in zip(members, outs):
+            m.combine(o)
+        torch.cuda.synchronize()
+        got = torch.cat(outs)
+        err = ((got - ref).norm(dim=1) / ref.norm(dim=1).clamp_min(1e-12)).max().item()
+        assert err < 1e-5, (it, err)
+    for m in members:
+        m.close()
+
+
+def test_peer_memory_ep_ipc_two_processes(oea):
+    """world-2 EP group as two processes on this GPU: CUDA IPC handle
+    exchange over gloo, peer-memory combine, each rank's tokens equal the
+    unsharded layer's (tests/ep_ipc_worker.py)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT="29517", WORLD_SIZE="2")
+    procs = [subprocess.Popen([sys.executable, os.path.join(here, "ep_ipc_worker.py")],
+                              env=dict(env, RANK=str(r)), stdout=subprocess.PIPE,
+                              stderr=subprocess.STDOUT, text=True) for r in range(2)]
+    outs = [p.communicate(timeout=300)[0] for p in procs]
+    for p, o in zip(procs, outs):
+        assert p.returncode == 0, o[-2000:]
+        assert "max_rel_err" in o
