@@ -175,18 +175,17 @@ int oea_phase2_f64_host(oea_ctx_t ctx, const uint8_t* mask, int32_t B, int32_t N
  * o = t / (B / world): recv[o][r][t - o B / world][D] (fp32), then every CTA
  * adds 1 to every owner's arrival counter cnt[o] (system-scope release).
  * recv[] / cnt[] are this rank's views of every rank's buffers
- * (oea_ipc_open_handle); recv[o] holds [world][B / world][D] floats.
- * oea_ep_combine (owner side, after its own partial launch) waits until its
- * counter reaches `expected` (launches so far x oea_ep_arrivals_per_launch;
- * the counter only grows) and sums the world slots in rank order into
- * out_local [B / world][D]. */
+ * (oea_ipc_open_handle); recv[o] holds [world][B / world][D] floats, cnt[o]
+ * two ints (arrivals, consumed; zero-filled at allocation).
+ * oea_ep_combine (owner side, after its own partial launch) waits for this
+ * launch's world x grid arrivals (the target is kept on the device, so both
+ * calls can be captured in a CUDA graph) and sums the world slots in rank
+ * order into out_local [B / world][D]. */
 int oea_moe_decode_ep_partial(oea_ctx_t ctx, oea_layer_t layer, const void* x_all_dev, int32_t B,
                               const oea_routing_cfg* cfg, int32_t world, int32_t rank,
                               float* const* recv, int32_t* const* cnt, void* stream);
-int32_t oea_ep_arrivals_per_launch(oea_ctx_t ctx, int32_t world);
-int oea_ep_combine(oea_ctx_t ctx, const float* recv_local, const int32_t* cnt_local,
-                   uint32_t expected, int32_t world, int32_t tokens_per_rank, int32_t D,
-                   float* out_local, void* stream);
+int oea_ep_combine(oea_ctx_t ctx, const float* recv_local, int32_t* cnt_local, int32_t world,
+                   int32_t tokens_per_rank, int32_t D, float* out_local, void* stream);
 /* CUDA IPC of a device buffer between the ranks' processes (64-byte handle;
  * use buffers from oea_device_alloc, whose base the handle maps exactly). */
 int oea_device_alloc(oea_ctx_t ctx, uint64_t bytes, void** dev_ptr); /* zero-filled */

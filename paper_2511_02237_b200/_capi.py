@@ -86,8 +86,7 @@ def lib():
                 "oea_gen_scores": [vp, vp, i32, i32, vp, vp],
                 "oea_residual_rmsnorm": [vp, vp, vp, vp, i32, i32, C.c_double, vp],
                 "oea_moe_decode_ep_partial": [vp, vp, vp, i32, vp, i32, i32, vp, vp, vp],
-                "oea_ep_arrivals_per_launch": [vp, i32],
-                "oea_ep_combine": [vp, vp, vp, C.c_uint32, i32, i32, i32, vp, vp],
+                "oea_ep_combine": [vp, vp, vp, i32, i32, i32, vp, vp],
                 "oea_device_alloc": [vp, C.c_uint64, vp],
                 "oea_device_free": [vp, vp],
                 "oea_ipc_get_handle": [vp, vp, vp],
@@ -133,7 +132,7 @@ EXPORTED = (
     "oea_ctx_synchronize", "oea_ctx_kernel_launches", "oea_config_resolve",
     "oea_plan_set_stride", "oea_route_f64_host", "oea_route_f64", "oea_route_f64_batched_host",
     "oea_gen_scores", "oea_gen_scores_host", "oea_residual_rmsnorm",
-    "oea_moe_decode_ep_partial", "oea_ep_arrivals_per_launch", "oea_ep_combine", "oea_device_alloc",
+    "oea_moe_decode_ep_partial", "oea_ep_combine", "oea_device_alloc",
     "oea_device_free", "oea_ipc_get_handle", "oea_ipc_open_handle", "oea_ipc_close_handle",
     "oea_sort_experts_f64_host",
     "oea_phase1_f64_host", "oea_phase2_f64_host", "oea_layer_create", "oea_layer_destroy",

@@ -1302,20 +1302,15 @@ int oea_moe_decode_ep_partial(oea_ctx_t ctx, oea_layer_t L, const void* x_all_de
                      false, world > 1 ? &ep : nullptr);
 }
 
-int32_t oea_ep_arrivals_per_launch(oea_ctx_t ctx, int32_t world) {
-  return ctx == nullptr ? 0 : world * ctx->num_sms;
-}
-
-int oea_ep_combine(oea_ctx_t ctx, const float* recv_local, const int32_t* cnt_local,
-                   uint32_t expected, int32_t world, int32_t tokens_per_rank, int32_t D,
-                   float* out_local, void* stream) {
+int oea_ep_combine(oea_ctx_t ctx, const float* recv_local, int32_t* cnt_local, int32_t world,
+                   int32_t tokens_per_rank, int32_t D, float* out_local, void* stream) {
   CHECK_CTX(ctx);
   if (recv_local == nullptr || cnt_local == nullptr || out_local == nullptr || world < 1 ||
       world > oea_dev::kMaxEpWorld || tokens_per_rank < 1 || D < 1)
     return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "ep_combine: bad arguments");
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-  return oea_host::ep_sum_launch(ctx, recv_local, cnt_local, expected, world, tokens_per_rank * D,
-                                 out_local, s);
+  return oea_host::ep_sum_launch(ctx, recv_local, cnt_local, world * ctx->num_sms, world,
+                                 tokens_per_rank * D, out_local, s);
 }
 
 // Zero-filled device allocation of its own (IPC handles of a cudaMalloc base

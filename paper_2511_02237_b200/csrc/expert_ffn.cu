@@ -1743,21 +1743,24 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
   if (threadIdx.x == 0) stamp(P, 15);
 }
 
-// Owner side of the peer-memory EP combine: wait until every rank's CTAs
-// have delivered this launch's partials (counter >= expected, monotonic
-// across launches), then out[i] = sum over source ranks in rank order
-// (deterministic).
-__global__ void __launch_bounds__(256)
-    k_ep_sum(const float* __restrict__ recv, const int* __restrict__ cnt, uint32_t expected,
-             int world, int n, float* __restrict__ out) {
+// Owner side of the peer-memory EP combine (one CTA): cnt[0] counts the
+// arriving CTAs of all ranks, cnt[1] the arrivals already consumed; wait
+// until this launch's `per_launch` arrivals are in, then out[i] = sum over
+// source ranks in rank order (deterministic). The target lives on the device,
+// so the pair (partial decode, combine) can be captured in a CUDA graph.
+__global__ void __launch_bounds__(1024)
+    k_ep_sum(const float* __restrict__ recv, int* __restrict__ cnt, int per_launch, int world,
+             int n, float* __restrict__ out) {
   if (threadIdx.x == 0) {
+    const uint32_t target = static_cast<uint32_t>(cnt[1]) + static_cast<uint32_t>(per_launch);
     uint32_t v;
-    do {  // (wrap-around safe: the counter only ever grows)
+    do {  // (wrap-around safe: both counters only grow)
       asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
-    } while (static_cast<int32_t>(v - expected) < 0);
+    } while (static_cast<int32_t>(v - target) < 0);
+    cnt[1] = static_cast<int>(target);
   }
   __syncthreads();
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
     float s = 0.0f;
     for (int r = 0; r < world; ++r) s += __ldcg(recv + static_cast<size_t>(r) * n + i);
     out[i] = s;
@@ -1994,10 +1997,9 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   return OEA_OK;
 }
 
-int ep_sum_launch(oea_ctx* ctx, const float* recv, const int* cnt, uint32_t expected, int world,
-                  int n, float* out, cudaStream_t s) {
-  k_ep_sum<<<std::max(1, std::min(148, (n + 255) / 256)), 256, 0, s>>>(recv, cnt, expected, world,
-                                                                      n, out);
+int ep_sum_launch(oea_ctx* ctx, const float* recv, int* cnt, int per_launch, int world, int n,
+                  float* out, cudaStream_t s) {
+  k_ep_sum<<<1, 1024, 0, s>>>(recv, cnt, per_launch, world, n, out);
   OEA_LAUNCHED(ctx);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? OEA_OK : oea_check_cuda(ctx, e, "k_ep_sum");

@@ -239,8 +239,8 @@ size_t ffn_route_smem_bytes(int B, int Np, int stride);
 size_t ffn_bf16_smem_bytes();
 int gen_scores_launch(oea_ctx* ctx, const oea_score_gen_cfg& c, int step0, int nsteps,
                       double* out, cudaStream_t s);
-int ep_sum_launch(oea_ctx* ctx, const float* recv, const int* cnt, uint32_t expected, int world,
-                  int n, float* out, cudaStream_t s);
+int ep_sum_launch(oea_ctx* ctx, const float* recv, int* cnt, int per_launch, int world, int n,
+                  float* out, cudaStream_t s);
 size_t ffn_params_bytes();
 void ffn_params_set_io(void* params, const void* x_in, void* out);
 size_t ffn_btile_bytes();

@@ -164,8 +164,6 @@ class PeerExpertParallelMoE:
         self.cnt_ptrs = [0] * world
         self.recv_ptrs[rank], self.cnt_ptrs[rank] = self.recv_local, self.cnt_local
         self._opened = []
-        self.launches = 0
-        self.per_launch = self._lib.oea_ep_arrivals_per_launch(self.ctx.h, world)
 
     def handles(self):
         """64-byte IPC handles of (receive buffer, counter)."""
@@ -210,18 +208,16 @@ class PeerExpertParallelMoE:
         self.ctx.check(self._lib.oea_moe_decode_ep_partial(
             self.ctx.h, self.layer.h, C.c_void_p(x_all.data_ptr()), self.B, self.cfg.c_ref(),
             self.world, self.rank, recv, cnt, C.c_void_p(st)))
-        self.launches += 1
 
     def combine(self, out_local, stream=None):
         """Owner side: wait for every rank's partials of this launch, then
         out_local [B / world][D] = sum over ranks in rank order."""
         import ctypes as C
         from .moe_layer import torch_stream
-        expected = (self.launches * self.per_launch) & 0xFFFFFFFF
         st = stream if stream is not None else torch_stream()
         self.ctx.check(self._lib.oea_ep_combine(
-            self.ctx.h, C.c_void_p(self.recv_local), C.c_void_p(self.cnt_local), expected,
-            self.world, self.tpr, self.D, C.c_void_p(out_local.data_ptr()), C.c_void_p(st)))
+            self.ctx.h, C.c_void_p(self.recv_local), C.c_void_p(self.cnt_local), self.world,
+            self.tpr, self.D, C.c_void_p(out_local.data_ptr()), C.c_void_p(st)))
 
     def forward(self, x_all, out_local, stream=None):
         """x_all [B, D] bf16 (the all-gathered batch) -> out_local [B/world, D]."""

@@ -144,6 +144,29 @@ def test_peer_memory_ep_emulated(oea, P):
         got = torch.cat(outs)
         err = ((got - ref).norm(dim=1) / ref.norm(dim=1).clamp_min(1e-12)).max().item()
         assert err < 1e-5, (it, err)
+    # the same group captured in one CUDA graph (device-side arrival
+    # targets), replayed with fresh tokens
+    xs = torch.empty(B, D, device="cuda", dtype=torch.bfloat16)
+    outs = [torch.empty(tpr, D, device="cuda") for _ in range(P)]
+    xs.copy_(torch.randn(B, D, device="cuda").to(torch.bfloat16))
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(graph, stream=s):
+            for m in members:
+                m.partial(xs)
+            for m, o in zip(members, outs):
+                m.combine(o)
+    for it in range(2):
+        xs.copy_(torch.randn(B, D, device="cuda").to(torch.bfloat16))
+        graph.replay()
+        ref = torch.empty(B, D, device="cuda")
+        full.decode(xs, cfg, ref, stream=oea.moe_layer.torch_stream())
+        torch.cuda.synchronize()
+        got = torch.cat(outs)
+        err = ((got - ref).norm(dim=1) / ref.norm(dim=1).clamp_min(1e-12)).max().item()
+        assert err < 1e-5, ("graph", it, err)
     for m in members:
         m.close()
 
