@@ -394,15 +394,9 @@ bool fused_ok(const oea_layer* L, int B, const oea_routing_cfg& rc) {
 constexpr int kNotFused = -1000;  // decode_bf16(x_mapped): not on the fused path, nothing launched
 // x_mapped: x and out are device views of mapped (pinned) host memory; only
 // the fused single launch takes them (the caller checks fused_path()).
-struct EpArgs {  // peer-memory EP combine (oea_moe_decode_ep_partial)
-  int world, rank;
-  float* const* recv;
-  int32_t* const* cnt;
-};
-
 int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const uint8_t* mask,
                 int B, const oea_routing_cfg& rc, void* out, cudaStream_t s, int part = 0,
-                bool x_mapped = false, const EpArgs* ep = nullptr) {
+                bool x_mapped = false, const oea_dev::EpPeers* ep = nullptr) {
   const int stride = stride_of(rc);
   const Cfg cfg = dev_cfg(rc, stride);
   oea_host::FusedRouterBuffers rb;
@@ -497,15 +491,7 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
     if (r || part == 1) return r;
   }
   oea_host::FfnBuffers fb;
-  if (ep != nullptr) {
-    fb.ep_world = ep->world;
-    fb.ep_rank = ep->rank;
-    fb.ep_tpr = B / ep->world;
-    for (int o = 0; o < ep->world; ++o) {
-      fb.ep_recv[o] = ep->recv[o];
-      fb.ep_cnt[o] = ep->cnt[o];
-    }
-  }
+  fb.ep = ep;
   fb.x = padded || x_mapped ? static_cast<const void*>(w.xpad) : x;
   fb.row_tok = w.row_tok;
   fb.row_slot = w.row_slot;
@@ -692,6 +678,7 @@ int oea_ctx_destroy(oea_ctx_t ctx) {
     delete x;
   }
   if (ctx->ffn_trace) cudaFree(ctx->ffn_trace);
+  if (ctx->ep_tables) cudaFree(ctx->ep_tables);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
   return OEA_OK;
@@ -1296,10 +1283,39 @@ int oea_moe_decode_ep_partial(oea_ctx_t ctx, oea_layer_t L, const void* x_all_de
   ctx->last_N = L->N;
   ctx->last_stride = stride_of(rc);
   ctx->last_kind = 1;
-  const EpArgs ep{world, rank, recv, cnt};
   // (world == 1 keeps the combine local: out = the receive buffer itself)
-  return decode_bf16(ctx, w, L, x_all_dev, nullptr, B, rc, world > 1 ? nullptr : recv[0], s, 0,
-                     false, world > 1 ? &ep : nullptr);
+  if (world == 1) return decode_bf16(ctx, w, L, x_all_dev, nullptr, B, rc, recv[0], s);
+  // the peer table lives in device memory (uploaded once per distinct table,
+  // outside any stream capture; later calls, captured or not, reuse it)
+  oea_dev::EpPeers t{};
+  for (int o = 0; o < world; ++o) {
+    t.recv[o] = recv[o];
+    t.cnt[o] = cnt[o];
+  }
+  t.world = world;
+  t.rank = rank;
+  t.tpr = B / world;
+  constexpr int kMaxTables = 16;
+  if (ctx->ep_tables == nullptr)
+    OEA_CUDA_TRY(ctx, cudaMalloc(&ctx->ep_tables, kMaxTables * sizeof(oea_dev::EpPeers)));
+  int slot = -1;
+  for (int i = 0; i < static_cast<int>(ctx->ep_host_tables.size()); ++i)
+    if (std::memcmp(&ctx->ep_host_tables[i], &t, sizeof t) == 0) slot = i;
+  if (slot < 0) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    if (cs != cudaStreamCaptureStatusNone)
+      return fail(ctx, OEA_ERR_INVALID_ARGUMENT,
+                  "moe_decode_ep: run a new EP group once outside graph capture first");
+    if (static_cast<int>(ctx->ep_host_tables.size()) >= kMaxTables)
+      return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "moe_decode_ep: too many EP groups on one context");
+    slot = static_cast<int>(ctx->ep_host_tables.size());
+    OEA_CUDA_TRY(ctx, cudaMemcpy(static_cast<oea_dev::EpPeers*>(ctx->ep_tables) + slot, &t,
+                                 sizeof t, cudaMemcpyHostToDevice));
+    ctx->ep_host_tables.push_back(t);
+  }
+  return decode_bf16(ctx, w, L, x_all_dev, nullptr, B, rc, nullptr, s, 0, false,
+                     static_cast<const oea_dev::EpPeers*>(ctx->ep_tables) + slot);
 }
 
 int oea_ep_combine(oea_ctx_t ctx, const float* recv_local, int32_t* cnt_local, int32_t world,

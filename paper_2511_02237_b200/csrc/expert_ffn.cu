@@ -85,12 +85,6 @@ struct FfnParams {
   __nv_bfloat16* xpad_out;      // [B][Dp], written in-kernel when D != Dp, else null
   int x_stage;                  // x_in is mapped host memory: staged into xpad_out first
   int prefetch_bytes;           // speculative L2 prefetch of every held expert's first W1 bytes
-  // Expert-parallel combine over peer memory (oea_moe_decode_ep): the partial
-  // mixture of token t goes straight to its owner's receive buffer, slot
-  // [ep_rank][t - owner * ep_tpr], then every CTA bumps every owner's counter.
-  float* ep_recv[kMaxEpWorld];
-  int* ep_cnt[kMaxEpWorld];
-  int ep_world, ep_rank, ep_tpr;
   float* logits;        // [B][Np]
   const uint8_t* mask;
   int N, Np;
@@ -107,6 +101,11 @@ struct FfnParams {
   int32_t* x_base_union;
   int32_t* x_base_union_count;
   FfnHeader* x_hdr;
+  // Expert-parallel combine over peer memory (oea_moe_decode_ep_partial): the
+  // partial mixture of token t goes straight to its owner's receive buffer,
+  // slot [rank][t - owner * tpr], then every CTA bumps every owner's counter.
+  // (Last member: the offsets of the hot fields stay as they were.)
+  const EpPeers* ep;  // null: local combine into out
 };
 
 // The compacted plan's tables (global from the router kernel, or this CTA's
@@ -1308,8 +1307,9 @@ constexpr int kRoundRing = 8;  // > kStages: a round spans >= 1 stage
 template <int MODE>
 __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) {
   constexpr bool kFused = MODE != 0;
-  constexpr bool kDense = MODE == 2;
+  constexpr bool kDense = MODE == 2 || MODE == 5;
   constexpr bool kRouteOnly = MODE == 3;  // plan only (B > 64); the FFN runs as MODE 0
+  constexpr bool kEp = MODE >= 4;         // 4 / 5: MODE 1 / 2 with the peer-memory EP combine
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
@@ -1708,36 +1708,41 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
   asm volatile("bar.sync 2, %0;" ::"r"(kComb + 32) : "memory");
   if (warp == kRouterWarp) return;
   if (threadIdx.x == 0) stamp(P, 2);
-  for (int64_t f = f0 + threadIdx.x; f < f1; f += kComb) {
-    if (f != f0 + threadIdx.x) prep(f, len, yo, w, 0);
-    float sum = 0.0f;
-    for (int s0 = 0;;) {
-      float y[kSlotBatch];
+  // (the local and the EP store are separate instantiations of the loop)
+  auto combine = [&](auto store) {
+    for (int64_t f = f0 + threadIdx.x; f < f1; f += kComb) {
+      if (f != f0 + threadIdx.x) prep(f, len, yo, w, 0);
+      float sum = 0.0f;
+      for (int s0 = 0;;) {
+        float y[kSlotBatch];
 #pragma unroll
-      for (int j = 0; j < kSlotBatch; ++j) y[j] = yo[j] >= 0 ? __ldcg(P.ybuf + yo[j]) : 0.0f;
+        for (int j = 0; j < kSlotBatch; ++j) y[j] = yo[j] >= 0 ? __ldcg(P.ybuf + yo[j]) : 0.0f;
 #pragma unroll
-      for (int j = 0; j < kSlotBatch; ++j)
-        if (s0 + j < len) sum = fmaf(w[j], y[j], sum);
-      s0 += kSlotBatch;
-      if (s0 >= len) break;
-      prep(f, len, yo, w, s0);
+        for (int j = 0; j < kSlotBatch; ++j)
+          if (s0 + j < len) sum = fmaf(w[j], y[j], sum);
+        s0 += kSlotBatch;
+        if (s0 >= len) break;
+        prep(f, len, yo, w, s0);
+      }
+      store(f, sum);
     }
-    if (P.ep_world > 1) {
+  };
+  if constexpr (!kEp) {
+    combine([&](int64_t f, float v) { P.out[f] = v; });
+  } else {
+    const EpPeers* ep = P.ep;
+    const int tpr = ep->tpr, rank = ep->rank;
+    combine([&](int64_t f, float v) {
       const int t = static_cast<int>(f / P.D), d = static_cast<int>(f % P.D);
-      const int owner = t / P.ep_tpr;
-      P.ep_recv[owner][(static_cast<size_t>(P.ep_rank) * P.ep_tpr + (t - owner * P.ep_tpr)) * P.D +
-                       d] = sum;
-    } else {
-      P.out[f] = sum;
-    }
-  }
-  if (P.ep_world > 1) {
+      const int owner = t / tpr;
+      ep->recv[owner][(static_cast<size_t>(rank) * tpr + (t - owner * tpr)) * P.D + d] = v;
+    });
     // this CTA's remote stores are issued (all combining threads), made
     // visible system-wide, then counted at every owner (sum in k_ep_sum)
     asm volatile("bar.sync 2, %0;" ::"r"(kComb) : "memory");
     if (threadIdx.x == 0) {
       __threadfence_system();
-      for (int o = 0; o < P.ep_world; ++o) atomicAdd_system(P.ep_cnt[o], 1);
+      for (int o = 0; o < ep->world; ++o) atomicAdd_system(ep->cnt[o], 1);
     }
   }
   if (threadIdx.x == 0) stamp(P, 15);
@@ -1926,13 +1931,7 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   // reduction overhead, tools/trace_ffn.py): opt-in for experiments
   P.split_ok = getenv("OEA_SPLIT") != nullptr;
   P.x_stage = fb.x_stage;
-  P.ep_world = fb.ep_world;
-  P.ep_rank = fb.ep_rank;
-  P.ep_tpr = fb.ep_tpr;
-  for (int o = 0; o < kMaxEpWorld; ++o) {
-    P.ep_recv[o] = o < fb.ep_world ? fb.ep_recv[o] : nullptr;
-    P.ep_cnt[o] = o < fb.ep_world ? fb.ep_cnt[o] : nullptr;
-  }
+  P.ep = fb.ep;
   {
     // ~32 MiB in total, about what HBM delivers while the prologue routes
     // (measured C1, N=128: 128 KiB per expert saves ~1.3 us, 224-288 KiB
@@ -1972,9 +1971,18 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
                       (fb.fused ? ffn_route_smem_bytes(B, L->Np, stride) : 0) +
                       (fb.dense ? ffn_dense_xs_bytes(L->Dp) : 0) +
                       (fb.dense || fb.route_only ? 0 : ffn_btile_bytes());
-  const int mode = fb.route_only ? 3 : fb.dense ? 2 : fb.fused ? 1 : 0;
-  auto kern = mode == 3 ? k_ffn_bf16<3>
-                        : mode == 2 ? k_ffn_bf16<2> : mode == 1 ? k_ffn_bf16<1> : k_ffn_bf16<0>;
+  if (fb.ep != nullptr && (!fb.fused || fb.route_only))
+    return oea_set_error(ctx, OEA_ERR_INVALID_ARGUMENT, "moe_decode_ep: needs the fused path");
+  const int mode = fb.route_only ? 3
+                   : fb.dense   ? (fb.ep ? 5 : 2)
+                   : fb.fused   ? (fb.ep ? 4 : 1)
+                                : 0;
+  auto kern = mode == 5   ? k_ffn_bf16<5>
+              : mode == 4 ? k_ffn_bf16<4>
+              : mode == 3 ? k_ffn_bf16<3>
+              : mode == 2 ? k_ffn_bf16<2>
+              : mode == 1 ? k_ffn_bf16<1>
+                          : k_ffn_bf16<0>;
   if (static_cast<int>(smem) > ctx->ffn_smem_set[mode]) {  // once per size, not per launch
     OEA_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem)));

@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "oea_cuda.h"
 
@@ -35,6 +36,12 @@ constexpr int kRouterTokChunk = 64;    // tokens per GEMV pass in the router
 constexpr int kMaxFusedB = 256;        // fused decode batch limit
 constexpr int kMaxFusedN = 256;        // fused router expert limit (Np <= 256)
 constexpr int kMaxEpWorld = 8;  // expert-parallel group size of the peer-memory combine
+// Peer table of the EP combine (device memory, read by the combine stage).
+struct EpPeers {
+  float* recv[kMaxEpWorld];
+  int* cnt[kMaxEpWorld];
+  int world, rank, tpr;
+};
 constexpr int kMaxRouteN = 1024;       // route_f64 expert limit
 
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
@@ -81,7 +88,10 @@ struct oea_ctx {
   unsigned long long* ffn_trace = nullptr;
   int ffn_mode = 0;
   // dynamic shared memory already allowed per k_ffn_bf16<MODE> on this device
-  int ffn_smem_set[4] = {0, 0, 0, 0};
+  int ffn_smem_set[6] = {0, 0, 0, 0, 0, 0};
+  // EP peer tables uploaded so far (device copies; matched by content)
+  void* ep_tables = nullptr;
+  std::vector<oea_dev::EpPeers> ep_host_tables;
 };
 
 struct oea_layer {
@@ -213,9 +223,7 @@ struct FfnBuffers {
   const __nv_bfloat16* x_in = nullptr;  // [B][D] caller tokens
   __nv_bfloat16* xpad_out = nullptr;    // [B][Dp] when D != Dp (or x_stage)
   int x_stage = 0;                      // x_in is mapped host memory (staged in-kernel)
-  int ep_world = 0, ep_rank = 0, ep_tpr = 0;  // peer-memory EP combine (ep_world > 1)
-  float* ep_recv[oea_dev::kMaxEpWorld] = {};
-  int* ep_cnt[oea_dev::kMaxEpWorld] = {};
+  const oea_dev::EpPeers* ep = nullptr;  // peer-memory EP combine (device table), or null
   float* logits = nullptr;              // [B][Np]
   unsigned long long* xlog = nullptr;   // tagged exchange words (fused path)
   unsigned long long* xuni = nullptr;
