@@ -349,16 +349,20 @@ struct DeviceLayer {
   }
 };
 
-void upload(const LayerView& v, DeviceLayer& dl, bool router, bool experts) {
+// experts: which experts' weights to upload (null: none). moe_forward reads
+// only the experts its plan names, so only those cross the host link (the
+// others stay unwritten device memory that no kernel reads).
+void upload(const LayerView& v, DeviceLayer& dl, bool router, const std::vector<char>* experts) {
   oea_ctx_t c = ctx();
   check(oea_layer_create(c, v.D, v.H < 1 ? 1 : v.H, v.N, v.dtype, &dl.h), c);
   if (router && v.router) check(oea_layer_upload_router(dl.h, v.router, v.dtype, 0), c);
   if (experts)
     for (int e = 0; e < static_cast<int>(v.gate.size()); ++e)
-      check(oea_layer_upload_expert(dl.h, e, v.gate[static_cast<std::size_t>(e)],
-                                    v.up[static_cast<std::size_t>(e)],
-                                    v.down[static_cast<std::size_t>(e)], v.dtype, 0),
-            c);
+      if ((*experts)[static_cast<std::size_t>(e)])
+        check(oea_layer_upload_expert(dl.h, e, v.gate[static_cast<std::size_t>(e)],
+                                      v.up[static_cast<std::size_t>(e)],
+                                      v.down[static_cast<std::size_t>(e)], v.dtype, 0),
+              c);
 }
 
 }  // namespace
@@ -366,7 +370,7 @@ void upload(const LayerView& v, DeviceLayer& dl, bool router, bool experts) {
 void router_scores_device(const LayerView& layer, const double* x, int B, double* scores) {
   if (B == 0) return;
   DeviceLayer dl;
-  upload(layer, dl, true, false);
+  upload(layer, dl, true, nullptr);
   oea_ctx_t c = ctx();
   check(oea_router_scores_host(c, dl.h, x, B, scores), c);
 }
@@ -376,8 +380,14 @@ void moe_forward_device(const LayerView& layer, const double* x, int B,
                         const std::vector<double>& weights, int stride, const bool* mask,
                         double* out) {
   if (B == 0) return;
+  std::vector<char> used(layer.gate.size(), 0);
+  for (int i = 0; i < B; ++i)
+    for (int j = 0; j < set_len[static_cast<std::size_t>(i)] && j < stride; ++j) {
+      const int e = sets[static_cast<std::size_t>(i) * stride + j];
+      if (e >= 0 && e < static_cast<int>(used.size())) used[static_cast<std::size_t>(e)] = 1;
+    }
   DeviceLayer dl;
-  upload(layer, dl, false, true);
+  upload(layer, dl, false, &used);
   std::vector<int32_t> s(sets.begin(), sets.end()), l(set_len.begin(), set_len.end());
   oea_ctx_t c = ctx();
   check(oea_moe_forward_plan_host(c, dl.h, x, B, s.data(), l.data(), weights.data(), stride,

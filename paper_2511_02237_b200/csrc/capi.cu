@@ -66,6 +66,7 @@ struct Workspace {
   void* xin = nullptr;   // device copy of caller input (host entry points)
   void* out = nullptr;   // device output (host entry points)
   float* out32 = nullptr;
+  int32_t* alias = nullptr;  // caller plans with duplicated experts: y slot per plan slot
 };
 
 struct Need {
@@ -123,6 +124,7 @@ size_t carve(Workspace& w, bool assign) {
   take(w.xin, B * D * 8);
   take(w.out, B * D * 8);
   take(w.out32, B * D * 4);
+  take(w.alias, B * S * 4);
   return off + 256;
 }
 
@@ -387,7 +389,9 @@ int blocks_for(size_t n) {
 // only on it.
 bool fused_ok(const oea_layer* L, int B, const oea_routing_cfg& rc) {
   return B <= kRouterTokChunk && L->router_t != nullptr && L->Np <= 128 && (L->D & 7) == 0 &&
-         (rc.mode == OEA_MODE_VANILLA || (rc.p == 1.0 && rc.max_p >= L->N));
+         (rc.mode == OEA_MODE_VANILLA || (rc.p == 1.0 && rc.max_p >= L->N)) &&
+         oea_host::ffn_bf16_smem_bytes() + oea_host::ffn_btile_bytes() +
+                 oea_host::ffn_route_smem_bytes(B, L->Np, stride_of(rc)) <= 227 * 1024;
 }
 
 // part: 0 = router + FFN (PDL-chained), 1 = router only, 2 = FFN only.
@@ -435,9 +439,7 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   // covers N <= 128, p == 1 and D % 8 == 0; other shapes/configs use the pair.)
   const bool shard = L->n_local < L->N;
   const bool fused = part == 0 && fused_ok(L, B, rc) &&
-                     (shard || getenv("OEA_TWO_KERNEL") == nullptr) &&
-                     oea_host::ffn_bf16_smem_bytes() + oea_host::ffn_btile_bytes() +
-                             oea_host::ffn_route_smem_bytes(B, L->Np, stride) <= 227 * 1024;
+                     (shard || getenv("OEA_TWO_KERNEL") == nullptr);
   // Large batches (64 < B <= 256) with the rank-routing conditions: a
   // route-only launch of the fused prologue (tensor-core gate GEMV, rank
   // routing, union, plan rows), the compaction, then the FFN (three launches
@@ -594,7 +596,8 @@ int validate_decode(oea_ctx* ctx, oea_layer* L, int B, const oea_routing_cfg* cf
     if (L->n_local < L->N && !fused_ok(L, B, *rc))
       return fail(ctx, OEA_ERR_INVALID_ARGUMENT,
                   "moe_decode: expert-parallel shards need the fused path (B <= 64, N <= 128, "
-                  "D % 8 == 0, p == 1, max_p = N)");
+                  "D % 8 == 0, p == 1, max_p = N, and the batch's routing tables within the "
+                  "227 KiB of shared memory)");
   }
   return OEA_OK;
 }
@@ -1325,6 +1328,15 @@ int oea_ep_combine(oea_ctx_t ctx, const float* recv_local, int32_t* cnt_local, i
       world > oea_dev::kMaxEpWorld || tokens_per_rank < 1 || D < 1)
     return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "ep_combine: bad arguments");
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  if (world == 1) {
+    // oea_moe_decode_ep_partial with world == 1 decodes straight into
+    // recv[0] (no peer stores, no arrivals to wait for): the combine is a copy
+    if (recv_local != out_local)
+      OEA_CUDA_TRY(ctx, cudaMemcpyAsync(out_local, recv_local,
+                                        sizeof(float) * static_cast<size_t>(tokens_per_rank) * D,
+                                        cudaMemcpyDeviceToDevice, s));
+    return OEA_OK;
+  }
   return oea_host::ep_sum_launch(ctx, recv_local, cnt_local, world * ctx->num_sms, world,
                                  tokens_per_rank * D, out_local, s);
 }
@@ -1682,19 +1694,46 @@ int oea_moe_forward_plan_host(oea_ctx_t ctx, oea_layer_t L, const double* x, int
       const int e = sets[static_cast<size_t>(i) * set_stride + j];
       if (e < 0 || e >= L->N)
         return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "moe_forward: expert index out of range");
-      for (int jj = 0; jj < j; ++jj)
-        if (sets[static_cast<size_t>(i) * set_stride + jj] == e)
-          return fail(ctx, OEA_ERR_INVALID_ARGUMENT,
-                      "moe_forward: duplicate expert in the set of token " + std::to_string(i));
     }
+  }
+  // A caller plan may name an expert twice in one set: the reference then
+  // adds w_j * y_e once per occurrence, in set order (moe_layer.hpp:146-155).
+  // Each (token, expert) is computed once (the first occurrence's FFN row);
+  // later occurrences are dropped from the compaction (expert -1) and the
+  // fp64 set-order combine reads the first occurrence's y for them (alias).
+  std::vector<int32_t> usets, alias;
+  bool dups = false;
+  for (int i = 0; i < B && !dups; ++i)
+    for (int j = 1; j < set_len[i] && !dups; ++j)
+      for (int jj = 0; jj < j; ++jj)
+        if (sets[static_cast<size_t>(i) * set_stride + jj] == sets[static_cast<size_t>(i) * set_stride + j])
+          dups = true;
+  if (dups) {
+    usets.assign(sets, sets + static_cast<size_t>(B) * set_stride);
+    alias.resize(usets.size());
+    for (int i = 0; i < B; ++i)
+      for (int j = 0; j < set_stride; ++j) {
+        const size_t o = static_cast<size_t>(i) * set_stride + j;
+        alias[o] = j;
+        if (j >= set_len[i]) continue;
+        for (int jj = 0; jj < j; ++jj)
+          if (sets[static_cast<size_t>(i) * set_stride + jj] == sets[o]) {
+            alias[o] = jj;
+            usets[o] = -1;
+            break;
+          }
+      }
   }
   Workspace& w = extra(ctx)->ws;
   int r = ensure(ctx, w, need_for(L, B, set_stride));
   if (r) return r;
   cudaStream_t s = ctx->stream;
   OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.x64, x, sizeof(double) * B * L->D, cudaMemcpyHostToDevice, s));
-  OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.sets, sets, sizeof(int32_t) * B * set_stride,
-                                    cudaMemcpyHostToDevice, s));
+  OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.sets, dups ? usets.data() : sets,
+                                    sizeof(int32_t) * B * set_stride, cudaMemcpyHostToDevice, s));
+  if (dups)
+    OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.alias, alias.data(), sizeof(int32_t) * B * set_stride,
+                                      cudaMemcpyHostToDevice, s));
   // zero lengths of masked rows are already 0 in the caller's plan
   OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.set_len, set_len, sizeof(int32_t) * B, cudaMemcpyHostToDevice, s));
   OEA_CUDA_TRY(ctx, cudaMemcpyAsync(w.w64, weights, sizeof(double) * B * set_stride,
@@ -1730,9 +1769,17 @@ int oea_moe_forward_plan_host(oea_ctx_t ctx, oea_layer_t L, const double* x, int
     fb.out = w.out32;
     r = oea_host::ffn_bf16_launch(ctx, L, B, set_stride, fb, false, s);
     if (r) return r;
-    k_f32_to_f64<<<blocks_for(static_cast<size_t>(B) * L->D), 256, 0, s>>>(
-        w.out32, static_cast<size_t>(B) * L->D, static_cast<double*>(w.out));
-    OEA_LAUNCHED(ctx);
+    if (dups) {
+      fb.alias = w.alias;
+      fb.weights_f64 = w.w64;
+      fb.out = w.out;
+      r = oea_host::combine_alias_f32_launch(ctx, B, L->D, L->Dp, set_stride, fb, s);
+      if (r) return r;
+    } else {
+      k_f32_to_f64<<<blocks_for(static_cast<size_t>(B) * L->D), 256, 0, s>>>(
+          w.out32, static_cast<size_t>(B) * L->D, static_cast<double*>(w.out));
+      OEA_LAUNCHED(ctx);
+    }
   } else {
     r = oea_host::cast_f64_launch(ctx, w.x64, static_cast<size_t>(B) * L->D, L->dtype, w.xT, s);
     if (r) return r;
@@ -1749,6 +1796,7 @@ int oea_moe_forward_plan_host(oea_ctx_t ctx, oea_layer_t L, const double* x, int
     fb.set_len = w.set_len;
     fb.weights_f64 = w.w64;
     fb.out = w.out;
+    fb.alias = dups ? w.alias : nullptr;
     r = oea_host::ffn_simt_launch(ctx, L, B, set_stride, fb, w.G, s);
     if (r) return r;
   }

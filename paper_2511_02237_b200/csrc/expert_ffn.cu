@@ -1858,19 +1858,26 @@ __global__ void __launch_bounds__(128)
 }
 
 // out[t][d] = sum_j w[t][j] * double(y[t][j][d]) in set order, fp64
-// (moe_layer.hpp:153: out.row(i) += w[j] * expert_forward(...)).
+// (moe_layer.hpp:153: out.row(i) += w[j] * expert_forward(...)). y rows are
+// ldy apart; alias (optional, [B][stride]): slot j reads the y of slot
+// alias[t][j] (a duplicated expert in a caller plan is computed once and
+// accumulated once per occurrence, as the reference does).
 template <typename T>
-__global__ void k_simt_combine(int B, int D, int stride, const int32_t* __restrict__ set_len,
-                               const double* __restrict__ w, const T* __restrict__ ybuf,
+__global__ void k_simt_combine(int B, int D, int ldy, int stride,
+                               const int32_t* __restrict__ set_len, const double* __restrict__ w,
+                               const int32_t* __restrict__ alias, const T* __restrict__ ybuf,
                                double* __restrict__ out) {
   const size_t total = static_cast<size_t>(B) * D;
   for (size_t f = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; f < total;
        f += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const int t = static_cast<int>(f / D), d = static_cast<int>(f % D);
     double acc = 0.0;
-    for (int j = 0; j < set_len[t]; ++j)
-      acc = __dadd_rn(acc, __dmul_rn(w[static_cast<size_t>(t) * stride + j],
-                                     static_cast<double>(ybuf[(static_cast<size_t>(t) * stride + j) * D + d])));
+    for (int j = 0; j < set_len[t]; ++j) {
+      const size_t o = static_cast<size_t>(t) * stride + j;
+      const int js = alias ? alias[o] : j;
+      acc = __dadd_rn(acc, __dmul_rn(w[o], static_cast<double>(
+                                               ybuf[(static_cast<size_t>(t) * stride + js) * ldy + d])));
+    }
     out[f] = acc;
   }
 }
@@ -1993,13 +2000,28 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   cfg.blockDim = dim3(kFfnThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
+  // The kernel is persistent and spins on grid-wide counters (union
+  // exchange, W1 release, combine arrival): every CTA must be resident at
+  // once. The cooperative attribute makes the driver guarantee that (or fail
+  // the launch loudly, e.g. under an MPS SM limit), instead of a CTA waiting
+  // for an SM held by a concurrent kernel that may itself wait on this one.
   // PDL only as the router kernel's dependent (two-kernel path); the fused
   // launch carries no programmatic-serialization attribute at all.
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  static const bool coop = getenv("OEA_NO_COOP") == nullptr;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (coop) {
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na].val.cooperative = 1;
+    ++na;
+  }
+  if (pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = na;
   OEA_CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, P));
   OEA_LAUNCHED(ctx);
   return OEA_OK;
@@ -2039,9 +2061,22 @@ static int simt_impl(oea_ctx* ctx, const oea_layer* L, int B, int stride, const 
   OEA_LAUNCHED(ctx);
   const size_t total = static_cast<size_t>(B) * D;
   const int blocks = static_cast<int>((total + 255) / 256 > 4096 ? 4096 : (total + 255) / 256);
-  k_simt_combine<T><<<blocks, 256, 0, s>>>(B, D, stride, fb.set_len, fb.weights_f64,
-                                           static_cast<const T*>(fb.ybuf),
+  k_simt_combine<T><<<blocks, 256, 0, s>>>(B, D, D, stride, fb.set_len, fb.weights_f64,
+                                           fb.alias, static_cast<const T*>(fb.ybuf),
                                            static_cast<double*>(fb.out));
+  OEA_LAUNCHED(ctx);
+  return OEA_OK;
+}
+
+// bf16 layers, caller plan with duplicated experts: the fp64 set-order
+// combine over the FFN's fp32 y ([B][stride][Dp]) with the slot aliases.
+int combine_alias_f32_launch(oea_ctx* ctx, int B, int D, int Dp, int stride, const FfnBuffers& fb,
+                             cudaStream_t s) {
+  const size_t total = static_cast<size_t>(B) * D;
+  const int blocks = static_cast<int>((total + 255) / 256 > 4096 ? 4096 : (total + 255) / 256);
+  k_simt_combine<float><<<blocks, 256, 0, s>>>(B, D, Dp, stride, fb.set_len, fb.weights_f64,
+                                               fb.alias, static_cast<const float*>(fb.ybuf),
+                                               static_cast<double*>(fb.out));
   OEA_LAUNCHED(ctx);
   return OEA_OK;
 }

@@ -213,6 +213,7 @@ struct FfnBuffers {
   const float* weights_f32;
   const double* weights_f64;
   void* out;               // [B][D] f32 (bf16 path) / f64 (simt)
+  const int32_t* alias = nullptr;       // [B][stride] y slot per plan slot (duplicates), or null
   unsigned long long* trace = nullptr;  // debug timeline (OEA_FFN_TRACE)
   int mode = 0;                         // debug mode (OEA_FFN_MODE)
   // Fused single-launch decode (B <= 64): the FFN grid computes the logits
@@ -257,6 +258,8 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride,
                     const FfnBuffers& fb, bool pdl, cudaStream_t s);
 int ffn_simt_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride,
                     const FfnBuffers& fb, int max_rows, cudaStream_t s);
+int combine_alias_f32_launch(oea_ctx* ctx, int B, int D, int Dp, int stride, const FfnBuffers& fb,
+                             cudaStream_t s);
 
 // router_fused.cu — K2+K3 for bf16 layers.
 struct FusedRouterBuffers {

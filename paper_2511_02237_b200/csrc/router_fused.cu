@@ -96,7 +96,9 @@ __device__ void compact_plan(int B, int N, int stride, const int32_t* sets, cons
   __syncthreads();
   for (int idx = threadIdx.x; idx < B * stride; idx += blockDim.x) {
     const int t = idx / stride, sl = idx % stride;
-    if (sl < set_len[t]) {
+    // (e < 0: a duplicate (token, expert) slot of a caller plan, served by the
+    // y of its first occurrence, oea_moe_forward_plan_host)
+    if (sl < set_len[t] && sets[idx] >= 0) {
       const int e = sets[idx];
       atomicAdd(&s_loads[e], 1);
       atomicOr(&tokbits[e * Bw + (t >> 5)], 1u << (t & 31));
@@ -151,7 +153,7 @@ __device__ void compact_plan(int B, int N, int stride, const int32_t* sets, cons
   int my_total = 0;
   for (int idx = threadIdx.x; idx < B * stride; idx += blockDim.x) {
     const int t = idx / stride, sl = idx % stride;
-    if (sl < set_len[t]) {
+    if (sl < set_len[t] && sets[idx] >= 0) {
       ++my_total;
       const int e = sets[idx];
       const uint32_t* bits = tokbits + e * Bw;
