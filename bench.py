@@ -8,20 +8,34 @@ random bf16 weights with make_random_layer's distributions, OEA simplified
 routing k0=4 (headline) and vanilla top-8 (comparison).
 
 One "step" = one layer call: fused router (gate GEMV, ranking, batch union,
-piggyback, renormalisation, compaction) + grouped SwiGLU FFN + combine, as one
-CUDA graph. `value` = device µs per step (CUDA events on the launching stream,
-inputs resident); L2 is defeated by rotating 4 distinct layer copies (4.8 GB)
-and a distinct token batch per step (each call streams ~480 MB of expert
-weights, >> 126 MB L2). `e2e` = the same call through the C ABI from pinned
-host buffers (H2D of x, D2H of the output inside the timed region).
+piggyback, renormalisation, compaction) + grouped SwiGLU FFN + combine, one
+kernel launch. The K timed steps run back to back as ONE CUDA graph of K
+layer calls (the way a decode step's layers run; each fused launch is a
+programmatic dependent of its predecessor, PDL), between CUDA events on the
+launching stream; `value` = device µs per step, inputs resident. L2 is
+defeated by rotating 4 distinct layer copies (4.8 GB) and a distinct token
+batch per step (each call streams ~480 MB of expert weights, >> 126 MB L2).
+The same steps as one graph per call are reported as `isolated_graph_us`.
+`e2e` = the same call through the C ABI from pinned host buffers (the input
+copy in and the output copy out inside the timed region).
+
+Extra keys of the default line (same run, same clocks record): C3 (the
+Qwen3-235B-shaped layer, OEA and top-8), the C2 points at B=16 for k0=1..8
+(latency vs unique experts), and C5 (router-only B=4096 route).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
+--gpus N without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one per GPU). For N > 1 the line is
+EXPERT PARALLEL (BASELINE configs[3]): the C1 layer's experts sharded in
+contiguous blocks over the N GPUs, tokens data-parallel (B/N per rank), with
+NCCL all-to-all dispatch / combine (`value`), plus the all-gather +
+reduce-scatter and the peer-memory combine paths, the C3 layer sharded and
+the 94-layer C3-shaped stack; timings are max over ranks.
+
 --impl reference times the reference's own CPU path (router_scores + route +
 moe_forward<double>, compiled from the reference sources into oracle/_ref) on
-the host cores. Under torchrun (N > 1) each rank runs an independent replica
-(the single-layer path has no exchange; expert-parallel sharding is the
-94-layer C4 config); timings are max over ranks.
+the host cores (rank 0 only).
 """
 from __future__ import annotations
 
@@ -168,11 +182,22 @@ def cpu_reference_decode(calls: int, threads: int, cfg_tuple, steps: int = 1, wa
     for _ in range(warmup):
         one_step()
     vals = [one_step() for _ in range(max(1, steps))]
-    sample = (f"{calls} C1 decode calls per step (B=16, D=2048, H=768, N=128, simplified "
+    sample = (f"{calls} C1 decode call(s) per sample (B=16, D=2048, H=768, N=128, simplified "
               f"k0=4/k=8): router_scores + route + moe_forward<double> of the "
-              f"{'reference sources compiled with the Eigen-subset shim (-O3)' if kind == 'reference' else 'C restatement'}"
-              f", {threads} thread(s)")
+              f"{'reference sources compiled unmodified against the repo Eigen-subset shim (-O3; its naive loops stand in for Eigen GEMMs)' if kind == 'reference' else 'C restatement'}"
+              f", {threads} thread(s), {max(1, steps)} sample(s)")
     return vals, kind, threads, sample
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def run_reference_arm(args):
@@ -182,18 +207,23 @@ def run_reference_arm(args):
     threads = os.cpu_count() or 1
     calls = max(threads, 4)
     cfg = (3, K_TOP, K0, 1.0, K_TOP, 0, 0)  # simplified(4, 8)
-    # each step: one call per host thread (~0.5 s); the layer is built once
+    # each sample: `calls` layer calls spread over the host threads (~0.5 s);
+    # the layer is built once. A step = one layer call (as in our arm).
     vals, kind, cores, sample = cpu_reference_decode(calls, threads, cfg, steps=args.steps,
                                                      warmup=args.warmup)
-    us = statistics.mean(vals)
+    us = statistics.median(vals)
     line = {"impl": "reference", "metric": METRIC, "value": us, "unit": "us/layer-call",
-            "n_gpus": args.gpus, "steps": len(vals), "warmup": args.warmup, "ms_per_step": us / 1000.0,
+            "n_gpus": args.gpus, "steps": len(vals) * calls, "warmup": args.warmup * calls,
+            "ms_per_step": us / 1000.0,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: make_random_layer weights, make_random_batch tokens",
-            "config": {"workload": "C1 Qwen3-30B-A3B-shaped MoE decode layer, CPU reference",
-                       "D": D, "H": H, "N": N, "k": K_TOP, "B": B, "routing": "simplified(k0=4,k=8)"},
+            "config": {"workload": "C1 Qwen3-30B-A3B-shaped MoE decode layer (BASELINE configs[0])",
+                       "D": D, "H": H, "N": N, "k": K_TOP, "B": B,
+                       "routing": f"simplified(k0={K0}, k={K_TOP})", "parallelism": "host threads",
+                       "samples": len(vals), "calls_per_sample": calls,
+                       "statistic": "median over samples of (sample wall time / calls)"},
             "cpu_baseline": {"value": us, "unit": "us/layer-call", "cores": cores, "kind": kind,
-                             "sample": sample},
+                             "sample": sample, "nproc": os.cpu_count(), "cpu_model": cpu_model()},
             "e2e": {"value": us, "unit": "us/layer-call", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -248,6 +278,15 @@ def plan_stats(layers, xs, cfg, out, B, idx, ctx):
     return Ts, loads
 
 
+def _free_port() -> int:
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    return port
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -255,13 +294,21 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c1", choices=["c1", "c2", "c3", "c4", "c5", "sweep"],
-                    help="c1 = the headline line (default); c2 = B x k0 sweep + latency fit; "
-                         "c3 = Qwen3-235B-shaped layer; c4 = 94-layer EP stack (torchrun); "
-                         "c5 = router-only B=4096; sweep = the 673-config routing sweep "
-                         "on the GPU simulator vs the reference's sweep on the host")
+                    help="c1 = the headline line (default; N > 1: expert parallel); c2 = full "
+                         "B x k0 sweep + latency fit; c3 = Qwen3-235B-shaped layer; c4 = 94-layer "
+                         "EP stack; c5 = router-only B=4096; sweep = the 673-config routing "
+                         "sweep on the GPU simulator vs the reference's sweep on the host")
     ap.add_argument("--out-dir", default=os.path.join(ROOT, "gpurun_out", "bench"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="headline only (skip the C3 / C2 / C5 keys of the default line)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torch.distributed.run
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
     if args.impl == "reference":
         return run_reference_arm(args)
 
@@ -270,19 +317,68 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("OEA_BENCH_ONE_GPU"):  # functional check of N > 1 on one GPU
+        local = 0
     torch.cuda.set_device(local)
     os.environ["OEA_DEVICE"] = str(local)
     dist = None
-    if world > 1:
+    if world > 1 and os.environ.get("OEA_BENCH_ONE_GPU"):
+        # functional check of the N > 1 code on ONE GPU (NCCL refuses two ranks
+        # per device): gloo collectives staged through host memory; timings
+        # from such a run mean nothing
+        import torch.distributed as tdist
+        tdist.init_process_group("gloo")
+        dist = _HostStagedDist(tdist, torch)
+    elif world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     env = {"torch": torch, "dist": dist, "rank": rank, "world": world, "local": local}
-    fn = {"c1": bench_c1, "c2": bench_c2, "c3": bench_c3, "c4": bench_c4, "c5": bench_c5,
-          "sweep": bench_sweep}[args.config]
+    fn = {"c1": bench_c1 if world == 1 else bench_ep, "c2": bench_c2, "c3": bench_c3,
+          "c4": bench_c4, "c5": bench_c5, "sweep": bench_sweep}[args.config]
     rc = fn(args, env)
     if dist is not None:
         dist.destroy_process_group()
     return rc
+
+
+class _HostStagedDist:
+    """torch.distributed look-alike over a gloo group that stages CUDA tensors
+    through host memory (OEA_BENCH_ONE_GPU functional runs only)."""
+
+    def __init__(self, d, torch):
+        self.d, self.torch = d, torch
+        self.ReduceOp = d.ReduceOp
+
+    def __getattr__(self, name):
+        return getattr(self.d, name)
+
+    def _rt(self, fn, out, *ins, **kw):
+        outs = out.cpu()
+        fn(outs, *[i.cpu() for i in ins], **kw)
+        out.copy_(outs)
+
+    def all_gather_into_tensor(self, out, inp, group=None):
+        self._rt(self.d.all_gather_into_tensor, out, inp, group=group)
+
+    def reduce_scatter_tensor(self, out, inp, op=None, group=None):
+        # (gloo has no reduce_scatter: all-reduce the whole tensor, keep ours)
+        full = inp.cpu()
+        self.d.all_reduce(full, group=group)
+        out.copy_(full.chunk(self.d.get_world_size())[self.d.get_rank()])
+
+    def all_to_all_single(self, out, inp, group=None):
+        self._rt(self.d.all_to_all_single, out, inp, group=group)
+
+    def all_reduce(self, t, op=None, group=None):
+        c = t.cpu()
+        self.d.all_reduce(c, op=op or self.d.ReduceOp.SUM, group=group)
+        t.copy_(c)
+
+    def all_gather(self, outs, t, group=None):
+        co = [o.cpu() for o in outs]
+        self.d.all_gather(co, t.cpu(), group=group)
+        for o, c in zip(outs, co):
+            o.copy_(c)
 
 
 def _barrier(env):
@@ -299,9 +395,152 @@ def _max_over_ranks(env, v):
     return float(t.item())
 
 
+def time_chain(torch, stream, layers, xs, cfg, out, W, K, ctx):
+    """W warm-up then K timed layer calls (layers[i % len]: xs[i] -> out), each
+    block captured as ONE CUDA graph of back-to-back decode calls (PDL edges),
+    timed with CUDA events on the launching stream. Returns (µs per call,
+    kernels launched by this library in the timed region)."""
+    import paper_2511_02237_b200 as oea
+    R = len(layers)
+    warm = oea.DeviceMoeLayer.chain_graph([layers[i % R] for i in range(W)], list(xs[:W]), cfg,
+                                          [out] * W)
+    timed = oea.DeviceMoeLayer.chain_graph([layers[i % R] for i in range(W, W + K)],
+                                           list(xs[W:W + K]), cfg, [out] * K)
+    warm.launch()
+    torch.cuda.synchronize()
+    l0 = ctx.kernel_launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        timed.launch()
+        e1.record(stream)
+    e1.synchronize()
+    us = e0.elapsed_time(e1) * 1000.0 / K
+    launched = ctx.kernel_launches - l0
+    warm.close()
+    timed.close()
+    return us, launched
+
+
+def fit_points(pts):
+    """OLS of µs on T over (T, µs) points (latency.cpp fit_linear's model)."""
+    from paper_2511_02237_b200 import latency as lat
+    f = lat.fit_linear([lat.LatencyObservation(t, u) for t, u in pts])
+    return {"slope_us_per_expert": f.b_us, "intercept_us": f.intercept_us,
+            "r_squared": f.r_squared}
+
+
+def c3_extra(torch, stream, W, K, peak):
+    """C3 (BASELINE configs[2]): the Qwen3-235B-A22B-shaped layer (D=4096,
+    H=1536, N=128, k=8), B=16, OEA simplified(4, 8) and top-8."""
+    import numpy as np
+    import paper_2511_02237_b200 as oea
+    D3, H3 = 4096, 1536
+    layers = []
+    for r in range(2):  # 2 x 4.83 GB; each call streams ~2-3 GB (>> 126 MB L2)
+        L = oea.DeviceMoeLayer(D3, H3, N, "bf16")
+        L.init_random(11 + r)
+        layers.append(L)
+    ctx = layers[0].ctx
+    gen = torch.Generator(device="cuda").manual_seed(99)
+    xs = torch.randn(W + K, B, D3, device="cuda", generator=gen).to(torch.bfloat16)
+    out = torch.empty(B, D3, device="cuda", dtype=torch.float32)
+    res = {}
+    for name, cfg in (("oea", oea.RoutingConfig.simplified(K0, K_TOP)),
+                      ("vanilla", oea.RoutingConfig.vanilla(K_TOP))):
+        us, _ = time_chain(torch, stream, layers, xs, cfg, out, W, K, ctx)
+        Ts, _ = plan_stats(layers, xs, cfg, out, B, range(W, W + K), ctx)
+        T = float(np.mean(Ts))
+        lb = layer_bytes(T, D3, H3, N, B)
+        res[name] = {"us": us, "T_mean": T, "GBps": lb / us / 1e3, "frac": lb / us / 1e3 / peak}
+    res["latency_ratio_oea_vs_vanilla"] = res["oea"]["us"] / res["vanilla"]["us"]
+    res["unique_expert_ratio_oea_vs_vanilla"] = res["oea"]["T_mean"] / res["vanilla"]["T_mean"]
+    res["config"] = {"D": D3, "H": H3, "N": N, "k": K_TOP, "B": B, "steps": K}
+    for L in layers:
+        L.close()
+    return res
+
+
+def c2_b16_extra(torch, stream, layers, W, K, peak):
+    """C2 (BASELINE configs[1]) at B=16: k0 = 1..8 (k0 = 8 is top-8) on the C1
+    layers: unique experts T vs µs per call, and the OLS line through them."""
+    import numpy as np
+    import paper_2511_02237_b200 as oea
+    ctx = layers[0].ctx
+    gen = torch.Generator(device="cuda").manual_seed(4321)
+    xs = torch.randn(W + K, B, D, device="cuda", generator=gen).to(torch.bfloat16)
+    out = torch.empty(B, D, device="cuda", dtype=torch.float32)
+    pts = []
+    for k0 in range(1, K_TOP + 1):
+        cfg = oea.RoutingConfig.simplified(k0, K_TOP)
+        us, _ = time_chain(torch, stream, layers, xs, cfg, out, W, K, ctx)
+        Ts, _ = plan_stats(layers, xs, cfg, out, B, range(W, W + K), ctx)
+        T = float(np.mean(Ts))
+        lb = layer_bytes(T, D, H, N, B)
+        pts.append({"k0": k0, "T_mean": T, "us": us, "frac": lb / us / 1e3 / peak})
+    return {"B": B, "steps_per_point": K, "points": pts,
+            "fit": fit_points([(p["T_mean"], p["us"]) for p in pts]),
+            "slope_at_measured_hbm_us": 3 * D * H * 2 / peak / 1e3}
+
+
+def c5_extra(torch, W, K):
+    """C5 (BASELINE configs[4]): router-only B=4096 x N=128 fp64 route (the
+    bit-exact route_f64 path on device-resident scores), k0 = 1..8."""
+    import ctypes as C
+    import paper_2511_02237_b200 as oea
+    from paper_2511_02237_b200._capi import PlanViewC, default_context, lib
+    from paper_2511_02237_b200.moe_layer import torch_stream
+    ctx = default_context()
+    Bc, Nc = 4096, 128
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    scores = torch.softmax(torch.randn(Bc, Nc, device="cuda", dtype=torch.float64,
+                                       generator=gen), dim=1)
+    res = []
+    for k0 in range(1, K_TOP + 1):
+        cfg = oea.RoutingConfig.simplified(k0, K_TOP)
+        stride = oea.plan_set_stride(cfg.resolved(Nc))
+        sets = torch.empty(Bc, stride, dtype=torch.int32, device="cuda")
+        set_len = torch.empty(Bc, dtype=torch.int32, device="cuda")
+        w = torch.empty(Bc, stride, dtype=torch.float64, device="cuda")
+        loads = torch.empty(Nc, dtype=torch.int32, device="cuda")
+        au = torch.empty(Nc, dtype=torch.int32, device="cuda")
+        cnt = torch.empty(1, dtype=torch.int32, device="cuda")
+        tot = torch.empty(1, dtype=torch.int64, device="cuda")
+        pv = PlanViewC(stride, sets.data_ptr(), set_len.data_ptr(), w.data_ptr(), None,
+                       loads.data_ptr(), au.data_ptr(), cnt.data_ptr(), tot.data_ptr(),
+                       None, None, None, None, None)
+        c = cfg.to_c()
+
+        def call():
+            ctx.check(lib().oea_route_f64(ctx.h, C.c_void_p(scores.data_ptr()), None, Bc, Nc,
+                                          C.byref(c), C.byref(pv), C.c_void_p(torch_stream())))
+        for _ in range(W):
+            call()
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for _ in range(K):  # K route calls back to back in one graph
+                call()
+        graph.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        graph.replay()
+        e1.record()
+        e1.synchronize()
+        us = e0.elapsed_time(e1) * 1000.0 / K
+        del graph
+        # algorithmic bytes: fp64 scores in; sets (int32), weights (fp64), set_len out
+        byts = Bc * Nc * 8 + Bc * stride * 12 + Bc * 4
+        res.append({"k0": k0, "us": us, "tokens_per_s": Bc / us * 1e6, "T": int(cnt.item()),
+                    "GBps": byts / us / 1e3})
+    return {"B": Bc, "N": Nc, "k": K_TOP, "steps": K, "sweep": res,
+            "us_k0_4": res[3]["us"]}
+
+
 def bench_c1(args, env):
     """The headline: C1 Qwen3-30B-A3B-shaped layer, B=16, OEA simplified(4, 8)
-    vs vanilla top-8 (BASELINE.json configs[0])."""
+    vs vanilla top-8 (BASELINE.json configs[0]); one GPU."""
     import numpy as np
     torch, rank, world, local = env["torch"], env["rank"], env["world"], env["local"]
     import paper_2511_02237_b200 as oea
@@ -319,35 +558,38 @@ def bench_c1(args, env):
     torch.cuda.synchronize()
     stream = torch.cuda.ExternalStream(ctx.stream)
     cfgs = {"oea": oea.RoutingConfig.simplified(K0, K_TOP), "vanilla": oea.RoutingConfig.vanilla(K_TOP)}
+    peak, peak_src = load_peak()
 
     results = {}
     clocks = None
     launches = 0
     for name, cfg in cfgs.items():
-        graphs = [layers[i % ROTATE].graph(xs[i], cfg, out) for i in range(W + K)]
-        _barrier(env)
         sampler = ClockSampler(local) if name == "oea" else None
         if sampler:
             sampler.__enter__()
-        us, _, launched = time_graphs(torch, stream, graphs, W, ctx=ctx)
+        us, launched = time_chain(torch, stream, layers, xs, cfg, out, W, K, ctx)
         if sampler:
             sampler.__exit__()
             clocks = sampler.summary()
         if name == "oea":
             launches = launched
-        _barrier(env)
-        us = _max_over_ranks(env, us)
         Ts, loads = plan_stats(layers, xs, cfg, out, B, range(W, W + K), ctx)
         T = float(np.mean(Ts))
         lb = layer_bytes(T, D, H, N, B)
         results[name] = {"us": us, "T_mean": T, "T_min": int(min(Ts)), "T_max": int(max(Ts)),
                          "total_load_mean": float(np.mean(loads)), "active_bytes": lb,
-                         "GBps": lb / us / 1e3, "kernels_per_call": launched / K}
-        for g in graphs:
-            g.close()
+                         "GBps": lb / us / 1e3, "frac": lb / us / 1e3 / peak,
+                         "kernels_per_call": launched / K}
+
+    # The previous methodology: one graph (one launch) per call, so each call
+    # pays the graph-to-graph launch gap.
+    cfg = cfgs["oea"]
+    graphs = [layers[i % ROTATE].graph(xs[i], cfg, out) for i in range(W + K)]
+    iso_us, _, _ = time_graphs(torch, stream, graphs, W, ctx=ctx)
+    for g in graphs:
+        g.close()
 
     # The two-kernel path (router cluster | FFN), for reference: per-stage times.
-    cfg = cfgs["oea"]
     stage = [layers[r].stage_graphs(xs[r], cfg, out) for r in range(ROTATE)]
     for i in range(W):
         stage[i % ROTATE][0].launch()
@@ -371,10 +613,9 @@ def bench_c1(args, env):
 
     # Roofline of the dominant (and only) kernel of the layer call: the fused
     # single-launch decode k_ffn_bf16<2> (gate GEMV + routing + grouped SwiGLU
-    # + combine). One graph = one launch, so the event-timed step IS the
-    # kernel's average launch duration.
+    # + combine). One call = one launch, so the event-timed step IS the
+    # kernel's average launch duration (plus the ~1 µs PDL launch gap).
     o, v = results["oea"], results["vanilla"]
-    peak, peak_src = load_peak()
     traffic, traffic_ratio = load_traffic()
     roofline = {"bound": "hbm", "achieved": o["GBps"], "peak": peak, "unit": "GB/s",
                 "frac": o["GBps"] / peak, "traffic": traffic,
@@ -398,21 +639,30 @@ def bench_c1(args, env):
     for i in range(W):
         ctypes.memmove(sp, x_src[i].data_ptr(), xb)
         layers[i % ROTATE].decode_host_ptr(sp, op, B, cfg)
-    _barrier(env)
     t0 = time.perf_counter()
     for i in range(W, W + K):
         ctypes.memmove(sp, x_src[i].data_ptr(), xb)
         layers[i % ROTATE].decode_host_ptr(sp, op, B, cfg)
     e2e_us = (time.perf_counter() - t0) * 1e6 / K
-    e2e_us = _max_over_ranks(env, e2e_us)
+
+    extras = {}
+    if not args.no_extras:
+        for key, fn in (("c2_b16", lambda: c2_b16_extra(torch, stream, layers, W, min(K, 20), peak)),
+                        ("c3", lambda: c3_extra(torch, stream, W, min(K, 20), peak)),
+                        ("c5", lambda: c5_extra(torch, W, 50))):
+            try:
+                extras[key] = fn()
+            except Exception as e:  # an extra key never costs the headline line
+                extras[key] = {"error": f"{type(e).__name__}: {e}"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         try:
-            vals, kind, cores, sample = cpu_reference_decode(3, 1, (3, K_TOP, K0, 1.0, K_TOP, 0, 0))
-            us_cpu = vals[0]
-            cpu = {"value": us_cpu, "unit": "us/layer-call", "cores": cores, "kind": kind,
-                   "sample": sample}
+            vals, kind, cores, sample = cpu_reference_decode(1, 1, (3, K_TOP, K0, 1.0, K_TOP, 0, 0),
+                                                             steps=5)
+            cpu = {"value": statistics.median(vals), "unit": "us/layer-call", "cores": cores,
+                   "kind": kind, "sample": sample + "; median of the samples",
+                   "nproc": os.cpu_count(), "cpu_model": cpu_model()}
         except Exception as e:  # the CPU baseline is reported, never required
             cpu = {"value": None, "unit": "us/layer-call", "cores": 1, "kind": "port",
                    "sample": f"failed: {e}"}
@@ -426,13 +676,16 @@ def bench_c1(args, env):
         "config": {"workload": "C1 Qwen3-30B-A3B-shaped MoE decode layer (BASELINE configs[0])",
                    "D": D, "H": H, "N": N, "k": K_TOP, "B": B,
                    "routing": f"simplified(k0={K0}, k={K_TOP}) vs vanilla top-{K_TOP}",
-                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
+                   "parallelism": "single GPU",
+                   "timing": f"{K} layer calls back to back in one CUDA graph (PDL edges), "
+                             "CUDA events on the launching stream",
                    "l2": f"rotating {ROTATE} distinct layer copies ({ROTATE * 1.21:.1f} GB) and a "
                          "distinct token batch per step; each call streams >400 MB of expert "
                          "weights (> 126 MB L2)"},
         "oea": o, "vanilla": v,
         "latency_ratio_oea_vs_vanilla": o["us"] / v["us"],
         "unique_expert_ratio_oea_vs_vanilla": o["T_mean"] / v["T_mean"],
+        "isolated_graph_us": iso_us,
         "two_kernel_path_us": two_kernel,
         "roofline": roofline,
         "cpu_baseline": cpu,
@@ -441,9 +694,298 @@ def bench_c1(args, env):
         "gpu_launches": launches,
         "clocks": clocks,
     }
+    line.update(extras)
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
+
+
+def _ep_time(env, step, W, K, capture=True):
+    """Two eager steps (workspace sizing, NCCL communicators), then K steps
+    captured as ONE CUDA graph (collectives included), replayed once as the
+    warm-up and once between CUDA events; max over ranks. Without capture: W
+    eager warm-up steps and K timed eager steps. Returns (µs per step, mode)."""
+    torch = env["torch"]
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    graph, mode = None, "eager"
+    if capture:
+        try:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                for _ in range(K):
+                    step()
+            mode = "cuda-graph"
+        except Exception as e:  # pragma: no cover - eager fallback
+            graph, mode = None, f"eager ({type(e).__name__})"
+            torch.cuda.synchronize()
+
+    def timed():
+        if graph is not None:
+            graph.replay()
+        else:
+            for _ in range(K):
+                step()
+    if graph is not None:
+        graph.replay()
+    else:
+        for _ in range(W):
+            step()
+    torch.cuda.synchronize()
+    _barrier(env)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    timed()
+    e1.record()
+    e1.synchronize()
+    us = e0.elapsed_time(e1) * 1000.0 / K
+    del graph
+    return _max_over_ranks(env, us), mode
+
+
+def bench_ep(args, env):
+    """N > 1 (torchrun): expert parallelism (BASELINE configs[3], SURVEY
+    §8(e)). The C1 layer's experts are sharded in contiguous blocks over the
+    N ranks (ep.ep_expert_range), tokens data-parallel (B/N rows per rank).
+    `value` = µs per layer call (max over ranks) with NCCL all-to-all token
+    dispatch and fp32 combine (ep.AllToAllExpertParallelMoE); the
+    all-gather + reduce-scatter path and the peer-memory combine fused into
+    the shard decode are reported next to it, with the C3 layer sharded the
+    same way and the 94-layer C3-shaped stack."""
+    import numpy as np
+    torch, dist, rank, world, local = (env["torch"], env["dist"], env["rank"], env["world"],
+                                       env["local"])
+    import paper_2511_02237_b200 as oea
+    from paper_2511_02237_b200 import ep
+    W, K = max(3, args.warmup), max(1, min(args.steps, 40))
+    if B % world:
+        raise SystemExit(f"EP: B={B} must split over {world} ranks")
+    peak, peak_src = load_peak()
+    e0, e1 = ep.ep_expert_range(N, world, rank)
+    t0, t1 = ep.ep_token_range(B, world, rank)
+    rows = t1 - t0
+    # the same seeds on every rank: shard r holds experts [e0, e1) of the same
+    # full layer (the router is whole on every rank)
+    shards = []
+    for r in range(ROTATE):
+        L = oea.DeviceMoeLayer(D, H, N, "bf16", experts=(e0, e1))
+        L.init_random(1 + r)
+        shards.append(L)
+    ctx = shards[0].ctx
+    gen = torch.Generator(device="cuda").manual_seed(1234)
+    xs_full = torch.randn(W + K, B, D, device="cuda", generator=gen).to(torch.bfloat16)
+    xs = xs_full[:, t0:t1].contiguous()
+    out_local = torch.empty(rows, D, device="cuda", dtype=torch.float32)
+    bufs = {"x_all": torch.empty(B, D, device="cuda", dtype=torch.bfloat16),
+            "partial": torch.empty(B, D, device="cuda", dtype=torch.float32)}
+    cfgs = {"oea": oea.RoutingConfig.simplified(K0, K_TOP), "vanilla": oea.RoutingConfig.vanilla(K_TOP)}
+
+    def per_rank_T(layer, cfg, x_all):
+        layer.decode(x_all, cfg, bufs["partial"])
+        torch.cuda.synchronize()
+        plan = layer.last_plan(B, cfg)
+        act = [int(e) for e in plan["active_union"]]
+        t_r = torch.tensor([sum(1 for e in act if e0 <= e < e1)], device="cuda")
+        allt = [torch.zeros_like(t_r) for _ in range(world)]
+        dist.all_gather(allt, t_r)
+        return int(plan["active_count"]), [int(v.item()) for v in allt]
+
+    res = {}
+    clocks = None
+    launches = 0
+    for name, cfg in cfgs.items():
+        mods = [ep.make_ep_layer("a2a", shards[r], cfg, world, rank, dist) for r in range(ROTATE)]
+        recv = torch.empty(world, rows, D, device="cuda", dtype=torch.float32)
+        it = [0]
+
+        def step():
+            i = it[0] % (W + K)
+            it[0] += 1
+            mods[i % ROTATE].forward(xs[i], out_local, recv=recv, **bufs)
+        sampler = ClockSampler(local) if name == "oea" else None
+        if sampler:
+            sampler.__enter__()
+        l0 = ctx.kernel_launches
+        us, mode = _ep_time(env, step, W, K)
+        if sampler:
+            sampler.__exit__()
+            clocks = sampler.summary()
+        if name == "oea":
+            launches = (ctx.kernel_launches - l0)
+        Ts, Trs = [], []
+        for i in range(W, W + min(K, 8)):
+            T, tr = per_rank_T(shards[i % ROTATE], cfg, xs_full[i])
+            Ts.append(T)
+            Trs.append(tr)
+        T = float(np.mean(Ts))
+        maxTr = float(np.mean([max(v) for v in Trs]))
+        lb_rank = maxTr * 3 * D * H * 2 + D * N * 2 + B * D * 2 + B * D * 4
+        res[name] = {"us": us, "mode": mode, "T_mean": T, "max_rank_T_mean": maxTr,
+                     "per_rank_T_first": Trs[0],
+                     "GBps_busiest_rank": lb_rank / us / 1e3,
+                     "frac_busiest_rank": lb_rank / us / 1e3 / peak}
+    o = res["oea"]
+
+    # the other data paths (OEA): all-gather + reduce-scatter, peer memory
+    paths = {"a2a": {"us": o["us"]}}
+    cfg = cfgs["oea"]
+    try:
+        mods = [ep.make_ep_layer("ag_rs", shards[r], cfg, world, rank, dist) for r in range(ROTATE)]
+        it = [0]
+
+        def step_ag():
+            i = it[0] % (W + K)
+            it[0] += 1
+            mods[i % ROTATE].forward(xs[i], out_local, **bufs)
+        paths["ag_rs"] = {"us": _ep_time(env, step_ag, W, K)[0]}
+    except Exception as e:
+        paths["ag_rs"] = {"error": f"{type(e).__name__}: {e}"}
+    try:
+        peers = [ep.PeerExpertParallelMoE(shards[r], cfg, world, rank, B) for r in range(ROTATE)]
+        for pm in peers:
+            pm.connect(dist)
+        it = [0]
+
+        def step_peer():
+            i = it[0] % (W + K)
+            it[0] += 1
+            dist.all_gather_into_tensor(bufs["x_all"], xs[i])
+            peers[i % ROTATE].forward(bufs["x_all"], out_local)
+        paths["peer"] = {"us": _ep_time(env, step_peer, W, K)[0],
+                         "note": "NCCL all-gather of the tokens, shard decode whose combine "
+                                 "stores partials into the owners' memory (CUDA IPC), owner sum"}
+        _barrier(env)
+        torch.cuda.synchronize()
+        for pm in peers:
+            pm.close()
+    except Exception as e:
+        paths["peer"] = {"error": f"{type(e).__name__}: {e}"}
+
+    extras = {}
+    if not args.no_extras:
+        try:
+            extras["c3_sharded"] = _ep_c3(env, W, min(K, 20), peak)
+        except Exception as e:
+            extras["c3_sharded"] = {"error": f"{type(e).__name__}: {e}"}
+        try:
+            extras["c4_stack"] = _ep_c4(env, W, min(K, 5))
+        except Exception as e:
+            extras["c4_stack"] = {"error": f"{type(e).__name__}: {e}"}
+
+    line = {"metric": METRIC, "value": o["us"], "unit": "us/layer-call", "n_gpus": world,
+            "steps": K, "warmup": W, "ms_per_step": o["us"] / 1000.0, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic: random bf16 weights with make_random_layer distributions, "
+                    "N(0,1) bf16 tokens",
+            "config": {"workload": "C1 Qwen3-30B-A3B-shaped MoE decode layer, expert parallel "
+                                   "(BASELINE configs[0] layer, configs[3] parallelism)",
+                       "D": D, "H": H, "N": N, "k": K_TOP, "B": B,
+                       "routing": f"simplified(k0={K0}, k={K_TOP}) vs vanilla top-{K_TOP}",
+                       "parallelism": f"ep{world}: experts [{N}r/{world}, {N}(r+1)/{world}) on "
+                                      f"rank r, tokens {B // world} per rank; NCCL all-to-all "
+                                      "dispatch + combine",
+                       "timing": f"{K} layer calls in one CUDA graph per rank, CUDA events, "
+                                 "max over ranks",
+                       "l2": f"rotating {ROTATE} distinct layers and a distinct batch per step"},
+            "oea": o, "vanilla": res["vanilla"],
+            "latency_ratio_oea_vs_vanilla": o["us"] / res["vanilla"]["us"],
+            "unique_expert_ratio_oea_vs_vanilla": o["T_mean"] / res["vanilla"]["T_mean"],
+            "paths_oea_us": paths,
+            "roofline": {"bound": "hbm", "achieved": o["GBps_busiest_rank"], "peak": peak,
+                         "unit": "GB/s", "frac": o["frac_busiest_rank"], "traffic": None,
+                         "kernel": "k_ffn_bf16<2> shard decode + NCCL all-to-all",
+                         "note": "bytes of the busiest rank (max_r T_r experts) over the whole "
+                                 "layer call incl. the collectives", "peak_source": peak_src},
+            "cpu_baseline": None,
+            "e2e": None,
+            "gpu_launches": launches,
+            "clocks": clocks}
+    line.update(extras)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def _ep_c3(env, W, K, peak):
+    """The C3 layer (D=4096, H=1536) sharded over the ranks, a2a path."""
+    import numpy as np
+    torch, dist, rank, world = env["torch"], env["dist"], env["rank"], env["world"]
+    import paper_2511_02237_b200 as oea
+    from paper_2511_02237_b200 import ep
+    D3, H3 = 4096, 1536
+    e0, e1 = ep.ep_expert_range(N, world, rank)
+    t0, t1 = ep.ep_token_range(B, world, rank)
+    shards = []
+    for r in range(2):
+        L = oea.DeviceMoeLayer(D3, H3, N, "bf16", experts=(e0, e1))
+        L.init_random(11 + r)
+        shards.append(L)
+    gen = torch.Generator(device="cuda").manual_seed(99)
+    xs = torch.randn(W + K, B, D3, device="cuda", generator=gen).to(torch.bfloat16)[:, t0:t1].contiguous()
+    out_local = torch.empty(t1 - t0, D3, device="cuda", dtype=torch.float32)
+    bufs = {"x_all": torch.empty(B, D3, device="cuda", dtype=torch.bfloat16),
+            "partial": torch.empty(B, D3, device="cuda", dtype=torch.float32)}
+    recv = torch.empty(world, t1 - t0, D3, device="cuda", dtype=torch.float32)
+    res = {}
+    for name, cfg in (("oea", oea.RoutingConfig.simplified(K0, K_TOP)),
+                      ("vanilla", oea.RoutingConfig.vanilla(K_TOP))):
+        mods = [ep.make_ep_layer("a2a", shards[r], cfg, world, rank, dist) for r in range(2)]
+        it = [0]
+
+        def step():
+            i = it[0] % (W + K)
+            it[0] += 1
+            mods[i % 2].forward(xs[i], out_local, recv=recv, **bufs)
+        res[name] = {"us": _ep_time(env, step, W, K)[0]}
+    res["latency_ratio_oea_vs_vanilla"] = res["oea"]["us"] / res["vanilla"]["us"]
+    for L in shards:
+        L.close()
+    return res
+
+
+def _ep_c4(env, W, K):
+    """The 94-layer C3-shaped stack (BASELINE configs[3]), a2a path: per
+    layer the fused residual + RMSNorm, the EP layer; one graph per step."""
+    torch, dist, rank, world = env["torch"], env["dist"], env["rank"], env["world"]
+    import paper_2511_02237_b200 as oea
+    from paper_2511_02237_b200 import ep
+    D4, H4, NL = 4096, 1536, 94
+    e0, e1 = ep.ep_expert_range(N, world, rank)
+    t0, t1 = ep.ep_token_range(B, world, rank)
+    shard_bytes = (e1 - e0) * 3 * D4 * H4 * 2 + D4 * N * 2 * 2
+    free, _ = torch.cuda.mem_get_info()
+    R = int(max(1, min(16, (free * 0.70 - (4 << 30)) // shard_bytes)))
+    t = torch.tensor([R], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    R = int(t.item())
+    pool = []
+    for l in range(R):
+        L = oea.DeviceMoeLayer(D4, H4, N, "bf16", experts=(e0, e1))
+        L.init_random(1000 + l)
+        pool.append(L)
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    x_full = torch.randn(B, D4, device="cuda", generator=gen).to(torch.bfloat16)
+    h0 = x_full[t0:t1].float().contiguous()
+    h_local = torch.empty_like(h0)
+    out_local = torch.empty(t1 - t0, D4, device="cuda", dtype=torch.float32)
+    bufs = {"x_all": torch.empty(B, D4, device="cuda", dtype=torch.bfloat16),
+            "partial": torch.empty(B, D4, device="cuda", dtype=torch.float32),
+            "recv": torch.empty(world, t1 - t0, D4, device="cuda", dtype=torch.float32)}
+    res = {"layers": NL, "distinct_layers_resident": R, "experts_per_rank": e1 - e0}
+    for name, cfg in (("oea", oea.RoutingConfig.simplified(K0, K_TOP)),
+                      ("vanilla", oea.RoutingConfig.vanilla(K_TOP))):
+        stack = [ep.make_ep_layer("a2a", pool[l % R], cfg, world, rank, dist) for l in range(NL)]
+
+        def step():
+            h_local.copy_(h0)
+            ep.residual_stack_forward(stack, h_local, out_local, bufs=bufs)
+        us, mode = _ep_time(env, step, 1, K)
+        res[name] = {"us_per_step": us, "us_per_layer": us / NL, "mode": mode}
+    res["latency_ratio_oea_vs_vanilla"] = res["oea"]["us_per_step"] / res["vanilla"]["us_per_step"]
+    for L in pool:
+        L.close()
+    return res
 
 
 def bench_c2(args, env):

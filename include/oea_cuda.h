@@ -292,6 +292,14 @@ int oea_decode_graph_create(oea_ctx_t ctx, oea_layer_t layer, const void* x_dev,
                             const uint8_t* mask_dev, int32_t B,
                             const oea_routing_cfg* cfg, void* out_dev,
                             oea_graph_t* out);
+/* n decode calls (layers[i]: xs_dev[i] -> outs_dev[i], same B / cfg / mask)
+ * captured back to back in ONE graph, as a decode step's layers run. The fused
+ * launches are programmatic dependents of the previous kernel (PDL), so each
+ * call's launch and setup overlap the previous call's tail. */
+int oea_decode_chain_graph_create(oea_ctx_t ctx, int32_t n, const oea_layer_t* layers,
+                                  const void* const* xs_dev, const uint8_t* mask_dev, int32_t B,
+                                  const oea_routing_cfg* cfg, void* const* outs_dev,
+                                  oea_graph_t* out);
 /* The same decode captured as two graphs (router+compaction | FFN), without
  * the programmatic overlap, so each stage can be timed on its own (bench). */
 int oea_decode_stage_graphs_create(oea_ctx_t ctx, oea_layer_t layer, const void* x_dev,

@@ -110,6 +110,7 @@ def lib():
                 "oea_last_plan_host": [vp, vp, vp, vp],
                 "oea_decode_graph_create": [vp, vp, vp, vp, i32, vp, vp, vp],
                 "oea_graph_launch": [vp, vp],
+                "oea_decode_chain_graph_create": [vp, i32, vp, vp, vp, i32, vp, vp, vp],
                 "oea_decode_stage_graphs_create": [vp, vp, vp, vp, i32, vp, vp, vp, vp],
                 "oea_graph_destroy": [vp],
                 "oea_moe_forward_plan_host": [vp, vp, vp, i32, vp, vp, vp, i32, vp, vp],
@@ -140,7 +141,8 @@ EXPORTED = (
     "oea_layer_download_router", "oea_layer_download_expert", "oea_layer_info",
     "oea_moe_decode", "oea_moe_decode_host", "oea_last_plan_host", "oea_decode_graph_create",
     "oea_graph_launch", "oea_decode_stage_graphs_create", "oea_graph_destroy", "oea_moe_forward_plan_host",
-    "oea_router_scores_host", "oea_ep_owner", "oea_debug_ffn_trace", "oea_layer_create_shard")
+    "oea_router_scores_host", "oea_ep_owner", "oea_debug_ffn_trace", "oea_layer_create_shard",
+    "oea_decode_chain_graph_create")
 
 
 def check(rc: int, ctx=None):

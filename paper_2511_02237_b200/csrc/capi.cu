@@ -452,7 +452,7 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
                            oea_host::ffn_route_smem_bytes(B, L->Np, stride) <= 227 * 1024;
   if (x_mapped && !fused) return kNotFused;  // the caller stages x itself
   int r = OEA_OK;
-  if (rb.trace) OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.trace, 0, 8 * 8 * 1024, s));
+  if (rb.trace && !fused) OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.trace, 0, 8 * 8 * 1024, s));
   if (big) {
     oea_host::FfnBuffers rf;
     rf.route_only = 1;
@@ -653,7 +653,12 @@ int oea_ctx_create(int32_t device, oea_ctx_t* out) {
   }
   ctx->ws = new CtxExtra;
   if (const char* tr = getenv("OEA_FFN_TRACE")) {
-    if (tr[0] == '1' && cudaMalloc(&ctx->ffn_trace, 8 * 8 * 1024) != cudaSuccess) ctx->ffn_trace = nullptr;
+    if (tr[0] == '1') {
+      if (cudaMalloc(&ctx->ffn_trace, 8 * oea_dev::kTraceWords) != cudaSuccess)
+        ctx->ffn_trace = nullptr;
+      else
+        cudaMemset(ctx->ffn_trace, 0, 8 * oea_dev::kTraceWords);
+    }
   }
   if (const char* md = getenv("OEA_FFN_MODE")) ctx->ffn_mode = atoi(md);
   *out = ctx;
@@ -664,7 +669,7 @@ int oea_debug_ffn_trace(oea_ctx_t ctx, uint64_t* host, int32_t n) {
   CHECK_CTX(ctx);
   if (ctx->ffn_trace == nullptr) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "OEA_FFN_TRACE not enabled");
   OEA_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  OEA_CUDA_TRY(ctx, cudaMemcpy(host, ctx->ffn_trace, sizeof(uint64_t) * std::min(n, 8 * 1024),
+  OEA_CUDA_TRY(ctx, cudaMemcpy(host, ctx->ffn_trace, sizeof(uint64_t) * std::min<size_t>(n, oea_dev::kTraceWords),
                                cudaMemcpyDeviceToHost));
   return OEA_OK;
 }
@@ -1594,10 +1599,90 @@ int oea_decode_graph_create(oea_ctx_t ctx, oea_layer_t L, const void* x_dev,
     delete g;
     return oea_check_cuda(ctx, e, "cudaGraphInstantiate");
   }
+  // upload now, so the first launch does not pay it
+  e = cudaGraphUpload(g->exec, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    cudaGraphExecDestroy(g->exec);
+    cudaGraphDestroy(graph);
+    delete g;
+    return oea_check_cuda(ctx, e, "cudaGraphUpload");
+  }
   ctx->last_B = B;
   ctx->last_N = L->N;
   ctx->last_stride = stride_of(rc);
   ctx->last_kind = L->dtype == OEA_DTYPE_BF16 ? 1 : 2;
+  *out = g;
+  return OEA_OK;
+}
+
+int oea_decode_chain_graph_create(oea_ctx_t ctx, int32_t n, const oea_layer_t* layers,
+                                  const void* const* xs_dev, const uint8_t* mask_dev, int32_t B,
+                                  const oea_routing_cfg* cfg, void* const* outs_dev,
+                                  oea_graph_t* out) {
+  CHECK_CTX(ctx);
+  if (out == nullptr || layers == nullptr || xs_dev == nullptr || outs_dev == nullptr)
+    return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "null output pointer");
+  *out = nullptr;
+  if (n < 1) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "chain graph: need n >= 1 decode calls");
+  oea_routing_cfg rc;
+  Workspace& w = extra(ctx)->ws;
+  for (int i = 0; i < n; ++i) {
+    int r = validate_decode(ctx, layers[i], B, cfg, &rc);
+    if (r) return r;
+    r = ensure(ctx, w, need_for(layers[i], B, stride_of(rc)));
+    if (r) return r;
+  }
+  OEA_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  auto* g = new oea_graph;
+  g->ctx = ctx;
+  cudaStream_t s = ctx->stream;
+  cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) {
+    delete g;
+    return oea_check_cuda(ctx, e, "cudaStreamBeginCapture");
+  }
+  // n decode calls back to back on one stream, as a decode step's layers run:
+  // the fused launches carry the programmatic-serialization attribute, so the
+  // captured kernel -> kernel edges are programmatic (PDL) edges.
+  int r = OEA_OK;
+  for (int i = 0; i < n && r == OEA_OK; ++i) {
+    oea_layer* L = layers[i];
+    if (L->dtype == OEA_DTYPE_BF16)
+      r = decode_bf16(ctx, w, L, xs_dev[i], mask_dev, B, rc, outs_dev[i], s);
+    else
+      r = decode_simt(ctx, w, L, static_cast<const double*>(xs_dev[i]), mask_dev, B, rc,
+                      static_cast<double*>(outs_dev[i]), s);
+  }
+  cudaGraph_t graph = nullptr;
+  e = cudaStreamEndCapture(s, &graph);
+  if (r || e != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    delete g;
+    return r ? r : oea_check_cuda(ctx, e, "cudaStreamEndCapture");
+  }
+  g->graph = graph;
+  g->kernels = count_kernel_nodes(graph);
+  e = cudaGraphInstantiate(&g->exec, graph, 0);
+  if (e != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    delete g;
+    return oea_check_cuda(ctx, e, "cudaGraphInstantiate");
+  }
+  // upload now, so the first launch does not pay it
+  e = cudaGraphUpload(g->exec, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    cudaGraphExecDestroy(g->exec);
+    cudaGraphDestroy(graph);
+    delete g;
+    return oea_check_cuda(ctx, e, "cudaGraphUpload");
+  }
+  oea_layer* last = layers[n - 1];
+  ctx->last_B = B;
+  ctx->last_N = last->N;
+  ctx->last_stride = stride_of(rc);
+  ctx->last_kind = last->dtype == OEA_DTYPE_BF16 ? 1 : 2;
   *out = g;
   return OEA_OK;
 }

@@ -85,6 +85,7 @@ struct FfnParams {
   __nv_bfloat16* xpad_out;      // [B][Dp], written in-kernel when D != Dp, else null
   int x_stage;                  // x_in is mapped host memory: staged into xpad_out first
   int prefetch_bytes;           // speculative L2 prefetch of every held expert's first W1 bytes
+  int pf_early;                 // issue that prefetch before griddepcontrol.wait (PDL launch)
   float* logits;        // [B][Np]
   const uint8_t* mask;
   int N, Np;
@@ -129,8 +130,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// debug timeline: this launch's region of the trace buffer (16 launches deep,
+// indexed by the launch epoch), set by thread 0 at kernel start
+__shared__ unsigned long long* s_trace;
 __device__ __forceinline__ void stamp(const FfnParams& P, int slot) {
-  if (P.trace) P.trace[blockIdx.x * 16 + slot] = gtimer();
+  if (P.trace && s_trace) s_trace[blockIdx.x * 16 + slot] = gtimer();
 }
 
 struct Unit {
@@ -224,7 +228,6 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
       while (ld_acquire_gpu(&P.w1_done[U.g]) < RB1) __nanosleep(64);
     __syncwarp();
   }
-  if (!W1 && warp == 0 && lane == 0 && P.trace && P.trace[blockIdx.x * 16 + 2] == 0) stamp(P, 2);
 
   // two accumulator sets (even / odd k-tiles) halve the dependent HMMA chain
   // (one n-block: two sets halve the dependent HMMA chain; more n-blocks
@@ -1319,6 +1322,12 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
       reinterpret_cast<PlanRef*>(rdesc + kRoundRing) + 1);  // dense: router warp -> W2
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+  // Programmatic dependent launch: the next kernel of the stream (the next
+  // layer's decode, a norm, ...) may be launched now; its CTAs take SMs as
+  // ours exit and do their own pre-wait setup while our tail runs. Nothing
+  // below depends on it (it cannot pass its griddepcontrol.wait until this
+  // grid has completed), so the trigger is safe at the very start.
+  if (kFused) pdl_launch_dependents();
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -1328,10 +1337,14 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
     mbar_init(plan_bar + 1, 1);  // split rounds: warp 0 has read the reduction buffer
     fence_mbar_init();
   }
+  // Before the wait (PDL launch: overlapping the previous kernel's tail),
+  // only what reads no predecessor output: the L2 prefetch of the weights.
+  const bool pf_early = kFused && !kRouteOnly && P.pf_early && P.prefetch_bytes > 0;
+  if (pf_early && warp == kProducerWarp) prefetch_w1_heads(P, lane);
   __syncthreads();
-  // Everything below reads the router kernel's outputs (two-kernel path).
+  // Everything below reads the router kernel's outputs (two-kernel path) or
+  // the previous launch's workspace (epoch, counters: fused path).
   pdl_wait();
-  if (threadIdx.x == 0) stamp(P, 0);
 
   PlanRef* PR = reinterpret_cast<PlanRef*>(rdesc + kRoundRing);
   uint8_t* rs = reinterpret_cast<uint8_t*>(PR + 1) + 16;
@@ -1348,6 +1361,15 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
   int* claims = P.claims;  // independent of the layer's shape (one workspace, many layers)
   // this launch's exchange tag (the epoch only changes when a launch retires)
   const uint32_t tag = static_cast<uint32_t>(__ldcg(claims + 7)) + 1u;
+  if (P.trace) {  // (debug builds of the context only; uniform branch)
+    if (threadIdx.x == 0) {
+      s_trace = P.trace + kTraceLegacy + (tag & (kTraceLaunches - 1)) * kTracePerLaunch;
+      stamp(P, 0);
+    }
+    __syncthreads();
+  } else if (threadIdx.x == 0) {
+    s_trace = nullptr;
+  }
   if (kFused) {
     if (warp == kRouterWarp && lane == 0) {
       // Touch every line of the parameter block once, early and all at once
@@ -1372,7 +1394,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
     }
     // (x in host memory: before the GEMV, inside the host round trip of
     // the x staging, when HBM idles longest)
-    if (!kRouteOnly && P.x_stage && warp == kProducerWarp && P.prefetch_bytes > 0)
+    if (!kRouteOnly && !pf_early && P.x_stage && warp == kProducerWarp && P.prefetch_bytes > 0)
       prefetch_w1_heads(P, lane);
     if (kRouteOnly)
       tile_gemv(P, SR.buf, tag);
@@ -1380,7 +1402,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
       fused_gemv(P, reinterpret_cast<float*>(rs + RL.red), claims + 3, tag);
     if (threadIdx.x == 0) stamp(P, 5);
     // (x in device memory: after the GEMV, whose loads it would delay)
-    if (!kRouteOnly && !P.x_stage && warp == kProducerWarp && P.prefetch_bytes > 0)
+    if (!kRouteOnly && !pf_early && !P.x_stage && warp == kProducerWarp && P.prefetch_bytes > 0)
       prefetch_w1_heads(P, lane);
     // R1: CTA t routes token t (thread per expert), then the union barrier
     if (threadIdx.x < 128) {
@@ -1395,6 +1417,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
     if (threadIdx.x == 0) {
       PR->G = T;
       stamp(P, 6);
+      if (s_trace && blockIdx.x == 0) s_trace[kTraceInfo] = static_cast<unsigned long long>(T);
     }
     if (kRouteOnly) {
       // plan rows (CTA t: token t, t + grid, ...); CTA 0 also gathers the batch
@@ -1947,6 +1970,12 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
     P.prefetch_bytes = pf >= 0 ? pf * 1024
                                : ((32 << 20) / max(L->n_local, 1)) & ~(32 * 1024 - 1);
   }
+  {
+    // (issuing it before the wait was measured slower: the CTAs only become
+    // resident as the previous grid's exit, so it just delays the GEMV's loads)
+    static const bool early = getenv("OEA_PF_EARLY") != nullptr;
+    P.pf_early = early && !fb.x_stage;
+  }
   P.e_begin = L->e_begin;
   P.e_count = L->n_local;
   P.router_t = static_cast<const uint4*>(L->router_t);
@@ -2008,6 +2037,9 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   // PDL only as the router kernel's dependent (two-kernel path); the fused
   // launch carries no programmatic-serialization attribute at all.
   static const bool coop = getenv("OEA_NO_COOP") == nullptr;
+  // Fused launches are programmatic dependents of the previous kernel in the
+  // stream (see the kernel head): launch latency and setup overlap its tail.
+  static const bool fused_pdl = getenv("OEA_NO_PDL") == nullptr;
   cudaLaunchAttribute attr[2];
   int na = 0;
   if (coop) {
@@ -2015,7 +2047,7 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
     attr[na].val.cooperative = 1;
     ++na;
   }
-  if (pdl) {
+  if (pdl || (fb.fused && fused_pdl)) {
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;

@@ -43,6 +43,14 @@ struct EpPeers {
   int world, rank, tpr;
 };
 constexpr int kMaxRouteN = 1024;       // route_f64 expert limit
+// Debug timeline buffer (OEA_FFN_TRACE=1): the router kernels' legacy area,
+// then one [grid][16] stamp region per FFN launch, 16 launches deep (indexed
+// by the launch epoch); word kTraceInfo of a region = the launch's T.
+constexpr int kTraceLegacy = 8192;
+constexpr int kTraceLaunches = 16;
+constexpr int kTracePerLaunch = 4096;
+constexpr int kTraceInfo = 2400;
+constexpr size_t kTraceWords = kTraceLegacy + static_cast<size_t>(kTraceLaunches) * kTracePerLaunch;
 
 inline int round_up(int v, int m) { return (v + m - 1) / m * m; }
 

@@ -24,7 +24,8 @@ from __future__ import annotations
 
 from typing import Callable, List, Optional
 
-__all__ = ["ep_expert_range", "ep_token_range", "ExpertParallelMoE", "PeerExpertParallelMoE"]
+__all__ = ["ep_expert_range", "ep_token_range", "ExpertParallelMoE", "AllToAllExpertParallelMoE",
+           "PeerExpertParallelMoE", "make_ep_layer"]
 
 
 def ep_expert_range(n_experts: int, world: int, rank: int):
@@ -87,6 +88,54 @@ class ExpertParallelMoE:
         self.dist.reduce_scatter_tensor(out_local, partial, op=self.dist.ReduceOp.SUM,
                                         group=self.group)
         return out_local
+
+
+class AllToAllExpertParallelMoE(ExpertParallelMoE):
+    """The same EP layer with NCCL all-to-all token dispatch and combine
+    (BASELINE C4's "NCCL all-to-all dispatch/combine"):
+
+      dispatch  all_to_all_single: rank r sends its B/P token rows to every
+                rank. OEA's union is batch-global (routing.cpp:262-266: the
+                piggyback pool is the union of ALL tokens' base sets), so every
+                expert owner routes the whole batch and needs every token: the
+                dispatch payload is the whole batch, split by source rank.
+      compute   the shard decode of the whole batch (partial mixture over the
+                held experts, plan bit-identical on every rank).
+      combine   all_to_all_single of the fp32 partials: rank r sends rows
+                [B o / P, B (o+1) / P) to their owner o; the owner sums the P
+                received slabs in source-rank order (deterministic, no float
+                atomics), the same sum the reduce-scatter path computes.
+    """
+
+    def forward(self, x_local, out_local, x_all=None, partial=None, recv=None):
+        import torch
+        P = self.world
+        rows, D = x_local.shape
+        B = rows * P
+        if self.world == 1:
+            self.partial_fn(x_local, out_local)
+            return out_local
+        if x_all is None:
+            x_all = torch.empty((B, D), dtype=x_local.dtype, device=x_local.device)
+        if partial is None:
+            partial = torch.empty((B, D), dtype=torch.float32, device=x_local.device)
+        if recv is None:
+            recv = torch.empty((P, rows, D), dtype=partial.dtype, device=x_local.device)
+        # dispatch: the same B/P rows to each of the P destinations
+        send = x_local.contiguous().unsqueeze(0).expand(P, rows, D).reshape(B, D)
+        self.dist.all_to_all_single(x_all, send, group=self.group)
+        self.partial_fn(x_all, partial)
+        # combine: slab o of the partials goes to owner o; slab r received = rank r's
+        self.dist.all_to_all_single(recv.view(B, D), partial, group=self.group)
+        torch.sum(recv, dim=0, out=out_local)
+        return out_local
+
+
+def make_ep_layer(kind: str, layer, cfg, world: int, rank: int, dist=None, group=None):
+    """The GPU EP layer of one data path: "ag_rs" (NCCL all-gather +
+    reduce-scatter), "a2a" (NCCL all-to-all dispatch / combine)."""
+    cls = {"ag_rs": ExpertParallelMoE, "a2a": AllToAllExpertParallelMoE}[kind]
+    return cls.from_shard(layer, cfg, world, rank, dist, group)
 
 
 def residual_stack_forward(layers: List[ExpertParallelMoE], h_local, out_local,

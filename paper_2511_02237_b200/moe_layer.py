@@ -254,6 +254,24 @@ class DeviceMoeLayer:
             C.byref(cfg.to_c()), C.c_void_p(_ptr(out)), C.byref(g)))
         return DecodeGraph(self, g)
 
+    @staticmethod
+    def chain_graph(layers, xs, cfg: RoutingConfig, outs, mask=None) -> DecodeGraph:
+        """ONE CUDA graph of len(layers) decode calls back to back (layers[i]:
+        xs[i] -> outs[i]), the way a decode step's MoE layers run: the fused
+        launches are programmatic dependents of their predecessor (PDL)."""
+        n = len(layers)
+        if n < 1 or len(xs) != n or len(outs) != n:
+            raise InvalidArgument("chain_graph: need matching non-empty layers / xs / outs")
+        ctx = layers[0].ctx
+        hs = (C.c_void_p * n)(*[L.h.value for L in layers])
+        xp = (C.c_void_p * n)(*[_ptr(x) for x in xs])
+        op = (C.c_void_p * n)(*[_ptr(o) for o in outs])
+        g = C.c_void_p()
+        ctx.check(lib().oea_decode_chain_graph_create(
+            ctx.h, n, hs, xp, C.c_void_p(_ptr(mask)) if mask is not None else None,
+            int(xs[0].shape[0]), C.byref(cfg.to_c()), op, C.byref(g)))
+        return DecodeGraph(layers[-1], g)
+
     def stage_graphs(self, x, cfg: RoutingConfig, out, mask=None):
         """(router graph, FFN graph) of one decode, for per-stage timing."""
         g1, g2 = C.c_void_p(), C.c_void_p()

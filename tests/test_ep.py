@@ -49,7 +49,7 @@ def _oracle_partial(x_all, owned, layer):
     return oracle.moe_forward(wg, wu, wd, x_all, plan.sets, plan.set_len, w)
 
 
-def _worker(rank, world, port, layer, x, want, results):
+def _worker(rank, world, port, layer, x, want, results, kind="ag_rs"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -58,7 +58,8 @@ def _worker(rank, world, port, layer, x, want, results):
 
         def fn(x_all, out_partial):
             out_partial.copy_(torch.from_numpy(_oracle_partial(x_all.numpy(), owned, layer)))
-        moe = ep.ExpertParallelMoE(fn, world, rank, dist)
+        cls = {"ag_rs": ep.ExpertParallelMoE, "a2a": ep.AllToAllExpertParallelMoE}[kind]
+        moe = cls(fn, world, rank, dist)
         t0, t1 = ep.ep_token_range(B, world, rank)
         x_local = torch.from_numpy(x[t0:t1].copy())
         out_local = torch.empty((t1 - t0, D), dtype=torch.float64)
@@ -79,8 +80,8 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2])
-def test_ep_orchestration_gloo(world):
+@pytest.mark.parametrize("world,kind", [(2, "ag_rs"), (2, "a2a"), (4, "a2a")])
+def test_ep_orchestration_gloo(world, kind):
     layer = oracle.make_random_layer(D, H, N, 3)
     x = oracle.make_random_batch(B, D, 17)
     router, wg, wu, wd = layer
@@ -88,7 +89,8 @@ def test_ep_orchestration_gloo(world):
     want = oracle.moe_forward(wg, wu, wd, x, plan.sets, plan.set_len, plan.weights)
     mgr = mp.Manager()
     results = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), layer, x, want, results), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), layer, x, want, results, kind), nprocs=world,
+             join=True)
     assert sorted(results.keys()) == list(range(world))
     for r, err in results.items():
         assert err < 1e-12, (r, err)

@@ -1,0 +1,105 @@
+"""Per-CTA stamp timeline of the fused decode launch (OEA_FFN_TRACE=1), for the
+last of REPS back-to-back graph replays, plus the event-timed µs per call, so
+the launch gap = per-call time - (last CTA done - first CTA start).
+
+  SHAPE=2048,768,128,16 K0=4 python tools/timeline.py
+"""
+import os
+import sys
+
+os.environ["OEA_FFN_TRACE"] = "1"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import ctypes as C  # noqa: E402
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2511_02237_b200 as oea  # noqa: E402
+from paper_2511_02237_b200._capi import lib  # noqa: E402
+
+D, H, N, B = [int(v) for v in os.environ.get("SHAPE", "2048,768,128,16").split(",")]
+K0 = int(os.environ.get("K0", "4"))
+REPS = int(os.environ.get("REPS", "20"))
+layers = []
+for r in range(4):
+    L = oea.DeviceMoeLayer(D, H, N, "bf16")
+    L.init_random(1 + r)
+    layers.append(L)
+ctx = layers[0].ctx
+torch.manual_seed(int(os.environ.get("SEED", "5")))
+xs = torch.randn(REPS, B, D, device="cuda").to(torch.bfloat16)
+out = torch.empty(B, D, device="cuda", dtype=torch.float32)
+torch.cuda.synchronize()
+stream = torch.cuda.ExternalStream(ctx.stream)
+
+SLOTS = [(0, "start"), (5, "logits published"), (11, "R1 ranked"), (12, "union words polled"),
+         (13, "union ballots"), (14, "union syncthreads"), (6, "union known"), (7, "plan ready"),
+         (1, "first W2 round"), (4, "producer done"), (3, "consumers done"), (9, "combine arrive"),
+         (10, "combine barrier"), (2, "combine start"), (15, "combine done")]
+
+for name, cfg in (("oea", oea.RoutingConfig.simplified(K0, 8)), ("vanilla", oea.RoutingConfig.vanilla(8))):
+    chain = os.environ.get("CHAIN", "0") == "1"
+    if chain:  # one graph of REPS - 4 calls (PDL edges) + a 4-call warm-up graph
+        warm = oea.DeviceMoeLayer.chain_graph([layers[i % 4] for i in range(4)], list(xs[:4]),
+                                              cfg, [out] * 4)
+        graphs = [warm, oea.DeviceMoeLayer.chain_graph(
+            [layers[i % 4] for i in range(4, REPS)], list(xs[4:]), cfg, [out] * (REPS - 4))]
+        runs = graphs[1:]
+    else:
+        graphs = [layers[i % 4].graph(xs[i], cfg, out) for i in range(REPS)]
+        runs = graphs[4:]
+    for g in graphs[:len(graphs) - len(runs)]:
+        g.launch()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for g in runs:
+            g.launch()
+        e1.record(stream)
+    e1.synchronize()
+    per_call = e0.elapsed_time(e1) * 1000.0 / (REPS - 4)
+    LEG, NL, PER, INFO = 8192, 16, 4096, 2400
+    buf = np.zeros(LEG + NL * PER, np.uint64)
+    ctx.check(lib().oea_debug_ffn_trace(ctx.h, buf.ctypes.data_as(C.c_void_p), buf.size))
+    regs = buf[LEG:].reshape(NL, PER).astype(np.int64)
+    launches = []
+    for r in regs:
+        t = r[:148 * 16].reshape(148, 16)
+        if t[:, 0].min() <= 0 or t[:, 15].max() <= 0:
+            continue
+        launches.append((t[:, 0].min(), t, int(r[INFO])))
+    launches.sort(key=lambda v: v[0])
+    print(f"== {name} B={B} D={D} H={H} N={N}: {per_call:.2f} us per call (events), "
+          f"{len(launches)} launches traced")
+    # median over the traced launches of each slot's (min, med, max) over CTAs
+    rows = {s: [] for s, _ in SLOTS}
+    spans, gaps, Ts = [], [], []
+    for i, (t0, t, T) in enumerate(launches):
+        for s, _ in SLOTS:
+            a = t[:, s]
+            a = a[a > 0]
+            if a.size:
+                r = (a - t0) / 1000.0
+                rows[s].append((r.min(), np.median(r), r.max()))
+        spans.append((t[:, 15].max() - t0) / 1000.0)
+        Ts.append(T)
+        if i + 1 < len(launches):
+            gaps.append((launches[i + 1][0] - t[:, 15].max()) / 1000.0)
+    for s, lab in SLOTS:
+        if rows[s]:
+            m = np.median(np.array(rows[s]), axis=0)
+            print(f"  {lab:20s} min {m[0]:7.2f} med {m[1]:7.2f} max {m[2]:7.2f}")
+    print(f"  T per launch {Ts}")
+    print(f"  span (first start -> last combine done) median {np.median(spans):.2f} us "
+          f"[{min(spans):.2f}, {max(spans):.2f}]")
+    if gaps:
+        print(f"  gap (last combine done -> next first start) median {np.median(gaps):.2f} us "
+              f"[{min(gaps):.2f}, {max(gaps):.2f}]")
+    for (t0, t, T), sp in zip(launches, spans):
+        pd = (t[:, 4] - t0) / 1000.0
+        print(f"    T={T:3d} span {sp:6.2f}  union {(t[:, 6].max() - t0) / 1000.0:5.2f}  "
+              f"producers done {pd.min():6.2f}..{pd.max():6.2f}  "
+              f"us/expert {(sp) / max(T, 1):.3f}")
+    for g in graphs:
+        g.close()
