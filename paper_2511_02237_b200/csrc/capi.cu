@@ -119,7 +119,9 @@ size_t carve(Workspace& w, bool assign) {
   take(w.xpad, B * Dp * 2);
   // (dense decode: h [G][16][Hp] bf16, y [G][16][Dp] f32 with G <= N)
   take(w.hbuf, std::max(R * std::max(Hp, H) * 8, Nmax * 16 * Hp * 2));
-  take(w.ybuf, std::max(B * S * std::max(Dp, D) * 8, Nmax * 16 * Dp * 4));
+  // (y: kW2KSplitMax K-part planes of [B][S][Dp] f32 on the dense path)
+  take(w.ybuf, std::max({B * S * std::max(Dp, D) * 8, Nmax * 16 * Dp * 4,
+                         std::min<size_t>(B, 16) * S * Dp * 4 * kW2KSplitMax}));
   take(w.mask, B);
   take(w.xin, B * D * 8);
   take(w.out, B * D * 8);

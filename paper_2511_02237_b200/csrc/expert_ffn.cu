@@ -86,6 +86,7 @@ struct FfnParams {
   int x_stage;                  // x_in is mapped host memory: staged into xpad_out first
   int prefetch_bytes;           // speculative L2 prefetch of every held expert's first W1 bytes
   int pf_early;                 // issue that prefetch before griddepcontrol.wait (PDL launch)
+  int w2_ks;                    // dense path: W2 rounds split into w2_ks K parts (1 = whole)
   float* logits;        // [B][Np]
   const uint8_t* mask;
   int N, Np;
@@ -144,6 +145,8 @@ struct Unit {
   int rows;    // real rows (tokens) in the group
   int ready;   // W2: the group's h is known complete (acquired by the producer)
   int nw;      // warps with a unit in this round (they share the B tile)
+  int sb;      // first K slice (stage) of this round's part (W2 K split; else 0)
+  int kp;      // K part: y plane this unit writes (W2 K split; else 0)
 };
 
 // Shared B-operand tiles (token-list units with >= 2 n-blocks): the 8 units
@@ -169,6 +172,23 @@ __device__ __forceinline__ int xs_chunk(int cc) { return (cc & 8) | ((cc + (cc >
 
 constexpr int kSplitRedBytes = kFfnWarps * 32 * 16 * 4;  // split-round reduction buffer
 
+// Dense path (B <= 16) h layout: per group [Hp/128 K slices][16 token rows]
+// [128] bf16, the 16-byte chunk c of row r stored at chunk hs_chunk(c, r).
+// One K slice of a W2 round is then ONE contiguous 4 KiB block, which the
+// producer bulk-copies into the stage next to the weights (no per-warp L2
+// loads of the B operand, no exposed L2 latency at round starts), and the
+// LDS.128 B-fragment loads of a quarter warp (2 token rows x 4 quads, chunks
+// {i, 4+i, 8+i, 12+i}) hit 8 distinct bank groups.
+constexpr int kHSlice = 16 * 128 * 2;  // one K slice of a group's h (4 KiB)
+static_assert(kStages * kHSlice <= kSplitRedBytes, "h slices live in the split-reduction area");
+__host__ __device__ __forceinline__ int hs_chunk(int c, int r) {
+  return (c & 8) | ((c + 2 * (c >> 3) + (r & 1)) & 7);
+}
+__host__ __device__ __forceinline__ size_t hs_index(int g, int r, int hh, int Hp) {
+  return static_cast<size_t>(g) * 16 * Hp + (hh >> 7) * 2048 + r * 128 +
+         hs_chunk((hh & 127) >> 3, r) * 8 + (hh & 7);
+}
+
 // Split rounds (few active experts): ONE unit per round, its K slices spread
 // over the 8 consumer warps (warp w takes slices w, w+8, ...), partial sums
 // reduced through shared memory into warp 0, which runs the epilogue. This
@@ -190,6 +210,7 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
   // dense W1: B operand = all B tokens from the swizzled shared-memory x tile;
   // dense W2: token lists as usual, h rows at [group][token] (written by W1)
   constexpr bool XSM = DENSE && W1;
+  constexpr bool HSM = DENSE && !W1 && !SPLIT;       // W2: h slices staged in the ring
   constexpr bool SHB = !DENSE && !SPLIT && NB >= 2;  // shared B tile
 
   // B-operand rows (uint4 view) for this lane's token in each n-block. The
@@ -207,6 +228,8 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
     bp[nb] = nullptr;
     if (SHB) {
       // (rows come from the shared tile)
+    } else if (HSM) {
+      // (rows come from the staged h slice: hrow_off below)
     } else if (XSM) {
       // token r; the per-quarter chunk offsets are added at the load
       bp[nb] = reinterpret_cast<const uint4*>(xs + r * P.xs_row);
@@ -220,7 +243,19 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
       }
     }
   }
-  if (!W1 && !U.ready) {
+  // HSM: byte offsets of this lane's token row (n-block nb) in an h slice;
+  // rows past the group's list read row 0 (their output columns are dropped)
+  int hoff[HSM ? NB : 1][4];
+  if constexpr (HSM) {
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+      const int r = nb * 8 + g;
+      const int tr = r < U.rows ? PR->row_tok[U.row0 + r] : 0;
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) hoff[nb][jj] = tr * 256 + hs_chunk(4 * q + jj, tr) * 16;
+    }
+  }
+  if (!W1 && !HSM && !U.ready) {
     // h of this token group must be complete (all RB1 W1 units released):
     // lane 0 acquires, the warp barrier orders the other lanes after it.
     // (U.ready: the producer already acquired it when it issued the round.)
@@ -275,7 +310,7 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
   // the current stage is consumed, so their latency hides behind the stage
   // barrier wait (two n-blocks measured slower: spills at the register cap).
   // More n-blocks: per quarter stage (2 k-tiles) one 16-byte load per n-block.
-  constexpr bool kPref = !XSM && NB <= 1 && !SPLIT;
+  constexpr bool kPref = !XSM && !HSM && NB <= 1 && !SPLIT;
   constexpr int PB = 1;  // prefetched n-blocks
   // slices of this unit (K / 128); SPLIT: this warp's slice of split-stage s
   const int nslices = (W1 ? P.Dp : P.Hp) >> 7;
@@ -284,7 +319,8 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
 #pragma unroll
     for (int nb = 0; nb < PB; ++nb)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) bpre[nb][i] = ldb(bp[nb] == nullptr ? nullptr : bp[nb] + i);
+      for (int i = 0; i < 4; ++i)
+        bpre[nb][i] = ldb(bp[nb] == nullptr ? nullptr : bp[nb] + U.sb * 16 + i);
 
   for (int s0 = 0; s0 < nst; ++s0) {
     if (SHB && math) {
@@ -298,7 +334,7 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
       if (s0 + 2 < nst) issue_tile(s0 + 2, (s0 + 2) % 3);
     }
     mbar_wait(&full[stage], phase);
-    const int s = SPLIT ? s0 * kFfnWarps + warp : s0;  // K slice of this stage for this warp
+    const int s = SPLIT ? s0 * kFfnWarps + warp : U.sb + s0;  // K slice of this stage for this warp
     const uint4* tiles =
         reinterpret_cast<const uint4*>(ring + stage * kStageBytes + warp * kSlotBytes);
     if (math && (!SPLIT || s < nslices)) {
@@ -328,6 +364,9 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
               v[nb] = lds128(PR->btile + (s0 % 3) * kBTileBuf + nb * 2048 + boff[jj]);
             else if (XSM)
               v[nb] = lds128(reinterpret_cast<const uint8_t*>(bp[nb]) + s * 256 + xoff[jj]);
+            else if (HSM)
+              v[nb] = lds128(reinterpret_cast<const uint8_t*>(SR.buf) + stage * kHSlice +
+                             hoff[HSM ? nb : 0][jj]);
             else
               v[nb] = ldb(bp[nb] == nullptr ? nullptr : bp[nb] + s * 16 + jj);
           }
@@ -391,7 +430,9 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
         const int r = nb * 8 + 2 * q + i;
         if (r < U.rows) {
           const float hv = silu_f(acc[nb][i]) * acc[nb][2 + i];
-          P.hbuf[static_cast<size_t>(U.row0 + r) * P.Hp + h] = __float2bfloat16_rn(hv);
+          const size_t hi = DENSE ? hs_index(U.g, r, h, P.Hp)
+                                  : static_cast<size_t>(U.row0 + r) * P.Hp + h;
+          P.hbuf[hi] = __float2bfloat16_rn(hv);
         }
       }
     }
@@ -409,7 +450,8 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
         if (r < U.rows) {
           const int row = U.row0 + r;
           const int t = PR->row_tok[row], sl = PR->row_slot[row];
-          float* y = P.ybuf + (static_cast<size_t>(t) * P.stride + sl) * P.Dp + d0;
+          float* y = P.ybuf +
+                     (static_cast<size_t>(U.kp * P.B + t) * P.stride + sl) * P.Dp + d0;
           y[g] = acc[nb][i];
           y[g + 8] = acc[nb][2 + i];
         }
@@ -1301,6 +1343,9 @@ struct RoundDesc {
   int n;     // units (one per consumer warp); 0 = end of work
   int kind;  // 1 = W1, 2 = W2
   int ready; // W2: the group's h was acquired complete by the producer
+  int sb;    // stages [sb, se) of the units' K (W2 K split: one part; else all)
+  int se;
+  int kp;    // K part (y plane)
 };
 constexpr int kRoundRing = 8;  // > kStages: a round spans >= 1 stage
 
@@ -1446,9 +1491,11 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
   const int U1 = G * RB1, U2 = G * RB2;
   // Split rounds (one unit per round, K over the 8 warps) when there are too
   // few 8-unit rounds to keep every SM streaming (B <= 16: <= 2 n-blocks).
-  const bool split = kFused && P.B <= 16 && P.split_ok &&
+  const bool split = kFused && !kDense && P.B <= 16 && P.split_ok &&
                      (U1 + kFfnWarps - 1) / kFfnWarps + (U2 + kFfnWarps - 1) / kFfnWarps <
                          2 * static_cast<int>(gridDim.x);
+  // W2 K parts per round (dense path; the combine sums the y planes)
+  const int w2ks = kDense && !split ? max(1, min(P.w2_ks, KT2 / kKtPerSlot)) : 1;
   // Dynamic scheduling: rounds of up to 8 consecutive units are claimed from
   // two global counters, all W1 (gate/up) rounds before any W2 (down) round.
   // A CTA therefore finishes its own W1 rounds before it starts W2 rounds,
@@ -1483,16 +1530,17 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
     if (lane == 0) {
       const uint64_t pol = l2_policy_evict_first();
       bool w1_left = true;
+      const int nst2 = KT2 / kKtPerSlot, ks2 = w2ks;
       auto claim = [&]() {
-        RoundDesc d{0, 0, 0, 0};
+        RoundDesc d{0, 0, 0, 0, 0, 0, 0};
         if (split) {  // one unit per round: kind 3 (W1) / 4 (W2)
           if (w1_left) {
             const int r = atomicAdd(&claims[0], 1);
-            if (r < U1) return RoundDesc{r, 1, 3, 0};
+            if (r < U1) return RoundDesc{r, 1, 3, 0, 0, 0, 0};
             w1_left = false;
           }
           const int r = atomicAdd(&claims[1], 1);
-          if (r < U2) d = RoundDesc{U1 + r, 1, 4, 0};
+          if (r < U2) d = RoundDesc{U1 + r, 1, 4, 0, 0, 0, 0};
           return d;
         }
         if (w1_left) {
@@ -1501,15 +1549,24 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
             d.u0 = r * kFfnWarps;
             d.n = min(kFfnWarps, U1 - d.u0);
             d.kind = 1;
+            d.se = KT1 / kKtPerSlot;
             return d;
           }
           w1_left = false;
         }
-        const int r = atomicAdd(&claims[1], 1);
+        // W2 (dense path): each round's K in w2_ks parts claimed one by one
+        // (consecutive claims: the parts of one round run on different SMs),
+        // so the last rounds are short and the SMs finish together; part kp
+        // writes y plane kp, summed in part order by the combine
+        const int rk = atomicAdd(&claims[1], 1);
+        const int r = rk / ks2, kp = rk - r * ks2;
         if (r * kFfnWarps < U2) {
           d.u0 = U1 + r * kFfnWarps;
           d.n = min(kFfnWarps, U2 - r * kFfnWarps);
           d.kind = 2;
+          d.sb = kp * nst2 / ks2;
+          d.se = (kp + 1) * nst2 / ks2;
+          d.kp = kp;
         }
         return d;
       };
@@ -1555,7 +1612,6 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
         }
         const bool is1 = d.kind == 1;
         const int KT = is1 ? KT1 : KT2;
-        const int nst = KT / kKtPerSlot;
         // The round's 8 units are 8 consecutive row blocks of one expert (RB1
         // and RB2 are multiples of 8, rounds start at multiples of 8), stored
         // round-interleaved: stage s is one contiguous block.
@@ -1565,23 +1621,42 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
         const uint4* base = (is1 ? P.w1 : P.w2) +
                             (static_cast<size_t>(PR->group_a[g] - P.e_begin) * RB + rr * kFfnWarps) *
                                 KT * 32;
-        for (int s = 0; s < nst; ++s) {
-          if (s > 0) mbar_wait(&empty[stage], phase ^ 1u);
-          if (s == 0 && !is1) {
-            // W2: while the first stage is in flight, check (non-blocking) that
-            // the group's h is complete; the descriptor is published by the
-            // arrive below, and consumers skip their own acquire-wait
-            mbar_expect_tx(&full[stage], d.n * kSlotBytes);
-            bulk_g2s(ring + stage * kStageBytes, base, d.n * kSlotBytes, &full[stage], pol);
-            rdesc[seq & (kRoundRing - 1)].ready = ld_acquire_gpu(&P.w1_done[g]) >= RB1;
-            mbar_arrive(&full[stage]);
-          } else {
-            mbar_arrive_expect_tx(&full[stage], d.n * kSlotBytes);
+        // dense W2: the group's h slice of each stage rides in the stage
+        const bool hst = kDense && !is1;
+        const uint32_t sbytes = d.n * kSlotBytes + (hst ? kHSlice : 0);
+        const __nv_bfloat16* hsrc = P.hbuf + static_cast<size_t>(g) * 16 * P.Hp;
+        for (int s = d.sb; s < d.se; ++s) {
+          if (s > d.sb) mbar_wait(&empty[stage], phase ^ 1u);
+          if (s == d.sb && !is1) {
+            // W2: while the first stage's weights are in flight, check that
+            // the group's h is complete (dense path: wait for it, then order
+            // the acquired h before the bulk copies of its slices); the
+            // descriptor is published by the arrive below, and consumers
+            // skip their own acquire-wait
+            mbar_expect_tx(&full[stage], sbytes);
             bulk_g2s(ring + stage * kStageBytes,
                      base + static_cast<size_t>(s) * kFfnWarps * kKtPerSlot * 32, d.n * kSlotBytes,
                      &full[stage], pol);
+            if (hst) {
+              while (ld_acquire_gpu(&P.w1_done[g]) < RB1) __nanosleep(32);
+              fence_proxy_async_global();
+              rdesc[seq & (kRoundRing - 1)].ready = 1;
+              bulk_g2s_nohint(reinterpret_cast<uint8_t*>(SR.buf) + stage * kHSlice,
+                              hsrc + static_cast<size_t>(s) * 2048, kHSlice, &full[stage]);
+            } else {
+              rdesc[seq & (kRoundRing - 1)].ready = ld_acquire_gpu(&P.w1_done[g]) >= RB1;
+            }
+            mbar_arrive(&full[stage]);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], sbytes);
+            bulk_g2s(ring + stage * kStageBytes,
+                     base + static_cast<size_t>(s) * kFfnWarps * kKtPerSlot * 32, d.n * kSlotBytes,
+                     &full[stage], pol);
+            if (hst)
+              bulk_g2s_nohint(reinterpret_cast<uint8_t*>(SR.buf) + stage * kHSlice,
+                              hsrc + static_cast<size_t>(s) * 2048, kHSlice, &full[stage]);
           }
-          if (s == 0) next = claim();  // overlap the next claim with this round
+          if (s == d.sb) next = claim();  // overlap the next claim with this round
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1u;
@@ -1624,7 +1699,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
       if (threadIdx.x == 0) stamp(P, 1);
     }
     const int nsl = (is1 ? KT1 : KT2) / kKtPerSlot;
-    const int nst = sp ? (nsl + kFfnWarps - 1) / kFfnWarps : nsl;
+    const int nst = sp ? (nsl + kFfnWarps - 1) / kFfnWarps : d.se - d.sb;
     if (sp || warp < d.n) {
       const int uu = sp ? d.u0 : d.u0 + warp;
       Unit U;
@@ -1645,6 +1720,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
       }
       U.ready = d.ready;
       U.nw = d.n;
+      U.sb = sp ? 0 : d.sb;
+      U.kp = d.kp;
       const int nbk = (U.rows + 7) >> 3;
       if (sp) {
         if (is1)
@@ -1740,6 +1817,12 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
         float y[kSlotBatch];
 #pragma unroll
         for (int j = 0; j < kSlotBatch; ++j) y[j] = yo[j] >= 0 ? __ldcg(P.ybuf + yo[j]) : 0.0f;
+        for (int kp = 1; kp < w2ks; ++kp) {  // W2 K parts, in part order
+          const float* yk = P.ybuf + static_cast<size_t>(kp) * P.B * P.stride * P.Dp;
+#pragma unroll
+          for (int j = 0; j < kSlotBatch; ++j)
+            if (yo[j] >= 0) y[j] += __ldcg(yk + yo[j]);
+        }
 #pragma unroll
         for (int j = 0; j < kSlotBatch; ++j)
           if (s0 + j < len) sum = fmaf(w[j], y[j], sum);
@@ -1975,6 +2058,10 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
     // resident as the previous grid's exit, so it just delays the GEMV's loads)
     static const bool early = getenv("OEA_PF_EARLY") != nullptr;
     P.pf_early = early && !fb.x_stage;
+  }
+  {
+    static const int ks = getenv("OEA_W2_KSPLIT") ? atoi(getenv("OEA_W2_KSPLIT")) : kW2KSplit;
+    P.w2_ks = std::max(1, std::min(ks, kW2KSplitMax));
   }
   P.e_begin = L->e_begin;
   P.e_count = L->n_local;

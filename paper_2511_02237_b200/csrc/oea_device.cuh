@@ -138,6 +138,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Bulk copy without a cache hint (data other CTAs re-read: default policy).
+__device__ __forceinline__ void bulk_g2s_nohint(void* dst, const void* src, uint32_t bytes,
+                                                uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// Orders this thread's prior generic-proxy view of global memory (e.g. data
+// acquired from other CTAs) before its subsequent async-proxy (TMA) reads.
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // 16-byte cp.async global -> shared (src_bytes 0 zero-fills the destination).
 // L2 prefetch of a contiguous block (no shared-memory destination).
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {

@@ -35,6 +35,11 @@ constexpr int kRouterThreads = 512;
 constexpr int kRouterTokChunk = 64;    // tokens per GEMV pass in the router
 constexpr int kMaxFusedB = 256;        // fused decode batch limit
 constexpr int kMaxFusedN = 256;        // fused router expert limit (Np <= 256)
+// Dense decode (B <= 16): W2 rounds split into this many K parts (the tail
+// of the weight stream is one part long instead of one round); y then holds
+// one [B][stride][Dp] plane per part.
+constexpr int kW2KSplit = 1;  // (2-6 measured slower at C1: per-round B-operand restarts, y traffic)
+constexpr int kW2KSplitMax = 4;
 constexpr int kMaxEpWorld = 8;  // expert-parallel group size of the peer-memory combine
 // Peer table of the EP combine (device memory, read by the combine stage).
 struct EpPeers {
