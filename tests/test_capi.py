@@ -121,3 +121,16 @@ def test_ep_owner_blocks():
         for r in range(P):
             lo, hi = N * r // P, N * (r + 1) // P
             assert owners[lo:hi] == [r] * (hi - lo)
+
+
+def test_device_layer_header_compiles(tmp_path):
+    """include/oea/device_layer.hpp is self-contained C++17 over oea_cuda.h
+    (no Eigen, no CUDA headers needed by a caller)."""
+    import subprocess
+    src = tmp_path / "t.cpp"
+    src.write_text('#include "oea/device_layer.hpp"\n'
+                   "int main() { auto r = oea::device::Routing::simplified(4, 8); return r.c.k0 - 4; }\n")
+    inc = os.path.join(ROOT, "include")
+    r = subprocess.run(["g++", "-std=c++17", "-Wall", "-Wextra", "-Werror", "-fsyntax-only",
+                        "-I", inc, str(src)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr

@@ -21,3 +21,14 @@ def test_reference_suite_on_gpu(exe):
     r = subprocess.run([path], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-4000:]
     assert "0 failed" in r.stdout
+
+
+def test_device_layer_cpp_caller():
+    """include/oea/device_layer.hpp from C++: eager / host-buffer / graph /
+    PDL chain-graph decodes bit-identical, plan well formed, argument errors
+    throw std::invalid_argument (tests/cpp/device_layer_test.cpp)."""
+    path = os.path.join(BIN, "device_layer_test")
+    assert os.path.exists(path), "built by build() (paper_2511_02237_b200/csrc/Makefile)"
+    r = subprocess.run([path], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
+    assert "device_layer_test ok" in r.stdout

@@ -32,7 +32,7 @@ out = torch.empty(B, D, device="cuda", dtype=torch.float32)
 torch.cuda.synchronize()
 stream = torch.cuda.ExternalStream(ctx.stream)
 
-SLOTS = [(0, "start"), (5, "logits published"), (11, "R1 ranked"), (12, "union words polled"),
+SLOTS = [(0, "start"), (5, "logits published"), (8, "slot8 (dense: logits polled)"), (11, "R1 ranked"), (12, "union words polled"),
          (13, "union ballots"), (14, "union syncthreads"), (6, "union known"), (7, "plan ready"),
          (1, "first W2 round"), (4, "producer done"), (3, "consumers done"), (9, "combine arrive"),
          (10, "combine barrier"), (2, "combine start"), (15, "combine done")]
@@ -69,6 +69,9 @@ for name, cfg in (("oea", oea.RoutingConfig.simplified(K0, 8)), ("vanilla", oea.
         if t[:, 0].min() <= 0 or t[:, 15].max() <= 0:
             continue
         launches.append((t[:, 0].min(), t, int(r[INFO])))
+        if r[INFO + 1]:
+            print(f"    CTA0: poll {int(r[INFO + 1])} cyc in {int(r[INFO + 2])} passes, "
+                  f"select {int(r[INFO + 3])} cyc (load+sort {int(r[INFO + 4])}, merge {int(r[INFO + 5])})")
     launches.sort(key=lambda v: v[0])
     print(f"== {name} B={B} D={D} H={H} N={N}: {per_call:.2f} us per call (events), "
           f"{len(launches)} launches traced")
