@@ -213,6 +213,7 @@ __global__ void __launch_bounds__(1024)
                 int32_t* __restrict__ active_count, const uint32_t* __restrict__ union_bits,
                 int32_t* __restrict__ base_union, int32_t* __restrict__ base_count,
                 int64_t* __restrict__ total_load) {
+  pdl_wait();  // (programmatic dependent of the fast set kernels; else a no-op)
   // batched routing (route_f64_batched): CTA b aggregates record b, whose
   // per-record buffers sit at stride N (bitmaps: ceil(N / 32) words)
   if (blockIdx.x > 0) {
@@ -370,6 +371,7 @@ __global__ void __launch_bounds__(kRouteWarps * 32)
               float* __restrict__ weights_f32, int32_t* __restrict__ loads,
               int32_t* __restrict__ err_token, const int32_t* __restrict__ seg) {
   __shared__ int s_loads[128];
+  pdl_launch_dependents();  // F2 / the aggregate may launch; they wait for this grid
   for (int e = threadIdx.x; e < 128; e += blockDim.x) s_loads[e] = 0;
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -419,8 +421,10 @@ __global__ void __launch_bounds__(kRouteWarps * 32)
               int32_t* __restrict__ loads, int32_t* __restrict__ err_token,
               const int32_t* __restrict__ seg) {
   __shared__ int s_loads[128];
+  pdl_launch_dependents();  // the aggregate may launch; it waits for this grid
   for (int e = threadIdx.x; e < 128; e += blockDim.x) s_loads[e] = 0;
   __syncthreads();
+  pdl_wait();  // F1's base sets, n and union bitmap (programmatic dependent)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x * kRouteWarps + warp;
   if (i < B) {
@@ -521,19 +525,38 @@ int route_f64_launch(oea_ctx* ctx, const Cfg& cfg, int B, int N, const RouteBuff
   return OEA_OK;
 }
 
+// Launch as a programmatic dependent of the previous kernel in the stream
+// (PDL): its launch and prologue overlap the predecessor's tail; the kernel
+// calls griddepcontrol.wait before it reads the predecessor's results.
+template <typename... Params, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(Params...), int grid, int block, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t c = {};
+  c.gridDim = dim3(grid);
+  c.blockDim = dim3(block);
+  c.stream = s;
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a[0].val.programmaticStreamSerializationAllowed = 1;
+  c.attrs = a;
+  c.numAttrs = 1;
+  return cudaLaunchKernelEx(&c, kern, static_cast<Params>(args)...);
+}
+
 template <int E>
-static void launch_fast(const Cfg& cfg, int B, int N, const RouteBuffers& rb, int set_mode,
-                        int do_weights, const int32_t* seg, cudaStream_t s) {
+static cudaError_t launch_fast(const Cfg& cfg, int B, int N, const RouteBuffers& rb, int set_mode,
+                               int do_weights, const int32_t* seg, cudaStream_t s) {
   const int grid = (B + kRouteWarps - 1) / kRouteWarps;
   k_fast_p1<E><<<grid, kRouteWarps * 32, 0, s>>>(cfg, B, N, set_mode, do_weights, rb.scores,
                                                  rb.mask, rb.sets, rb.set_len, rb.t, rb.n,
                                                  rb.union_bits, rb.weights, rb.weights_f32,
                                                  rb.loads, rb.err_token, seg);
-  if (set_mode == 2)
-    k_fast_p2<E><<<grid, kRouteWarps * 32, 0, s>>>(cfg, B, N, do_weights, rb.scores, rb.mask,
-                                                   rb.n, rb.union_bits, rb.sets, rb.set_len,
-                                                   rb.weights, rb.weights_f32, rb.loads,
-                                                   rb.err_token, seg);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && set_mode == 2)
+    e = launch_pdl(k_fast_p2<E>, grid, kRouteWarps * 32, s, cfg, B, N, do_weights, rb.scores,
+                   rb.mask, rb.n, rb.union_bits, rb.sets, rb.set_len, rb.weights, rb.weights_f32,
+                   rb.loads, rb.err_token, seg);
+  return e;
 }
 
 bool route_fast_ok(const Cfg& cfg, int N, bool need_order) {
@@ -553,17 +576,19 @@ int route_f64_fast_launch(oea_ctx* ctx, const Cfg& cfg, int B, int N, const Rout
   OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.err_token, 0x7f, sizeof(int32_t), s));
   const int do_weights = (rb.weights != nullptr || rb.weights_f32 != nullptr) ? 1 : 0;
   const int32_t* sg = R > 1 ? seg : nullptr;
+  cudaError_t e;
   if (N <= 32)
-    launch_fast<1>(cfg, B, N, rb, set_mode, do_weights, sg, s);
+    e = launch_fast<1>(cfg, B, N, rb, set_mode, do_weights, sg, s);
   else if (N <= 64)
-    launch_fast<2>(cfg, B, N, rb, set_mode, do_weights, sg, s);
+    e = launch_fast<2>(cfg, B, N, rb, set_mode, do_weights, sg, s);
   else
-    launch_fast<4>(cfg, B, N, rb, set_mode, do_weights, sg, s);
+    e = launch_fast<4>(cfg, B, N, rb, set_mode, do_weights, sg, s);
+  OEA_CUDA_TRY(ctx, e);
   OEA_LAUNCHED(ctx);
   if (set_mode == 2) OEA_LAUNCHED(ctx);
-  k_aggregate<<<R, N <= 128 ? 128 : 1024, 0, s>>>(N, rb.loads, rb.active_union, rb.active_count,
-                                                  rb.union_bits, rb.base_union,
-                                                  rb.base_union_count, rb.total_load);
+  OEA_CUDA_TRY(ctx, launch_pdl(k_aggregate, R, N <= 128 ? 128 : 1024, s, N, rb.loads,
+                               rb.active_union, rb.active_count, rb.union_bits, rb.base_union,
+                               rb.base_union_count, rb.total_load));
   OEA_LAUNCHED(ctx);
   return OEA_OK;
 }
