@@ -629,9 +629,20 @@ def bench_c1(args, env):
     # ---- e2e through the C ABI from pinned host buffers ----
     # A serving loop's shape: each step's tokens (host memory) are written
     # into one pinned staging buffer (the CPU copy is inside the timed
-    # region), the decode reads it and writes out to a pinned buffer, and the
-    # call returns when out is on the host.
+    # region), the decode reads it over the host link and writes out to a
+    # pinned buffer, and the call returns when out is on the host. Timed from
+    # C (lib/e2e_host, tools/e2e_host.c: oea_moe_decode_host, no Python in
+    # the loop) and, for comparison, through the Python API (ctypes).
     import ctypes
+    e2e_c = None
+    exe = os.path.join(ROOT, "paper_2511_02237_b200", "lib", "e2e_host")
+    try:
+        r = subprocess.run([exe, str(D), str(H), str(N), str(B), str(K0), str(max(K, 100)), str(W),
+                            str(ROTATE)], capture_output=True, text=True, timeout=300,
+                           env=dict(os.environ, CUDA_VISIBLE_DEVICES=str(local)))
+        e2e_c = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # reported, the Python loop below still measures e2e
+        e2e_c = {"error": f"{type(e).__name__}: {e}"}
     x_src = xs.cpu().contiguous()          # the steps' inputs, host memory
     x_stage = torch.empty(B, D, dtype=torch.bfloat16).pin_memory()
     out_host = torch.empty(B, D, dtype=torch.float32).pin_memory()
@@ -643,7 +654,8 @@ def bench_c1(args, env):
     for i in range(W, W + K):
         ctypes.memmove(sp, x_src[i].data_ptr(), xb)
         layers[i % ROTATE].decode_host_ptr(sp, op, B, cfg)
-    e2e_us = (time.perf_counter() - t0) * 1e6 / K
+    e2e_py = (time.perf_counter() - t0) * 1e6 / K
+    e2e_us = e2e_c["us_per_step_mean"] if "us_per_step_mean" in e2e_c else e2e_py
 
     extras = {}
     if not args.no_extras:
@@ -690,7 +702,12 @@ def bench_c1(args, env):
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_us, "unit": "us/layer-call", "h2d_bytes_per_step": B * D * 2,
-                "d2h_bytes_per_step": B * D * 4},
+                "d2h_bytes_per_step": B * D * 4,
+                "how": "C caller (lib/e2e_host) of oea_moe_decode_host: per step the host copy "
+                       "of the tokens into a pinned buffer, the zero-copy fused decode (x read "
+                       "and out written over the host link), return when out is on the host; "
+                       "mean over the steps",
+                "c_harness": e2e_c, "python_api_us": e2e_py},
         "gpu_launches": launches,
         "clocks": clocks,
     }

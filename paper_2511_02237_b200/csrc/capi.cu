@@ -10,6 +10,8 @@
 #include <climits>
 #include <cstdlib>
 #include <cstring>
+#include <ctime>
+#include <cstdio>
 #include <string>
 #include <vector>
 
@@ -198,6 +200,9 @@ struct CtxExtra {
   size_t seg_bytes = 0;
   std::vector<HostGraph> host_graphs;
   uint64_t host_graph_clock = 0;
+  // completion flag of host-buffer decodes (mapped pinned int), lazily
+  int* done_flag = nullptr;
+  int* done_flag_dev = nullptr;
 };
 
 void host_graph_release(HostGraph& h) {
@@ -523,6 +528,7 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
     fb.x_in = static_cast<const __nv_bfloat16*>(x);
     fb.xpad_out = padded || x_mapped ? w.xpad : nullptr;
     fb.x_stage = x_mapped ? 1 : 0;
+    fb.done_flag = x_mapped ? extra(ctx)->done_flag_dev : nullptr;
     fb.logits = w.logits;
     fb.xlog = w.xlog;
     fb.xuni = w.xuni;
@@ -685,6 +691,7 @@ int oea_ctx_destroy(oea_ctx_t ctx) {
     for (auto& h : x->host_graphs) host_graph_release(h);
     if (x->ws.base) cudaFree(x->ws.base);
     if (x->seg_buf) cudaFree(x->seg_buf);
+    if (x->done_flag) cudaFreeHost(x->done_flag);
     delete x;
   }
   if (ctx->ffn_trace) cudaFree(ctx->ffn_trace);
@@ -1506,12 +1513,33 @@ int oea_moe_decode_host(oea_ctx_t ctx, oea_layer_t L, const void* x_host,
     // host link; no DMA copies, one launch. Other buffers take the copies.
     const void* xd = mapped_view(x_host, xbytes);
     void* od = const_cast<void*>(mapped_view(out_host, obytes));
+    CtxExtra* ex = extra(ctx);
+    if (ex->done_flag == nullptr) {
+      void* f = nullptr;
+      OEA_CUDA_TRY(ctx, cudaHostAlloc(&f, 64, cudaHostAllocMapped));
+      ex->done_flag = static_cast<int*>(f);
+      OEA_CUDA_TRY(ctx, cudaHostGetDevicePointer(reinterpret_cast<void**>(&ex->done_flag_dev), f, 0));
+    }
     if (xd != nullptr && od != nullptr) {
       ctx->last_kind = 1;
+      volatile int* flag = ex->done_flag;
+      *flag = 0;
       r = decode_host_graph(ctx, w, L, xd, B, rc, od);
       if (r == OEA_OK) {
-        OEA_CUDA_TRY(ctx, cudaStreamSynchronize(s));
-        return OEA_OK;
+        // out is on the host once the kernel raises the flag: spin on it
+        // (cheaper than a stream synchronisation's wake-up); a fault ends
+        // the wait through the stream status
+        for (uint32_t spin = 1;; ++spin) {
+          if (*flag != 0) return OEA_OK;
+          if ((spin & 1023u) == 0) {
+            const cudaError_t q = cudaStreamQuery(s);
+            if (q == cudaSuccess) {
+              if (*flag != 0) return OEA_OK;
+              return fail(ctx, OEA_ERR_CUDA, "moe_decode_host: kernel finished without completion flag");
+            }
+            if (q != cudaErrorNotReady) return oea_check_cuda(ctx, q, "moe_decode_host");
+          }
+        }
       }
       if (r != kNotFused) return r;
     }

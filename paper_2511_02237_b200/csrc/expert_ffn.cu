@@ -103,6 +103,10 @@ struct FfnParams {
   int32_t* x_base_union;
   int32_t* x_base_union_count;
   FfnHeader* x_hdr;
+  // Host-buffer decode (oea_moe_decode_host): mapped host flag the last CTA
+  // to finish its slice of out sets to 1 (the caller spins on it instead of
+  // a stream synchronisation), or null.
+  int* done_flag;
   // Expert-parallel combine over peer memory (oea_moe_decode_ep_partial): the
   // partial mixture of token t goes straight to its owner's receive buffer,
   // slot [rank][t - owner * tpr], then every CTA bumps every owner's counter.
@@ -1835,6 +1839,20 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
   };
   if constexpr (!kEp) {
     combine([&](int64_t f, float v) { P.out[f] = v; });
+    if (P.done_flag != nullptr) {
+      // out lives in mapped host memory: once every CTA's slice is visible
+      // system-wide, the last CTA raises the caller's flag (claims[6]: the
+      // completion count, reset by that last CTA)
+      asm volatile("bar.sync 2, %0;" ::"r"(kComb) : "memory");
+      if (threadIdx.x == 0) {
+        __threadfence_system();
+        if (atomicAdd(&claims[6], 1) == static_cast<int>(gridDim.x) - 1) {
+          claims[6] = 0;
+          __threadfence_system();
+          *reinterpret_cast<volatile int*>(P.done_flag) = 1;
+        }
+      }
+    }
   } else {
     const EpPeers* ep = P.ep;
     const int tpr = ep->tpr, rank = ep->rank;
@@ -2044,6 +2062,7 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   // reduction overhead, tools/trace_ffn.py): opt-in for experiments
   P.split_ok = getenv("OEA_SPLIT") != nullptr;
   P.x_stage = fb.x_stage;
+  P.done_flag = fb.done_flag;
   P.ep = fb.ep;
   {
     // ~32 MiB in total, about what HBM delivers while the prologue routes

@@ -237,6 +237,7 @@ struct FfnBuffers {
   const __nv_bfloat16* x_in = nullptr;  // [B][D] caller tokens
   __nv_bfloat16* xpad_out = nullptr;    // [B][Dp] when D != Dp (or x_stage)
   int x_stage = 0;                      // x_in is mapped host memory (staged in-kernel)
+  int* done_flag = nullptr;             // mapped host flag set to 1 when out is on the host
   const oea_dev::EpPeers* ep = nullptr;  // peer-memory EP combine (device table), or null
   float* logits = nullptr;              // [B][Np]
   unsigned long long* xlog = nullptr;   // tagged exchange words (fused path)
