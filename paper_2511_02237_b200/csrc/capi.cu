@@ -58,6 +58,7 @@ struct Workspace {
   int32_t* group_rows = nullptr;
   FfnHeader* hdr = nullptr;
   int32_t* counters = nullptr;
+  int32_t* slice_done = nullptr;  // dense path: per-group 64-bit W1 K-slot counts
   unsigned long long* xlog = nullptr;   // fused decode: tagged logits [B][Np]
   unsigned long long* xuni = nullptr;   // tagged per-token base bitmaps [B][4]
   unsigned long long* xplan = nullptr;  // tagged plan rows [B][1 + 2 S]
@@ -129,6 +130,7 @@ size_t carve(Workspace& w, bool assign) {
   take(w.out, B * D * 8);
   take(w.out32, B * D * 4);
   take(w.alias, B * S * 4);
+  take(w.slice_done, G * 8);  // (zeroed at allocation; the kernel self-resets)
   return off + 256;
 }
 
@@ -509,6 +511,7 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   fb.group_rows = w.group_rows;
   fb.hdr = w.hdr;
   fb.counters = w.counters;
+  fb.slice_done = w.slice_done;
   fb.max_groups = w.G;
   fb.hbuf = w.hbuf;
   fb.ybuf = w.ybuf;
@@ -522,7 +525,8 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
     fb.fused = 1;
     // dense-over-batch FFN when the batch is one or two n-blocks and the
     // swizzled x tile fits next to the ring (OEA_SPARSE=1 forces token lists)
-    fb.dense = B <= 16 && getenv("OEA_SPARSE") == nullptr &&
+    // (Hp <= 8192: the per-group W1 K-slot counts are 8-bit fields)
+    fb.dense = B <= 16 && L->Hp <= 8192 && getenv("OEA_SPARSE") == nullptr &&
                oea_host::ffn_bf16_smem_bytes() + oea_host::ffn_route_smem_bytes(B, L->Np, stride) +
                        oea_host::ffn_dense_xs_bytes(L->Dp) <= 227 * 1024;
     fb.x_in = static_cast<const __nv_bfloat16*>(x);

@@ -58,6 +58,11 @@ struct FfnParams {
   const int32_t* group_rows;
   const FfnHeader* hdr;
   int* w1_done;  // [max_groups]
+  // dense path: W1 release counts per group as 8 byte-wide K-slot fields of
+  // one 64-bit word [max_groups] (a slot = the h columns of ceil(Hp/128 / 8)
+  // W2 K slices): one release RMW per W1 unit, one acquire per W2 round
+  unsigned long long* w1_slots;
+  unsigned long long w1_full;  // the count word of a group whose W1 is complete
   int* claims;   // grid counters after w1_done (fixed offset, see the kernel)
   __nv_bfloat16* hbuf;  // [rows][Hp]
   float* ybuf;          // [B][stride][Dp]
@@ -152,6 +157,15 @@ struct Unit {
   int sb;      // first K slice (stage) of this round's part (W2 K split; else 0)
   int kp;      // K part: y plane this unit writes (W2 K split; else 0)
 };
+
+// Dense path: W2 stage s (h columns 128 s .. 128 s + 127) needs only the W1
+// row blocks 16 s .. 16 s + 15 of its group, so W1 releases and W2 waits go
+// per K slot instead of per group: a W2 round starts on a group's first h
+// columns while later W1 rounds of the group are still streaming.
+constexpr int kW1Slots = 8;
+__device__ __forceinline__ int w1_slot_q(int Hp) {
+  return ((Hp >> 7) + kW1Slots - 1) / kW1Slots;
+}
 
 // Shared B-operand tiles (token-list units with >= 2 n-blocks): the 8 units
 // of a round are 8 row blocks of ONE expert, so they multiply the same token
@@ -443,7 +457,12 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
     // release: the warp barrier orders the lanes' h stores before lane 0's
     // gpu-scope release increment (cumulative; no full fence, no L1 flush)
     __syncwarp();
-    if (lane == 0) red_release_gpu_add(&P.w1_done[U.g], 1);
+    if (lane == 0) {
+      if (DENSE)
+        red_release_gpu_add_u64(&P.w1_slots[U.g], 1ull << (8 * ((U.rb >> 4) / w1_slot_q(P.Hp))));
+      else
+        red_release_gpu_add(&P.w1_done[U.g], 1);
+    }
   } else {
     const int d0 = U.rb * 16;
 #pragma unroll
@@ -1146,109 +1165,6 @@ __device__ __forceinline__ void compact_smem(const FfnParams& P, uint8_t* rs, co
   sync();
 }
 
-// R2 for the WHOLE batch on the router warp of every CTA (dense path, B <=
-// 16): no plan exchange. Every token's set is the top-len union members in
-// rank order (its base set is the top n_i experts, all of them union
-// members; piggyback = the next members up to the cap, routing.cpp:270-303;
-// vanilla / pruned: len = n_i), so only the union members' logits are
-// needed: they are already published as tagged words (R1 read them). Then
-// the per-expert loads and the W2 token lists, as compact_smem. CTA 0
-// exports the plan.
-__device__ __forceinline__ void dense_route_phase2_local(const FfnParams& P, uint8_t* rs,
-                                                         const RouteSmem& L, int T) {
-  const int lane = threadIdx.x & 31;
-  const int B = P.B, N = P.N, stride = P.cfg.stride, Np = P.Np;
-  const int Bw = (B + 31) >> 5;
-  const bool exporter = blockIdx.x == 0;
-  const uint32_t* uni = reinterpret_cast<const uint32_t*>(rs + L.uni);
-  int* umem = reinterpret_cast<int*>(rs + L.ukeys);          // [T] member experts, ascending
-  float* ulg = reinterpret_cast<float*>(rs + L.rtok);         // [B][T] member logits (scratch)
-  int* len = reinterpret_cast<int*>(rs + L.len);
-  int* sets = reinterpret_cast<int*>(rs + L.sets);
-  float* se = reinterpret_cast<float*>(rs + L.e);
-  int* loads = reinterpret_cast<int*>(rs + L.loads);
-  uint32_t* tokbits = reinterpret_cast<uint32_t*>(rs + L.tokbits);
-  const uint32_t below = lanemask_lt();
-  {
-    int ub = 0;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const int e = 32 * w + lane;
-      if (e < N && ((uni[w] >> lane) & 1u)) umem[ub + __popc(uni[w] & below)] = e;
-      ub += __popc(uni[w]);
-    }
-  }
-  for (int i = lane; i < Np; i += 32) loads[i] = 0;
-  for (int i = lane; i < Np * Bw; i += 32) tokbits[i] = 0u;
-  __syncwarp();
-  // every (token, member) logit at once: one round trip for the batch
-#pragma unroll 4
-  for (int idx = lane; idx < B * T; idx += 32) {
-    const int t = idx / T, i = idx % T;
-    ulg[idx] = __uint_as_float(static_cast<uint32_t>(
-        ld_relaxed_u64(P.xlog + static_cast<size_t>(t) * Np + umem[i])));
-  }
-  __syncwarp();
-  const bool piggy = P.cfg.mode == OEA_MODE_OEA || P.cfg.mode == OEA_MODE_SIMPLIFIED;
-  const int want = P.cfg.mode == OEA_MODE_VANILLA ? P.cfg.k : P.cfg.k0;
-#pragma unroll 1
-  for (int t = 0; t < B; ++t) {
-    const bool masked = P.mask != nullptr && P.mask[t] == 0;
-    const int n = masked ? 0 : min(want, N);
-    const int cap = max(n, P.cfg.limit);
-    const int ln = masked ? 0 : piggy ? min(T, cap) : n;
-    const float* row = ulg + t * T;
-    int* srow = sets + t * stride;
-    float* erow = se + t * stride;
-#pragma unroll 1
-    for (int i = lane; i < T && ln > 0; i += 32) {
-      const uint32_t key = order_key32(row[i]);
-      int urank = 0;
-#pragma unroll 4
-      for (int j = 0; j < T; ++j) {
-        const uint32_t kj = order_key32(row[j]);
-        urank += (kj > key) | ((kj == key) & (j < i));
-      }
-      if (urank < ln) {
-        srow[urank] = umem[i];
-        erow[urank] = row[i];  // logit for now; the max (rank 0) is known below
-      }
-    }
-    __syncwarp();
-    if (lane == 0) {
-      len[t] = ln;
-      float mass = 0.0f;  // e_j = exp(l_j - l_max); sequential fp32 mass in set order
-      const float mx = ln > 0 ? erow[0] : 0.0f;
-      for (int j = 0; j < ln; ++j) {
-        erow[j] = expf(erow[j] - mx);
-        mass += erow[j];
-      }
-      for (int j = 0; j < ln; ++j) erow[j] = erow[j] / mass;
-    }
-    __syncwarp();
-    for (int j = lane; j < stride; j += 32) {
-      const bool in = j < ln;
-      if (in) {
-        atomicAdd(&loads[srow[j]], 1);
-        atomicOr(&tokbits[srow[j] * Bw + (t >> 5)], 1u << (t & 31));
-      }
-      if (exporter) {
-        const size_t o = static_cast<size_t>(t) * stride + j;
-        const float w = in ? erow[j] : 0.0f;
-        P.x_sets[o] = in ? srow[j] : -1;
-        P.x_w32[o] = w;
-        if (P.x_w64) P.x_w64[o] = static_cast<double>(w);
-      }
-    }
-    if (exporter && lane == 0) {
-      P.x_set_len[t] = ln;
-      if (P.x_phase1_n) P.x_phase1_n[t] = P.cfg.mode == OEA_MODE_VANILLA ? 0 : n;
-    }
-  }
-  __syncwarp();
-  compact_smem<1>(P, rs, L, reinterpret_cast<const int*>(rs + L.misc)[0], exporter);
-}
-
 // R2 + plan exchange + compaction on NW warps (8 consumer warps on the token
 // list path, the router warp on the dense path).
 template <int NW>
@@ -1519,11 +1435,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
       // exchange latency before W2, which matters when W1 is short); many:
       // CTA t ranks token t and the plan rows are exchanged (the O(B T^2)
       // redundant work would otherwise steal issue slots from the consumers)
-      const int Tu = reinterpret_cast<const int*>(rs + RL.misc)[1];
-      if (Tu * P.B <= 512)
-        dense_route_phase2_local(P, rs, RL, Tu);
-      else
-        route_phase2_plan<1>(P, rs, RL, G, tag);
+      route_phase2_plan<1>(P, rs, RL, G, tag);
       if (lane == 0) {
         stamp(P, 7);
         mbar_arrive(plan_bar);  // W2 rounds may start
@@ -1575,9 +1487,18 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
         return d;
       };
       RoundDesc next = claim();
+      // debug round log: per CTA kTraceRounds x {start, kind/group/unit, W2 h ready}
+      unsigned long long* rlog =
+          s_trace ? s_trace + kTraceRoundLog + blockIdx.x * kTraceRounds * 3 : nullptr;
       for (int seq = 0;; ++seq) {
         const RoundDesc d = next;
         mbar_wait(&empty[stage], phase ^ 1u);
+        if (rlog != nullptr && seq < kTraceRounds) {
+          rlog[3 * seq] = gtimer();
+          rlog[3 * seq + 1] = (static_cast<unsigned long long>(d.kind) << 56) |
+                              (static_cast<unsigned long long>(d.n) << 48) |
+                              static_cast<unsigned long long>(static_cast<uint32_t>(d.u0));
+        }
         rdesc[seq & (kRoundRing - 1)] = d;
         if (d.n == 0) {
           mbar_arrive(&full[stage]);  // end-of-work message, no payload
@@ -1629,9 +1550,36 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
         const bool hst = kDense && !is1;
         const uint32_t sbytes = d.n * kSlotBytes + (hst ? kHSlice : 0);
         const __nv_bfloat16* hsrc = P.hbuf + static_cast<size_t>(g) * 16 * P.Hp;
+        const int sq = hst ? w1_slot_q(P.Hp) : 1;
+        unsigned long long* const wsl = hst ? P.w1_slots + g : nullptr;
+        // slot field c is complete when it equals its row-block count, so
+        // (count word ^ full) has a zero byte c exactly for the complete slots
+        unsigned long long miss = ~0ull;
         for (int s = d.sb; s < d.se; ++s) {
           if (s > d.sb) mbar_wait(&empty[stage], phase ^ 1u);
-          if (s == d.sb && !is1) {
+          if (hst) {
+            // the stage's weights first, then wait for its h slot and copy it
+            // (h rides in the stage: consumers never wait on W1 themselves)
+            if (s == d.sb) rdesc[seq & (kRoundRing - 1)].ready = 1;
+            mbar_arrive_expect_tx(&full[stage], sbytes);
+            bulk_g2s(ring + stage * kStageBytes,
+                     base + static_cast<size_t>(s) * kFfnWarps * kKtPerSlot * 32, d.n * kSlotBytes,
+                     &full[stage], pol);
+            const int c = s / sq;
+            if (s == d.sb) miss = ld_acquire_u64(wsl) ^ P.w1_full;  // every slot, one acquire
+            bool acq = s == d.sb;
+            while ((miss >> (8 * c)) & 0xffu) {
+              __nanosleep(32);
+              miss = ld_acquire_u64(wsl) ^ P.w1_full;
+              acq = true;
+            }
+            if (acq) {  // h acquired since the last fence: order it before the async-proxy copy
+              if (rlog != nullptr && seq < kTraceRounds && s == d.sb) rlog[3 * seq + 2] = gtimer();
+              fence_proxy_async_global();
+            }
+            bulk_g2s_nohint(reinterpret_cast<uint8_t*>(SR.buf) + stage * kHSlice,
+                            hsrc + static_cast<size_t>(s) * 2048, kHSlice, &full[stage]);
+          } else if (s == d.sb && !is1) {
             // W2: while the first stage's weights are in flight, check that
             // the group's h is complete (dense path: wait for it, then order
             // the acquired h before the bulk copies of its slices); the
@@ -1641,24 +1589,13 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
             bulk_g2s(ring + stage * kStageBytes,
                      base + static_cast<size_t>(s) * kFfnWarps * kKtPerSlot * 32, d.n * kSlotBytes,
                      &full[stage], pol);
-            if (hst) {
-              while (ld_acquire_gpu(&P.w1_done[g]) < RB1) __nanosleep(32);
-              fence_proxy_async_global();
-              rdesc[seq & (kRoundRing - 1)].ready = 1;
-              bulk_g2s_nohint(reinterpret_cast<uint8_t*>(SR.buf) + stage * kHSlice,
-                              hsrc + static_cast<size_t>(s) * 2048, kHSlice, &full[stage]);
-            } else {
-              rdesc[seq & (kRoundRing - 1)].ready = ld_acquire_gpu(&P.w1_done[g]) >= RB1;
-            }
+            rdesc[seq & (kRoundRing - 1)].ready = ld_acquire_gpu(&P.w1_done[g]) >= RB1;
             mbar_arrive(&full[stage]);
           } else {
             mbar_arrive_expect_tx(&full[stage], sbytes);
             bulk_g2s(ring + stage * kStageBytes,
                      base + static_cast<size_t>(s) * kFfnWarps * kKtPerSlot * 32, d.n * kSlotBytes,
                      &full[stage], pol);
-            if (hst)
-              bulk_g2s_nohint(reinterpret_cast<uint8_t*>(SR.buf) + stage * kHSlice,
-                              hsrc + static_cast<size_t>(s) * 2048, kHSlice, &full[stage]);
           }
           if (s == d.sb) next = claim();  // overlap the next claim with this round
           if (++stage == kStages) {
@@ -1795,6 +1732,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
       int* done = claims + ((tag & 1u) ? 5 : 2);
       if (atom_add_acq_rel_gpu(done, 1) == static_cast<int>(gridDim.x) - 1) {
         for (int g = 0; g < G; ++g) P.w1_done[g] = 0;
+        if (kDense)
+          for (int g = 0; g < G; ++g) P.w1_slots[g] = 0ull;
         claims[0] = 0;
         claims[1] = 0;
         claims[3] = 0;
@@ -2049,6 +1988,13 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   P.group_rows = fb.group_rows;
   P.hdr = fb.hdr;
   P.w1_done = fb.counters;
+  P.w1_slots = reinterpret_cast<unsigned long long*>(fb.slice_done);
+  {
+    const int ns = L->Hp >> 7, q = (ns + kW1Slots - 1) / kW1Slots;
+    P.w1_full = 0ull;
+    for (int c = 0; c * q < ns; ++c)
+      P.w1_full |= static_cast<unsigned long long>(16 * (std::min(ns, (c + 1) * q) - c * q)) << (8 * c);
+  }
   P.claims = fb.counters + fb.max_groups;
   P.hbuf = static_cast<__nv_bfloat16*>(fb.hbuf);
   P.ybuf = static_cast<float*>(fb.ybuf);

@@ -53,7 +53,9 @@ constexpr int kMaxRouteN = 1024;       // route_f64 expert limit
 // by the launch epoch); word kTraceInfo of a region = the launch's T.
 constexpr int kTraceLegacy = 8192;
 constexpr int kTraceLaunches = 16;
-constexpr int kTracePerLaunch = 4096;
+constexpr int kTracePerLaunch = 16384;
+constexpr int kTraceRoundLog = 4096;  // per-CTA producer round log inside a launch region
+constexpr int kTraceRounds = 24;
 constexpr int kTraceInfo = 2400;
 constexpr size_t kTraceWords = kTraceLegacy + static_cast<size_t>(kTraceLaunches) * kTracePerLaunch;
 
@@ -219,6 +221,7 @@ struct FfnBuffers {
   const int32_t* group_rows;
   const oea_dev::FfnHeader* hdr;
   int32_t* counters;       // [max_groups] w1_done then [Dp/16] combine counters
+  int32_t* slice_done = nullptr;  // dense path: [max_groups] u64, 8-bit W1 K-slot counts
   int max_groups;
   void* hbuf;              // [rows][Hp] (bf16) / [rows][H] (T)
   void* ybuf;              // [B][stride][Dp] f32 / [B][stride][D] T

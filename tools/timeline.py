@@ -32,7 +32,7 @@ out = torch.empty(B, D, device="cuda", dtype=torch.float32)
 torch.cuda.synchronize()
 stream = torch.cuda.ExternalStream(ctx.stream)
 
-SLOTS = [(0, "start"), (5, "logits published"), (8, "slot8 (dense: logits polled)"), (11, "R1 ranked"), (12, "union words polled"),
+SLOTS = [(0, "start"), (5, "logits published"), (8, "slot8 (dense: logits polled)"), (11, "R1 ranked"), (12, "logits polled (local) / union words polled"),
          (13, "union ballots"), (14, "union syncthreads"), (6, "union known"), (7, "plan ready"),
          (1, "first W2 round"), (4, "producer done"), (3, "consumers done"), (9, "combine arrive"),
          (10, "combine barrier"), (2, "combine start"), (15, "combine done")]
@@ -59,7 +59,8 @@ for name, cfg in (("oea", oea.RoutingConfig.simplified(K0, 8)), ("vanilla", oea.
         e1.record(stream)
     e1.synchronize()
     per_call = e0.elapsed_time(e1) * 1000.0 / (REPS - 4)
-    LEG, NL, PER, INFO = 8192, 16, 4096, 2400
+    LEG, NL, PER, INFO = 8192, 16, 16384, 2400
+    RLOG, NR = 4096, 24
     buf = np.zeros(LEG + NL * PER, np.uint64)
     ctx.check(lib().oea_debug_ffn_trace(ctx.h, buf.ctypes.data_as(C.c_void_p), buf.size))
     regs = buf[LEG:].reshape(NL, PER).astype(np.int64)
@@ -99,6 +100,49 @@ for name, cfg in (("oea", oea.RoutingConfig.simplified(K0, 8)), ("vanilla", oea.
     if gaps:
         print(f"  gap (last combine done -> next first start) median {np.median(gaps):.2f} us "
               f"[{min(gaps):.2f}, {max(gaps):.2f}]")
+    if os.environ.get("ROUNDS") == "1" and launches:
+        # producer round log of the median-span launch: per-kind round times and
+        # the aggregate weight stream rate per 2 us bin
+        order = np.argsort(spans)
+        li = int(order[len(order) // 2])
+        t0, t, T = launches[li]
+        reg = [r for r in regs if r[:148 * 16].reshape(148, 16)[:, 0].min() == t0][0]
+        rl = reg[RLOG:RLOG + 148 * NR * 3].reshape(148, NR, 3)
+        KT1, KT2 = (D + 15) // 16 // 8, (H + 15) // 16 // 8
+        rows = []
+        for c in range(148):
+            ends = list(rl[c, 1:, 0]) + [0]
+            for j in range(NR):
+                st, desc, hr = rl[c, j]
+                if st <= 0:
+                    break
+                kind, n = int(desc) >> 56, (int(desc) >> 48) & 0xff
+                if n == 0:
+                    break
+                en = ends[j] if ends[j] > 0 else t[c, 4]
+                nst = KT1 if kind == 1 else KT2
+                rows.append((c, kind, (st - t0) / 1e3, (en - t0) / 1e3, n * 4096 * nst,
+                             (hr - t0) / 1e3 if hr > 0 else None))
+        for kind in (1, 2):
+            d = [r[3] - r[2] for r in rows if r[1] == kind]
+            if d:
+                print(f"  kind {kind}: {len(d)} rounds, dur med {np.median(d):.2f} min {min(d):.2f} max {max(d):.2f} us")
+        w2w = [r[5] - r[2] for r in rows if r[1] == 2 and r[5] is not None]
+        if w2w:
+            print(f"  W2 h-wait (ready - round start): med {np.median(w2w):.2f} max {max(w2w):.2f} us, >0.5us: {sum(1 for v in w2w if v > 0.5)}")
+        end = max(r[3] for r in rows)
+        bins = np.zeros(int(end // 2) + 2)
+        act = np.zeros_like(bins)
+        for r in rows:
+            a, b, by = r[2], r[3], r[4]
+            rate = by / max(b - a, 1e-3)  # bytes per us
+            for k in range(int(a // 2), int(b // 2) + 1):
+                lo, hi = max(a, 2 * k), min(b, 2 * k + 2)
+                if hi > lo:
+                    bins[k] += rate * (hi - lo) / 2.0
+                    act[k] += (hi - lo) / 2.0
+        print("  stream TB/s per 2us bin: " + " ".join(f"{v / 1e6:.1f}" for v in bins))
+        print("  active SMs per 2us bin:  " + " ".join(f"{v:.0f}" for v in act))
     for (t0, t, T), sp in zip(launches, spans):
         pd = (t[:, 4] - t0) / 1000.0
         print(f"    T={T:3d} span {sp:6.2f}  union {(t[:, 6].max() - t0) / 1000.0:5.2f}  "
