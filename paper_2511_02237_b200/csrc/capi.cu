@@ -59,6 +59,7 @@ struct Workspace {
   FfnHeader* hdr = nullptr;
   int32_t* counters = nullptr;
   int32_t* slice_done = nullptr;  // dense path: per-group 64-bit W1 K-slot counts
+  void* xg = nullptr;             // tcgen05 FFN: token rows in plan order, UMMA layout
   unsigned long long* xlog = nullptr;   // fused decode: tagged logits [B][Np]
   unsigned long long* xuni = nullptr;   // tagged per-token base bitmaps [B][4]
   unsigned long long* xplan = nullptr;  // tagged plan rows [B][1 + 2 S]
@@ -130,7 +131,8 @@ size_t carve(Workspace& w, bool assign) {
   take(w.out, B * D * 8);
   take(w.out32, B * D * 4);
   take(w.alias, B * S * 4);
-  take(w.slice_done, G * 8);  // (zeroed at allocation; the kernel self-resets)
+  take(w.slice_done, G * 8);
+  take(w.xg, (R + 16) * Dp * 2);  // (zeroed at allocation; the kernel self-resets)
   return off + 256;
 }
 
@@ -403,6 +405,18 @@ bool fused_ok(const oea_layer* L, int B, const oea_routing_cfg& rc) {
                  oea_host::ffn_route_smem_bytes(B, L->Np, stride_of(rc)) <= 227 * 1024;
 }
 
+// Large batches take the tcgen05 FFN unless OEA_UMMA=0. Its weight copy is
+// allocated on first use, which a stream capture cannot do: captured before
+// that first use, the mma.sync FFN is captured instead.
+bool umma_ok(oea_ctx* ctx, const oea_layer* L, cudaStream_t s) {
+  static const bool off = getenv("OEA_UMMA") != nullptr && atoi(getenv("OEA_UMMA")) == 0;
+  if (off || L->dtype != OEA_DTYPE_BF16 || L->n_local < L->N) return false;
+  if (L->w1u != nullptr && !L->umma_stale) return true;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s == nullptr ? ctx->stream : s, &cs) != cudaSuccess) return false;
+  return cs == cudaStreamCaptureStatusNone;
+}
+
 // part: 0 = router + FFN (PDL-chained), 1 = router only, 2 = FFN only.
 constexpr int kNotFused = -1000;  // decode_bf16(x_mapped): not on the fused path, nothing launched
 // x_mapped: x and out are device views of mapped (pinned) host memory; only
@@ -551,6 +565,17 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
     fb.x_base_union = w.base_union;
     fb.x_base_union_count = w.base_union_count;
     fb.x_hdr = w.hdr;
+  }
+  if (big && umma_ok(ctx, L, s)) {
+    // tcgen05 (UMMA + TMEM) grouped FFN; the layer's UMMA-layout weight copy
+    // is made (or refreshed in place) on first use
+    if (L->w1u == nullptr || L->umma_stale) {
+      if (L->w1u != nullptr) oea_host::layer_drop_umma(L);  // (not capturing: checked)
+      r = oea_host::layer_prepare_umma(ctx, L, s);
+      if (r) return r;
+      L->umma_stale = 0;
+    }
+    return oea_host::ffn_umma_launch(ctx, L, B, stride, fb, w.xg, static_cast<int>((w.R + 16) / 8), s);
   }
   return oea_host::ffn_bf16_launch(ctx, L, B, stride, fb, part == 0 && !fused && !big, s);
 }
@@ -1186,6 +1211,7 @@ int oea_layer_destroy(oea_layer_t L) {
   cudaFree(L->w1);
   cudaFree(L->w_up);
   cudaFree(L->w2);
+  oea_host::layer_drop_umma(L);
   delete L;
   return OEA_OK;
 }
@@ -1212,11 +1238,13 @@ int oea_layer_upload_expert(oea_layer_t L, int32_t e, const void* w_gate, const 
     return fail(L->ctx, OEA_ERR_INVALID_ARGUMENT, "expert index out of range");
   int r = check_dtype(L->ctx, src_dtype);
   if (r) return r;
+  L->umma_stale = 1;
   return oea_host::layer_upload_expert(L, e, w_gate, w_up, w_down, src_dtype, src_on_device);
 }
 
 int oea_layer_init_random(oea_layer_t L, uint64_t seed) {
   if (L == nullptr) return fail(nullptr, OEA_ERR_INVALID_ARGUMENT, "null layer");
+  L->umma_stale = 1;
   return oea_host::layer_init_random(L, seed);
 }
 

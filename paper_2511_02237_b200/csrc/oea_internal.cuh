@@ -123,6 +123,12 @@ struct oea_layer {
   void* w_up = nullptr;        // f32/f64 only: [N][D][H]
   void* w2 = nullptr;          // bf16: [N][Dp/16][Hp/16][32][8]; else down [N][H][D]
   size_t router_bytes = 0, w1_bytes = 0, w2_bytes = 0, up_bytes = 0;
+  // bf16, large batches (B > 64): the expert weights again in the canonical
+  // K-major UMMA layout for the tcgen05 FFN (umma_ffn.cu), made on first use;
+  // umma_stale: the weights changed since (re-packed in place on next use)
+  void* w1u = nullptr;
+  void* w2u = nullptr;
+  int umma_stale = 0;
 };
 
 struct oea_graph {
@@ -271,6 +277,11 @@ size_t ffn_params_bytes();
 void ffn_params_set_io(void* params, const void* x_in, void* out);
 size_t ffn_btile_bytes();
 size_t ffn_dense_xs_bytes(int Dp);
+// tcgen05 grouped FFN (umma_ffn.cu)
+int layer_prepare_umma(oea_ctx* ctx, oea_layer* L, cudaStream_t s);
+void layer_drop_umma(oea_layer* L);
+int ffn_umma_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const FfnBuffers& fb,
+                    void* xg, int RG, cudaStream_t s);
 int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride,
                     const FfnBuffers& fb, bool pdl, cudaStream_t s);
 int ffn_simt_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride,
