@@ -507,7 +507,8 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
     r = oea_host::ffn_bf16_launch(ctx, L, B, stride, rf, false, s);
     if (r) return r;
     oea_host::CompactBuffers cb{w.sets, w.set_len, w.row_tok, w.row_slot, w.group_a,
-                                w.group_row0, w.group_rows, w.hdr, w.counters, w.G + 7};
+                                w.group_row0, w.group_rows, w.hdr, w.counters, w.G + 7, w.loads,
+                                w.total_load};
     r = oea_host::compact_launch(ctx, B, L->N, stride, cb, w.tokbits, w.active_union,
                                  w.active_count, s);
     if (r) return r;

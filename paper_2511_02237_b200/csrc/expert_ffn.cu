@@ -776,27 +776,37 @@ __device__ __forceinline__ void tile_gemv(const FfnParams& P, float* red, uint32
 #pragma unroll
       for (int nb = 0; nb < 2; ++nb) acc[nb][0] = acc[nb][1] = acc[nb][2] = acc[nb][3] = 0.0f;
       const int kt0 = warp * KT / kFfnWarps, kt1 = (warp + 1) * KT / kFfnWarps;
+      // (route-only launches have D == Dp; tokens past B read row B-1 and
+      // their logits are dropped below: no branches around the loads, so a
+      // warp's loads for up to 16 k-tiles are all in flight at once)
       const uint32_t* xr[2];
 #pragma unroll
-      for (int nb = 0; nb < 2; ++nb) {
-        const int t = tb * 16 + nb * 8 + gq;
-        xr[nb] = t < P.B ? reinterpret_cast<const uint32_t*>(P.x_in + static_cast<size_t>(t) * P.D)
-                         : nullptr;
-      }
-#pragma unroll 4
-      for (int kt = kt0; kt < kt1; ++kt) {
-        const uint4 a = __ldcg(P.router_frag + (static_cast<size_t>(eb) * KT + kt) * 32 + lane);
-        const int k = kt * 16 + 2 * q;
+      for (int nb = 0; nb < 2; ++nb)
+        xr[nb] = reinterpret_cast<const uint32_t*>(
+            P.x_in + static_cast<size_t>(min(tb * 16 + nb * 8 + gq, P.B - 1)) * P.D);
+      const uint4* arow = P.router_frag + static_cast<size_t>(eb) * KT * 32 + lane;
+#pragma unroll 1
+      for (int k0 = kt0; k0 < kt1; k0 += 16) {
+        uint4 a[16];
+        uint32_t b[16][2][2];
 #pragma unroll
-        for (int nb = 0; nb < 2; ++nb) {
-          uint32_t b0 = 0, b1 = 0;
-          if (xr[nb] != nullptr) {
-            if (k < P.D) b0 = __ldcg(xr[nb] + (k >> 1));
-            if (k + 8 < P.D) b1 = __ldcg(xr[nb] + ((k + 8) >> 1));
+        for (int i = 0; i < 16; ++i) {
+          const int kt = min(k0 + i, kt1 - 1);
+          a[i] = __ldg(arow + static_cast<size_t>(kt) * 32);
+          const int kw = (kt * 16 + 2 * q) >> 1;
+#pragma unroll
+          for (int nb = 0; nb < 2; ++nb) {
+            b[i][nb][0] = __ldg(xr[nb] + kw);
+            b[i][nb][1] = __ldg(xr[nb] + kw + 4);
           }
-          mma_bf16_16816(acc[nb], a, b0, b1);
         }
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (k0 + i < kt1)
+#pragma unroll
+            for (int nb = 0; nb < 2; ++nb) mma_bf16_16816(acc[nb], a[i], b[i][nb][0], b[i][nb][1]);
       }
+      if (threadIdx.x == 0) stamp(P, 9);
       float* mine = red + (warp * 32 + lane) * 8;
 #pragma unroll
       for (int nb = 0; nb < 2; ++nb)
@@ -804,6 +814,7 @@ __device__ __forceinline__ void tile_gemv(const FfnParams& P, float* red, uint32
         for (int i = 0; i < 4; ++i) mine[nb * 4 + i] = acc[nb][i];
     }
     __syncthreads();
+    if (threadIdx.x == 0) stamp(P, 10);
     if (warp == 0) {
       // lane (gq, q): experts 16eb + gq (+8), tokens 16tb + 8nb + 2q (+1)
 #pragma unroll
@@ -972,7 +983,7 @@ __device__ __forceinline__ void rank_phase2(const FfnParams& P, int t, uint8_t* 
 // (slot -1 for the others). Returns the number of groups; CTA 0 exports the
 // full base / active union.
 __device__ __forceinline__ int union_barrier(const FfnParams& P, uint8_t* rs, const RouteSmem& L,
-                                             uint32_t tag) {
+                                             uint32_t tag, const int* arrived = nullptr) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t* uni = reinterpret_cast<uint32_t*>(rs + L.uni);
   int* active = reinterpret_cast<int*>(rs + L.active);
@@ -980,6 +991,13 @@ __device__ __forceinline__ int union_barrier(const FfnParams& P, uint8_t* rs, co
   int* misc = reinterpret_cast<int*>(rs + L.misc);
   const bool exporter = blockIdx.x == 0;
   {
+    // many tokens (route-only launch): one poller per CTA on the count of
+    // routed tokens instead of B pollers per CTA on the words themselves
+    if (arrived != nullptr) {
+      if (threadIdx.x == 0)
+        while (ld_acquire_gpu(arrived) < P.B) __nanosleep(64);
+      __syncthreads();
+    }
     // union = OR of the tokens' base bitmaps: thread t < B polls token t's
     // four tagged words (all in flight at once) until they carry this
     // launch's tag; rows OR-ed by lanes 0..3 of warp 0 below
@@ -997,7 +1015,8 @@ __device__ __forceinline__ int union_barrier(const FfnParams& P, uint8_t* rs, co
         for (int i = 0; i < 4; ++i) ready &= static_cast<uint32_t>(v[i] >> 32) == tag;
         v4 = make_uint4(static_cast<uint32_t>(v[0]), static_cast<uint32_t>(v[1]),
                         static_cast<uint32_t>(v[2]), static_cast<uint32_t>(v[3]));
-        if (!ready) __nanosleep(40);  // every CTA polls the same words: back off
+        // every CTA polls the same words: back off (more with many pollers)
+        if (!ready) __nanosleep(P.B > 64 ? 200 : 40);
       } while (!ready);
       reinterpret_cast<uint4*>(rows)[t] = v4;
     }
@@ -1361,9 +1380,10 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
     // the x staging, when HBM idles longest)
     if (!kRouteOnly && !pf_early && P.x_stage && warp == kProducerWarp && P.prefetch_bytes > 0)
       prefetch_w1_heads(P, lane);
-    if (kRouteOnly)
+    if (kRouteOnly) {
+      if (threadIdx.x == 0) stamp(P, 8);
       tile_gemv(P, SR.buf, tag);
-    else
+    } else
       fused_gemv(P, reinterpret_cast<float*>(rs + RL.red), claims + 3, tag);
     if (threadIdx.x == 0) stamp(P, 5);
     // (x in device memory: after the GEMV, whose loads it would delay)
@@ -1376,19 +1396,29 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
         rank_phase1(P, t, rs, RL, tag);
         asm volatile("bar.sync 3, 128;" ::: "memory");  // keys[] reused by the next token
       }
+      // route-only: count this CTA's routed tokens (the barrier above orders
+      // the 4 warps' base-bitmap words before the cumulative release)
+      if (kRouteOnly && threadIdx.x == 0 && static_cast<int>(blockIdx.x) < P.B)
+        red_release_gpu_add(claims + 3, (P.B - 1 - static_cast<int>(blockIdx.x)) /
+                                                static_cast<int>(gridDim.x) + 1);
       if (threadIdx.x == 0) stamp(P, 11);
     }
-    const int T = union_barrier(P, rs, RL, tag);  // ends with __syncthreads
+    // (ends with __syncthreads)
+    const int T = union_barrier(P, rs, RL, tag, kRouteOnly ? claims + 3 : nullptr);
     if (threadIdx.x == 0) {
       PR->G = T;
       stamp(P, 6);
       if (s_trace && blockIdx.x == 0) s_trace[kTraceInfo] = static_cast<unsigned long long>(T);
     }
     if (kRouteOnly) {
-      // plan rows (CTA t: token t, t + grid, ...); CTA 0 also gathers the batch
-      // plan and exports the aggregates. The FFN tables follow from k_compact.
-      if (warp < kFfnWarps) route_phase2_plan<kFfnWarps>(P, rs, RL, T, tag, blockIdx.x == 0);
-      if (threadIdx.x == 0) grid_exit(P, claims, 0);
+      // plan rows (CTA t: token t, t + grid, ...); the FFN tables and the
+      // aggregates (loads, header) follow from k_compact.
+      if (warp < kFfnWarps) route_phase2_plan<kFfnWarps>(P, rs, RL, T, tag, false);
+      if (threadIdx.x == 0) {
+        stamp(P, 7);
+        grid_exit(P, claims, 0);
+        stamp(P, 15);
+      }
       return;
     }
   } else if (threadIdx.x == 0) {

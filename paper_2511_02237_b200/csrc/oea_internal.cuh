@@ -210,6 +210,8 @@ struct CompactBuffers {
   oea_dev::FfnHeader* hdr;
   int32_t* counters;     // zeroed: [G + Dp/16 + 1]
   int n_counters;
+  int32_t* loads_out = nullptr;  // [N] per-expert loads (exported plan), or null
+  int64_t* total_load = nullptr;
 };
 int compact_launch(oea_ctx* ctx, int B, int N, int stride, const CompactBuffers& cb,
                    uint32_t* tokbits, int32_t* active_union, int32_t* active_count,

@@ -191,14 +191,23 @@ __global__ void __launch_bounds__(512)
               int32_t* __restrict__ row_tok, int32_t* __restrict__ row_slot,
               int32_t* __restrict__ group_a, int32_t* __restrict__ group_row0,
               int32_t* __restrict__ group_rows, FfnHeader* __restrict__ hdr,
-              int32_t* __restrict__ counters, int n_counters) {
+              int32_t* __restrict__ counters, int n_counters, int32_t* __restrict__ loads_out,
+              int64_t* __restrict__ total_load) {
   extern __shared__ int s_dyn[];
   int* s_loads = s_dyn;
   int* s_eslot = s_loads + N;
   int* s_rowb = s_eslot + N;
   int* s_grpb = s_rowb + N;
+  // token bitmaps in shared memory when they fit (else the zeroed global copy)
+  const int nbits = N * ((B + 31) >> 5);
+  uint32_t* s_bits = reinterpret_cast<uint32_t*>(s_grpb + N);
+  if (tokbits == nullptr) {
+    for (int i = threadIdx.x; i < nbits; i += blockDim.x) s_bits[i] = 0u;
+    tokbits = s_bits;
+    __syncthreads();
+  }
   __shared__ int s_tmp[40];
-  CompactOut o{active_union, active_count, nullptr, nullptr, row_tok, row_slot, group_a,
+  CompactOut o{active_union, active_count, total_load, loads_out, row_tok, row_slot, group_a,
                group_row0, group_rows, hdr, counters, n_counters};
   compact_plan(B, N, stride, sets, set_len, s_loads, s_eslot, s_rowb, s_grpb, tokbits, s_tmp, o);
 }
@@ -882,14 +891,18 @@ int compact_launch(oea_ctx* ctx, int B, int N, int stride, const CompactBuffers&
                    uint32_t* tokbits, int32_t* active_union, int32_t* active_count,
                    cudaStream_t s) {
   const size_t bits = static_cast<size_t>(N) * ((B + 31) / 32) * 4;
-  OEA_CUDA_TRY(ctx, cudaMemsetAsync(tokbits, 0, bits, s));
-  const size_t smem = static_cast<size_t>(4) * N * sizeof(int);
+  // token bitmaps in shared memory (zeroed in-kernel) when they fit
+  const bool sbits = static_cast<size_t>(4) * N * sizeof(int) + bits <= 96 * 1024;
+  if (!sbits) OEA_CUDA_TRY(ctx, cudaMemsetAsync(tokbits, 0, bits, s));
+  const size_t smem = static_cast<size_t>(4) * N * sizeof(int) + (sbits ? bits : 0);
   if (smem > 48 * 1024)
     OEA_CUDA_TRY(ctx, cudaFuncSetAttribute(k_compact, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem)));
-  k_compact<<<1, 512, smem, s>>>(B, N, stride, cb.sets, cb.set_len, tokbits, active_union,
+  k_compact<<<1, 512, smem, s>>>(B, N, stride, cb.sets, cb.set_len, sbits ? nullptr : tokbits,
+                                 active_union,
                                  active_count, cb.row_tok, cb.row_slot, cb.group_a, cb.group_row0,
-                                 cb.group_rows, cb.hdr, cb.counters, cb.n_counters);
+                                 cb.group_rows, cb.hdr, cb.counters, cb.n_counters, cb.loads_out,
+                                 cb.total_load);
   OEA_LAUNCHED(ctx);
   return OEA_OK;
 }

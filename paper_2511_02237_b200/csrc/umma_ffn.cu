@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(kUmThreads, 1) k_ffn_umma(const UmmaParams P) 
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();  // plan tables and x come from the preceding launches
+  pdl_launch_dependents();  // (the combine waits for this grid's completion)
 
   const int G = P.hdr->n_groups;
   const int M1 = P.Hp >> 6, M2 = P.Dp >> 7;  // m-blocks per group (W1: 64 h; W2: 128 d)
@@ -348,34 +349,61 @@ __global__ void __launch_bounds__(kUmThreads, 1) k_ffn_umma(const UmmaParams P) 
 }
 
 // Token rows of the plan (row -> token, -1 = padding) gathered into the CM
-// layout of xg: one thread per 16-byte chunk (8 k of one row).
+// layout of xg: one thread per 16-byte chunk (8 k of one row), threads in
+// destination order (8 rows of a core matrix, then its 16 k-groups), so a
+// warp's stores are one contiguous 512-byte run.
 __global__ void k_gather_xg(const __nv_bfloat16* __restrict__ x, int Dp, const int32_t* __restrict__ row_tok,
                             const FfnHeader* __restrict__ hdr, int RG, uint8_t* __restrict__ xg) {
-  const int R = min(hdr->n_rows + 16, RG * 8);
-  const int nch = Dp >> 3;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < R * nch; i += gridDim.x * blockDim.x) {
-    const int r = i / nch, ch = i - r * nch;
-    const int t = r < hdr->n_rows ? row_tok[r] : -1;
-    const uint4 v = t >= 0 ? *reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * Dp + ch * 8)
+  const int nrows = hdr->n_rows;
+  const int rgs = min((nrows + 16 + 7) >> 3, RG);  // row groups to fill (+ the N round-up slack)
+  const int S = Dp >> 7;
+  const int total = S * rgs * 128;                 // 16-byte chunks
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int r8 = i & 7, kg = (i >> 3) & 15, blk = i >> 7;
+    const int rg = blk % rgs, s = blk / rgs;
+    const int r = rg * 8 + r8;
+    const int t = r < nrows ? row_tok[r] : -1;
+    const uint4 v = t >= 0 ? __ldg(reinterpret_cast<const uint4*>(x + static_cast<size_t>(t) * Dp +
+                                                                   s * 128 + kg * 8))
                            : make_uint4(0u, 0u, 0u, 0u);
-    const int s = ch >> 4, kg = ch & 15;
-    *reinterpret_cast<uint4*>(xg + (static_cast<size_t>(s) * RG + (r >> 3)) * 2048 + kg * 128 +
-                              (r & 7) * 16) = v;
+    *reinterpret_cast<uint4*>(xg + (static_cast<size_t>(s) * RG + rg) * 2048 + kg * 128 + r8 * 16) = v;
   }
 }
 
-// out[t][d] = sum_j w[t][j] y[t][j][d] in set order (moe_layer.hpp:148-155)
-__global__ void k_umma_combine(int D, int Dp, int stride, const int32_t* __restrict__ set_len,
-                               const float* __restrict__ w32, const float* __restrict__ y,
-                               float* __restrict__ out) {
-  const int t = blockIdx.x;
+// out[t][d] = sum_j w[t][j] y[t][j][d] in set order (moe_layer.hpp:148-155):
+// a thread per 4 outputs, all slots' y loads in flight before the ordered FMAs
+__global__ void __launch_bounds__(256) k_umma_combine(int D, int Dp, int stride,
+                                                      const int32_t* __restrict__ set_len,
+                                                      const float* __restrict__ w32,
+                                                      const float* __restrict__ y,
+                                                      float* __restrict__ out) {
+  pdl_wait();
+  const int t = blockIdx.y;
+  const int d = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (d >= D) return;
   const int len = set_len[t];
-  for (int d = threadIdx.x; d < D; d += blockDim.x) {
-    float s = 0.0f;
-    for (int j = 0; j < len; ++j)
-      s = fmaf(w32[t * stride + j], y[(static_cast<size_t>(t) * stride + j) * Dp + d], s);
-    out[static_cast<size_t>(t) * D + d] = s;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int j0 = 0; j0 < len; j0 += 8) {
+    float4 v[8];
+    float w[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const bool ok = j0 + j < len;
+      w[j] = ok ? w32[t * stride + j0 + j] : 0.0f;
+      v[j] = ok ? __ldcg(reinterpret_cast<const float4*>(
+                      y + (static_cast<size_t>(t) * stride + j0 + j) * Dp + d))
+                : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j0 + j < len) {
+        s.x = fmaf(w[j], v[j].x, s.x);
+        s.y = fmaf(w[j], v[j].y, s.y);
+        s.z = fmaf(w[j], v[j].z, s.z);
+        s.w = fmaf(w[j], v[j].w, s.w);
+      }
   }
+  *reinterpret_cast<float4*>(out + static_cast<size_t>(t) * D + d) = s;
 }
 
 // Fragment-ordered bf16 expert weights -> CM layout (one 16-byte output
@@ -447,7 +475,10 @@ size_t umma_smem_bytes() {
 
 int ffn_umma_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const FfnBuffers& fb,
                     void* xg, int RG, cudaStream_t s) {
-  k_gather_xg<<<2 * 148, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(fb.x), L->Dp, fb.row_tok,
+  // one 16-byte chunk per thread (all loads in one wave; rows past the plan's
+  // are cut off in-kernel)
+  const int gx = static_cast<int>(std::min<size_t>(65535, (static_cast<size_t>(L->Dp >> 7) * RG * 128 + 255) / 256));
+  k_gather_xg<<<gx, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(fb.x), L->Dp, fb.row_tok,
                                       fb.hdr, RG, static_cast<uint8_t*>(xg));
   OEA_LAUNCHED(ctx);
   UmmaParams P;
@@ -498,9 +529,19 @@ int ffn_umma_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   lc.numAttrs = 1;
   OEA_CUDA_TRY(ctx, cudaLaunchKernelEx(&lc, k_ffn_umma, P));
   OEA_LAUNCHED(ctx);
-  k_umma_combine<<<B, 256, 0, s>>>(L->D, L->Dp, stride, fb.set_len, fb.weights_f32,
-                                   static_cast<const float*>(fb.ybuf), static_cast<float*>(fb.out));
-  OEA_LAUNCHED(ctx);
+  {
+    // (programmatic dependent: launched while the FFN drains, waits for it)
+    cudaLaunchConfig_t cc = {};
+    cc.gridDim = dim3((L->D / 4 + 255) / 256, B);
+    cc.blockDim = dim3(256);
+    cc.stream = s;
+    cc.attrs = at;
+    cc.numAttrs = 1;
+    OEA_CUDA_TRY(ctx, cudaLaunchKernelEx(&cc, k_umma_combine, L->D, L->Dp, stride, fb.set_len,
+                                         static_cast<const float*>(fb.weights_f32),
+                                         static_cast<const float*>(fb.ybuf), static_cast<float*>(fb.out)));
+    OEA_LAUNCHED(ctx);
+  }
   return OEA_OK;
 }
 
