@@ -684,6 +684,11 @@ int oea_ctx_create(int32_t device, oea_ctx_t* out) {
   auto* ctx = new oea_ctx;
   ctx->device = device;
   ctx->num_sms = prop.multiProcessorCount;
+  // (zeroed once; the single-launch route resets it at every launch's end)
+  if (cudaMalloc(&ctx->route_scratch, 1024) == cudaSuccess)
+    cudaMemset(ctx->route_scratch, 0, 1024);
+  else
+    ctx->route_scratch = nullptr;
   e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     delete ctx;
@@ -725,6 +730,7 @@ int oea_ctx_destroy(oea_ctx_t ctx) {
     delete x;
   }
   if (ctx->ffn_trace) cudaFree(ctx->ffn_trace);
+  if (ctx->route_scratch) cudaFree(ctx->route_scratch);
   if (ctx->ep_tables) cudaFree(ctx->ep_tables);
   cudaStreamDestroy(ctx->stream);
   delete ctx;

@@ -19,6 +19,10 @@
 // the reference's order (no FMA contraction is possible: adds and divides only).
 #include <climits>
 
+#ifndef OEA_ROUTE_TPT
+#define OEA_ROUTE_TPT 16
+#endif
+
 #include "oea_device.cuh"
 #include "oea_internal.cuh"
 
@@ -468,6 +472,324 @@ __global__ void __launch_bounds__(kRouteWarps * 32)
   if (seg == nullptr) flush_loads(N, s_loads, loads);
 }
 
+
+// ---------------------------------------------------------------------------
+// Single-launch fast path (same conditions as k_fast_p1/p2, one batch):
+// TPT threads per token, thread q holds experts e = TPT j + q (EPT = 128 /
+// TPT of them). A pick is the best (score desc, index asc) expert ranked
+// after the previous pick: each thread scans its EPT keys (ascending index,
+// so the strict compare keeps the lowest index among equal scores), then
+// log2(TPT) shuffle levels inside the group. Picks come out in rank order,
+// like pick_top, but a pick costs EPT register compares + 4 shuffle levels
+// instead of 5 levels of 64-bit butterflies over the whole warp.
+//   phase 1: the first n_i = min(k0, N) (p == 1: t_i = N, routing.cpp:243-245)
+//            or, vanilla, k picks (route_topk :205-224); base union bitmap.
+//   phase 2 (Oea / Simplified, after a grid barrier): union members ranked
+//            after the base set, in rank order, until the cap
+//            (phase2_piggyback :270-303); weights (renormalize_weights :33-49)
+//            and loads.
+// ---------------------------------------------------------------------------
+
+template <int TPT>
+__device__ __forceinline__ unsigned group_mask() {
+  const int lane = threadIdx.x & 31;
+  return (TPT == 32 ? 0xffffffffu : ((1u << TPT) - 1u)) << (lane & ~(TPT - 1));
+}
+
+// Single-launch route (one batch, grid co-resident: cooperative launch): G1
+// and G2 above as two phases of one kernel, with everything a token needs
+// after the picks kept in registers (its keys and raw scores; each pick's
+// expert and score round robin over the group: pick r in thread r % TPT,
+// slot r / TPT), so the only global round trip is the score load; one grid
+// barrier for the batch union (set_mode 2); the aggregates (fill_aggregates,
+// routing.cpp:17-31) by the last CTA to finish. The union / load / error
+// accumulators live in a self-resetting scratch block (the last CTA clears
+// it), so no memset precedes the launch.
+struct RouteScratch {
+  int32_t loads[128];
+  uint32_t uni[4];
+  int32_t bar;   // CTAs past phase 1
+  int32_t done;  // CTAs finished
+  int32_t err;   // INT_MAX - first degenerate token (0 = none)
+  int32_t pad;
+};
+static_assert(sizeof(RouteScratch) <= 1024, "the context allocates 1 KiB of route scratch");
+
+// m picks (ranked after (pk, pe), eligible by elig_mask) in rank order; pick
+// r lands in thread r % TPT's slot r / TPT (expert, raw score). Returns the
+// number of picks (uniform over the group); (pk, pe) = the last pick.
+// inverse of order_key_f64 (exact but for the sign of a zero score)
+__device__ __forceinline__ double key_to_f64(uint64_t k) {
+  return __longlong_as_double(static_cast<long long>((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+
+template <int TPT, int EPT, int U>
+__device__ __forceinline__ int group_pick_regs(const uint64_t (&k)[EPT], uint32_t elig_mask, int q,
+                                               int m, int at, int (&ex)[U], uint64_t (&sk)[U],
+                                               uint64_t& pk, int& pe) {
+  // (m is uniform over the warp and nothing diverges around the shuffles:
+  // the whole warp takes part, so the full mask, no sub-warp syncs)
+  const unsigned gm = 0xffffffffu;
+  int got = 0;
+#pragma unroll 1
+  for (int r = 0; r < m; ++r) {
+    uint64_t bk = 0ull;
+    int be = 0x7fffffff;
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) {
+      const int e = TPT * j + q;
+      const bool after = k[j] < pk || (k[j] == pk && e > pe);
+      if (((elig_mask >> j) & 1u) && after && k[j] > bk) {
+        bk = k[j];
+        be = e;
+      }
+    }
+#pragma unroll
+    for (int off = 1; off < TPT; off <<= 1) {
+      const uint64_t ok = __shfl_xor_sync(gm, bk, off);
+      const int oe = __shfl_xor_sync(gm, be, off);
+      if (ranks_before(ok, static_cast<uint32_t>(oe), bk, static_cast<uint32_t>(be))) {
+        bk = ok;
+        be = oe;
+      }
+    }
+    if (bk != 0ull) {
+      const int slot = at + got;
+      if (q == slot % TPT) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (u == slot / TPT) {
+            ex[u] = be;
+            sk[u] = bk;
+          }
+      }
+      ++got;
+      pk = bk;
+      pe = be;
+    } else {
+      pk = 0ull;
+      pe = 0x7fffffff;
+    }
+  }
+  return got;
+}
+
+template <int TPT, int kGroupThreads>
+__global__ void __launch_bounds__(kGroupThreads)
+    k_group_route(const Cfg cfg, const int B, const int N, const int set_mode, const int do_weights,
+                  const double* __restrict__ scores, const uint8_t* __restrict__ mask,
+                  int32_t* __restrict__ sets, int32_t* __restrict__ set_len,
+                  int32_t* __restrict__ t_out, int32_t* __restrict__ n_out,
+                  double* __restrict__ weights, float* __restrict__ weights_f32,
+                  RouteScratch* __restrict__ scr, int32_t* __restrict__ loads_out,
+                  int32_t* __restrict__ active_union, int32_t* __restrict__ active_count,
+                  int64_t* __restrict__ total_load, int32_t* __restrict__ base_union,
+                  int32_t* __restrict__ base_count, uint32_t* __restrict__ union_out,
+                  int32_t* __restrict__ err_token, unsigned long long* __restrict__ trace) {
+  constexpr int EPT = 128 / TPT;
+  constexpr int U = 32 / TPT;  // sets of <= 32 (route_fast_ok)
+  auto stamp = [&](int sl) {  // (debug timeline, OEA_FFN_TRACE=1)
+    if (trace != nullptr && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[blockIdx.x * 8 + sl] = t;
+    }
+  };
+  stamp(0);
+  __shared__ int s_loads[128];
+  __shared__ uint32_t s_union[4];
+  __shared__ int s_err;
+  __shared__ bool s_last;
+  for (int e = threadIdx.x; e < 128; e += blockDim.x) s_loads[e] = 0;
+  if (threadIdx.x < 4) s_union[threadIdx.x] = 0u;
+  if (threadIdx.x == 0) s_err = INT_MAX;
+  __syncthreads();
+  const int q = threadIdx.x & (TPT - 1);
+  const int i = blockIdx.x * (kGroupThreads / TPT) + static_cast<int>(threadIdx.x) / TPT;
+  const bool valid = i < B;
+  const bool real = valid && (mask == nullptr || mask[i] != 0);
+  const double* row = scores + static_cast<size_t>(valid ? i : 0) * N;
+  uint64_t k[EPT];
+#pragma unroll
+  for (int j = 0; j < EPT; ++j) {
+    const int e = TPT * j + q;
+    k[j] = real && e < N ? order_key_f64(__ldcg(row + e)) : 0ull;
+  }
+  int ex[U];
+  uint64_t sk[U];  // the picks' keys (the score is recovered from the key)
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    ex[u] = -1;
+    sk[u] = 0ull;
+  }
+  // phase 1: base set (vanilla: the top k)
+  const int want = min(set_mode == 0 ? cfg.k : cfg.k0, N);
+  uint64_t pk = ~0ull;
+  int pe = -1;
+  const int n = group_pick_regs<TPT, EPT, U>(k, 0xffffffffu, q, want, 0, ex, sk, pk, pe);
+  stamp(1);
+  if (valid && set_mode != 0) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (q + TPT * u < n) atomicOr(&s_union[ex[u] >> 5], 1u << (ex[u] & 31));
+  }
+  if (valid && q == 0) {
+    if (t_out) t_out[i] = set_mode == 0 ? 0 : (real ? N : 0);
+    if (n_out) n_out[i] = set_mode == 0 ? 0 : n;
+  }
+  int len = n;
+  if (set_mode == 2) {
+    // the batch union: every CTA's base bits, then a grid barrier
+    __syncthreads();
+    if (threadIdx.x < 4 && s_union[threadIdx.x]) atomicOr(&scr->uni[threadIdx.x], s_union[threadIdx.x]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(&scr->bar, 1);
+      stamp(2);
+      while (ld_acquire_gpu(&scr->bar) < static_cast<int>(gridDim.x)) {
+      }
+    }
+    __syncthreads();
+    stamp(3);
+    // phase 2: union members ranked after the base set, until the cap
+    uint32_t um = 0u;
+    {
+      uint32_t uw[4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) uw[w] = __ldcg(&scr->uni[w]);
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) {
+        const int e = TPT * j + q;
+        if (e < N && ((uw[e >> 5] >> (e & 31)) & 1u)) um |= 1u << j;
+      }
+    }
+    const int m = max(0, cfg.limit - min(cfg.k0, N));
+    const int got = group_pick_regs<TPT, EPT, U>(k, n > 0 ? um : 0u, q, m, n, ex, sk, pk, pe);
+    len = real ? n + min(got, max(0, cfg.limit - n)) : 0;
+  }
+  if (valid) {
+    // the set, its loads and weights (renormalize_weights, routing.cpp:33-49:
+    // sequential fp64 mass in set order, through group shuffles)
+    const int stride = cfg.stride;
+    int32_t* srow = sets + static_cast<size_t>(i) * stride;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int r = q + TPT * u;
+      if (r < len) {
+        srow[r] = ex[u];
+        atomicAdd(&s_loads[ex[u]], 1);
+      }
+    }
+    for (int j = len + q; j < stride; j += TPT) {
+      srow[j] = -1;
+      if (weights) weights[static_cast<size_t>(i) * stride + j] = 0.0;
+      if (weights_f32) weights_f32[static_cast<size_t>(i) * stride + j] = 0.0f;
+    }
+    if (q == 0) set_len[i] = len;
+    if (do_weights && len > 0) {
+      // scores from the keys; a zero key may be a -0.0 score: read it back
+      double sc[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        sc[u] = key_to_f64(sk[u]);
+        if (q + TPT * u < len && sk[u] == 0x8000000000000000ull) sc[u] = __ldcg(row + ex[u]);
+      }
+      const unsigned gm = group_mask<TPT>();
+      double mass = 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int qq = 0; qq < TPT; ++qq) {
+          const double x = __shfl_sync(gm, sc[u], qq, TPT);
+          if (u * TPT + qq < len) mass = __dadd_rn(mass, x);
+        }
+      if (q == 0 && !(mass > 1e-12)) atomicMin(&s_err, i);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int r = q + TPT * u;
+        if (r < len) {
+          const double w = __ddiv_rn(sc[u], mass);
+          if (weights) weights[static_cast<size_t>(i) * stride + r] = w;
+          if (weights_f32) weights_f32[static_cast<size_t>(i) * stride + r] = static_cast<float>(w);
+        }
+      }
+    }
+  }
+  // flush this CTA's loads (and, pruned, its union bits)
+  stamp(4);
+  __syncthreads();
+  for (int e = threadIdx.x; e < N; e += blockDim.x)
+    if (s_loads[e]) atomicAdd(&scr->loads[e], s_loads[e]);
+  if (set_mode == 1 && threadIdx.x < 4 && s_union[threadIdx.x])
+    atomicOr(&scr->uni[threadIdx.x], s_union[threadIdx.x]);
+  if (threadIdx.x == 0 && s_err != INT_MAX) atomicMax(&scr->err, INT_MAX - s_err);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&scr->done, 1) == static_cast<int>(gridDim.x) - 1;
+  }
+  __syncthreads();
+  stamp(5);
+  if (!s_last) return;
+  // the last CTA (one warp: N <= 128): aggregates, exports, and the scratch
+  // reset for the next launch
+  __threadfence();
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  const unsigned below = lanemask_lt();
+  int32_t l[4];
+  uint32_t uw = 0u;
+  long long part = 0;
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const int e = 32 * w + lane;
+    l[w] = e < N ? __ldcg(&scr->loads[e]) : 0;
+    part += l[w];
+    if (e < N && loads_out) loads_out[e] = l[w];
+    scr->loads[e] = 0;
+  }
+  if (lane < 4) {
+    uw = __ldcg(&scr->uni[lane]);
+    if (union_out) union_out[lane] = uw;
+    scr->uni[lane] = 0u;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+  if (lane == 0) {
+    if (total_load) *total_load = part;
+    const int ev = __ldcg(&scr->err);
+    *err_token = ev ? INT_MAX - ev : INT_MAX;
+    scr->err = 0;
+    scr->bar = 0;
+    scr->done = 0;
+  }
+  // active_union (load > 0) and the base union, ascending, by ballots
+  int na = 0, nb = 0;
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const int e = 32 * w + lane;
+    const uint32_t uword = __shfl_sync(0xffffffffu, uw, w);
+    const bool fa = e < N && l[w] > 0, fb = e < N && ((uword >> lane) & 1u);
+    const unsigned ma = __ballot_sync(0xffffffffu, fa), mb = __ballot_sync(0xffffffffu, fb);
+    if (fa && active_union) active_union[na + __popc(ma & below)] = e;
+    if (fb && base_union) base_union[nb + __popc(mb & below)] = e;
+    na += __popc(ma);
+    nb += __popc(mb);
+  }
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const int e = 32 * w + lane;
+    if (e >= na && e < N && active_union) active_union[e] = -1;
+    if (e >= nb && e < N && base_union) base_union[e] = -1;
+  }
+  if (lane == 0) {
+    if (active_count) *active_count = na;
+    if (base_count) *base_count = nb;
+  }
+  stamp(6);
+}
+
 }  // namespace oea_dev
 
 namespace oea_host {
@@ -571,12 +893,45 @@ bool route_fast_ok(const Cfg& cfg, int N, bool need_order) {
 int route_f64_fast_launch(oea_ctx* ctx, const Cfg& cfg, int B, int N, const RouteBuffers& rb,
                           int set_mode, cudaStream_t s, int R, const int32_t* seg) {
   const int words = ((N + 31) / 32) * R;
+  const int32_t* sg = R > 1 ? seg : nullptr;
+  cudaError_t e;
+  static const int fused = getenv("OEA_ROUTE_FUSED") ? atoi(getenv("OEA_ROUTE_FUSED")) : 1;
+  if (fused && R == 1 && N <= 128 && ctx->route_scratch != nullptr) {
+    // one cooperative launch (phase 1, grid barrier, phase 2, aggregates)
+    constexpr int TPT = OEA_ROUTE_TPT, BT = 256;
+    const int grid = (B + BT / TPT - 1) / (BT / TPT);
+    static int max_blocks = -1;
+    if (max_blocks < 0) {
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_group_route<TPT, BT>, BT, 0);
+      max_blocks = per_sm * ctx->num_sms;
+    }
+    if (grid <= max_blocks) {
+      const int do_weights = (rb.weights != nullptr || rb.weights_f32 != nullptr) ? 1 : 0;
+      cudaLaunchConfig_t c = {};
+      c.gridDim = dim3(grid);
+      c.blockDim = dim3(BT);
+      c.stream = s;
+      cudaLaunchAttribute a[1];
+      a[0].id = cudaLaunchAttributeCooperative;
+      a[0].val.cooperative = 1;
+      c.attrs = a;
+      c.numAttrs = 1;
+      OEA_CUDA_TRY(ctx, cudaLaunchKernelEx(&c, k_group_route<TPT, BT>, cfg, B, N, set_mode, do_weights,
+                                           rb.scores, rb.mask, rb.sets, rb.set_len, rb.t, rb.n,
+                                           rb.weights, rb.weights_f32,
+                                           static_cast<RouteScratch*>(ctx->route_scratch), rb.loads,
+                                           rb.active_union, rb.active_count, rb.total_load,
+                                           rb.base_union, rb.base_union_count, rb.union_bits,
+                                           rb.err_token, ctx->ffn_trace));
+      OEA_LAUNCHED(ctx);
+      return OEA_OK;
+    }
+  }
   OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.union_bits, 0, words * 4, s));
   OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.loads, 0, sizeof(int32_t) * N * R, s));
   OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.err_token, 0x7f, sizeof(int32_t), s));
   const int do_weights = (rb.weights != nullptr || rb.weights_f32 != nullptr) ? 1 : 0;
-  const int32_t* sg = R > 1 ? seg : nullptr;
-  cudaError_t e;
   if (N <= 32)
     e = launch_fast<1>(cfg, B, N, rb, set_mode, do_weights, sg, s);
   else if (N <= 64)
