@@ -193,7 +193,14 @@ class PeerExpertParallelMoE:
     owner's arrival counter; the owner then sums the `world` slots in rank
     order (oea_ep_combine). Buffers come from oea_device_alloc and are mapped
     into the other ranks with CUDA IPC (`connect`), or, for a single-process
-    emulation of the group on one GPU, shared directly (`emulate_group`)."""
+    emulation of the group on one GPU, shared directly (`emulate_group`).
+
+    Reuse contract: each owner has ONE receive buffer, so a rank must not
+    start its next `partial` before every owner's `combine` of the current
+    launch has read it. The per-layer token all-gather that produces the next
+    x_all (a collective over the group) orders this in the decode stack; a
+    caller that replays partial / combine back to back without such a
+    collective must put a group barrier between launches."""
 
     def __init__(self, layer, cfg, world: int, rank: int, B: int):
         import ctypes as C
