@@ -571,8 +571,7 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
     // tcgen05 (UMMA + TMEM) grouped FFN; the layer's UMMA-layout weight copy
     // is made (or refreshed in place) on first use
     if (L->w1u == nullptr || L->umma_stale) {
-      if (L->w1u != nullptr) oea_host::layer_drop_umma(L);  // (not capturing: checked)
-      r = oea_host::layer_prepare_umma(ctx, L, s);
+      r = oea_host::layer_prepare_umma(ctx, L, s);  // (not capturing: umma_ok checked)
       if (r) return r;
       L->umma_stale = 0;
     }

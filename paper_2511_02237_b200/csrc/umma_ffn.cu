@@ -447,12 +447,15 @@ namespace oea_host {
 
 using namespace oea_dev;
 
+// Makes the UMMA-layout copy (first use) or refreshes it IN PLACE (the
+// weights changed): graphs captured with its pointers stay valid.
 int layer_prepare_umma(oea_ctx* ctx, oea_layer* L, cudaStream_t s) {
-  if (L->w1u != nullptr) return OEA_OK;
-  const size_t b1 = static_cast<size_t>(2 * L->Hp) * L->Dp * 2 * L->n_local;
-  const size_t b2 = static_cast<size_t>(L->Dp) * L->Hp * 2 * L->n_local;
-  OEA_CUDA_TRY(ctx, cudaMalloc(&L->w1u, b1));
-  OEA_CUDA_TRY(ctx, cudaMalloc(&L->w2u, b2));
+  if (L->w1u == nullptr) {
+    const size_t b1 = static_cast<size_t>(2 * L->Hp) * L->Dp * 2 * L->n_local;
+    const size_t b2 = static_cast<size_t>(L->Dp) * L->Hp * 2 * L->n_local;
+    OEA_CUDA_TRY(ctx, cudaMalloc(&L->w1u, b1));
+    OEA_CUDA_TRY(ctx, cudaMalloc(&L->w2u, b2));
+  }
   k_repack_cm<1><<<4 * 148, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(L->w1), L->n_local,
                                           L->Dp, L->Hp, static_cast<__nv_bfloat16*>(L->w1u));
   OEA_LAUNCHED(ctx);
