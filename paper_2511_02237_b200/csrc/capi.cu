@@ -1389,8 +1389,10 @@ int oea_ep_combine(oea_ctx_t ctx, const float* recv_local, int32_t* cnt_local, i
                                         cudaMemcpyDeviceToDevice, s));
     return OEA_OK;
   }
-  return oea_host::ep_sum_launch(ctx, recv_local, cnt_local, world * ctx->num_sms, world,
-                                 tokens_per_rank * D, out_local, s);
+  if (D % 4 != 0) return fail(ctx, OEA_ERR_INVALID_ARGUMENT, "ep_combine: D must be a multiple of 4");
+  // every rank's shard decode adds the float4 quads it wrote for this owner
+  return oea_host::ep_sum_launch(ctx, recv_local, cnt_local, world * tokens_per_rank * (D / 4),
+                                 world, tokens_per_rank * D, out_local, s);
 }
 
 // Zero-filled device allocation of its own (IPC handles of a cudaMalloc base

@@ -1823,19 +1823,53 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
       }
     }
   } else {
+    // Expert-parallel combine: token t's partial goes to its owner's receive
+    // buffer (peer memory), slot [rank][t - owner * tpr], 4 outputs per store
+    // (16-byte NVLink writes; D % 4 == 0 on this path) over the CTA's slice
+    // of whole float4 quads; then the CTA adds the number of quads it wrote
+    // for each owner whose tokens its slice touched (an owner expects
+    // world x tpr x D / 4 per launch, whatever the grid)
     const EpPeers* ep = P.ep;
     const int tpr = ep->tpr, rank = ep->rank;
-    combine([&](int64_t f, float v) {
+    const int64_t Q = BD >> 2;  // float4 quads
+    const int64_t q0 = Q * blockIdx.x / gridDim.x, q1 = Q * (blockIdx.x + 1) / gridDim.x;
+    for (int64_t qd = q0 + threadIdx.x; qd < q1; qd += kComb) {
+      const int64_t f = qd << 2;
       const int t = static_cast<int>(f / P.D), d = static_cast<int>(f % P.D);
+      const int len = PR->set_len[t];
+      float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int j = 0; j < len; ++j) {
+        const int o = t * P.stride + j;
+        if (eslot[ssets[o]] < 0) continue;  // (an expert this shard does not hold)
+        const float w = PR->wts[o];
+        float4 y = __ldcg(reinterpret_cast<const float4*>(P.ybuf + static_cast<size_t>(o) * P.Dp + d));
+        for (int kp = 1; kp < w2ks; ++kp) {
+          const float4 yk = __ldcg(reinterpret_cast<const float4*>(
+              P.ybuf + (static_cast<size_t>(kp) * P.B * P.stride + o) * P.Dp + d));
+          y.x += yk.x;
+          y.y += yk.y;
+          y.z += yk.z;
+          y.w += yk.w;
+        }
+        sum.x = fmaf(w, y.x, sum.x);
+        sum.y = fmaf(w, y.y, sum.y);
+        sum.z = fmaf(w, y.z, sum.z);
+        sum.w = fmaf(w, y.w, sum.w);
+      }
       const int owner = t / tpr;
-      ep->recv[owner][(static_cast<size_t>(rank) * tpr + (t - owner * tpr)) * P.D + d] = v;
-    });
+      *reinterpret_cast<float4*>(
+          ep->recv[owner] + (static_cast<size_t>(rank) * tpr + (t - owner * tpr)) * P.D + d) = sum;
+    }
     // this CTA's remote stores are issued (all combining threads), made
-    // visible system-wide, then counted at every owner (sum in k_ep_sum)
+    // visible system-wide, then counted at the owners its slice covers
     asm volatile("bar.sync 2, %0;" ::"r"(kComb) : "memory");
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && q1 > q0) {
       __threadfence_system();
-      for (int o = 0; o < ep->world; ++o) atomicAdd_system(ep->cnt[o], 1);
+      const int64_t qpo = static_cast<int64_t>(tpr) * P.D / 4;  // quads per owner
+      for (int o = static_cast<int>(q0 / qpo); o <= static_cast<int>((q1 - 1) / qpo); ++o) {
+        const int64_t n = min(q1, (o + 1) * qpo) - max(q0, o * qpo);
+        atomicAdd_system(ep->cnt[o], static_cast<int>(n));
+      }
     }
   }
   if (threadIdx.x == 0) stamp(P, 15);
