@@ -475,6 +475,17 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
                            oea_host::ffn_route_smem_bytes(B, L->Np, stride) <= 227 * 1024;
   if (x_mapped && !fused) return kNotFused;  // the caller stages x itself
   int r = OEA_OK;
+  // large batches: the tcgen05 FFN (its weight copy made / refreshed here,
+  // outside any capture), and the compaction (+ its token-row gather) inside
+  // the route-only launch (OEA_BIG_COMPACT=0: the separate k_compact)
+  const bool use_umma = big && umma_ok(ctx, L, s);
+  if (use_umma && (L->w1u == nullptr || L->umma_stale)) {
+    r = oea_host::layer_prepare_umma(ctx, L, s);
+    if (r) return r;
+    L->umma_stale = 0;
+  }
+  static const bool big_compact = getenv("OEA_BIG_COMPACT") == nullptr || atoi(getenv("OEA_BIG_COMPACT")) != 0;
+  const int xg_rg = static_cast<int>((w.R + 16) / 8);
   if (rb.trace && !fused) OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.trace, 0, 8 * 8 * 1024, s));
   if (big) {
     oea_host::FfnBuffers rf;
@@ -504,14 +515,24 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
     rf.x_base_union_count = w.base_union_count;
     rf.x_hdr = w.hdr;
     rf.trace = ctx->ffn_trace;
+    rf.row_tok = w.row_tok;
+    rf.row_slot = w.row_slot;
+    rf.group_a = w.group_a;
+    rf.group_row0 = w.group_row0;
+    rf.group_rows = w.group_rows;
+    rf.compact_in_kernel = big_compact ? 1 : 0;
+    rf.xg = big_compact && use_umma ? w.xg : nullptr;
+    rf.xg_rg = xg_rg;
     r = oea_host::ffn_bf16_launch(ctx, L, B, stride, rf, false, s);
     if (r) return r;
-    oea_host::CompactBuffers cb{w.sets, w.set_len, w.row_tok, w.row_slot, w.group_a,
-                                w.group_row0, w.group_rows, w.hdr, w.counters, w.G + 7, w.loads,
-                                w.total_load};
-    r = oea_host::compact_launch(ctx, B, L->N, stride, cb, w.tokbits, w.active_union,
-                                 w.active_count, s);
-    if (r) return r;
+    if (!big_compact) {
+      oea_host::CompactBuffers cb{w.sets, w.set_len, w.row_tok, w.row_slot, w.group_a,
+                                  w.group_row0, w.group_rows, w.hdr, w.counters, w.G + 7,
+                                  w.loads, w.total_load};
+      r = oea_host::compact_launch(ctx, B, L->N, stride, cb, w.tokbits, w.active_union,
+                                   w.active_count, s);
+      if (r) return r;
+    }
   } else if (part != 2 && !fused) {
     r = oea_host::router_fused_launch(ctx, L, cfg, B, rb, s);
     if (r || part == 1) return r;
@@ -567,16 +588,8 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
     fb.x_base_union_count = w.base_union_count;
     fb.x_hdr = w.hdr;
   }
-  if (big && umma_ok(ctx, L, s)) {
-    // tcgen05 (UMMA + TMEM) grouped FFN; the layer's UMMA-layout weight copy
-    // is made (or refreshed in place) on first use
-    if (L->w1u == nullptr || L->umma_stale) {
-      r = oea_host::layer_prepare_umma(ctx, L, s);  // (not capturing: umma_ok checked)
-      if (r) return r;
-      L->umma_stale = 0;
-    }
-    return oea_host::ffn_umma_launch(ctx, L, B, stride, fb, w.xg, static_cast<int>((w.R + 16) / 8), s);
-  }
+  if (use_umma)  // tcgen05 (UMMA + TMEM) grouped FFN
+    return oea_host::ffn_umma_launch(ctx, L, B, stride, fb, w.xg, xg_rg, s, big_compact);
   return oea_host::ffn_bf16_launch(ctx, L, B, stride, fb, part == 0 && !fused && !big, s);
 }
 

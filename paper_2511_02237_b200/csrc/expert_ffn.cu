@@ -117,6 +117,12 @@ struct FfnParams {
   // slot [rank][t - owner * tpr], then every CTA bumps every owner's counter.
   // (Last member: the offsets of the hot fields stay as they were.)
   const EpPeers* ep;  // null: local combine into out
+  // Route-only launch (B > 64): the compaction in the same launch (CTA e
+  // builds expert e's token groups; route_compact_dist) and, for the tcgen05
+  // FFN, the token rows gathered into the CM layout (xg, xg_rg row groups)
+  int compact_in_kernel;
+  uint8_t* xg;
+  int xg_rg;
 };
 
 // The compacted plan's tables (global from the router kernel, or this CTA's
@@ -1260,6 +1266,156 @@ __device__ __forceinline__ void route_phase2_plan(const FfnParams& P, uint8_t* r
   compact_smem<NW>(P, rs, L, T, blockIdx.x == 0);
 }
 
+// Route-only launch (64 < B <= 256): the compaction of k_compact
+// (router_fused.cu compact_plan) distributed over the grid in the same
+// launch. Once every token's plan row is out (claims[0] = B), CTA e takes
+// expert e: its tokens in token order (a ballot scan of the batch's sets) and
+// its load, published in x_loads (claims[1] counts the experts); then each
+// CTA places its expert's token groups (<= 64 rows, the last padded to 8) and
+// rows after the groups / rows of the experts before it (ascending experts =
+// the active-union order), writes row -> (token, slot) and, for the tcgen05
+// FFN, the token rows in the CM layout (xg). CTA 0 writes the header and the
+// total load.
+__device__ __forceinline__ void route_compact_dist(const FfnParams& P, uint8_t* rs,
+                                                   const RouteSmem& L, int* claims) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NT = kFfnThreads, NWARP = kFfnThreads / 32;
+  const int B = P.B, N = P.N, stride = P.cfg.stride;
+  int* tl_tok = reinterpret_cast<int*>(rs + L.rtok);   // [<= B] this expert's tokens
+  int* tl_slot = reinterpret_cast<int*>(rs + L.rslot);
+  int* wcnt = reinterpret_cast<int*>(rs + L.red);      // [NWARP]
+  int* misc = reinterpret_cast<int*>(rs + L.misc);
+  if (tid == 0)
+    while (ld_acquire_gpu(claims) < B) __nanosleep(32);
+  __syncthreads();
+  const int e = blockIdx.x;
+  int load = 0;
+  if (e < N) {
+#pragma unroll 1
+    for (int t0 = 0; t0 < B; t0 += NT) {
+      const int t = t0 + tid;
+      // (the exported rows are -1 past the set length: the whole row's loads
+      // go out at once, no length round trip, no early exit)
+      int slot = -1;
+      if (t < B) {
+        const int32_t* row = P.x_sets + static_cast<size_t>(t) * stride;
+#pragma unroll 8
+        for (int j = 0; j < stride; ++j)
+          if (__ldcg(row + j) == e && slot < 0) slot = j;
+      }
+      const unsigned m = __ballot_sync(kFull, slot >= 0);
+      if (lane == 0) wcnt[warp] = __popc(m);
+      __syncthreads();
+      int before = load, tot = 0;
+#pragma unroll
+      for (int w = 0; w < NWARP; ++w) {
+        before += w < warp ? wcnt[w] : 0;
+        tot += wcnt[w];
+      }
+      if (slot >= 0) {
+        const int pos = before + __popc(m & lanemask_lt());
+        tl_tok[pos] = t;
+        tl_slot[pos] = slot;
+      }
+      __syncthreads();
+      load += tot;
+    }
+    if (tid == 0) {
+      P.x_loads[e] = load;
+      red_release_gpu_add(claims + 1, 1);  // (after the barrier: cumulative)
+    }
+  }
+  if (tid == 0)
+    while (ld_acquire_gpu(claims + 1) < N) __nanosleep(32);
+  __syncthreads();
+  // groups / rows of the experts before e (k_compact's formulas)
+  if (warp == 0) {
+    int gb = 0, rb = 0, ng_all = 0, nr_all = 0, act = 0, tl = 0;
+    for (int i = lane; i < N; i += 32) {
+      const int m = __ldcg(P.x_loads + i);
+      const int ng = (m + kTokGroup - 1) / kTokGroup;
+      const int nr = m > 0 ? (m / kTokGroup) * kTokGroup + ((m % kTokGroup) + 7) / 8 * 8 : 0;
+      if (i < e) {
+        gb += ng;
+        rb += nr;
+      }
+      ng_all += ng;
+      nr_all += nr;
+      act += m > 0;
+      tl += m;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      gb += __shfl_xor_sync(kFull, gb, off);
+      rb += __shfl_xor_sync(kFull, rb, off);
+      ng_all += __shfl_xor_sync(kFull, ng_all, off);
+      nr_all += __shfl_xor_sync(kFull, nr_all, off);
+      act += __shfl_xor_sync(kFull, act, off);
+      tl += __shfl_xor_sync(kFull, tl, off);
+    }
+    if (lane == 0) {
+      misc[2] = gb;
+      misc[3] = rb;
+      if (blockIdx.x == 0) {
+        P.x_hdr->n_groups = ng_all;
+        P.x_hdr->T = act;
+        P.x_hdr->total_load = tl;
+        P.x_hdr->n_rows = nr_all;
+        *P.x_total_load = tl;
+      }
+    }
+  }
+  __syncthreads();
+  if (e < N && load > 0) {
+    const int gb = misc[2], rb = misc[3];
+    const int ng = (load + kTokGroup - 1) / kTokGroup;
+    const int nr = (load / kTokGroup) * kTokGroup + ((load % kTokGroup) + 7) / 8 * 8;
+    int32_t* ga = const_cast<int32_t*>(P.group_a);
+    int32_t* g0 = const_cast<int32_t*>(P.group_row0);
+    int32_t* gr = const_cast<int32_t*>(P.group_rows);
+    int32_t* rt = const_cast<int32_t*>(P.row_tok);
+    int32_t* rsl = const_cast<int32_t*>(P.row_slot);
+    for (int k = tid; k < ng; k += NT) {
+      ga[gb + k] = e;
+      g0[gb + k] = rb + k * kTokGroup;
+      gr[gb + k] = min(kTokGroup, load - k * kTokGroup);
+    }
+    for (int i = tid; i < nr; i += NT) {
+      rt[rb + i] = i < load ? tl_tok[i] : -1;
+      rsl[rb + i] = i < load ? tl_slot[i] : 0;
+    }
+    if (P.xg != nullptr) {
+      // token rows -> xg (CM: [Dp/128 slices][row groups] x 2 KiB, 16-byte
+      // chunk (kg, row % 8) at kg * 128 + (row % 8) * 16), rows past the
+      // expert's tokens zero
+      const int nch = P.Dp >> 3, total = nr * nch;
+      constexpr int kU = 8;  // a thread's chunks: all loads in flight, then the stores
+#pragma unroll 1
+      for (int i0 = tid; i0 < total; i0 += NT * kU) {
+        uint4 v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int idx = i0 + u * NT;
+          const int i = idx / nch, ch = idx - i * nch;
+          const int t = idx < total && i < load ? tl_tok[i] : -1;
+          v[u] = t >= 0 ? __ldg(reinterpret_cast<const uint4*>(P.x_in + static_cast<size_t>(t) * P.Dp +
+                                                              ch * 8))
+                        : make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int idx = i0 + u * NT;
+          if (idx < total) {
+            const int i = idx / nch, ch = idx - i * nch, r = rb + i;
+            *reinterpret_cast<uint4*>(P.xg + (static_cast<size_t>(ch >> 4) * P.xg_rg + (r >> 3)) * 2048 +
+                                      (ch & 15) * 128 + (r & 7) * 16) = v[u];
+          }
+        }
+      }
+    }
+  }
+}
+
 // The last CTA to leave resets the grid's counters (round claims, combine /
 // logits barriers, per-group W1 release counters), so the next launch (fused
 // or two-kernel, graph-captured or not) starts from zero. Called by thread 0
@@ -1412,8 +1568,17 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
     }
     if (kRouteOnly) {
       // plan rows (CTA t: token t, t + grid, ...); the FFN tables and the
-      // aggregates (loads, header) follow from k_compact.
+      // aggregates (loads, header) follow: in this launch (route_compact_dist)
+      // or from k_compact.
       if (warp < kFfnWarps) route_phase2_plan<kFfnWarps>(P, rs, RL, T, tag, false);
+      if (P.compact_in_kernel) {
+        __syncthreads();  // (this CTA's rows are out: cumulative release below)
+        if (threadIdx.x == 0 && static_cast<int>(blockIdx.x) < P.B)
+          red_release_gpu_add(claims, (P.B - 1 - static_cast<int>(blockIdx.x)) /
+                                          static_cast<int>(gridDim.x) + 1);
+        route_compact_dist(P, rs, RL, claims);
+        __syncthreads();
+      }
       if (threadIdx.x == 0) {
         stamp(P, 7);
         grid_exit(P, claims, 0);
@@ -2092,6 +2257,9 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
     static const int ks = getenv("OEA_W2_KSPLIT") ? atoi(getenv("OEA_W2_KSPLIT")) : kW2KSplit;
     P.w2_ks = std::max(1, std::min(ks, kW2KSplitMax));
   }
+  P.compact_in_kernel = fb.compact_in_kernel;
+  P.xg = static_cast<uint8_t*>(fb.xg);
+  P.xg_rg = fb.xg_rg;
   P.e_begin = L->e_begin;
   P.e_count = L->n_local;
   P.router_t = static_cast<const uint4*>(L->router_t);

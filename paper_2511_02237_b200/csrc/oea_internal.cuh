@@ -251,6 +251,9 @@ struct FfnBuffers {
   int x_stage = 0;                      // x_in is mapped host memory (staged in-kernel)
   int* done_flag = nullptr;             // mapped host flag set to 1 when out is on the host
   const oea_dev::EpPeers* ep = nullptr;  // peer-memory EP combine (device table), or null
+  int compact_in_kernel = 0;            // route-only: the compaction in the same launch
+  void* xg = nullptr;                   // ... and the tcgen05 FFN's gathered rows (or null)
+  int xg_rg = 0;
   float* logits = nullptr;              // [B][Np]
   unsigned long long* xlog = nullptr;   // tagged exchange words (fused path)
   unsigned long long* xuni = nullptr;
@@ -284,7 +287,7 @@ size_t ffn_dense_xs_bytes(int Dp);
 int layer_prepare_umma(oea_ctx* ctx, oea_layer* L, cudaStream_t s);
 void layer_drop_umma(oea_layer* L);
 int ffn_umma_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const FfnBuffers& fb,
-                    void* xg, int RG, cudaStream_t s);
+                    void* xg, int RG, cudaStream_t s, bool gathered = false);
 int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride,
                     const FfnBuffers& fb, bool pdl, cudaStream_t s);
 int ffn_simt_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride,

@@ -477,13 +477,16 @@ size_t umma_smem_bytes() {
 }
 
 int ffn_umma_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const FfnBuffers& fb,
-                    void* xg, int RG, cudaStream_t s) {
+                    void* xg, int RG, cudaStream_t s, bool gathered) {
   // one 16-byte chunk per thread (all loads in one wave; rows past the plan's
   // are cut off in-kernel)
-  const int gx = static_cast<int>(std::min<size_t>(65535, (static_cast<size_t>(L->Dp >> 7) * RG * 128 + 255) / 256));
-  k_gather_xg<<<gx, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(fb.x), L->Dp, fb.row_tok,
-                                      fb.hdr, RG, static_cast<uint8_t*>(xg));
-  OEA_LAUNCHED(ctx);
+  // (gathered: the route-only launch already wrote xg with the compaction)
+  if (!gathered) {
+    const int gx = static_cast<int>(std::min<size_t>(65535, (static_cast<size_t>(L->Dp >> 7) * RG * 128 + 255) / 256));
+    k_gather_xg<<<gx, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(fb.x), L->Dp, fb.row_tok,
+                                   fb.hdr, RG, static_cast<uint8_t*>(xg));
+    OEA_LAUNCHED(ctx);
+  }
   UmmaParams P;
   P.w1u = static_cast<const uint8_t*>(L->w1u);
   P.w2u = static_cast<const uint8_t*>(L->w2u);
