@@ -461,18 +461,24 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
   // (The fused prologue is kept small — it runs cold once per launch — so it
   // covers N <= 128, p == 1 and D % 8 == 0; other shapes/configs use the pair.)
   const bool shard = L->n_local < L->N;
-  const bool fused = part == 0 && fused_ok(L, B, rc) &&
-                     (shard || getenv("OEA_TWO_KERNEL") == nullptr);
-  // Large batches (64 < B <= 256) with the rank-routing conditions: a
-  // route-only launch of the fused prologue (tensor-core gate GEMV, rank
-  // routing, union, plan rows), the compaction, then the FFN (three launches
-  // instead of the single-cluster router kernel).
-  const bool big = part == 0 && !fused && !shard && B > kRouterTokChunk && B <= kMaxFusedB &&
-                   L->router_t != nullptr && L->Np <= 128 && L->D == L->Dp &&
-                   (rc.mode == OEA_MODE_VANILLA || (rc.p == 1.0 && rc.max_p >= L->N)) &&
-                   getenv("OEA_TWO_KERNEL") == nullptr &&
-                   oea_host::ffn_bf16_smem_bytes() +
-                           oea_host::ffn_route_smem_bytes(B, L->Np, stride) <= 227 * 1024;
+  // Large batches (B > 64, and from OEA_BIG_MIN = 32 when the tcgen05 FFN is
+  // available for the layer: measured faster than the fused token-list
+  // launch from ~B = 32, e.g. B = 64 194 -> 172 us) with the rank-routing
+  // conditions: a route-only launch of the fused prologue (tensor-core gate
+  // GEMV, rank routing, union, plan rows, compaction), then the FFN.
+  static const int big_min = getenv("OEA_BIG_MIN") ? atoi(getenv("OEA_BIG_MIN")) : 32;
+  const bool fused_cand = part == 0 && fused_ok(L, B, rc) &&
+                          (shard || getenv("OEA_TWO_KERNEL") == nullptr);
+  const bool big_shape = part == 0 && !shard && B > 16 && B <= kMaxFusedB &&
+                         L->router_t != nullptr && L->Np <= 128 && L->D == L->Dp &&
+                         (rc.mode == OEA_MODE_VANILLA || (rc.p == 1.0 && rc.max_p >= L->N)) &&
+                         getenv("OEA_TWO_KERNEL") == nullptr &&
+                         oea_host::ffn_bf16_smem_bytes() +
+                                 oea_host::ffn_route_smem_bytes(B, L->Np, stride) <= 227 * 1024;
+  const bool big = big_shape && (B > kRouterTokChunk
+                                     ? !fused_cand
+                                     : B >= big_min && !x_mapped && umma_ok(ctx, L, s));
+  const bool fused = fused_cand && !big;
   if (x_mapped && !fused) return kNotFused;  // the caller stages x itself
   int r = OEA_OK;
   // large batches: the tcgen05 FFN (its weight copy made / refreshed here,

@@ -40,7 +40,13 @@ def test_shards_sum_to_unsharded(oea, D, H, N, B, P):
         for key in ("sets", "set_len", "active_union", "loads"):
             assert np.array_equal(plan[key], wplan[key]), key
         assert plan["active_count"] == wplan["active_count"]
-        assert np.array_equal(plan["weights"], wplan["weights"])
+        if B < 32:
+            assert np.array_equal(plan["weights"], wplan["weights"])
+        else:
+            # one GPU takes the large-batch path from B = 32 (tensor-core gate
+            # GEMV, another fp32 accumulation order than a shard's fused GEMV):
+            # same sets, weights equal to fp32 rounding
+            assert np.abs(plan["weights"] - wplan["weights"]).max() <= 1e-6
         total += part
         sh.close()
     # fp32 partial mixtures; a shard holding few experts takes split rounds

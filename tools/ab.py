@@ -25,14 +25,13 @@ ctx = layers[0].ctx
 stream = torch.cuda.ExternalStream(ctx.stream)
 res = []
 SETS = {"small": ((16, 1), (16, 2), (16, 4), (16, 8), (4, 4), (1, 4)),
-        "big": ((128, 4), (128, 8), (256, 4), (256, 8))}
+        "big": ((128, 4), (128, 8), (256, 4), (256, 8)),
+        "mid": ((24, 4), (32, 4), (32, 8), (48, 4), (64, 4), (64, 8))}
 for B, k0 in SETS[os.environ.get("AB_SET", "small")]:
     gen = torch.Generator(device="cuda").manual_seed(1234)
     xs = torch.randn(W + K, B, D, device="cuda", generator=gen).to(torch.bfloat16)
     out = torch.empty(B, D, device="cuda", dtype=torch.float32)
     cfg = oea.RoutingConfig.simplified(k0, 8) if k0 < 8 else oea.RoutingConfig.vanilla(8)
-    for L in layers:  # eager first call: the tcgen05 path's weight copy (B > 64)
-        L.decode(xs[0], cfg, out)
     us, _ = bench.time_chain(torch, stream, layers, xs, cfg, out, W, K, ctx)
     Ts, _ = bench.plan_stats(layers, xs, cfg, out, B, range(W, W + K), ctx)
     res.append(f"B{B}k{k0}: {us:6.2f}us T={np.mean(Ts):5.1f}")
