@@ -490,7 +490,7 @@ def c2_b16_extra(torch, stream, layers, W, K, peak):
 
 def c2_large_extra(torch, stream, layers, W, K, peak):
     """C2 (BASELINE configs[1]) large batches on the C1 layers: B = 32..256
-    (B > 64: route-only prologue + compaction + the tcgen05 (UMMA/TMEM)
+    (B >= 32: route-only prologue + compaction + the tcgen05 (UMMA/TMEM)
     grouped FFN), OEA simplified(4, 8) and top-8: µs, T, fraction of the
     measured HBM peak for the active experts' bytes."""
     import numpy as np
@@ -509,7 +509,7 @@ def c2_large_extra(torch, stream, layers, W, K, peak):
             lb = layer_bytes(T, D, H, N, Bs)
             pts.append({"B": Bs, "routing": name, "us": us, "T_mean": T,
                         "frac": lb / us / 1e3 / peak, "kernels_per_call": launched / K,
-                        "ffn": "tcgen05 (UMMA + TMEM)" if Bs > 64 else "fused mma.sync"})
+                        "ffn": "tcgen05 (UMMA + TMEM)" if Bs >= 32 else "fused mma.sync"})
     return {"steps_per_point": K, "points": pts}
 
 
@@ -1058,7 +1058,7 @@ def bench_c2(args, env):
     for Bs in (1, 4, 8, 16, 32, 64, 128, 256):
         xs = torch.randn(W + K, Bs, D, device="cuda", generator=gen).to(torch.bfloat16)
         out = torch.empty(Bs, D, device="cuda", dtype=torch.float32)
-        if Bs > 64:  # eager first call: the tcgen05 FFN's weight copy (see time_chain)
+        if Bs >= 32:  # eager first call: the tcgen05 FFN's weight copy (see time_chain)
             for L in layers:
                 L.decode(xs[0], oea.RoutingConfig.simplified(1, K_TOP), out)
         for k0 in range(1, K_TOP + 1):
