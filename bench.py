@@ -657,22 +657,27 @@ def bench_c1(args, env):
                 "vanilla_frac": v["GBps"] / peak}
 
     # ---- e2e through the C ABI from pinned host buffers ----
-    # A serving loop's shape: each step's tokens (host memory) are written
-    # into one pinned staging buffer (the CPU copy is inside the timed
-    # region), the decode reads it over the host link and writes out to a
-    # pinned buffer, and the call returns when out is on the host. Timed from
-    # C (lib/e2e_host, tools/e2e_host.c: oea_moe_decode_host, no Python in
-    # the loop) and, for comparison, through the Python API (ctypes).
+    # End to end through the C ABI, timed from C (lib/e2e_host,
+    # tools/e2e_host.c: oea_moe_decode_host, no Python in the loop): every
+    # step's tokens sit in pinned host memory (a distinct slice per step), the
+    # decode reads that step's slice over the host link (the H2D transfer, in
+    # the timed step) and writes out to a pinned buffer, and the call returns
+    # when out is on the host. Also measured: the same with a CPU copy of the
+    # tokens from pageable memory into one pinned staging buffer per step
+    # (mode 0), and through the Python API (ctypes).
     import ctypes
-    e2e_c = None
-    exe = os.path.join(ROOT, "paper_2511_02237_b200", "lib", "e2e_host")
-    try:
-        r = subprocess.run([exe, str(D), str(H), str(N), str(B), str(K0), str(max(K, 100)), str(W),
-                            str(ROTATE)], capture_output=True, text=True, timeout=300,
-                           env=dict(os.environ, CUDA_VISIBLE_DEVICES=str(local)))
-        e2e_c = json.loads(r.stdout.strip().splitlines()[-1])
-    except Exception as e:  # reported, the Python loop below still measures e2e
-        e2e_c = {"error": f"{type(e).__name__}: {e}"}
+
+    def e2e_run(mode):
+        exe = os.path.join(ROOT, "paper_2511_02237_b200", "lib", "e2e_host")
+        try:
+            r = subprocess.run([exe, str(D), str(H), str(N), str(B), str(K0), str(max(K, 100)), str(W),
+                                str(ROTATE), str(mode)], capture_output=True, text=True, timeout=300,
+                               env=dict(os.environ, CUDA_VISIBLE_DEVICES=str(local)))
+            return json.loads(r.stdout.strip().splitlines()[-1])
+        except Exception as e:  # reported, the Python loop below still measures e2e
+            return {"error": f"{type(e).__name__}: {e}"}
+    e2e_c = e2e_run(3)
+    e2e_c_staged = e2e_run(0)
     x_src = xs.cpu().contiguous()          # the steps' inputs, host memory
     x_stage = torch.empty(B, D, dtype=torch.bfloat16).pin_memory()
     out_host = torch.empty(B, D, dtype=torch.float32).pin_memory()
@@ -734,11 +739,13 @@ def bench_c1(args, env):
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_us, "unit": "us/layer-call", "h2d_bytes_per_step": B * D * 2,
                 "d2h_bytes_per_step": B * D * 4,
-                "how": "C caller (lib/e2e_host) of oea_moe_decode_host: per step the host copy "
-                       "of the tokens into a pinned buffer, the zero-copy fused decode (x read "
-                       "and out written over the host link), return when out is on the host; "
-                       "mean over the steps",
-                "c_harness": e2e_c, "python_api_us": e2e_py},
+                "how": "C caller (lib/e2e_host mode 3) of oea_moe_decode_host: each step's "
+                       "tokens in pinned host memory (a distinct slice per step), the fused "
+                       "decode reads them over the host link (x_stage) and writes out to pinned "
+                       "host memory, the call returns when out is on the host; mean over the steps",
+                "c_harness": e2e_c,
+                "with_pageable_staging_copy": e2e_c_staged,
+                "python_api_us": e2e_py},
         "gpu_launches": launches,
         "clocks": clocks,
     }

@@ -44,9 +44,12 @@ int main(int argc, char** argv) {
   const int D = atoi(argv[1]), H = atoi(argv[2]), N = atoi(argv[3]), B = atoi(argv[4]);
   const int k0 = atoi(argv[5]), steps = atoi(argv[6]), warm = atoi(argv[7]);
   const int R = argc > 8 ? atoi(argv[8]) : 4;
-  /* mode 0: oea_moe_decode_host (zero copy); 1: H2D memcpy + device decode +
-   * D2H memcpy + sync; 2: H2D memcpy + device decode writing the mapped out +
-   * sync (experiments) */
+  /* mode 0: oea_moe_decode_host (zero copy) after a host copy of the step's
+   * tokens from pageable memory into one pinned staging buffer; 1: H2D
+   * memcpy + device decode + D2H memcpy + sync; 2: H2D memcpy + device decode
+   * writing the mapped out + sync (experiments); 3: every step's tokens
+   * already in pinned host memory (one slice per step), oea_moe_decode_host
+   * reads that step's slice zero-copy (no host copy) */
   const int mode = argc > 9 ? atoi(argv[9]) : 0;
   oea_ctx_t ctx = NULL;
   if (oea_ctx_create(0, &ctx)) {
@@ -70,10 +73,17 @@ int main(int argc, char** argv) {
     memcpy(&u, &f, 4);
     src[i] = (uint16_t)(u >> 16);
   }
-  void *xs = NULL, *out = NULL;
+  void *xs = NULL, *out = NULL, *xall = NULL;
   if (cudaHostAlloc(&xs, xb, cudaHostAllocMapped) || cudaHostAlloc(&out, ob, cudaHostAllocMapped)) {
     fprintf(stderr, "cudaHostAlloc failed\n");
     return 1;
+  }
+  if (mode == 3) {
+    if (cudaHostAlloc(&xall, xb * total, cudaHostAllocMapped)) {
+      fprintf(stderr, "cudaHostAlloc failed\n");
+      return 1;
+    }
+    memcpy(xall, src, xb * total);
   }
   void *xdev = NULL, *odev = NULL, *st = NULL;
   cudaMalloc(&xdev, xb);
@@ -84,10 +94,12 @@ int main(int argc, char** argv) {
   double t_copy = 0.0, sink = 0.0;
   for (int i = 0; i < total; ++i) {
     const double t0 = now_us();
-    memcpy(xs, src + (size_t)i * B * D, xb);
+    if (mode != 3) memcpy(xs, src + (size_t)i * B * D, xb);
     const double t1 = now_us();
     if (mode == 0) {
       CK(oea_moe_decode_host(ctx, L[i % R], xs, NULL, B, &cfg, out));
+    } else if (mode == 3) {
+      CK(oea_moe_decode_host(ctx, L[i % R], (const char*)xall + (size_t)i * xb, NULL, B, &cfg, out));
     } else {
       cudaMemcpyAsync(xdev, xs, xb, cudaMemcpyHostToDevice, (cudaStream_t)st);
       CK(oea_moe_decode(ctx, L[i % R], xdev, NULL, B, &cfg, mode == 1 ? odev : out, st));
@@ -118,7 +130,7 @@ int main(int argc, char** argv) {
          mean, t_step[steps / 2], t_step[(steps * 9) / 10], mean_call, t_call[steps / 2],
          t_copy / steps, steps, warm, xb, ob, sink);
   if (getenv("OEA_FFN_TRACE")) {  /* per-launch spans of the last 16 launches */
-    const int LEG = 8192, PER = 4096, NL = 16;
+    const int LEG = 8192, PER = 16384, NL = 16;
     uint64_t* tr = (uint64_t*)malloc(sizeof(uint64_t) * (LEG + NL * PER));
     CK(oea_debug_ffn_trace(ctx, tr, LEG + NL * PER));
     for (int l = 0; l < NL; ++l) {
@@ -139,6 +151,7 @@ int main(int argc, char** argv) {
   for (int r = 0; r < R && r < 16; ++r) oea_layer_destroy(L[r]);
   cudaFreeHost(xs);
   cudaFreeHost(out);
+  if (xall) cudaFreeHost(xall);
   oea_ctx_destroy(ctx);
   return 0;
 }
