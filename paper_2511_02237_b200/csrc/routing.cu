@@ -574,6 +574,49 @@ __device__ __forceinline__ int group_pick_regs(const uint64_t (&k)[EPT], uint32_
   return got;
 }
 
+// The same picks from per-thread lists sorted once (lane_sort_desc): a
+// pick's candidate is the thread's head, the owner of the group's best
+// shifts its list, so a pick costs the group reduction only.
+template <int TPT, int EPT, int U>
+__device__ __forceinline__ int group_pick_sorted(uint64_t (&k)[EPT], int (&id)[EPT], int q, int m,
+                                                 int at, int (&ex)[U], uint64_t (&sk)[U]) {
+  const unsigned gm = 0xffffffffu;  // (m uniform over the warp: converged)
+  int got = 0;
+#pragma unroll 1
+  for (int r = 0; r < m; ++r) {
+    uint64_t bk = k[0];
+    int be = k[0] != 0ull ? id[0] : 0x7fffffff;
+#pragma unroll
+    for (int off = 1; off < TPT; off <<= 1) {
+      const uint64_t ok = __shfl_xor_sync(gm, bk, off);
+      const int oe = __shfl_xor_sync(gm, be, off);
+      if (ranks_before(ok, static_cast<uint32_t>(oe), bk, static_cast<uint32_t>(be))) {
+        bk = ok;
+        be = oe;
+      }
+    }
+    if (bk == 0ull) continue;  // nothing left (uniform over the group)
+    const bool own = k[0] == bk && id[0] == be;
+#pragma unroll
+    for (int j = 0; j + 1 < EPT; ++j) {
+      k[j] = own ? k[j + 1] : k[j];
+      id[j] = own ? id[j + 1] : id[j];
+    }
+    if (own) k[EPT - 1] = 0ull;
+    const int slot = at + got;
+    if (q == slot % TPT) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (u == slot / TPT) {
+          ex[u] = be;
+          sk[u] = bk;
+        }
+    }
+    ++got;
+  }
+  return got;
+}
+
 template <int TPT, int kGroupThreads>
 __global__ void __launch_bounds__(kGroupThreads)
     k_group_route(const Cfg cfg, const int B, const int N, const int set_mode, const int do_weights,
@@ -624,9 +667,11 @@ __global__ void __launch_bounds__(kGroupThreads)
   }
   // phase 1: base set (vanilla: the top k)
   const int want = min(set_mode == 0 ? cfg.k : cfg.k0, N);
-  uint64_t pk = ~0ull;
-  int pe = -1;
-  const int n = group_pick_regs<TPT, EPT, U>(k, 0xffffffffu, q, want, 0, ex, sk, pk, pe);
+  int id[EPT];
+#pragma unroll
+  for (int j = 0; j < EPT; ++j) id[j] = TPT * j + q;
+  lane_sort_desc<EPT>(k, id);
+  const int n = group_pick_sorted<TPT, EPT, U>(k, id, q, want, 0, ex, sk);
   stamp(1);
   if (valid && set_mode != 0) {
 #pragma unroll
@@ -652,20 +697,23 @@ __global__ void __launch_bounds__(kGroupThreads)
     }
     __syncthreads();
     stamp(3);
-    // phase 2: union members ranked after the base set, until the cap
-    uint32_t um = 0u;
+    // phase 2: union members ranked after the base set, until the cap: the
+    // lists' remaining entries all rank after the base (it is the top n);
+    // drop the non-members and sort again
     {
       uint32_t uw[4];
 #pragma unroll
       for (int w = 0; w < 4; ++w) uw[w] = __ldcg(&scr->uni[w]);
 #pragma unroll
       for (int j = 0; j < EPT; ++j) {
-        const int e = TPT * j + q;
-        if (e < N && ((uw[e >> 5] >> (e & 31)) & 1u)) um |= 1u << j;
+        const int e = id[j];
+        const uint32_t word = e < 32 ? uw[0] : e < 64 ? uw[1] : e < 96 ? uw[2] : uw[3];
+        if (n == 0 || !((word >> (e & 31)) & 1u)) k[j] = 0ull;
       }
     }
+    lane_sort_desc<EPT>(k, id);
     const int m = max(0, cfg.limit - min(cfg.k0, N));
-    const int got = group_pick_regs<TPT, EPT, U>(k, n > 0 ? um : 0u, q, m, n, ex, sk, pk, pe);
+    const int got = group_pick_sorted<TPT, EPT, U>(k, id, q, m, n, ex, sk);
     len = real ? n + min(got, max(0, cfg.limit - n)) : 0;
   }
   if (valid) {

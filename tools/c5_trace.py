@@ -11,6 +11,7 @@ from paper_2511_02237_b200._capi import lib as _lib  # noqa: E402
 buf = np.zeros(8192, np.uint64)
 ctx.check(_lib().oea_debug_ffn_trace(ctx.h, buf.ctypes.data_as(C.c_void_p), buf.size))
 t = buf[:256 * 8].reshape(256, 8).astype(np.int64)
+t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
 names = ["start", "phase1 picks", "union flushed", "barrier passed", "phase2+finish", "done counted", "last CTA aggregate"]
 for sl, nm in enumerate(names):
