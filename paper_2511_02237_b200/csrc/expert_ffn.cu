@@ -1027,11 +1027,21 @@ __device__ __forceinline__ int union_barrier(const FfnParams& P, uint8_t* rs, co
       reinterpret_cast<uint4*>(rows)[t] = v4;
     }
     __syncthreads();
-    if (threadIdx.x < 4) {
-      uint32_t o = 0u;
+    if (P.B <= 32) {
+      if (threadIdx.x < 4) {
+        uint32_t o = 0u;
 #pragma unroll 4
-      for (int t = 0; t < P.B; ++t) o |= rows[4 * t + threadIdx.x];
-      uni[threadIdx.x] = o;
+        for (int t = 0; t < P.B; ++t) o |= rows[4 * t + threadIdx.x];
+        uni[threadIdx.x] = o;
+      }
+    } else if (warp < 4) {
+      // many tokens: warp w ORs word w of every row, 32 rows per step, then
+      // a shuffle butterfly (a serial loop over B rows would cost ~B x 30 cycles)
+      uint32_t o = 0u;
+      for (int t = lane; t < P.B; t += 32) o |= rows[4 * t + warp];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) o |= __shfl_xor_sync(kFull, o, off);
+      if (lane == 0) uni[warp] = o;
     }
     __syncthreads();
   }
