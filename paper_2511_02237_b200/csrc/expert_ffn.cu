@@ -117,6 +117,8 @@ struct FfnParams {
   // slot [rank][t - owner * tpr], then every CTA bumps every owner's counter.
   // (Last member: the offsets of the hot fields stay as they were.)
   const EpPeers* ep;  // null: local combine into out
+  int pf_guess_hi, pf_guess_lo;  // W1-head prefetch of guessed-active / -inactive own experts
+  float pf_tau;                  // guess: max logit > pf_tau x rms of the batch's logits
   // Route-only launch (B > 64): the compaction in the same launch (CTA e
   // builds expert e's token groups; route_compact_dist) and, for the tcgen05
   // FFN, the token rows gathered into the CM layout (xg, xg_rg row groups)
@@ -577,7 +579,7 @@ __device__ __forceinline__ void dispatch_w2_dense(int nbk, const FfnParams& P, c
 // ---------------------------------------------------------------------------
 struct RouteSmem {
   size_t keys, ukeys, uni, sets, e, len, n, mx, loads, tokbits, active, eslot, rowb, rows, rtok,
-      rslot, red, misc, total;
+      rslot, red, misc, lgp, total;
 };
 
 __host__ __device__ inline RouteSmem route_smem_layout(int B, int Np, int stride) {
@@ -608,6 +610,7 @@ __host__ __device__ inline RouteSmem route_smem_layout(int B, int Np, int stride
   L.rtok = take(rmax * 4);
   L.rslot = take(rmax * 4);
   L.red = take((kFfnThreads / 32) * 16 * 4);
+  L.lgp = take(64 * 4);  // this CTA's expert's logits (first 64 tokens): the prefetch guess
   L.misc = take(8 * 4);
   L.total = o;
   return L;
@@ -626,7 +629,7 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float (&f)[8]) {
 // FFN's B fragments read when D is not a tile multiple. Ends with the grid
 // barrier after which every CTA may read all logits (and xpad).
 __device__ __forceinline__ void fused_gemv(const FfnParams& P, float* red, int* sync_cnt,
-                                           uint32_t tag) {
+                                           uint32_t tag, float* lgp = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NT = kFfnThreads;
   const int nch = P.Dp >> 3;
@@ -715,6 +718,7 @@ __device__ __forceinline__ void fused_gemv(const FfnParams& P, float* red, int* 
 #pragma unroll
         for (int w = 0; w < kFfnThreads / 32; ++w) s += red[w * 16 + tid];
         // the token's router CTA polls this word (no grid barrier needed)
+        if (e == static_cast<int>(blockIdx.x) && lgp != nullptr && tc + tid < 64) lgp[tc + tid] = s;
         st_relaxed_u64(P.xlog + static_cast<size_t>(tc + tid) * P.Np + e,
                        tagged(tag, __float_as_uint(s)));
       }
@@ -739,13 +743,36 @@ __device__ __forceinline__ void fused_gemv(const FfnParams& P, float* red, int* 
 // every held expert (each is active with probability ~T/N; the stream reads
 // them as L2 hits, and its evict_first lines leave before these). Producer
 // warp, one 32 KiB prefetch per lane.
-__device__ __forceinline__ void prefetch_w1_heads(const FfnParams& P, int lane) {
+__device__ __forceinline__ void prefetch_w1_heads(const FfnParams& P, int lane,
+                                                  const float* lgp = nullptr) {
   const size_t per = static_cast<size_t>(P.Hp >> 3) * (P.Dp >> 4) * 512;  // W1 bytes per expert
-  const uint32_t nb = static_cast<uint32_t>(min(per, static_cast<size_t>(P.prefetch_bytes)));
-  for (int e = blockIdx.x; e < P.e_count; e += gridDim.x)
+  size_t want = static_cast<size_t>(P.prefetch_bytes);
+  const int nt = min(P.B, 64);
+  if (lgp != nullptr && P.pf_guess_hi > 0 && nt >= 4) {
+    // Guess from this CTA's own expert's logits (known right after its GEMV,
+    // no exchange): a base-set member ranks in some token's top k0 of N, so
+    // its largest logit over the batch sits far above this expert's mean
+    // (C1: ~2 standard deviations for a top-4 of 128). Likely-active experts
+    // get a deep prefetch (1.5 MiB: their first W1 rounds), the others none:
+    // HBM idles during the routing prologue, and a right guess turns it into
+    // stream time (C1 82.6 -> 78.7 us; a wrong one only costs traffic).
+    float mx = -INFINITY, sm = 0.0f, ss = 0.0f;
+    for (int t = 0; t < nt; ++t) {
+      mx = fmaxf(mx, lgp[t]);
+      sm += lgp[t];
+      ss += lgp[t] * lgp[t];
+    }
+    const float mean = sm / nt, sd = sqrtf(fmaxf(ss / nt - mean * mean, 0.0f));
+    want = mx - mean > P.pf_tau * sd ? static_cast<size_t>(P.pf_guess_hi)
+                                     : static_cast<size_t>(P.pf_guess_lo);
+  }
+  for (int e = blockIdx.x; e < P.e_count; e += gridDim.x) {
+    const uint32_t nb = static_cast<uint32_t>(
+        min(per, e == static_cast<int>(blockIdx.x) ? want : static_cast<size_t>(P.prefetch_bytes)));
     for (uint32_t o = 32u * 1024u * lane; o < nb; o += 32u * 32u * 1024u)
       bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(P.w1) + e * per + o,
                        min(32u * 1024u, nb - o));
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1550,11 +1577,13 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
       if (threadIdx.x == 0) stamp(P, 8);
       tile_gemv(P, SR.buf, tag);
     } else
-      fused_gemv(P, reinterpret_cast<float*>(rs + RL.red), claims + 3, tag);
+      fused_gemv(P, reinterpret_cast<float*>(rs + RL.red), claims + 3, tag,
+                 reinterpret_cast<float*>(rs + RL.lgp));
     if (threadIdx.x == 0) stamp(P, 5);
     // (x in device memory: after the GEMV, whose loads it would delay)
-    if (!kRouteOnly && !pf_early && !P.x_stage && warp == kProducerWarp && P.prefetch_bytes > 0)
-      prefetch_w1_heads(P, lane);
+    if (!kRouteOnly && !pf_early && !P.x_stage && warp == kProducerWarp &&
+        (P.prefetch_bytes > 0 || P.pf_guess_hi > 0))
+      prefetch_w1_heads(P, lane, P.e_begin == 0 && P.e_count == P.N ? reinterpret_cast<const float*>(rs + RL.lgp) : nullptr);
     // R1: CTA t routes token t (thread per expert), then the union barrier
     if (threadIdx.x < 128) {
 #pragma unroll 1
@@ -1583,6 +1612,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
       if (warp < kFfnWarps) route_phase2_plan<kFfnWarps>(P, rs, RL, T, tag, false);
       if (P.compact_in_kernel) {
         __syncthreads();  // (this CTA's rows are out: cumulative release below)
+        if (threadIdx.x == 0) stamp(P, 1);
         if (threadIdx.x == 0 && static_cast<int>(blockIdx.x) < P.B)
           red_release_gpu_add(claims, (P.B - 1 - static_cast<int>(blockIdx.x)) /
                                           static_cast<int>(gridDim.x) + 1);
@@ -2266,6 +2296,14 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   {
     static const int ks = getenv("OEA_W2_KSPLIT") ? atoi(getenv("OEA_W2_KSPLIT")) : kW2KSplit;
     P.w2_ks = std::max(1, std::min(ks, kW2KSplitMax));
+  }
+  {
+    static const int hi = getenv("OEA_PF_HI_KB") ? atoi(getenv("OEA_PF_HI_KB")) : 1536;
+    static const int lo = getenv("OEA_PF_LO_KB") ? atoi(getenv("OEA_PF_LO_KB")) : 0;
+    static const int tau = getenv("OEA_PF_TAU") ? atoi(getenv("OEA_PF_TAU")) : 215;
+    P.pf_guess_hi = hi * 1024;
+    P.pf_guess_lo = lo * 1024;
+    P.pf_tau = tau / 100.0f;
   }
   P.compact_in_kernel = fb.compact_in_kernel;
   P.xg = static_cast<uint8_t*>(fb.xg);
