@@ -528,6 +528,7 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
     rf.group_rows = w.group_rows;
     rf.compact_in_kernel = big_compact ? 1 : 0;
     rf.xg = big_compact && use_umma ? w.xg : nullptr;
+    rf.pf_w1u = use_umma ? L->w1u : nullptr;
     rf.xg_rg = xg_rg;
     r = oea_host::ffn_bf16_launch(ctx, L, B, stride, rf, false, s);
     if (r) return r;

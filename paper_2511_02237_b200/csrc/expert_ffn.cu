@@ -117,6 +117,11 @@ struct FfnParams {
   // slot [rank][t - owner * tpr], then every CTA bumps every owner's counter.
   // (Last member: the offsets of the hot fields stay as they were.)
   const EpPeers* ep;  // null: local combine into out
+  // route-only launch: L2 prefetch of the tcgen05 FFN's first W1 bytes (the
+  // active experts' UMMA-layout W1 in group order), while this launch routes
+  const uint8_t* pf_w1u;
+  size_t pf_w1u_stride;
+  size_t pf_total;
   int pf_guess_hi, pf_guess_lo;  // W1-head prefetch of guessed-active / -inactive own experts
   float pf_tau;                  // guess: max logit > pf_tau x rms of the batch's logits
   // Route-only launch (B > 64): the compaction in the same launch (CTA e
@@ -1605,6 +1610,19 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
       stamp(P, 6);
       if (s_trace && blockIdx.x == 0) s_trace[kTraceInfo] = static_cast<unsigned long long>(T);
     }
+    if (kRouteOnly && P.pf_w1u != nullptr && warp == kProducerWarp) {
+      // HBM idles until the FFN launch: the first pf_total bytes of the
+      // active experts' W1 streams (the FFN claims W1 group-major, experts
+      // ascending) into L2, 32 KiB per lane, spread over the grid
+      const int* act = reinterpret_cast<const int*>(rs + RL.active);
+      const size_t total = min(P.pf_total, static_cast<size_t>(T) * P.pf_w1u_stride);
+      for (size_t c = static_cast<size_t>(blockIdx.x) * 32 + lane; c * 32768 < total;
+           c += static_cast<size_t>(gridDim.x) * 32) {
+        const size_t byte = c * 32768, i = byte / P.pf_w1u_stride, off = byte - i * P.pf_w1u_stride;
+        bulk_prefetch_l2(P.pf_w1u + static_cast<size_t>(act[i] - P.e_begin) * P.pf_w1u_stride + off,
+                         static_cast<uint32_t>(min(static_cast<size_t>(32768), P.pf_w1u_stride - off)));
+      }
+    }
     if (kRouteOnly) {
       // plan rows (CTA t: token t, t + grid, ...); the FFN tables and the
       // aggregates (loads, header) follow: in this launch (route_compact_dist)
@@ -2304,6 +2322,12 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
     P.pf_guess_hi = hi * 1024;
     P.pf_guess_lo = lo * 1024;
     P.pf_tau = tau / 100.0f;
+  }
+  P.pf_w1u = static_cast<const uint8_t*>(fb.pf_w1u);
+  P.pf_w1u_stride = static_cast<size_t>(2 * L->Hp) * L->Dp * 2;
+  {
+    static const int mb = getenv("OEA_BIG_PF_MB") ? atoi(getenv("OEA_BIG_PF_MB")) : 32;
+    P.pf_total = static_cast<size_t>(mb) << 20;
   }
   P.compact_in_kernel = fb.compact_in_kernel;
   P.xg = static_cast<uint8_t*>(fb.xg);

@@ -252,6 +252,7 @@ struct FfnBuffers {
   int* done_flag = nullptr;             // mapped host flag set to 1 when out is on the host
   const oea_dev::EpPeers* ep = nullptr;  // peer-memory EP combine (device table), or null
   int compact_in_kernel = 0;            // route-only: the compaction in the same launch
+  const void* pf_w1u = nullptr;         // route-only: the tcgen05 FFN's W1 copy to prefetch (or null)
   void* xg = nullptr;                   // ... and the tcgen05 FFN's gathered rows (or null)
   int xg_rg = 0;
   float* logits = nullptr;              // [B][Np]
