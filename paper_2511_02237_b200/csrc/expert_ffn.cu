@@ -124,6 +124,7 @@ struct FfnParams {
   size_t pf_total;
   int pf_guess_hi, pf_guess_lo;  // W1-head prefetch of guessed-active / -inactive own experts
   float pf_tau;                  // guess: max logit > pf_tau x rms of the batch's logits
+  int host_pf_guess;             // x in host memory: the guided prefetch after the GEMV too
   // Route-only launch (B > 64): the compaction in the same launch (CTA e
   // builds expert e's token groups; route_compact_dist) and, for the tcgen05
   // FFN, the token rows gathered into the CM layout (xg, xg_rg row groups)
@@ -1586,7 +1587,9 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
                  reinterpret_cast<float*>(rs + RL.lgp));
     if (threadIdx.x == 0) stamp(P, 5);
     // (x in device memory: after the GEMV, whose loads it would delay)
-    if (!kRouteOnly && !pf_early && !P.x_stage && warp == kProducerWarp &&
+    // (x in host memory: the blind heads went out before the staging; the
+    // guided ones follow here when the guess is on: OEA_HOST_PF_GUESS)
+    if (!kRouteOnly && !pf_early && (!P.x_stage || P.host_pf_guess) && warp == kProducerWarp &&
         (P.prefetch_bytes > 0 || P.pf_guess_hi > 0))
       prefetch_w1_heads(P, lane, P.e_begin == 0 && P.e_count == P.N ? reinterpret_cast<const float*>(rs + RL.lgp) : nullptr);
     // R1: CTA t routes token t (thread per expert), then the union barrier
@@ -2301,9 +2304,13 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
     // ~32 MiB in total, about what HBM delivers while the prologue routes
     // (measured C1, N=128: 128 KiB per expert saves ~1.3 us, 224-288 KiB
     // ~2.2 us, 320 KiB less again; issuing it before the gate GEMV is slower)
+    // Round 2: full layers use the logit-guided prefetch instead (below,
+    // prefetch_w1_heads); the blind heads stay for EP shards (no guess: a
+    // shard's CTAs compute other experts' logits than the ones it holds)
     static const int pf = getenv("OEA_PREFETCH_KB") ? atoi(getenv("OEA_PREFETCH_KB")) : -1;
     P.prefetch_bytes = pf >= 0 ? pf * 1024
-                               : ((32 << 20) / max(L->n_local, 1)) & ~(32 * 1024 - 1);
+                       : L->n_local < L->N ? ((32 << 20) / max(L->n_local, 1)) & ~(32 * 1024 - 1)
+                                           : 0;
   }
   {
     // (issuing it before the wait was measured slower: the CTAs only become
@@ -2322,6 +2329,8 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
     P.pf_guess_hi = hi * 1024;
     P.pf_guess_lo = lo * 1024;
     P.pf_tau = tau / 100.0f;
+    static const int hg = getenv("OEA_HOST_PF_GUESS") ? atoi(getenv("OEA_HOST_PF_GUESS")) : 1;
+    P.host_pf_guess = hg;
   }
   P.pf_w1u = static_cast<const uint8_t*>(fb.pf_w1u);
   P.pf_w1u_stride = static_cast<size_t>(2 * L->Hp) * L->Dp * 2;
