@@ -117,6 +117,7 @@ struct FfnParams {
   // slot [rank][t - owner * tpr], then every CTA bumps every owner's counter.
   // (Last member: the offsets of the hot fields stay as they were.)
   const EpPeers* ep;  // null: local combine into out
+  int r0;             // dense W1: rounds claimed round-major first
   // route-only launch: L2 prefetch of the tcgen05 FFN's first W1 bytes (the
   // active experts' UMMA-layout W1 in group order), while this launch routes
   const uint8_t* pf_w1u;
@@ -1718,7 +1719,19 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
         if (w1_left) {
           const int r = atomicAdd(&claims[0], 1);
           if (r * kFfnWarps < U1) {
-            d.u0 = r * kFfnWarps;
+            // the first r0 rounds of every group first (round-major: the
+            // heads the prologue prefetched into L2), then group-major
+            const int RR = RB1 / kFfnWarps, r0 = min(P.r0, RR);
+            int g, rr;
+            if (r < r0 * G) {
+              rr = r / G;
+              g = r - rr * G;
+            } else {
+              const int q = r - r0 * G;
+              g = q / (RR - r0);
+              rr = r0 + (q - g * (RR - r0));
+            }
+            d.u0 = g * RB1 + rr * kFfnWarps;
             d.n = min(kFfnWarps, U1 - d.u0);
             d.kind = 1;
             d.se = KT1 / kKtPerSlot;
@@ -2337,6 +2350,10 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   {
     static const int mb = getenv("OEA_BIG_PF_MB") ? atoi(getenv("OEA_BIG_PF_MB")) : 32;
     P.pf_total = static_cast<size_t>(mb) << 20;
+  }
+  {
+    static const int r0 = getenv("OEA_R0") ? atoi(getenv("OEA_R0")) : 2;
+    P.r0 = fb.dense ? r0 : 0;
   }
   P.compact_in_kernel = fb.compact_in_kernel;
   P.xg = static_cast<uint8_t*>(fb.xg);
