@@ -38,6 +38,10 @@
 #include "oea_internal.cuh"
 #include "route_dev.cuh"
 
+#ifndef P_NA_MAXNB
+#define P_NA_MAXNB 2
+#endif
+
 namespace oea_dev {
 
 // 8 consumer warps, 1 producer warp (lane 0 streams weights), 1 router warp
@@ -300,7 +304,7 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
   // two accumulator sets (even / odd k-tiles) halve the dependent HMMA chain
   // (one n-block: two sets halve the dependent HMMA chain; more n-blocks
   // already interleave independent chains, so they use one set)
-  constexpr int NA = NB == 1 ? 2 : 1;
+  constexpr int NA = NB <= P_NA_MAXNB ? 2 : 1;
   float acc2[NA][NB][4];
 #pragma unroll
   for (int h2 = 0; h2 < NA; ++h2)
@@ -393,7 +397,9 @@ __device__ __forceinline__ void consume_unit(const FfnParams& P, const PlanRef* 
           uint4 v[NB];
 #pragma unroll
           for (int nb = 0; nb < NB; ++nb) {
-            if (SHB)
+            if (P.mode == 2)  // (debug: no B-operand loads)
+              v[nb] = make_uint4(0u, 0u, 0u, 0u);
+            else if (SHB)
               v[nb] = lds128(PR->btile + (s0 % 3) * kBTileBuf + nb * 2048 + boff[jj]);
             else if (XSM)
               v[nb] = lds128(reinterpret_cast<const uint8_t*>(bp[nb]) + s * 256 + xoff[jj]);
