@@ -572,6 +572,28 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
     fb.dense = B <= 16 && L->Hp <= 8192 && getenv("OEA_SPARSE") == nullptr &&
                oea_host::ffn_bf16_smem_bytes() + oea_host::ffn_route_smem_bytes(B, L->Np, stride) +
                        oea_host::ffn_dense_xs_bytes(L->Dp) <= 227 * 1024;
+    // OEA_UMMA_DENSE=1 (experimental, off by default: measured slower, DESIGN.md
+    // §3b): dense decode on tcgen05 (MODE 6) when the layer's UMMA-layout copy
+    // exists or can be made now (not during a capture, enough free memory)
+    static const bool udense = getenv("OEA_UMMA_DENSE") != nullptr && atoi(getenv("OEA_UMMA_DENSE")) != 0;
+    if (fb.dense && udense && !ep && !shard && !x_mapped && umma_ok(ctx, L, s)) {
+      bool have = L->w1u != nullptr;
+      if (!have) {
+        size_t fr = 0, tot = 0;
+        const size_t need = static_cast<size_t>(3 * L->Hp) * L->Dp * 2 * L->n_local;
+        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess && fr > need + (size_t(4) << 30)) {
+          r = oea_host::layer_prepare_umma(ctx, L, s);
+          if (r) return r;
+          L->umma_stale = 0;
+          have = true;
+        }
+      } else if (L->umma_stale) {
+        r = oea_host::layer_prepare_umma(ctx, L, s);
+        if (r) return r;
+        L->umma_stale = 0;
+      }
+      fb.umma_dense = have ? 1 : 0;
+    }
     fb.x_in = static_cast<const __nv_bfloat16*>(x);
     fb.xpad_out = padded || x_mapped ? w.xpad : nullptr;
     fb.x_stage = x_mapped ? 1 : 0;

@@ -121,6 +121,10 @@ struct FfnParams {
   // slot [rank][t - owner * tpr], then every CTA bumps every owner's counter.
   // (Last member: the offsets of the hot fields stay as they were.)
   const EpPeers* ep;  // null: local combine into out
+  // MODE 6 (dense decode on tcgen05): the UMMA-layout expert weights
+  const uint8_t* w1u;
+  const uint8_t* w2u;
+  size_t w1u_stride, w2u_stride;
   int r0;             // dense W1: rounds claimed round-major first
   // route-only launch: L2 prefetch of the tcgen05 FFN's first W1 bytes (the
   // active experts' UMMA-layout W1 in group order), while this launch routes
@@ -1482,6 +1486,48 @@ __device__ __forceinline__ void grid_exit(const FfnParams& P, int* claims, int G
   }
 }
 
+// ---- tcgen05 helpers of the dense tensor-core consumer (MODE 6) ----------
+// canonical K-major no-swizzle UMMA operand: LBO 128 B (K), SBO 2 KiB (M/N)
+__device__ __forceinline__ uint64_t d_umma_desc(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4) | (static_cast<uint64_t>(128 >> 4) << 16) |
+         (static_cast<uint64_t>(2048 >> 4) << 32) | (1ull << 46);
+}
+// D fp32, A / B bf16 K-major, N = 16, M = 128
+constexpr uint32_t kDenseIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (2u << 17) | (8u << 24);
+__device__ __forceinline__ void d_umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %4, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(acc), "r"(kDenseIdesc)
+      : "memory");
+}
+__device__ __forceinline__ void d_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void d_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void d_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void d_tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+// dense h / x tiles in the UMMA layout: [128-wide K slice][2 row groups of 8
+// tokens][16 k-groups][8 tokens][8 k] bf16 (4 KiB per slice)
+__host__ __device__ __forceinline__ size_t cm16_index(int r, int k) {
+  return static_cast<size_t>(k >> 7) * 2048 + (r >> 3) * 1024 + ((k & 127) >> 3) * 64 + (r & 7) * 8 +
+         (k & 7);
+}
+
 // Round descriptor published by the producer through the stage barrier.
 struct RoundDesc {
   int u0;    // first unit
@@ -1500,9 +1546,10 @@ constexpr int kRoundRing = 8;  // > kStages: a round spans >= 1 stage
 template <int MODE>
 __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) {
   constexpr bool kFused = MODE != 0;
-  constexpr bool kDense = MODE == 2 || MODE == 5;
+  constexpr bool kUmma = MODE == 6;  // dense decode, tcgen05 consumer
+  constexpr bool kDense = MODE == 2 || MODE == 5 || kUmma;
   constexpr bool kRouteOnly = MODE == 3;  // plan only (B > 64); the FFN runs as MODE 0
-  constexpr bool kEp = MODE >= 4;         // 4 / 5: MODE 1 / 2 with the peer-memory EP combine
+  constexpr bool kEp = MODE == 4 || MODE == 5;  // MODE 1 / 2 with the peer-memory EP combine
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
@@ -1521,7 +1568,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kFfnWarps);
+      mbar_init(&empty[s], kUmma ? 1 : kFfnWarps);  // (MODE 6: the MMA commit frees it)
     }
     mbar_init(plan_bar, 1);
     mbar_init(plan_bar + 1, 1);  // split rounds: warp 0 has read the reduction buffer
@@ -1818,9 +1865,15 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
         const int v = is1 ? d.u0 : d.u0 - U1;
         const int RB = is1 ? RB1 : RB2;
         const int g = v / RB, rr = (v % RB) / kFfnWarps;
-        const uint4* base = (is1 ? P.w1 : P.w2) +
-                            (static_cast<size_t>(PR->group_a[g] - P.e_begin) * RB + rr * kFfnWarps) *
-                                KT * 32;
+        // (MODE 6: the UMMA-layout copy, m-block rr = these 8 row blocks;
+        // a stage is the same 32 KiB block size in both layouts)
+        const uint4* base =
+            kUmma ? reinterpret_cast<const uint4*>(
+                        (is1 ? P.w1u : P.w2u) +
+                        static_cast<size_t>(PR->group_a[g] - P.e_begin) * (is1 ? P.w1u_stride : P.w2u_stride) +
+                        static_cast<size_t>(rr) * (KT / kKtPerSlot) * kStageBytes)
+                  : (is1 ? P.w1 : P.w2) +
+                        (static_cast<size_t>(PR->group_a[g] - P.e_begin) * RB + rr * kFfnWarps) * KT * 32;
         // dense W2: the group's h slice of each stage rides in the stage
         const bool hst = kDense && !is1;
         const uint32_t sbytes = d.n * kSlotBytes + (hst ? kHSlice : 0);
@@ -1887,21 +1940,136 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
   if (kDense) {
     // x (final since the logits barrier) -> swizzled shared tile, 16 rows
     // (rows >= B zero-filled), while the producer's first stages land
+    // (MODE 6: the UMMA layout, cm16_index)
     const int nch = P.Dp >> 3;
 #pragma unroll 4
     for (int i = threadIdx.x; i < 16 * nch; i += kFfnWarps * 32) {
       const int t = i / nch, c = i % nch;
-      const uint32_t dst = smem_u32(xs + t * P.xs_row + (c >> 4) * 256 + xs_chunk(c & 15) * 16);
+      const uint32_t dst =
+          kUmma ? smem_u32(xs + cm16_index(t, c * 8) * 2)
+                : smem_u32(xs + t * P.xs_row + (c >> 4) * 256 + xs_chunk(c & 15) * 16);
       const __nv_bfloat16* src = P.xpad + static_cast<size_t>(t < P.B ? t : 0) * P.Dp + c * 8;
       cp_async16(dst, src, t < P.B ? 16 : 0);
     }
     cp_async_commit();
     cp_async_wait_all();
+    if (kUmma) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // (tcgen05 reads it)
     asm volatile("bar.sync 1, %0;" ::"r"(kFfnWarps * 32) : "memory");
   } else if (kFused) {
     route_phase2_plan<kFfnWarps>(P, rs, RL, G, tag);  // overlaps the first stages
     if (threadIdx.x == 0) stamp(P, 7);
   }
+  if constexpr (kUmma) {
+    // ---- tcgen05 consumer (dense decode): warp 0 allocates TMEM and its lane
+    // 0 issues the MMAs (M = 128 rows of the round, N = the 16 token rows,
+    // K = 16 per instruction, 8 per stage; A = the stage, B = the x tile slice
+    // (W1) or the stage's h slice (W2)); warps 4-7 drain the accumulator
+    // (TMEM lanes 32 (warp % 4) ..): W1 -> silu(g) * u -> h, W2 -> y[group][token]
+    uint8_t* ext = xs + static_cast<size_t>(16) * P.Dp * 2;  // (the tile's row padding)
+    uint64_t* tfull = reinterpret_cast<uint64_t*>(ext);      // [2] accumulator ready
+    uint64_t* tempty = tfull + 2;                             // [2] drained (4 warps)
+    uint64_t* dready = tempty + 2;                            // [2] round descriptor out
+    RoundDesc* udesc = reinterpret_cast<RoundDesc*>(dready + 2);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(udesc + 2);
+    if (threadIdx.x == 0) {
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&tfull[b], 1);
+        mbar_init(&tempty[b], 4);
+        mbar_init(&dready[b], 1);
+      }
+      fence_mbar_init();
+    }
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tslot)),
+                   "r"(32)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    d_fence_before();
+    asm volatile("bar.sync 1, %0;" ::"r"(kFfnWarps * 32) : "memory");
+    d_fence_after();
+    const uint32_t tmem = *tslot;
+    if (warp == 0) {
+      if (lane == 0) {
+        for (int seq = 0;; ++seq) {
+          mbar_wait(&full[stage], phase);  // the round's first stage carries its descriptor
+          const RoundDesc d = rdesc[seq & (kRoundRing - 1)];
+          const int buf = seq & 1;
+          if (d.n == 0) {
+            udesc[buf] = d;
+            mbar_arrive(&dready[buf]);
+            break;
+          }
+          mbar_wait(&tempty[buf], ((seq >> 1) & 1) ^ 1u);
+          d_fence_after();
+          const bool is1 = d.kind == 1;
+          const uint32_t dt = tmem + buf * 16;
+          const int nst = d.se - d.sb;
+          for (int s0 = 0; s0 < nst; ++s0) {
+            if (s0 > 0) mbar_wait(&full[stage], phase);
+            d_fence_after();
+            const int s = d.sb + s0;
+            const uint32_t a0 = smem_u32(ring + stage * kStageBytes);
+            const uint32_t b0 = is1 ? smem_u32(xs + s * 4096)
+                                    : smem_u32(reinterpret_cast<uint8_t*>(SR.buf) + stage * kHSlice);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+              d_umma(dt, d_umma_desc(a0 + kk * 256), d_umma_desc(b0 + kk * 256), (s0 | kk) != 0);
+            d_commit(&empty[stage]);  // the stage is free once these MMAs are done
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+          udesc[buf] = d;
+          mbar_arrive(&dready[buf]);
+          d_commit(&tfull[buf]);
+        }
+      }
+      __syncwarp();
+    } else if (warp >= 4) {
+      const int q = warp & 3, m = 32 * q + lane;
+      for (int seq = 0;; ++seq) {
+        const int buf = seq & 1;
+        mbar_wait(&dready[buf], (seq >> 1) & 1);
+        const RoundDesc d = udesc[buf];
+        if (d.n == 0) break;
+        mbar_wait(&tfull[buf], (seq >> 1) & 1);
+        d_fence_after();
+        float v[16];
+        d_tmem_ld16(tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * 16, v);
+        d_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+        const bool is1 = d.kind == 1;
+        const int vu = is1 ? d.u0 : d.u0 - U1;
+        const int RB = is1 ? RB1 : RB2;
+        const int g = vu / RB, rr = (vu % RB) / kFfnWarps;
+        if (is1) {
+          // rows m: row block j = m / 16 holds gate (m % 16 < 8) and up of
+          // h = 64 rr + 8 j + m % 8; the gate lane takes up from lane + 8
+          const bool gate = (m & 15) < 8;
+          const int hh = 64 * rr + 8 * (m >> 4) + (m & 7);
+          __nv_bfloat16* hgp = P.hbuf + static_cast<size_t>(g) * 16 * P.Hp;
+#pragma unroll
+          for (int n = 0; n < 16; ++n) {
+            const float up = __shfl_down_sync(kFull, v[n], 8);
+            if (gate) hgp[cm16_index(n, hh)] = __float2bfloat16_rn(silu_f(v[n]) * up);
+          }
+          // the round's h (8 row blocks) out: the epilogue barrier orders the
+          // 128 threads' stores before one cumulative release
+          asm volatile("bar.sync 6, 128;" ::: "memory");
+          if (warp == 4 && lane == 0)
+            red_release_gpu_add_u64(&P.w1_slots[g], 8ull << (8 * ((rr >> 1) / w1_slot_q(P.Hp))));
+        } else {
+          float* yg = P.ybuf + static_cast<size_t>(g) * 16 * P.Dp + 128 * rr + m;
+#pragma unroll
+          for (int n = 0; n < 16; ++n) yg[static_cast<size_t>(n) * P.Dp] = v[n];
+        }
+      }
+    }
+  } else {
   bool in_w2 = false;
   for (int seq = 0;; ++seq) {
     mbar_wait(&full[stage], phase);  // the round's first stage carries its descriptor
@@ -1959,6 +2127,7 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
       skip_unit(full, empty, stage, phase, nst);
     }
   }
+  }  // (mma.sync consumers)
   if (threadIdx.x == 0) stamp(P, 3);
   }
 
@@ -1988,7 +2157,8 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
       const int o = t * P.stride + s0 + j;
       // expert-parallel shard: this layer's partial sum over its experts
       const bool ok = s0 + j < len && (!kShard || eslot[ssets[o]] >= 0);
-      yo[j] = ok ? o * P.Dp + d : -1;
+      // (MODE 6: y per (expert group, token): [G][16][Dp])
+      yo[j] = ok ? (kUmma ? (eslot[ssets[o]] * 16 + t) * P.Dp + d : o * P.Dp + d) : -1;
       w[j] = ok ? PR->wts[o] : 0.0f;
     }
   };
@@ -2025,6 +2195,14 @@ __global__ void __launch_bounds__(kFfnThreads, 1) k_ffn_bf16(const FfnParams P) 
   }
   asm volatile("bar.sync 2, %0;" ::"r"(kComb + 32) : "memory");
   if (warp == kRouterWarp) return;
+  if (kUmma && warp == 0) {  // (every tcgen05 op of the CTA is done: the barrier above)
+    d_fence_after();
+    const uint32_t* tslot = reinterpret_cast<const uint32_t*>(
+        reinterpret_cast<const RoundDesc*>(
+            reinterpret_cast<const uint64_t*>(xs + static_cast<size_t>(16) * P.Dp * 2) + 6) + 2);
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tslot), "r"(32)
+                 : "memory");
+  }
   if (threadIdx.x == 0) stamp(P, 2);
   // (the local and the EP store are separate instantiations of the loop)
   auto combine = [&](auto store) {
@@ -2352,6 +2530,10 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
     P.host_pf_guess = hg;
   }
   P.pf_w1u = static_cast<const uint8_t*>(fb.pf_w1u);
+  P.w1u = static_cast<const uint8_t*>(L->w1u);
+  P.w2u = static_cast<const uint8_t*>(L->w2u);
+  P.w1u_stride = static_cast<size_t>(2 * L->Hp) * L->Dp * 2;
+  P.w2u_stride = static_cast<size_t>(L->Dp) * L->Hp * 2;
   P.pf_w1u_stride = static_cast<size_t>(2 * L->Hp) * L->Dp * 2;
   {
     static const int mb = getenv("OEA_BIG_PF_MB") ? atoi(getenv("OEA_BIG_PF_MB")) : 32;
@@ -2398,10 +2580,11 @@ int ffn_bf16_launch(oea_ctx* ctx, const oea_layer* L, int B, int stride, const F
   if (fb.ep != nullptr && (!fb.fused || fb.route_only))
     return oea_set_error(ctx, OEA_ERR_INVALID_ARGUMENT, "moe_decode_ep: needs the fused path");
   const int mode = fb.route_only ? 3
-                   : fb.dense   ? (fb.ep ? 5 : 2)
+                   : fb.dense   ? (fb.ep ? 5 : fb.umma_dense ? 6 : 2)
                    : fb.fused   ? (fb.ep ? 4 : 1)
                                 : 0;
-  auto kern = mode == 5   ? k_ffn_bf16<5>
+  auto kern = mode == 6   ? k_ffn_bf16<6>
+              : mode == 5 ? k_ffn_bf16<5>
               : mode == 4 ? k_ffn_bf16<4>
               : mode == 3 ? k_ffn_bf16<3>
               : mode == 2 ? k_ffn_bf16<2>

@@ -104,7 +104,7 @@ struct oea_ctx {
   void* route_scratch = nullptr;  // single-launch route accumulators (self-resetting)
   int ffn_mode = 0;
   // dynamic shared memory already allowed per k_ffn_bf16<MODE> on this device
-  int ffn_smem_set[6] = {0, 0, 0, 0, 0, 0};
+  int ffn_smem_set[7] = {0, 0, 0, 0, 0, 0, 0};
   // EP peer tables uploaded so far (device copies; matched by content)
   void* ep_tables = nullptr;
   std::vector<oea_dev::EpPeers> ep_host_tables;
@@ -253,6 +253,7 @@ struct FfnBuffers {
   const oea_dev::EpPeers* ep = nullptr;  // peer-memory EP combine (device table), or null
   int compact_in_kernel = 0;            // route-only: the compaction in the same launch
   const void* pf_w1u = nullptr;         // route-only: the tcgen05 FFN's W1 copy to prefetch (or null)
+  int umma_dense = 0;                   // dense decode on tcgen05 (MODE 6; the layer's UMMA copy)
   void* xg = nullptr;                   // ... and the tcgen05 FFN's gathered rows (or null)
   int xg_rg = 0;
   float* logits = nullptr;              // [B][Np]

@@ -91,3 +91,44 @@ def test_masked_tokens_large_batch(oea):
     rng = np.random.default_rng(8)
     mask = rng.integers(0, 2, size=160).astype(bool)
     run_case(oea, 512, 256, 64, 160, oea.RoutingConfig.vanilla(8), seed=9, mask=mask)
+
+
+_DENSE_OPT_IN = r"""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, sys.argv[1])
+import oracle
+import paper_2511_02237_b200 as oea
+from test_decode_gpu import OUT_TOL, oracle_output, to_bf16_bits
+for D, H, N, B, k0 in ((2048, 768, 128, 16, 4), (512, 256, 32, 1, 2), (1024, 328, 64, 9, 8)):
+    cfg = oea.RoutingConfig.simplified(k0, 8) if k0 < 8 else oea.RoutingConfig.vanilla(8)
+    layer = oea.DeviceMoeLayer(D, H, N, dtype="bf16")
+    layer.init_random(B + k0)
+    x, xbits = to_bf16_bits(oracle.make_random_batch(B, D, 50 + B))
+    xd = torch.from_numpy(xbits.view(np.int16)).view(torch.bfloat16).cuda()
+    out = torch.empty(B, D, device="cuda", dtype=torch.float32)
+    layer.decode(xd, cfg, out)
+    layer.ctx.synchronize()
+    plan = layer.last_plan(B, cfg)
+    want = oracle.route(oracle.softmax_rows(plan["logits"].astype(np.float64)), cfg, None)
+    for i in range(B):
+        assert [int(v) for v in plan["sets"][i, : plan["set_len"][i]]] == want.set_list(i)
+    _, rel = oracle.output_divergence(oracle_output(layer, x, want), out.cpu().numpy().astype(np.float64))
+    assert rel <= OUT_TOL, (D, H, N, B, rel)
+    layer.close()
+print("ok")
+"""
+
+
+def test_dense_tcgen05_opt_in():
+    # OEA_UMMA_DENSE=1 (read once per process, hence the subprocess): the
+    # experimental tcgen05 consumer of the dense decode (MODE 6) vs the oracle
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, OEA_UMMA_DENSE="1")
+    r = subprocess.run([sys.executable, "-c", _DENSE_OPT_IN, here], env=env, cwd=os.path.dirname(here),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]

@@ -25,7 +25,7 @@ buf = np.zeros(LEG + NL * PER, np.uint64)
 L.ctx.check(lib().oea_debug_ffn_trace(L.ctx.h, buf.ctypes.data_as(C.c_void_p), buf.size))
 regs = buf[LEG:].reshape(NL, PER).astype(np.int64)
 names = {0: "start", 8: "gemv start", 9: "gemv k-loop done (w0)", 10: "gemv partials in smem", 5: "gemv done", 11: "R1 done", 12: "union polled", 13: "union scan",
-         6: "union known", 7: "R2 + plan (CTA0: gather+compact)", 15: "grid exit"}
+         6: "union known", 1: "R2 + plan rows out", 7: "compaction + row gather done", 15: "grid exit"}
 for r in regs:
     t = r[:148 * 16].reshape(148, 16)
     if t[:, 0].min() <= 0 or t[:, 7].max() <= 0:

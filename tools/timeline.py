@@ -38,6 +38,8 @@ SLOTS = [(0, "start"), (5, "logits published"), (8, "slot8 (dense: logits polled
          (10, "combine barrier"), (2, "combine start"), (15, "combine done")]
 
 for name, cfg in (("oea", oea.RoutingConfig.simplified(K0, 8)), ("vanilla", oea.RoutingConfig.vanilla(8))):
+    for L in layers:  # eager first call (a tcgen05 path's weight copy is made outside capture)
+        L.decode(xs[0], cfg, out)
     chain = os.environ.get("CHAIN", "0") == "1"
     if chain:  # one graph of REPS - 4 calls (PDL edges) + a 4-call warm-up graph
         warm = oea.DeviceMoeLayer.chain_graph([layers[i % 4] for i in range(4)], list(xs[:4]),
