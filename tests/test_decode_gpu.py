@@ -39,10 +39,10 @@ def oracle_output(layer, x, want):
     return oracle.moe_forward(wg, wu, wd, x, sets.astype(np.int32), want.set_len, want.weights)
 
 
-def run_case(oea, D, H, N, B, cfg, seed=1, mask=None, check_logits=True):
+def run_case(oea, D, H, N, B, cfg, seed=1, mask=None, check_logits=True, x_scale=1.0):
     layer = oea.DeviceMoeLayer(D, H, N, dtype="bf16")
     layer.init_random(seed)
-    x, xbits = to_bf16_bits(oracle.make_random_batch(B, D, 1000 + seed))
+    x, xbits = to_bf16_bits(oracle.make_random_batch(B, D, 1000 + seed) * x_scale)
     out = layer.decode_host(xbits, cfg, mask=mask)
     plan = layer.last_plan(B, cfg)
     m8 = None if mask is None else np.asarray(mask, np.uint8)
@@ -90,6 +90,24 @@ def test_decode_modes_small(oea, mode):
            "oea": R.oea(2, 1.0, 4, 10, 4), "simplified": R.simplified(2, 4),
            "strict": R.simplified(2, 4, oea.CapSemantics.PseudocodeStrict)}[mode]
     run_case(oea, 256, 128, 16, 8, cfg, seed=3)
+
+
+@pytest.mark.parametrize("cfg_name,B", [("mass", 16), ("max_p", 16), ("mass", 48), ("both", 16)])
+def test_decode_two_kernel_configs_c1_shape(oea, cfg_name, B):
+    """The configs outside the fused prologue's rank routing (p < 1: the
+    cumulative-mass baseline of routing.cpp:226-268; max_p < N: phase 2
+    limited to the first max_p ranks, :270-303) at the C1 layer shape: the
+    router cluster + FFN pair. Sets bit-exact vs the oracle on the exported
+    logits (p < 1: the fp64 softmax of the fp32 logits on both sides)."""
+    R = oea.RoutingConfig
+    cfg = {"mass": R.oea(4, 0.5, 8, 128, 8), "max_p": R.oea(4, 1.0, 8, 24, 8),
+           "both": R.oea(3, 0.4, 6, 40, 8)}[cfg_name]
+    # x scaled so the softmax is peaked enough for the mass rule to bite
+    plan, _ = run_case(oea, 2048, 768, 128, B, cfg, seed=21 + B, x_scale=2.0 if cfg.p < 1.0 else 1.0)
+    want = oracle.route(oracle.softmax_rows(plan["logits"].astype(np.float64)), cfg, None)
+    assert np.array_equal(plan["phase1_n"], want.n)
+    if cfg.p < 1.0:  # the mass rule really cut some baselines below k0
+        assert int(want.n.min()) < cfg.k0
 
 
 def test_decode_odd_dims_and_mask(oea):
