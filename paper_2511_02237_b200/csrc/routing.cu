@@ -505,15 +505,16 @@ __device__ __forceinline__ unsigned group_mask() {
 // routing.cpp:17-31) by the last CTA to finish. The union / load / error
 // accumulators live in a self-resetting scratch block (the last CTA clears
 // it), so no memset precedes the launch.
+constexpr int kLoadCopies = 8;  // CTA c adds its loads into copy c % 8 (8x fewer same-line atomics)
 struct RouteScratch {
-  int32_t loads[128];
+  int32_t loads[kLoadCopies][128];
   uint32_t uni[4];
   int32_t bar;   // CTAs past phase 1
   int32_t done;  // CTAs finished
   int32_t err;   // INT_MAX - first degenerate token (0 = none)
   int32_t pad;
 };
-static_assert(sizeof(RouteScratch) <= 1024, "the context allocates 1 KiB of route scratch");
+static_assert(sizeof(RouteScratch) <= 8192, "the context allocates 8 KiB of route scratch");
 
 // m picks (ranked after (pk, pe), eligible by elig_mask) in rank order; pick
 // r lands in thread r % TPT's slot r / TPT (expert, raw score). Returns the
@@ -638,7 +639,10 @@ __global__ void __launch_bounds__(kGroupThreads)
       trace[blockIdx.x * 8 + sl] = t;
     }
   };
-  stamp(0);
+  // programmatic dependent: the next launch in the stream may get resident
+  // now; this grid's global reads (scores, the scratch the previous route
+  // reset) wait for its predecessor
+  pdl_launch_dependents();
   __shared__ int s_loads[128];
   __shared__ uint32_t s_union[4];
   __shared__ int s_err;
@@ -646,6 +650,8 @@ __global__ void __launch_bounds__(kGroupThreads)
   for (int e = threadIdx.x; e < 128; e += blockDim.x) s_loads[e] = 0;
   if (threadIdx.x < 4) s_union[threadIdx.x] = 0u;
   if (threadIdx.x == 0) s_err = INT_MAX;
+  pdl_wait();
+  stamp(0);
   __syncthreads();
   const int q = threadIdx.x & (TPT - 1);
   const int i = blockIdx.x * (kGroupThreads / TPT) + static_cast<int>(threadIdx.x) / TPT;
@@ -700,6 +706,7 @@ __global__ void __launch_bounds__(kGroupThreads)
     // phase 2: union members ranked after the base set, until the cap: the
     // lists' remaining entries all rank after the base (it is the top n);
     // drop the non-members and sort again
+    bool cut = false;
     {
       uint32_t uw[4];
 #pragma unroll
@@ -708,10 +715,14 @@ __global__ void __launch_bounds__(kGroupThreads)
       for (int j = 0; j < EPT; ++j) {
         const int e = id[j];
         const uint32_t word = e < 32 ? uw[0] : e < 64 ? uw[1] : e < 96 ? uw[2] : uw[3];
-        if (n == 0 || !((word >> (e & 31)) & 1u)) k[j] = 0ull;
+        if (k[j] != 0ull && (n == 0 || !((word >> (e & 31)) & 1u))) {
+          k[j] = 0ull;
+          cut = true;
+        }
       }
     }
-    lane_sort_desc<EPT>(k, id);
+    // (a full union, as at large B, drops nothing: the lists stay sorted)
+    if (__any_sync(0xffffffffu, cut)) lane_sort_desc<EPT>(k, id);
     const int m = max(0, cfg.limit - min(cfg.k0, N));
     const int got = group_pick_sorted<TPT, EPT, U>(k, id, q, m, n, ex, sk);
     len = real ? n + min(got, max(0, cfg.limit - n)) : 0;
@@ -745,13 +756,13 @@ __global__ void __launch_bounds__(kGroupThreads)
       }
       const unsigned gm = group_mask<TPT>();
       double mass = 0.0;
+#pragma unroll 1
+      for (int r = 0; r < len; ++r) {  // (len uniform over the group)
+        double v = sc[0];
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int qq = 0; qq < TPT; ++qq) {
-          const double x = __shfl_sync(gm, sc[u], qq, TPT);
-          if (u * TPT + qq < len) mass = __dadd_rn(mass, x);
-        }
+        for (int u = 1; u < U; ++u) v = r / TPT == u ? sc[u] : v;
+        mass = __dadd_rn(mass, __shfl_sync(gm, v, r % TPT, TPT));
+      }
       if (q == 0 && !(mass > 1e-12)) atomicMin(&s_err, i);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -768,7 +779,7 @@ __global__ void __launch_bounds__(kGroupThreads)
   stamp(4);
   __syncthreads();
   for (int e = threadIdx.x; e < N; e += blockDim.x)
-    if (s_loads[e]) atomicAdd(&scr->loads[e], s_loads[e]);
+    if (s_loads[e]) atomicAdd(&scr->loads[blockIdx.x % kLoadCopies][e], s_loads[e]);
   if (set_mode == 1 && threadIdx.x < 4 && s_union[threadIdx.x])
     atomicOr(&scr->uni[threadIdx.x], s_union[threadIdx.x]);
   if (threadIdx.x == 0 && s_err != INT_MAX) atomicMax(&scr->err, INT_MAX - s_err);
@@ -789,16 +800,26 @@ __global__ void __launch_bounds__(kGroupThreads)
   int32_t l[4];
   uint32_t uw = 0u;
   long long part = 0;
+  // (every global read of the aggregate issued at once: one round trip)
+  if (lane < 4) uw = __ldcg(&scr->uni[lane]);
+  const int ev = __ldcg(&scr->err);
 #pragma unroll
   for (int w = 0; w < 4; ++w) {
     const int e = 32 * w + lane;
-    l[w] = e < N ? __ldcg(&scr->loads[e]) : 0;
+    l[w] = 0;
+#pragma unroll
+    for (int c = 0; c < kLoadCopies; ++c) l[w] += e < N ? __ldcg(&scr->loads[c][e]) : 0;
+  }
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const int e = 32 * w + lane;
     part += l[w];
     if (e < N && loads_out) loads_out[e] = l[w];
-    scr->loads[e] = 0;
+#pragma unroll
+    for (int c = 0; c < kLoadCopies; ++c) scr->loads[c][e] = 0;
   }
+  stamp(7);
   if (lane < 4) {
-    uw = __ldcg(&scr->uni[lane]);
     if (union_out) union_out[lane] = uw;
     scr->uni[lane] = 0u;
   }
@@ -806,7 +827,6 @@ __global__ void __launch_bounds__(kGroupThreads)
   for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
   if (lane == 0) {
     if (total_load) *total_load = part;
-    const int ev = __ldcg(&scr->err);
     *err_token = ev ? INT_MAX - ev : INT_MAX;
     scr->err = 0;
     scr->bar = 0;
@@ -954,17 +974,22 @@ int route_f64_fast_launch(oea_ctx* ctx, const Cfg& cfg, int B, int N, const Rout
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_group_route<TPT, BT>, BT, 0);
       max_blocks = per_sm * ctx->num_sms;
     }
+    // (OEA_ROUTE_PDL=1: launched as a programmatic dependent; measured slower
+    // back to back, 15.8 -> 21.2 us: the next grid's CTAs sit on the SMs)
+    static const bool route_pdl = getenv("OEA_ROUTE_PDL") != nullptr && atoi(getenv("OEA_ROUTE_PDL")) != 0;
     if (grid <= max_blocks) {
       const int do_weights = (rb.weights != nullptr || rb.weights_f32 != nullptr) ? 1 : 0;
       cudaLaunchConfig_t c = {};
       c.gridDim = dim3(grid);
       c.blockDim = dim3(BT);
       c.stream = s;
-      cudaLaunchAttribute a[1];
+      cudaLaunchAttribute a[2];
       a[0].id = cudaLaunchAttributeCooperative;
       a[0].val.cooperative = 1;
+      a[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      a[1].val.programmaticStreamSerializationAllowed = 1;
       c.attrs = a;
-      c.numAttrs = 1;
+      c.numAttrs = route_pdl ? 2 : 1;
       OEA_CUDA_TRY(ctx, cudaLaunchKernelEx(&c, k_group_route<TPT, BT>, cfg, B, N, set_mode, do_weights,
                                            rb.scores, rb.mask, rb.sets, rb.set_len, rb.t, rb.n,
                                            rb.weights, rb.weights_f32,
