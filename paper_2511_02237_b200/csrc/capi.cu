@@ -398,9 +398,16 @@ int blocks_for(size_t n) {
 // The fused single-launch decode covers B <= 64, N <= 128, D % 8 == 0 and
 // p == 1 with a full piggyback window (max_p = N); expert-parallel shards run
 // only on it.
+static bool rank_routing_ok(const oea_layer* L, const oea_routing_cfg& rc) {
+  static const bool mass = getenv("OEA_FUSED_MASS") == nullptr || atoi(getenv("OEA_FUSED_MASS")) != 0;
+  return mass || rc.mode == OEA_MODE_VANILLA || (rc.p == 1.0 && rc.max_p >= L->N);
+}
+
 bool fused_ok(const oea_layer* L, int B, const oea_routing_cfg& rc) {
+  // (every routing config: p < 1 and max_p < N are part of the rank routing;
+  // OEA_FUSED_MASS=0 sends them to the router cluster + FFN pair instead)
   return B <= kRouterTokChunk && L->router_t != nullptr && L->Np <= 128 && (L->D & 7) == 0 &&
-         (rc.mode == OEA_MODE_VANILLA || (rc.p == 1.0 && rc.max_p >= L->N)) &&
+         rank_routing_ok(L, rc) &&
          oea_host::ffn_bf16_smem_bytes() + oea_host::ffn_btile_bytes() +
                  oea_host::ffn_route_smem_bytes(B, L->Np, stride_of(rc)) <= 227 * 1024;
 }
@@ -471,7 +478,7 @@ int decode_bf16(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* x, const u
                           (shard || getenv("OEA_TWO_KERNEL") == nullptr);
   const bool big_shape = part == 0 && !shard && B > 16 && B <= kMaxFusedB &&
                          L->router_t != nullptr && L->Np <= 128 && L->D == L->Dp &&
-                         (rc.mode == OEA_MODE_VANILLA || (rc.p == 1.0 && rc.max_p >= L->N)) &&
+                         rank_routing_ok(L, rc) &&
                          getenv("OEA_TWO_KERNEL") == nullptr &&
                          oea_host::ffn_bf16_smem_bytes() +
                                  oea_host::ffn_route_smem_bytes(B, L->Np, stride) <= 227 * 1024;

@@ -596,7 +596,7 @@ __device__ __forceinline__ void dispatch_w2_dense(int nbk, const FfnParams& P, c
 // ---------------------------------------------------------------------------
 struct RouteSmem {
   size_t keys, ukeys, uni, sets, e, len, n, mx, loads, tokbits, active, eslot, rowb, rows, rtok,
-      rslot, red, misc, lgp, total;
+      rslot, red, misc, lgp, thr, pe, total;
 };
 
 __host__ __device__ inline RouteSmem route_smem_layout(int B, int Np, int stride) {
@@ -629,6 +629,10 @@ __host__ __device__ inline RouteSmem route_smem_layout(int B, int Np, int stride
   L.red = take((kFfnThreads / 32) * 16 * 4);
   L.lgp = take(64 * 4);  // this CTA's expert's logits (first 64 tokens): the prefetch guess
   L.misc = take(8 * 4);
+  L.thr = take(static_cast<size_t>(B) * 8);  // max_p < N: (key, expert) at rank max_p - 1
+  // p < 1: the base candidates' exp(l - max) by rank, 4 warp partials of the
+  // softmax denominator, the resulting n, the phase-2 placed count
+  L.pe = take(static_cast<size_t>(Np) * 8 + 4 * 8 + 16);
   L.total = o;
   return L;
 }
@@ -914,7 +918,44 @@ __device__ __forceinline__ void rank_phase1(const FfnParams& P, int t, uint8_t* 
     const uint32_t kf = keys[f];
     rank += (kf > key) | ((kf == key) & (f < e));
   }
-  const int n = masked ? 0 : min(P.cfg.mode == OEA_MODE_VANILLA ? P.cfg.k : P.cfg.k0, N);
+  int n = masked ? 0 : min(P.cfg.mode == OEA_MODE_VANILLA ? P.cfg.k : P.cfg.k0, N);
+  if (P.cfg.mode != OEA_MODE_VANILLA && P.cfg.max_p < N && key != 0u && rank == P.cfg.max_p - 1) {
+    uint32_t* thr = reinterpret_cast<uint32_t*>(rs + L.thr) + 2 * t;
+    thr[0] = key;
+    thr[1] = static_cast<uint32_t>(e);
+  }
+  if (P.cfg.mode != OEA_MODE_VANILLA && P.cfg.p < 1.0 && n > 0) {
+    // mass rule (routing.cpp:243-257): t_i = the first rank whose cumulative
+    // softmax mass reaches p, n = min(k0, t_i); fp64 softmax of the fp32
+    // logits as the router cluster computes it (tok_phase1)
+    double* pe = reinterpret_cast<double*>(rs + L.pe);
+    double* zp = pe + P.Np;
+    int* nn = reinterpret_cast<int*>(zp + 4);
+    if (key != 0u && rank == 0) mx[t] = l;
+    asm volatile("bar.sync 3, 128;" ::: "memory");
+    const double ed = key != 0u ? exp(static_cast<double>(l) - static_cast<double>(mx[t])) : 0.0;
+    double z = ed;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) z += __shfl_xor_sync(kFull, z, off);
+    if ((e & 31) == 0) zp[e >> 5] = z;
+    if (key != 0u && rank < n) pe[rank] = ed;
+    asm volatile("bar.sync 3, 128;" ::: "memory");
+    if (e == 0) {
+      const double zz = (zp[0] + zp[1]) + (zp[2] + zp[3]);
+      double cum = 0.0;
+      int m = n;
+      for (int j = 0; j < n; ++j) {
+        cum = __dadd_rn(cum, pe[j] / zz);
+        if (cum >= P.cfg.p) {
+          m = j + 1;
+          break;
+        }
+      }
+      *nn = m;
+    }
+    asm volatile("bar.sync 3, 128;" ::: "memory");
+    n = *nn;
+  }
   const bool base = key != 0u && rank < n;
   if (base) sets[rank] = e;
   const unsigned bw = __ballot_sync(kFull, base);  // warp w holds experts 32w..32w+31
@@ -939,11 +980,17 @@ __device__ __forceinline__ void rank_phase2(const FfnParams& P, int t, uint8_t* 
   const int n = reinterpret_cast<const int*>(rs + L.n)[t];
   const bool piggy = !masked && (P.cfg.mode == OEA_MODE_OEA || P.cfg.mode == OEA_MODE_SIMPLIFIED);
   const int cap = max(n, P.cfg.limit);
-  const int len = masked ? 0 : piggy ? min(T, cap) : n;
+  // max_p < N: members ranked at or after max_p (overall) are not candidates;
+  // they are a suffix of the members' rank order, so `placed` counts the rest
+  const bool lim = piggy && P.cfg.max_p < N;
+  const uint32_t* thr = reinterpret_cast<const uint32_t*>(rs + L.thr) + 2 * t;
+  int* placed = reinterpret_cast<int*>(reinterpret_cast<double*>(rs + L.pe) + P.Np + 4) + 1;
+  int len = masked ? 0 : piggy ? min(T, cap) : n;
   if (piggy) {
     // the union members' keys, compacted in ascending expert order (member i
     // is the i-th set bit): union ranks then cost T compares, not N
     uint32_t* ukeys = reinterpret_cast<uint32_t*>(rs + L.ukeys);
+    if (gt == 0 && lim) *placed = 0;
     if (gt < 32) {
       const uint32_t below = lanemask_lt();
       int ub = 0;
@@ -968,21 +1015,28 @@ __device__ __forceinline__ void rank_phase2(const FfnParams& P, int t, uint8_t* 
       }
       return c;
     };
-    auto place = [&](int i, uint32_t key, int urank) {
-      if (urank >= n && urank < len) {
-        // expert index of member i: the i-th set bit of the union
-        int e = 0, r = i;
+    auto member_expert = [&](int i) {  // expert index of member i: the i-th set bit of the union
+      int e = 0, r = i;
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          const int c = __popc(uni[w]);
-          if (r < c) {
-            uint32_t m = uni[w];
-            for (int k = 0; k < r; ++k) m &= m - 1;  // drop the r lowest set bits
-            e = 32 * w + __ffs(m) - 1;
-            break;
-          }
-          r -= c;
+      for (int w = 0; w < 4; ++w) {
+        const int c = __popc(uni[w]);
+        if (r < c) {
+          uint32_t m = uni[w];
+          for (int k = 0; k < r; ++k) m &= m - 1;  // drop the r lowest set bits
+          e = 32 * w + __ffs(m) - 1;
+          break;
         }
+        r -= c;
+      }
+      return e;
+    };
+    auto place = [&](int i, uint32_t key, int urank) {
+      bool ok = urank >= n && urank < len;
+      if (lim && ok)  // overall rank < max_p: ranks before (or is) the rank max_p - 1 expert
+        ok = key != thr[0] ? key > thr[0] : member_expert(i) <= static_cast<int>(thr[1]);
+      if (ok) {
+        const int e = member_expert(i);
+        if (lim) atomicAdd(placed, 1);
         sets[urank] = e;
         se[urank] = expf(key32_to_logit(key) - rowmax);
       }
@@ -1006,6 +1060,7 @@ __device__ __forceinline__ void rank_phase2(const FfnParams& P, int t, uint8_t* 
     }
   }
   sync();
+  if (lim && !masked) len = n + *placed;
   if (gt == 0) {
     float mass = 0.0f;  // sequential fp32 mass in set order
     for (int j = 0; j < len; ++j) mass += se[j];

@@ -94,11 +94,12 @@ def test_decode_modes_small(oea, mode):
 
 @pytest.mark.parametrize("cfg_name,B", [("mass", 16), ("max_p", 16), ("mass", 48), ("both", 16)])
 def test_decode_two_kernel_configs_c1_shape(oea, cfg_name, B):
-    """The configs outside the fused prologue's rank routing (p < 1: the
-    cumulative-mass baseline of routing.cpp:226-268; max_p < N: phase 2
-    limited to the first max_p ranks, :270-303) at the C1 layer shape: the
-    router cluster + FFN pair. Sets bit-exact vs the oracle on the exported
-    logits (p < 1: the fp64 softmax of the fp32 logits on both sides)."""
+    """p < 1 (the cumulative-mass baseline of routing.cpp:226-268) and
+    max_p < N (phase 2 limited to the first max_p ranks, :270-303) at the C1
+    layer shape, through the fused rank routing (B = 16: the single launch;
+    B = 48: the route-only launch + tcgen05 FFN). Sets bit-exact vs the
+    oracle on the exported logits (p < 1: the fp64 softmax of the fp32
+    logits on both sides), phase-1 baseline sizes equal."""
     R = oea.RoutingConfig
     cfg = {"mass": R.oea(4, 0.5, 8, 128, 8), "max_p": R.oea(4, 1.0, 8, 24, 8),
            "both": R.oea(3, 0.4, 6, 40, 8)}[cfg_name]
@@ -108,6 +109,17 @@ def test_decode_two_kernel_configs_c1_shape(oea, cfg_name, B):
     assert np.array_equal(plan["phase1_n"], want.n)
     if cfg.p < 1.0:  # the mass rule really cut some baselines below k0
         assert int(want.n.min()) < cfg.k0
+
+
+@pytest.mark.parametrize("cfg_name", ["mass", "max_p"])
+def test_decode_router_cluster_configs(oea, cfg_name):
+    """N > 128 experts: the router cluster + FFN pair (k_router_fused's
+    distributed warp-sort routing) with p < 1 and max_p < N."""
+    R = oea.RoutingConfig
+    cfg = {"mass": R.oea(3, 0.5, 8, 160, 8), "max_p": R.oea(3, 1.0, 8, 20, 8)}[cfg_name]
+    plan, _ = run_case(oea, 512, 256, 160, 16, cfg, seed=31, x_scale=2.0 if cfg.p < 1.0 else 1.0)
+    want = oracle.route(oracle.softmax_rows(plan["logits"].astype(np.float64)), cfg, None)
+    assert np.array_equal(plan["phase1_n"], want.n)
 
 
 def test_decode_odd_dims_and_mask(oea):

@@ -32,6 +32,10 @@ for B, k0 in SETS[os.environ.get("AB_SET", "small")]:
     xs = torch.randn(W + K, B, D, device="cuda", generator=gen).to(torch.bfloat16)
     out = torch.empty(B, D, device="cuda", dtype=torch.float32)
     cfg = oea.RoutingConfig.simplified(k0, 8) if k0 < 8 else oea.RoutingConfig.vanilla(8)
+    if os.environ.get("AB_CFG") == "mass":  # p < 1 (x scaled so the mass rule cuts)
+        cfg, xs = oea.RoutingConfig.oea(k0, 0.5, 8, 128, 8), (xs.float() * 2).to(torch.bfloat16)
+    elif os.environ.get("AB_CFG") == "maxp":
+        cfg = oea.RoutingConfig.oea(k0, 1.0, 8, 24, 8)
     us, _ = bench.time_chain(torch, stream, layers, xs, cfg, out, W, K, ctx)
     Ts, _ = bench.plan_stats(layers, xs, cfg, out, B, range(W, W + K), ctx)
     res.append(f"B{B}k{k0}: {us:6.2f}us T={np.mean(Ts):5.1f}")
