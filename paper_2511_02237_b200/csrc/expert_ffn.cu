@@ -1379,8 +1379,8 @@ __device__ __forceinline__ void route_phase2_plan(const FfnParams& P, uint8_t* r
 // (router_fused.cu compact_plan) distributed over the grid in the same
 // launch. Once every token's plan row is out (claims[0] = B), CTA e takes
 // expert e: its tokens in token order (a ballot scan of the batch's sets) and
-// its load, published in x_loads (claims[1] counts the experts); then each
-// CTA places its expert's token groups (<= 64 rows, the last padded to 8) and
+// its load (x_loads); the same scan counts every expert's load in shared
+// memory, so each CTA places its expert's token groups (<= 64 rows, the last padded to 8) and
 // rows after the groups / rows of the experts before it (ascending experts =
 // the active-union order), writes row -> (token, slot) and, for the tcgen05
 // FFN, the token rows in the CM layout (xg). CTA 0 writes the header and the
@@ -1394,6 +1394,8 @@ __device__ __forceinline__ void route_compact_dist(const FfnParams& P, uint8_t* 
   int* tl_slot = reinterpret_cast<int*>(rs + L.rslot);
   int* wcnt = reinterpret_cast<int*>(rs + L.red);      // [NWARP]
   int* misc = reinterpret_cast<int*>(rs + L.misc);
+  int* cnt = reinterpret_cast<int*>(rs + L.loads);     // [N] every expert's load
+  for (int i = tid; i < N; i += NT) cnt[i] = 0;
   if (tid == 0)
     while (ld_acquire_gpu(claims) < B) __nanosleep(32);
   __syncthreads();
@@ -1404,13 +1406,18 @@ __device__ __forceinline__ void route_compact_dist(const FfnParams& P, uint8_t* 
     for (int t0 = 0; t0 < B; t0 += NT) {
       const int t = t0 + tid;
       // (the exported rows are -1 past the set length: the whole row's loads
-      // go out at once, no length round trip, no early exit)
+      // go out at once, no length round trip, no early exit); every CTA
+      // counts every expert's load from the same scan, so the group / row
+      // bases need no second grid-wide exchange
       int slot = -1;
       if (t < B) {
         const int32_t* row = P.x_sets + static_cast<size_t>(t) * stride;
 #pragma unroll 8
-        for (int j = 0; j < stride; ++j)
-          if (__ldcg(row + j) == e && slot < 0) slot = j;
+        for (int j = 0; j < stride; ++j) {
+          const int v = __ldcg(row + j);
+          if (v >= 0) atomicAdd(&cnt[v], 1);
+          if (v == e && slot < 0) slot = j;
+        }
       }
       const unsigned m = __ballot_sync(kFull, slot >= 0);
       if (lane == 0) wcnt[warp] = __popc(m);
@@ -1429,19 +1436,14 @@ __device__ __forceinline__ void route_compact_dist(const FfnParams& P, uint8_t* 
       __syncthreads();
       load += tot;
     }
-    if (tid == 0) {
-      P.x_loads[e] = load;
-      red_release_gpu_add(claims + 1, 1);  // (after the barrier: cumulative)
-    }
+    if (tid == 0) P.x_loads[e] = load;
   }
-  if (tid == 0)
-    while (ld_acquire_gpu(claims + 1) < N) __nanosleep(32);
   __syncthreads();
   // groups / rows of the experts before e (k_compact's formulas)
   if (warp == 0) {
     int gb = 0, rb = 0, ng_all = 0, nr_all = 0, act = 0, tl = 0;
     for (int i = lane; i < N; i += 32) {
-      const int m = __ldcg(P.x_loads + i);
+      const int m = cnt[i];
       const int ng = (m + kTokGroup - 1) / kTokGroup;
       const int nr = m > 0 ? (m / kTokGroup) * kTokGroup + ((m % kTokGroup) + 7) / 8 * 8 : 0;
       if (i < e) {
