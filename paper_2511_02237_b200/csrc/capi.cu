@@ -733,8 +733,8 @@ int oea_ctx_create(int32_t device, oea_ctx_t* out) {
   ctx->device = device;
   ctx->num_sms = prop.multiProcessorCount;
   // (zeroed once; the single-launch route resets it at every launch's end)
-  if (cudaMalloc(&ctx->route_scratch, 8192) == cudaSuccess)
-    cudaMemset(ctx->route_scratch, 0, 8192);
+  if (cudaMalloc(&ctx->route_scratch, oea_dev::kRouteScratchBytes) == cudaSuccess)
+    cudaMemset(ctx->route_scratch, 0, oea_dev::kRouteScratchBytes);
   else
     ctx->route_scratch = nullptr;
   e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);

@@ -80,6 +80,10 @@ struct FfnHeader {
   int pad[3];
 };
 
+// Single-launch route scratch (routing.cu, RouteScratch): a 32-byte header
+// (the launch epoch) + 4 tagged union words per CTA.
+constexpr size_t kRouteScratchBytes = 64 * 1024;
+
 }  // namespace oea_dev
 
 // ---------------------------------------------------------------------------
@@ -101,7 +105,7 @@ struct oea_ctx {
   int last_B = 0, last_N = 0, last_stride = 0, last_kind = 0;  // kind 1 = fused bf16, 2 = f64 route
   // Debug instrumentation of the FFN (env OEA_FFN_TRACE=1 / OEA_FFN_MODE=n).
   unsigned long long* ffn_trace = nullptr;
-  void* route_scratch = nullptr;  // single-launch route accumulators (self-resetting)
+  void* route_scratch = nullptr;  // single-launch route: epoch + per-CTA tagged union words
   int ffn_mode = 0;
   // dynamic shared memory already allowed per k_ffn_bf16<MODE> on this device
   int ffn_smem_set[7] = {0, 0, 0, 0, 0, 0, 0};

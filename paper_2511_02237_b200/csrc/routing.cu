@@ -19,10 +19,6 @@
 // the reference's order (no FMA contraction is possible: adds and divides only).
 #include <climits>
 
-#ifndef OEA_ROUTE_TPT
-#define OEA_ROUTE_TPT 16
-#endif
-
 #include "oea_device.cuh"
 #include "oea_internal.cuh"
 
@@ -275,18 +271,37 @@ __global__ void k_union_from_list(const int32_t* __restrict__ list, const int co
 // ---------------------------------------------------------------------------
 template <int E>
 __device__ __forceinline__ void lane_sort_desc(uint64_t (&k)[E], int (&id)[E]) {
+  if constexpr (E == 8) {
+    // optimal 8-input network (19 compare-exchanges, depth 6) instead of the
+    // 28 of the bubble network below
+    constexpr int net[19][2] = {{0, 2}, {1, 3}, {4, 6}, {5, 7}, {0, 4}, {1, 5}, {2, 6},
+                                {3, 7}, {0, 1}, {2, 3}, {4, 5}, {6, 7}, {2, 4}, {3, 5},
+                                {1, 4}, {3, 6}, {1, 2}, {3, 4}, {5, 6}};
 #pragma unroll
-  for (int a = 0; a < E; ++a)
+    for (int c = 0; c < 19; ++c) {
+      const int a = net[c][0], b = net[c][1];
+      const bool sw = ranks_before(k[b], id[b], k[a], id[a]);
+      const uint64_t ka = k[a], kb = k[b];
+      const int ia = id[a], ib = id[b];
+      k[a] = sw ? kb : ka;
+      k[b] = sw ? ka : kb;
+      id[a] = sw ? ib : ia;
+      id[b] = sw ? ia : ib;
+    }
+  } else {
 #pragma unroll
-    for (int b = E - 1; b > a; --b)
-      if (ranks_before(k[b], id[b], k[b - 1], id[b - 1])) {
-        const uint64_t tk = k[b];
-        k[b] = k[b - 1];
-        k[b - 1] = tk;
-        const int ti = id[b];
-        id[b] = id[b - 1];
-        id[b - 1] = ti;
-      }
+    for (int a = 0; a < E; ++a)
+#pragma unroll
+      for (int b = E - 1; b > a; --b)
+        if (ranks_before(k[b], id[b], k[b - 1], id[b - 1])) {
+          const uint64_t tk = k[b];
+          k[b] = k[b - 1];
+          k[b - 1] = tk;
+          const int ti = id[b];
+          id[b] = id[b - 1];
+          id[b - 1] = ti;
+        }
+  }
 }
 
 // Best (key desc, id asc) over the warp, in every lane.
@@ -501,20 +516,25 @@ __device__ __forceinline__ unsigned group_mask() {
 // after the picks kept in registers (its keys and raw scores; each pick's
 // expert and score round robin over the group: pick r in thread r % TPT,
 // slot r / TPT), so the only global round trip is the score load; one grid
-// barrier for the batch union (set_mode 2); the aggregates (fill_aggregates,
-// routing.cpp:17-31) by the last CTA to finish. The union / load / error
-// accumulators live in a self-resetting scratch block (the last CTA clears
-// it), so no memset precedes the launch.
-constexpr int kLoadCopies = 8;  // CTA c adds its loads into copy c % 8 (8x fewer same-line atomics)
+// exchange for the batch union: CTA c stores its 4 pick-bitmap words as
+// epoch-tagged words {tag:32 | bits:32} in its own slot, every CTA polls all
+// slots until the tags are this launch's (no counter, no fence round trip,
+// no reset: the next launch has another tag). The aggregates
+// (fill_aggregates, routing.cpp:17-31) need no second grid-wide step: the
+// experts with a load are the union of the phase-1 picks (every base-set
+// member stays in its token's set, phase 2 only adds union members;
+// vanilla: the picks are the sets), so CTA 0 writes the union exports right
+// after the exchange, and the per-expert loads / total load / first
+// degenerate token are atomics into the outputs, which CTA 0 clears before
+// it publishes its words (release). CTA 0 advances the epoch once every
+// CTA's words are in (every CTA read it before). No memsets precede the
+// launch, no CTA waits at the end.
 struct RouteScratch {
-  int32_t loads[kLoadCopies][128];
-  uint32_t uni[4];
-  int32_t bar;   // CTAs past phase 1
-  int32_t done;  // CTAs finished
-  int32_t err;   // INT_MAX - first degenerate token (0 = none)
-  int32_t pad;
+  int32_t epoch;  // launches so far (tag = (epoch & 0x7fffffff) + 1, never 0)
+  int32_t pad[7];
+  unsigned long long words[1];  // [grid][4] tagged union words
 };
-static_assert(sizeof(RouteScratch) <= 8192, "the context allocates 8 KiB of route scratch");
+constexpr int kRouteMaxCtas = static_cast<int>((kRouteScratchBytes - 32) / 32);
 
 // m picks (ranked after (pk, pe), eligible by elig_mask) in rank order; pick
 // r lands in thread r % TPT's slot r / TPT (expert, raw score). Returns the
@@ -556,13 +576,13 @@ __device__ __forceinline__ int group_pick_regs(const uint64_t (&k)[EPT], uint32_
     }
     if (bk != 0ull) {
       const int slot = at + got;
-      if (q == slot % TPT) {
+      // (selects, not an indexed store: ex / sk stay in registers)
+      const bool mine = q == slot % TPT;
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (u == slot / TPT) {
-            ex[u] = be;
-            sk[u] = bk;
-          }
+      for (int u = 0; u < U; ++u) {
+        const bool hit = mine && u == slot / TPT;
+        ex[u] = hit ? be : ex[u];
+        sk[u] = hit ? bk : sk[u];
       }
       ++got;
       pk = bk;
@@ -578,22 +598,46 @@ __device__ __forceinline__ int group_pick_regs(const uint64_t (&k)[EPT], uint32_
 // The same picks from per-thread lists sorted once (lane_sort_desc): a
 // pick's candidate is the thread's head, the owner of the group's best
 // shifts its list, so a pick costs the group reduction only.
-template <int TPT, int EPT, int U>
+// KEYPICK: the group reduces the keys alone (2 shuffles a level instead of
+// 3, a max instead of the (key, index) compare); the best key's head owner
+// is found by a ballot, and only when several heads share that key (an
+// exact tie, rare) does the warp reduce the indices too.
+template <int TPT, int EPT, int U, bool KEYPICK = false>
 __device__ __forceinline__ int group_pick_sorted(uint64_t (&k)[EPT], int (&id)[EPT], int q, int m,
-                                                 int at, int (&ex)[U], uint64_t (&sk)[U]) {
+                                                 int at, int (&ex)[U], uint64_t (&sk)[U],
+                                                 uint64_t& pk, int& pe, bool track = true) {
   const unsigned gm = 0xffffffffu;  // (m uniform over the warp: converged)
   int got = 0;
 #pragma unroll 1
   for (int r = 0; r < m; ++r) {
     uint64_t bk = k[0];
-    int be = k[0] != 0ull ? id[0] : 0x7fffffff;
+    int be;
+    if constexpr (KEYPICK) {
 #pragma unroll
-    for (int off = 1; off < TPT; off <<= 1) {
-      const uint64_t ok = __shfl_xor_sync(gm, bk, off);
-      const int oe = __shfl_xor_sync(gm, be, off);
-      if (ranks_before(ok, static_cast<uint32_t>(oe), bk, static_cast<uint32_t>(be))) {
-        bk = ok;
-        be = oe;
+      for (int off = 1; off < TPT; off <<= 1) {
+        const uint64_t ok = __shfl_xor_sync(gm, bk, off);
+        bk = ok > bk ? ok : bk;
+      }
+      const unsigned grp = group_mask<TPT>();
+      const unsigned heads = __ballot_sync(gm, bk != 0ull && k[0] == bk) & grp;
+      be = __shfl_sync(gm, id[0], heads ? __ffs(heads) - 1 : 0);
+      if (__any_sync(gm, (heads & (heads - 1u)) != 0u)) {
+        // equal best keys at several heads: the lowest index among them
+        int ce = (heads >> (threadIdx.x & 31)) & 1u ? id[0] : 0x7fffffff;
+#pragma unroll
+        for (int off = 1; off < TPT; off <<= 1) ce = min(ce, __shfl_xor_sync(gm, ce, off));
+        if (heads & (heads - 1u)) be = ce;
+      }
+    } else {
+      be = k[0] != 0ull ? id[0] : 0x7fffffff;
+#pragma unroll
+      for (int off = 1; off < TPT; off <<= 1) {
+        const uint64_t ok = __shfl_xor_sync(gm, bk, off);
+        const int oe = __shfl_xor_sync(gm, be, off);
+        if (ranks_before(ok, static_cast<uint32_t>(oe), bk, static_cast<uint32_t>(be))) {
+          bk = ok;
+          be = oe;
+        }
       }
     }
     if (bk == 0ull) continue;  // nothing left (uniform over the group)
@@ -604,21 +648,25 @@ __device__ __forceinline__ int group_pick_sorted(uint64_t (&k)[EPT], int (&id)[E
       id[j] = own ? id[j + 1] : id[j];
     }
     if (own) k[EPT - 1] = 0ull;
+    if (track) {
+      pk = bk;
+      pe = be;
+    }
     const int slot = at + got;
-    if (q == slot % TPT) {
+    // (selects, not an indexed store: ex / sk stay in registers)
+    const bool mine = q == slot % TPT;
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (u == slot / TPT) {
-          ex[u] = be;
-          sk[u] = bk;
-        }
+    for (int u = 0; u < U; ++u) {
+      const bool hit = mine && u == slot / TPT;
+      ex[u] = hit ? be : ex[u];
+      sk[u] = hit ? bk : sk[u];
     }
     ++got;
   }
   return got;
 }
 
-template <int TPT, int kGroupThreads>
+template <int TPT, int kGroupThreads, bool KEYPICK>
 __global__ void __launch_bounds__(kGroupThreads)
     k_group_route(const Cfg cfg, const int B, const int N, const int set_mode, const int do_weights,
                   const double* __restrict__ scores, const uint8_t* __restrict__ mask,
@@ -645,24 +693,42 @@ __global__ void __launch_bounds__(kGroupThreads)
   pdl_launch_dependents();
   __shared__ int s_loads[128];
   __shared__ uint32_t s_union[4];
+  __shared__ uint32_t s_batch[4];
   __shared__ int s_err;
-  __shared__ bool s_last;
+  __shared__ int s_total;
   for (int e = threadIdx.x; e < 128; e += blockDim.x) s_loads[e] = 0;
-  if (threadIdx.x < 4) s_union[threadIdx.x] = 0u;
-  if (threadIdx.x == 0) s_err = INT_MAX;
+  if (threadIdx.x < 4) {
+    s_union[threadIdx.x] = 0u;
+    s_batch[threadIdx.x] = 0u;
+  }
+  if (threadIdx.x == 0) {
+    s_err = INT_MAX;
+    s_total = 0;
+  }
   pdl_wait();
   stamp(0);
-  __syncthreads();
   const int q = threadIdx.x & (TPT - 1);
   const int i = blockIdx.x * (kGroupThreads / TPT) + static_cast<int>(threadIdx.x) / TPT;
   const bool valid = i < B;
   const bool real = valid && (mask == nullptr || mask[i] != 0);
   const double* row = scores + static_cast<size_t>(valid ? i : 0) * N;
+  // every score load of the thread issued before the first use (read-only
+  // path, unconditional addresses): one memory round trip, not EPT
+  double raw[EPT];
+#pragma unroll
+  for (int j = 0; j < EPT; ++j) raw[j] = __ldg(row + min(TPT * j + q, N - 1));
+  const int epoch = __ldcg(&scr->epoch);
+  const uint32_t tag = (static_cast<uint32_t>(epoch) & 0x7fffffffu) + 1u;
+  __syncthreads();
   uint64_t k[EPT];
 #pragma unroll
-  for (int j = 0; j < EPT; ++j) {
-    const int e = TPT * j + q;
-    k[j] = real && e < N ? order_key_f64(__ldcg(row + e)) : 0ull;
+  for (int j = 0; j < EPT; ++j) k[j] = real && TPT * j + q < N ? order_key_f64(raw[j]) : 0ull;
+  if (trace != nullptr) {  // (debug timeline: the keys are in registers)
+    uint64_t any = 0ull;
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) any |= k[j];
+    if (any == 1ull) trace[0] = 0ull;
+    stamp(6);
   }
   int ex[U];
   uint64_t sk[U];  // the picks' keys (the score is recovered from the key)
@@ -677,9 +743,13 @@ __global__ void __launch_bounds__(kGroupThreads)
 #pragma unroll
   for (int j = 0; j < EPT; ++j) id[j] = TPT * j + q;
   lane_sort_desc<EPT>(k, id);
-  const int n = group_pick_sorted<TPT, EPT, U>(k, id, q, want, 0, ex, sk);
+  if (trace != nullptr && k[0] == 1ull) trace[1] = 0ull;
+  stamp(7);
+  uint64_t pk = 0ull;  // the last base pick (phase 2 picks rank after it)
+  int pe = -1;
+  const int n = group_pick_sorted<TPT, EPT, U, KEYPICK>(k, id, q, want, 0, ex, sk, pk, pe);
   stamp(1);
-  if (valid && set_mode != 0) {
+  if (valid) {
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (q + TPT * u < n) atomicOr(&s_union[ex[u] >> 5], 1u << (ex[u] & 31));
@@ -688,59 +758,62 @@ __global__ void __launch_bounds__(kGroupThreads)
     if (t_out) t_out[i] = set_mode == 0 ? 0 : (real ? N : 0);
     if (n_out) n_out[i] = set_mode == 0 ? 0 : n;
   }
+  // the batch union: CTA 0 clears the accumulated outputs, then every CTA
+  // publishes its pick bits as tagged words (CTA 0 with release: its clears
+  // before any CTA's adds)
+  __syncthreads();
+  if (blockIdx.x == 0) {
+    if (loads_out)
+      for (int e = threadIdx.x; e < N; e += blockDim.x) loads_out[e] = 0;
+    if (threadIdx.x == 0) {
+      if (total_load) *total_load = 0;
+      *err_token = INT_MAX;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < 4) {
+    unsigned long long* wp = &scr->words[blockIdx.x * 4 + threadIdx.x];
+    const unsigned long long v = tagged(tag, s_union[threadIdx.x]);
+    if (blockIdx.x == 0)
+      st_release_u64(wp, v);
+    else
+      st_relaxed_u64(wp, v);
+    stamp(2);
+  }
+  // phase 2, speculatively while the other CTAs' words arrive: the next
+  // picks over the whole list (the lists' remaining entries all rank after
+  // the base). They are phase2_piggyback's picks (routing.cpp:270-303)
+  // whenever every one is a union member, checked after the exchange; else
+  // the warp picks again among the members (rare at large B, where the
+  // union is full).
+  const int m = set_mode == 2 ? max(0, cfg.limit - min(cfg.k0, N)) : 0;
   int len = n;
   if (set_mode == 2) {
-    // the batch union: every CTA's base bits, then a grid barrier
-    __syncthreads();
-    if (threadIdx.x < 4 && s_union[threadIdx.x]) atomicOr(&scr->uni[threadIdx.x], s_union[threadIdx.x]);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(&scr->bar, 1);
-      stamp(2);
-      while (ld_acquire_gpu(&scr->bar) < static_cast<int>(gridDim.x)) {
-      }
-    }
-    __syncthreads();
-    stamp(3);
-    // phase 2: union members ranked after the base set, until the cap: the
-    // lists' remaining entries all rank after the base (it is the top n);
-    // drop the non-members and sort again
-    bool cut = false;
-    {
-      uint32_t uw[4];
-#pragma unroll
-      for (int w = 0; w < 4; ++w) uw[w] = __ldcg(&scr->uni[w]);
-#pragma unroll
-      for (int j = 0; j < EPT; ++j) {
-        const int e = id[j];
-        const uint32_t word = e < 32 ? uw[0] : e < 64 ? uw[1] : e < 96 ? uw[2] : uw[3];
-        if (k[j] != 0ull && (n == 0 || !((word >> (e & 31)) & 1u))) {
-          k[j] = 0ull;
-          cut = true;
-        }
-      }
-    }
-    // (a full union, as at large B, drops nothing: the lists stay sorted)
-    if (__any_sync(0xffffffffu, cut)) lane_sort_desc<EPT>(k, id);
-    const int m = max(0, cfg.limit - min(cfg.k0, N));
-    const int got = group_pick_sorted<TPT, EPT, U>(k, id, q, m, n, ex, sk);
+    const int got = group_pick_sorted<TPT, EPT, U, KEYPICK>(k, id, q, m, n, ex, sk, pk, pe, false);
     len = real ? n + min(got, max(0, cfg.limit - n)) : 0;
   }
-  if (valid) {
-    // the set, its loads and weights (renormalize_weights, routing.cpp:33-49:
-    // sequential fp64 mass in set order, through group shuffles)
-    const int stride = cfg.stride;
-    int32_t* srow = sets + static_cast<size_t>(i) * stride;
+  const int stride = cfg.stride;
+  int32_t* srow = sets + static_cast<size_t>(valid ? i : 0) * stride;
+  // the set, its length, loads and weights (renormalize_weights,
+  // routing.cpp:33-49: sequential fp64 mass in set order, through group
+  // shuffles); returns whether the mass is degenerate. sign = -1 takes the
+  // set's slots from `from` on back out (a speculative set replaced).
+  auto count = [&](int from, int sign) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int r = q + TPT * u;
-      if (r < len) {
-        srow[r] = ex[u];
-        atomicAdd(&s_loads[ex[u]], 1);
-      }
+      if (r >= from && r < len) atomicAdd(&s_loads[ex[u]], sign);
     }
-    for (int j = len + q; j < stride; j += TPT) {
+    if (q == 0 && len > from) atomicAdd(&s_total, sign * (len - from));
+  };
+  auto emit = [&](int from) -> bool {
+    bool bad = false;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int r = q + TPT * u;
+      if (r >= from && r < len) srow[r] = ex[u];
+    }
+    for (int j = max(len, from) + q; j < stride; j += TPT) {
       srow[j] = -1;
       if (weights) weights[static_cast<size_t>(i) * stride + j] = 0.0;
       if (weights_f32) weights_f32[static_cast<size_t>(i) * stride + j] = 0.0f;
@@ -752,7 +825,7 @@ __global__ void __launch_bounds__(kGroupThreads)
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         sc[u] = key_to_f64(sk[u]);
-        if (q + TPT * u < len && sk[u] == 0x8000000000000000ull) sc[u] = __ldcg(row + ex[u]);
+        if (q + TPT * u < len && sk[u] == 0x8000000000000000ull) sc[u] = __ldg(row + ex[u]);
       }
       const unsigned gm = group_mask<TPT>();
       double mass = 0.0;
@@ -763,7 +836,7 @@ __global__ void __launch_bounds__(kGroupThreads)
         for (int u = 1; u < U; ++u) v = r / TPT == u ? sc[u] : v;
         mass = __dadd_rn(mass, __shfl_sync(gm, v, r % TPT, TPT));
       }
-      if (q == 0 && !(mass > 1e-12)) atomicMin(&s_err, i);
+      bad = !(mass > 1e-12);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int r = q + TPT * u;
@@ -774,88 +847,125 @@ __global__ void __launch_bounds__(kGroupThreads)
         }
       }
     }
+    return bad;
+  };
+  bool bad = false;
+  if (valid) {
+    bad = emit(0);
+    count(0, 1);
   }
-  // flush this CTA's loads (and, pruned, its union bits)
   stamp(4);
+  // the batch union: poll every CTA's words (thread t: CTAs t, t + blockDim, ..)
+  {
+    uint32_t acc[4] = {0u, 0u, 0u, 0u};
+    for (int c = threadIdx.x; c < static_cast<int>(gridDim.x); c += blockDim.x) {
+      const unsigned long long* wp = &scr->words[c * 4];
+      unsigned long long v[4];
+      for (;;) {
+#pragma unroll
+        for (int w = 0; w < 4; ++w) v[w] = ld_relaxed_u64(wp + w);
+        if ((v[0] >> 32) == tag && (v[1] >> 32) == tag && (v[2] >> 32) == tag && (v[3] >> 32) == tag) break;
+      }
+      if (c == 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");  // (acquire: CTA 0's clears)
+#pragma unroll
+      for (int w = 0; w < 4; ++w) acc[w] |= static_cast<uint32_t>(v[w]);
+    }
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const uint32_t o = __reduce_or_sync(0xffffffffu, acc[w]);
+      if ((threadIdx.x & 31) == 0 && o) atomicOr(&s_batch[w], o);
+    }
+  }
   __syncthreads();
-  for (int e = threadIdx.x; e < N; e += blockDim.x)
-    if (s_loads[e]) atomicAdd(&scr->loads[blockIdx.x % kLoadCopies][e], s_loads[e]);
-  if (set_mode == 1 && threadIdx.x < 4 && s_union[threadIdx.x])
-    atomicOr(&scr->uni[threadIdx.x], s_union[threadIdx.x]);
-  if (threadIdx.x == 0 && s_err != INT_MAX) atomicMax(&scr->err, INT_MAX - s_err);
+  stamp(3);
+  uint32_t uw[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) uw[w] = s_batch[w];
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    // the union exports (fill_aggregates): active experts = the union of
+    // the picks; the base union (pruned / piggyback modes) is the same set
+    const int lane = threadIdx.x;
+    const unsigned below = lanemask_lt();
+    const bool base = set_mode != 0;
+    if (lane < 4 && union_out) union_out[lane] = base ? uw[lane] : 0u;
+    int na = 0;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const int e = 32 * w + lane;
+      const bool f = e < N && ((uw[w] >> lane) & 1u);
+      const unsigned mb = __ballot_sync(0xffffffffu, f);
+      if (f && active_union) active_union[na + __popc(mb & below)] = e;
+      if (f && base && base_union) base_union[na + __popc(mb & below)] = e;
+      na += __popc(mb);
+    }
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const int e = 32 * w + lane;
+      if (e >= na && e < N && active_union) active_union[e] = -1;
+      if ((e >= na || !base) && e < N && base_union) base_union[e] = -1;
+    }
+    if (lane == 0) {
+      if (active_count) *active_count = na;
+      if (base_count) *base_count = base ? na : 0;
+      scr->epoch = epoch + 1;  // (every CTA has read it: its words are in)
+    }
+  }
+  auto member = [&](int e) -> bool {
+    const uint32_t word = e < 32 ? uw[0] : e < 64 ? uw[1] : e < 96 ? uw[2] : uw[3];
+    return (word >> (e & 31)) & 1u;
+  };
+  bool miss = false;
+  if (set_mode == 2) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int r = q + TPT * u;
+      if (r >= n && r < len && !member(ex[u])) miss = true;
+    }
+  }
+  if (__syncthreads_or(miss)) {
+    // (taken by whole warps: the picks' full-warp shuffles; a group whose
+    // picks were all members gets the same picks again)
+    if (__any_sync(0xffffffffu, miss)) {
+      if (valid) count(n, -1);
+      // the union members ranked after the base set, from the raw scores
+      uint32_t elig = 0u;
+      uint64_t kk[EPT];
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) {
+        const int e = TPT * j + q;
+        kk[j] = real && e < N ? order_key_f64(raw[j]) : 0ull;
+        if (e < N && member(e)) elig |= 1u << j;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (q + TPT * u >= n) {
+          ex[u] = -1;
+          sk[u] = 0ull;
+        }
+      uint64_t ak = pk;
+      int ae = pe;
+      const int got = group_pick_regs<TPT, EPT, U>(kk, elig, q, m, n, ex, sk, ak, ae);
+      len = real ? n + min(got, max(0, cfg.limit - n)) : 0;
+      if (valid) {
+        bad = emit(n);
+        count(n, 1);
+      }
+    }
+    __syncthreads();
+  }
+  if (valid && q == 0 && bad) atomicMin(&s_err, i);
+  // this CTA's loads, total load and first degenerate token into the outputs
+  // (cleared by CTA 0 before it published its words)
   __syncthreads();
+  if (loads_out)
+    for (int e = threadIdx.x; e < N; e += blockDim.x)
+      if (s_loads[e]) atomicAdd(&loads_out[e], s_loads[e]);
   if (threadIdx.x == 0) {
-    __threadfence();
-    s_last = atomicAdd(&scr->done, 1) == static_cast<int>(gridDim.x) - 1;
+    if (total_load && s_total)
+      atomicAdd(reinterpret_cast<unsigned long long*>(total_load), static_cast<unsigned long long>(s_total));
+    if (s_err != INT_MAX) atomicMin(err_token, s_err);
   }
-  __syncthreads();
   stamp(5);
-  if (!s_last) return;
-  // the last CTA (one warp: N <= 128): aggregates, exports, and the scratch
-  // reset for the next launch
-  __threadfence();
-  if (threadIdx.x >= 32) return;
-  const int lane = threadIdx.x;
-  const unsigned below = lanemask_lt();
-  int32_t l[4];
-  uint32_t uw = 0u;
-  long long part = 0;
-  // (every global read of the aggregate issued at once: one round trip)
-  if (lane < 4) uw = __ldcg(&scr->uni[lane]);
-  const int ev = __ldcg(&scr->err);
-#pragma unroll
-  for (int w = 0; w < 4; ++w) {
-    const int e = 32 * w + lane;
-    l[w] = 0;
-#pragma unroll
-    for (int c = 0; c < kLoadCopies; ++c) l[w] += e < N ? __ldcg(&scr->loads[c][e]) : 0;
-  }
-#pragma unroll
-  for (int w = 0; w < 4; ++w) {
-    const int e = 32 * w + lane;
-    part += l[w];
-    if (e < N && loads_out) loads_out[e] = l[w];
-#pragma unroll
-    for (int c = 0; c < kLoadCopies; ++c) scr->loads[c][e] = 0;
-  }
-  stamp(7);
-  if (lane < 4) {
-    if (union_out) union_out[lane] = uw;
-    scr->uni[lane] = 0u;
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
-  if (lane == 0) {
-    if (total_load) *total_load = part;
-    *err_token = ev ? INT_MAX - ev : INT_MAX;
-    scr->err = 0;
-    scr->bar = 0;
-    scr->done = 0;
-  }
-  // active_union (load > 0) and the base union, ascending, by ballots
-  int na = 0, nb = 0;
-#pragma unroll
-  for (int w = 0; w < 4; ++w) {
-    const int e = 32 * w + lane;
-    const uint32_t uword = __shfl_sync(0xffffffffu, uw, w);
-    const bool fa = e < N && l[w] > 0, fb = e < N && ((uword >> lane) & 1u);
-    const unsigned ma = __ballot_sync(0xffffffffu, fa), mb = __ballot_sync(0xffffffffu, fb);
-    if (fa && active_union) active_union[na + __popc(ma & below)] = e;
-    if (fb && base_union) base_union[nb + __popc(mb & below)] = e;
-    na += __popc(ma);
-    nb += __popc(mb);
-  }
-#pragma unroll
-  for (int w = 0; w < 4; ++w) {
-    const int e = 32 * w + lane;
-    if (e >= na && e < N && active_union) active_union[e] = -1;
-    if (e >= nb && e < N && base_union) base_union[e] = -1;
-  }
-  if (lane == 0) {
-    if (active_count) *active_count = na;
-    if (base_count) *base_count = nb;
-  }
-  stamp(6);
 }
 
 }  // namespace oea_dev
@@ -955,6 +1065,45 @@ bool route_fast_ok(const Cfg& cfg, int N, bool need_order) {
          cfg.limit <= 32;
 }
 
+// The single-launch route if its grid fits co-resident (cooperative launch):
+// OEA_OK / an error, or -1 when it does not fit (the caller falls back).
+template <int TPT, int BT, bool KEYPICK = false>
+static int launch_group_route(oea_ctx* ctx, const Cfg& cfg, int B, int N, const RouteBuffers& rb,
+                              int set_mode, cudaStream_t s) {
+  const int grid = (B + BT / TPT - 1) / (BT / TPT);
+  static int max_blocks = -1;
+  if (max_blocks < 0) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_group_route<TPT, BT, KEYPICK>, BT, 0);
+    max_blocks = per_sm * ctx->num_sms;
+  }
+  if (grid > max_blocks || grid > kRouteMaxCtas) return -1;
+  // (OEA_ROUTE_PDL=1: launched as a programmatic dependent; measured slower
+  // back to back, 15.8 -> 21.2 us: the next grid's CTAs sit on the SMs)
+  static const bool route_pdl = getenv("OEA_ROUTE_PDL") != nullptr && atoi(getenv("OEA_ROUTE_PDL")) != 0;
+  const int do_weights = (rb.weights != nullptr || rb.weights_f32 != nullptr) ? 1 : 0;
+  cudaLaunchConfig_t c = {};
+  c.gridDim = dim3(grid);
+  c.blockDim = dim3(BT);
+  c.stream = s;
+  cudaLaunchAttribute a[2];
+  a[0].id = cudaLaunchAttributeCooperative;
+  a[0].val.cooperative = 1;
+  a[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a[1].val.programmaticStreamSerializationAllowed = 1;
+  c.attrs = a;
+  c.numAttrs = route_pdl ? 2 : 1;
+  OEA_CUDA_TRY(ctx, cudaLaunchKernelEx(&c, k_group_route<TPT, BT, KEYPICK>, cfg, B, N, set_mode, do_weights,
+                                       rb.scores, rb.mask, rb.sets, rb.set_len, rb.t, rb.n,
+                                       rb.weights, rb.weights_f32,
+                                       static_cast<RouteScratch*>(ctx->route_scratch), rb.loads,
+                                       rb.active_union, rb.active_count, rb.total_load,
+                                       rb.base_union, rb.base_union_count, rb.union_bits,
+                                       rb.err_token, ctx->ffn_trace));
+  OEA_LAUNCHED(ctx);
+  return OEA_OK;
+}
+
 // R > 1: batched independent records (route_f64_batched); seg[i] = record of
 // row i, and union_bits / loads / active_union / active_count / total_load /
 // base_union / base_union_count are per record ([R][4] words, [R][N], [R]).
@@ -965,41 +1114,12 @@ int route_f64_fast_launch(oea_ctx* ctx, const Cfg& cfg, int B, int N, const Rout
   cudaError_t e;
   static const int fused = getenv("OEA_ROUTE_FUSED") ? atoi(getenv("OEA_ROUTE_FUSED")) : 1;
   if (fused && R == 1 && N <= 128 && ctx->route_scratch != nullptr) {
-    // one cooperative launch (phase 1, grid barrier, phase 2, aggregates)
-    constexpr int TPT = OEA_ROUTE_TPT, BT = 256;
-    const int grid = (B + BT / TPT - 1) / (BT / TPT);
-    static int max_blocks = -1;
-    if (max_blocks < 0) {
-      int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_group_route<TPT, BT>, BT, 0);
-      max_blocks = per_sm * ctx->num_sms;
-    }
-    // (OEA_ROUTE_PDL=1: launched as a programmatic dependent; measured slower
-    // back to back, 15.8 -> 21.2 us: the next grid's CTAs sit on the SMs)
-    static const bool route_pdl = getenv("OEA_ROUTE_PDL") != nullptr && atoi(getenv("OEA_ROUTE_PDL")) != 0;
-    if (grid <= max_blocks) {
-      const int do_weights = (rb.weights != nullptr || rb.weights_f32 != nullptr) ? 1 : 0;
-      cudaLaunchConfig_t c = {};
-      c.gridDim = dim3(grid);
-      c.blockDim = dim3(BT);
-      c.stream = s;
-      cudaLaunchAttribute a[2];
-      a[0].id = cudaLaunchAttributeCooperative;
-      a[0].val.cooperative = 1;
-      a[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      a[1].val.programmaticStreamSerializationAllowed = 1;
-      c.attrs = a;
-      c.numAttrs = route_pdl ? 2 : 1;
-      OEA_CUDA_TRY(ctx, cudaLaunchKernelEx(&c, k_group_route<TPT, BT>, cfg, B, N, set_mode, do_weights,
-                                           rb.scores, rb.mask, rb.sets, rb.set_len, rb.t, rb.n,
-                                           rb.weights, rb.weights_f32,
-                                           static_cast<RouteScratch*>(ctx->route_scratch), rb.loads,
-                                           rb.active_union, rb.active_count, rb.total_load,
-                                           rb.base_union, rb.base_union_count, rb.union_bits,
-                                           rb.err_token, ctx->ffn_trace));
-      OEA_LAUNCHED(ctx);
-      return OEA_OK;
-    }
+    // one cooperative launch (phase 1, union exchange, phase 2, exports):
+    // 16 threads per token, 28 tokens per CTA (B = 4096: 147 CTAs, one per
+    // SM; 16 per CTA put 2 CTAs on most SMs and 3 on some: stragglers),
+    // key-only pick reductions (C5 10.0 us vs 10.3 us with (key, index))
+    const int rc = launch_group_route<16, 448, true>(ctx, cfg, B, N, rb, set_mode, s);
+    if (rc >= 0) return rc;
   }
   OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.union_bits, 0, words * 4, s));
   OEA_CUDA_TRY(ctx, cudaMemsetAsync(rb.loads, 0, sizeof(int32_t) * N * R, s));

@@ -13,7 +13,7 @@ ctx.check(_lib().oea_debug_ffn_trace(ctx.h, buf.ctypes.data_as(C.c_void_p), buf.
 t = buf[:256 * 8].reshape(256, 8).astype(np.int64)
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
-names = ["start", "phase1 picks", "union flushed", "barrier passed", "phase2+finish", "done counted", "last CTA aggregate", "last CTA loads read"]
+names = ["start", "phase1 picks", "arrived", "barrier passed", "spec picks+sets", "loads flushed", "keys loaded", "sorted"]
 for sl, nm in enumerate(names):
     a = t[:, sl]
     a = a[a > 0]
