@@ -177,6 +177,26 @@ int ensure(oea_ctx* ctx, Workspace& w, Need nd) {
   return OEA_OK;
 }
 
+// OEA_HOST_PROFILE=1: per-phase host times of oea_moe_decode_host's zero-copy
+// path (mean us, printed at exit): checks, pointer lookups, node patch,
+// graph launch, the spin until the completion flag.
+struct HostProfile {
+  bool on = getenv("OEA_HOST_PROFILE") != nullptr;
+  double sum[5] = {0, 0, 0, 0, 0};
+  long n = 0, calls = 0;
+  static double now() {
+    timespec t;
+    clock_gettime(CLOCK_MONOTONIC, &t);
+    return t.tv_sec * 1e6 + t.tv_nsec * 1e-3;
+  }
+  ~HostProfile() {
+    if (on && n)
+      fprintf(stderr, "host profile (%ld calls, mean us): checks %.2f lookups %.2f patch %.2f launch %.2f spin %.2f\n",
+              n, sum[0] / n, sum[1] / n, sum[2] / n, sum[3] / n, sum[4] / n);
+  }
+};
+HostProfile g_hprof;
+
 // oea_moe_decode_host's zero-copy launches, captured once per (layer, B,
 // config, workspace) as a one-kernel graph; each call patches the kernel
 // node's x / out pointers and replays it (a graph launch costs ~2 us of host
@@ -1543,6 +1563,7 @@ int decode_host_graph(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* xd, 
     h = &ex->host_graphs.back();
   }
   h->used = ++ex->host_graph_clock;
+  const double tp0 = g_hprof.on ? HostProfile::now() : 0.0;
   if (xd != h->x_set || od != h->out_set) {  // serving loops reuse their pinned buffers
     oea_host::ffn_params_set_io(h->params.data(), xd, od);
     h->args[0] = h->params.data();
@@ -1552,8 +1573,13 @@ int decode_host_graph(oea_ctx* ctx, Workspace& w, oea_layer* L, const void* xd, 
     h->x_set = xd;
     h->out_set = od;
   }
+  const double tp1 = g_hprof.on ? HostProfile::now() : 0.0;
   OEA_CUDA_TRY(ctx, cudaGraphLaunch(h->exec, s));
   OEA_LAUNCHED(ctx);
+  if (g_hprof.on) {
+    g_hprof.sum[2] += tp1 - tp0;
+    g_hprof.sum[3] += HostProfile::now() - tp1;
+  }
   return OEA_OK;
 }
 
@@ -1581,6 +1607,7 @@ int oea_moe_decode_host(oea_ctx_t ctx, oea_layer_t L, const void* x_host,
                         const uint8_t* mask_host, int32_t B, const oea_routing_cfg* cfg,
                         void* out_host) {
   CHECK_CTX(ctx);
+  const double th0 = g_hprof.on ? HostProfile::now() : 0.0;
   oea_routing_cfg rc;
   int r = validate_decode(ctx, L, B, cfg, &rc);
   if (r) return r;
@@ -1600,8 +1627,10 @@ int oea_moe_decode_host(oea_ctx_t ctx, oea_layer_t L, const void* x_host,
     // Zero copy: x and out in pinned (mapped) host memory go straight to the
     // fused kernel, which stages x into HBM itself and writes out over the
     // host link; no DMA copies, one launch. Other buffers take the copies.
+    const double th1 = g_hprof.on ? HostProfile::now() : 0.0;
     const void* xd = mapped_view(x_host, xbytes);
     void* od = const_cast<void*>(mapped_view(out_host, obytes));
+    const double th2 = g_hprof.on ? HostProfile::now() : 0.0;
     CtxExtra* ex = extra(ctx);
     if (ex->done_flag == nullptr) {
       void* f = nullptr;
@@ -1614,6 +1643,15 @@ int oea_moe_decode_host(oea_ctx_t ctx, oea_layer_t L, const void* x_host,
       volatile int* flag = ex->done_flag;
       *flag = 0;
       r = decode_host_graph(ctx, w, L, xd, B, rc, od);
+      const double th3 = g_hprof.on ? HostProfile::now() : 0.0;
+      if (r == OEA_OK && g_hprof.on && ++g_hprof.calls > 8) {  // (steady state: past the captures)
+        while (*flag == 0) {
+        }
+        g_hprof.sum[0] += th1 - th0;
+        g_hprof.sum[1] += th2 - th1;
+        g_hprof.sum[4] += HostProfile::now() - th3;
+        ++g_hprof.n;
+      }
       if (r == OEA_OK) {
         // out is on the host once the kernel raises the flag: spin on it
         // (cheaper than a stream synchronisation's wake-up); a fault ends
