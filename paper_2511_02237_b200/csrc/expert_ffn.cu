@@ -993,14 +993,24 @@ __device__ __forceinline__ void rank_phase2(const FfnParams& P, int t, uint8_t* 
     if (gt == 0 && lim) *placed = 0;
     if (gt < 32) {
       const uint32_t below = lanemask_lt();
+      // (published by the GEMV; keys[] is per CTA, not per token): the lane's
+      // four words are loaded before any is used, one round trip instead of
+      // four (the relaxed loads are ordered asm: a use between them, a shared
+      // store, would serialise them)
+      unsigned long long v[4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const int e = 32 * w + gt;
+        v[w] = e < N && ((uni[w] >> gt) & 1u) ? ld_relaxed_u64(P.xlog + static_cast<size_t>(t) * P.Np + e)
+                                               : 0ull;
+      }
       int ub = 0;
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
         const uint32_t uw = uni[w];
         const int e = 32 * w + gt;
-        if (e < N && ((uw >> gt) & 1u))  // (published by the GEMV; keys[] is per CTA, not per token)
-          ukeys[ub + __popc(uw & below)] = order_key32(__uint_as_float(static_cast<uint32_t>(
-              ld_relaxed_u64(P.xlog + static_cast<size_t>(t) * P.Np + e))));
+        if (e < N && ((uw >> gt) & 1u))
+          ukeys[ub + __popc(uw & below)] = order_key32(__uint_as_float(static_cast<uint32_t>(v[w])));
         ub += __popc(uw);
       }
     }
