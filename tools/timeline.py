@@ -78,6 +78,14 @@ for name, cfg in (("oea", oea.RoutingConfig.simplified(K0, 8)), ("vanilla", oea.
     launches.sort(key=lambda v: v[0])
     print(f"== {name} B={B} D={D} H={H} N={N}: {per_call:.2f} us per call (events), "
           f"{len(launches)} launches traced")
+    if os.environ.get("PERCTA"):  # per-CTA medians over the launches of a few prologue slots
+        sl = [0, 8, 5, 11, 12, 6]
+        per = np.median(np.stack([np.stack([(t[:, s] - t0) / 1000.0 for s in sl], 1)
+                                  for t0, t, _ in launches]), 0)
+        print("    per CTA (median us):", " ".join(f"s{s}" for s in sl))
+        worst = np.argsort(-per[:, 3])[:6]
+        for c in list(range(0, 20)) + [int(w) for w in worst]:
+            print(f"    CTA {c:3d}: " + " ".join(f"{v:6.2f}" for v in per[c]))
     # median over the traced launches of each slot's (min, med, max) over CTAs
     rows = {s: [] for s, _ in SLOTS}
     spans, gaps, Ts = [], [], []
