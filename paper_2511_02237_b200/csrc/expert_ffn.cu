@@ -911,13 +911,24 @@ __device__ __forceinline__ void rank_phase1(const FfnParams& P, int t, uint8_t* 
   }
   const uint32_t key = e < N && !masked ? order_key32(l) : 0u;
   if (e < P.Np) keys[e] = key;  // (keys[] holds Np entries)
+  if (s_trace && e == 0 && t < 16) s_trace[2368 + 2 * t] = gtimer();  // (debug: own word polled)
   asm volatile("bar.sync 3, 128;" ::: "memory");
-  int rank = 0;
-#pragma unroll 8
-  for (int f = 0; f < N; ++f) {
-    const uint32_t kf = keys[f];
-    rank += (kf > key) | ((kf == key) & (f < e));
+  if (s_trace && e == 0 && t < 16) s_trace[2368 + 2 * t + 1] = gtimer();  // (debug: all polled)
+  // experts ranked before e: four keys per 16-byte shared load, two
+  // accumulators (the padding keys past N are 0 and never count for a real
+  // key; a zero key's rank is not used)
+  int r0 = 0, r1 = 0;
+  const uint4* k4 = reinterpret_cast<const uint4*>(keys);
+#pragma unroll 4
+  for (int f4 = 0; f4 < (P.Np >> 2); ++f4) {
+    const uint4 kv = k4[f4];
+    const int f = 4 * f4;
+    r0 += (kv.x > key) | ((kv.x == key) & (f < e));
+    r1 += (kv.y > key) | ((kv.y == key) & (f + 1 < e));
+    r0 += (kv.z > key) | ((kv.z == key) & (f + 2 < e));
+    r1 += (kv.w > key) | ((kv.w == key) & (f + 3 < e));
   }
+  const int rank = r0 + r1;
   int n = masked ? 0 : min(P.cfg.mode == OEA_MODE_VANILLA ? P.cfg.k : P.cfg.k0, N);
   if (P.cfg.mode != OEA_MODE_VANILLA && P.cfg.max_p < N && key != 0u && rank == P.cfg.max_p - 1) {
     uint32_t* thr = reinterpret_cast<uint32_t*>(rs + L.thr) + 2 * t;

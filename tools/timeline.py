@@ -71,7 +71,7 @@ for name, cfg in (("oea", oea.RoutingConfig.simplified(K0, 8)), ("vanilla", oea.
         t = r[:148 * 16].reshape(148, 16)
         if t[:, 0].min() <= 0 or t[:, 15].max() <= 0:
             continue
-        launches.append((t[:, 0].min(), t, int(r[INFO])))
+        launches.append((t[:, 0].min(), t, int(r[INFO]), r))
         if r[INFO + 1]:
             print(f"    CTA0: poll {int(r[INFO + 1])} cyc in {int(r[INFO + 2])} passes, "
                   f"select {int(r[INFO + 3])} cyc (load+sort {int(r[INFO + 4])}, merge {int(r[INFO + 5])})")
@@ -81,15 +81,19 @@ for name, cfg in (("oea", oea.RoutingConfig.simplified(K0, 8)), ("vanilla", oea.
     if os.environ.get("PERCTA"):  # per-CTA medians over the launches of a few prologue slots
         sl = [0, 8, 5, 11, 12, 6]
         per = np.median(np.stack([np.stack([(t[:, s] - t0) / 1000.0 for s in sl], 1)
-                                  for t0, t, _ in launches]), 0)
+                                  for t0, t, _, _ in launches]), 0)
         print("    per CTA (median us):", " ".join(f"s{s}" for s in sl))
+        r1 = np.median(np.stack([(r[2368:2400].reshape(16, 2) - t0) / 1000.0
+                                 for t0, _, _, r in launches]), 0)
+        print("    R1 CTAs 0..15: own logit word polled / all polled (median us):",
+              " ".join(f"{a:.2f}/{b:.2f}" for a, b in r1))
         worst = np.argsort(-per[:, 3])[:6]
         for c in list(range(0, 20)) + [int(w) for w in worst]:
             print(f"    CTA {c:3d}: " + " ".join(f"{v:6.2f}" for v in per[c]))
     # median over the traced launches of each slot's (min, med, max) over CTAs
     rows = {s: [] for s, _ in SLOTS}
     spans, gaps, Ts = [], [], []
-    for i, (t0, t, T) in enumerate(launches):
+    for i, (t0, t, T, _) in enumerate(launches):
         for s, _ in SLOTS:
             a = t[:, s]
             a = a[a > 0]
