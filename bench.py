@@ -636,7 +636,10 @@ def bench_c1(args, env):
             ev[i][2].record(stream)
     torch.cuda.synchronize()
     two_kernel = {"router_us": statistics.mean(ev[i][0].elapsed_time(ev[i][1]) * 1000 for i in range(K)),
-                  "ffn_us": statistics.mean(ev[i][1].elapsed_time(ev[i][2]) * 1000 for i in range(K))}
+                  "ffn_us": statistics.mean(ev[i][1].elapsed_time(ev[i][2]) * 1000 for i in range(K)),
+                  "used_for": "fallback only: layers with N > 128 and expert-parallel shards whose fused "
+                              "prologue does not fit in shared memory (every N <= 128 config, p < 1 and "
+                              "max_p < N included, takes the fused single launch); timed here for reference"}
     for gr, gf in stage:
         gr.close()
         gf.close()
