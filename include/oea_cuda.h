@@ -134,6 +134,10 @@ int32_t oea_plan_set_stride(const oea_routing_cfg* resolved);
 int oea_route_f64_host(oea_ctx_t ctx, const double* scores, const uint8_t* mask,
                        int32_t B, int32_t N, const oea_routing_cfg* cfg,
                        const oea_plan_view* plan);
+/* Device-buffer route() on `stream` (asynchronous). The single-launch path
+ * (p == 1, max_p >= N, N <= 128) exchanges the batch union through the
+ * context's epoch-tagged scratch: like decodes, routes of one context must
+ * not run concurrently on different streams. */
 int oea_route_f64(oea_ctx_t ctx, const double* scores_dev, const uint8_t* mask_dev,
                   int32_t B, int32_t N, const oea_routing_cfg* cfg,
                   const oea_plan_view* plan_dev, void* stream);
