@@ -688,8 +688,8 @@ __global__ void __launch_bounds__(kGroupThreads)
     }
   };
   // programmatic dependent: the next launch in the stream may get resident
-  // now; this grid's global reads (scores, the scratch the previous route
-  // reset) wait for its predecessor
+  // now; this grid's global reads (scores, the scratch epoch the previous
+  // route advanced) wait for its predecessor
   pdl_launch_dependents();
   __shared__ int s_loads[128];
   __shared__ uint32_t s_union[4];
