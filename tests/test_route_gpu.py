@@ -224,3 +224,29 @@ def test_fast_path_equals_sort_path(oea, N, B, monkeypatch):
         assert fast.sets == slow.sets and fast.weights == slow.weights, cfg
         assert fast.active_union == slow.active_union and fast.total_load == slow.total_load
         assert np.array_equal(fast.loads, slow.loads)
+
+
+def test_single_launch_speculative_phase2_fallback(oea):
+    """The single-launch route picks phase 2 speculatively (the next experts of
+    the whole list) before the batch union is known and re-picks among the
+    union members when a speculative pick is not one. Token 0 prefers experts
+    0, 1, 2, 3 and token 1 prefers 7, 6, 5, 4: with k0 = 1 the union is {0, 7},
+    so both tokens' speculative picks (1, 2 / 6, 5) miss and the sets must be
+    the reference's {0, 7} / {7, 0} (phase2_piggyback, routing.cpp:270-303).
+    Also a batch with a full union (speculation kept) and a masked row."""
+    s = np.array([[0.30, 0.20, 0.15, 0.10, 0.09, 0.07, 0.05, 0.04],
+                  [0.04, 0.05, 0.07, 0.09, 0.10, 0.15, 0.20, 0.30]])
+    cfg = oea.RoutingConfig.simplified(1, 3)
+    got = oea.route(s, cfg)
+    assert got.sets[0] == [0, 7] and got.sets[1] == [7, 0]
+    assert plan_matches(got, oracle.route(s, cfg), 2) == ""
+    rng = np.random.default_rng(11)
+    for B, k0, k in ((300, 2, 6), (64, 4, 8), (7, 1, 8)):
+        x = rng.random((B, 128)) ** 4
+        x /= x.sum(axis=1, keepdims=True)
+        mask = np.ones(B, bool)
+        mask[B // 2] = False
+        cfg = oea.RoutingConfig.simplified(k0, k)
+        want = oracle.route(x, cfg, mask.astype(np.uint8))
+        got = oea.route(oea.ScoreMatrix(x, mask), cfg)
+        assert plan_matches(got, want, B) == "", (B, k0, k)
